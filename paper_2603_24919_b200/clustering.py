@@ -1,0 +1,106 @@
+"""k-means (reference clustering.py) with the arithmetic on the GPU.
+
+The host keeps only the random stream: ``default_rng(seed)`` draws the
+first centroid with ``integers(n)`` and one ``random()`` per k-means++
+draw, exactly the calls ``Generator.choice(n, p=...)`` makes in the
+reference (clustering.py:44-51).  The device does the D^2 updates, the
+certified CDF search (k_pp_search), the Lloyd assignments and the
+sequential per-cluster sums (build.cu).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DimensionMismatchError, InsufficientDataError, ParameterError
+
+MAX_HALF_DIM = 32
+MAX_CLUSTERS = 256
+
+
+@dataclass(frozen=True)
+class KMeansModel:
+    centroids: np.ndarray             # (k, m) float32
+    assignments: np.ndarray | None    # (n,) int32; None for models loaded from disk
+    inertia: float
+    inertia_history: tuple = ()
+    n_iter: int = 0
+
+    @property
+    def n_clusters(self) -> int:
+        return self.centroids.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.centroids.shape[1]
+
+
+def draw_plan(n: int, k: int, seed: int):
+    """(first, uniforms[k-1]) of the reference's k-means++ stream."""
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(n))
+    uni = np.array([rng.random() for _ in range(k - 1)], dtype=np.float64)
+    return first, uni
+
+
+def forced_plan(n: int, k: int, seed: int, degenerate_at: int):
+    """Replay when the D^2 total hit 0 at draw ``degenerate_at``: from there on
+    every draw is ``rng.integers(n)`` (clustering.py:50-51)."""
+    rng = np.random.default_rng(seed)
+    rng.integers(n)
+    forced = np.full(max(k - 1, 0), -1, np.int64)
+    for i in range(1, k):
+        if i < degenerate_at:
+            rng.random()
+        else:
+            forced[i - 1] = int(rng.integers(n))
+    return forced
+
+
+def check_kmeans_args(X, n_clusters, max_iter):
+    if X.ndim != 2:
+        raise ParameterError(f"k-means expects a 2-D matrix, got shape {X.shape}")
+    n, m = X.shape
+    if n_clusters < 1:
+        raise ParameterError(f"cluster count must be positive, got {n_clusters}")
+    if m < 1:
+        raise ParameterError("points need at least one dimension")
+    if max_iter < 1:
+        raise ParameterError(f"iteration cap must be positive, got {max_iter}")
+    if n < n_clusters:
+        raise InsufficientDataError(f"{n} points cannot fill {n_clusters} clusters")
+    if m > MAX_HALF_DIM or n_clusters > MAX_CLUSTERS:
+        raise ParameterError(f"B200 k-means supports m <= {MAX_HALF_DIM} and k <= {MAX_CLUSTERS} "
+                             f"(got m={m}, k={n_clusters})")
+
+
+def kmeans(data, n_clusters: int, max_iter: int = 20, seed: int = 0) -> KMeansModel:
+    """Seeded k-means++ then at most max_iter Lloyd iterations (GPU)."""
+    X = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+    check_kmeans_args(X, n_clusters, max_iter)
+    n, m = X.shape
+    k = int(n_clusters)
+    first, uni = draw_plan(n, k, seed)
+    cent = np.empty((k, m), np.float32)
+    lab = np.empty(n, np.int32)
+    hist = np.zeros(max_iter)
+    nit = np.zeros(1, np.int32)
+    deg = np.zeros(1, np.int32)
+
+    def run(forced):
+        nat.call("taco_kmeans", nat.device_id(), nat.ptr(X), n, m, k, int(max_iter), first,
+                 nat.ptr(uni), nat.ptr(forced), nat.ptr(cent), nat.ptr(lab), nat.ptr(hist),
+                 nat.ptr(nit), nat.ptr(deg))
+
+    run(None)
+    if deg[0] < k:
+        run(forced_plan(n, k, seed, int(deg[0])))
+    history = tuple(float(v) for v in hist[: int(nit[0])])
+    return KMeansModel(centroids=cent, assignments=lab, inertia=history[-1],
+                       inertia_history=history, n_iter=len(history))
+
+
+__all__ = ["KMeansModel", "kmeans", "draw_plan", "forced_plan", "DimensionMismatchError"]

@@ -1,0 +1,995 @@
+// TaCo index build on sm_100a.
+//
+//  covariance   k_nonfinite, k_colmean_seq (sequential fp64, bit-exact mean),
+//               k_gram (split-K fp64 Gram tiles) + k_gram_reduce     spectral.py:94-111
+//  transform    k_transform (index.cu)                                spectral.py:301-316
+//  k-means++    k_xsq, k_pp_update (D^2 min + block sums), k_pp_search
+//               (certified CDF search, exact numpy fallback)          clustering.py:41-54
+//  Lloyd        k_assign (fp64 expansion, dgemm FMA order, first argmin),
+//               k_lloyd_ctl, stable counting sort by label (k_label_*),
+//               k_cluster_sums (sequential per-cluster fp64 sums in index
+//               order == np.add.at), k_reseed                         clustering.py:86-107
+//  cells        k_cell_hist / k_cell_offsets / k_cell_scatter: stable
+//               counting sort by (l1,l2) into the chunk-major CSR     imi.py:70-81
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "index.cuh"
+
+namespace taco {
+
+// ============================================================ covariance
+__global__ void k_nonfinite(const float* __restrict__ X, int64_t total, int d,
+                            unsigned long long* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = i; e < total; e += stride) {
+    if (!isfinite(X[e])) atomicMin(bad, (unsigned long long)(e / d));
+  }
+}
+
+// numpy mean(axis=0) of a C-contiguous matrix: out = X[0]; out += X[r] for
+// r = 1..n-1 (row-sequential), then / n.  One thread per column.
+__global__ void k_colmean_seq(const float* __restrict__ X, int64_t n, int d, double* __restrict__ mean) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  double acc = (double)X[c];
+  int64_t r = 1;
+  for (; r + 8 <= n; r += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (r + u) * d + c);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+  }
+  for (; r < n; ++r) acc = __dadd_rn(acc, (double)X[r * d + c]);
+  mean[c] = __ddiv_rn(acc, (double)n);
+}
+
+constexpr int GT = 64, GK = 16;
+// partial[s] = sum over rows of split s of (x - mu)(x - mu)^T, 64x64 tile.
+__global__ void __launch_bounds__(256) k_gram(const float* __restrict__ X, int64_t n, int d,
+                                              const double* __restrict__ mean, int64_t rows_per,
+                                              double* __restrict__ partial) {
+  __shared__ double A[GK][GT + 1];
+  __shared__ double B[GK][GT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.x * GT, j0 = blockIdx.y * GT;
+  const int64_t r0 = (int64_t)blockIdx.z * rows_per;
+  const int64_t r1 = min(n, r0 + rows_per);
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += GK) {
+    for (int e = threadIdx.x; e < GK * GT; e += 256) {
+      const int kk = e / GT, cc = e % GT;
+      const int64_t r = rb + kk;
+      double va = 0.0, vb = 0.0;
+      if (r < r1) {
+        if (i0 + cc < d) va = __dsub_rn((double)X[r * d + i0 + cc], mean[i0 + cc]);
+        if (j0 + cc < d) vb = __dsub_rn((double)X[r * d + j0 + cc], mean[j0 + cc]);
+      }
+      A[kk][cc] = va;
+      B[kk][cc] = vb;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < GK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = A[kk][ty + 16 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = B[kk][tx + 16 * u];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = __fma_rn(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+  double* P = partial + (size_t)blockIdx.z * d * d;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int i = i0 + ty + 16 * x;
+    if (i >= d) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int j = j0 + tx + 16 * y;
+      if (j < d) P[(size_t)i * d + j] = acc[x][y];
+    }
+  }
+}
+
+__global__ void k_gram_reduce(const double* __restrict__ partial, int splits, int64_t dd,
+                              double* __restrict__ G) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= dd) return;
+  double acc = 0.0;
+  for (int s = 0; s < splits; ++s) acc = __dadd_rn(acc, partial[(size_t)s * dd + e]);
+  G[e] = acc;
+}
+
+// ================================================================ k-means
+constexpr int PP_THREADS = 256;
+constexpr int PP_PPT = 4;                       // points per thread in one block
+constexpr int PP_BLOCK = PP_THREADS * PP_PPT;   // points per block-sum
+constexpr double U0 = 1.1102230246251565e-16;   // 2^-53
+
+struct HalfView {
+  const float* X;   // dimension-major: X[t*n + i]
+  int64_t n;
+  int m;
+  int k;
+};
+
+__global__ void k_xsq(HalfView h, double* __restrict__ xsq, double* __restrict__ xsqmax_blk) {
+  __shared__ double red[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < h.n) {
+    v = einsum_sq([&](int t) { return (double)h.X[(size_t)t * h.n + i]; }, h.m);
+    xsq[i] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double w = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+    if (threadIdx.x == 0) xsqmax_blk[blockIdx.x] = w;
+  }
+}
+
+// status layout (int64): [0] degenerate draw index (k if none), [1] fallbacks,
+// [2] converged flag, [3] n_iter, [4] changed count
+// D^2 update for centroid `ci` (= picks[ci]) and per-block sums of best.
+__global__ void __launch_bounds__(PP_THREADS) k_pp_update(HalfView h, const double* __restrict__ xsq,
+                                                          const int64_t* __restrict__ picks, int ci,
+                                                          double* __restrict__ best,
+                                                          double* __restrict__ C64,
+                                                          double* __restrict__ bsum) {
+  __shared__ double cv[64];
+  __shared__ double red[PP_THREADS / 32];
+  __shared__ double s_csq;
+  const int64_t p = picks[ci];
+  if (threadIdx.x < h.m) cv[threadIdx.x] = (double)h.X[(size_t)threadIdx.x * h.n + p];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_csq = einsum_sq([&](int t) { return cv[t]; }, h.m);
+    if (blockIdx.x == 0)
+      for (int t = 0; t < h.m; ++t) C64[(size_t)ci * h.m + t] = cv[t];
+  }
+  __syncthreads();
+  const double csq = s_csq;
+  const int64_t b0 = (int64_t)blockIdx.x * PP_BLOCK + threadIdx.x;
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < PP_PPT; ++u) {
+    const int64_t i = b0 + (int64_t)u * PP_THREADS;
+    if (i < h.n) {
+      const double dot = dot_fma([&](int t) { return (double)h.X[(size_t)t * h.n + i]; },
+                                 [&](int t) { return cv[t]; }, h.m);
+      const double d2 = sq_dist_expand(xsq[i], dot, csq);
+      double b = d2;
+      if (ci > 0) {
+        const double old = best[i];
+        b = d2 < old ? d2 : old;
+      }
+      best[i] = b;
+      s = __dadd_rn(s, b);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) of a
+// contiguous double array, restated for the exact fallback path.
+__device__ double np_pairwise(const double* a, int64_t n) {
+  // explicit stack of (ptr offset, len, state)
+  struct Fr { int64_t off, len; double left; int state; };
+  Fr st[64];
+  int sp = 0;
+  st[sp++] = {0, n, 0.0, 0};
+  double ret = 0.0;
+  while (sp > 0) {
+    Fr& f = st[sp - 1];
+    if (f.len < 8) {
+      double r = 0.0;
+      for (int64_t i = 0; i < f.len; ++i) r = __dadd_rn(r, a[f.off + i]);
+      ret = r;
+      --sp;
+    } else if (f.len <= 128) {
+      double r[8];
+      for (int j = 0; j < 8; ++j) r[j] = a[f.off + j];
+      int64_t i = 8;
+      for (; i < f.len - (f.len % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[f.off + i + j]);
+      double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < f.len; ++i) res = __dadd_rn(res, a[f.off + i]);
+      ret = res;
+      --sp;
+    } else {
+      int64_t n2 = f.len / 2;
+      n2 -= n2 % 8;
+      if (f.state == 0) {
+        f.state = 1;
+        st[sp++] = {f.off, n2, 0.0, 0};
+      } else if (f.state == 1) {
+        f.left = ret;
+        f.state = 2;
+        st[sp++] = {f.off + n2, f.len - n2, 0.0, 0};
+      } else {
+        ret = __dadd_rn(f.left, ret);
+        --sp;
+      }
+    }
+  }
+  return ret;
+}
+
+// One CTA: chooses picks[ci+1] from best (after centroids 0..ci) and u.
+// Fast path: fp64 prefix over block sums, locate the crossing, then certify
+// that numpy's sequential cumsum/normalise/searchsorted (the reference's
+// Generator.choice, clustering.py:48) cannot land elsewhere.  Otherwise
+// replay numpy's arithmetic exactly (single thread).
+constexpr int PS_THREADS = 1024;
+__global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const double* __restrict__ best,
+                                                          const double* __restrict__ bsum, int64_t nb,
+                                                          const double* __restrict__ uni,
+                                                          const int64_t* __restrict__ forced,
+                                                          double xsqmax, int ci,
+                                                          int64_t* __restrict__ picks,
+                                                          int64_t* __restrict__ status) {
+  __shared__ double wsum[32];
+  __shared__ double s_total;
+  __shared__ int64_t s_blk;
+  __shared__ double s_before;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int draw = ci + 1;                 // centroid index being chosen
+  if (forced && forced[ci] >= 0) {
+    if (tid == 0) picks[draw] = forced[ci];
+    return;
+  }
+  // per-thread contiguous block-sum ranges, then a block scan (fixed order)
+  const int64_t per = (nb + PS_THREADS - 1) / PS_THREADS;
+  const int64_t a0 = (int64_t)tid * per, a1 = min(nb, a0 + per);
+  double loc = 0.0;
+  for (int64_t b = a0; b < a1; ++b) loc = __dadd_rn(loc, bsum[b]);
+  double v = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    double x = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = __dadd_rn(v, x);
+  }
+  if (lane == 31) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double w = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      double x = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = __dadd_rn(w, x);
+    }
+    wsum[lane] = w;
+    if (lane == 31) s_total = w;
+  }
+  if (tid == 0) s_blk = -1;
+  __syncthreads();
+  const double S = s_total;
+  if (!(S > 0.0)) {
+    // reference: total == 0 -> rng.integers(n); the host replays this draw
+    if (tid == 0) {
+      if (status[0] > draw) status[0] = draw;
+      picks[draw] = 0;
+    }
+    return;
+  }
+  const double u = uni[ci];
+  const double target = u * S;
+  // thread whose range holds the first inclusive prefix > target
+  double run = (wid ? wsum[wid - 1] : 0.0) + (v - loc);   // exclusive prefix (approx order ok: bounded)
+  {
+    double pre = run;
+    for (int64_t b = a0; b < a1; ++b) {
+      const double nx = __dadd_rn(pre, bsum[b]);
+      if (nx > target && pre <= target) {
+        s_blk = b;
+        s_before = pre;
+      }
+      pre = nx;
+    }
+  }
+  __syncthreads();
+  int64_t blk = s_blk;
+  if (tid == 0) {
+    int64_t kstar = -1;
+    double Pk = 0.0, Pkm1 = 0.0;
+    if (blk < 0) {  // rounding put the target at/after the end: take the last positive point
+      blk = nb - 1;
+    }
+    double pre = blk >= 0 && s_blk >= 0 ? s_before : S - bsum[blk];
+    const int64_t i0 = blk * PP_BLOCK, i1 = min(h.n, i0 + PP_BLOCK);
+    for (int64_t i = i0; i < i1; ++i) {
+      const double nx = __dadd_rn(pre, best[i]);
+      if (nx > target) { kstar = i; Pk = nx; Pkm1 = pre; break; }
+      pre = nx;
+    }
+    if (kstar < 0) { kstar = i1 - 1; Pk = pre; Pkm1 = pre - best[kstar]; }
+    // error budget: numpy cumsum (n terms) + normalisation, our tree sums,
+    // and the reference's best[] differing from ours by rounding of the
+    // (dgemv-ordered) dot products: |delta d2| <= 8u0 (|x| + |c|)^2.
+    const double n = (double)h.n;
+    const double rel = (2.0 * n + 4.0 * log2(n + 2.0) + 4.0 * PP_BLOCK + 256.0) * U0;
+    const double absU = 32.0 * U0 * n * xsqmax;
+    const double margin = 3.0 * rel * S + 2.0 * absU;
+    bool ok = (Pk - target > margin) && (target - Pkm1 >= margin);
+    if (ok) {
+      picks[draw] = kstar;
+    } else {
+      // exact replay of Generator.choice(n, p=best/total)
+      const double total = np_pairwise(best, h.n);
+      double cdf = 0.0;
+      // cdf_last first (sequential cumsum of p = best/total)
+      for (int64_t i = 0; i < h.n; ++i) cdf = __dadd_rn(cdf, __ddiv_rn(best[i], total));
+      const double last = cdf;
+      cdf = 0.0;
+      int64_t idx = h.n - 1;
+      for (int64_t i = 0; i < h.n; ++i) {
+        cdf = __dadd_rn(cdf, __ddiv_rn(best[i], total));
+        if (__ddiv_rn(cdf, last) > u) { idx = i; break; }
+      }
+      picks[draw] = idx;
+      status[1] += 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Lloyd
+constexpr int AS_THREADS = 256;
+template <int MM>
+__global__ void __launch_bounds__(AS_THREADS) k_assign(HalfView h, const double* __restrict__ xsq,
+                                                       const double* __restrict__ C64,
+                                                       const int32_t* __restrict__ lab,
+                                                       int32_t* __restrict__ newlab,
+                                                       double* __restrict__ pd, int iter,
+                                                       int64_t* __restrict__ status,
+                                                       double* __restrict__ hsum) {
+  extern __shared__ double ash[];
+  if (status[2]) return;
+  const int m = h.m;
+  double* C = ash;                    // k*m
+  double* csq = ash + (size_t)h.k * m; // k
+  __shared__ double red[AS_THREADS / 32];
+  __shared__ int chg;
+  for (int e = threadIdx.x; e < h.k * m; e += AS_THREADS) C[e] = C64[e];
+  if (threadIdx.x == 0) chg = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < h.k; c += AS_THREADS)
+    csq[c] = einsum_sq([&](int t) { return C[c * m + t]; }, m);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * AS_THREADS + threadIdx.x;
+  double my = 0.0;
+  int changed = 0;
+  if (i < h.n) {
+    double x[MM];
+#pragma unroll
+    for (int t = 0; t < MM; ++t) x[t] = t < m ? (double)h.X[(size_t)t * h.n + i] : 0.0;
+    const double xs = xsq[i];
+    double bd = 0.0;
+    int bl = 0;
+    for (int c = 0; c < h.k; ++c) {
+      const double* cr = C + c * m;
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < MM; ++t)
+        if (t < m) acc = __fma_rn(x[t], cr[t], acc);
+      const double d2 = sq_dist_expand(xs, acc, csq[c]);
+      if (c == 0 || d2 < bd) { bd = d2; bl = c; }
+    }
+    newlab[i] = bl;
+    pd[i] = bd;
+    my = bd;
+    if (iter > 0 && lab[i] != bl) changed = 1;
+  }
+  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) atomicOr(&chg, 1);
+  for (int o = 16; o > 0; o >>= 1) my = __dadd_rn(my, __shfl_xor_sync(0xffffffffu, my, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = my;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < AS_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
+    hsum[blockIdx.x] = t;
+    if (chg) atomicAdd((unsigned long long*)&status[4], 1ull);
+  }
+}
+
+// history, convergence flag (clustering.py:90-93)
+__global__ void k_lloyd_ctl(const double* __restrict__ hsum, int64_t nb, int iter,
+                            int64_t* __restrict__ status, double* __restrict__ history,
+                            int32_t* __restrict__ n_iter) {
+  __shared__ double red[32];
+  if (status[2]) return;
+  double s = 0.0;
+  for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) s = __dadd_rn(s, hsum[b]);
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = __dadd_rn(t, red[w]);
+    history[iter] = t;
+    *n_iter = iter + 1;
+    status[3] = iter + 1;
+    if (iter > 0 && status[4] == 0) status[2] = 1;
+    status[4] = 0;
+  }
+}
+
+constexpr int LT = 4096;  // points per label tile
+__global__ void k_label_hist(int64_t n, int k, const int64_t* __restrict__ status,
+                             const int32_t* __restrict__ newlab, int32_t* __restrict__ lab,
+                             int32_t* __restrict__ lhist) {
+  if (status[2]) return;
+  __shared__ int cnt[256];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * LT;
+  const int64_t i1 = min(n, i0 + LT);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const int32_t l = newlab[i];
+    lab[i] = l;
+    atomicAdd(&cnt[l], 1);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) lhist[(size_t)blockIdx.x * k + c] = cnt[c];
+}
+
+// loff[tile][c] = start of (cluster c, tile) in the label-sorted order; counts[c]
+__global__ void k_label_offsets(int64_t ntiles, int k, const int64_t* __restrict__ status,
+                                const int32_t* __restrict__ lhist, int64_t* __restrict__ loff,
+                                int64_t* __restrict__ counts) {
+  if (status[2]) return;
+  __shared__ int64_t tot[256];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    int64_t s = 0;
+    for (int64_t t = 0; t < ntiles; ++t) s += lhist[(size_t)t * k + c];
+    tot[c] = s;
+    counts[c] = s;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    int64_t base = 0;
+    for (int c2 = 0; c2 < c; ++c2) base += tot[c2];
+    for (int64_t t = 0; t < ntiles; ++t) {
+      loff[(size_t)t * k + c] = base;
+      base += lhist[(size_t)t * k + c];
+    }
+  }
+}
+
+// one warp per tile, rounds of 32 ascending points: stable ranks via match_any
+__global__ void k_label_scatter(int64_t n, int k, const int64_t* __restrict__ status,
+                                const int32_t* __restrict__ lab, const int64_t* __restrict__ loff,
+                                int64_t* __restrict__ perm) {
+  if (status[2]) return;
+  __shared__ int64_t cur[256];
+  for (int c = threadIdx.x; c < k; c += 32) cur[c] = loff[(size_t)blockIdx.x * k + c];
+  __syncwarp();
+  const int lane = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * LT;
+  const int64_t i1 = min(n, i0 + LT);
+  for (int64_t r = i0; r < i1; r += 32) {
+    const int64_t i = r + lane;
+    const bool live = i < i1;
+    const int l = live ? lab[i] : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    const unsigned grp = __match_any_sync(0xffffffffu, l) & act;
+    if (live) {
+      const int rank = __popc(grp & ((1u << lane) - 1u));
+      perm[cur[l] + rank] = i;
+    }
+    __syncwarp();
+    if (live && lane == __ffs(grp) - 1) cur[l] += __popc(grp);
+    __syncwarp();
+  }
+}
+
+// centroid = (sequential fp64 sum over the cluster's points in index order) / count
+__global__ void k_cluster_sums(HalfView h, const int64_t* __restrict__ status,
+                               const int64_t* __restrict__ perm, const int64_t* __restrict__ counts,
+                               double* __restrict__ C64) {
+  if (status[2]) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= h.k * h.m) return;
+  const int c = e / h.m, t = e % h.m;
+  const int64_t cnt = counts[c];
+  if (cnt == 0) return;
+  int64_t start = 0;
+  for (int c2 = 0; c2 < c; ++c2) start += counts[c2];
+  const float* xt = h.X + (size_t)t * h.n;
+  double acc = 0.0;
+  int64_t p = 0;
+  for (; p + 8 <= cnt; p += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(xt + perm[start + p + u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+  }
+  for (; p < cnt; ++p) acc = __dadd_rn(acc, (double)xt[perm[start + p]]);
+  C64[(size_t)c * h.m + t] = __ddiv_rn(acc, (double)cnt);
+}
+
+// empty clusters (ascending): farthest point (first argmax of point_d2 with
+// already-taken points at -1) becomes the centroid and moves its label.
+__global__ void k_reseed(HalfView h, const int64_t* __restrict__ status,
+                         const int64_t* __restrict__ counts, double* __restrict__ far,
+                         int32_t* __restrict__ lab, double* __restrict__ C64) {
+  if (status[2]) return;
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  __shared__ int64_t s_p;
+  for (int c = 0; c < h.k; ++c) {
+    if (counts[c] != 0) continue;
+    double v = -INFINITY;
+    int64_t vi = INT64_MAX;
+    for (int64_t i = threadIdx.x; i < h.n; i += blockDim.x) {
+      const double f = far[i];
+      if (f > v) { v = f; vi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = v; bi[threadIdx.x >> 5] = vi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double w = bv[0];
+      int64_t wi = bi[0];
+      for (int k2 = 1; k2 < (int)(blockDim.x >> 5); ++k2)
+        if (bv[k2] > w || (bv[k2] == w && bi[k2] < wi)) { w = bv[k2]; wi = bi[k2]; }
+      s_p = wi;
+      for (int t = 0; t < h.m; ++t) C64[(size_t)c * h.m + t] = (double)h.X[(size_t)t * h.n + wi];
+      lab[wi] = c;
+      far[wi] = -1.0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_centroids_out(const double* __restrict__ C64, int km, float* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < km) out[e] = __double2float_rn(C64[e]);
+}
+
+__global__ void k_status_init(int64_t* status, int k) {
+  status[0] = k;
+  status[1] = 0;
+  status[2] = 0;
+  status[3] = 0;
+  status[4] = 0;
+}
+
+struct KMeansRun {
+  HalfView h;
+  BuildScratch* s;
+  int32_t* labels;     // n (device, output)
+  double* history;     // iters (device)
+  int32_t* n_iter;     // 1 (device)
+  float* cent_out;     // k*m (device)
+  int iters;
+};
+
+static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h,
+                          const int64_t* forced_h, cudaStream_t st) {
+  BuildScratch& s = *r.s;
+  const HalfView h = r.h;
+  const int64_t n = h.n;
+  const int k = h.k;
+  const int m = h.m;
+  if (m > 32) TACO_FAIL(TACO_ERR_PARAMETER, "half width %d exceeds 32", m);
+  if (k > 256) TACO_FAIL(TACO_ERR_PARAMETER, "codebook size %d exceeds 256", k);
+  const int64_t nbx = ceil_div(n, 256);
+  const int64_t nbp = ceil_div(n, PP_BLOCK);
+  const int64_t nba = ceil_div(n, AS_THREADS);
+  const int64_t ntile = ceil_div(n, LT);
+  TACO_TRY(s.xsq.ensure(8 * n));
+  TACO_TRY(s.best.ensure(8 * n));
+  TACO_TRY(s.bsum.ensure(8 * std::max(nbp, nbx)));
+  TACO_TRY(s.picks.ensure(8 * k));
+  TACO_TRY(s.uni.ensure(8 * std::max(k, 1)));
+  TACO_TRY(s.forced.ensure(8 * std::max(k, 1)));
+  TACO_TRY(s.status.ensure(8 * 8));
+  TACO_TRY(s.C64.ensure(8 * (size_t)k * m));
+  TACO_TRY(s.newlab.ensure(4 * n));
+  TACO_TRY(s.pd.ensure(8 * n));
+  TACO_TRY(s.perm.ensure(8 * n));
+  TACO_TRY(s.lhist.ensure(4 * (size_t)ntile * k));
+  TACO_TRY(s.loff.ensure(8 * (size_t)ntile * k));
+  TACO_TRY(s.ctl.ensure(8 * k));       // counts
+  TACO_TRY(s.hsum.ensure(8 * nba));
+  TACO_TRY(s.draws.ensure(8 * nbx));   // xsq block maxima
+  // xsq + its maximum (bound for the certified draw)
+  k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.draws.as<double>());
+  TACO_LAUNCHED();
+  std::vector<double> bm(nbx);
+  TACO_CHECK_CUDA(cudaMemcpyAsync(bm.data(), s.draws.p, 8 * nbx, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  double xsqmax = 0.0;
+  for (double v : bm) xsqmax = std::max(xsqmax, v);
+  TACO_CHECK_CUDA(cudaMemcpyAsync(s.picks.p, &first, 8, cudaMemcpyHostToDevice, st));
+  if (k > 1) {
+    TACO_CHECK_CUDA(cudaMemcpyAsync(s.uni.p, uni_h, 8 * (k - 1), cudaMemcpyHostToDevice, st));
+    if (forced_h)
+      TACO_CHECK_CUDA(cudaMemcpyAsync(s.forced.p, forced_h, 8 * (k - 1), cudaMemcpyHostToDevice, st));
+  }
+  k_status_init<<<1, 1, 0, st>>>(s.status.as<int64_t>(), k);
+  TACO_LAUNCHED();
+  for (int ci = 0; ci < k; ++ci) {
+    k_pp_update<<<(unsigned)nbp, PP_THREADS, 0, st>>>(h, s.xsq.as<double>(), s.picks.as<int64_t>(), ci,
+                                                      s.best.as<double>(), s.C64.as<double>(),
+                                                      s.bsum.as<double>());
+    TACO_LAUNCHED();
+    if (ci + 1 < k) {
+      k_pp_search<<<1, PS_THREADS, 0, st>>>(h, s.best.as<double>(), s.bsum.as<double>(), nbp,
+                                            s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
+                                            xsqmax, ci, s.picks.as<int64_t>(), s.status.as<int64_t>());
+      TACO_LAUNCHED();
+    }
+  }
+  const size_t ash = sizeof(double) * ((size_t)k * m + k);
+  auto* kas = m <= 8 ? k_assign<8> : m <= 16 ? k_assign<16> : k_assign<32>;
+  if (ash > 48 * 1024)
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
+  for (int it = 0; it < r.iters; ++it) {
+    kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,
+                                                s.newlab.as<int32_t>(), s.pd.as<double>(), it,
+                                                s.status.as<int64_t>(), s.hsum.as<double>());
+    TACO_LAUNCHED();
+    k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nba, it, s.status.as<int64_t>(), r.history,
+                                    r.n_iter);
+    TACO_LAUNCHED();
+    k_label_hist<<<(unsigned)ntile, 256, 0, st>>>(n, k, s.status.as<int64_t>(), s.newlab.as<int32_t>(),
+                                                  r.labels, s.lhist.as<int32_t>());
+    TACO_LAUNCHED();
+    k_label_offsets<<<1, 256, 0, st>>>(ntile, k, s.status.as<int64_t>(), s.lhist.as<int32_t>(),
+                                       s.loff.as<int64_t>(), s.ctl.as<int64_t>());
+    TACO_LAUNCHED();
+    k_label_scatter<<<(unsigned)ntile, 32, 0, st>>>(n, k, s.status.as<int64_t>(), r.labels,
+                                                    s.loff.as<int64_t>(), s.perm.as<int64_t>());
+    TACO_LAUNCHED();
+    k_cluster_sums<<<(unsigned)ceil_div((int64_t)k * m, 128), 128, 0, st>>>(
+        h, s.status.as<int64_t>(), s.perm.as<int64_t>(), s.ctl.as<int64_t>(), s.C64.as<double>());
+    TACO_LAUNCHED();
+    k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), s.ctl.as<int64_t>(), s.pd.as<double>(),
+                                 r.labels, s.C64.as<double>());
+    TACO_LAUNCHED();
+  }
+  k_centroids_out<<<(unsigned)ceil_div((int64_t)k * m, 256), 256, 0, st>>>(s.C64.as<double>(), k * m,
+                                                                            r.cent_out);
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
+// ================================================================== cells
+__global__ void k_cell_hist(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2, int64_t n,
+                            int kp, uint32_t* __restrict__ chist) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int key = l1[i] * kp + l2[i];
+  atomicAdd(&chist[(size_t)(i >> kChunkShift) * kp * kp + key], 1u);
+}
+
+// per chunk: offs[c*K2 + cell] = c*CH + exclusive prefix within the chunk
+__global__ void k_cell_offsets(const uint32_t* __restrict__ chist, int K2, int64_t nchunks, int64_t n,
+                               uint32_t* __restrict__ offs) {
+  __shared__ uint32_t wsum[32];
+  const int64_t c = blockIdx.x;
+  const uint32_t* hc = chist + (size_t)c * K2;
+  const int per = (K2 + blockDim.x - 1) / blockDim.x;
+  const int a0 = threadIdx.x * per, a1 = min(K2, a0 + per);
+  uint32_t loc = 0;
+  for (int e = a0; e < a1; ++e) loc += hc[e];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t v = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t x = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += x;
+  }
+  if (lane == 31) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t x = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += x;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)(c << kChunkShift) + (wid ? wsum[wid - 1] : 0u) + v - loc;
+  for (int e = a0; e < a1; ++e) {
+    offs[(size_t)c * K2 + e] = run;
+    run += hc[e];
+  }
+  if (c == nchunks - 1 && threadIdx.x == 0) offs[(size_t)nchunks * K2] = (uint32_t)n;
+}
+
+__global__ void k_cell_sizes(const uint32_t* __restrict__ chist, int K2, int64_t nchunks,
+                             int64_t* __restrict__ gsize) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K2) return;
+  int64_t s = 0;
+  for (int64_t c = 0; c < nchunks; ++c) s += chist[(size_t)c * K2 + e];
+  gsize[e] = s;
+}
+
+// one warp per chunk: stable scatter of ascending ids into their cells
+__global__ void k_cell_scatter(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2,
+                               int64_t n, int kp, uint32_t* __restrict__ cursor,
+                               uint32_t* __restrict__ ids) {
+  const int lane = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  const int K2 = kp * kp;
+  uint32_t* cur = cursor + (size_t)c * K2;
+  const int64_t i0 = c << kChunkShift;
+  const int64_t i1 = min(n, i0 + kChunk);
+  for (int64_t r = i0; r < i1; r += 32) {
+    const int64_t i = r + lane;
+    const bool live = i < i1;
+    const int key = live ? l1[i] * kp + l2[i] : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    const unsigned grp = __match_any_sync(0xffffffffu, key) & act;
+    uint32_t base = 0;
+    const int leader = live ? __ffs(grp) - 1 : 0;
+    if (live && lane == leader) base = atomicAdd(&cur[key], (uint32_t)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (live) ids[base + __popc(grp & ((1u << lane) - 1u))] = (uint32_t)i;
+  }
+}
+
+}  // namespace taco
+
+using namespace taco;
+
+namespace {
+int ensure_half_streams(taco_index* idx, int want) {
+  while ((int)idx->half_streams.size() < want) {
+    cudaStream_t s;
+    TACO_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    idx->half_streams.push_back(s);
+  }
+  return TACO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, double* mean_h,
+                           double* gram_h, int64_t* bad_row) {
+  DevBuf bad, mean, part, G;
+  int rc = TACO_OK;
+  do {
+    if ((rc = bad.ensure(8)) || (rc = mean.ensure(8 * d)) || (rc = G.ensure(8 * (size_t)d * d))) break;
+    unsigned long long init = ~0ull;
+    cudaMemcpyAsync(bad.p, &init, 8, cudaMemcpyHostToDevice, st);
+    k_nonfinite<<<1184, 256, 0, st>>>(Xd, n * d, d, bad.as<unsigned long long>());
+    count_launch();
+    unsigned long long b = 0;
+    cudaMemcpyAsync(&b, bad.p, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
+    *bad_row = b == ~0ull ? -1 : (int64_t)b;
+    if (b != ~0ull) break;
+    k_colmean_seq<<<(unsigned)ceil_div(d, 32), 32, 0, st>>>(Xd, n, d, mean.as<double>());
+    count_launch();
+    const int tiles = (int)ceil_div(d, GT);
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(592, tiles * tiles), ceil_div(n, 256)));
+    const int64_t rows_per = ceil_div(ceil_div(n, splits), GK) * GK;
+    splits = (int)ceil_div(n, rows_per);
+    if ((rc = part.ensure(8 * (size_t)splits * d * d))) break;
+    k_gram<<<dim3(tiles, tiles, splits), 256, 0, st>>>(Xd, n, d, mean.as<double>(), rows_per,
+                                                      part.as<double>());
+    count_launch();
+    const int64_t dd = (int64_t)d * d;
+    k_gram_reduce<<<(unsigned)ceil_div(dd, 256), 256, 0, st>>>(part.as<double>(), splits, dd, G.as<double>());
+    count_launch();
+    cudaMemcpyAsync(mean_h, mean.p, 8 * d, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(gram_h, G.p, 8 * dd, cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; }
+  } while (0);
+  bad.release(); mean.release(); part.release(); G.release();
+  return rc;
+}
+
+int taco_fit_covariance(taco_index* idx, double* mean_h, double* gram_h, int64_t* bad_row) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "no data uploaded");
+  return covariance_impl(idx->X.as<float>(), idx->n, idx->d, idx->stream, mean_h, gram_h, bad_row);
+}
+
+int taco_covariance(int device, const float* X_h, int64_t n, int32_t d, double* mean_h, double* gram_h,
+                    int64_t* bad_row) {
+  TACO_TRY(with_device(device));
+  DevBuf X;
+  TACO_TRY(X.ensure(4 * (size_t)n * d));
+  cudaError_t e = cudaMemcpy(X.p, X_h, 4 * (size_t)n * d, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { X.release(); TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e)); }
+  int rc = covariance_impl(X.as<float>(), n, d, nullptr, mean_h, gram_h, bad_row);
+  X.release();
+  return rc;
+}
+
+int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* uniforms_h,
+                    const int64_t* forced_h, int32_t* degenerate_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_T) TACO_FAIL(TACO_ERR_STATE, "transformed data not available");
+  const int H = 2 * idx->n_sub;
+  const int kp = idx->kp;
+  const int64_t n = idx->n;
+  if (n < kp) TACO_FAIL(TACO_ERR_INSUFFICIENT, "%lld points cannot fill %d clusters", (long long)n, kp);
+  const int NS = std::min(H, 16);
+  TACO_TRY(ensure_half_streams(idx, NS));
+  if ((int)idx->bs.size() < NS) idx->bs.resize(NS);
+  TACO_TRY(idx->labels.ensure(sizeof(int32_t) * (size_t)n * H));
+  TACO_TRY(idx->hist.ensure(sizeof(double) * (size_t)H * std::max(idx->iters, 1)));
+  TACO_TRY(idx->niter.ensure(sizeof(int32_t) * H));
+  TACO_TRY(idx->cb1.ensure(sizeof(float) * (size_t)idx->n_sub * kp * idx->m1));
+  TACO_TRY(idx->cb2.ensure(sizeof(float) * (size_t)idx->n_sub * kp * std::max(idx->m2, 1)));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  std::vector<int64_t> status_h(8);
+  for (int w0 = 0; w0 < H; w0 += NS) {
+    const int w1 = std::min(H, w0 + NS);
+    for (int hh = w0; hh < w1; ++hh) {
+      const int j = hh / 2, b = hh % 2;
+      KMeansRun r;
+      const int m = b ? idx->m2 : idx->m1;
+      r.h.X = idx->T.as<float>() + (size_t)(j * idx->s + (b ? idx->m1 : 0)) * n;
+      r.h.n = n;
+      r.h.m = m;
+      r.h.k = kp;
+      r.s = &idx->bs[hh - w0];
+      r.labels = idx->labels.as<int32_t>() + (size_t)hh * n;
+      r.history = idx->hist.as<double>() + (size_t)hh * idx->iters;
+      r.n_iter = idx->niter.as<int32_t>() + hh;
+      r.cent_out = b ? idx->cb2.as<float>() + (size_t)j * kp * idx->m2 : idx->cb1.as<float>() + (size_t)j * kp * idx->m1;
+      r.iters = idx->iters;
+      TACO_TRY(kmeans_enqueue(r, first_h[hh], uniforms_h + (size_t)hh * std::max(kp - 1, 0),
+                              forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr,
+                              idx->half_streams[hh - w0]));
+    }
+    for (int hh = w0; hh < w1; ++hh) {
+      cudaStream_t st = idx->half_streams[hh - w0];
+      TACO_CHECK_CUDA(cudaMemcpyAsync(status_h.data(), idx->bs[hh - w0].status.p, 8 * 5, cudaMemcpyDeviceToHost, st));
+      TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+      degenerate_h[hh] = (int32_t)status_h[0];
+    }
+  }
+  idx->has_cb = true;
+  idx->has_labels = true;
+  return TACO_OK;
+}
+
+int taco_build_cells(taco_index* idx) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_labels) TACO_FAIL(TACO_ERR_STATE, "labels not available");
+  const int64_t n = idx->n, nc = idx->nchunks;
+  const int kp = idx->kp, K2 = kp * kp;
+  const size_t offs_len = (size_t)nc * K2 + 1;
+  cudaStream_t st = idx->stream;
+  for (auto s : idx->half_streams) TACO_CHECK_CUDA(cudaStreamSynchronize(s));
+  TACO_TRY(idx->ids.ensure(sizeof(uint32_t) * (size_t)n * idx->n_sub));
+  TACO_TRY(idx->offs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
+  TACO_TRY(idx->gsize.ensure(sizeof(int64_t) * (size_t)K2 * idx->n_sub));
+  DevBuf chist, cursor;
+  TACO_TRY(chist.ensure(sizeof(uint32_t) * (size_t)nc * K2));
+  TACO_TRY(cursor.ensure(sizeof(uint32_t) * (size_t)nc * K2));
+  for (int j = 0; j < idx->n_sub; ++j) {
+    const int32_t* l1 = idx->labels.as<int32_t>() + (size_t)(2 * j) * n;
+    const int32_t* l2 = idx->labels.as<int32_t>() + (size_t)(2 * j + 1) * n;
+    uint32_t* offs = idx->offs.as<uint32_t>() + (size_t)j * offs_len;
+    TACO_CHECK_CUDA(cudaMemsetAsync(chist.p, 0, sizeof(uint32_t) * (size_t)nc * K2, st));
+    k_cell_hist<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(l1, l2, n, kp, chist.as<uint32_t>());
+    TACO_LAUNCHED();
+    k_cell_offsets<<<(unsigned)nc, 1024, 0, st>>>(chist.as<uint32_t>(), K2, nc, n, offs);
+    TACO_LAUNCHED();
+    if (idx->n_global == idx->n) {
+      k_cell_sizes<<<(unsigned)ceil_div(K2, 256), 256, 0, st>>>(chist.as<uint32_t>(), K2, nc,
+                                                               idx->gsize.as<int64_t>() + (size_t)j * K2);
+      TACO_LAUNCHED();
+    }
+    TACO_CHECK_CUDA(cudaMemcpyAsync(cursor.p, offs, sizeof(uint32_t) * (size_t)nc * K2, cudaMemcpyDeviceToDevice, st));
+    k_cell_scatter<<<(unsigned)nc, 32, 0, st>>>(l1, l2, n, kp, cursor.as<uint32_t>(),
+                                                idx->ids.as<uint32_t>() + (size_t)j * n);
+    TACO_LAUNCHED();
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  chist.release();
+  cursor.release();
+  if (e != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  idx->has_cells = true;
+  if (idx->n_global == idx->n) idx->has_gsize = true;
+  return TACO_OK;
+}
+
+// local cell sizes of a shard (to be all-reduced into global sizes)
+int taco_get_local_sizes(taco_index* idx, int64_t* sizes_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_cells) TACO_FAIL(TACO_ERR_STATE, "cells not built");
+  const int64_t nc = idx->nchunks;
+  const int K2 = idx->kp * idx->kp;
+  const size_t offs_len = (size_t)nc * K2 + 1;
+  std::vector<uint32_t> offs(offs_len);
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  for (int j = 0; j < idx->n_sub; ++j) {
+    TACO_CHECK_CUDA(cudaMemcpy(offs.data(), idx->offs.as<uint32_t>() + (size_t)j * offs_len,
+                               sizeof(uint32_t) * offs_len, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < K2; ++c) {
+      int64_t s = 0;
+      for (int64_t ch = 0; ch < nc; ++ch) s += offs[ch * K2 + c + 1] - offs[ch * K2 + c];
+      sizes_h[(size_t)j * K2 + c] = s;
+    }
+  }
+  return TACO_OK;
+}
+
+int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, int32_t max_iter,
+                int64_t first, const double* uniforms_h, const int64_t* forced_h, float* centroids_h,
+                int32_t* labels_h, double* history_h, int32_t* n_iter_h, int32_t* degenerate_h) {
+  TACO_TRY(with_device(device));
+  if (k < 1) TACO_FAIL(TACO_ERR_PARAMETER, "cluster count must be positive, got %d", k);
+  if (max_iter < 1) TACO_FAIL(TACO_ERR_PARAMETER, "iteration cap must be positive, got %d", max_iter);
+  if (n < k) TACO_FAIL(TACO_ERR_INSUFFICIENT, "%lld points cannot fill %d clusters", (long long)n, k);
+  // dimension-major copy
+  std::vector<float> tr((size_t)n * m);
+  for (int64_t i = 0; i < n; ++i)
+    for (int t = 0; t < m; ++t) tr[(size_t)t * n + i] = X_h[(size_t)i * m + t];
+  DevBuf X, lab, hist, nit, cent;
+  BuildScratch s;
+  int rc = TACO_OK;
+  cudaStream_t st = nullptr;
+  do {
+    if ((rc = X.ensure(4 * tr.size())) || (rc = lab.ensure(4 * n)) || (rc = hist.ensure(8 * max_iter)) ||
+        (rc = nit.ensure(4)) || (rc = cent.ensure(4 * (size_t)k * m)))
+      break;
+    cudaMemcpy(X.p, tr.data(), 4 * tr.size(), cudaMemcpyHostToDevice);
+    KMeansRun r;
+    r.h.X = X.as<float>();
+    r.h.n = n;
+    r.h.m = m;
+    r.h.k = k;
+    r.s = &s;
+    r.labels = lab.as<int32_t>();
+    r.history = hist.as<double>();
+    r.n_iter = nit.as<int32_t>();
+    r.cent_out = cent.as<float>();
+    r.iters = max_iter;
+    if ((rc = kmeans_enqueue(r, first, uniforms_h, forced_h, st))) break;
+    std::vector<int64_t> status(5);
+    cudaMemcpy(status.data(), s.status.p, 8 * 5, cudaMemcpyDeviceToHost);
+    cudaMemcpy(centroids_h, cent.p, 4 * (size_t)k * m, cudaMemcpyDeviceToHost);
+    cudaMemcpy(labels_h, lab.p, 4 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(history_h, hist.p, 8 * max_iter, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(n_iter_h, nit.p, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
+    *degenerate_h = (int32_t)status[0];
+  } while (0);
+  X.release(); lab.release(); hist.release(); nit.release(); cent.release();
+  DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
+                  &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws};
+  for (auto* b : sb) b->release();
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,435 @@
+// Index lifecycle, host<->device import/export, the fp64 transform GEMM.
+#include <atomic>
+#include <cstring>
+#include <vector>
+
+#include "index.cuh"
+
+namespace taco {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+int DevBuf::ensure(size_t want) {
+  if (want <= bytes && p) return TACO_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  size_t b = want < 256 ? 256 : want;
+  TACO_CHECK_CUDA(cudaMalloc(&p, b));
+  bytes = b;
+  return TACO_OK;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+int with_device(int device) {
+  TACO_CHECK_CUDA(cudaSetDevice(device));
+  return TACO_OK;
+}
+
+int index_check(taco_index* idx) {
+  if (!idx) TACO_FAIL(TACO_ERR_STATE, "null index handle");
+  return with_device(idx->device);
+}
+
+// ------------------------------------------------------------ transform GEMM
+// out = f32((f64 P - f64 mean) @ f64 M) (spectral.py:314-316).  Each output is
+// one FMA chain over k = 0..d-1 starting from 0 -- the OpenBLAS dgemm order
+// (DESIGN.md numerics).  64x64 output tile per 256-thread CTA, 4x4 per thread,
+// k staged 16 at a time through shared memory in fp64.
+constexpr int TM = 64, TN = 64, TK = 16;
+
+__global__ void __launch_bounds__(256) k_transform(const float* __restrict__ P, int64_t np_, int d,
+                                                   int D, const float* __restrict__ mean,
+                                                   const float* __restrict__ M,
+                                                   float* __restrict__ out, int dim_major) {
+  __shared__ double As[TK][TM + 1];
+  __shared__ double Bs[TK][TN + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = int64_t(blockIdx.x) * TM;
+  const int c0 = blockIdx.y * TN;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < d; k0 += TK) {
+    for (int e = threadIdx.x; e < TK * TM; e += 256) {
+      int kk = e % TK, rr = e / TK;
+      int64_t r = r0 + rr;
+      int k = k0 + kk;
+      double v = 0.0;
+      if (r < np_ && k < d) v = __dsub_rn((double)P[r * d + k], (double)mean[k]);
+      As[kk][rr] = v;
+    }
+    for (int e = threadIdx.x; e < TK * TN; e += 256) {
+      int cc = e % TN, kk = e / TN;
+      int c = c0 + cc, k = k0 + kk;
+      Bs[kk][cc] = (c < D && k < d) ? (double)M[(int64_t)k * D + c] : 0.0;
+    }
+    __syncthreads();
+    int kmax = min(TK, d - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = As[kk][ty + 16 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = Bs[kk][tx + 16 * u];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = __fma_rn(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    int64_t r = r0 + ty + 16 * x;
+    if (r >= np_) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      int c = c0 + tx + 16 * y;
+      if (c >= D) continue;
+      float v = __double2float_rn(acc[x][y]);
+      if (dim_major)
+        out[(int64_t)c * np_ + r] = v;
+      else
+        out[r * D + c] = v;
+    }
+  }
+}
+
+int launch_transform(cudaStream_t st, const float* P, int64_t np_, int d, int D, const float* mean,
+                     const float* M, float* out, bool dim_major) {
+  if (np_ == 0) return TACO_OK;
+  dim3 grid((unsigned)ceil_div(np_, TM), (unsigned)ceil_div(D, TN));
+  k_transform<<<grid, 256, 0, st>>>(P, np_, d, D, mean, M, out, dim_major ? 1 : 0);
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
+}  // namespace taco
+
+using namespace taco;
+
+extern "C" {
+
+const char* taco_last_error(void) { return g_err.c_str(); }
+int taco_version(void) { return 1; }
+int64_t taco_launch_count(void) { return g_launches.load(); }
+
+int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int32_t subspace_dim,
+                      int32_t clusters, int32_t kmeans_iters, int64_t n_global, int64_t id_base,
+                      taco_index** out) {
+  if (!out) TACO_FAIL(TACO_ERR_PARAMETER, "null output handle");
+  if (n < 1 || d < 1) TACO_FAIL(TACO_ERR_PARAMETER, "empty data (%lld x %d)", (long long)n, d);
+  if (n_subspaces < 1 || n_subspaces > 255)
+    TACO_FAIL(TACO_ERR_PARAMETER, "subspace count %d outside [1, 255]", n_subspaces);
+  if (subspace_dim < 2) TACO_FAIL(TACO_ERR_PARAMETER, "subspace dimension %d is below 2", subspace_dim);
+  int kp = 0;
+  while ((int64_t)(kp + 1) * (kp + 1) <= clusters) ++kp;
+  if (kp < 1 || kp * kp != clusters)
+    TACO_FAIL(TACO_ERR_PARAMETER, "cluster count %d is not a perfect square", clusters);
+  if (kp > 256) TACO_FAIL(TACO_ERR_PARAMETER, "per-codebook cluster count %d exceeds 256", kp);
+  if ((int64_t)n_subspaces * subspace_dim > d)
+    TACO_FAIL(TACO_ERR_PARAMETER, "subspace budget %d (%d x %d) exceeds data dimension %d",
+              n_subspaces * subspace_dim, n_subspaces, subspace_dim, d);
+  if (n > 0xFFFFFFFFLL) TACO_FAIL(TACO_ERR_PARAMETER, "shard of %lld points exceeds 2^32", (long long)n);
+  if (n_global < n) n_global = n;
+  TACO_TRY(with_device(device));
+  auto* idx = new taco_index();
+  idx->device = device;
+  idx->n = n;
+  idx->n_global = n_global;
+  idx->id_base = id_base;
+  idx->d = d;
+  idx->n_sub = n_subspaces;
+  idx->s = subspace_dim;
+  idx->K = clusters;
+  idx->kp = kp;
+  idx->m1 = (subspace_dim + 1) / 2;
+  idx->m2 = subspace_dim - idx->m1;
+  idx->D = n_subspaces * subspace_dim;
+  idx->iters = kmeans_iters;
+  idx->nchunks = ceil_div(n, kChunk);
+  cudaError_t e = cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete idx;
+    TACO_FAIL(TACO_ERR_CUDA, "stream create: %s", cudaGetErrorString(e));
+  }
+  *out = idx;
+  return TACO_OK;
+}
+
+int taco_index_destroy(taco_index* idx) {
+  if (!idx) return TACO_OK;
+  cudaSetDevice(idx->device);
+  cudaStreamSynchronize(idx->stream);
+  DevBuf* bufs[] = {&idx->X, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
+                    &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
+  for (auto* b : bufs) b->release();
+  QueryTile& q = idx->qt;
+  DevBuf* qb[] = {&q.Q, &q.qt, &q.sd, &q.sl, &q.pops, &q.npop, &q.ret, &q.scores, &q.part,
+                  &q.hist, &q.lvl, &q.cnum, &q.clocal, &q.coff, &q.qbase, &q.total, &q.cand,
+                  &q.d2, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d, &q.out_num, &q.out_lvl};
+  for (auto* b : qb) b->release();
+  for (auto& s : idx->bs) {
+    DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
+                    &s.csq, &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl,
+                    &s.hsum, &s.draws};
+    for (auto* b : sb) b->release();
+  }
+  for (auto st : idx->half_streams) cudaStreamDestroy(st);
+  cudaStreamDestroy(idx->stream);
+  delete idx;
+  return TACO_OK;
+}
+
+int taco_index_set_data(taco_index* idx, const float* X_h) {
+  TACO_TRY(index_check(idx));
+  size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
+  TACO_TRY(idx->X.ensure(bytes));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_h, bytes, cudaMemcpyHostToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->has_X = true;
+  return TACO_OK;
+}
+
+int taco_index_set_data_device(taco_index* idx, const float* X_d) {
+  TACO_TRY(index_check(idx));
+  size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
+  TACO_TRY(idx->X.ensure(bytes));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_d, bytes, cudaMemcpyDeviceToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->has_X = true;
+  return TACO_OK;
+}
+
+int taco_index_set_transform(taco_index* idx, const float* mean_h, const float* matrix_h) {
+  TACO_TRY(index_check(idx));
+  TACO_TRY(idx->mean.ensure(sizeof(float) * idx->d));
+  TACO_TRY(idx->M.ensure(sizeof(float) * (size_t)idx->d * idx->D));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->mean.p, mean_h, sizeof(float) * idx->d, cudaMemcpyHostToDevice));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->M.p, matrix_h, sizeof(float) * (size_t)idx->d * idx->D,
+                             cudaMemcpyHostToDevice));
+  idx->has_model = true;
+  return TACO_OK;
+}
+
+int taco_transform_data(taco_index* idx) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_X || !idx->has_model) TACO_FAIL(TACO_ERR_STATE, "transform needs data and model");
+  TACO_TRY(idx->T.ensure(sizeof(float) * (size_t)idx->n * idx->D));
+  TACO_TRY(launch_transform(idx->stream, idx->X.as<float>(), idx->n, idx->d, idx->D,
+                            idx->mean.as<float>(), idx->M.as<float>(), idx->T.as<float>(), true));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->has_T = true;
+  return TACO_OK;
+}
+
+int taco_index_set_transformed(taco_index* idx, const float* T_h) {
+  TACO_TRY(index_check(idx));
+  const int64_t n = idx->n;
+  const int D = idx->D;
+  std::vector<float> tr((size_t)n * D);
+  for (int64_t r = 0; r < n; ++r)
+    for (int c = 0; c < D; ++c) tr[(size_t)c * n + r] = T_h[(size_t)r * D + c];
+  TACO_TRY(idx->T.ensure(sizeof(float) * tr.size()));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->T.p, tr.data(), sizeof(float) * tr.size(), cudaMemcpyHostToDevice));
+  idx->has_T = true;
+  return TACO_OK;
+}
+
+int taco_get_transformed(taco_index* idx, float* T_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_T) TACO_FAIL(TACO_ERR_STATE, "transformed matrix not available");
+  const int64_t n = idx->n;
+  const int D = idx->D;
+  std::vector<float> tr((size_t)n * D);
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_CHECK_CUDA(cudaMemcpy(tr.data(), idx->T.p, sizeof(float) * tr.size(), cudaMemcpyDeviceToHost));
+  for (int64_t r = 0; r < n; ++r)
+    for (int c = 0; c < D; ++c) T_h[(size_t)r * D + c] = tr[(size_t)c * n + r];
+  return TACO_OK;
+}
+
+int taco_index_set_codebooks(taco_index* idx, const float* cb1_h, const float* cb2_h) {
+  TACO_TRY(index_check(idx));
+  size_t b1 = sizeof(float) * (size_t)idx->n_sub * idx->kp * idx->m1;
+  size_t b2 = sizeof(float) * (size_t)idx->n_sub * idx->kp * idx->m2;
+  TACO_TRY(idx->cb1.ensure(b1));
+  TACO_TRY(idx->cb2.ensure(b2));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->cb1.p, cb1_h, b1, cudaMemcpyHostToDevice));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->cb2.p, cb2_h, b2, cudaMemcpyHostToDevice));
+  idx->has_cb = true;
+  return TACO_OK;
+}
+
+int taco_get_codebooks(taco_index* idx, float* cb1_h, float* cb2_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_cb) TACO_FAIL(TACO_ERR_STATE, "codebooks not built");
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_CHECK_CUDA(cudaMemcpy(cb1_h, idx->cb1.p, sizeof(float) * (size_t)idx->n_sub * idx->kp * idx->m1,
+                             cudaMemcpyDeviceToHost));
+  TACO_CHECK_CUDA(cudaMemcpy(cb2_h, idx->cb2.p, sizeof(float) * (size_t)idx->n_sub * idx->kp * idx->m2,
+                             cudaMemcpyDeviceToHost));
+  return TACO_OK;
+}
+
+int taco_index_set_labels(taco_index* idx, const int32_t* lab1_h, const int32_t* lab2_h) {
+  TACO_TRY(index_check(idx));
+  const int64_t n = idx->n;
+  TACO_TRY(idx->labels.ensure(sizeof(int32_t) * (size_t)n * 2 * idx->n_sub));
+  int32_t* L = idx->labels.as<int32_t>();
+  for (int j = 0; j < idx->n_sub; ++j) {
+    TACO_CHECK_CUDA(cudaMemcpy(L + (size_t)(2 * j) * n, lab1_h + (size_t)j * n, sizeof(int32_t) * n,
+                               cudaMemcpyHostToDevice));
+    TACO_CHECK_CUDA(cudaMemcpy(L + (size_t)(2 * j + 1) * n, lab2_h + (size_t)j * n,
+                               sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  }
+  idx->has_labels = true;
+  return TACO_OK;
+}
+
+int taco_get_labels(taco_index* idx, int32_t* lab1_h, int32_t* lab2_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_labels) TACO_FAIL(TACO_ERR_STATE, "labels not available");
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  const int64_t n = idx->n;
+  const int32_t* L = idx->labels.as<int32_t>();
+  for (int j = 0; j < idx->n_sub; ++j) {
+    TACO_CHECK_CUDA(cudaMemcpy(lab1_h + (size_t)j * n, L + (size_t)(2 * j) * n, sizeof(int32_t) * n,
+                               cudaMemcpyDeviceToHost));
+    TACO_CHECK_CUDA(cudaMemcpy(lab2_h + (size_t)j * n, L + (size_t)(2 * j + 1) * n,
+                               sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  }
+  return TACO_OK;
+}
+
+int taco_get_history(taco_index* idx, double* hist_h, int32_t* n_iter_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->hist.p) TACO_FAIL(TACO_ERR_STATE, "no k-means history (index was imported)");
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_CHECK_CUDA(cudaMemcpy(hist_h, idx->hist.p, sizeof(double) * 2 * idx->n_sub * idx->iters,
+                             cudaMemcpyDeviceToHost));
+  TACO_CHECK_CUDA(cudaMemcpy(n_iter_h, idx->niter.p, sizeof(int32_t) * 2 * idx->n_sub,
+                             cudaMemcpyDeviceToHost));
+  return TACO_OK;
+}
+
+// Cell-major CSR import: rebuild the chunk-major layout on the host (import
+// is not a hot path; it is the v1-file / oracle bridge).
+int taco_index_set_cells(taco_index* idx, const int64_t* offsets_h, const uint32_t* ids_h) {
+  TACO_TRY(index_check(idx));
+  const int64_t n = idx->n, nc = idx->nchunks;
+  const int K2 = idx->kp * idx->kp;
+  const size_t offs_len = (size_t)nc * K2 + 1;
+  TACO_TRY(idx->ids.ensure(sizeof(uint32_t) * (size_t)n * idx->n_sub));
+  TACO_TRY(idx->offs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
+  TACO_TRY(idx->gsize.ensure(sizeof(int64_t) * (size_t)K2 * idx->n_sub));
+  std::vector<uint32_t> ids(n), offs(offs_len);
+  std::vector<int64_t> gs(K2);
+  std::vector<int64_t> cnt((size_t)nc * K2);
+  for (int j = 0; j < idx->n_sub; ++j) {
+    const int64_t* O = offsets_h + (size_t)j * (K2 + 1);
+    const uint32_t* I = ids_h + (size_t)j * n;
+    if (O[0] != 0 || O[K2] != n)
+      TACO_FAIL(TACO_ERR_FORMAT, "subspace %d cells hold %lld ids, expected %lld", j,
+                (long long)(O[K2] - O[0]), (long long)n);
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (int c = 0; c < K2; ++c) {
+      gs[c] = O[c + 1] - O[c];
+      for (int64_t p = O[c]; p < O[c + 1]; ++p) {
+        if (I[p] >= (uint64_t)n) TACO_FAIL(TACO_ERR_FORMAT, "cell id %u out of range", I[p]);
+        cnt[(size_t)(I[p] >> kChunkShift) * K2 + c]++;
+      }
+    }
+    int64_t run = 0;
+    for (size_t e = 0; e < (size_t)nc * K2; ++e) {
+      offs[e] = (uint32_t)run;
+      run += cnt[e];
+    }
+    offs[(size_t)nc * K2] = (uint32_t)run;
+    std::vector<uint32_t> cur(offs.begin(), offs.end() - 1);
+    for (int c = 0; c < K2; ++c)
+      for (int64_t p = O[c]; p < O[c + 1]; ++p) {
+        size_t slot = (size_t)(I[p] >> kChunkShift) * K2 + c;
+        ids[cur[slot]++] = I[p];
+      }
+    TACO_CHECK_CUDA(cudaMemcpy(idx->ids.as<uint32_t>() + (size_t)j * n, ids.data(),
+                               sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    TACO_CHECK_CUDA(cudaMemcpy(idx->offs.as<uint32_t>() + (size_t)j * offs_len, offs.data(),
+                               sizeof(uint32_t) * offs_len, cudaMemcpyHostToDevice));
+    if (!idx->has_gsize || idx->n_global == idx->n)
+      TACO_CHECK_CUDA(cudaMemcpy(idx->gsize.as<int64_t>() + (size_t)j * K2, gs.data(),
+                                 sizeof(int64_t) * K2, cudaMemcpyHostToDevice));
+  }
+  idx->has_cells = true;
+  if (idx->n_global == idx->n) idx->has_gsize = true;
+  return TACO_OK;
+}
+
+int taco_index_set_global_sizes(taco_index* idx, const int64_t* sizes_h) {
+  TACO_TRY(index_check(idx));
+  const int K2 = idx->kp * idx->kp;
+  TACO_TRY(idx->gsize.ensure(sizeof(int64_t) * (size_t)K2 * idx->n_sub));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_CHECK_CUDA(cudaMemcpy(idx->gsize.p, sizes_h, sizeof(int64_t) * (size_t)K2 * idx->n_sub,
+                             cudaMemcpyHostToDevice));
+  idx->has_gsize = true;
+  return TACO_OK;
+}
+
+int taco_get_global_sizes(taco_index* idx, int64_t* sizes_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_gsize) TACO_FAIL(TACO_ERR_STATE, "cell sizes not available");
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  const int K2 = idx->kp * idx->kp;
+  TACO_CHECK_CUDA(cudaMemcpy(sizes_h, idx->gsize.p, sizeof(int64_t) * (size_t)K2 * idx->n_sub,
+                             cudaMemcpyDeviceToHost));
+  return TACO_OK;
+}
+
+int taco_get_cells(taco_index* idx, int32_t j, int64_t* offsets_h, uint32_t* ids_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_cells) TACO_FAIL(TACO_ERR_STATE, "cells not built");
+  if (j < 0 || j >= idx->n_sub) TACO_FAIL(TACO_ERR_PARAMETER, "subspace %d out of range", j);
+  const int64_t n = idx->n, nc = idx->nchunks;
+  const int K2 = idx->kp * idx->kp;
+  const size_t offs_len = (size_t)nc * K2 + 1;
+  std::vector<uint32_t> ids(n), offs(offs_len);
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_CHECK_CUDA(cudaMemcpy(ids.data(), idx->ids.as<uint32_t>() + (size_t)j * n,
+                             sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+  TACO_CHECK_CUDA(cudaMemcpy(offs.data(), idx->offs.as<uint32_t>() + (size_t)j * offs_len,
+                             sizeof(uint32_t) * offs_len, cudaMemcpyDeviceToHost));
+  // cell-major = for each cell, its chunk slices in chunk order (ids ascending)
+  int64_t w = 0;
+  for (int c = 0; c < K2; ++c) {
+    offsets_h[c] = w;
+    for (int64_t ch = 0; ch < nc; ++ch) {
+      size_t e = (size_t)ch * K2 + c;
+      for (uint32_t p = offs[e]; p < offs[e + 1]; ++p) ids_h[w++] = ids[p];
+    }
+  }
+  offsets_h[K2] = w;
+  return TACO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// Device-resident TaCo index (one point shard per GPU) and its scratch.
+//
+// HBM layout:
+//   X      f32 [n][d]            base vectors (row-major, rerank gathers rows)
+//   T      f32 [D][n]            transformed points, dimension-major so each
+//                                 k-means half is m contiguous n-vectors
+//   cb1/2  f32 [Ns][K'][m1|m2]   codebooks (centroids), labels i32 [2Ns][n]
+//   ids    u32 [Ns][n]           CSR ids, ordered (chunk, cell, id): chunk c
+//                                 holds ids [c*CH, (c+1)*CH) so one CTA's
+//                                 score table covers exactly one chunk
+//   offs   u32 [Ns][nchunks*K'^2+1] start of (chunk, cell) inside ids
+//   gsize  i64 [Ns][K'^2]        GLOBAL cell sizes (all shards) for traversal
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace taco {
+
+constexpr int kChunkShift = 16;                 // CH = 65536 ids per score table
+constexpr int64_t kChunk = int64_t(1) << kChunkShift;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct QueryTile {
+  DevBuf Q, qt, sd, sl, pops, npop, ret, scores, part, hist, lvl, cnum, clocal, coff, qbase, total,
+      cand, d2, tk_d2, tk_ids, out_ids, out_d, out_num, out_lvl;
+};
+
+struct BuildScratch {
+  DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
+      loff, ctl, hsum, draws;
+};
+
+}  // namespace taco
+
+struct taco_index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0, n_global = 0, id_base = 0, nchunks = 0;
+  int d = 0, n_sub = 0, s = 0, K = 0, kp = 0, m1 = 0, m2 = 0, D = 0, iters = 0;
+  taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
+  bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,
+       has_cells = false, has_gsize = false;
+  std::vector<cudaStream_t> half_streams;
+  taco::QueryTile qt;
+  std::vector<taco::BuildScratch> bs;
+};
+
+namespace taco {
+int with_device(int device);
+int index_check(taco_index* idx);
+// kernels shared between translation units
+int launch_transform(cudaStream_t st, const float* P, int64_t np_, int d, int D,
+                     const float* mean, const float* M, float* out, bool dim_major);
+}  // namespace taco

@@ -1,0 +1,136 @@
+"""GPU parity of the build path."""
+
+import numpy as np
+import pytest
+
+import paper_2603_24919_b200 as T
+from oracle import taco_oracle as O
+from paper_2603_24919_b200.workloads import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+def test_kmeans_units_bit_exact(golden):
+    u = golden("units")
+    for c in range(6):
+        n, m, k, it, sd = (int(v) for v in u[f"km{c}_cfg"])
+        X = np.random.default_rng(1000 + c).normal(size=(n, m)).astype(np.float32)
+        if c == 3:
+            X[100:300] = X[0]
+        r = T.kmeans(X, k, it, sd)
+        np.testing.assert_array_equal(r.assignments, u[f"km{c}_lab"])
+        np.testing.assert_array_equal(r.centroids, u[f"km{c}_cent"])
+        assert r.n_iter == len(u[f"km{c}_hist"])
+        np.testing.assert_allclose(r.inertia_history, u[f"km{c}_hist"], rtol=1e-12, atol=1e-9)
+
+
+def test_kmeans_reference_unit_cases():
+    # clustering tests of the reference (test_clustering.py:12-86)
+    data = np.array([[0.0], [1.0], [10.0], [11.0]], dtype=np.float32)
+    m = T.kmeans(data, 2, max_iter=10, seed=3)
+    assert sorted(m.centroids[:, 0].tolist()) == pytest.approx([0.5, 10.5])
+    assert m.inertia == pytest.approx(1.0)
+    rng = np.random.default_rng(0)
+    data = rng.normal(size=(30, 4)).astype(np.float32)
+    m = T.kmeans(data, 1, max_iter=5, seed=1)
+    np.testing.assert_allclose(m.centroids[0], data.astype(np.float64).mean(axis=0), rtol=1e-5)
+    assert np.all(m.assignments == 0)
+    with pytest.raises(T.InsufficientDataError):
+        T.kmeans(np.ones((2, 3), dtype=np.float32), 4)
+    dup = np.zeros((20, 2), np.float32)      # all points identical -> D^2 total 0
+    dup[:3] = [[1, 1], [2, 2], [3, 3]]
+    r = T.kmeans(dup, 6, 5, 9)
+    o = O.kmeans(dup, 6, 5, 9)
+    np.testing.assert_array_equal(r.assignments, o.labels)
+    np.testing.assert_array_equal(r.centroids, o.centroids)
+
+
+@pytest.mark.parametrize("shape,k,seed", [((5000, 8), 64, 1), ((3000, 30), 50, 2),
+                                          ((70000, 6), 128, 3), ((200, 2), 256 - 60, 4)])
+def test_kmeans_vs_oracle(shape, k, seed):
+    X = np.random.default_rng(seed).normal(size=shape).astype(np.float32)
+    r = T.kmeans(X, k, 20, seed)
+    o = O.kmeans(X, k, 20, seed)
+    np.testing.assert_array_equal(r.assignments, o.labels)
+    np.testing.assert_array_equal(r.centroids, o.centroids)
+
+
+def test_build_subspace_index_vs_oracle():
+    X = np.random.default_rng(7).normal(size=(4000, 7)).astype(np.float32)
+    imi = T.build_subspace_index(X, 49, 10, 11)
+    split = 4
+    c1 = O.kmeans(X[:, :split], 7, 10, O.derive_seed(11, 0))
+    c2 = O.kmeans(X[:, split:], 7, 10, O.derive_seed(11, 1))
+    cells = O.cells_from_labels(c1.labels, c2.labels)
+    assert imi.split == 4 and imi.codebook2.dim == 3
+    assert sorted(imi.cells) == sorted(cells)
+    for key in cells:
+        np.testing.assert_array_equal(imi.cells[key], cells[key])
+
+
+@pytest.fixture(scope="module", params=["rig1", "rig2", "rig3"])
+def built(request, golden):
+    g = golden(request.param)
+    cfg, n, nq, d, ns, s, kp, it, seed = (int(v) for v in g["params"])
+    X, Q, _ = make_config(cfg, n=n, nq=nq, d=d)
+    idx = T.build_index(X, T.IndexParams(ns, s, kp * kp, it, seed))
+    return g, X, Q, idx
+
+
+def test_build_transform(built):
+    g, X, Q, idx = built
+    np.testing.assert_array_equal(idx.transform.mean, g["mean"])   # sequential fp64 mean
+    blocks = np.stack(idx.transform.blocks)
+    # covariance accumulates in a different fp64 order than OpenBLAS syrk:
+    # blocks agree to a few f32 ulps
+    np.testing.assert_allclose(blocks, g["blocks"], rtol=0, atol=2e-6)
+
+
+def test_build_end_to_end(built):
+    g, X, Q, idx = built
+    blob = T.serialize_index(idx)
+    same_model = np.array_equal(np.stack(idx.transform.blocks), g["blocks"])
+    if same_model:
+        assert blob == g["blob"].tobytes()
+    # oracle reads the GPU-built index and must answer identically
+    oidx = O.deserialize(blob)
+    for gi, (alpha, beta, k) in enumerate(g["grid"]):
+        qp = T.QueryParams(float(alpha), float(beta), int(k))
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+        oi, od, on, ol = O.knn_batch(oidx, X, Q, float(alpha), float(beta), int(k))
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(dists, od)
+        np.testing.assert_array_equal(num, on)
+        np.testing.assert_array_equal(lvl, ol)
+
+
+def test_build_stagewise_kmeans_cells(built):
+    """Given the GPU transform, every label / centroid / cell equals the
+    oracle's k-means over the same T (P2, P3)."""
+    g, X, Q, idx = built
+    p = idx.params
+    model = (idx.transform.mean, list(idx.transform.blocks))
+    Tm = T.transform_points(idx.transform, X)
+    o = O.build_index(X, p.n_subspaces, p.subspace_dim, p.clusters, p.kmeans_iters, p.seed,
+                      T=Tm, model=model)
+    for j, sub in enumerate(idx.subspaces):
+        np.testing.assert_array_equal(sub.codebook1.assignments, o.labels[j][0])
+        np.testing.assert_array_equal(sub.codebook2.assignments, o.labels[j][1])
+        np.testing.assert_array_equal(sub.codebook1.centroids, o.cb1[j])
+        np.testing.assert_array_equal(sub.codebook2.centroids, o.cb2[j])
+        assert sorted(sub.cells) == sorted(o.cells[j])
+    assert T.serialize_index(idx) == O.serialize(o)
+
+
+def test_build_validation():
+    X = np.random.default_rng(6).normal(size=(50, 6)).astype(np.float32)
+    with pytest.raises(T.ParameterError) as err:
+        T.build_index(X, T.IndexParams(n_subspaces=3, subspace_dim=4, clusters=4))
+    assert "12" in str(err.value) and "6" in str(err.value)
+    bad = X.copy()
+    bad[7, 2] = np.nan
+    with pytest.raises(T.NumericError):
+        T.build_index(bad, T.IndexParams(n_subspaces=1, subspace_dim=4, clusters=4))
+    one = T.build_index(X, T.IndexParams(n_subspaces=1, subspace_dim=4, clusters=1, kmeans_iters=3))
+    (cells,) = [s.cells for s in one.subspaces]
+    assert list(cells) == [(0, 0)] and cells[(0, 0)].size == 50

@@ -1,0 +1,157 @@
+"""GPU parity of the query path: the reference-built index
+(golden v1 bytes) imported onto the B200 must reproduce the reference's
+scores, pop traces, candidate counts, thresholds, top-k ids and distances
+bit-for-bit."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2603_24919_b200 as T
+from oracle import taco_oracle as O
+from paper_2603_24919_b200.workloads import make_config
+
+pytestmark = pytest.mark.gpu
+RIGS = ["rig1", "rig2", "rig3"]
+
+
+def _digest(a):
+    return hashlib.blake2b(np.ascontiguousarray(a).tobytes(), digest_size=16).hexdigest()
+
+
+@pytest.fixture(scope="module", params=RIGS)
+def rig(request, golden):
+    g = golden(request.param)
+    cfg, n, nq, d, ns, s, kp, it, seed = (int(v) for v in g["params"])
+    X, Q, _ = make_config(cfg, n=n, nq=nq, d=d)
+    idx = T.deserialize_index(g["blob"].tobytes())
+    return g, X, Q, idx
+
+
+def test_batch_matches_reference(rig):
+    g, X, Q, idx = rig
+    for gi, (alpha, beta, k) in enumerate(g["grid"]):
+        qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+        np.testing.assert_array_equal(num, g[f"num_{gi}"])
+        np.testing.assert_array_equal(lvl, g[f"lvl_{gi}"])
+        np.testing.assert_array_equal(ids, g[f"ids_{gi}"])
+        np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
+
+
+def test_single_query_api(rig):
+    g, X, Q, idx = rig
+    alpha, beta, k = g["grid"][0]
+    qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
+    for qi in range(min(4, Q.shape[0])):
+        res = T.knn_query(idx, X, Q[qi], qp)
+        want = g["ids_0"][qi]
+        want = want[want >= 0]
+        np.testing.assert_array_equal(res.ids, want)
+        assert res.ids.dtype == np.int32 and res.dists.dtype == np.float32
+
+
+def test_scores_and_traces(rig):
+    g, X, Q, idx = rig
+    for gi, (alpha, _, _) in enumerate(g["grid"]):
+        for qi in range(Q.shape[0]):
+            sc = T.count_collisions(idx, Q[qi], float(alpha))
+            assert _digest(sc) == g[f"scores_digest_{gi}"][qi]
+        pops = g[f"pops_{gi}"]
+        s = idx.params.subspace_dim
+        for qi in range(4):
+            qt = T.transform_points(idx.transform, Q[qi][None, :])[0]
+            for j, sub in enumerate(idx.subspaces):
+                d1, i1, d2, i2 = T.sorted_centroid_distances(sub, qt[j * s:(j + 1) * s])
+                act = T.scalable_dynamic_activation(float(alpha), idx.n, idx.params.clusters,
+                                                    d1, i1, d2, i2, sub)
+                ref = pops[(pops[:, 0] == qi) & (pops[:, 1] == j)]
+                mine = np.array([(qi, j, a, b, key, act.retrieved_num) for key, a, b in act.pop_trace])
+                np.testing.assert_array_equal(mine, ref)
+
+
+def test_select_and_rerank_taps(rig):
+    g, X, Q, idx = rig
+    alpha, beta, k = g["grid"][0]
+    for qi in range(3):
+        sc = T.count_collisions(idx, Q[qi], float(alpha))
+        cand = T.select_candidates(sc, float(beta), idx.params.n_subspaces, idx.n)
+        ids, num, lvl, _ = O.select(sc, float(beta), idx.params.n_subspaces, idx.n)
+        np.testing.assert_array_equal(cand.ids, ids)
+        assert (cand.candidate_num, cand.last_collision) == (num, lvl)
+        res = T.rerank(X, Q[qi], cand, int(k))
+        rid, rd, _ = O.rerank(X, Q[qi], ids, int(k))
+        np.testing.assert_array_equal(res.ids, rid)
+        np.testing.assert_array_equal(res.dists, rd)
+
+
+def test_transform_points_matches_reference(rig):
+    g, X, Q, idx = rig
+    np.testing.assert_array_equal(T.transform_points(idx.transform, X[:200]), g["T_head"])
+    qt = T.transform_points(idx.transform, Q)
+    # reference transforms one query at a time through dgemv (different fp64
+    # summation order); after the f32 cast at most isolated 1-ulp flips remain
+    diff = qt != g["QT"]
+    assert diff.mean() < 1e-3
+    np.testing.assert_allclose(qt, g["QT"], rtol=2e-7, atol=1e-6)
+
+
+def test_select_edge_cases():
+    rng = np.random.default_rng(0)
+    for hist, beta, ns, want in [([70, 20, 7, 3], 0.1, 3, (2, 10)), ([60, 20, 12, 8], 0.1, 3, (3, 8))]:
+        sc = np.repeat(np.arange(len(hist)), hist).astype(np.uint8)
+        rng.shuffle(sc)
+        c = T.select_candidates(sc, beta, ns)
+        assert (c.last_collision, c.candidate_num) == want
+        assert np.all(sc[c.ids] >= c.last_collision)
+    sc = np.zeros(10, np.uint8)
+    sc[:2] = 1
+    c = T.select_candidates(sc, 0.99, 2)              # clamp at 0 -> everything
+    assert (c.last_collision, c.candidate_num) == (0, 10)
+    np.testing.assert_array_equal(c.ids, np.arange(10))
+    big = rng.integers(0, 9, 300_000).astype(np.uint8)  # several 64 Ki chunks
+    for beta in (0.001, 0.01, 0.2, 0.9):
+        c = T.select_candidates(big, beta, 8)
+        ids, num, lvl, _ = O.select(big, beta, 8)
+        np.testing.assert_array_equal(c.ids, ids)
+        assert (c.candidate_num, c.last_collision) == (num, lvl)
+
+
+def test_rerank_edge_cases():
+    rng = np.random.default_rng(1)
+    X = rng.normal(size=(500, 7)).astype(np.float32)      # d not a multiple of 4
+    X[10] = X[20]                                          # exact distance tie
+    q = X[10].copy()
+    ids = np.array([300, 20, 10, 5, 499], np.int64)       # unsorted input
+    res = T.rerank(X, q, ids, 3)
+    rid, rd, _ = O.rerank(X, q, ids, 3)
+    np.testing.assert_array_equal(res.ids, rid)
+    np.testing.assert_array_equal(res.dists, rd)
+    assert list(res.ids[:2]) == [10, 20] and res.dists[0] == 0.0
+    res = T.rerank(X, q, np.array([7], np.int64), 10)      # |C| < k
+    assert res.ids.size == 1
+    res = T.rerank(X, q, np.empty(0, np.int64), 10)
+    assert res.ids.size == 0 and res.ids.dtype == np.int32
+
+
+def test_traversal_units(golden):
+    u = golden("units")
+    for c in range(int(u["n_trav"][0])):
+        d1, d2, sizes = u[f"tr{c}_d1"], u[f"tr{c}_d2"], u[f"tr{c}_sizes"]
+        kp = d1.size
+        cells = {}
+        base = 0
+        for a in range(kp):
+            for b in range(kp):
+                if sizes[a, b]:
+                    cells[(a, b)] = np.arange(base, base + sizes[a, b], dtype=np.uint32)
+                    base += sizes[a, b]
+        cb = T.KMeansModel(np.zeros((kp, 1), np.float32), None, 0.0)
+        imi = T.InvertedMultiIndex(cb, cb, cells, kp, 1)
+        act = T.scalable_dynamic_activation(float(u[f"tr{c}_alpha"][0]), int(sizes.sum()), kp * kp,
+                                            d1, np.argsort(d1, kind="stable"), d2,
+                                            np.argsort(d2, kind="stable"), imi)
+        np.testing.assert_array_equal(np.array([(a, b) for _, a, b in act.pop_trace]).reshape(-1, 2),
+                                      u[f"tr{c}_pops"].reshape(-1, 2))
+        assert act.retrieved_num == int(u[f"tr{c}_ret"][0])
