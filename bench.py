@@ -1,0 +1,360 @@
+"""TaCo B200 benchmark: batched k-ANN queries/sec (+ index build seconds).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json metric "queries/sec at matched recall@10 (1Mx128
+fp32, batch 10k); index build seconds"): config 2 -- n=1,000,000 d=128
+integer-valued fp32 (SURVEY 8(d) generator), N_s=8, s=16, K'=64, alpha=0.03,
+beta=0.003, k=10, one step = one batch of 10,000 queries.
+
+ours:      device-resident timed steps (CUDA events on the library stream,
+           L2 flushed between steps) -> value; the public API with pinned
+           host buffers -> e2e; one profiled pass -> per-kernel roofline;
+           the CPU oracle on a bounded query sample -> cpu_baseline.
+reference: the oracle port (numpy restatement of the reference path, all
+           host cores, thread pool like bench._query_pass) on bounded
+           samples of the same workload.  Its index is the GPU-built one
+           loaded through the v1 format (same bytes the oracle would read).
+N > 1 (torchrun): points sharded over ranks, NCCL all-reduce of the per-query
+           score histograms + top-k merge (paper_2603_24919_b200.distributed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries/sec at matched recall@10 (1Mx128 fp32, batch 10k); index build seconds"
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        busy = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(busy or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def workload(args):
+    from paper_2603_24919_b200.workloads import make_config
+    t = time.perf_counter()
+    X, Q, meta = make_config(args.config, n=args.n, nq=args.nq)
+    meta["gen_seconds"] = time.perf_counter() - t
+    return X, Q, meta
+
+
+def workload_name(meta):
+    return (f"cfg{meta['cfg']}: n={meta['n']:,} d={meta['d']} N_s={meta['n_sub']} s={meta['s']} "
+            f"K'={meta['kprime']} alpha={meta['alpha']} beta={meta['beta']} k={meta['k']} "
+            f"batch={meta['nq']:,}")
+
+
+def build(X, meta):
+    import paper_2603_24919_b200 as T
+    params = T.IndexParams(meta["n_sub"], meta["s"], meta["clusters"], meta["kmeans_iters"], meta["seed"])
+    t = time.perf_counter()
+    index = T.build_index(X, params)
+    wall = time.perf_counter() - t
+    return index, wall
+
+
+def path_bytes(stats, meta, nq_total):
+    """B_q = 4*sum_j R_j + n + (4d+4)|C| + 4d + 8 min(k,|C|)."""
+    d, n, k = meta["d"], meta["n"], meta["k"]
+    return (4 * stats["sum_retrieved"] + n * nq_total + (4 * d + 4) * stats["sum_candidates"]
+            + 4 * d * nq_total + 8 * k * nq_total)
+
+
+def kernel_bytes(name, stats, meta):
+    d = meta["d"]
+    C, R, P = stats["sum_candidates"], stats["sum_retrieved"], stats["sum_pops"]
+    return {
+        "k_rerank": (4 * d + 4 + 8) * C,
+        "k_count": 4 * R + stats["score_bytes"] + 10 * P * max(1, meta["n"] // 65536),
+        "k_compact": stats["score_bytes"] + 4 * C,
+        "k_topk": 12 * C,
+    }.get(name)
+
+
+def ncu_traffic(name):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(name)
+    except Exception:
+        return None
+
+
+def cpu_baseline(index, X, Q, meta, ids_gpu, budget_s=15.0, threads=None):
+    """Oracle port on the host cores, bounded sample; checks parity too."""
+    import paper_2603_24919_b200 as T
+    from oracle import taco_oracle as O
+    threads = threads or os.cpu_count() or 1
+    oidx = O.deserialize(T.serialize_index(index))
+    a, b, k = meta["alpha"], meta["beta"], meta["k"]
+    probe = min(32, Q.shape[0])
+    t = time.perf_counter()
+    O.knn_batch(oidx, X, Q[:probe], a, b, k, threads=threads)
+    rate = probe / (time.perf_counter() - t)
+    sample = int(min(Q.shape[0], max(probe, rate * budget_s)))
+    t = time.perf_counter()
+    oi, od, on, ol = O.knn_batch(oidx, X, Q[:sample], a, b, k, threads=threads)
+    el = time.perf_counter() - t
+    parity = None if ids_gpu is None else bool(np.array_equal(oi, ids_gpu[:sample]))
+    return {"value": sample / el, "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"first {sample} of {Q.shape[0]} queries of the same batch, GPU-built index via v1 bytes",
+            "seconds": el, "topk_identical_to_gpu": parity}
+
+
+def run_reference(args):
+    """--impl reference: timed CPU oracle (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2603_24919_b200 as T
+    from oracle import taco_oracle as O
+    X, Q, meta = workload(args)
+    index, _ = build(X, meta)
+    oidx = O.deserialize(T.serialize_index(index))
+    threads = os.cpu_count() or 1
+    a, b, k = meta["alpha"], meta["beta"], meta["k"]
+    per = args.ref_sample
+    times = []
+    for s in range(args.warmup + args.steps):
+        lo = (s * per) % Q.shape[0]
+        qs = Q[lo:lo + per]
+        t = time.perf_counter()
+        O.knn_batch(oidx, X, qs, a, b, k, threads=threads)
+        el = time.perf_counter() - t
+        if s >= args.warmup:
+            times.append((qs.shape[0], el))
+    nq = sum(c for c, _ in times)
+    tot = sum(e for _, e in times)
+    value = nq / tot
+    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(meta), "step": f"{per} queries of the batch"},
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+                             "sample": f"{per} queries per step, {args.steps} timed steps"},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import paper_2603_24919_b200 as T
+    from paper_2603_24919_b200 import _native as nat
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_2603_24919_b200 import distributed as dist_mod
+        return dist_mod.bench_main(args, METRIC)
+    torch.cuda.set_device(0)
+    X, Q, meta = workload(args)
+    index, build_wall = build(X, meta)
+    dev = index.device
+    qp = T.QueryParams(meta["alpha"], meta["beta"], meta["k"])
+    nq, d, k = Q.shape[0], meta["d"], meta["k"]
+    stream_ptr = nat.lib().taco_index_stream(dev.h)
+    stream = torch.cuda.ExternalStream(stream_ptr)
+    Qd = torch.from_numpy(Q).cuda()
+    ids_d = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    dist_d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    num_d = torch.empty(nq, dtype=torch.int64, device="cuda")
+    lvl_d = torch.empty(nq, dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+
+    def device_step():
+        nat.call("taco_query_batch_device", dev.h, Qd.data_ptr(), nq, qp.alpha, qp.beta, k,
+                 ids_d.data_ptr(), dist_d.data_ptr(), num_d.data_ptr(), lvl_d.data_ptr(), stream_ptr)
+
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+    times = []
+    launches0 = nat.launch_count()
+    with Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0)) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            device_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = (nat.launch_count() - launches0) // args.steps
+    ms = statistics.mean(times)
+    value = nq / (ms / 1000.0)
+    ids_gpu = ids_d.cpu().numpy()
+
+    # e2e through the public API: pinned host queries in, host results out
+    Qp = torch.empty((nq, d), dtype=torch.float32, pin_memory=True).numpy()
+    Qp[:] = Q
+    T.knn_query_batch(index, X, Qp, qp)
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = T.knn_query_batch(index, X, Qp, qp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    assert np.array_equal(out[0], ids_gpu), "public API and device path disagree"
+    e2e_ms = statistics.mean(e2e_times)
+
+    # one profiled pass: per-kernel CUDA-event times on the launching stream
+    nat.profile_enable(True)
+    flush.zero_()
+    torch.cuda.synchronize()
+    device_step()
+    torch.cuda.synchronize()
+    prof, stats = nat.profile_read(reset=True)
+    nat.profile_enable(False)
+    total_prof = sum(v[0] for v in prof.values())
+    dom = max(prof, key=lambda kname: prof[kname][0])
+    peak, peak_kind = peaks()
+    kb = kernel_bytes(dom, stats, meta)
+    dom_ms, dom_n = prof[dom]
+    roof = None
+    if kb is not None and dom_ms > 0:
+        ach = kb / (dom_ms / 1000.0) / 1e9
+        tr = ncu_traffic(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": tr, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": kb / max(dom_n, 1),
+                "avg_launch_ms": dom_ms / max(dom_n, 1), "launches": dom_n,
+                "share_of_step": dom_ms / total_prof}
+    pb = path_bytes(stats, meta, nq)
+    path = {"algorithmic_bytes_per_step": pb, "achieved": pb / (ms / 1000.0) / 1e9, "peak": peak,
+            "frac": pb / (ms / 1000.0) / 1e9 / peak, "unit": "GB/s",
+            "kernels_ms": {kname: round(v[0], 4) for kname, v in prof.items()},
+            "mean_candidates": stats["sum_candidates"] / nq,
+            "mean_retrieved_per_subspace": stats["sum_retrieved"] / nq / meta["n_sub"],
+            "mean_pops_per_subspace": stats["sum_pops"] / nq / meta["n_sub"]}
+
+    # recall@10 on a 100-query sample against exact ground truth (oracle GT)
+    from oracle import taco_oracle as O
+    gs = min(100, nq)
+    gt_ids, _ = O.ground_truth(X, Q[:gs], k)
+    rec = float(np.mean([len(set(ids_gpu[i]) & set(gt_ids[i])) / k for i in range(gs)]))
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline(index, X, Q, meta, ids_gpu, args.cpu_budget)
+    h2d = nq * d * 4
+    d2h = nq * k * 8 + nq * 12
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8(d) generator, seeded)",
+        "config": {"workload": workload_name(meta), "n": meta["n"], "d": d, "batch": nq,
+                   "l2": "256 MiB buffer written between timed steps; X (512 MB) > L2",
+                   "build_seconds": build_wall, "build_breakdown": {
+                       kk: index.metadata[kk] for kk in ("covariance_seconds", "eigensolve_seconds",
+                                                         "transform_seconds", "kmeans_seconds")},
+                   "recall@10_sample100": rec},
+        "build_seconds": build_wall,
+        "e2e": {"value": nq / (e2e_ms / 1000.0), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "path_roofline": path,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "step_ms": times,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-sample", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,15 @@ int taco_topk_merge_device(int32_t ranks, int64_t nq, int32_t k, const double* d
                            const int64_t* ids_d, int32_t* ids_out_d, float* dists_out_d,
                            void* stream);
 
+/* --------------------------------------------------------------- profiling */
+/* Per-kernel CUDA-event timing of the query path on its launching stream. */
+int taco_profile_enable(int on);
+int taco_profile_read(double* ms_out, int64_t* cnt_out, int64_t* stats_out, int reset);
+const char* taco_profile_name(int i);
+int taco_profile_kernels(void);
+/* The index's own CUDA stream (cudaStream_t as void*). */
+void* taco_index_stream(taco_index* idx);
+
 /* -------------------------------------------------- fine-grained taps/API */
 /* engine.count_collisions for one query (engine.py:188-220): scores_h[n] u8. */
 int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* scores_h);

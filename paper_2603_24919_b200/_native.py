@@ -62,10 +62,16 @@ _SIGS = {
     "taco_centroid_order": [_c_int, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_traverse": [_c_int, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp],
     "taco_transform_points": [_c_int, _vp, _vp, _c_i32, _c_i32, _vp, _c_i64, _vp],
+    "taco_profile_enable": [_c_int],
+    "taco_profile_read": [_vp, _vp, _vp, _c_int],
+    "taco_profile_name": [_c_int],
+    "taco_profile_kernels": [],
+    "taco_index_stream": [_vp],
     "taco_kmeans": [_c_int, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp],
 }
-_RESTYPES = {"taco_last_error": ctypes.c_char_p, "taco_launch_count": _c_i64}
+_RESTYPES = {"taco_last_error": ctypes.c_char_p, "taco_launch_count": _c_i64,
+             "taco_profile_name": ctypes.c_char_p, "taco_index_stream": _vp}
 
 _CODES = {
     1: errors.ParameterError,
@@ -156,3 +162,19 @@ class DeviceIndex:
             self.close()
         except Exception:
             pass
+
+
+def profile_enable(on: bool):
+    check(lib().taco_profile_enable(1 if on else 0))
+
+
+def profile_read(reset=True):
+    """{kernel: (total_ms, launches)}, stats dict."""
+    nk = lib().taco_profile_kernels()
+    ms = np.zeros(nk)
+    cnt = np.zeros(nk, np.int64)
+    st = np.zeros(6, np.int64)
+    check(lib().taco_profile_read(ptr(ms), ptr(cnt), ptr(st), 1 if reset else 0))
+    names = [lib().taco_profile_name(i).decode() for i in range(nk)]
+    keys = ("sum_retrieved", "sum_candidates", "sum_pops", "queries", "tiles", "score_bytes")
+    return {n: (float(m), int(c)) for n, m, c in zip(names, ms, cnt)}, dict(zip(keys, map(int, st)))

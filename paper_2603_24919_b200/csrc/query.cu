@@ -19,6 +19,57 @@
 
 namespace taco {
 
+// ------------------------------------------------------------- profiler
+// Optional per-kernel timing with CUDA events recorded on the launching
+// stream (bench.py's roofline), plus algorithmic-work counters.
+enum KId { K_TRANSFORM, K_CSORT, K_TRAVERSE, K_COUNT, K_HIST, K_SELECT, K_COMPACT, K_RERANK, K_TOPK,
+           K_FINAL, K_NKIDS };
+static const char* kKNames[K_NKIDS] = {"k_transform", "k_csort", "k_traverse", "k_count", "k_hist_reduce",
+                                       "k_select", "k_compact", "k_rerank", "k_topk", "k_finalize"};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct P { int kid; cudaEvent_t a, b; };
+  std::vector<P> pend;
+  double ms[K_NKIDS] = {};
+  int64_t cnt[K_NKIDS] = {};
+  int64_t sumR = 0, sumC = 0, sumPops = 0, queries = 0, tiles = 0, bytes_scores = 0;
+};
+static Prof g_prof;
+static cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) { cudaEvent_t e = g_prof.pool.back(); g_prof.pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  int kid;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, cudaStream_t s) : kid(k), st(s) {
+    if (g_prof.on) { a = prof_event(); cudaEventRecord(a, st); }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, st);
+      g_prof.pend.push_back({kid, a, b});
+    }
+  }
+};
+static void prof_drain() {
+  for (auto& p : g_prof.pend) {
+    cudaEventSynchronize(p.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    g_prof.ms[p.kid] += ms;
+    g_prof.cnt[p.kid] += 1;
+    g_prof.pool.push_back(p.a);
+    g_prof.pool.push_back(p.b);
+  }
+  g_prof.pend.clear();
+}
+
 // ------------------------------------------------------------------ csort
 // One warp per (query, subspace, half): fp64 direct-form distances to the K'
 // centroids (einsum order) and their stable ascending rank (ties -> lower label).
@@ -783,11 +834,15 @@ static int run_count_stage(taco_index* idx, int Q, double alpha, cudaStream_t st
                            double* keys_out) {
   QueryTile& t = idx->qt;
   const int kp = idx->kp;
-  TACO_TRY(launch_transform(st, t.Q.as<float>(), Q, idx->d, idx->D, idx->mean.as<float>(),
-                            idx->M.as<float>(), t.qt.as<float>(), false));
+  {
+    ProfScope ps(K_TRANSFORM, st);
+    TACO_TRY(launch_transform(st, t.Q.as<float>(), Q, idx->d, idx->D, idx->mean.as<float>(),
+                              idx->M.as<float>(), t.qt.as<float>(), false));
+  }
   {
     const int64_t warps = (int64_t)Q * idx->n_sub * 2;
     const int wpb = 8;
+    ProfScope ps(K_CSORT, st);
     k_csort<<<(unsigned)ceil_div(warps, wpb), wpb * 32, sizeof(double) * kp * wpb, st>>>(
         t.qt.as<float>(), Q, idx->n_sub, idx->s, idx->m1, idx->m2, kp, idx->cb1.as<float>(),
         idx->cb2.as<float>(), t.sd.as<double>(), t.sl.as<uint16_t>());
@@ -797,6 +852,7 @@ static int run_count_stage(taco_index* idx, int Q, double alpha, cudaStream_t st
     const int64_t th = (int64_t)Q * idx->n_sub;
     const int64_t target = retrieval_target(alpha, idx->n_global);
     const unsigned g = (unsigned)ceil_div(th, 128);
+    ProfScope ps(K_TRAVERSE, st);
 #define TRAV(KM)                                                                              \
   k_traverse<KM><<<g, 128, 0, st>>>(t.sd.as<double>(), t.sl.as<uint16_t>(),                   \
                                     idx->gsize.as<int64_t>(), Q, idx->n_sub, kp, target,        \
@@ -817,15 +873,19 @@ static int run_count_stage(taco_index* idx, int Q, double alpha, cudaStream_t st
       attr = true;
     }
     dim3 g((unsigned)idx->nchunks, (unsigned)Q);
+    ProfScope ps(K_COUNT, st);
     k_count<<<g, CNT_THREADS, smem, st>>>(t.pops.as<uint16_t>(), t.npop.as<int32_t>(), idx->K,
                                           idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
                                           idx->n_sub, idx->K, idx->n, idx->nchunks,
                                           t.scores.as<uint8_t>(), t.part.as<int32_t>());
     TACO_LAUNCHED();
   }
-  k_hist_reduce<<<Q, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub,
-                                  t.hist.as<int64_t>());
-  TACO_LAUNCHED();
+  {
+    ProfScope ps(K_HIST, st);
+    k_hist_reduce<<<Q, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub,
+                                    t.hist.as<int64_t>());
+    TACO_LAUNCHED();
+  }
   return TACO_OK;
 }
 
@@ -834,17 +894,33 @@ static int run_finish_stage(taco_index* idx, int Q, const int64_t* ghist, double
                             cudaStream_t st) {
   QueryTile& t = idx->qt;
   const double budget = beta * (double)idx->n_global;   // engine.py:240
-  k_select<<<1, 1024, 0, st>>>(ghist, t.part.as<int32_t>(), Q, idx->nchunks, idx->n_sub, budget,
-                               t.lvl.as<int32_t>(), t.cnum.as<int64_t>(), t.coff.as<int64_t>(),
-                               t.qbase.as<int64_t>(), t.total.as<int64_t>());
-  TACO_LAUNCHED();
+  {
+    ProfScope ps_sel(K_SELECT, st);
+    k_select<<<1, 1024, 0, st>>>(ghist, t.part.as<int32_t>(), Q, idx->nchunks, idx->n_sub, budget,
+                                 t.lvl.as<int32_t>(), t.cnum.as<int64_t>(), t.coff.as<int64_t>(),
+                                 t.qbase.as<int64_t>(), t.total.as<int64_t>());
+    TACO_LAUNCHED();
+  }
   int64_t total = 0;
   TACO_CHECK_CUDA(cudaMemcpyAsync(&total, t.total.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (g_prof.on) {
+    std::vector<int64_t> r((size_t)Q * idx->n_sub);
+    std::vector<int32_t> np((size_t)Q * idx->n_sub);
+    cudaMemcpy(r.data(), t.ret.p, 8 * r.size(), cudaMemcpyDeviceToHost);
+    cudaMemcpy(np.data(), t.npop.p, 4 * np.size(), cudaMemcpyDeviceToHost);
+    for (auto v : r) g_prof.sumR += v;
+    for (auto v : np) g_prof.sumPops += v;
+    g_prof.sumC += total;
+    g_prof.queries += Q;
+    g_prof.tiles += 1;
+    g_prof.bytes_scores += (int64_t)Q * idx->nchunks * kChunk;
+  }
   TACO_TRY(t.cand.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1)));
   TACO_TRY(t.d2.ensure(sizeof(double) * (size_t)std::max<int64_t>(total, 1)));
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)Q);
+    ProfScope ps(K_COMPACT, st);
     k_compact<<<g, CMP_THREADS, 0, st>>>(t.scores.as<uint8_t>(), idx->n, idx->nchunks,
                                          t.lvl.as<int32_t>(), t.coff.as<int64_t>(),
                                          t.qbase.as<int64_t>(), t.cand.as<uint32_t>());
@@ -852,6 +928,7 @@ static int run_finish_stage(taco_index* idx, int Q, const int64_t* ghist, double
   }
   if (total > 0) {
     const unsigned g = (unsigned)ceil_div(total, RR_WARPS * 32);
+    ProfScope ps(K_RERANK, st);
     if (idx->d % 4 == 0)
       k_rerank<true><<<g, RR_WARPS * 32, 0, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), Q,
                                                   t.qbase.as<int64_t>(), t.cand.as<uint32_t>(),
@@ -863,6 +940,7 @@ static int run_finish_stage(taco_index* idx, int Q, const int64_t* ghist, double
     TACO_LAUNCHED();
   }
   if (k > 0) {
+    ProfScope ps(K_TOPK, st);
     k_topk<<<Q, TK_THREADS, 0, st>>>(t.d2.as<double>(), t.cand.as<uint32_t>(), t.qbase.as<int64_t>(),
                                      k, idx->id_base, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>());
     TACO_LAUNCHED();
@@ -890,6 +968,7 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
     TACO_TRY(run_count_stage(idx, Q, alpha, st, nullptr));
     TACO_TRY(run_finish_stage(idx, Q, t.hist.as<int64_t>(), beta, k, st));
     const int64_t tot = (int64_t)Q * k;
+    ProfScope ps(K_FINAL, st);
     k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(),
                                                              tot, t.out_ids.as<int32_t>(), t.out_d.as<float>());
     TACO_LAUNCHED();
@@ -1236,5 +1315,30 @@ int taco_traverse(int device, int32_t kp, const double* d1s_h, const int32_t* l1
   sd.release(); sl.release(); gs.release(); pops.release(); keys.release(); np.release(); ret.release();
   return rc;
 }
+
+int taco_profile_enable(int on) {
+  taco::prof_drain();
+  taco::g_prof.on = on != 0;
+  return TACO_OK;
+}
+
+// ms_out/cnt_out[K_NKIDS]; names via taco_profile_name; stats_out[6] =
+// {sum retrieved ids, sum candidates, sum pops, queries, tiles, score-table bytes}
+int taco_profile_read(double* ms_out, int64_t* cnt_out, int64_t* stats_out, int reset) {
+  taco::prof_drain();
+  for (int i = 0; i < taco::K_NKIDS; ++i) { ms_out[i] = taco::g_prof.ms[i]; cnt_out[i] = taco::g_prof.cnt[i]; }
+  stats_out[0] = taco::g_prof.sumR; stats_out[1] = taco::g_prof.sumC; stats_out[2] = taco::g_prof.sumPops;
+  stats_out[3] = taco::g_prof.queries; stats_out[4] = taco::g_prof.tiles; stats_out[5] = taco::g_prof.bytes_scores;
+  if (reset) {
+    for (int i = 0; i < taco::K_NKIDS; ++i) { taco::g_prof.ms[i] = 0; taco::g_prof.cnt[i] = 0; }
+    taco::g_prof.sumR = taco::g_prof.sumC = taco::g_prof.sumPops = 0;
+    taco::g_prof.queries = taco::g_prof.tiles = taco::g_prof.bytes_scores = 0;
+  }
+  return TACO_OK;
+}
+
+const char* taco_profile_name(int i) { return (i >= 0 && i < taco::K_NKIDS) ? taco::kKNames[i] : ""; }
+int taco_profile_kernels(void) { return taco::K_NKIDS; }
+void* taco_index_stream(taco_index* idx) { return idx ? (void*)idx->stream : nullptr; }
 
 }  // extern "C"

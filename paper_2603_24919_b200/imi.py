@@ -108,14 +108,14 @@ def run_kmeans_all(dev, n, n_sub, s, kprime, iters, seed_of):
         seeds.append(sd)
         firsts[hh], unis[hh] = draw_plan(n, kprime, sd)
     deg = np.zeros(H, np.int32)
-    nat.call("taco_kmeans_all", dev.h, nat.ptr(firsts), nat.ptr(np.ascontiguousarray(unis)), None,
-             nat.ptr(deg))
+    unis = np.ascontiguousarray(unis)
+    nat.call("taco_kmeans_all", dev.h, nat.ptr(firsts), nat.ptr(unis), None, nat.ptr(deg))
     if (deg < kprime).any():
         forced = np.full((H, max(kprime - 1, 0)), -1, np.int64)
         for hh in np.flatnonzero(deg < kprime):
             forced[hh] = forced_plan(n, kprime, seeds[hh], int(deg[hh]))
-        nat.call("taco_kmeans_all", dev.h, nat.ptr(firsts), nat.ptr(np.ascontiguousarray(unis)),
-                 nat.ptr(forced), nat.ptr(deg))
+        nat.call("taco_kmeans_all", dev.h, nat.ptr(firsts), nat.ptr(unis), nat.ptr(forced),
+                 nat.ptr(deg))
     m1 = (s + 1) // 2
     m2 = s - m1
     cb1 = np.empty((n_sub, kprime, m1), np.float32)
@@ -199,9 +199,11 @@ def scalable_dynamic_activation(alpha, n, n_cells, dists1, idx1, dists2, idx2,
     keys = np.empty(kp * kp)
     npop = np.zeros(1, np.int32)
     got = np.zeros(1, np.int64)
-    nat.call("taco_traverse", nat.device_id(), kp, nat.ptr(d1s), nat.ptr(i1.astype(np.int32)),
-             nat.ptr(d2s), nat.ptr(i2.astype(np.int32)), nat.ptr(sizes), target, nat.ptr(pops),
-             nat.ptr(keys), nat.ptr(npop), nat.ptr(got))
+    l1s = np.ascontiguousarray(i1, dtype=np.int32)   # keep the buffers alive across the call
+    l2s = np.ascontiguousarray(i2, dtype=np.int32)
+    nat.call("taco_traverse", nat.device_id(), kp, nat.ptr(d1s), nat.ptr(l1s), nat.ptr(d2s),
+             nat.ptr(l2s), nat.ptr(sizes), target, nat.ptr(pops), nat.ptr(keys), nat.ptr(npop),
+             nat.ptr(got))
     cells = imi.cells
     retrieved, trace = [], []
     for p, key in zip(pops[: npop[0]], keys[: npop[0]]):
