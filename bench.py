@@ -132,11 +132,14 @@ def path_bytes(stats, meta, nq_total):
 def kernel_bytes(name, stats, meta):
     d = meta["d"]
     C, R, P = stats["sum_candidates"], stats["sum_retrieved"], stats["sum_pops"]
+    nch = stats.get("nchunks", 1)
     return {
-        "k_rerank": (4 * d + 4 + 8) * C,
-        "k_count": 4 * R + stats["score_bytes"] + 10 * P * max(1, meta["n"] // 65536),
+        # candidate rows gathered + candidate ids read + per-CTA partial top-k
+        "k_rerank_topk": (4 * d + 4) * C,
+        # ids of popped cells + CSR bounds per (cell, chunk) + pop lists + candidate ids
+        # written (+ score tables through HBM in global mode)
+        "k_count": 4 * R + (8 * nch + 2) * P + 4 * C + 2 * stats["score_bytes"],
         "k_compact": stats["score_bytes"] + 4 * C,
-        "k_topk": 12 * C,
     }.get(name)
 
 
@@ -281,6 +284,7 @@ def run_ours(args):
     device_step()
     torch.cuda.synchronize()
     prof, stats = nat.profile_read(reset=True)
+    stats["nchunks"] = -(-meta["n"] // (-(-meta["n"] // 8) if meta["n"] <= 1572864 else 65536))
     nat.profile_enable(False)
     total_prof = sum(v[0] for v in prof.values())
     dom = max(prof, key=lambda kname: prof[kname][0])

@@ -683,16 +683,16 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
 
 // ================================================================== cells
 __global__ void k_cell_hist(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2, int64_t n,
-                            int kp, uint32_t* __restrict__ chist) {
+                            int kp, int64_t chunk, uint32_t* __restrict__ chist) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int key = l1[i] * kp + l2[i];
-  atomicAdd(&chist[(size_t)(i >> kChunkShift) * kp * kp + key], 1u);
+  atomicAdd(&chist[(size_t)(i / chunk) * kp * kp + key], 1u);
 }
 
 // per chunk: offs[c*K2 + cell] = c*CH + exclusive prefix within the chunk
 __global__ void k_cell_offsets(const uint32_t* __restrict__ chist, int K2, int64_t nchunks, int64_t n,
-                               uint32_t* __restrict__ offs) {
+                               int64_t chunk, uint32_t* __restrict__ offs) {
   __shared__ uint32_t wsum[32];
   const int64_t c = blockIdx.x;
   const uint32_t* hc = chist + (size_t)c * K2;
@@ -717,7 +717,7 @@ __global__ void k_cell_offsets(const uint32_t* __restrict__ chist, int K2, int64
     wsum[lane] = w;
   }
   __syncthreads();
-  uint32_t run = (uint32_t)(c << kChunkShift) + (wid ? wsum[wid - 1] : 0u) + v - loc;
+  uint32_t run = (uint32_t)(c * chunk) + (wid ? wsum[wid - 1] : 0u) + v - loc;
   for (int e = a0; e < a1; ++e) {
     offs[(size_t)c * K2 + e] = run;
     run += hc[e];
@@ -736,14 +736,14 @@ __global__ void k_cell_sizes(const uint32_t* __restrict__ chist, int K2, int64_t
 
 // one warp per chunk: stable scatter of ascending ids into their cells
 __global__ void k_cell_scatter(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2,
-                               int64_t n, int kp, uint32_t* __restrict__ cursor,
+                               int64_t n, int kp, int64_t chunk, uint32_t* __restrict__ cursor,
                                uint32_t* __restrict__ ids) {
   const int lane = threadIdx.x;
   const int64_t c = blockIdx.x;
   const int K2 = kp * kp;
   uint32_t* cur = cursor + (size_t)c * K2;
-  const int64_t i0 = c << kChunkShift;
-  const int64_t i1 = min(n, i0 + kChunk);
+  const int64_t i0 = c * chunk;
+  const int64_t i1 = min(n, i0 + chunk);
   for (int64_t r = i0; r < i1; r += 32) {
     const int64_t i = r + lane;
     const bool live = i < i1;
@@ -900,9 +900,9 @@ int taco_build_cells(taco_index* idx) {
     const int32_t* l2 = idx->labels.as<int32_t>() + (size_t)(2 * j + 1) * n;
     uint32_t* offs = idx->offs.as<uint32_t>() + (size_t)j * offs_len;
     TACO_CHECK_CUDA(cudaMemsetAsync(chist.p, 0, sizeof(uint32_t) * (size_t)nc * K2, st));
-    k_cell_hist<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(l1, l2, n, kp, chist.as<uint32_t>());
+    k_cell_hist<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(l1, l2, n, kp, idx->chunk, chist.as<uint32_t>());
     TACO_LAUNCHED();
-    k_cell_offsets<<<(unsigned)nc, 1024, 0, st>>>(chist.as<uint32_t>(), K2, nc, n, offs);
+    k_cell_offsets<<<(unsigned)nc, 1024, 0, st>>>(chist.as<uint32_t>(), K2, nc, n, idx->chunk, offs);
     TACO_LAUNCHED();
     if (idx->n_global == idx->n) {
       k_cell_sizes<<<(unsigned)ceil_div(K2, 256), 256, 0, st>>>(chist.as<uint32_t>(), K2, nc,
@@ -910,7 +910,7 @@ int taco_build_cells(taco_index* idx) {
       TACO_LAUNCHED();
     }
     TACO_CHECK_CUDA(cudaMemcpyAsync(cursor.p, offs, sizeof(uint32_t) * (size_t)nc * K2, cudaMemcpyDeviceToDevice, st));
-    k_cell_scatter<<<(unsigned)nc, 32, 0, st>>>(l1, l2, n, kp, cursor.as<uint32_t>(),
+    k_cell_scatter<<<(unsigned)nc, 32, 0, st>>>(l1, l2, n, kp, idx->chunk, cursor.as<uint32_t>(),
                                                 idx->ids.as<uint32_t>() + (size_t)j * n);
     TACO_LAUNCHED();
   }

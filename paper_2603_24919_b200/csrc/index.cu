@@ -1,4 +1,5 @@
 // Index lifecycle, host<->device import/export, the fp64 transform GEMM.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <vector>
@@ -167,7 +168,15 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
   idx->m2 = subspace_dim - idx->m1;
   idx->D = n_subspaces * subspace_dim;
   idx->iters = kmeans_iters;
-  idx->nchunks = ceil_div(n, kChunk);
+  if (n_global == n && n <= kClusterMaxN) {
+    const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, 131072)));
+    idx->chunk = ceil_div(ceil_div(n, ctas), 1024) * 1024;
+    idx->cluster_mode = true;
+  } else {
+    idx->chunk = kGlobalChunk;
+    idx->cluster_mode = false;
+  }
+  idx->nchunks = ceil_div(n, idx->chunk);
   cudaError_t e = cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete idx;
@@ -185,9 +194,9 @@ int taco_index_destroy(taco_index* idx) {
                     &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
   for (auto* b : bufs) b->release();
   QueryTile& q = idx->qt;
-  DevBuf* qb[] = {&q.Q, &q.qt, &q.sd, &q.sl, &q.pops, &q.npop, &q.ret, &q.scores, &q.part,
-                  &q.hist, &q.lvl, &q.cnum, &q.clocal, &q.coff, &q.qbase, &q.total, &q.cand,
-                  &q.d2, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d, &q.out_num, &q.out_lvl};
+  DevBuf* qb[] = {&q.Q, &q.qt, &q.sd, &q.sl, &q.pops, &q.npop, &q.ret, &q.flags, &q.scores, &q.part,
+                  &q.hist, &q.lvl, &q.cnum, &q.clocal, &q.coff, &q.qbase, &q.cursor, &q.cand,
+                  &q.bpref, &q.pd2, &q.ppos, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d};
   for (auto* b : qb) b->release();
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
@@ -357,7 +366,7 @@ int taco_index_set_cells(taco_index* idx, const int64_t* offsets_h, const uint32
       gs[c] = O[c + 1] - O[c];
       for (int64_t p = O[c]; p < O[c + 1]; ++p) {
         if (I[p] >= (uint64_t)n) TACO_FAIL(TACO_ERR_FORMAT, "cell id %u out of range", I[p]);
-        cnt[(size_t)(I[p] >> kChunkShift) * K2 + c]++;
+        cnt[(size_t)(I[p] / idx->chunk) * K2 + c]++;
       }
     }
     int64_t run = 0;
@@ -369,7 +378,7 @@ int taco_index_set_cells(taco_index* idx, const int64_t* offsets_h, const uint32
     std::vector<uint32_t> cur(offs.begin(), offs.end() - 1);
     for (int c = 0; c < K2; ++c)
       for (int64_t p = O[c]; p < O[c + 1]; ++p) {
-        size_t slot = (size_t)(I[p] >> kChunkShift) * K2 + c;
+        size_t slot = (size_t)(I[p] / idx->chunk) * K2 + c;
         ids[cur[slot]++] = I[p];
       }
     TACO_CHECK_CUDA(cudaMemcpy(idx->ids.as<uint32_t>() + (size_t)j * n, ids.data(),

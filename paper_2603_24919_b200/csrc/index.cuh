@@ -18,8 +18,14 @@
 
 namespace taco {
 
-constexpr int kChunkShift = 16;                 // CH = 65536 ids per score table
-constexpr int64_t kChunk = int64_t(1) << kChunkShift;
+// Score-table chunk: the id range one CTA counts in shared memory.
+//  cluster mode (single GPU, n <= kClusterMaxN): n is split over <= 8 CTAs of
+//    one thread-block cluster, chunk = ceil(n / ctas) rounded to 1 KiB;
+//  global mode (larger shards / multi-GPU): chunk = 64 KiB, tables in HBM.
+constexpr int64_t kGlobalChunk = 65536;
+constexpr int64_t kClusterMaxChunk = 196608;
+constexpr int kClusterMaxCtas = 8;
+constexpr int64_t kClusterMaxN = kClusterMaxChunk * kClusterMaxCtas;
 
 struct DevBuf {
   void* p = nullptr;
@@ -31,8 +37,10 @@ struct DevBuf {
 };
 
 struct QueryTile {
-  DevBuf Q, qt, sd, sl, pops, npop, ret, scores, part, hist, lvl, cnum, clocal, coff, qbase, total,
-      cand, d2, tk_d2, tk_ids, out_ids, out_d, out_num, out_lvl;
+  DevBuf Q, qt, sd, sl, pops, npop, ret, flags, scores, part, hist, lvl, cnum, clocal, coff, qbase,
+      cursor, cand, bpref, pd2, ppos, tk_d2, tk_ids, out_ids, out_d;
+  int64_t cand_cap = 0;
+  int pop_cap = 0;
 };
 
 struct BuildScratch {
@@ -45,7 +53,8 @@ struct BuildScratch {
 struct taco_index {
   int device = 0;
   cudaStream_t stream = nullptr;
-  int64_t n = 0, n_global = 0, id_base = 0, nchunks = 0;
+  int64_t n = 0, n_global = 0, id_base = 0, nchunks = 0, chunk = 0;
+  bool cluster_mode = false;
   int d = 0, n_sub = 0, s = 0, K = 0, kp = 0, m1 = 0, m2 = 0, D = 0, iters = 0;
   taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
   bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,

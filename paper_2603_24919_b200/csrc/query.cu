@@ -1,31 +1,45 @@
 // Batched TaCo query path on sm_100a.
 //
-//  per tile of Qt queries, all on one stream:
-//   k_transform      qt = f32((q - mu) @ M)                spectral.py:301-316
-//   k_csort          fp64 centroid distances + stable rank  imi.py:88-106
-//   k_traverse       multi-sequence heap traversal          imi.py:130-166
-//   k_count          uint8 collision counts, one 64 KiB id chunk per CTA in
-//                    shared memory, + per-chunk level histograms   engine.py:201-219
-//   k_hist_reduce    per-query histograms (all-reduced across shards here)
-//   k_select         Alg. 5 threshold + candidate offsets   engine.py:239-251
-//   k_compact        ordered candidate ids (score >= L)     engine.py:250
-//   k_rerank         fp64 exact distances, rows staged through smem   engine.py:272-274
-//   k_topk           radix select + bitonic sort on (d2, id)          engine.py:275-279
+// Whole-batch stages (super-tiles of up to kSuperTile queries), one stream:
+//   k_transform       qt = f32((q - mu) @ M)                     spectral.py:301-316
+//   k_csort           fp64 centroid distances + stable rank       imi.py:88-106
+//   k_traverse        multi-sequence heap traversal, one thread per (query,
+//                     subspace)                                   imi.py:130-166
+//   cluster mode (single GPU, n <= 1.5M):
+//   k_count_cluster   one thread-block CLUSTER per query, each CTA counts one id
+//                     chunk in shared memory; level histograms are exchanged
+//                     through DSMEM, Alg. 5 runs in-cluster and every CTA
+//                     compacts its candidates straight from smem   engine.py:201-251
+//   global mode (large shards / multi-GPU, query tiles):
+//   k_count           per (query, 64 Ki chunk) smem counting -> HBM tables +
+//                     per-chunk histograms;  k_hist_reduce -> (all-reduce across
+//                     ranks) -> k_select (Alg. 5) -> k_compact
+//   k_rr_plan         candidate blocks per query
+//   k_rerank_topk     fp64 exact distances of 256 candidates per CTA (rows
+//                     staged through smem) + CTA-local top-k       engine.py:272-275
+//   k_topk            final per-query top-k over the CTA partials (radix select
+//                     + bitonic sort on (d2, position == id order)) engine.py:275-279
+//   k_finalize        ids int32 / dists f32(sqrt(d2))              engine.py:276-279
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
 
 #include "index.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace taco {
 
 // ------------------------------------------------------------- profiler
 // Optional per-kernel timing with CUDA events recorded on the launching
 // stream (bench.py's roofline), plus algorithmic-work counters.
-enum KId { K_TRANSFORM, K_CSORT, K_TRAVERSE, K_COUNT, K_HIST, K_SELECT, K_COMPACT, K_RERANK, K_TOPK,
-           K_FINAL, K_NKIDS };
+enum KId { K_TRANSFORM, K_CSORT, K_TRAVERSE, K_COUNT, K_HIST, K_SELECT, K_COMPACT, K_PLAN, K_RERANK,
+           K_TOPK, K_FINAL, K_NKIDS };
 static const char* kKNames[K_NKIDS] = {"k_transform", "k_csort", "k_traverse", "k_count", "k_hist_reduce",
-                                       "k_select", "k_compact", "k_rerank", "k_topk", "k_finalize"};
+                                       "k_select", "k_compact", "k_rr_plan", "k_rerank_topk", "k_topk",
+                                       "k_finalize"};
 struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> pool;
@@ -111,18 +125,20 @@ __global__ void k_csort(const float* __restrict__ qt, int Q, int n_sub, int s, i
 // One thread per (query, subspace).  Min-heap of (key, row rank, col rank)
 // with the frontier rule of imi.py:155-165; each row holds at most one heap
 // entry, so KMAX >= K' suffices.  Cell sizes are the GLOBAL sizes so every
-// shard derives the same popped set.
+// shard derives the same popped set.  At most `cap` cells are
+// stored; a longer traversal raises flags[0] and the host re-runs with cap=K'^2.
 template <int KMAX>
 __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
                                                   const uint16_t* __restrict__ sl,
-                                                  const int64_t* __restrict__ gsize, int Q,
+                                                  const int64_t* __restrict__ gsize, int64_t Q,
                                                   int n_sub, int kp, int64_t target,
                                                   uint16_t* __restrict__ pops, int cap,
                                                   double* __restrict__ keys_out,
                                                   int32_t* __restrict__ npop,
-                                                  int64_t* __restrict__ ret) {
+                                                  int64_t* __restrict__ ret,
+                                                  int64_t* __restrict__ flags) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)Q * n_sub) return;
+  if (t >= Q * n_sub) return;
   const int j = (int)(t % n_sub);
   const double* d1 = sd + t * 2 * kp;
   const double* d2 = d1 + kp;
@@ -155,7 +171,6 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
   while (hn > 0) {
     const double key = hk[0];
     const uint32_t pc = hp[0];
-    // pop: move last to root and sift down
     --hn;
     if (hn > 0) {
       const double lk = hk[hn];
@@ -176,8 +191,10 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
     }
     const int r = (int)(pc >> 16), c = (int)(pc & 0xFFFF);
     const int cell = (int)l1[r] * kp + (int)l2[c];
-    out[np] = (uint16_t)cell;
-    if (kout) kout[np] = key;
+    if (np < cap) {
+      out[np] = (uint16_t)cell;
+      if (kout) kout[np] = key;
+    }
     ++np;
     got += gs[cell];
     if (got >= target) break;
@@ -186,11 +203,39 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
   }
   npop[t] = np;
   ret[t] = got;
+  if (np > cap) atomicMax((unsigned long long*)&flags[0], (unsigned long long)np);
+}
+
+// ---------------------------------------------------------- block helpers
+// Exclusive scan of one value per thread (uint32), returns the block total.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < NT / 32 ? wtot[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) wtot[lane] = w;
+  }
+  __syncthreads();
+  total = wtot[NT / 32 - 1];
+  const uint32_t excl = (wid ? wtot[wid - 1] : 0u) + x - v;
+  __syncthreads();
+  return excl;
 }
 
 // ---------------------------------------------------------- level counting
-// Histogram of levels 1..n_sub over `nbytes` score bytes (4-byte words),
-// per-thread partial counts accumulated into cnt[] (shared, n_sub+1 ints).
 __device__ __forceinline__ void count_levels_words(const uint32_t* words, int nwords, int n_sub,
                                                    int* cnt_sh) {
   if (n_sub <= 15) {
@@ -218,149 +263,282 @@ __device__ __forceinline__ void count_levels_words(const uint32_t* words, int nw
     for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
       uint32_t w = words[i];
       while (w) {
-        int b = __ffs(w) - 1;
-        int byte = b >> 3;
-        int v = (int)((w >> (byte * 8)) & 0xFF);
-        atomicAdd(&cnt_sh[v], 1);
+        const int b = __ffs(w) - 1;
+        const int byte = b >> 3;
+        atomicAdd(&cnt_sh[(w >> (byte * 8)) & 0xFF], 1);
         w &= ~(0xFFu << (byte * 8));
       }
     }
   }
 }
 
-// ------------------------------------------------------------------ count
-constexpr int CNT_THREADS = 512;
-constexpr int CNT_PB = 1024;   // popped cells staged per batch
-constexpr int CNT_E = 8;       // ids gathered per thread before the byte RMWs
+// ------------------------------------------------------------ chunk counting
+// Counts into `table` (ids [base, base+chunk)) every id of the cells popped for
+// query q in subspaces 0..n_sub-1.  Slices of all subspaces are staged PB at a
+// time (phase A: one round trip for their CSR bounds); ids are then gathered
+// E per thread with independent loads (phase B) and applied subspace by
+// subspace with a barrier in between: ids are unique inside one subspace, so
+// the byte increments need no atomics.
+constexpr int CT_THREADS = 512;
+constexpr int CT_PB = 2 * CT_THREADS;
+constexpr int CT_E = 16;
 
-__global__ void __launch_bounds__(CNT_THREADS) k_count(
-    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
-    const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2,
-    int64_t n, int64_t nchunks, uint8_t* __restrict__ scores, int32_t* __restrict__ part) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* table = smem;
-  uint32_t* st = reinterpret_cast<uint32_t*>(smem + kChunk);
-  uint32_t* pref = st + CNT_PB;
-  __shared__ int wtot[CNT_THREADS / 32];
-  __shared__ int cnt_sh[256];
-  const int c = blockIdx.x;
-  const int64_t q = blockIdx.y;
-  const int tid = threadIdx.x;
-  const int64_t base = (int64_t)c << kChunkShift;
-  const int valid = (int)min((int64_t)kChunk, n - base);
-  uint4* t4 = reinterpret_cast<uint4*>(table);
-  for (int i = tid; i < (int)(kChunk / 16); i += CNT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 256; i += CNT_THREADS) cnt_sh[i] = 0;
-  __syncthreads();
-  const size_t offs_len = (size_t)nchunks * K2 + 1;
-  for (int j = 0; j < n_sub; ++j) {
-    const uint16_t* P = pops + ((size_t)q * n_sub + j) * cap;
-    const int np = npop[q * n_sub + j];
-    const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
-    const uint32_t* I = ids + (size_t)j * n;
-    for (int b0 = 0; b0 < np; b0 += CNT_PB) {
-      const int nb = min(CNT_PB, np - b0);
-      // phase A: slice [O[cell], O[cell+1]) of every popped cell in this chunk
-      for (int t = tid; t < CNT_PB; t += CNT_THREADS) {
-        uint32_t len = 0;
-        if (t < nb) {
-          const int cell = P[b0 + t];
-          const uint32_t s0 = O[cell], s1 = O[cell + 1];
-          st[t] = s0;
-          len = s1 - s0;
-        }
-        pref[t + 1] = len;
-      }
-      __syncthreads();
-      // inclusive scan of pref[1..CNT_PB]: 2 elements per thread
-      {
-        uint32_t a = pref[2 * tid + 1], b = pref[2 * tid + 2];
-        uint32_t sum = a + b;
-        uint32_t v = sum;
-        const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          uint32_t x = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += x;
-        }
-        if (lane == 31) wtot[wid] = (int)v;
-        __syncthreads();
-        if (wid == 0) {
-          uint32_t wv = lane < CNT_THREADS / 32 ? (uint32_t)wtot[lane] : 0u;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            uint32_t x = __shfl_up_sync(0xffffffffu, wv, o);
-            if (lane >= o) wv += x;
-          }
-          if (lane < CNT_THREADS / 32) wtot[lane] = (int)wv;
-        }
-        __syncthreads();
-        const uint32_t off = (wid ? (uint32_t)wtot[wid - 1] : 0u) + v - sum;
-        pref[2 * tid + 1] = off + a;
-        pref[2 * tid + 2] = off + a + b;
-        if (tid == 0) pref[0] = 0;
-      }
-      __syncthreads();
-      const uint32_t total = pref[nb];
-      // phase B: each thread owns a contiguous range of the flattened ids
-      const uint32_t per = (total + CNT_THREADS - 1) / CNT_THREADS;
-      uint32_t f = per * tid;
-      const uint32_t f1 = min(total, f + per);
-      if (f < f1) {
-        int lo = 0, hi = nb;  // largest t with pref[t] <= f
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if (pref[mid] <= f) lo = mid; else hi = mid;
-        }
-        int t = lo;
-        while (f < f1) {
-          uint32_t idv[CNT_E];
-          int cntv = 0;
-#pragma unroll
-          for (int e = 0; e < CNT_E; ++e) {
-            if (f < f1) {
-              while (f >= pref[t + 1]) ++t;
-              idv[e] = __ldg(I + st[t] + (f - pref[t]));
-              ++f;
-              ++cntv;
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < CNT_E; ++e)
-            if (e < cntv) table[idv[e] - (uint32_t)base] += 1;
-        }
-      }
-      __syncthreads();
-    }
+struct CountSmem {
+  uint32_t st[CT_PB];
+  uint32_t pref[CT_PB + 1];
+  uint8_t sj[CT_PB];
+  uint32_t wtot[CT_THREADS / 32];
+  int jpref[257];
+  int lh[256];
+};
+
+__device__ __forceinline__ int slice_of(const uint32_t* pref, int nb, uint32_t f) {
+  int lo = 0, hi = nb;  // largest t with pref[t] <= f
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= f) lo = mid; else hi = mid;
   }
-  // store the chunk's table and its level histogram
-  uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * kChunk);
-  for (int i = tid; i < (int)(kChunk / 16); i += CNT_THREADS) dst[i] = t4[i];
-  count_levels_words(reinterpret_cast<const uint32_t*>(table), (valid + 3) / 4, n_sub, cnt_sh);
+  return lo;
+}
+
+__device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+                            const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs,
+                            size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
+                            int64_t base, uint8_t* table, CountSmem& S) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int acc = 0;
+    for (int j = 0; j < n_sub; ++j) {
+      S.jpref[j] = acc;
+      acc += min(npop[q * n_sub + j], cap);
+    }
+    S.jpref[n_sub] = acc;
+  }
   __syncthreads();
-  int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
+  const int P_all = S.jpref[n_sub];
+  for (int b0 = 0; b0 < P_all; b0 += CT_PB) {
+    const int nb = min(CT_PB, P_all - b0);
+    uint32_t len2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = 2 * tid + u;
+      uint32_t len = 0;
+      if (t < nb) {
+        const int g = b0 + t;
+        int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.jpref[mid] <= g) lo = mid; else hi = mid;
+        }
+        const int j = lo;
+        const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
+        const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
+        const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
+        S.st[t] = s0;
+        S.sj[t] = (uint8_t)j;
+        len = s1 - s0;
+      }
+      len2[u] = len;
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<CT_THREADS>(len2[0] + len2[1], S.wtot, tot);
+    S.pref[2 * tid] = ex;
+    S.pref[2 * tid + 1] = ex + len2[0];
+    if (tid == CT_THREADS - 1) S.pref[CT_PB] = tot;
+    __syncthreads();
+    const uint32_t total = S.pref[nb];
+    for (uint32_t r0 = 0; r0 < total; r0 += CT_THREADS * CT_E) {
+      const uint32_t r1 = min(total, r0 + (uint32_t)(CT_THREADS * CT_E));
+      const uint32_t per = (r1 - r0 + CT_THREADS - 1) / CT_THREADS;
+      uint32_t f = r0 + per * tid;
+      const uint32_t fe = min(r1, f + per);
+      uint32_t idv[CT_E];
+      uint32_t jv[CT_E];
+      int cntv = 0;
+      if (f < fe) {
+        int t = slice_of(S.pref, nb, f);
+#pragma unroll
+        for (int e = 0; e < CT_E; ++e) {
+          if (f < fe) {
+            while (f >= S.pref[t + 1]) ++t;
+            const int j = S.sj[t];
+            idv[e] = __ldg(ids + (size_t)j * n + S.st[t] + (f - S.pref[t]));
+            jv[e] = (uint32_t)j;
+            ++f;
+            cntv = e + 1;
+          }
+        }
+      }
+      const int jlo = S.sj[slice_of(S.pref, nb, r0)];
+      const int jhi = S.sj[slice_of(S.pref, nb, r1 - 1)];
+      for (int j = jlo; j <= jhi; ++j) {
+#pragma unroll
+        for (int e = 0; e < CT_E; ++e)
+          if (e < cntv && jv[e] == (uint32_t)j) table[idv[e] - (uint32_t)base] += 1;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Ordered compaction of ids (id0 + position) whose score >= L from a table of
+// `valid` bytes (16-byte aligned, zero padded to a multiple of 16).
+template <int NT>
+__device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
+                              uint32_t* wtot) {
+  const uint32_t Lrep = 0x01010101u * L;
+  const uint4* t4 = reinterpret_cast<const uint4*>(tab);
+  uint32_t run = 0;
+  for (int r0 = 0; r0 < valid; r0 += NT * 16) {
+    const int p0 = r0 + threadIdx.x * 16;
+    uint32_t mask = 0;
+    if (p0 < valid) {
+      const uint4 v = t4[p0 >> 4];
+      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t ge = __vcmpgeu4(ws[u], Lrep);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if ((ge >> (8 * b)) & 1u) mask |= 1u << (u * 4 + b);
+      }
+      const int lim = valid - p0;
+      if (lim < 16) mask &= (1u << lim) - 1u;
+    }
+    uint32_t tot;
+    uint32_t pos = run + block_excl_scan<NT>((uint32_t)__popc(mask), wtot, tot);
+    while (mask) {
+      const int b = __ffs(mask) - 1;
+      dst[pos++] = (uint32_t)(id0 + p0 + b);
+      mask &= mask - 1u;
+    }
+    run += tot;
+  }
+}
+
+// Alg. 5 (engine.py:239-249) on a histogram fetched through `get(level)`.
+template <typename Get>
+__device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& cand) {
+  int L = n_sub;
+  cand = 0;
+  for (int j = n_sub; j >= 0; --j) {
+    const int64_t h = get(j);
+    cand += h;
+    if ((double)h <= __dsub_rn(budget, (double)cand)) L -= 1; else break;
+  }
+  return L < 0 ? 0 : L;
+}
+
+// ------------------------------------------------- cluster-fused count/select
+__global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
+    int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ qbase, int64_t* __restrict__ clocal,
+    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ CountSmem S;
+  __shared__ int s_L;
+  __shared__ int64_t s_cand, s_off, s_base;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int csz = (int)cluster.num_blocks();
+  const int64_t q = blockIdx.y;
+  const int64_t c = rank;
+  const int tid = threadIdx.x;
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  uint4* t4 = reinterpret_cast<uint4*>(table);
+  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < 256; i += CT_THREADS) S.lh[i] = 0;
+  __syncthreads();
+  count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  count_levels_words(reinterpret_cast<const uint32_t*>(table), (valid + 3) / 4, n_sub, S.lh);
+  __syncthreads();
   if (tid == 0) {
     int nz = 0;
-    for (int l = 1; l <= n_sub; ++l) nz += cnt_sh[l];
+    for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
+    S.lh[0] = valid - nz;
+  }
+  cluster.sync();
+  if (tid == 0) {
+    int* rl[kClusterMaxCtas];
+    for (int r = 0; r < csz; ++r) rl[r] = cluster.map_shared_rank(S.lh, r);
+    int64_t cands = 0;
+    const int L = alg5([&](int l) {
+      int64_t h = 0;
+      for (int r = 0; r < csz; ++r) h += rl[r][l];
+      return h;
+    }, n_sub, budget, cands);
+    int64_t off = 0;
+    for (int r = 0; r < rank; ++r)
+      for (int l = L; l <= n_sub; ++l) off += rl[r][l];
+    s_L = L;
+    s_cand = cands;
+    s_off = off;
+    if (rank == 0) {
+      const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)cands);
+      s_base = b;
+      if (b + cands > cand_cap) flags[1] = 1;
+      qbase[q] = b;
+      clocal[q] = cands;
+      cnum[q] = cands;
+      lvl[q] = L;
+    }
+  }
+  cluster.sync();
+  if (tid == 0 && rank != 0) s_base = *cluster.map_shared_rank(&s_base, 0);
+  cluster.sync();
+  const int64_t b = s_base;
+  if (b + s_cand > cand_cap) return;
+  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + b + s_off, S.wtot);
+}
+
+// ------------------------------------------------------- global-mode count
+__global__ void __launch_bounds__(CT_THREADS) k_count(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
+    int64_t nchunks, int64_t chunk, int64_t q0, uint8_t* __restrict__ scores, int32_t* __restrict__ part) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ CountSmem S;
+  const int64_t c = blockIdx.x;
+  const int64_t qt = blockIdx.y;          // query within the tile
+  const int64_t q = q0 + qt;              // query within the super-tile
+  const int tid = threadIdx.x;
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  uint4* t4 = reinterpret_cast<uint4*>(table);
+  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < 256; i += CT_THREADS) S.lh[i] = 0;
+  __syncthreads();
+  count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)qt * nchunks + c) * chunk);
+  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
+  count_levels_words(reinterpret_cast<const uint32_t*>(table), (valid + 3) / 4, n_sub, S.lh);
+  __syncthreads();
+  int32_t* pp = part + ((size_t)qt * nchunks + c) * (n_sub + 1);
+  if (tid == 0) {
+    int nz = 0;
+    for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
     pp[0] = valid - nz;
   }
-  for (int l = 1 + tid; l <= n_sub; l += CNT_THREADS) pp[l] = cnt_sh[l];
+  for (int l = 1 + tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
 }
 
 // Level histograms of externally provided score chunks (select_candidates tap).
-__global__ void k_chunk_hist(const uint8_t* __restrict__ scores, int64_t n, int64_t nchunks,
+__global__ void k_chunk_hist(const uint8_t* __restrict__ scores, int64_t n, int64_t nchunks, int64_t chunk,
                              int n_sub, int32_t* __restrict__ part) {
   __shared__ int cnt_sh[256];
-  const int c = blockIdx.x;
-  const int64_t q = blockIdx.y;
+  const int64_t c = blockIdx.x;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt_sh[i] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)c << kChunkShift;
-  const int valid = (int)min((int64_t)kChunk, n - base);
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(scores + ((size_t)q * nchunks + c) * kChunk);
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(scores + (size_t)c * chunk);
   count_levels_words(w, (valid + 3) / 4, n_sub, cnt_sh);
   __syncthreads();
-  int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
+  int32_t* pp = part + (size_t)c * (n_sub + 1);
   if (threadIdx.x == 0) {
     int nz = 0;
     for (int l = 1; l <= n_sub; ++l) nz += cnt_sh[l];
@@ -379,43 +557,67 @@ __global__ void k_hist_reduce(const int32_t* __restrict__ part, int64_t nchunks,
   }
 }
 
-// ----------------------------------------------------------------- select
-// One thread per query: Alg. 5 on the (global) histogram exactly as
-// engine.py:239-249 evaluates it in Python doubles, then the local candidate
-// count per chunk and the block-wide query offsets.
-__global__ void __launch_bounds__(1024) k_select(const int64_t* __restrict__ ghist,
-                                                 const int32_t* __restrict__ part, int Q,
-                                                 int64_t nchunks, int n_sub, double budget,
-                                                 int32_t* __restrict__ lvl,
-                                                 int64_t* __restrict__ cnum_global,
-                                                 int64_t* __restrict__ coff,
-                                                 int64_t* __restrict__ qbase,
-                                                 int64_t* __restrict__ total) {
-  __shared__ int64_t wsum[32];
-  const int q = threadIdx.x;
+// Global mode: one thread per query of the tile.  Alg. 5 on the (global)
+// histogram, local candidate offsets per chunk, space reserved in the
+// super-tile candidate buffer through the cursor flags[3].
+__global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __restrict__ part, int Q,
+                         int64_t q0, int64_t nchunks, int n_sub, double budget,
+                         int64_t* __restrict__ coff, int64_t cand_cap, int64_t* __restrict__ flags,
+                         int64_t* __restrict__ qbase, int64_t* __restrict__ clocal,
+                         int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  const int qt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qt >= Q) return;
+  const int64_t* h = ghist + (size_t)qt * (n_sub + 1);
+  int64_t cands = 0;
+  const int L = alg5([&](int l) { return h[l]; }, n_sub, budget, cands);
   int64_t local = 0;
-  if (q < Q) {
-    const int64_t* h = ghist + (size_t)q * (n_sub + 1);
-    int L = n_sub;
-    int64_t cand = 0;
-    for (int j = n_sub; j >= 0; --j) {
-      cand += h[j];
-      if ((double)h[j] <= __dsub_rn(budget, (double)cand)) L -= 1; else break;
-    }
-    if (L < 0) L = 0;
-    lvl[q] = L;
-    cnum_global[q] = cand;
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
-      int64_t cc = 0;
-      for (int l = L; l <= n_sub; ++l) cc += pp[l];
-      coff[(size_t)q * nchunks + c] = local;
-      local += cc;
-    }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int32_t* pp = part + ((size_t)qt * nchunks + c) * (n_sub + 1);
+    int64_t cc = 0;
+    for (int l = L; l <= n_sub; ++l) cc += pp[l];
+    coff[(size_t)qt * nchunks + c] = local;
+    local += cc;
   }
-  // exclusive scan of `local` over the block
+  const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)local);
+  if (b + local > cand_cap) flags[1] = 1;
+  const int64_t q = q0 + qt;
+  qbase[q] = b;
+  clocal[q] = local;
+  cnum[q] = cands;
+  lvl[q] = L;
+}
+
+constexpr int CMP_THREADS = 256;
+__global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restrict__ scores, int64_t n,
+                                                          int64_t nchunks, int64_t chunk, int64_t q0,
+                                                          const int32_t* __restrict__ lvl,
+                                                          const int64_t* __restrict__ coff,
+                                                          const int64_t* __restrict__ qbase,
+                                                          const int64_t* __restrict__ clocal,
+                                                          int64_t cand_cap,
+                                                          uint32_t* __restrict__ cand) {
+  __shared__ uint32_t wtot[CMP_THREADS / 32];
+  const int64_t c = blockIdx.x;
+  const int64_t qt = blockIdx.y, q = q0 + qt;
+  const int64_t b = qbase[q];
+  if (b + clocal[q] > cand_cap) return;
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  compact_table<CMP_THREADS>(scores + ((size_t)qt * nchunks + c) * chunk, valid, (uint32_t)lvl[q], base,
+                             cand + b + coff[(size_t)qt * nchunks + c], wtot);
+}
+
+// ------------------------------------------------------------ rerank plan
+constexpr int RB = 256;   // candidates per rerank CTA
+__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ clocal, int64_t Q,
+                                                  int64_t* __restrict__ bpref, int64_t* __restrict__ flags) {
+  __shared__ int64_t wsum[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t v = local;
+  const int64_t per = (Q + 1023) / 1024;
+  const int64_t a0 = threadIdx.x * per, a1 = min(Q, a0 + per);
+  int64_t loc = 0;
+  for (int64_t q = a0; q < a1; ++q) loc += (clocal[q] + RB - 1) / RB;
+  int64_t v = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     int64_t x = __shfl_up_sync(0xffffffffu, v, o);
@@ -424,280 +626,261 @@ __global__ void __launch_bounds__(1024) k_select(const int64_t* __restrict__ ghi
   if (lane == 31) wsum[wid] = v;
   __syncthreads();
   if (wid == 0) {
-    int64_t wv = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+    int64_t w = wsum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int64_t x = __shfl_up_sync(0xffffffffu, wv, o);
-      if (lane >= o) wv += x;
+      int64_t x = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += x;
     }
-    wsum[lane] = wv;
+    wsum[lane] = w;
   }
   __syncthreads();
-  const int64_t incl = (wid ? wsum[wid - 1] : 0) + v;
-  if (q < Q) qbase[q] = incl - local;
-  if (q == Q - 1) {
-    qbase[Q] = incl;
-    *total = incl;
+  int64_t run = (wid ? wsum[wid - 1] : 0) + v - loc;
+  for (int64_t q = a0; q < a1; ++q) {
+    bpref[q] = run;
+    run += (clocal[q] + RB - 1) / RB;
+  }
+  if (threadIdx.x == 1023) {
+    bpref[Q] = run;
+    flags[2] = run;
   }
 }
 
-// ---------------------------------------------------------------- compact
-constexpr int CMP_THREADS = 256;
-__global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restrict__ scores,
-                                                          int64_t n, int64_t nchunks,
-                                                          const int32_t* __restrict__ lvl,
-                                                          const int64_t* __restrict__ coff,
-                                                          const int64_t* __restrict__ qbase,
-                                                          uint32_t* __restrict__ cand) {
-  __shared__ int wtot[CMP_THREADS / 32];
-  const int c = blockIdx.x;
-  const int64_t q = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t base = (int64_t)c << kChunkShift;
-  const int valid = (int)min((int64_t)kChunk, n - base);
-  const uint32_t L = (uint32_t)lvl[q];
-  const uint32_t Lrep = 0x01010101u * L;
-  const uint4* sc = reinterpret_cast<const uint4*>(scores + ((size_t)q * nchunks + c) * kChunk);
-  uint32_t* dst = cand + qbase[q] + coff[(size_t)q * nchunks + c];
-  int64_t run = 0;
-  for (int r0 = 0; r0 < valid; r0 += CMP_THREADS * 16) {
-    const int p0 = r0 + tid * 16;
-    uint32_t mask = 0;
-    if (p0 < valid) {
-      const uint4 v = sc[p0 >> 4];
-      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t ge = __vcmpgeu4(ws[u], Lrep);
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if ((ge >> (8 * b)) & 1u) mask |= 1u << (u * 4 + b);
-      }
-      const int lim = valid - p0;
-      if (lim < 16) mask &= (1u << lim) - 1u;
-    }
-    const int cnt = __popc(mask);
-    int v = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int x = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += x;
-    }
-    if (lane == 31) wtot[wid] = v;
-    __syncthreads();
-    int woff = 0, btot = 0;
-    for (int w = 0; w < CMP_THREADS / 32; ++w) {
-      if (w < wid) woff += wtot[w];
-      btot += wtot[w];
-    }
-    int pos = (int)run + woff + v - cnt;
-    while (mask) {
-      const int b = __ffs(mask) - 1;
-      dst[pos++] = (uint32_t)(base + p0 + b);
-      mask &= mask - 1u;
-    }
-    run += btot;
-    __syncthreads();
-  }
-}
-
-// ----------------------------------------------------------------- rerank
-// Flattened over every candidate of the tile.  Each warp stages 32 candidate
-// rows through shared memory 64 dims at a time (16-byte coalesced loads of
-// whole row segments), then lane l folds row l into the two einsum lanes
-// (engine.py:272-274) reading float4s conflict-free (row stride 68 floats).
-constexpr int RR_WARPS = 4;
+// ------------------------------------------------------------ rerank + top-k
+// One CTA = 256 candidates of one query.  Each warp stages its 32 rows
+// through shared memory 64 dims at a time (coalesced 16-byte loads of whole
+// row segments), lane l folds row l into numpy's two einsum lanes (engine.py
+// :272-274) against the query held in shared memory as fp64; then the CTA
+// sorts its (d2, position) pairs and keeps the first min(k, 256).
+constexpr int RR_WARPS = RB / 32;
 constexpr int RR_SEG = 64;
 constexpr int RR_PITCH = RR_SEG + 4;
 
-template <bool VEC>
-__global__ void __launch_bounds__(RR_WARPS * 32) k_rerank(const float* __restrict__ X, int d,
-                                                          const float* __restrict__ Qf, int Q,
-                                                          const int64_t* __restrict__ qbase,
-                                                          const uint32_t* __restrict__ cand,
-                                                          double* __restrict__ d2out) {
-  __shared__ __align__(16) float rows[RR_WARPS][32][RR_PITCH];
-  __shared__ uint32_t wcid[RR_WARPS][32];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t M = qbase[Q];
-  const int64_t i = ((int64_t)blockIdx.x * RR_WARPS + wid) * 32 + lane;
-  const bool live = i < M;
-  const uint32_t cid = live ? cand[i] : 0u;
-  int qi = 0;
-  if (live) {
-    int lo = 0, hi = Q;  // largest q with qbase[q] <= i
-    while (hi - lo > 1) {
-      int mid = (lo + hi) >> 1;
-      if (qbase[mid] <= i) lo = mid; else hi = mid;
+__device__ __forceinline__ void bitonic_pairs(unsigned long long* key, int* pos, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool up = (i & size) == 0;
+          const unsigned long long ka = key[i], kb = key[jx];
+          const int pa = pos[i], pb = pos[jx];
+          const bool gt = ka > kb || (ka == kb && pa > pb);
+          if (gt == up) {
+            key[i] = kb; key[jx] = ka;
+            pos[i] = pb; pos[jx] = pa;
+          }
+        }
+      }
+      __syncthreads();
     }
-    qi = lo;
   }
-  wcid[wid][lane] = cid;
-  __syncwarp();
-  const float* qrow = Qf + (size_t)qi * d;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(RB) k_rerank_topk(const float* __restrict__ X, int d,
+                                                    const float* __restrict__ Qf, int64_t Q,
+                                                    const int64_t* __restrict__ bpref,
+                                                    const int64_t* __restrict__ qbase,
+                                                    const int64_t* __restrict__ clocal,
+                                                    const uint32_t* __restrict__ cand, int kk,
+                                                    unsigned long long* __restrict__ pkey,
+                                                    int* __restrict__ ppos) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  float(*rows)[32][RR_PITCH] = reinterpret_cast<float(*)[32][RR_PITCH]>(rsm);
+  double* qv = reinterpret_cast<double*>(rsm + sizeof(float) * RR_WARPS * 32 * RR_PITCH);
+  __shared__ unsigned long long skey[RB];
+  __shared__ int spos[RB];
+  __shared__ uint32_t wcid[RR_WARPS][32];
+  const int64_t b = blockIdx.x;
+  int lo = 0, hi = (int)Q;  // largest q with bpref[q] <= b
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (bpref[mid] <= b) lo = mid; else hi = mid;
+  }
+  const int64_t q = lo;
+  const int64_t off = (b - bpref[q]) * RB;
+  const int m = (int)min((int64_t)RB, clocal[q] - off);
+  const uint32_t* cq = cand + qbase[q] + off;
+  for (int t = threadIdx.x; t < d; t += RB) qv[t] = (double)Qf[q * d + t];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = wid * 32 + lane;
+  wcid[wid][lane] = r < m ? cq[r] : cq[0];
+  __syncthreads();
   double a0 = 0.0, a1 = 0.0;
   float(*R)[RR_PITCH] = rows[wid];
-  for (int seg = 0; seg < d; seg += RR_SEG) {
-    const int len = min(RR_SEG, d - seg);
-    if (VEC) {
-      const int nv = len >> 2;  // float4 per row segment
-      for (int e = lane; e < 32 * (RR_SEG / 4); e += 32) {
-        const int r = e / (RR_SEG / 4), v = e % (RR_SEG / 4);
-        if (v < nv) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)wcid[wid][r] * d + seg) + v);
-          *reinterpret_cast<float4*>(&R[r][v * 4]) = x;
-        }
-      }
-    } else {
-      for (int e = lane; e < 32 * RR_SEG; e += 32) {
-        const int r = e / RR_SEG, v = e % RR_SEG;
-        if (v < len) R[r][v] = __ldg(X + (size_t)wcid[wid][r] * d + seg + v);
-      }
-    }
-    __syncwarp();
-    const bool last = seg + RR_SEG >= d;
-    const int full = last ? (len & ~7) : len;
-    for (int b = 0; b < full; b += 8) {
-      float xv[8];
+  const bool wlive = wid * 32 < m;
+  if (wlive) {
+    for (int seg = 0; seg < d; seg += RR_SEG) {
+      const int len = min(RR_SEG, d - seg);
       if (VEC) {
-        const float4 u = *reinterpret_cast<const float4*>(&R[lane][b]);
-        const float4 w = *reinterpret_cast<const float4*>(&R[lane][b + 4]);
-        xv[0] = u.x; xv[1] = u.y; xv[2] = u.z; xv[3] = u.w;
-        xv[4] = w.x; xv[5] = w.y; xv[6] = w.z; xv[7] = w.w;
+        const int nv = len >> 2;
+#pragma unroll 4
+        for (int e = lane; e < 32 * (RR_SEG / 4); e += 32) {
+          const int rr = e / (RR_SEG / 4), v = e % (RR_SEG / 4);
+          if (v < nv) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)wcid[wid][rr] * d + seg) + v);
+            *reinterpret_cast<float4*>(&R[rr][v * 4]) = x;
+          }
+        }
       } else {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) xv[t] = R[lane][b + t];
-      }
-      double p[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const double e = __dsub_rn((double)xv[t], (double)qrow[seg + b + t]);
-        p[t] = __dmul_rn(e, e);
-      }
-      a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
-      a0 = __dadd_rn(p[4], a0); a1 = __dadd_rn(p[5], a1);
-      a0 = __dadd_rn(p[2], a0); a1 = __dadd_rn(p[3], a1);
-      a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
-    }
-    if (last) {
-      for (int b = full; b < len; b += 2) {
-        const double e0 = __dsub_rn((double)R[lane][b], (double)qrow[seg + b]);
-        a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
-        if (b + 1 < len) {
-          const double e1 = __dsub_rn((double)R[lane][b + 1], (double)qrow[seg + b + 1]);
-          a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
+        for (int e = lane; e < 32 * RR_SEG; e += 32) {
+          const int rr = e / RR_SEG, v = e % RR_SEG;
+          if (v < len) R[rr][v] = __ldg(X + (size_t)wcid[wid][rr] * d + seg + v);
         }
       }
+      __syncwarp();
+      const bool last = seg + RR_SEG >= d;
+      const int full = last ? (len & ~7) : len;
+      for (int bb = 0; bb < full; bb += 8) {
+        float xv[8];
+        if (VEC) {
+          const float4 u = *reinterpret_cast<const float4*>(&R[lane][bb]);
+          const float4 w = *reinterpret_cast<const float4*>(&R[lane][bb + 4]);
+          xv[0] = u.x; xv[1] = u.y; xv[2] = u.z; xv[3] = u.w;
+          xv[4] = w.x; xv[5] = w.y; xv[6] = w.z; xv[7] = w.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) xv[t] = R[lane][bb + t];
+        }
+        double p[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double e = __dsub_rn((double)xv[t], qv[seg + bb + t]);
+          p[t] = __dmul_rn(e, e);
+        }
+        a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
+        a0 = __dadd_rn(p[4], a0); a1 = __dadd_rn(p[5], a1);
+        a0 = __dadd_rn(p[2], a0); a1 = __dadd_rn(p[3], a1);
+        a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
+      }
+      if (last) {
+        for (int bb = full; bb < len; bb += 2) {
+          const double e0 = __dsub_rn((double)R[lane][bb], qv[seg + bb]);
+          a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
+          if (bb + 1 < len) {
+            const double e1 = __dsub_rn((double)R[lane][bb + 1], qv[seg + bb + 1]);
+            a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
+          }
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
-  if (live) {
-    const double v = __dadd_rn(a0, a1);
-    d2out[i] = v >= 0.0 ? v : 0.0;
+  double v = __dadd_rn(a0, a1);
+  v = v >= 0.0 ? v : 0.0;
+  skey[r] = r < m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+  spos[r] = r < m ? (int)(off + r) : 0x7fffffff;
+  __syncthreads();
+  bitonic_pairs(skey, spos, RB);
+  for (int t = threadIdx.x; t < kk; t += RB) {
+    pkey[(size_t)b * kk + t] = skey[t];
+    ppos[(size_t)b * kk + t] = spos[t];
   }
 }
 
 // ------------------------------------------------------------------- top-k
-// One CTA per query: 8-bit-digit radix select of the k-th smallest d2 (fp64
-// bits are order-preserving for d2 >= 0), ordered collection (ties -> earlier
-// position == lower id, since candidates are ascending ids), bitonic sort.
+// One CTA per query over its CTA partial lists: radix select of the k-th
+// smallest (d2 bits, then position among exact d2 ties), then bitonic sort
+// of the kk survivors on (d2, position); writes d2 and global ids.
 constexpr int TK_THREADS = 256;
 constexpr int TK_MAX = 2048;
 
-__global__ void __launch_bounds__(TK_THREADS) k_topk(const double* __restrict__ d2,
-                                                      const uint32_t* __restrict__ cand,
-                                                      const int64_t* __restrict__ qbase, int k,
-                                                      int64_t id_base,
-                                                      double* __restrict__ out_d2,
+__device__ void radix_select_u64(const unsigned long long* keys, const int* pos, int64_t m, int kk,
+                                 bool by_pos, unsigned long long key_eq, unsigned long long& out,
+                                 int& remain, unsigned* hist, unsigned long long* s_pre, int* s_rem) {
+  // selects the kk-th smallest of (by_pos ? pos among key==key_eq : key)
+  const int tid = threadIdx.x;
+  if (tid == 0) { *s_pre = 0ull; *s_rem = kk; }
+  __syncthreads();
+  unsigned long long msk = 0ull;
+  const int passes = by_pos ? 4 : 8;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = (passes - 1 - p) * 8;
+    for (int i = tid; i < 256; i += TK_THREADS) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long pre = *s_pre;
+    for (int64_t i = tid; i < m; i += TK_THREADS) {
+      unsigned long long v;
+      if (by_pos) {
+        if (keys[i] != key_eq) continue;
+        v = (unsigned long long)(unsigned)pos[i];
+      } else {
+        v = keys[i];
+      }
+      if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255ull], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int rem = *s_rem;
+      unsigned acc = 0;
+      int dg = 0;
+      for (; dg < 255; ++dg) {
+        if (acc + hist[dg] >= (unsigned)rem) break;
+        acc += hist[dg];
+      }
+      *s_rem = rem - (int)acc;
+      *s_pre = pre | ((unsigned long long)dg << shift);
+    }
+    msk |= 255ull << shift;
+    __syncthreads();
+  }
+  out = *s_pre;
+  remain = *s_rem;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* __restrict__ pkey,
+                                                      const int* __restrict__ ppos,
+                                                      const int64_t* __restrict__ bpref, int kk_part,
+                                                      const int64_t* __restrict__ qbase,
+                                                      const int64_t* __restrict__ clocal,
+                                                      const uint32_t* __restrict__ cand, int k,
+                                                      int64_t id_base, double* __restrict__ out_d2,
                                                       int64_t* __restrict__ out_ids) {
   __shared__ unsigned hist[256];
-  __shared__ unsigned long long s_prefix, s_mask;
-  __shared__ int s_rem;
+  __shared__ unsigned long long s_pre;
+  __shared__ int s_rem, s_fill;
   __shared__ unsigned long long skey[TK_MAX];
   __shared__ int spos[TK_MAX];
-  __shared__ int s_nless, s_ntie, wtmp[TK_THREADS / 32][2];
   const int64_t q = blockIdx.x;
-  const int64_t lo = qbase[q];
-  const int64_t m = qbase[q + 1] - lo;
-  const int kk = (int)min((int64_t)k, m);
+  const int64_t lo = bpref[q] * kk_part;
+  const int64_t m = (bpref[q + 1] - bpref[q]) * kk_part;
+  const int kk = (int)min((int64_t)k, clocal[q]);
+  const unsigned long long* keys = pkey + lo;
+  const int* pos = ppos + lo;
   const int tid = threadIdx.x;
-  const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(d2 + lo);
-  if (tid == 0) {
-    s_prefix = 0ull;
-    s_mask = 0ull;
-    s_rem = kk;
-    s_nless = 0;
-    s_ntie = 0;
-  }
+  if (tid == 0) s_fill = 0;
   __syncthreads();
   if (kk > 0) {
-    for (int pass = 0; pass < 8; ++pass) {
-      const int shift = 56 - 8 * pass;
-      for (int i = tid; i < 256; i += TK_THREADS) hist[i] = 0;
-      __syncthreads();
-      const unsigned long long pre = s_prefix, msk = s_mask;
-      for (int64_t i = tid; i < m; i += TK_THREADS) {
-        const unsigned long long kv = keys[i];
-        if ((kv & msk) == pre) atomicAdd(&hist[(kv >> shift) & 255ull], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int rem = s_rem;
-        unsigned acc = 0;
-        int dg = 0;
-        for (; dg < 256; ++dg) {
-          if (acc + hist[dg] >= (unsigned)rem) break;
-          acc += hist[dg];
-        }
-        s_rem = rem - (int)acc;
-        s_prefix = pre | ((unsigned long long)dg << shift);
-        s_mask = msk | (255ull << shift);
-      }
-      __syncthreads();
+    unsigned long long tau;
+    int take;
+    radix_select_u64(keys, pos, m, kk, false, 0ull, tau, take, hist, &s_pre, &s_rem);
+    // among the exact ties at tau keep the `take` smallest positions
+    int64_t nties = 0;
+    for (int64_t i = tid; i < m; i += TK_THREADS) nties += keys[i] == tau;
+    for (int o = 16; o > 0; o >>= 1) nties += __shfl_xor_sync(0xffffffffu, nties, o);
+    __shared__ int64_t s_ties;
+    if (tid == 0) s_ties = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicAdd((unsigned long long*)&s_ties, (unsigned long long)nties);
+    __syncthreads();
+    unsigned long long pi = ~0ull;
+    if (s_ties > take) {
+      int dummy;
+      radix_select_u64(keys, pos, m, take, true, tau, pi, dummy, hist, &s_pre, &s_rem);
     }
-    const unsigned long long tau = s_prefix;
-    const int take_ties = s_rem;
-    // ordered collection in position order
-    const int lane = tid & 31, wid = tid >> 5;
-    int nl_run = 0, nt_run = 0;
-    for (int64_t r0 = 0; r0 < m; r0 += TK_THREADS) {
-      const int64_t i = r0 + tid;
-      unsigned long long kv = 0;
-      int isl = 0, ist = 0;
-      if (i < m) {
-        kv = keys[i];
-        isl = kv < tau;
-        ist = kv == tau;
-      }
-      int vl = isl, vt = ist;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, vl, o);
-        int b = __shfl_up_sync(0xffffffffu, vt, o);
-        if (lane >= o) { vl += a; vt += b; }
-      }
-      if (lane == 31) { wtmp[wid][0] = vl; wtmp[wid][1] = vt; }
-      __syncthreads();
-      int ol = 0, ot = 0, tl = 0, tt = 0;
-      for (int w = 0; w < TK_THREADS / 32; ++w) {
-        if (w < wid) { ol += wtmp[w][0]; ot += wtmp[w][1]; }
-        tl += wtmp[w][0];
-        tt += wtmp[w][1];
-      }
-      const int rl = nl_run + ol + vl - isl;   // rank among "less"
-      const int rt = nt_run + ot + vt - ist;   // rank among ties
-      if (isl) { skey[rl] = kv; spos[rl] = (int)i; }
-      if (ist && rt < take_ties) {
-        const int slot = (kk - take_ties) + rt;
+    for (int64_t i = tid; i < m; i += TK_THREADS) {
+      const unsigned long long kv = keys[i];
+      const bool sel = kv < tau || (kv == tau && (unsigned long long)(unsigned)pos[i] <= pi);
+      if (sel) {
+        const int slot = atomicAdd(&s_fill, 1);
         skey[slot] = kv;
-        spos[slot] = (int)i;
+        spos[slot] = pos[i];
       }
-      nl_run += tl;
-      nt_run += tt;
-      __syncthreads();
     }
+    __syncthreads();
   }
-  // bitonic sort of kk items on (key, pos), padded to a power of two
   int P = 1;
   while (P < kk) P <<= 1;
   for (int i = kk + tid; i < P; i += TK_THREADS) {
@@ -705,28 +888,12 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const double* __restrict__ 
     spos[i] = 0x7fffffff;
   }
   __syncthreads();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < P; i += TK_THREADS) {
-        const int jx = i ^ stride;
-        if (jx > i) {
-          const bool up = (i & size) == 0;
-          const unsigned long long ka = skey[i], kb = skey[jx];
-          const int pa = spos[i], pb = spos[jx];
-          const bool gt = ka > kb || (ka == kb && pa > pb);
-          if (gt == up) {
-            skey[i] = kb; skey[jx] = ka;
-            spos[i] = pb; spos[jx] = pa;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
+  bitonic_pairs(skey, spos, P);
+  const uint32_t* cq = cand + qbase[q];
   for (int r = tid; r < k; r += TK_THREADS) {
     if (r < kk) {
       out_d2[q * k + r] = __longlong_as_double((long long)skey[r]);
-      out_ids[q * k + r] = (int64_t)cand[lo + spos[r]] + id_base;
+      out_ids[q * k + r] = (int64_t)cq[spos[r]] + id_base;
     } else {
       out_d2[q * k + r] = __longlong_as_double(0x7ff0000000000000LL);
       out_ids[q * k + r] = -1;
@@ -734,7 +901,6 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const double* __restrict__ 
   }
 }
 
-// Final outputs: ids int32 (-1 padded), dists f32(sqrt(d2)) (+inf padded).
 __global__ void k_finalize(const double* __restrict__ d2, const int64_t* __restrict__ ids, int64_t total,
                            int32_t* __restrict__ out_ids, float* __restrict__ out_d) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -776,41 +942,57 @@ __global__ void k_merge(int R, int k, int64_t nq, const double* __restrict__ d2,
 }
 
 // ===================================================================== host
-struct TileDims {
-  int Q;
-  int cap;
-};
+constexpr int64_t kSuperTile = 16384;
 
-static int tile_queries(const taco_index* idx) {
-  // keep the Q x n score tables within ~96 MiB (L2-resident) and Q <= 1024
-  const int64_t per = idx->nchunks * kChunk;
-  int64_t Q = (int64_t)(96ll << 20) / per;
-  const int64_t popcap = (int64_t)idx->n_sub * idx->K * 2;
-  Q = std::min<int64_t>(Q, (int64_t)(256ll << 20) / std::max<int64_t>(popcap, 1));
-  Q = std::max<int64_t>(16, std::min<int64_t>(Q, 1024));
-  return (int)Q;
+static int64_t super_tile(const taco_index* idx, int cap) {
+  const int64_t per = (int64_t)idx->n_sub * (2LL * cap + 20LL * idx->kp + 16) + 8LL * (idx->d + idx->D) + 64;
+  const int64_t Q = (int64_t)(1ll << 30) / std::max<int64_t>(per, 1);
+  return std::max<int64_t>(64, std::min<int64_t>(Q, kSuperTile));
 }
 
-static int ensure_tile(taco_index* idx, int Q, int k) {
+static int global_tile(const taco_index* idx) {
+  const int64_t per = idx->nchunks * idx->chunk;
+  const int64_t Q = (int64_t)(96ll << 20) / per;
+  return (int)std::max<int64_t>(8, std::min<int64_t>(Q, 1024));
+}
+
+static int ensure_front(taco_index* idx, int64_t QS, int k) {
   QueryTile& t = idx->qt;
-  const size_t QS = (size_t)Q * idx->n_sub;
-  TACO_TRY(t.Q.ensure(sizeof(float) * (size_t)Q * idx->d));
-  TACO_TRY(t.qt.ensure(sizeof(float) * (size_t)Q * idx->D));
-  TACO_TRY(t.sd.ensure(sizeof(double) * QS * 2 * idx->kp));
-  TACO_TRY(t.sl.ensure(sizeof(uint16_t) * QS * 2 * idx->kp));
-  TACO_TRY(t.pops.ensure(sizeof(uint16_t) * QS * idx->K));
-  TACO_TRY(t.npop.ensure(sizeof(int32_t) * QS));
-  TACO_TRY(t.ret.ensure(sizeof(int64_t) * QS));
-  TACO_TRY(t.scores.ensure((size_t)Q * idx->nchunks * kChunk));
-  TACO_TRY(t.part.ensure(sizeof(int32_t) * (size_t)Q * idx->nchunks * (idx->n_sub + 1)));
-  TACO_TRY(t.hist.ensure(sizeof(int64_t) * (size_t)Q * (idx->n_sub + 1)));
-  TACO_TRY(t.lvl.ensure(sizeof(int32_t) * Q));
-  TACO_TRY(t.cnum.ensure(sizeof(int64_t) * Q));
-  TACO_TRY(t.coff.ensure(sizeof(int64_t) * (size_t)Q * idx->nchunks));
-  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * (Q + 1)));
-  TACO_TRY(t.total.ensure(sizeof(int64_t)));
-  TACO_TRY(t.tk_d2.ensure(sizeof(double) * (size_t)Q * k));
-  TACO_TRY(t.tk_ids.ensure(sizeof(int64_t) * (size_t)Q * k));
+  if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
+  const size_t QN = (size_t)QS * idx->n_sub;
+  TACO_TRY(t.Q.ensure(sizeof(float) * (size_t)QS * idx->d));
+  TACO_TRY(t.qt.ensure(sizeof(float) * (size_t)QS * idx->D));
+  TACO_TRY(t.sd.ensure(sizeof(double) * QN * 2 * idx->kp));
+  TACO_TRY(t.sl.ensure(sizeof(uint16_t) * QN * 2 * idx->kp));
+  TACO_TRY(t.pops.ensure(sizeof(uint16_t) * QN * t.pop_cap));
+  TACO_TRY(t.npop.ensure(sizeof(int32_t) * QN));
+  TACO_TRY(t.ret.ensure(sizeof(int64_t) * QN));
+  TACO_TRY(t.flags.ensure(sizeof(int64_t) * 8));
+  TACO_TRY(t.lvl.ensure(sizeof(int32_t) * QS));
+  TACO_TRY(t.cnum.ensure(sizeof(int64_t) * QS));
+  TACO_TRY(t.clocal.ensure(sizeof(int64_t) * QS));
+  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * QS));
+  TACO_TRY(t.bpref.ensure(sizeof(int64_t) * (QS + 1)));
+  TACO_TRY(t.tk_d2.ensure(sizeof(double) * (size_t)QS * std::max(k, 1)));
+  TACO_TRY(t.tk_ids.ensure(sizeof(int64_t) * (size_t)QS * std::max(k, 1)));
+  TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)QS * std::max(k, 1)));
+  TACO_TRY(t.out_d.ensure(sizeof(float) * (size_t)QS * std::max(k, 1)));
+  if (!idx->cluster_mode) {
+    const int Qt = global_tile(idx);
+    TACO_TRY(t.scores.ensure((size_t)Qt * idx->nchunks * idx->chunk));
+    TACO_TRY(t.part.ensure(sizeof(int32_t) * (size_t)Qt * idx->nchunks * (idx->n_sub + 1)));
+    TACO_TRY(t.hist.ensure(sizeof(int64_t) * (size_t)Qt * (idx->n_sub + 1)));
+    TACO_TRY(t.coff.ensure(sizeof(int64_t) * (size_t)Qt * idx->nchunks));
+  }
+  return TACO_OK;
+}
+
+static int ensure_cand(taco_index* idx, int64_t want) {
+  QueryTile& t = idx->qt;
+  if (want > t.cand_cap) {
+    TACO_TRY(t.cand.ensure(sizeof(uint32_t) * (size_t)want));
+    t.cand_cap = want;
+  }
   return TACO_OK;
 }
 
@@ -820,7 +1002,8 @@ static int check_query_ready(taco_index* idx, double alpha, int k) {
     TACO_FAIL(TACO_ERR_STATE, "index is not built (model %d codebooks %d cells %d sizes %d)",
               idx->has_model, idx->has_cb, idx->has_cells, idx->has_gsize);
   if (!(alpha > 0.0 && alpha <= 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "collision ratio %g outside (0, 1]", alpha);
-  if (k < 0 || k > TK_MAX) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d outside [1, %d]", k, TK_MAX);
+  if (k < 1 || k > TK_MAX) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d outside [1, %d]", k, TK_MAX);
+  if (idx->d > 4096) TACO_FAIL(TACO_ERR_PARAMETER, "dimension %d exceeds 4096", idx->d);
   return TACO_OK;
 }
 
@@ -829,35 +1012,34 @@ static int64_t retrieval_target(double alpha, int64_t n) {
   return std::min<int64_t>(n, (int64_t)t);
 }
 
-// Stages 1-5 for one tile already resident in idx->qt.Q: leaves part + hist.
-static int run_count_stage(taco_index* idx, int Q, double alpha, cudaStream_t st,
-                           double* keys_out) {
+// transform + centroid ranks + traversal for QS queries resident in t.Q
+static int stage_front(taco_index* idx, int64_t QS, double alpha, cudaStream_t st, double* keys_out) {
   QueryTile& t = idx->qt;
   const int kp = idx->kp;
   {
     ProfScope ps(K_TRANSFORM, st);
-    TACO_TRY(launch_transform(st, t.Q.as<float>(), Q, idx->d, idx->D, idx->mean.as<float>(),
+    TACO_TRY(launch_transform(st, t.Q.as<float>(), QS, idx->d, idx->D, idx->mean.as<float>(),
                               idx->M.as<float>(), t.qt.as<float>(), false));
   }
   {
-    const int64_t warps = (int64_t)Q * idx->n_sub * 2;
+    const int64_t warps = QS * idx->n_sub * 2;
     const int wpb = 8;
     ProfScope ps(K_CSORT, st);
     k_csort<<<(unsigned)ceil_div(warps, wpb), wpb * 32, sizeof(double) * kp * wpb, st>>>(
-        t.qt.as<float>(), Q, idx->n_sub, idx->s, idx->m1, idx->m2, kp, idx->cb1.as<float>(),
+        t.qt.as<float>(), (int)QS, idx->n_sub, idx->s, idx->m1, idx->m2, kp, idx->cb1.as<float>(),
         idx->cb2.as<float>(), t.sd.as<double>(), t.sl.as<uint16_t>());
     TACO_LAUNCHED();
   }
   {
-    const int64_t th = (int64_t)Q * idx->n_sub;
+    const int64_t th = QS * idx->n_sub;
     const int64_t target = retrieval_target(alpha, idx->n_global);
     const unsigned g = (unsigned)ceil_div(th, 128);
     ProfScope ps(K_TRAVERSE, st);
-#define TRAV(KM)                                                                              \
-  k_traverse<KM><<<g, 128, 0, st>>>(t.sd.as<double>(), t.sl.as<uint16_t>(),                   \
-                                    idx->gsize.as<int64_t>(), Q, idx->n_sub, kp, target,        \
-                                    t.pops.as<uint16_t>(), idx->K, keys_out, t.npop.as<int32_t>(), \
-                                    t.ret.as<int64_t>())
+#define TRAV(KM)                                                                                  \
+  k_traverse<KM><<<g, 128, 0, st>>>(t.sd.as<double>(), t.sl.as<uint16_t>(), idx->gsize.as<int64_t>(), \
+                                    QS, idx->n_sub, kp, target, t.pops.as<uint16_t>(), t.pop_cap,     \
+                                    keys_out, t.npop.as<int32_t>(), t.ret.as<int64_t>(),              \
+                                    t.flags.as<int64_t>())
     if (kp <= 32) TRAV(32);
     else if (kp <= 64) TRAV(64);
     else if (kp <= 128) TRAV(128);
@@ -865,118 +1047,226 @@ static int run_count_stage(taco_index* idx, int Q, double alpha, cudaStream_t st
 #undef TRAV
     TACO_LAUNCHED();
   }
+  return TACO_OK;
+}
+
+static int set_count_attrs(taco_index* idx) {
+  static int64_t cur_c = -1, cur_g = -1;
+  if (idx->cluster_mode && cur_c < idx->chunk) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kClusterMaxChunk));
+    cur_c = kClusterMaxChunk;
+  }
+  if (cur_g < kClusterMaxChunk) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kClusterMaxChunk));
+    cur_g = kClusterMaxChunk;
+  }
+  return TACO_OK;
+}
+
+// global-mode counting of queries [q0, q0+Q) of the super-tile: tables + histograms
+static int global_count_tile(taco_index* idx, int64_t q0, int Q, cudaStream_t st) {
+  QueryTile& t = idx->qt;
+  TACO_TRY(set_count_attrs(idx));
   {
-    const size_t smem = kChunk + sizeof(uint32_t) * (2 * CNT_PB + 1);
-    static bool attr = false;
-    if (!attr) {
-      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
     dim3 g((unsigned)idx->nchunks, (unsigned)Q);
     ProfScope ps(K_COUNT, st);
-    k_count<<<g, CNT_THREADS, smem, st>>>(t.pops.as<uint16_t>(), t.npop.as<int32_t>(), idx->K,
-                                          idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-                                          idx->n_sub, idx->K, idx->n, idx->nchunks,
-                                          t.scores.as<uint8_t>(), t.part.as<int32_t>());
+    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap,
+                                                       idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+                                                       idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, q0,
+                                                       t.scores.as<uint8_t>(), t.part.as<int32_t>());
     TACO_LAUNCHED();
   }
   {
     ProfScope ps(K_HIST, st);
-    k_hist_reduce<<<Q, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub,
-                                    t.hist.as<int64_t>());
+    k_hist_reduce<<<Q, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub, t.hist.as<int64_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
 }
 
-// Stages 6-9: select on `ghist`, compact, rerank, top-k into t.tk_d2/tk_ids.
-static int run_finish_stage(taco_index* idx, int Q, const int64_t* ghist, double beta, int k,
-                            cudaStream_t st) {
+static int global_select_tile(taco_index* idx, int64_t q0, int Q, const int64_t* ghist, double beta,
+                              cudaStream_t st) {
   QueryTile& t = idx->qt;
   const double budget = beta * (double)idx->n_global;   // engine.py:240
   {
-    ProfScope ps_sel(K_SELECT, st);
-    k_select<<<1, 1024, 0, st>>>(ghist, t.part.as<int32_t>(), Q, idx->nchunks, idx->n_sub, budget,
-                                 t.lvl.as<int32_t>(), t.cnum.as<int64_t>(), t.coff.as<int64_t>(),
-                                 t.qbase.as<int64_t>(), t.total.as<int64_t>());
+    ProfScope ps(K_SELECT, st);
+    k_select<<<(unsigned)ceil_div(Q, 128), 128, 0, st>>>(ghist, t.part.as<int32_t>(), Q, q0, idx->nchunks,
+                                                          idx->n_sub, budget, t.coff.as<int64_t>(), t.cand_cap,
+                                                          t.flags.as<int64_t>(), t.qbase.as<int64_t>(),
+                                                          t.clocal.as<int64_t>(), t.cnum.as<int64_t>(),
+                                                          t.lvl.as<int32_t>());
     TACO_LAUNCHED();
   }
-  int64_t total = 0;
-  TACO_CHECK_CUDA(cudaMemcpyAsync(&total, t.total.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (g_prof.on) {
-    std::vector<int64_t> r((size_t)Q * idx->n_sub);
-    std::vector<int32_t> np((size_t)Q * idx->n_sub);
-    cudaMemcpy(r.data(), t.ret.p, 8 * r.size(), cudaMemcpyDeviceToHost);
-    cudaMemcpy(np.data(), t.npop.p, 4 * np.size(), cudaMemcpyDeviceToHost);
-    for (auto v : r) g_prof.sumR += v;
-    for (auto v : np) g_prof.sumPops += v;
-    g_prof.sumC += total;
-    g_prof.queries += Q;
-    g_prof.tiles += 1;
-    g_prof.bytes_scores += (int64_t)Q * idx->nchunks * kChunk;
-  }
-  TACO_TRY(t.cand.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1)));
-  TACO_TRY(t.d2.ensure(sizeof(double) * (size_t)std::max<int64_t>(total, 1)));
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)Q);
     ProfScope ps(K_COMPACT, st);
-    k_compact<<<g, CMP_THREADS, 0, st>>>(t.scores.as<uint8_t>(), idx->n, idx->nchunks,
-                                         t.lvl.as<int32_t>(), t.coff.as<int64_t>(),
-                                         t.qbase.as<int64_t>(), t.cand.as<uint32_t>());
-    TACO_LAUNCHED();
-  }
-  if (total > 0) {
-    const unsigned g = (unsigned)ceil_div(total, RR_WARPS * 32);
-    ProfScope ps(K_RERANK, st);
-    if (idx->d % 4 == 0)
-      k_rerank<true><<<g, RR_WARPS * 32, 0, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), Q,
-                                                  t.qbase.as<int64_t>(), t.cand.as<uint32_t>(),
-                                                  t.d2.as<double>());
-    else
-      k_rerank<false><<<g, RR_WARPS * 32, 0, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), Q,
-                                                   t.qbase.as<int64_t>(), t.cand.as<uint32_t>(),
-                                                   t.d2.as<double>());
-    TACO_LAUNCHED();
-  }
-  if (k > 0) {
-    ProfScope ps(K_TOPK, st);
-    k_topk<<<Q, TK_THREADS, 0, st>>>(t.d2.as<double>(), t.cand.as<uint32_t>(), t.qbase.as<int64_t>(),
-                                     k, idx->id_base, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>());
+    k_compact<<<g, CMP_THREADS, 0, st>>>(t.scores.as<uint8_t>(), idx->n, idx->nchunks, idx->chunk, q0,
+                                         t.lvl.as<int32_t>(), t.coff.as<int64_t>(), t.qbase.as<int64_t>(),
+                                         t.clocal.as<int64_t>(), t.cand_cap, t.cand.as<uint32_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
 }
 
-static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, int64_t nq,
-                            double alpha, double beta, int k, int32_t* ids_o, float* dists_o,
-                            int64_t* cnum_o, int32_t* lvl_o, bool dst_host, cudaStream_t st) {
+static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t st) {
+  QueryTile& t = idx->qt;
+  TACO_TRY(set_count_attrs(idx));
+  const double budget = beta * (double)idx->n_global;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)idx->nchunks, (unsigned)QS, 1);
+  cfg.blockDim = dim3(CT_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)idx->chunk;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)idx->nchunks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps(K_COUNT, st);
+  TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_count_cluster, (const uint16_t*)t.pops.as<uint16_t>(),
+                                     (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
+                                     (const uint32_t*)idx->ids.as<uint32_t>(),
+                                     (const uint32_t*)idx->offs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
+                                     idx->nchunks, idx->chunk, budget, t.cand.as<uint32_t>(), t.cand_cap,
+                                     t.flags.as<int64_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(),
+                                     t.cnum.as<int64_t>(), t.lvl.as<int32_t>()));
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
+static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t fl[4]) {
+  QueryTile& t = idx->qt;
+  {
+    ProfScope ps(K_PLAN, st);
+    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS, t.bpref.as<int64_t>(), t.flags.as<int64_t>());
+    TACO_LAUNCHED();
+  }
+  TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  return TACO_OK;
+}
+
+static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t nblocks, cudaStream_t st) {
+  QueryTile& t = idx->qt;
+  const int kk = std::min(k, RB);
+  TACO_TRY(t.pd2.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(nblocks, 1) * kk));
+  TACO_TRY(t.ppos.ensure(sizeof(int) * (size_t)std::max<int64_t>(nblocks, 1) * kk));
+  if (nblocks > 0) {
+    const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * idx->d;
+    static size_t attr_set = 0;
+    if (attr_set < smem) {
+      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set = smem;
+    }
+    ProfScope ps(K_RERANK, st);
+    if (idx->d % 4 == 0)
+      k_rerank_topk<true><<<(unsigned)nblocks, RB, smem, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS,
+                                                               t.bpref.as<int64_t>(), t.qbase.as<int64_t>(),
+                                                               t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), kk,
+                                                               t.pd2.as<unsigned long long>(), t.ppos.as<int>());
+    else
+      k_rerank_topk<false><<<(unsigned)nblocks, RB, smem, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS,
+                                                                t.bpref.as<int64_t>(), t.qbase.as<int64_t>(),
+                                                                t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), kk,
+                                                                t.pd2.as<unsigned long long>(), t.ppos.as<int>());
+    TACO_LAUNCHED();
+  }
+  {
+    ProfScope ps(K_TOPK, st);
+    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(t.pd2.as<unsigned long long>(), t.ppos.as<int>(),
+                                                t.bpref.as<int64_t>(), kk, t.qbase.as<int64_t>(),
+                                                t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), k, idx->id_base,
+                                                t.tk_d2.as<double>(), t.tk_ids.as<int64_t>());
+    TACO_LAUNCHED();
+  }
+  return TACO_OK;
+}
+
+static void prof_stats(taco_index* idx, int64_t QS, int64_t total) {
+  if (!g_prof.on) return;
+  QueryTile& t = idx->qt;
+  std::vector<int64_t> r((size_t)QS * idx->n_sub);
+  std::vector<int32_t> np((size_t)QS * idx->n_sub);
+  cudaMemcpy(r.data(), t.ret.p, 8 * r.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(np.data(), t.npop.p, 4 * np.size(), cudaMemcpyDeviceToHost);
+  for (auto v : r) g_prof.sumR += v;
+  for (auto v : np) g_prof.sumPops += v;
+  g_prof.sumC += total;
+  g_prof.queries += QS;
+  g_prof.tiles += 1;
+  g_prof.bytes_scores += idx->cluster_mode ? 0 : QS * idx->nchunks * idx->chunk;
+}
+
+// Full single-GPU pipeline for QS queries already in t.Q -> t.tk_d2 / t.tk_ids (+ cnum, lvl).
+static int run_super_tile(taco_index* idx, int64_t QS, double alpha, double beta, int k, cudaStream_t st) {
+  QueryTile& t = idx->qt;
+  if (t.cand_cap == 0) {
+    const int64_t est = QS * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n_global)) + (1 << 20);
+    TACO_TRY(ensure_cand(idx, std::min<int64_t>(est, (int64_t)1 << 31)));
+  }
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
+    TACO_TRY(stage_front(idx, QS, alpha, st, nullptr));
+    if (idx->cluster_mode) {
+      TACO_TRY(cluster_count(idx, QS, beta, st));
+    } else {
+      const int Qt = global_tile(idx);
+      for (int64_t q0 = 0; q0 < QS; q0 += Qt) {
+        const int Q = (int)std::min<int64_t>(Qt, QS - q0);
+        TACO_TRY(global_count_tile(idx, q0, Q, st));
+        TACO_TRY(global_select_tile(idx, q0, Q, t.hist.as<int64_t>(), beta, st));
+      }
+    }
+    int64_t fl[4];
+    TACO_TRY(plan_and_read(idx, QS, st, fl));
+    if (fl[0] > t.pop_cap) {           // a traversal popped more cells than stored
+      t.pop_cap = idx->K;
+      TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)QS * idx->n_sub * t.pop_cap));
+      continue;
+    }
+    if (fl[1]) {                       // candidate buffer too small: grow to what was asked
+      TACO_TRY(ensure_cand(idx, fl[3] + fl[3] / 4 + 1024));
+      continue;
+    }
+    prof_stats(idx, QS, fl[3]);
+    return rerank_stage(idx, QS, k, fl[2], st);
+  }
+  TACO_FAIL(TACO_ERR_CUDA, "query scratch did not converge");
+}
+
+static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, int64_t nq, double alpha,
+                            double beta, int k, int32_t* ids_o, float* dists_o, int64_t* cnum_o,
+                            int32_t* lvl_o, bool dst_host, cudaStream_t st) {
   TACO_TRY(check_query_ready(idx, alpha, k));
   if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "base vectors are not resident");
   if (!(beta > 0.0 && beta < 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "re-rank ratio %g outside (0, 1)", beta);
-  if (k < 1) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d is below 1", k);
   if (nq == 0) return TACO_OK;
-  const int Qt = tile_queries(idx);
-  TACO_TRY(ensure_tile(idx, Qt, k));
   QueryTile& t = idx->qt;
-  TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)Qt * k));
-  TACO_TRY(t.out_d.ensure(sizeof(float) * (size_t)Qt * k));
-  for (int64_t q0 = 0; q0 < nq; q0 += Qt) {
-    const int Q = (int)std::min<int64_t>(Qt, nq - q0);
-    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_src + (size_t)q0 * idx->d, sizeof(float) * (size_t)Q * idx->d,
-                                    src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
-    TACO_TRY(run_count_stage(idx, Q, alpha, st, nullptr));
-    TACO_TRY(run_finish_stage(idx, Q, t.hist.as<int64_t>(), beta, k, st));
-    const int64_t tot = (int64_t)Q * k;
-    ProfScope ps(K_FINAL, st);
-    k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(),
-                                                             tot, t.out_ids.as<int32_t>(), t.out_d.as<float>());
-    TACO_LAUNCHED();
-    const cudaMemcpyKind kind = dst_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    TACO_CHECK_CUDA(cudaMemcpyAsync(ids_o + q0 * k, t.out_ids.p, sizeof(int32_t) * tot, kind, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(dists_o + q0 * k, t.out_d.p, sizeof(float) * tot, kind, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(cnum_o + q0, t.cnum.p, sizeof(int64_t) * Q, kind, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(lvl_o + q0, t.lvl.p, sizeof(int32_t) * Q, kind, st));
+  if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
+  const int64_t QSmax = std::min<int64_t>(nq, super_tile(idx, t.pop_cap));
+  TACO_TRY(ensure_front(idx, QSmax, k));
+  const cudaMemcpyKind kin = src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind kout = dst_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  for (int64_t q0 = 0; q0 < nq; q0 += QSmax) {
+    const int64_t QS = std::min<int64_t>(QSmax, nq - q0);
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_src + (size_t)q0 * idx->d, sizeof(float) * (size_t)QS * idx->d, kin, st));
+    TACO_TRY(run_super_tile(idx, QS, alpha, beta, k, st));
+    const int64_t tot = QS * k;
+    {
+      ProfScope ps(K_FINAL, st);
+      k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), tot,
+                                                               t.out_ids.as<int32_t>(), t.out_d.as<float>());
+      TACO_LAUNCHED();
+    }
+    TACO_CHECK_CUDA(cudaMemcpyAsync(ids_o + q0 * k, t.out_ids.p, sizeof(int32_t) * tot, kout, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(dists_o + q0 * k, t.out_d.p, sizeof(float) * tot, kout, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(cnum_o + q0, t.cnum.p, sizeof(int64_t) * QS, kout, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(lvl_o + q0, t.lvl.p, sizeof(int32_t) * QS, kout, st));
   }
   if (dst_host) TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   return TACO_OK;
@@ -1005,45 +1295,72 @@ int taco_query_batch_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
                           last_coll_d, false, st);
 }
 
+int taco_query_tile_size(taco_index* idx) {
+  if (!idx) return 0;
+  return idx->cluster_mode ? (int)kSuperTile : global_tile(idx);
+}
+
+// Split query (multi-GPU): only global-mode (sharded) indexes.
 int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, double alpha,
                             int64_t* hist_d, void* stream) {
   TACO_TRY(check_query_ready(idx, alpha, 1));
+  if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
-  const int Qt = tile_queries(idx);
+  const int Qt = global_tile(idx);
   if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %d", (long long)nq, Qt);
-  TACO_TRY(ensure_tile(idx, Qt, 1));
   QueryTile& t = idx->qt;
-  TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d,
-                                  cudaMemcpyDeviceToDevice, st));
-  TACO_TRY(run_count_stage(idx, (int)nq, alpha, st, nullptr));
+  TACO_TRY(ensure_front(idx, Qt, 1));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
+    TACO_TRY(stage_front(idx, nq, alpha, st, nullptr));
+    int64_t f0 = 0;
+    TACO_CHECK_CUDA(cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st));
+    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (f0 <= t.pop_cap) break;
+    t.pop_cap = idx->K;
+    TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)Qt * idx->n_sub * t.pop_cap));
+  }
+  TACO_TRY(global_count_tile(idx, 0, (int)nq, st));
   TACO_CHECK_CUDA(cudaMemcpyAsync(hist_d, t.hist.p, sizeof(int64_t) * (size_t)nq * (idx->n_sub + 1),
                                   cudaMemcpyDeviceToDevice, st));
   return TACO_OK;
 }
 
 int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d, double beta,
-                               int32_t k, double* topk_d2_d, int64_t* topk_ids_d,
-                               int64_t* cand_num_d, int32_t* last_coll_d, void* stream) {
+                             int32_t k, double* topk_d2_d, int64_t* topk_ids_d,
+                             int64_t* cand_num_d, int32_t* last_coll_d, void* stream) {
   TACO_TRY(index_check(idx));
   if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "base vectors are not resident");
   if (!(beta > 0.0 && beta < 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "re-rank ratio %g outside (0, 1)", beta);
   if (k < 1 || k > TK_MAX) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d outside [1, %d]", k, TK_MAX);
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
-  const int Qt = tile_queries(idx);
+  const int Qt = global_tile(idx);
   if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %d", (long long)nq, Qt);
-  TACO_TRY(ensure_tile(idx, Qt, k));
+  TACO_TRY(ensure_front(idx, Qt, k));
   QueryTile& t = idx->qt;
-  TACO_TRY(run_finish_stage(idx, (int)nq, ghist_d, beta, k, st));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(topk_d2_d, t.tk_d2.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(topk_ids_d, t.tk_ids.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(cand_num_d, t.cnum.p, sizeof(int64_t) * nq, cudaMemcpyDeviceToDevice, st));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(last_coll_d, t.lvl.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToDevice, st));
-  return TACO_OK;
-}
-
-int taco_query_tile_size(taco_index* idx) {
-  if (!idx) return 0;
-  return tile_queries(idx);
+  if (t.cand_cap == 0)
+    TACO_TRY(ensure_cand(idx, Qt * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n_global)) + (1 << 20)));
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    int64_t zero[2] = {0, 0};
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 1, zero, 8, cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 3, zero, 8, cudaMemcpyHostToDevice, st));
+    TACO_TRY(global_select_tile(idx, 0, (int)nq, ghist_d, beta, st));
+    int64_t fl[4];
+    TACO_TRY(plan_and_read(idx, nq, st, fl));
+    if (fl[1]) {
+      TACO_TRY(ensure_cand(idx, fl[3] + fl[3] / 4 + 1024));
+      continue;
+    }
+    prof_stats(idx, nq, fl[3]);
+    TACO_TRY(rerank_stage(idx, nq, k, fl[2], st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(topk_d2_d, t.tk_d2.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(topk_ids_d, t.tk_ids.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(cand_num_d, t.cnum.p, sizeof(int64_t) * nq, cudaMemcpyDeviceToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(last_coll_d, t.lvl.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToDevice, st));
+    return TACO_OK;
+  }
+  TACO_FAIL(TACO_ERR_CUDA, "candidate buffer did not converge");
 }
 
 int taco_topk_merge_device(int32_t ranks, int64_t nq, int32_t k, const double* d2_d,
@@ -1060,38 +1377,64 @@ int taco_topk_merge_device(int32_t ranks, int64_t nq, int32_t k, const double* d
 // ------------------------------------------------------------ debug taps
 int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* scores_h) {
   TACO_TRY(check_query_ready(idx, alpha, 1));
-  const int Qt = tile_queries(idx);
-  TACO_TRY(ensure_tile(idx, Qt, 1));
   QueryTile& t = idx->qt;
   cudaStream_t st = idx->stream;
-  TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, q_h, sizeof(float) * idx->d, cudaMemcpyHostToDevice, st));
-  TACO_TRY(run_count_stage(idx, 1, alpha, st, nullptr));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(scores_h, t.scores.p, idx->n, cudaMemcpyDeviceToHost, st));
-  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
-  return TACO_OK;
+  TACO_TRY(ensure_front(idx, 1, 1));
+  DevBuf sc, part, hist;
+  TACO_TRY(sc.ensure((size_t)idx->nchunks * idx->chunk));
+  TACO_TRY(part.ensure(sizeof(int32_t) * idx->nchunks * (idx->n_sub + 1)));
+  int rc = TACO_OK;
+  do {
+    if (cudaMemcpyAsync(t.Q.p, q_h, sizeof(float) * idx->d, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      rc = TACO_ERR_CUDA; break;
+    }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st);
+      if ((rc = stage_front(idx, 1, alpha, st, nullptr))) break;
+      int64_t f0 = 0;
+      cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (f0 <= t.pop_cap) break;
+      t.pop_cap = idx->K;
+      if ((rc = t.pops.ensure(sizeof(uint16_t) * idx->n_sub * (size_t)t.pop_cap * super_tile(idx, t.pop_cap)))) break;
+    }
+    if (rc) break;
+    if ((rc = set_count_attrs(idx))) break;
+    k_count<<<dim3((unsigned)idx->nchunks, 1), CT_THREADS, (size_t)idx->chunk, st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, 0, sc.as<uint8_t>(), part.as<int32_t>());
+    count_launch();
+    cudaMemcpyAsync(scores_h, sc.p, idx->n, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; }
+  } while (0);
+  sc.release(); part.release(); hist.release();
+  return rc;
 }
 
 int taco_activation_trace(taco_index* idx, const float* q_h, int32_t j, double alpha, int32_t cap,
                           int32_t* pops_h, double* keys_h, int32_t* npop_h, int64_t* retrieved_h) {
   TACO_TRY(check_query_ready(idx, alpha, 1));
   if (j < 0 || j >= idx->n_sub) TACO_FAIL(TACO_ERR_PARAMETER, "subspace %d out of range", j);
-  const int Qt = tile_queries(idx);
-  TACO_TRY(ensure_tile(idx, Qt, 1));
   QueryTile& t = idx->qt;
   cudaStream_t st = idx->stream;
+  const int saved = t.pop_cap;
+  t.pop_cap = idx->K;
+  TACO_TRY(ensure_front(idx, 1, 1));
   DevBuf keys;
   TACO_TRY(keys.ensure(sizeof(double) * (size_t)idx->n_sub * idx->K));
   TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, q_h, sizeof(float) * idx->d, cudaMemcpyHostToDevice, st));
-  int rc = run_count_stage(idx, 1, alpha, st, keys.as<double>());
+  int rc = stage_front(idx, 1, alpha, st, keys.as<double>());
+  t.pop_cap = saved;
   if (rc != TACO_OK) { keys.release(); return rc; }
   int32_t np = 0;
   int64_t got = 0;
   std::vector<uint16_t> p16(idx->K);
+  std::vector<double> kv(idx->K);
   cudaMemcpyAsync(&np, t.npop.as<int32_t>() + j, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&got, t.ret.as<int64_t>() + j, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(p16.data(), t.pops.as<uint16_t>() + (size_t)j * idx->K, sizeof(uint16_t) * idx->K,
                   cudaMemcpyDeviceToHost, st);
-  std::vector<double> kv(idx->K);
   cudaMemcpyAsync(kv.data(), keys.as<double>() + (size_t)j * idx->K, sizeof(double) * idx->K,
                   cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
@@ -1111,42 +1454,37 @@ int taco_select_candidates(int device, const uint8_t* scores_h, int64_t n, int32
   TACO_TRY(with_device(device));
   if (n_sub < 0 || n_sub > 255) TACO_FAIL(TACO_ERR_PARAMETER, "subspace count %d outside [0, 255]", n_sub);
   if (n < 1) TACO_FAIL(TACO_ERR_PARAMETER, "empty score table");
-  const int64_t nc = ceil_div(n, kChunk);
-  DevBuf sc, part, hist, lvl, cnum, coff, qbase, total, cand;
-  auto cleanup = [&]() {
-    sc.release(); part.release(); hist.release(); lvl.release(); cnum.release(); coff.release();
-    qbase.release(); total.release(); cand.release();
-  };
+  const int64_t chunk = kGlobalChunk;
+  const int64_t nc = ceil_div(n, chunk);
+  DevBuf sc, part, hist, lvl, cnum, coff, qbase, clocal, flags, cand;
   int rc = TACO_OK;
   do {
-    if ((rc = sc.ensure(nc * kChunk)) != TACO_OK) break;
-    if ((rc = part.ensure(sizeof(int32_t) * nc * (n_sub + 1))) != TACO_OK) break;
-    if ((rc = hist.ensure(sizeof(int64_t) * (n_sub + 1))) != TACO_OK) break;
-    if ((rc = lvl.ensure(4)) || (rc = cnum.ensure(8)) || (rc = coff.ensure(8 * nc)) ||
-        (rc = qbase.ensure(16)) || (rc = total.ensure(8)) || (rc = cand.ensure(4 * n)))
+    if ((rc = sc.ensure(nc * chunk)) || (rc = part.ensure(sizeof(int32_t) * nc * (n_sub + 1))) ||
+        (rc = hist.ensure(sizeof(int64_t) * (n_sub + 1))) || (rc = lvl.ensure(4)) || (rc = cnum.ensure(8)) ||
+        (rc = coff.ensure(8 * nc)) || (rc = qbase.ensure(8)) || (rc = clocal.ensure(8)) ||
+        (rc = flags.ensure(64)) || (rc = cand.ensure(4 * n)))
       break;
-    cudaMemset(sc.p, 0, nc * kChunk);
+    cudaMemset(sc.p, 0, nc * chunk);
+    cudaMemset(flags.p, 0, 64);
     cudaMemcpy(sc.p, scores_h, n, cudaMemcpyHostToDevice);
-    // scores above n_sub would index past the histogram: reject like bincount would overflow minlength
-    k_chunk_hist<<<dim3((unsigned)nc, 1), 256>>>(sc.as<uint8_t>(), n, nc, n_sub, part.as<int32_t>());
+    k_chunk_hist<<<(unsigned)nc, 256>>>(sc.as<uint8_t>(), n, nc, chunk, n_sub, part.as<int32_t>());
     count_launch();
     k_hist_reduce<<<1, 64>>>(part.as<int32_t>(), nc, n_sub, hist.as<int64_t>());
     count_launch();
-    k_select<<<1, 1024>>>(hist.as<int64_t>(), part.as<int32_t>(), 1, nc, n_sub, beta * (double)n,
-                          lvl.as<int32_t>(), cnum.as<int64_t>(), coff.as<int64_t>(),
-                          qbase.as<int64_t>(), total.as<int64_t>());
+    k_select<<<1, 32>>>(hist.as<int64_t>(), part.as<int32_t>(), 1, 0, nc, n_sub, beta * (double)n,
+                        coff.as<int64_t>(), n, flags.as<int64_t>(), qbase.as<int64_t>(), clocal.as<int64_t>(),
+                        cnum.as<int64_t>(), lvl.as<int32_t>());
     count_launch();
-    k_compact<<<dim3((unsigned)nc, 1), CMP_THREADS>>>(sc.as<uint8_t>(), n, nc, lvl.as<int32_t>(),
-                                                      coff.as<int64_t>(), qbase.as<int64_t>(),
-                                                      cand.as<uint32_t>());
+    k_compact<<<dim3((unsigned)nc, 1), CMP_THREADS>>>(sc.as<uint8_t>(), n, nc, chunk, 0, lvl.as<int32_t>(),
+                                                      coff.as<int64_t>(), qbase.as<int64_t>(), clocal.as<int64_t>(),
+                                                      n, cand.as<uint32_t>());
     count_launch();
-    int64_t tot = 0;
+    int64_t tot = 0, cn = 0;
     int32_t L = 0;
-    cudaMemcpy(&tot, total.p, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&tot, clocal.p, 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(&L, lvl.p, 4, cudaMemcpyDeviceToHost);
-    int64_t cn = 0;
     cudaMemcpy(&cn, cnum.p, 8, cudaMemcpyDeviceToHost);
-    std::vector<uint32_t> ids(tot);
+    std::vector<uint32_t> ids(std::max<int64_t>(tot, 1));
     cudaMemcpy(ids.data(), cand.p, 4 * tot, cudaMemcpyDeviceToHost);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
@@ -1155,7 +1493,8 @@ int taco_select_candidates(int device, const uint8_t* scores_h, int64_t n, int32
     *last_coll_h = L;
     if (tot != cn) { set_error("candidate count %lld != histogram count %lld", (long long)tot, (long long)cn); rc = TACO_ERR_NUMERIC; }
   } while (0);
-  cleanup();
+  sc.release(); part.release(); hist.release(); lvl.release(); cnum.release(); coff.release();
+  qbase.release(); clocal.release(); flags.release(); cand.release();
   return rc;
 }
 
@@ -1164,47 +1503,56 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
                 double* d2_out_h) {
   TACO_TRY(with_device(device));
   if (k < 1 || k > TK_MAX) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d outside [1, %d]", k, TK_MAX);
+  if (d > 4096) TACO_FAIL(TACO_ERR_PARAMETER, "dimension %d exceeds 4096", d);
   if (m < 0) TACO_FAIL(TACO_ERR_PARAMETER, "negative candidate count");
   if (m == 0) return TACO_OK;
   for (int64_t i = 0; i < m; ++i)
     if (ids_h[i] < 0 || ids_h[i] >= n || ids_h[i] > 0xFFFFFFFFll)
       TACO_FAIL(TACO_ERR_PARAMETER, "candidate id %lld out of range", (long long)ids_h[i]);
-  // candidates must be processed in ascending-id order for the position tie-break
   std::vector<uint32_t> c32(m);
   bool sorted = true;
   for (int64_t i = 0; i < m; ++i) {
     c32[i] = (uint32_t)ids_h[i];
     if (i && c32[i] < c32[i - 1]) sorted = false;
   }
-  if (!sorted) std::sort(c32.begin(), c32.end());
-  // gather the candidate rows on the host into a compact matrix (X may be huge)
+  if (!sorted) std::stable_sort(c32.begin(), c32.end());
   std::vector<float> rowsv((size_t)m * d);
   for (int64_t i = 0; i < m; ++i)
     std::copy(X_h + (size_t)c32[i] * d, X_h + (size_t)c32[i] * d + d, rowsv.begin() + (size_t)i * d);
-  DevBuf Xd, Qd, qb, cd, d2, tkd, tki, oi, od;
+  const int kk = std::min(k, RB);
+  const int64_t nb = ceil_div(m, RB);
+  DevBuf Xd, Qd, qb, cl, bp, cd, pk, pp, tkd, tki, fl;
   int rc = TACO_OK;
   do {
     if ((rc = Xd.ensure(sizeof(float) * rowsv.size())) || (rc = Qd.ensure(sizeof(float) * d)) ||
-        (rc = qb.ensure(16)) || (rc = cd.ensure(4 * m)) || (rc = d2.ensure(8 * m)) ||
-        (rc = tkd.ensure(8 * k)) || (rc = tki.ensure(8 * k)))
+        (rc = qb.ensure(8)) || (rc = cl.ensure(8)) || (rc = bp.ensure(16)) || (rc = cd.ensure(4 * m)) ||
+        (rc = pk.ensure(8 * nb * kk)) || (rc = pp.ensure(4 * nb * kk)) || (rc = tkd.ensure(8 * k)) ||
+        (rc = tki.ensure(8 * k)) || (rc = fl.ensure(64)))
       break;
     std::vector<uint32_t> local(m);
     for (int64_t i = 0; i < m; ++i) local[i] = (uint32_t)i;
-    int64_t qbh[2] = {0, m};
+    const int64_t zero = 0;
     cudaMemcpy(Xd.p, rowsv.data(), sizeof(float) * rowsv.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(Qd.p, q_h, sizeof(float) * d, cudaMemcpyHostToDevice);
-    cudaMemcpy(qb.p, qbh, 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(qb.p, &zero, 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(cl.p, &m, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
-    const unsigned g = (unsigned)ceil_div(m, RR_WARPS * 32);
-    if (d % 4 == 0)
-      k_rerank<true><<<g, RR_WARPS * 32>>>(Xd.as<float>(), d, Qd.as<float>(), 1, qb.as<int64_t>(),
-                                           cd.as<uint32_t>(), d2.as<double>());
-    else
-      k_rerank<false><<<g, RR_WARPS * 32>>>(Xd.as<float>(), d, Qd.as<float>(), 1, qb.as<int64_t>(),
-                                            cd.as<uint32_t>(), d2.as<double>());
+    k_rr_plan<<<1, 1024>>>(cl.as<int64_t>(), 1, bp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
-    k_topk<<<1, TK_THREADS>>>(d2.as<double>(), cd.as<uint32_t>(), qb.as<int64_t>(), k, 0,
-                              tkd.as<double>(), tki.as<int64_t>());
+    const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * d;
+    cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (d % 4 == 0)
+      k_rerank_topk<true><<<(unsigned)nb, RB, smem>>>(Xd.as<float>(), d, Qd.as<float>(), 1, bp.as<int64_t>(),
+                                                      qb.as<int64_t>(), cl.as<int64_t>(), cd.as<uint32_t>(), kk,
+                                                      pk.as<unsigned long long>(), pp.as<int>());
+    else
+      k_rerank_topk<false><<<(unsigned)nb, RB, smem>>>(Xd.as<float>(), d, Qd.as<float>(), 1, bp.as<int64_t>(),
+                                                       qb.as<int64_t>(), cl.as<int64_t>(), cd.as<uint32_t>(), kk,
+                                                       pk.as<unsigned long long>(), pp.as<int>());
+    count_launch();
+    k_topk<<<1, TK_THREADS>>>(pk.as<unsigned long long>(), pp.as<int>(), bp.as<int64_t>(), kk, qb.as<int64_t>(),
+                              cl.as<int64_t>(), cd.as<uint32_t>(), k, 0, tkd.as<double>(), tki.as<int64_t>());
     count_launch();
     std::vector<double> td(k);
     std::vector<int64_t> ti(k);
@@ -1212,14 +1560,15 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     cudaMemcpy(ti.data(), tki.p, 8 * k, cudaMemcpyDeviceToHost);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
-    const int kk = (int)std::min<int64_t>(k, m);
-    for (int r = 0; r < kk; ++r) {
+    const int kr = (int)std::min<int64_t>(k, m);
+    for (int r = 0; r < kr; ++r) {
       ids_out_h[r] = (int32_t)c32[ti[r]];
       d2_out_h[r] = td[r];
       dists_out_h[r] = (float)std::sqrt(td[r]);
     }
   } while (0);
-  Xd.release(); Qd.release(); qb.release(); cd.release(); d2.release(); tkd.release(); tki.release();
+  Xd.release(); Qd.release(); qb.release(); cl.release(); bp.release(); cd.release(); pk.release();
+  pp.release(); tkd.release(); tki.release(); fl.release();
   return rc;
 }
 
@@ -1280,12 +1629,12 @@ int taco_traverse(int device, int32_t kp, const double* d1s_h, const int32_t* l1
   TACO_TRY(with_device(device));
   if (kp < 1 || kp > 256) TACO_FAIL(TACO_ERR_PARAMETER, "codebook size %d out of range", kp);
   const int K2 = kp * kp;
-  DevBuf sd, sl, gs, pops, keys, np, ret;
+  DevBuf sd, sl, gs, pops, keys, np, ret, fl;
   int rc = TACO_OK;
   do {
     if ((rc = sd.ensure(16 * (size_t)kp)) || (rc = sl.ensure(4 * (size_t)kp)) || (rc = gs.ensure(8 * (size_t)K2)) ||
         (rc = pops.ensure(2 * (size_t)K2)) || (rc = keys.ensure(8 * (size_t)K2)) || (rc = np.ensure(4)) ||
-        (rc = ret.ensure(8)))
+        (rc = ret.ensure(8)) || (rc = fl.ensure(64)))
       break;
     std::vector<uint16_t> l(2 * kp);
     for (int i = 0; i < kp; ++i) { l[i] = (uint16_t)l1s_h[i]; l[kp + i] = (uint16_t)l2s_h[i]; }
@@ -1295,7 +1644,7 @@ int taco_traverse(int device, int32_t kp, const double* d1s_h, const int32_t* l1
     cudaMemcpy(gs.p, sizes_h, 8 * (size_t)K2, cudaMemcpyHostToDevice);
 #define TRAV1(KM) k_traverse<KM><<<1, 128>>>(sd.as<double>(), sl.as<uint16_t>(), gs.as<int64_t>(), 1, 1, kp, \
                                             target, pops.as<uint16_t>(), K2, keys.as<double>(),        \
-                                            np.as<int32_t>(), ret.as<int64_t>())
+                                            np.as<int32_t>(), ret.as<int64_t>(), fl.as<int64_t>())
     if (kp <= 32) TRAV1(32);
     else if (kp <= 64) TRAV1(64);
     else if (kp <= 128) TRAV1(128);
@@ -1313,6 +1662,7 @@ int taco_traverse(int device, int32_t kp, const double* d1s_h, const int32_t* l1
     *npop_h = n;
   } while (0);
   sd.release(); sl.release(); gs.release(); pops.release(); keys.release(); np.release(); ret.release();
+  fl.release();
   return rc;
 }
 
