@@ -1150,6 +1150,18 @@ static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t f
   return TACO_OK;
 }
 
+// dynamic smem of k_rerank_topk: staging rows + the query in fp64 (d <= 4096)
+static int set_rerank_attrs() {
+  static bool done = false;
+  if (!done) {
+    const int smem = (int)(sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * 4096);
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    done = true;
+  }
+  return TACO_OK;
+}
+
 static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t nblocks, cudaStream_t st) {
   QueryTile& t = idx->qt;
   const int kk = std::min(k, RB);
@@ -1157,12 +1169,7 @@ static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t nblocks, cud
   TACO_TRY(t.ppos.ensure(sizeof(int) * (size_t)std::max<int64_t>(nblocks, 1) * kk));
   if (nblocks > 0) {
     const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * idx->d;
-    static size_t attr_set = 0;
-    if (attr_set < smem) {
-      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set = smem;
-    }
+    TACO_TRY(set_rerank_attrs());
     ProfScope ps(K_RERANK, st);
     if (idx->d % 4 == 0)
       k_rerank_topk<true><<<(unsigned)nblocks, RB, smem, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS,
@@ -1540,8 +1547,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     k_rr_plan<<<1, 1024>>>(cl.as<int64_t>(), 1, bp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
     const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * d;
-    cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if ((rc = set_rerank_attrs())) break;
     if (d % 4 == 0)
       k_rerank_topk<true><<<(unsigned)nb, RB, smem>>>(Xd.as<float>(), d, Qd.as<float>(), 1, bp.as<int64_t>(),
                                                       qb.as<int64_t>(), cl.as<int64_t>(), cd.as<uint32_t>(), kk,
