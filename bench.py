@@ -135,7 +135,7 @@ def kernel_bytes(name, stats, meta):
     nch = stats.get("nchunks", 1)
     return {
         # candidate rows gathered + candidate ids read + per-CTA partial top-k
-        "k_rerank_topk": (4 * d + 4) * C,
+        "k_rerank": (4 * d + 4) * C,
         # ids of popped cells + CSR bounds per (cell, chunk) + pop lists + candidate ids
         # written (+ score tables through HBM in global mode)
         "k_count": 4 * R + (8 * nch + 2) * P + 4 * C + 2 * stats["score_bytes"],

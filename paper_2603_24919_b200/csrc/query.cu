@@ -14,11 +14,12 @@
 //   k_count           per (query, 64 Ki chunk) smem counting -> HBM tables +
 //                     per-chunk histograms;  k_hist_reduce -> (all-reduce across
 //                     ranks) -> k_select (Alg. 5) -> k_compact
-//   k_rr_plan         candidate blocks per query
-//   k_rerank_topk     fp64 exact distances of 256 candidates per CTA (rows
-//                     staged through smem) + CTA-local top-k       engine.py:272-275
-//   k_topk            final per-query top-k over the CTA partials (radix select
-//                     + bitonic sort on (d2, position == id order)) engine.py:275-279
+//   k_rr_plan         32-candidate tiles per candidate segment
+//   k_rerank_tma      persistent warp-specialised gather: cp.async.bulk (TMA
+//                     bulk copies) of candidate row segments into an mbarrier
+//                     ring, fp64 einsum-order distances, warp top-k  engine.py:272-275
+//   k_topk            final per-query top-k over the tile partials (radix select
+//                     on d2 bits then id, bitonic sort on (d2, id))  engine.py:275-279
 //   k_finalize        ids int32 / dists f32(sqrt(d2))              engine.py:276-279
 #include <cooperative_groups.h>
 
@@ -38,7 +39,7 @@ namespace taco {
 enum KId { K_TRANSFORM, K_CSORT, K_TRAVERSE, K_COUNT, K_HIST, K_SELECT, K_COMPACT, K_PLAN, K_RERANK,
            K_TOPK, K_FINAL, K_NKIDS };
 static const char* kKNames[K_NKIDS] = {"k_transform", "k_csort", "k_traverse", "k_count", "k_hist_reduce",
-                                       "k_select", "k_compact", "k_rr_plan", "k_rerank_topk", "k_topk",
+                                       "k_select", "k_compact", "k_rr_plan", "k_rerank", "k_topk",
                                        "k_finalize"};
 struct Prof {
   bool on = false;
@@ -235,50 +236,15 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
   return excl;
 }
 
-// ---------------------------------------------------------- level counting
-__device__ __forceinline__ void count_levels_words(const uint32_t* words, int nwords, int n_sub,
-                                                   int* cnt_sh) {
-  if (n_sub <= 15) {
-    int loc[16];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) loc[l] = 0;
-    for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
-      const uint32_t w = words[i];
-      if (w == 0) continue;
-#pragma unroll
-      for (int l = 1; l < 16; ++l) {
-        if (l > n_sub) break;
-        loc[l] += __popc(__vcmpeq4(w, 0x01010101u * (uint32_t)l) & 0x01010101u);
-      }
-    }
-#pragma unroll
-    for (int l = 1; l < 16; ++l) {
-      if (l > n_sub) break;
-      int v = loc[l];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt_sh[l], v);
-    }
-  } else {
-    for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
-      uint32_t w = words[i];
-      while (w) {
-        const int b = __ffs(w) - 1;
-        const int byte = b >> 3;
-        atomicAdd(&cnt_sh[(w >> (byte * 8)) & 0xFF], 1);
-        w &= ~(0xFFu << (byte * 8));
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------ chunk counting
 // Counts into `table` (ids [base, base+chunk)) every id of the cells popped for
 // query q in subspaces 0..n_sub-1.  Slices of all subspaces are staged PB at a
 // time (phase A: one round trip for their CSR bounds); ids are then gathered
 // E per thread with independent loads (phase B) and applied subspace by
 // subspace with a barrier in between: ids are unique inside one subspace, so
-// the byte increments need no atomics.
+// the byte increments need no atomics.  Every increment from level v to v+1 is
+// tallied (packed 16-bit counters), which yields the level histogram without
+// rescanning the table: #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
 constexpr int CT_PB = 2 * CT_THREADS;
 constexpr int CT_E = 16;
@@ -289,7 +255,8 @@ struct CountSmem {
   uint8_t sj[CT_PB];
   uint32_t wtot[CT_THREADS / 32];
   int jpref[257];
-  int lh[256];
+  int ge[257];      // ge[l] = #ids of the chunk with score >= l  (l >= 1)
+  int lh[256];      // level histogram (lh[0] = ids at score 0)
 };
 
 __device__ __forceinline__ int slice_of(const uint32_t* pref, int nb, uint32_t f) {
@@ -306,6 +273,8 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
                             int64_t base, uint8_t* table, CountSmem& S) {
   const int tid = threadIdx.x;
+  const bool track = n_sub <= 16;
+  uint64_t lv0 = 0, lv1 = 0, lv2 = 0, lv3 = 0;   // packed per-level increment tallies
   if (tid == 0) {
     int acc = 0;
     for (int j = 0; j < n_sub; ++j) {
@@ -373,47 +342,122 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       const int jhi = S.sj[slice_of(S.pref, nb, r1 - 1)];
       for (int j = jlo; j <= jhi; ++j) {
 #pragma unroll
-        for (int e = 0; e < CT_E; ++e)
-          if (e < cntv && jv[e] == (uint32_t)j) table[idv[e] - (uint32_t)base] += 1;
+        for (int e = 0; e < CT_E; ++e) {
+          if (e < cntv && jv[e] == (uint32_t)j) {
+            uint8_t* p = table + (idv[e] - (uint32_t)base);
+            const uint32_t old = *p;
+            *p = (uint8_t)(old + 1);
+            const uint64_t inc = 1ull << ((old & 3u) << 4);
+            const uint32_t w = old >> 2;
+            lv0 += w == 0 ? inc : 0ull;
+            lv1 += w == 1 ? inc : 0ull;
+            lv2 += w == 2 ? inc : 0ull;
+            lv3 += w == 3 ? inc : 0ull;
+          }
+        }
         __syncthreads();
       }
     }
     __syncthreads();
   }
+  // ge[l] = #increments that left level l-1 (per-thread tallies <= 2^16 - 1:
+  // a thread applies at most CT_E ids per round and rounds are few)
+  for (int i = tid; i < 257; i += CT_THREADS) S.ge[i] = 0;
+  __syncthreads();
+  if (track) {
+    uint64_t v[4] = {lv0, lv1, lv2, lv3};
+#pragma unroll
+    for (int wv = 0; wv < 4; ++wv) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        int x = (int)((v[wv] >> (16 * s)) & 0xFFFFull);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        const int l = wv * 4 + s + 1;
+        if ((tid & 31) == 0 && x && l <= n_sub) atomicAdd(&S.ge[l], x);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Level histogram of a chunk table.  n_sub <= 16: from the tallies; else by a
+// scan of the table (atomics per nonzero byte).
+__device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSmem& S) {
+  const int tid = threadIdx.x;
+  if (n_sub <= 16) {
+    for (int l = tid; l <= n_sub; l += blockDim.x) {
+      const int gl = l == 0 ? valid : S.ge[l];
+      const int gn = l == n_sub ? 0 : S.ge[l + 1];
+      S.lh[l] = gl - gn;
+    }
+  } else {
+    for (int l = tid; l < 256; l += blockDim.x) S.lh[l] = 0;
+    __syncthreads();
+    const uint32_t* w4 = reinterpret_cast<const uint32_t*>(table);
+    for (int i = tid; i < (valid + 3) / 4; i += blockDim.x) {
+      uint32_t w = w4[i];
+      while (w) {
+        const int b = __ffs(w) - 1;
+        const int byte = b >> 3;
+        atomicAdd(&S.lh[(w >> (byte * 8)) & 0xFF], 1);
+        w &= ~(0xFFu << (byte * 8));
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int nz = 0;
+      for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
+      S.lh[0] = valid - nz;
+    }
+  }
+  __syncthreads();
 }
 
 // Ordered compaction of ids (id0 + position) whose score >= L from a table of
-// `valid` bytes (16-byte aligned, zero padded to a multiple of 16).
+// `valid` bytes (16-byte aligned, zero padded): every thread owns a contiguous
+// run of 16-byte vectors, one block scan places the runs.
 template <int NT>
 __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                               uint32_t* wtot) {
   const uint32_t Lrep = 0x01010101u * L;
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
-  uint32_t run = 0;
-  for (int r0 = 0; r0 < valid; r0 += NT * 16) {
-    const int p0 = r0 + threadIdx.x * 16;
-    uint32_t mask = 0;
-    if (p0 < valid) {
-      const uint4 v = t4[p0 >> 4];
-      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+  const int nvec = (valid + 15) >> 4;
+  const int per = (nvec + NT - 1) / NT;          // vectors per thread (<= 16 for chunks <= 128 Ki)
+  const int v0 = threadIdx.x * per, v1 = min(nvec, v0 + per);
+  uint32_t cnt = 0;
+  uint32_t hit = 0;                              // which of my vectors hold matches (first 32)
+  for (int i = 0; i < v1 - v0; ++i) {
+    const int vi = v0 + (i + threadIdx.x) % max(v1 - v0, 1);   // rotated: bank-conflict free
+    const uint4 v = t4[vi];
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+    uint32_t c = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t ge = __vcmpgeu4(ws[u], Lrep);
+    for (int u = 0; u < 4; ++u) c += __popc(__vcmpgeu4(ws[u], Lrep) & 0x01010101u);
+    const int p0 = vi << 4;
+    if (valid - p0 < 16) {                       // tail vector: drop padding bytes
+      c = 0;
+      for (int bb = 0; bb < valid - p0; ++bb) c += tab[p0 + bb] >= L;
+    }
+    cnt += c;
+    if (c && vi - v0 < 32) hit |= 1u << (vi - v0);
+  }
+  uint32_t tot;
+  uint32_t pos = block_excl_scan<NT>(cnt, wtot, tot);
+  for (int i = 0; i < v1 - v0; ++i) {
+    if (i < 32 && !((hit >> i) & 1u)) continue;
+    const int vi = v0 + i;
+    const int p0 = vi << 4;
+    const int lim = min(16, valid - p0);
+    const uint4 v = t4[vi];
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if ((ge >> (8 * b)) & 1u) mask |= 1u << (u * 4 + b);
-      }
-      const int lim = valid - p0;
-      if (lim < 16) mask &= (1u << lim) - 1u;
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t ge = __vcmpgeu4(ws[u], Lrep);
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb)
+        if (((ge >> (8 * bb)) & 1u) && u * 4 + bb < lim) dst[pos++] = (uint32_t)(id0 + p0 + u * 4 + bb);
     }
-    uint32_t tot;
-    uint32_t pos = run + block_excl_scan<NT>((uint32_t)__popc(mask), wtot, tot);
-    while (mask) {
-      const int b = __ffs(mask) - 1;
-      dst[pos++] = (uint32_t)(id0 + p0 + b);
-      mask &= mask - 1u;
-    }
-    run += tot;
   }
 }
 
@@ -431,16 +475,18 @@ __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& 
 }
 
 // ------------------------------------------------- cluster-fused count/select
+// Candidates of a query live in per-CTA segments (segment q*S + rank); the
+// final top-k breaks distance ties by id, so segment order is irrelevant.
 __global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
-    int64_t* __restrict__ flags, int64_t* __restrict__ qbase, int64_t* __restrict__ clocal,
+    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
     int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
   extern __shared__ __align__(16) uint8_t table[];
   __shared__ CountSmem S;
   __shared__ int s_L;
-  __shared__ int64_t s_cand, s_off, s_base;
+  __shared__ int64_t s_base, s_cnt;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int csz = (int)cluster.num_blocks();
@@ -451,16 +497,9 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
   uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 256; i += CT_THREADS) S.lh[i] = 0;
   __syncthreads();
   count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
-  count_levels_words(reinterpret_cast<const uint32_t*>(table), (valid + 3) / 4, n_sub, S.lh);
-  __syncthreads();
-  if (tid == 0) {
-    int nz = 0;
-    for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
-    S.lh[0] = valid - nz;
-  }
+  chunk_levels(table, valid, n_sub, S);
   cluster.sync();
   if (tid == 0) {
     int* rl[kClusterMaxCtas];
@@ -471,28 +510,23 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
       for (int r = 0; r < csz; ++r) h += rl[r][l];
       return h;
     }, n_sub, budget, cands);
-    int64_t off = 0;
-    for (int r = 0; r < rank; ++r)
-      for (int l = L; l <= n_sub; ++l) off += rl[r][l];
+    int64_t mine = 0;
+    for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
+    const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
+    if (b + mine > cand_cap) flags[1] = 1;
     s_L = L;
-    s_cand = cands;
-    s_off = off;
+    s_base = b;
+    s_cnt = mine;
+    sbase[q * csz + rank] = b;
+    scnt[q * csz + rank] = mine;
     if (rank == 0) {
-      const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)cands);
-      s_base = b;
-      if (b + cands > cand_cap) flags[1] = 1;
-      qbase[q] = b;
-      clocal[q] = cands;
       cnum[q] = cands;
       lvl[q] = L;
     }
   }
-  cluster.sync();
-  if (tid == 0 && rank != 0) s_base = *cluster.map_shared_rank(&s_base, 0);
-  cluster.sync();
-  const int64_t b = s_base;
-  if (b + s_cand > cand_cap) return;
-  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + b + s_off, S.wtot);
+  cluster.sync();   // remote histograms no longer needed by anyone after this point
+  if (s_base + s_cnt > cand_cap) return;
+  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
 }
 
 // ------------------------------------------------------- global-mode count
@@ -510,41 +544,45 @@ __global__ void __launch_bounds__(CT_THREADS) k_count(
   const int valid = (int)min(chunk, n - base);
   uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 256; i += CT_THREADS) S.lh[i] = 0;
   __syncthreads();
   count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
   uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)qt * nchunks + c) * chunk);
   for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
-  count_levels_words(reinterpret_cast<const uint32_t*>(table), (valid + 3) / 4, n_sub, S.lh);
-  __syncthreads();
+  chunk_levels(table, valid, n_sub, S);
   int32_t* pp = part + ((size_t)qt * nchunks + c) * (n_sub + 1);
-  if (tid == 0) {
-    int nz = 0;
-    for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
-    pp[0] = valid - nz;
-  }
-  for (int l = 1 + tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
+  for (int l = tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
 }
 
 // Level histograms of externally provided score chunks (select_candidates tap).
-__global__ void k_chunk_hist(const uint8_t* __restrict__ scores, int64_t n, int64_t nchunks, int64_t chunk,
-                             int n_sub, int32_t* __restrict__ part) {
-  __shared__ int cnt_sh[256];
+__global__ void __launch_bounds__(CT_THREADS) k_chunk_hist(const uint8_t* __restrict__ scores, int64_t n,
+                                                           int64_t nchunks, int64_t chunk, int n_sub,
+                                                           int32_t* __restrict__ part) {
+  __shared__ CountSmem S;
   const int64_t c = blockIdx.x;
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt_sh[i] = 0;
-  __syncthreads();
   const int64_t base = c * chunk;
   const int valid = (int)min(chunk, n - base);
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(scores + (size_t)c * chunk);
-  count_levels_words(w, (valid + 3) / 4, n_sub, cnt_sh);
+  const uint8_t* tab = scores + (size_t)c * chunk;
+  // force the scan path (no tallies here)
+  for (int l = threadIdx.x; l < 256; l += blockDim.x) S.lh[l] = 0;
+  __syncthreads();
+  const uint32_t* w4 = reinterpret_cast<const uint32_t*>(tab);
+  for (int i = threadIdx.x; i < (valid + 3) / 4; i += blockDim.x) {
+    uint32_t w = w4[i];
+    while (w) {
+      const int b = __ffs(w) - 1;
+      const int byte = b >> 3;
+      atomicAdd(&S.lh[(w >> (byte * 8)) & 0xFF], 1);
+      w &= ~(0xFFu << (byte * 8));
+    }
+  }
   __syncthreads();
   int32_t* pp = part + (size_t)c * (n_sub + 1);
   if (threadIdx.x == 0) {
     int nz = 0;
-    for (int l = 1; l <= n_sub; ++l) nz += cnt_sh[l];
+    for (int l = 1; l <= n_sub; ++l) nz += S.lh[l];
     pp[0] = valid - nz;
   }
-  for (int l = 1 + threadIdx.x; l <= n_sub; l += blockDim.x) pp[l] = cnt_sh[l];
+  for (int l = 1 + threadIdx.x; l <= n_sub; l += blockDim.x) pp[l] = S.lh[l];
 }
 
 __global__ void k_hist_reduce(const int32_t* __restrict__ part, int64_t nchunks, int n_sub,
@@ -558,12 +596,12 @@ __global__ void k_hist_reduce(const int32_t* __restrict__ part, int64_t nchunks,
 }
 
 // Global mode: one thread per query of the tile.  Alg. 5 on the (global)
-// histogram, local candidate offsets per chunk, space reserved in the
-// super-tile candidate buffer through the cursor flags[3].
+// histogram, local candidate offsets per chunk, one segment per query reserved
+// in the super-tile candidate buffer through the cursor flags[3].
 __global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __restrict__ part, int Q,
                          int64_t q0, int64_t nchunks, int n_sub, double budget,
                          int64_t* __restrict__ coff, int64_t cand_cap, int64_t* __restrict__ flags,
-                         int64_t* __restrict__ qbase, int64_t* __restrict__ clocal,
+                         int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
                          int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
   const int qt = blockIdx.x * blockDim.x + threadIdx.x;
   if (qt >= Q) return;
@@ -581,8 +619,8 @@ __global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __res
   const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)local);
   if (b + local > cand_cap) flags[1] = 1;
   const int64_t q = q0 + qt;
-  qbase[q] = b;
-  clocal[q] = local;
+  sbase[q] = b;
+  scnt[q] = local;
   cnum[q] = cands;
   lvl[q] = L;
 }
@@ -592,15 +630,15 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
                                                           int64_t nchunks, int64_t chunk, int64_t q0,
                                                           const int32_t* __restrict__ lvl,
                                                           const int64_t* __restrict__ coff,
-                                                          const int64_t* __restrict__ qbase,
-                                                          const int64_t* __restrict__ clocal,
+                                                          const int64_t* __restrict__ sbase,
+                                                          const int64_t* __restrict__ scnt,
                                                           int64_t cand_cap,
                                                           uint32_t* __restrict__ cand) {
   __shared__ uint32_t wtot[CMP_THREADS / 32];
   const int64_t c = blockIdx.x;
   const int64_t qt = blockIdx.y, q = q0 + qt;
-  const int64_t b = qbase[q];
-  if (b + clocal[q] > cand_cap) return;
+  const int64_t b = sbase[q];
+  if (b + scnt[q] > cand_cap) return;
   const int64_t base = c * chunk;
   const int valid = (int)min(chunk, n - base);
   compact_table<CMP_THREADS>(scores + ((size_t)qt * nchunks + c) * chunk, valid, (uint32_t)lvl[q], base,
@@ -608,15 +646,16 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
 }
 
 // ------------------------------------------------------------ rerank plan
-constexpr int RB = 256;   // candidates per rerank CTA
-__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ clocal, int64_t Q,
-                                                  int64_t* __restrict__ bpref, int64_t* __restrict__ flags) {
+constexpr int GR = 32;    // candidate rows per rerank tile (one warp: lane = row)
+// tiles per segment -> exclusive prefix tpref[0..nseg], total in flags[2]
+__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ scnt, int64_t nseg,
+                                                  int64_t* __restrict__ tpref, int64_t* __restrict__ flags) {
   __shared__ int64_t wsum[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t per = (Q + 1023) / 1024;
-  const int64_t a0 = threadIdx.x * per, a1 = min(Q, a0 + per);
+  const int64_t per = (nseg + 1023) / 1024;
+  const int64_t a0 = threadIdx.x * per, a1 = min(nseg, a0 + per);
   int64_t loc = 0;
-  for (int64_t q = a0; q < a1; ++q) loc += (clocal[q] + RB - 1) / RB;
+  for (int64_t s = a0; s < a1; ++s) loc += (scnt[s] + GR - 1) / GR;
   int64_t v = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -636,165 +675,261 @@ __global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ cl
   }
   __syncthreads();
   int64_t run = (wid ? wsum[wid - 1] : 0) + v - loc;
-  for (int64_t q = a0; q < a1; ++q) {
-    bpref[q] = run;
-    run += (clocal[q] + RB - 1) / RB;
+  for (int64_t s = a0; s < a1; ++s) {
+    tpref[s] = run;
+    run += (scnt[s] + GR - 1) / GR;
   }
   if (threadIdx.x == 1023) {
-    bpref[Q] = run;
+    tpref[nseg] = run;
     flags[2] = run;
   }
 }
 
-// ------------------------------------------------------------ rerank + top-k
-// One CTA = 256 candidates of one query.  Each warp stages its 32 rows
-// through shared memory 64 dims at a time (coalesced 16-byte loads of whole
-// row segments), lane l folds row l into numpy's two einsum lanes (engine.py
-// :272-274) against the query held in shared memory as fp64; then the CTA
-// sorts its (d2, position) pairs and keeps the first min(k, 256).
-constexpr int RR_WARPS = RB / 32;
-constexpr int RR_SEG = 64;
-constexpr int RR_PITCH = RR_SEG + 4;
-
-__device__ __forceinline__ void bitonic_pairs(unsigned long long* key, int* pos, int P) {
-  for (int size = 2; size <= P; size <<= 1) {
+// ---------------------------------------------------- warp top-k helpers
+// warp-wide bitonic sort of one (key, id) pair per lane, ascending.
+__device__ __forceinline__ void warp_sort_pairs(unsigned long long& key, uint32_t& id) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int jx = i ^ stride;
-        if (jx > i) {
-          const bool up = (i & size) == 0;
-          const unsigned long long ka = key[i], kb = key[jx];
-          const int pa = pos[i], pb = pos[jx];
-          const bool gt = ka > kb || (ka == kb && pa > pb);
-          if (gt == up) {
-            key[i] = kb; key[jx] = ka;
-            pos[i] = pb; pos[jx] = pa;
-          }
-        }
-      }
-      __syncthreads();
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, stride);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
+      const bool up = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      const bool other_less = ok < key || (ok == key && oi < id);
+      // lower lane keeps the min when sorting up
+      const bool take = (lower == up) ? other_less : !other_less && !(ok == key && oi == id);
+      if (take) { key = ok; id = oi; }
     }
   }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(RB) k_rerank_topk(const float* __restrict__ X, int d,
-                                                    const float* __restrict__ Qf, int64_t Q,
-                                                    const int64_t* __restrict__ bpref,
-                                                    const int64_t* __restrict__ qbase,
-                                                    const int64_t* __restrict__ clocal,
-                                                    const uint32_t* __restrict__ cand, int kk,
-                                                    unsigned long long* __restrict__ pkey,
-                                                    int* __restrict__ ppos) {
-  extern __shared__ __align__(16) unsigned char rsm[];
-  float(*rows)[32][RR_PITCH] = reinterpret_cast<float(*)[32][RR_PITCH]>(rsm);
-  double* qv = reinterpret_cast<double*>(rsm + sizeof(float) * RR_WARPS * 32 * RR_PITCH);
-  __shared__ unsigned long long skey[RB];
-  __shared__ int spos[RB];
-  __shared__ uint32_t wcid[RR_WARPS][32];
-  const int64_t b = blockIdx.x;
-  int lo = 0, hi = (int)Q;  // largest q with bpref[q] <= b
+__device__ __forceinline__ int64_t tile_segment(const int64_t* tpref, int64_t nseg, int64_t tile) {
+  int64_t lo = 0, hi = nseg;  // largest s with tpref[s] <= tile
   while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (bpref[mid] <= b) lo = mid; else hi = mid;
+    const int64_t mid = (lo + hi) >> 1;
+    if (tpref[mid] <= tile) lo = mid; else hi = mid;
   }
-  const int64_t q = lo;
-  const int64_t off = (b - bpref[q]) * RB;
-  const int m = (int)min((int64_t)RB, clocal[q] - off);
-  const uint32_t* cq = cand + qbase[q] + off;
-  for (int t = threadIdx.x; t < d; t += RB) qv[t] = (double)Qf[q * d + t];
+  return lo;
+}
+
+// fold 8 products of a block into numpy's two einsum lanes (engine.py:273)
+__device__ __forceinline__ void einsum_block8(const float* xv, const float* qv8, double& a0, double& a1) {
+  double p[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const double e = __dsub_rn((double)xv[t], (double)qv8[t]);
+    p[t] = __dmul_rn(e, e);
+  }
+  a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
+  a0 = __dadd_rn(p[4], a0); a1 = __dadd_rn(p[5], a1);
+  a0 = __dadd_rn(p[2], a0); a1 = __dadd_rn(p[3], a1);
+  a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
+}
+
+// ------------------------------------------ rerank: TMA bulk-copy gather
+// Persistent, warp-specialised (one producer warp, RW consumer warps).  Work
+// unit = (tile of 32 candidate rows, 128-dim segment).  The producer warp's
+// lane r issues cp.async.bulk for row r's segment (plus lane 0 the query
+// segment) into a ring of RS shared-memory stages guarded by full/empty
+// mbarriers; consumer lane r folds row r into the einsum lanes.  After the last
+// segment the warp sorts its 32 (d2, id) pairs and emits the first min(k,32).
+constexpr int RSEG = 128;
+constexpr int RPITCH = RSEG + 4;       // 528 B rows: float4 reads are bank-conflict free
+constexpr int RS = 8;                  // stages
+constexpr int RW = 4;                  // consumer warps
+struct RStage {
+  float rows[GR][RPITCH];
+  float q[RSEG];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }\n" ::"r"(smem_u32(b)), "r"(parity));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
+    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int64_t* __restrict__ tpref,
+    int64_t nseg, int S, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
+    const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
+    uint32_t* __restrict__ pid) {
+  extern __shared__ __align__(128) unsigned char rsm[];
+  RStage* stg = reinterpret_cast<RStage*>(rsm);
+  __shared__ __align__(8) uint64_t full[RS], empty[RS];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = wid * 32 + lane;
-  wcid[wid][lane] = r < m ? cq[r] : cq[0];
+  const int nsg = (d + RSEG - 1) / RSEG;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
   __syncthreads();
+  if (wid == 0) {
+    // ---------------- producer warp
+    int64_t u = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t sg = tile_segment(tpref, nseg, tile);
+      const int64_t off = (tile - tpref[sg]) * GR;
+      const int m = (int)min((int64_t)GR, scnt[sg] - off);
+      const int64_t q = sg / S;
+      const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0u;
+      for (int g = 0; g < nsg; ++g, ++u) {
+        const int slot = (int)(u % RS);
+        const uint32_t par = (uint32_t)((u / RS) & 1);
+        const int s0 = g * RSEG;
+        const int len = min(RSEG, d - s0);
+        if (lane == 0) {
+          mbar_wait(&empty[slot], par ^ 1u);
+          mbar_expect_tx(&full[slot], (uint32_t)((m + 1) * len * 4));
+        }
+        __syncwarp();
+        if (lane < m) bulk_g2s(stg[slot].rows[lane], X + (size_t)cid * d + s0, (uint32_t)(len * 4), &full[slot]);
+        if (lane == 0) bulk_g2s(stg[slot].q, Qf + (size_t)q * d + s0, (uint32_t)(len * 4), &full[slot]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- consumer warps
+    const int cw = wid - 1;
+    int64_t i = 0;
+    for (int64_t tile = blockIdx.x + (int64_t)cw * gridDim.x; tile < ntiles;
+         tile += (int64_t)RW * gridDim.x, i += RW) {
+      const int64_t sg = tile_segment(tpref, nseg, tile);
+      const int64_t off = (tile - tpref[sg]) * GR;
+      const int m = (int)min((int64_t)GR, scnt[sg] - off);
+      const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0xFFFFFFFFu;
+      double a0 = 0.0, a1 = 0.0;
+      const int64_t ubase = (i + cw) * nsg;
+      for (int g = 0; g < nsg; ++g) {
+        const int64_t u = ubase + g;
+        const int slot = (int)(u % RS);
+        mbar_wait(&full[slot], (uint32_t)((u / RS) & 1));
+        const float* row = stg[slot].rows[lane];
+        const float* qv = stg[slot].q;
+        const int s0 = g * RSEG;
+        const int len = min(RSEG, d - s0);
+        const bool last = g == nsg - 1;
+        const int full8 = last ? (len & ~7) : len;
+        for (int b = 0; b < full8; b += 8) {
+          const float4 x0 = *reinterpret_cast<const float4*>(row + b);
+          const float4 x1 = *reinterpret_cast<const float4*>(row + b + 4);
+          const float4 q0 = *reinterpret_cast<const float4*>(qv + b);
+          const float4 q1 = *reinterpret_cast<const float4*>(qv + b + 4);
+          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          const float q8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          einsum_block8(xv, q8, a0, a1);
+        }
+        if (last) {
+          for (int b = full8; b < len; b += 2) {
+            const double e0 = __dsub_rn((double)row[b], (double)qv[b]);
+            a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
+            if (b + 1 < len) {
+              const double e1 = __dsub_rn((double)row[b + 1], (double)qv[b + 1]);
+              a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+      double v = __dadd_rn(a0, a1);
+      v = v >= 0.0 ? v : 0.0;
+      unsigned long long key = lane < m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+      uint32_t id = cid;
+      warp_sort_pairs(key, id);
+      if (lane < kk) {
+        pkey[tile * kk + lane] = key;
+        pid[tile * kk + lane] = id;
+      }
+    }
+  }
+}
+
+// Generic rerank for d % 4 != 0: lane = row, direct loads.
+__global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ X, int d,
+                                                      const float* __restrict__ Qf,
+                                                      const int64_t* __restrict__ tpref, int64_t nseg, int S,
+                                                      const int64_t* __restrict__ sbase,
+                                                      const int64_t* __restrict__ scnt,
+                                                      const uint32_t* __restrict__ cand, int64_t ntiles, int kk,
+                                                      unsigned long long* __restrict__ pkey,
+                                                      uint32_t* __restrict__ pid) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (tile >= ntiles) return;
+  const int64_t sg = tile_segment(tpref, nseg, tile);
+  const int64_t off = (tile - tpref[sg]) * GR;
+  const int m = (int)min((int64_t)GR, scnt[sg] - off);
+  const int64_t q = sg / S;
+  const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0xFFFFFFFFu;
+  const float* row = X + (size_t)(lane < m ? cid : 0u) * d;
+  const float* qv = Qf + (size_t)q * d;
   double a0 = 0.0, a1 = 0.0;
-  float(*R)[RR_PITCH] = rows[wid];
-  const bool wlive = wid * 32 < m;
-  if (wlive) {
-    for (int seg = 0; seg < d; seg += RR_SEG) {
-      const int len = min(RR_SEG, d - seg);
-      if (VEC) {
-        const int nv = len >> 2;
-#pragma unroll 4
-        for (int e = lane; e < 32 * (RR_SEG / 4); e += 32) {
-          const int rr = e / (RR_SEG / 4), v = e % (RR_SEG / 4);
-          if (v < nv) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)wcid[wid][rr] * d + seg) + v);
-            *reinterpret_cast<float4*>(&R[rr][v * 4]) = x;
-          }
-        }
-      } else {
-        for (int e = lane; e < 32 * RR_SEG; e += 32) {
-          const int rr = e / RR_SEG, v = e % RR_SEG;
-          if (v < len) R[rr][v] = __ldg(X + (size_t)wcid[wid][rr] * d + seg + v);
-        }
-      }
-      __syncwarp();
-      const bool last = seg + RR_SEG >= d;
-      const int full = last ? (len & ~7) : len;
-      for (int bb = 0; bb < full; bb += 8) {
-        float xv[8];
-        if (VEC) {
-          const float4 u = *reinterpret_cast<const float4*>(&R[lane][bb]);
-          const float4 w = *reinterpret_cast<const float4*>(&R[lane][bb + 4]);
-          xv[0] = u.x; xv[1] = u.y; xv[2] = u.z; xv[3] = u.w;
-          xv[4] = w.x; xv[5] = w.y; xv[6] = w.z; xv[7] = w.w;
-        } else {
+  const int full8 = d & ~7;
+  for (int b = 0; b < full8; b += 8) {
+    float xv[8], q8[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) xv[t] = R[lane][bb + t];
-        }
-        double p[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const double e = __dsub_rn((double)xv[t], qv[seg + bb + t]);
-          p[t] = __dmul_rn(e, e);
-        }
-        a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
-        a0 = __dadd_rn(p[4], a0); a1 = __dadd_rn(p[5], a1);
-        a0 = __dadd_rn(p[2], a0); a1 = __dadd_rn(p[3], a1);
-        a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
-      }
-      if (last) {
-        for (int bb = full; bb < len; bb += 2) {
-          const double e0 = __dsub_rn((double)R[lane][bb], qv[seg + bb]);
-          a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
-          if (bb + 1 < len) {
-            const double e1 = __dsub_rn((double)R[lane][bb + 1], qv[seg + bb + 1]);
-            a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
-          }
-        }
-      }
-      __syncwarp();
+    for (int t = 0; t < 8; ++t) { xv[t] = row[b + t]; q8[t] = qv[b + t]; }
+    einsum_block8(xv, q8, a0, a1);
+  }
+  for (int b = full8; b < d; b += 2) {
+    const double e0 = __dsub_rn((double)row[b], (double)qv[b]);
+    a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
+    if (b + 1 < d) {
+      const double e1 = __dsub_rn((double)row[b + 1], (double)qv[b + 1]);
+      a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
     }
   }
   double v = __dadd_rn(a0, a1);
   v = v >= 0.0 ? v : 0.0;
-  skey[r] = r < m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
-  spos[r] = r < m ? (int)(off + r) : 0x7fffffff;
-  __syncthreads();
-  bitonic_pairs(skey, spos, RB);
-  for (int t = threadIdx.x; t < kk; t += RB) {
-    pkey[(size_t)b * kk + t] = skey[t];
-    ppos[(size_t)b * kk + t] = spos[t];
+  unsigned long long key = lane < m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+  uint32_t id = cid;
+  warp_sort_pairs(key, id);
+  if (lane < kk) {
+    pkey[tile * kk + lane] = key;
+    pid[tile * kk + lane] = id;
   }
 }
 
 // ------------------------------------------------------------------- top-k
-// One CTA per query over its CTA partial lists: radix select of the k-th
-// smallest (d2 bits, then position among exact d2 ties), then bitonic sort
-// of the kk survivors on (d2, position); writes d2 and global ids.
+// One CTA per query over its tiles' partial lists: radix select of the k-th
+// smallest d2 bits, then of the id among exact d2 ties (lower id wins,
+// engine.py:275), bitonic sort of the kk survivors on (d2, id).
 constexpr int TK_THREADS = 256;
 constexpr int TK_MAX = 2048;
 
-__device__ void radix_select_u64(const unsigned long long* keys, const int* pos, int64_t m, int kk,
-                                 bool by_pos, unsigned long long key_eq, unsigned long long& out,
-                                 int& remain, unsigned* hist, unsigned long long* s_pre, int* s_rem) {
-  // selects the kk-th smallest of (by_pos ? pos among key==key_eq : key)
+__device__ void radix_select(const unsigned long long* keys, const uint32_t* ids, int64_t m, int kk,
+                             bool by_id, unsigned long long key_eq, unsigned long long& out, int& remain,
+                             unsigned* hist, unsigned long long* s_pre, int* s_rem) {
   const int tid = threadIdx.x;
   if (tid == 0) { *s_pre = 0ull; *s_rem = kk; }
   __syncthreads();
   unsigned long long msk = 0ull;
-  const int passes = by_pos ? 4 : 8;
+  const int passes = by_id ? 4 : 8;
   for (int p = 0; p < passes; ++p) {
     const int shift = (passes - 1 - p) * 8;
     for (int i = tid; i < 256; i += TK_THREADS) hist[i] = 0;
@@ -802,9 +937,9 @@ __device__ void radix_select_u64(const unsigned long long* keys, const int* pos,
     const unsigned long long pre = *s_pre;
     for (int64_t i = tid; i < m; i += TK_THREADS) {
       unsigned long long v;
-      if (by_pos) {
+      if (by_id) {
         if (keys[i] != key_eq) continue;
-        v = (unsigned long long)(unsigned)pos[i];
+        v = (unsigned long long)ids[i];
       } else {
         v = keys[i];
       }
@@ -830,53 +965,74 @@ __device__ void radix_select_u64(const unsigned long long* keys, const int* pos,
   __syncthreads();
 }
 
+__device__ __forceinline__ void bitonic_pairs(unsigned long long* key, uint32_t* id, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool up = (i & size) == 0;
+          const unsigned long long ka = key[i], kb = key[jx];
+          const uint32_t pa = id[i], pb = id[jx];
+          const bool gt = ka > kb || (ka == kb && pa > pb);
+          if (gt == up) {
+            key[i] = kb; key[jx] = ka;
+            id[i] = pb; id[jx] = pa;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* __restrict__ pkey,
-                                                      const int* __restrict__ ppos,
-                                                      const int64_t* __restrict__ bpref, int kk_part,
-                                                      const int64_t* __restrict__ qbase,
-                                                      const int64_t* __restrict__ clocal,
-                                                      const uint32_t* __restrict__ cand, int k,
-                                                      int64_t id_base, double* __restrict__ out_d2,
+                                                      const uint32_t* __restrict__ pid,
+                                                      const int64_t* __restrict__ tpref, int S, int kk_part,
+                                                      const int64_t* __restrict__ scnt, int k, int64_t id_base,
+                                                      double* __restrict__ out_d2,
                                                       int64_t* __restrict__ out_ids) {
   __shared__ unsigned hist[256];
   __shared__ unsigned long long s_pre;
   __shared__ int s_rem, s_fill;
+  __shared__ int64_t s_ties, s_m;
   __shared__ unsigned long long skey[TK_MAX];
-  __shared__ int spos[TK_MAX];
+  __shared__ uint32_t sid[TK_MAX];
   const int64_t q = blockIdx.x;
-  const int64_t lo = bpref[q] * kk_part;
-  const int64_t m = (bpref[q + 1] - bpref[q]) * kk_part;
-  const int kk = (int)min((int64_t)k, clocal[q]);
-  const unsigned long long* keys = pkey + lo;
-  const int* pos = ppos + lo;
   const int tid = threadIdx.x;
-  if (tid == 0) s_fill = 0;
+  if (tid == 0) {
+    int64_t c = 0;
+    for (int r = 0; r < S; ++r) c += scnt[q * S + r];
+    s_m = c;
+    s_fill = 0;
+    s_ties = 0;
+  }
   __syncthreads();
+  const int64_t lo = tpref[q * S] * kk_part;
+  const int64_t m = (tpref[(q + 1) * S] - tpref[q * S]) * kk_part;
+  const int kk = (int)min((int64_t)k, s_m);
+  const unsigned long long* keys = pkey + lo;
+  const uint32_t* ids = pid + lo;
   if (kk > 0) {
     unsigned long long tau;
     int take;
-    radix_select_u64(keys, pos, m, kk, false, 0ull, tau, take, hist, &s_pre, &s_rem);
-    // among the exact ties at tau keep the `take` smallest positions
+    radix_select(keys, ids, m, kk, false, 0ull, tau, take, hist, &s_pre, &s_rem);
     int64_t nties = 0;
     for (int64_t i = tid; i < m; i += TK_THREADS) nties += keys[i] == tau;
     for (int o = 16; o > 0; o >>= 1) nties += __shfl_xor_sync(0xffffffffu, nties, o);
-    __shared__ int64_t s_ties;
-    if (tid == 0) s_ties = 0;
-    __syncthreads();
-    if ((tid & 31) == 0) atomicAdd((unsigned long long*)&s_ties, (unsigned long long)nties);
+    if ((tid & 31) == 0 && nties) atomicAdd((unsigned long long*)&s_ties, (unsigned long long)nties);
     __syncthreads();
     unsigned long long pi = ~0ull;
     if (s_ties > take) {
       int dummy;
-      radix_select_u64(keys, pos, m, take, true, tau, pi, dummy, hist, &s_pre, &s_rem);
+      radix_select(keys, ids, m, take, true, tau, pi, dummy, hist, &s_pre, &s_rem);
     }
     for (int64_t i = tid; i < m; i += TK_THREADS) {
       const unsigned long long kv = keys[i];
-      const bool sel = kv < tau || (kv == tau && (unsigned long long)(unsigned)pos[i] <= pi);
-      if (sel) {
+      if (kv < tau || (kv == tau && (unsigned long long)ids[i] <= pi)) {
         const int slot = atomicAdd(&s_fill, 1);
         skey[slot] = kv;
-        spos[slot] = pos[i];
+        sid[slot] = ids[i];
       }
     }
     __syncthreads();
@@ -885,15 +1041,14 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* _
   while (P < kk) P <<= 1;
   for (int i = kk + tid; i < P; i += TK_THREADS) {
     skey[i] = ~0ull;
-    spos[i] = 0x7fffffff;
+    sid[i] = 0xFFFFFFFFu;
   }
   __syncthreads();
-  bitonic_pairs(skey, spos, P);
-  const uint32_t* cq = cand + qbase[q];
+  bitonic_pairs(skey, sid, P);
   for (int r = tid; r < k; r += TK_THREADS) {
     if (r < kk) {
       out_d2[q * k + r] = __longlong_as_double((long long)skey[r]);
-      out_ids[q * k + r] = (int64_t)cq[spos[r]] + id_base;
+      out_ids[q * k + r] = (int64_t)sid[r] + id_base;
     } else {
       out_d2[q * k + r] = __longlong_as_double(0x7ff0000000000000LL);
       out_ids[q * k + r] = -1;
@@ -970,9 +1125,10 @@ static int ensure_front(taco_index* idx, int64_t QS, int k) {
   TACO_TRY(t.flags.ensure(sizeof(int64_t) * 8));
   TACO_TRY(t.lvl.ensure(sizeof(int32_t) * QS));
   TACO_TRY(t.cnum.ensure(sizeof(int64_t) * QS));
-  TACO_TRY(t.clocal.ensure(sizeof(int64_t) * QS));
-  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * QS));
-  TACO_TRY(t.bpref.ensure(sizeof(int64_t) * (QS + 1)));
+  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;   // candidate segments per query
+  TACO_TRY(t.clocal.ensure(sizeof(int64_t) * QS * S));
+  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * QS * S));
+  TACO_TRY(t.bpref.ensure(sizeof(int64_t) * (QS * S + 1)));
   TACO_TRY(t.tk_d2.ensure(sizeof(double) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.tk_ids.ensure(sizeof(int64_t) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)QS * std::max(k, 1)));
@@ -1096,7 +1252,7 @@ static int global_select_tile(taco_index* idx, int64_t q0, int Q, const int64_t*
                                                           idx->n_sub, budget, t.coff.as<int64_t>(), t.cand_cap,
                                                           t.flags.as<int64_t>(), t.qbase.as<int64_t>(),
                                                           t.clocal.as<int64_t>(), t.cnum.as<int64_t>(),
-                                                          t.lvl.as<int32_t>());
+                                                          t.lvl.as<int32_t>());  // qbase/clocal = segment base/count
     TACO_LAUNCHED();
   }
   {
@@ -1133,16 +1289,17 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
                                      (const uint32_t*)idx->offs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
                                      idx->nchunks, idx->chunk, budget, t.cand.as<uint32_t>(), t.cand_cap,
                                      t.flags.as<int64_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(),
-                                     t.cnum.as<int64_t>(), t.lvl.as<int32_t>()));
+                                     t.cnum.as<int64_t>(), t.lvl.as<int32_t>()));  // segment base/count per (q, rank)
   TACO_LAUNCHED();
   return TACO_OK;
 }
 
 static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t fl[4]) {
   QueryTile& t = idx->qt;
+  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   {
     ProfScope ps(K_PLAN, st);
-    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS, t.bpref.as<int64_t>(), t.flags.as<int64_t>());
+    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, t.bpref.as<int64_t>(), t.flags.as<int64_t>());
     TACO_LAUNCHED();
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
@@ -1150,48 +1307,64 @@ static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t f
   return TACO_OK;
 }
 
-// dynamic smem of k_rerank_topk: staging rows + the query in fp64 (d <= 4096)
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
 static int set_rerank_attrs() {
   static bool done = false;
   if (!done) {
-    const int smem = (int)(sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * 4096);
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_topk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(RStage) * RS)));
     done = true;
   }
   return TACO_OK;
 }
 
-static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t nblocks, cudaStream_t st) {
-  QueryTile& t = idx->qt;
-  const int kk = std::min(k, RB);
-  TACO_TRY(t.pd2.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(nblocks, 1) * kk));
-  TACO_TRY(t.ppos.ensure(sizeof(int) * (size_t)std::max<int64_t>(nblocks, 1) * kk));
-  if (nblocks > 0) {
-    const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * idx->d;
-    TACO_TRY(set_rerank_attrs());
+// rows of candidates -> CTA partial top-k -> per-query top-k (t.tk_d2 / t.tk_ids)
+static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64_t S, const int64_t* tpref,
+                       const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
+                       int64_t id_base, DevBuf& pkey, DevBuf& pid, double* out_d2, int64_t* out_ids,
+                       cudaStream_t st) {
+  const int kk = std::min(k, GR);
+  TACO_TRY(pkey.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
+  TACO_TRY(pid.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
+  if (ntiles > 0) {
     ProfScope ps(K_RERANK, st);
-    if (idx->d % 4 == 0)
-      k_rerank_topk<true><<<(unsigned)nblocks, RB, smem, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS,
-                                                               t.bpref.as<int64_t>(), t.qbase.as<int64_t>(),
-                                                               t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), kk,
-                                                               t.pd2.as<unsigned long long>(), t.ppos.as<int>());
-    else
-      k_rerank_topk<false><<<(unsigned)nblocks, RB, smem, st>>>(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS,
-                                                                t.bpref.as<int64_t>(), t.qbase.as<int64_t>(),
-                                                                t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), kk,
-                                                                t.pd2.as<unsigned long long>(), t.ppos.as<int>());
+    if (d % 4 == 0) {
+      TACO_TRY(set_rerank_attrs());
+      const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms());
+      k_rerank_tma<<<(unsigned)grid, 32 * (RW + 1), sizeof(RStage) * RS, st>>>(
+          X, d, Qf, tpref, QS * S, (int)S, sbase, scnt, cand, ntiles, kk, pkey.as<unsigned long long>(),
+          pid.as<uint32_t>());
+    } else {
+      k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, tpref, QS * S, (int)S, sbase, scnt,
+                                                                   cand, ntiles, kk, pkey.as<unsigned long long>(),
+                                                                   pid.as<uint32_t>());
+    }
     TACO_LAUNCHED();
   }
   {
     ProfScope ps(K_TOPK, st);
-    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(t.pd2.as<unsigned long long>(), t.ppos.as<int>(),
-                                                t.bpref.as<int64_t>(), kk, t.qbase.as<int64_t>(),
-                                                t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), k, idx->id_base,
-                                                t.tk_d2.as<double>(), t.tk_ids.as<int64_t>());
+    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tpref, (int)S,
+                                                kk, scnt, k, id_base, out_d2, out_ids);
     TACO_LAUNCHED();
   }
   return TACO_OK;
+}
+
+static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
+  QueryTile& t = idx->qt;
+  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
+  return rerank_core(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
+                     t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
+                     t.pd2, t.ppos, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
 }
 
 static void prof_stats(taco_index* idx, int64_t QS, int64_t total) {
@@ -1526,40 +1699,28 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
   std::vector<float> rowsv((size_t)m * d);
   for (int64_t i = 0; i < m; ++i)
     std::copy(X_h + (size_t)c32[i] * d, X_h + (size_t)c32[i] * d + d, rowsv.begin() + (size_t)i * d);
-  const int kk = std::min(k, RB);
-  const int64_t nb = ceil_div(m, RB);
-  DevBuf Xd, Qd, qb, cl, bp, cd, pk, pp, tkd, tki, fl;
+  const int64_t ntiles = ceil_div(m, GR);
+  DevBuf Xd, Qd, sb, sc, tp, cd, pk, pi, tkd, tki, fl;
   int rc = TACO_OK;
   do {
     if ((rc = Xd.ensure(sizeof(float) * rowsv.size())) || (rc = Qd.ensure(sizeof(float) * d)) ||
-        (rc = qb.ensure(8)) || (rc = cl.ensure(8)) || (rc = bp.ensure(16)) || (rc = cd.ensure(4 * m)) ||
-        (rc = pk.ensure(8 * nb * kk)) || (rc = pp.ensure(4 * nb * kk)) || (rc = tkd.ensure(8 * k)) ||
-        (rc = tki.ensure(8 * k)) || (rc = fl.ensure(64)))
+        (rc = sb.ensure(8)) || (rc = sc.ensure(8)) || (rc = tp.ensure(16)) || (rc = cd.ensure(4 * m)) ||
+        (rc = tkd.ensure(8 * k)) || (rc = tki.ensure(8 * k)) || (rc = fl.ensure(64)))
       break;
     std::vector<uint32_t> local(m);
     for (int64_t i = 0; i < m; ++i) local[i] = (uint32_t)i;
     const int64_t zero = 0;
     cudaMemcpy(Xd.p, rowsv.data(), sizeof(float) * rowsv.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(Qd.p, q_h, sizeof(float) * d, cudaMemcpyHostToDevice);
-    cudaMemcpy(qb.p, &zero, 8, cudaMemcpyHostToDevice);
-    cudaMemcpy(cl.p, &m, 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(sb.p, &zero, 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(sc.p, &m, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
-    k_rr_plan<<<1, 1024>>>(cl.as<int64_t>(), 1, bp.as<int64_t>(), fl.as<int64_t>());
+    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, tp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
-    const size_t smem = sizeof(float) * RR_WARPS * 32 * RR_PITCH + sizeof(double) * d;
-    if ((rc = set_rerank_attrs())) break;
-    if (d % 4 == 0)
-      k_rerank_topk<true><<<(unsigned)nb, RB, smem>>>(Xd.as<float>(), d, Qd.as<float>(), 1, bp.as<int64_t>(),
-                                                      qb.as<int64_t>(), cl.as<int64_t>(), cd.as<uint32_t>(), kk,
-                                                      pk.as<unsigned long long>(), pp.as<int>());
-    else
-      k_rerank_topk<false><<<(unsigned)nb, RB, smem>>>(Xd.as<float>(), d, Qd.as<float>(), 1, bp.as<int64_t>(),
-                                                       qb.as<int64_t>(), cl.as<int64_t>(), cd.as<uint32_t>(), kk,
-                                                       pk.as<unsigned long long>(), pp.as<int>());
-    count_launch();
-    k_topk<<<1, TK_THREADS>>>(pk.as<unsigned long long>(), pp.as<int>(), bp.as<int64_t>(), kk, qb.as<int64_t>(),
-                              cl.as<int64_t>(), cd.as<uint32_t>(), k, 0, tkd.as<double>(), tki.as<int64_t>());
-    count_launch();
+    if ((rc = rerank_core(Xd.as<float>(), d, Qd.as<float>(), 1, 1, tp.as<int64_t>(), sb.as<int64_t>(),
+                          sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, tkd.as<double>(),
+                          tki.as<int64_t>(), nullptr)))
+      break;
     std::vector<double> td(k);
     std::vector<int64_t> ti(k);
     cudaMemcpy(td.data(), tkd.p, 8 * k, cudaMemcpyDeviceToHost);
@@ -1573,8 +1734,8 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
       dists_out_h[r] = (float)std::sqrt(td[r]);
     }
   } while (0);
-  Xd.release(); Qd.release(); qb.release(); cl.release(); bp.release(); cd.release(); pk.release();
-  pp.release(); tkd.release(); tki.release(); fl.release();
+  Xd.release(); Qd.release(); sb.release(); sc.release(); tp.release(); cd.release(); pk.release();
+  pi.release(); tkd.release(); tki.release(); fl.release();
   return rc;
 }
 
