@@ -247,7 +247,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // rescanning the table: #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
 constexpr int CT_PB = 2 * CT_THREADS;
-constexpr int CT_E = 16;
+constexpr int CT_E = 32;
 
 struct CountSmem {
   uint32_t st[CT_PB];
@@ -322,17 +322,24 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       uint32_t f = r0 + per * tid;
       const uint32_t fe = min(r1, f + per);
       uint32_t idv[CT_E];
-      uint32_t jv[CT_E];
+      uint8_t jv[CT_E];
       int cntv = 0;
       if (f < fe) {
         int t = slice_of(S.pref, nb, f);
+        uint32_t nextb = S.pref[t + 1];
+        const uint32_t* src = ids + (size_t)S.sj[t] * n + S.st[t] - S.pref[t];
+        uint8_t jcur = S.sj[t];
 #pragma unroll
         for (int e = 0; e < CT_E; ++e) {
           if (f < fe) {
-            while (f >= S.pref[t + 1]) ++t;
-            const int j = S.sj[t];
-            idv[e] = __ldg(ids + (size_t)j * n + S.st[t] + (f - S.pref[t]));
-            jv[e] = (uint32_t)j;
+            while (f >= nextb) {
+              ++t;
+              nextb = S.pref[t + 1];
+              jcur = S.sj[t];
+              src = ids + (size_t)jcur * n + S.st[t] - S.pref[t];
+            }
+            idv[e] = __ldg(src + f);
+            jv[e] = jcur;
             ++f;
             cntv = e + 1;
           }
@@ -343,16 +350,15 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       for (int j = jlo; j <= jhi; ++j) {
 #pragma unroll
         for (int e = 0; e < CT_E; ++e) {
-          if (e < cntv && jv[e] == (uint32_t)j) {
+          if (e < cntv && jv[e] == (uint8_t)j) {
             uint8_t* p = table + (idv[e] - (uint32_t)base);
             const uint32_t old = *p;
             *p = (uint8_t)(old + 1);
             const uint64_t inc = 1ull << ((old & 3u) << 4);
-            const uint32_t w = old >> 2;
-            lv0 += w == 0 ? inc : 0ull;
-            lv1 += w == 1 ? inc : 0ull;
-            lv2 += w == 2 ? inc : 0ull;
-            lv3 += w == 3 ? inc : 0ull;
+            if (old < 4) lv0 += inc;
+            else if (old < 8) lv1 += inc;
+            else if (old < 12) lv2 += inc;
+            else lv3 += inc;
           }
         }
         __syncthreads();
@@ -417,46 +423,52 @@ __device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSm
 // Ordered compaction of ids (id0 + position) whose score >= L from a table of
 // `valid` bytes (16-byte aligned, zero padded): every thread owns a contiguous
 // run of 16-byte vectors, one block scan places the runs.
+// 16-bit mask of the bytes of v that are >= L (bit i = byte i).
+__device__ __forceinline__ uint32_t ge_mask16(const uint4 v, uint32_t Lrep) {
+  uint32_t m = 0;
+  const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x01010101u;   // bit 0 of each byte
+    g = (g | (g >> 7) | (g >> 14) | (g >> 21)) & 0xFu;     // compress to 4 bits
+    m |= g << (4 * u);
+  }
+  return m;
+}
+
 template <int NT>
 __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                               uint32_t* wtot) {
   const uint32_t Lrep = 0x01010101u * L;
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
   const int nvec = (valid + 15) >> 4;
-  const int per = (nvec + NT - 1) / NT;          // vectors per thread (<= 16 for chunks <= 128 Ki)
+  const int per = (nvec + NT - 1) / NT;          // vectors per thread
   const int v0 = threadIdx.x * per, v1 = min(nvec, v0 + per);
+  const int nv = max(v1 - v0, 0);
   uint32_t cnt = 0;
-  uint32_t hit = 0;                              // which of my vectors hold matches (first 32)
-  for (int i = 0; i < v1 - v0; ++i) {
-    const int vi = v0 + (i + threadIdx.x) % max(v1 - v0, 1);   // rotated: bank-conflict free
-    const uint4 v = t4[vi];
-    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-    uint32_t c = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) c += __popc(__vcmpgeu4(ws[u], Lrep) & 0x01010101u);
-    const int p0 = vi << 4;
-    if (valid - p0 < 16) {                       // tail vector: drop padding bytes
-      c = 0;
-      for (int bb = 0; bb < valid - p0; ++bb) c += tab[p0 + bb] >= L;
-    }
-    cnt += c;
-    if (c && vi - v0 < 32) hit |= 1u << (vi - v0);
+  uint32_t hit = 0;                              // which of my first 32 vectors hold matches
+  for (int i = 0; i < nv; ++i) {
+    const int vi = v0 + (i + threadIdx.x) % nv;  // rotated start: bank-conflict free
+    uint32_t m = ge_mask16(t4[vi], Lrep);
+    const int lim = valid - (vi << 4);
+    if (lim < 16) m &= (1u << lim) - 1u;
+    cnt += __popc(m);
+    if (m && vi - v0 < 32) hit |= 1u << (vi - v0);
+    if (m && vi - v0 >= 32) hit |= 0x80000000u;  // conservative
   }
   uint32_t tot;
   uint32_t pos = block_excl_scan<NT>(cnt, wtot, tot);
-  for (int i = 0; i < v1 - v0; ++i) {
-    if (i < 32 && !((hit >> i) & 1u)) continue;
+  for (int i = 0; i < nv; ++i) {
+    if (i < 31 && !((hit >> i) & 1u)) continue;
     const int vi = v0 + i;
-    const int p0 = vi << 4;
-    const int lim = min(16, valid - p0);
-    const uint4 v = t4[vi];
-    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t ge = __vcmpgeu4(ws[u], Lrep);
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb)
-        if (((ge >> (8 * bb)) & 1u) && u * 4 + bb < lim) dst[pos++] = (uint32_t)(id0 + p0 + u * 4 + bb);
+    uint32_t m = ge_mask16(t4[vi], Lrep);
+    const int lim = valid - (vi << 4);
+    if (lim < 16) m &= (1u << lim) - 1u;
+    const int64_t idb = id0 + ((int64_t)vi << 4);
+    while (m) {
+      const int bb = __ffs(m) - 1;
+      dst[pos++] = (uint32_t)(idb + bb);
+      m &= m - 1u;
     }
   }
 }
@@ -770,6 +782,45 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+struct TileRef {
+  int64_t sg, off, q;
+  int m;
+  uint32_t cid;   // this lane's candidate id (valid if lane < m)
+};
+
+// Walks tiles in increasing order: segment pointer only moves forward.
+struct TileWalker {
+  const int64_t* tpref;
+  const int64_t* sbase;
+  const int64_t* scnt;
+  const uint32_t* cand;
+  int64_t nseg, sg, seg_lo, seg_hi, base, cnt;
+  int S;
+  __device__ void init(int64_t tile) {
+    sg = tile_segment(tpref, nseg, tile);
+    load_seg();
+  }
+  __device__ void load_seg() {
+    seg_lo = tpref[sg];
+    seg_hi = tpref[sg + 1];
+    base = sbase[sg];
+    cnt = scnt[sg];
+  }
+  __device__ TileRef at(int64_t tile, int lane) {
+    while (tile >= seg_hi) {
+      ++sg;
+      load_seg();
+    }
+    TileRef r;
+    r.sg = sg;
+    r.off = (tile - seg_lo) * GR;
+    r.m = (int)min((int64_t)GR, cnt - r.off);
+    r.q = sg / S;
+    r.cid = lane < r.m ? cand[base + r.off + lane] : 0xFFFFFFFFu;
+    return r;
+  }
+};
+
 __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
     const float* __restrict__ X, int d, const float* __restrict__ Qf, const int64_t* __restrict__ tpref,
     int64_t nseg, int S, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
@@ -780,6 +831,8 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
   __shared__ __align__(8) uint64_t full[RS], empty[RS];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nsg = (d + RSEG - 1) / RSEG;
+  const int64_t t0 = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) {
       mbar_init(&full[s], 1);
@@ -788,15 +841,16 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
+  if (t0 >= t1) return;
+  TileWalker W{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};
   if (wid == 0) {
-    // ---------------- producer warp
+    // ---------------- producer warp: one tile of lookahead on the id loads
+    W.init(t0);
+    TileRef cur = W.at(t0, lane);
     int64_t u = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t sg = tile_segment(tpref, nseg, tile);
-      const int64_t off = (tile - tpref[sg]) * GR;
-      const int m = (int)min((int64_t)GR, scnt[sg] - off);
-      const int64_t q = sg / S;
-      const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0u;
+    for (int64_t tile = t0; tile < t1; ++tile) {
+      TileRef nxt = cur;
+      if (tile + 1 < t1) nxt = W.at(tile + 1, lane);
       for (int g = 0; g < nsg; ++g, ++u) {
         const int slot = (int)(u % RS);
         const uint32_t par = (uint32_t)((u / RS) & 1);
@@ -804,26 +858,26 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
         const int len = min(RSEG, d - s0);
         if (lane == 0) {
           mbar_wait(&empty[slot], par ^ 1u);
-          mbar_expect_tx(&full[slot], (uint32_t)((m + 1) * len * 4));
+          mbar_expect_tx(&full[slot], (uint32_t)((cur.m + 1) * len * 4));
         }
         __syncwarp();
-        if (lane < m) bulk_g2s(stg[slot].rows[lane], X + (size_t)cid * d + s0, (uint32_t)(len * 4), &full[slot]);
-        if (lane == 0) bulk_g2s(stg[slot].q, Qf + (size_t)q * d + s0, (uint32_t)(len * 4), &full[slot]);
+        if (lane < cur.m)
+          bulk_g2s(stg[slot].rows[lane], X + (size_t)cur.cid * d + s0, (uint32_t)(len * 4), &full[slot]);
+        if (lane == 0) bulk_g2s(stg[slot].q, Qf + (size_t)cur.q * d + s0, (uint32_t)(len * 4), &full[slot]);
         __syncwarp();
       }
+      cur = nxt;
     }
   } else {
-    // ---------------- consumer warps
+    // ---------------- consumer warps: local tiles cw, cw + RW, ...
     const int cw = wid - 1;
-    int64_t i = 0;
-    for (int64_t tile = blockIdx.x + (int64_t)cw * gridDim.x; tile < ntiles;
-         tile += (int64_t)RW * gridDim.x, i += RW) {
-      const int64_t sg = tile_segment(tpref, nseg, tile);
-      const int64_t off = (tile - tpref[sg]) * GR;
-      const int m = (int)min((int64_t)GR, scnt[sg] - off);
-      const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0xFFFFFFFFu;
+    if (t0 + cw >= t1) return;
+    W.init(t0 + cw);
+    for (int64_t i = cw; t0 + i < t1; i += RW) {
+      const int64_t tile = t0 + i;
+      const TileRef tr = W.at(tile, lane);
       double a0 = 0.0, a1 = 0.0;
-      const int64_t ubase = (i + cw) * nsg;
+      const int64_t ubase = i * nsg;
       for (int g = 0; g < nsg; ++g) {
         const int64_t u = ubase + g;
         const int slot = (int)(u % RS);
@@ -858,8 +912,8 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
       }
       double v = __dadd_rn(a0, a1);
       v = v >= 0.0 ? v : 0.0;
-      unsigned long long key = lane < m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
-      uint32_t id = cid;
+      unsigned long long key = lane < tr.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+      uint32_t id = tr.cid;
       warp_sort_pairs(key, id);
       if (lane < kk) {
         pkey[tile * kk + lane] = key;
