@@ -246,8 +246,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // tallied (packed 16-bit counters), which yields the level histogram without
 // rescanning the table: #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
-constexpr int CT_PB = 2 * CT_THREADS;
-constexpr int CT_E = 32;
+constexpr int CT_PB = 2 * CT_THREADS;   // slices staged per batch
+constexpr int CT_E = 8;
 
 struct CountSmem {
   uint32_t st[CT_PB];
@@ -315,54 +315,98 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
     S.pref[2 * tid + 1] = ex + len2[0];
     if (tid == CT_THREADS - 1) S.pref[CT_PB] = tot;
     __syncthreads();
-    const uint32_t total = S.pref[nb];
-    for (uint32_t r0 = 0; r0 < total; r0 += CT_THREADS * CT_E) {
-      const uint32_t r1 = min(total, r0 + (uint32_t)(CT_THREADS * CT_E));
-      const uint32_t per = (r1 - r0 + CT_THREADS - 1) / CT_THREADS;
-      uint32_t f = r0 + per * tid;
-      const uint32_t fe = min(r1, f + per);
-      uint32_t idv[CT_E];
-      uint8_t jv[CT_E];
-      int cntv = 0;
+    // Rounds never mix subspaces: subspace j's ids in this batch form the
+    // flattened range [pref[slo_j], pref[shi_j]).  A round's ids are fetched
+    // (CT_E per thread) while the previous round's increments are applied;
+    // a barrier separates rounds of different subspaces only.
+    int rj = -1;                 // subspace of the pending round
+    uint32_t rb = 0;             // end of its flattened id range
+    int jn = 0;                  // next subspace to open
+    uint32_t jb_end = 0;         // end of the current subspace's range
+    int slo = 0, shi = 0;
+    auto next_round = [&](int& j, uint32_t& x0, uint32_t& x1, int& s0, int& s1) -> bool {
+      if (rj >= 0 && rb < jb_end) {       // more of the same subspace
+        j = rj; x0 = rb; x1 = min(jb_end, rb + (uint32_t)(CT_THREADS * CT_E)); s0 = slo; s1 = shi;
+        return true;
+      }
+      while (jn < n_sub) {
+        const int jj = jn++;
+        const int lo_s = max(S.jpref[jj], b0) - b0, hi_s = min(S.jpref[jj + 1], b0 + nb) - b0;
+        if (hi_s <= lo_s) continue;
+        const uint32_t A = S.pref[lo_s], B = S.pref[hi_s];
+        if (B <= A) continue;
+        slo = lo_s; shi = hi_s; jb_end = B;
+        j = jj; x0 = A; x1 = min(B, A + (uint32_t)(CT_THREADS * CT_E)); s0 = lo_s; s1 = hi_s;
+        return true;
+      }
+      return false;
+    };
+    auto fetch = [&](uint32_t x0, uint32_t x1, int s0, int s1, uint32_t* idv, int& cntv) {
+      const uint32_t per = (x1 - x0 + CT_THREADS - 1) / CT_THREADS;
+      uint32_t f = x0 + per * tid;
+      const uint32_t fe = min(x1, f + per);
+      cntv = 0;
       if (f < fe) {
-        int t = slice_of(S.pref, nb, f);
+        int lo = s0, hi = s1;  // largest t in [s0, s1) with pref[t] <= f
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.pref[mid] <= f) lo = mid; else hi = mid;
+        }
+        int t = lo;
         uint32_t nextb = S.pref[t + 1];
         const uint32_t* src = ids + (size_t)S.sj[t] * n + S.st[t] - S.pref[t];
-        uint8_t jcur = S.sj[t];
 #pragma unroll
         for (int e = 0; e < CT_E; ++e) {
           if (f < fe) {
             while (f >= nextb) {
               ++t;
               nextb = S.pref[t + 1];
-              jcur = S.sj[t];
-              src = ids + (size_t)jcur * n + S.st[t] - S.pref[t];
+              src = ids + (size_t)S.sj[t] * n + S.st[t] - S.pref[t];
             }
             idv[e] = __ldg(src + f);
-            jv[e] = jcur;
             ++f;
             cntv = e + 1;
           }
         }
       }
-      const int jlo = S.sj[slice_of(S.pref, nb, r0)];
-      const int jhi = S.sj[slice_of(S.pref, nb, r1 - 1)];
-      for (int j = jlo; j <= jhi; ++j) {
+    };
+    auto apply = [&](const uint32_t* idv, int cntv) {
 #pragma unroll
-        for (int e = 0; e < CT_E; ++e) {
-          if (e < cntv && jv[e] == (uint8_t)j) {
-            uint8_t* p = table + (idv[e] - (uint32_t)base);
-            const uint32_t old = *p;
-            *p = (uint8_t)(old + 1);
-            const uint64_t inc = 1ull << ((old & 3u) << 4);
-            if (old < 4) lv0 += inc;
-            else if (old < 8) lv1 += inc;
-            else if (old < 12) lv2 += inc;
-            else lv3 += inc;
-          }
+      for (int e = 0; e < CT_E; ++e) {
+        if (e < cntv) {
+          uint8_t* p = table + (idv[e] - (uint32_t)base);
+          const uint32_t old = *p;
+          *p = (uint8_t)(old + 1);
+          const uint64_t inc = 1ull << ((old & 3u) << 4);
+          if (old < 4) lv0 += inc;
+          else if (old < 8) lv1 += inc;
+          else if (old < 12) lv2 += inc;
+          else lv3 += inc;
         }
-        __syncthreads();
       }
+    };
+    uint32_t idA[CT_E], idB[CT_E];
+    int cA = 0, cB = 0;
+    int jA, sA0, sA1;
+    uint32_t xA0, xA1;
+    bool haveA = next_round(jA, xA0, xA1, sA0, sA1);
+    if (haveA) {
+      rj = jA; rb = xA1;
+      fetch(xA0, xA1, sA0, sA1, idA, cA);
+    }
+    while (haveA) {
+      int jB, sB0, sB1;
+      uint32_t xB0, xB1;
+      const bool haveB = next_round(jB, xB0, xB1, sB0, sB1);
+      if (haveB) {
+        rj = jB; rb = xB1;
+        fetch(xB0, xB1, sB0, sB1, idB, cB);
+      }
+      apply(idA, cA);
+      if (!haveB || jB != jA) __syncthreads();
+#pragma unroll
+      for (int e = 0; e < CT_E; ++e) idA[e] = idB[e];
+      cA = cB; jA = jB; haveA = haveB;
     }
     __syncthreads();
   }
@@ -923,6 +967,118 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
   }
 }
 
+// ----------------------------------------- rerank: cp.async warp pipelines
+// Each warp owns a contiguous range of 32-row candidate tiles and streams
+// (tile, 128-dim segment) units through its own ring of AST shared-memory
+// stages with cp.async (LDGSTS, 16 B per lane, L2-only): the next AST-1
+// units are always in flight while lane r folds row r of the current unit
+// into numpy's two einsum lanes.  Warp top-k of the 32 (d2, id) pairs per tile.
+constexpr int AST = 3;                 // stages per warp
+constexpr int AWARPS = 4;              // warps per CTA
+struct AStage {
+  float rows[GR][RPITCH];
+  float q[RSEG];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
+    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int64_t* __restrict__ tpref,
+    int64_t nseg, int S, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
+    const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
+    uint32_t* __restrict__ pid) {
+  extern __shared__ __align__(128) unsigned char asm_[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  AStage* ring = reinterpret_cast<AStage*>(asm_) + wid * AST;
+  const int64_t gw = (int64_t)blockIdx.x * AWARPS + wid, nw = (int64_t)gridDim.x * AWARPS;
+  const int64_t t0 = ntiles * gw / nw, t1 = ntiles * (gw + 1) / nw;
+  if (t0 >= t1) return;
+  const int nsg = (d + RSEG - 1) / RSEG;
+  const int64_t U = (t1 - t0) * nsg;
+  TileWalker Wi{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};   // issue side
+  TileWalker Wc{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};   // compute side
+  Wi.init(t0);
+  Wc.init(t0);
+  TileRef ti = Wi.at(t0, lane);
+  int64_t ti_tile = t0;
+  auto issue = [&](int64_t u) {
+    const int64_t tile = t0 + u / nsg;
+    const int g = (int)(u % nsg);
+    if (tile != ti_tile) {
+      ti = Wi.at(tile, lane);
+      ti_tile = tile;
+    }
+    AStage& st = ring[u % AST];
+    const int s0 = g * RSEG;
+    const int len = min(RSEG, d - s0);
+    const int nv = len >> 2;                       // float4 per row segment
+    const float* xs = X + s0;
+    for (int r = 0; r < ti.m; ++r) {
+      const uint32_t cid = __shfl_sync(0xffffffffu, ti.cid, r);
+      if (lane < nv) cp_async16(&st.rows[r][lane * 4], xs + (size_t)cid * d + lane * 4);
+    }
+    if (lane < nv) cp_async16(&st.q[lane * 4], Qf + (size_t)ti.q * d + s0 + lane * 4);
+  };
+  for (int64_t u = 0; u < AST - 1; ++u) {
+    if (u < U) issue(u);
+    cp_async_commit();
+  }
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t u = 0; u < U; ++u) {
+    if (u + AST - 1 < U) issue(u + AST - 1);
+    cp_async_commit();
+    cp_async_wait<AST - 1>();
+    __syncwarp();
+    const int64_t tile = t0 + u / nsg;
+    const int g = (int)(u % nsg);
+    const AStage& st = ring[u % AST];
+    const float* row = st.rows[lane];
+    const float* qv = st.q;
+    const int s0 = g * RSEG;
+    const int len = min(RSEG, d - s0);
+    const bool last = g == nsg - 1;
+    const int full8 = last ? (len & ~7) : len;
+    for (int b = 0; b < full8; b += 8) {
+      const float4 x0 = *reinterpret_cast<const float4*>(row + b);
+      const float4 x1 = *reinterpret_cast<const float4*>(row + b + 4);
+      const float4 q0 = *reinterpret_cast<const float4*>(qv + b);
+      const float4 q1 = *reinterpret_cast<const float4*>(qv + b + 4);
+      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      const float q8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      einsum_block8(xv, q8, a0, a1);
+    }
+    if (last) {
+      for (int b = full8; b < len; b += 2) {
+        const double e0 = __dsub_rn((double)row[b], (double)qv[b]);
+        a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
+        if (b + 1 < len) {
+          const double e1 = __dsub_rn((double)row[b + 1], (double)qv[b + 1]);
+          a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
+        }
+      }
+      const TileRef tr = Wc.at(tile, lane);
+      double v = __dadd_rn(a0, a1);
+      v = v >= 0.0 ? v : 0.0;
+      unsigned long long key = lane < tr.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+      uint32_t id = tr.cid;
+      warp_sort_pairs(key, id);
+      if (lane < kk) {
+        pkey[tile * kk + lane] = key;
+        pid[tile * kk + lane] = id;
+      }
+      a0 = 0.0;
+      a1 = 0.0;
+    }
+    __syncwarp();   // the slot is refilled by the next issue
+  }
+  cp_async_wait<0>();
+}
+
 // Generic rerank for d % 4 != 0: lane = row, direct loads.
 __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ X, int d,
                                                       const float* __restrict__ Qf,
@@ -1374,8 +1530,8 @@ static int num_sms() {
 static int set_rerank_attrs() {
   static bool done = false;
   if (!done) {
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(RStage) * RS)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(AStage) * AST * AWARPS)));
     done = true;
   }
   return TACO_OK;
@@ -1393,8 +1549,8 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
     ProfScope ps(K_RERANK, st);
     if (d % 4 == 0) {
       TACO_TRY(set_rerank_attrs());
-      const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms());
-      k_rerank_tma<<<(unsigned)grid, 32 * (RW + 1), sizeof(RStage) * RS, st>>>(
+      const int64_t grid = std::min<int64_t>(ceil_div(ntiles, AWARPS), (int64_t)num_sms());
+      k_rerank_async<<<(unsigned)grid, 32 * AWARPS, sizeof(AStage) * AST * AWARPS, st>>>(
           X, d, Qf, tpref, QS * S, (int)S, sbase, scnt, cand, ntiles, kk, pkey.as<unsigned long long>(),
           pid.as<uint32_t>());
     } else {
