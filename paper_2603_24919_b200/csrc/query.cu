@@ -493,17 +493,21 @@ __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t
   uint32_t hit = 0;                              // which of my first 32 vectors hold matches
   for (int i = 0; i < nv; ++i) {
     const int vi = v0 + (i + threadIdx.x) % nv;  // rotated start: bank-conflict free
-    uint32_t m = ge_mask16(t4[vi], Lrep);
-    const int lim = valid - (vi << 4);
-    if (lim < 16) m &= (1u << lim) - 1u;
-    cnt += __popc(m);
-    if (m && vi - v0 < 32) hit |= 1u << (vi - v0);
-    if (m && vi - v0 >= 32) hit |= 0x80000000u;  // conservative
+    const uint4 v = t4[vi];
+    const uint32_t g0 = __vcmpgeu4(v.x, Lrep), g1 = __vcmpgeu4(v.y, Lrep);
+    const uint32_t g2 = __vcmpgeu4(v.z, Lrep), g3 = __vcmpgeu4(v.w, Lrep);
+    if (g0 | g1 | g2 | g3) {
+      uint32_t m = ge_mask16(v, Lrep);
+      const int lim = valid - (vi << 4);
+      if (lim < 16) m &= (1u << lim) - 1u;
+      cnt += __popc(m);
+      if (m) hit |= vi - v0 < 31 ? 1u << (vi - v0) : 0x80000000u;
+    }
   }
   uint32_t tot;
   uint32_t pos = block_excl_scan<NT>(cnt, wtot, tot);
   for (int i = 0; i < nv; ++i) {
-    if (i < 31 && !((hit >> i) & 1u)) continue;
+    if (i < 31 ? !((hit >> i) & 1u) : !(hit >> 31)) continue;
     const int vi = v0 + i;
     uint32_t m = ge_mask16(t4[vi], Lrep);
     const int lim = valid - (vi << 4);
@@ -969,15 +973,23 @@ __global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
 
 // ----------------------------------------- rerank: cp.async warp pipelines
 // Each warp owns a contiguous range of 32-row candidate tiles and streams
-// (tile, 128-dim segment) units through its own ring of AST shared-memory
-// stages with cp.async (LDGSTS, 16 B per lane, L2-only): the next AST-1
-// units are always in flight while lane r folds row r of the current unit
-// into numpy's two einsum lanes.  Warp top-k of the 32 (d2, id) pairs per tile.
-constexpr int AST = 3;                 // stages per warp
-constexpr int AWARPS = 4;              // warps per CTA
+// (tile, 64-dim segment) units through its own ring of AST shared-memory
+// stages with cp.async (LDGSTS, 16 B per lane, L2-only; one instruction moves
+// two 256-byte row segments): the next AST-1 units are in flight while lane r
+// folds row r of the current unit into numpy's two einsum lanes against the
+// query segment (pre-converted to fp64 in shared memory).  Warp top-k of the
+// 32 (d2, id) pairs per tile.
+constexpr int ASEG = 64;               // dims per unit
+constexpr int APITCH = ASEG + 4;       // 272 B rows: float4 reads are bank-conflict free
+constexpr int AST = 2;                 // stages per warp (the id lookahead assumes 2)
+constexpr int AWARPS = 12;             // warps per CTA
 struct AStage {
-  float rows[GR][RPITCH];
-  float q[RSEG];
+  float rows[GR][APITCH];
+  float q[ASEG];
+};
+struct AWarpSmem {
+  AStage st[AST];
+  double qd[ASEG];
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -994,35 +1006,38 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
     uint32_t* __restrict__ pid) {
   extern __shared__ __align__(128) unsigned char asm_[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  AStage* ring = reinterpret_cast<AStage*>(asm_) + wid * AST;
+  AWarpSmem& W = reinterpret_cast<AWarpSmem*>(asm_)[wid];
   const int64_t gw = (int64_t)blockIdx.x * AWARPS + wid, nw = (int64_t)gridDim.x * AWARPS;
   const int64_t t0 = ntiles * gw / nw, t1 = ntiles * (gw + 1) / nw;
   if (t0 >= t1) return;
-  const int nsg = (d + RSEG - 1) / RSEG;
+  const int nsg = (d + ASEG - 1) / ASEG;
   const int64_t U = (t1 - t0) * nsg;
-  TileWalker Wi{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};   // issue side
-  TileWalker Wc{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};   // compute side
+  TileWalker Wi{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};
   Wi.init(t0);
-  Wc.init(t0);
-  TileRef ti = Wi.at(t0, lane);
-  int64_t ti_tile = t0;
+  TileRef tcur = Wi.at(t0, lane);                         // tile being issued
+  TileRef tnext = t0 + 1 < t1 ? Wi.at(t0 + 1, lane) : tcur;  // its successor (ids prefetched)
+  int64_t tcur_tile = t0;
+  TileRef tcomp = tcur;                                   // tile being computed
+  const int half = lane >> 4, hl = lane & 15;
   auto issue = [&](int64_t u) {
     const int64_t tile = t0 + u / nsg;
     const int g = (int)(u % nsg);
-    if (tile != ti_tile) {
-      ti = Wi.at(tile, lane);
-      ti_tile = tile;
+    if (tile != tcur_tile) {
+      tcur = tnext;
+      tcur_tile = tile;
+      if (tile + 1 < t1) tnext = Wi.at(tile + 1, lane);
     }
-    AStage& st = ring[u % AST];
-    const int s0 = g * RSEG;
-    const int len = min(RSEG, d - s0);
-    const int nv = len >> 2;                       // float4 per row segment
-    const float* xs = X + s0;
-    for (int r = 0; r < ti.m; ++r) {
-      const uint32_t cid = __shfl_sync(0xffffffffu, ti.cid, r);
-      if (lane < nv) cp_async16(&st.rows[r][lane * 4], xs + (size_t)cid * d + lane * 4);
+    AStage& st = W.st[u % AST];
+    const int s0 = g * ASEG;
+    const int len = min(ASEG, d - s0);
+    const int nv = len >> 2;                              // float4 per row segment (<= 16)
+    const float* xs = X + s0 + hl * 4;
+    for (int r = 0; r < tcur.m; r += 2) {
+      const int rr = r + half;
+      const uint32_t cid = __shfl_sync(0xffffffffu, tcur.cid, rr & 31);
+      if (hl < nv && rr < tcur.m) cp_async16(&st.rows[rr][hl * 4], xs + (size_t)cid * d);
     }
-    if (lane < nv) cp_async16(&st.q[lane * 4], Qf + (size_t)ti.q * d + s0 + lane * 4);
+    if (lane < nv) cp_async16(&st.q[lane * 4], Qf + (size_t)tcur.q * d + s0 + lane * 4);
   };
   for (int64_t u = 0; u < AST - 1; ++u) {
     if (u < U) issue(u);
@@ -1030,42 +1045,50 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
   }
   double a0 = 0.0, a1 = 0.0;
   for (int64_t u = 0; u < U; ++u) {
+    const int64_t tile = t0 + u / nsg;
+    const int g = (int)(u % nsg);
+    if (g == 0) tcomp = (tile == tcur_tile) ? tcur : tnext;   // ids of the tile computed now
     if (u + AST - 1 < U) issue(u + AST - 1);
     cp_async_commit();
     cp_async_wait<AST - 1>();
     __syncwarp();
-    const int64_t tile = t0 + u / nsg;
-    const int g = (int)(u % nsg);
-    const AStage& st = ring[u % AST];
+    const AStage& st = W.st[u % AST];
+    const int s0 = g * ASEG;
+    const int len = min(ASEG, d - s0);
+    for (int t = lane; t < len; t += 32) W.qd[t] = (double)st.q[t];
+    __syncwarp();
     const float* row = st.rows[lane];
-    const float* qv = st.q;
-    const int s0 = g * RSEG;
-    const int len = min(RSEG, d - s0);
+    const double* qv = W.qd;
     const bool last = g == nsg - 1;
     const int full8 = last ? (len & ~7) : len;
     for (int b = 0; b < full8; b += 8) {
       const float4 x0 = *reinterpret_cast<const float4*>(row + b);
       const float4 x1 = *reinterpret_cast<const float4*>(row + b + 4);
-      const float4 q0 = *reinterpret_cast<const float4*>(qv + b);
-      const float4 q1 = *reinterpret_cast<const float4*>(qv + b + 4);
       const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-      const float q8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-      einsum_block8(xv, q8, a0, a1);
+      double p[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double e = __dsub_rn((double)xv[t], qv[b + t]);
+        p[t] = __dmul_rn(e, e);
+      }
+      a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
+      a0 = __dadd_rn(p[4], a0); a1 = __dadd_rn(p[5], a1);
+      a0 = __dadd_rn(p[2], a0); a1 = __dadd_rn(p[3], a1);
+      a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
     }
     if (last) {
       for (int b = full8; b < len; b += 2) {
-        const double e0 = __dsub_rn((double)row[b], (double)qv[b]);
+        const double e0 = __dsub_rn((double)row[b], qv[b]);
         a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
         if (b + 1 < len) {
-          const double e1 = __dsub_rn((double)row[b + 1], (double)qv[b + 1]);
+          const double e1 = __dsub_rn((double)row[b + 1], qv[b + 1]);
           a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
         }
       }
-      const TileRef tr = Wc.at(tile, lane);
       double v = __dadd_rn(a0, a1);
       v = v >= 0.0 ? v : 0.0;
-      unsigned long long key = lane < tr.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
-      uint32_t id = tr.cid;
+      unsigned long long key = lane < tcomp.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+      uint32_t id = tcomp.cid;
       warp_sort_pairs(key, id);
       if (lane < kk) {
         pkey[tile * kk + lane] = key;
@@ -1074,7 +1097,7 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
       a0 = 0.0;
       a1 = 0.0;
     }
-    __syncwarp();   // the slot is refilled by the next issue
+    __syncwarp();   // the slot (and qd) are refilled next
   }
   cp_async_wait<0>();
 }
