@@ -1554,7 +1554,7 @@ static int set_rerank_attrs() {
   static bool done = false;
   if (!done) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(AStage) * AST * AWARPS)));
+                                         (int)(sizeof(AWarpSmem) * AWARPS)));
     done = true;
   }
   return TACO_OK;
@@ -1573,7 +1573,7 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
     if (d % 4 == 0) {
       TACO_TRY(set_rerank_attrs());
       const int64_t grid = std::min<int64_t>(ceil_div(ntiles, AWARPS), (int64_t)num_sms());
-      k_rerank_async<<<(unsigned)grid, 32 * AWARPS, sizeof(AStage) * AST * AWARPS, st>>>(
+      k_rerank_async<<<(unsigned)grid, 32 * AWARPS, sizeof(AWarpSmem) * AWARPS, st>>>(
           X, d, Qf, tpref, QS * S, (int)S, sbase, scnt, cand, ntiles, kk, pkey.as<unsigned long long>(),
           pid.as<uint32_t>());
     } else {
