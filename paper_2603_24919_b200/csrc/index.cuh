@@ -23,7 +23,7 @@ namespace taco {
 //    one thread-block cluster, chunk = ceil(n / ctas) rounded to 1 KiB;
 //  global mode (larger shards / multi-GPU): chunk = 64 KiB, tables in HBM.
 constexpr int64_t kGlobalChunk = 65536;
-constexpr int64_t kClusterMaxChunk = 196608;
+constexpr int64_t kClusterMaxChunk = 184320;   // + ~40 KiB static smem <= 227 KiB
 constexpr int kClusterMaxCtas = 8;
 constexpr int64_t kClusterMaxN = kClusterMaxChunk * kClusterMaxCtas;
 

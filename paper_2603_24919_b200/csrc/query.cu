@@ -238,34 +238,148 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 
 // ------------------------------------------------------------ chunk counting
 // Counts into `table` (ids [base, base+chunk)) every id of the cells popped for
-// query q in subspaces 0..n_sub-1.  Slices of all subspaces are staged PB at a
-// time (phase A: one round trip for their CSR bounds); ids are then gathered
-// E per thread with independent loads (phase B) and applied subspace by
-// subspace with a barrier in between: ids are unique inside one subspace, so
-// the byte increments need no atomics.  Every increment from level v to v+1 is
-// tallied (packed 16-bit counters), which yields the level histogram without
-// rescanning the table: #(score >= l) = #(increments leaving level l-1).
+// query q in subspaces 0..n_sub-1.  Phase A stages the slices of all popped
+// cells (one round trip for their CSR bounds, one block scan).  Phase B walks
+// subspace by subspace; each warp owns a contiguous part of the subspace's
+// flattened id list and fetches it 32 consecutive ids per instruction
+// (coalesced inside a slice), CT_E steps per round, the next round's ids in
+// flight while the current round's byte increments are applied.  Ids are
+// unique inside one subspace, so increments need no atomics; a barrier
+// separates subspaces.  Every increment leaving level v is tallied (packed
+// 16-bit counters), which gives the level histogram without rescanning:
+// #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
-constexpr int CT_PB = 2 * CT_THREADS;   // slices staged per batch
-constexpr int CT_E = 8;
+constexpr int CT_WARPS = CT_THREADS / 32;
+constexpr int CT_PB = 4096;   // slices staged per batch
+constexpr int CT_E = 8;       // 32-id steps per warp per round
 
 struct CountSmem {
-  uint32_t st[CT_PB];
-  uint32_t pref[CT_PB + 1];
-  uint8_t sj[CT_PB];
+  int32_t dl[CT_PB];          // slice delta: the slice's id at flattened f is ids[j*n + dl + f]
+  uint32_t pref[CT_PB + 1];   // flattened start of each slice
+  uint8_t sj[CT_PB];          // subspace of each slice
   uint32_t wtot[CT_THREADS / 32];
-  int jpref[257];
-  int ge[257];      // ge[l] = #ids of the chunk with score >= l  (l >= 1)
-  int lh[256];      // level histogram (lh[0] = ids at score 0)
+  int jpref[257];             // pop prefix over subspaces
+  int ge[257];                // ge[l] = #ids of the chunk with score >= l  (l >= 1)
+  int lh[256];                // level histogram (lh[0] = ids at score 0)
+  int batches;                // number of slice batches the query needed
+  uint32_t cursor;            // candidates emitted so far (cluster compaction)
 };
 
-__device__ __forceinline__ int slice_of(const uint32_t* pref, int nb, uint32_t f) {
-  int lo = 0, hi = nb;  // largest t with pref[t] <= f
-  while (hi - lo > 1) {
+__device__ __forceinline__ int slice_in(const uint32_t* pref, int lo, int hi, uint32_t f) {
+  while (hi - lo > 1) {       // largest t in [lo, hi) with pref[t] <= f
     const int mid = (lo + hi) >> 1;
     if (pref[mid] <= f) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// Stages batch b0 of the popped slices (phase A).  Returns the slice count.
+__device__ int stage_slices(const uint16_t* __restrict__ pops, int cap, const uint32_t* __restrict__ offs,
+                            size_t offs_len, int n_sub, int K2, int64_t c, int64_t q, int b0, CountSmem& S) {
+  const int tid = threadIdx.x;
+  const int P_all = S.jpref[n_sub];
+  const int nb = min(CT_PB, P_all - b0);
+  constexpr int PER = CT_PB / CT_THREADS;
+  uint32_t len[PER];
+  uint32_t loc = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = tid * PER + u;
+    len[u] = 0;
+    if (t < nb) {
+      const int g = b0 + t;
+      int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (S.jpref[mid] <= g) lo = mid; else hi = mid;
+      }
+      const int j = lo;
+      const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
+      const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
+      const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
+      S.dl[t] = (int32_t)s0;
+      S.sj[t] = (uint8_t)j;
+      len[u] = s1 - s0;
+    }
+    loc += len[u];
+  }
+  uint32_t tot;
+  uint32_t run = block_excl_scan<CT_THREADS>(loc, S.wtot, tot);
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = tid * PER + u;
+    S.pref[t] = run;
+    if (t < nb) S.dl[t] -= (int32_t)run;
+    run += len[u];
+  }
+  if (tid == 0) S.pref[CT_PB] = tot;
+  __syncthreads();
+  return nb;
+}
+
+// One (subspace, round) step of a warp: fetch up to 32*CT_E ids into idv
+// (lane-major: idv[i] is flattened id ws + 32 i + lane).  Returns the count of
+// valid steps for this lane through `nval`.
+__device__ __forceinline__ void fetch_round(const uint32_t* __restrict__ ids, int64_t n, const CountSmem& S,
+                                            int j, int lo_s, int hi_s, uint32_t ws, uint32_t we,
+                                            uint32_t* idv, int& nval) {
+  const int lane = threadIdx.x & 31;
+  nval = 0;
+  if (ws >= we) return;
+  int t = slice_in(S.pref, lo_s, hi_s, ws);
+  const uint32_t* src = ids + (size_t)j * n;
+#pragma unroll
+  for (int i = 0; i < CT_E; ++i) {
+    const uint32_t f = ws + (uint32_t)(i * 32 + lane);
+    if (f < we) {
+      while (f >= S.pref[t + 1]) ++t;
+      idv[i] = __ldg(src + (int64_t)S.dl[t] + f);
+      nval = i + 1;
+    }
+  }
+}
+
+template <bool SMALL>
+__device__ __forceinline__ void apply_round(uint8_t* table, uint32_t base, const uint32_t* idv, int nval,
+                                            uint64_t& lv0, uint64_t& lv1, uint64_t& lv2, uint64_t& lv3) {
+#pragma unroll
+  for (int i = 0; i < CT_E; ++i) {
+    if (i < nval) {
+      uint8_t* p = table + (idv[i] - base);
+      const uint32_t old = *p;
+      *p = (uint8_t)(old + 1);
+      const uint64_t inc = 1ull << ((old & 3u) << 4);
+      if (SMALL) {
+        if (old < 4) lv0 += inc; else lv1 += inc;
+      } else {
+        if (old < 4) lv0 += inc;
+        else if (old < 8) lv1 += inc;
+        else if (old < 12) lv2 += inc;
+        else lv3 += inc;
+      }
+    }
+  }
+}
+
+// Iterates the (subspace, round) steps of the current batch in order; calls
+// body(j, lo_s, hi_s, ws, we) per warp-step, `sep()` between subspaces.
+template <typename Body>
+__device__ __forceinline__ void for_each_round(const CountSmem& S, int n_sub, int b0, int nb, Body body) {
+  const int w = threadIdx.x >> 5;
+  for (int j = 0; j < n_sub; ++j) {
+    const int lo_s = max(S.jpref[j], b0) - b0, hi_s = min(S.jpref[j + 1], b0 + nb) - b0;
+    if (hi_s <= lo_s) continue;
+    const uint32_t A = S.pref[lo_s], B = S.pref[hi_s];
+    if (B <= A) continue;
+    const uint32_t per = (B - A + CT_WARPS - 1) / CT_WARPS;
+    const uint32_t Lw = (per + 31u) & ~31u;
+    const uint32_t w0 = A + (uint32_t)w * Lw, w1 = min(B, w0 + Lw);
+    const int rounds = (int)((Lw + 32u * CT_E - 1) / (32u * CT_E));
+    for (int r = 0; r < rounds; ++r) {
+      const uint32_t ws = w0 + (uint32_t)r * 32u * CT_E;
+      body(j, lo_s, hi_s, ws, min(w1, ws + 32u * CT_E), r == rounds - 1);
+    }
+  }
 }
 
 __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
@@ -273,7 +387,6 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
                             int64_t base, uint8_t* table, CountSmem& S) {
   const int tid = threadIdx.x;
-  const bool track = n_sub <= 16;
   uint64_t lv0 = 0, lv1 = 0, lv2 = 0, lv3 = 0;   // packed per-level increment tallies
   if (tid == 0) {
     int acc = 0;
@@ -282,142 +395,45 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       acc += min(npop[q * n_sub + j], cap);
     }
     S.jpref[n_sub] = acc;
+    S.batches = (acc + CT_PB - 1) / CT_PB;
   }
   __syncthreads();
   const int P_all = S.jpref[n_sub];
   for (int b0 = 0; b0 < P_all; b0 += CT_PB) {
-    const int nb = min(CT_PB, P_all - b0);
-    uint32_t len2[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int t = 2 * tid + u;
-      uint32_t len = 0;
-      if (t < nb) {
-        const int g = b0 + t;
-        int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (S.jpref[mid] <= g) lo = mid; else hi = mid;
-        }
-        const int j = lo;
-        const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
-        const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
-        const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
-        S.st[t] = s0;
-        S.sj[t] = (uint8_t)j;
-        len = s1 - s0;
-      }
-      len2[u] = len;
-    }
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan<CT_THREADS>(len2[0] + len2[1], S.wtot, tot);
-    S.pref[2 * tid] = ex;
-    S.pref[2 * tid + 1] = ex + len2[0];
-    if (tid == CT_THREADS - 1) S.pref[CT_PB] = tot;
-    __syncthreads();
-    // Rounds never mix subspaces: subspace j's ids in this batch form the
-    // flattened range [pref[slo_j], pref[shi_j]).  A round's ids are fetched
-    // (CT_E per thread) while the previous round's increments are applied;
-    // a barrier separates rounds of different subspaces only.
-    int rj = -1;                 // subspace of the pending round
-    uint32_t rb = 0;             // end of its flattened id range
-    int jn = 0;                  // next subspace to open
-    uint32_t jb_end = 0;         // end of the current subspace's range
-    int slo = 0, shi = 0;
-    auto next_round = [&](int& j, uint32_t& x0, uint32_t& x1, int& s0, int& s1) -> bool {
-      if (rj >= 0 && rb < jb_end) {       // more of the same subspace
-        j = rj; x0 = rb; x1 = min(jb_end, rb + (uint32_t)(CT_THREADS * CT_E)); s0 = slo; s1 = shi;
-        return true;
-      }
-      while (jn < n_sub) {
-        const int jj = jn++;
-        const int lo_s = max(S.jpref[jj], b0) - b0, hi_s = min(S.jpref[jj + 1], b0 + nb) - b0;
-        if (hi_s <= lo_s) continue;
-        const uint32_t A = S.pref[lo_s], B = S.pref[hi_s];
-        if (B <= A) continue;
-        slo = lo_s; shi = hi_s; jb_end = B;
-        j = jj; x0 = A; x1 = min(B, A + (uint32_t)(CT_THREADS * CT_E)); s0 = lo_s; s1 = hi_s;
-        return true;
-      }
-      return false;
-    };
-    auto fetch = [&](uint32_t x0, uint32_t x1, int s0, int s1, uint32_t* idv, int& cntv) {
-      const uint32_t per = (x1 - x0 + CT_THREADS - 1) / CT_THREADS;
-      uint32_t f = x0 + per * tid;
-      const uint32_t fe = min(x1, f + per);
-      cntv = 0;
-      if (f < fe) {
-        int lo = s0, hi = s1;  // largest t in [s0, s1) with pref[t] <= f
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (S.pref[mid] <= f) lo = mid; else hi = mid;
-        }
-        int t = lo;
-        uint32_t nextb = S.pref[t + 1];
-        const uint32_t* src = ids + (size_t)S.sj[t] * n + S.st[t] - S.pref[t];
-#pragma unroll
-        for (int e = 0; e < CT_E; ++e) {
-          if (f < fe) {
-            while (f >= nextb) {
-              ++t;
-              nextb = S.pref[t + 1];
-              src = ids + (size_t)S.sj[t] * n + S.st[t] - S.pref[t];
-            }
-            idv[e] = __ldg(src + f);
-            ++f;
-            cntv = e + 1;
-          }
-        }
-      }
-    };
-    auto apply = [&](const uint32_t* idv, int cntv) {
-#pragma unroll
-      for (int e = 0; e < CT_E; ++e) {
-        if (e < cntv) {
-          uint8_t* p = table + (idv[e] - (uint32_t)base);
-          const uint32_t old = *p;
-          *p = (uint8_t)(old + 1);
-          const uint64_t inc = 1ull << ((old & 3u) << 4);
-          if (old < 4) lv0 += inc;
-          else if (old < 8) lv1 += inc;
-          else if (old < 12) lv2 += inc;
-          else lv3 += inc;
-        }
-      }
-    };
+    const int nb = stage_slices(pops, cap, offs, offs_len, n_sub, K2, c, q, b0, S);
+    // software pipeline over the (subspace, round) steps
     uint32_t idA[CT_E], idB[CT_E];
-    int cA = 0, cB = 0;
-    int jA, sA0, sA1;
-    uint32_t xA0, xA1;
-    bool haveA = next_round(jA, xA0, xA1, sA0, sA1);
-    if (haveA) {
-      rj = jA; rb = xA1;
-      fetch(xA0, xA1, sA0, sA1, idA, cA);
-    }
-    while (haveA) {
-      int jB, sB0, sB1;
-      uint32_t xB0, xB1;
-      const bool haveB = next_round(jB, xB0, xB1, sB0, sB1);
-      if (haveB) {
-        rj = jB; rb = xB1;
-        fetch(xB0, xB1, sB0, sB1, idB, cB);
+    int nA = 0, jA = -1;
+    bool haveA = false;
+    auto run_step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we, bool last_of_j) {
+      int nB;
+      fetch_round(ids, n, S, j, lo_s, hi_s, ws, we, idB, nB);
+      if (haveA) {
+        if (n_sub <= 8) apply_round<true>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
+        else apply_round<false>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
+        if (jA != j) __syncthreads();   // increments of a new subspace wait for the previous one
       }
-      apply(idA, cA);
-      if (!haveB || jB != jA) __syncthreads();
 #pragma unroll
-      for (int e = 0; e < CT_E; ++e) idA[e] = idB[e];
-      cA = cB; jA = jB; haveA = haveB;
+      for (int i = 0; i < CT_E; ++i) idA[i] = idB[i];
+      nA = nB;
+      jA = j;
+      haveA = true;
+      (void)last_of_j;
+    };
+    for_each_round(S, n_sub, b0, nb, run_step);
+    if (haveA) {
+      if (n_sub <= 8) apply_round<true>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
+      else apply_round<false>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
     }
     __syncthreads();
   }
-  // ge[l] = #increments that left level l-1 (per-thread tallies <= 2^16 - 1:
-  // a thread applies at most CT_E ids per round and rounds are few)
   for (int i = tid; i < 257; i += CT_THREADS) S.ge[i] = 0;
   __syncthreads();
-  if (track) {
+  if (n_sub <= 16) {
     uint64_t v[4] = {lv0, lv1, lv2, lv3};
 #pragma unroll
     for (int wv = 0; wv < 4; ++wv) {
+      if (wv * 4 >= n_sub) break;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         int x = (int)((v[wv] >> (16 * s)) & 0xFFFFull);
@@ -429,6 +445,43 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
     }
   }
   __syncthreads();
+}
+
+// Candidates of the last staged batch by re-walking its id lists: the first
+// time an id with score >= L is seen it is emitted and flagged (bit 7), so
+// every candidate is written exactly once (order irrelevant: ties break by id).
+__device__ void emit_candidates(const uint32_t* __restrict__ ids, int64_t n, int n_sub, uint8_t* table,
+                                uint32_t base, uint32_t L, uint32_t* dst, CountSmem& S) {
+  const int lane = threadIdx.x & 31;
+  const int nb = S.jpref[n_sub];   // single batch
+  auto step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we, bool last_of_j) {
+    uint32_t idv[CT_E];
+    int nv;
+    fetch_round(ids, n, S, j, lo_s, hi_s, ws, we, idv, nv);
+#pragma unroll
+    for (int i = 0; i < CT_E; ++i) {
+      bool e = false;
+      uint32_t x = 0;
+      if (i < nv) {
+        x = idv[i];
+        uint8_t* p = table + (x - base);
+        const uint32_t v = *p;
+        if (v >= L && v < 0x80u) {
+          *p = (uint8_t)(v | 0x80u);
+          e = true;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, e);
+      if (m) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&S.cursor, (uint32_t)__popc(m));
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (e) dst[b + __popc(m & ((1u << lane) - 1u))] = x;
+      }
+    }
+    if (last_of_j) __syncthreads();
+  };
+  for_each_round(S, n_sub, 0, nb, step);
 }
 
 // Level histogram of a chunk table.  n_sub <= 16: from the tallies; else by a
@@ -586,7 +639,13 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
   }
   cluster.sync();   // remote histograms no longer needed by anyone after this point
   if (s_base + s_cnt > cand_cap) return;
-  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
+  if (s_L >= 1 && S.batches == 1 && n_sub <= 127) {
+    if (tid == 0) S.cursor = 0;
+    __syncthreads();
+    emit_candidates(ids, n, n_sub, table, (uint32_t)base, (uint32_t)s_L, cand + s_base, S);
+  } else {
+    compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
+  }
 }
 
 // ------------------------------------------------------- global-mode count
