@@ -255,14 +255,13 @@ constexpr int CT_E = 8;       // 32-id steps per warp per round
 
 struct CountSmem {
   int32_t dl[CT_PB];          // slice delta: the slice's id at flattened f is ids[j*n + dl + f]
-  uint32_t pref[CT_PB + 1];   // flattened start of each slice
-  uint8_t sj[CT_PB];          // subspace of each slice
+  uint32_t pref[CT_PB + 1];   // flattened start of each (non-empty) slice
   uint32_t wtot[CT_THREADS / 32];
   int jpref[257];             // pop prefix over subspaces
+  int js[257];                // non-empty slices of subspace j: [js[j], js[j+1])
   int ge[257];                // ge[l] = #ids of the chunk with score >= l  (l >= 1)
   int lh[256];                // level histogram (lh[0] = ids at score 0)
   int batches;                // number of slice batches the query needed
-  uint32_t cursor;            // candidates emitted so far (cluster compaction)
 };
 
 __device__ __forceinline__ int slice_in(const uint32_t* pref, int lo, int hi, uint32_t f) {
@@ -273,19 +272,23 @@ __device__ __forceinline__ int slice_in(const uint32_t* pref, int lo, int hi, ui
   return lo;
 }
 
-// Stages batch b0 of the popped slices (phase A).  Returns the slice count.
-__device__ int stage_slices(const uint16_t* __restrict__ pops, int cap, const uint32_t* __restrict__ offs,
-                            size_t offs_len, int n_sub, int K2, int64_t c, int64_t q, int b0, CountSmem& S) {
+// Stages batch b0 of the popped slices (phase A), keeping only the slices
+// that hold ids of this chunk (most popped cells have none in a given chunk).
+__device__ void stage_slices(const uint16_t* __restrict__ pops, int cap, const uint32_t* __restrict__ offs,
+                             size_t offs_len, int n_sub, int K2, int64_t c, int64_t q, int b0, CountSmem& S) {
   const int tid = threadIdx.x;
   const int P_all = S.jpref[n_sub];
   const int nb = min(CT_PB, P_all - b0);
   constexpr int PER = CT_PB / CT_THREADS;
-  uint32_t len[PER];
-  uint32_t loc = 0;
+  uint32_t len[PER], st[PER];
+  uint32_t loc = 0, ne = 0;
+  for (int j = tid; j <= n_sub; j += CT_THREADS) S.js[j] = 0;
+  __syncthreads();
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
     const int t = tid * PER + u;
     len[u] = 0;
+    st[u] = 0;
     if (t < nb) {
       const int g = b0 + t;
       int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
@@ -297,44 +300,58 @@ __device__ int stage_slices(const uint16_t* __restrict__ pops, int cap, const ui
       const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
       const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
       const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
-      S.dl[t] = (int32_t)s0;
-      S.sj[t] = (uint8_t)j;
+      st[u] = s0;
       len[u] = s1 - s0;
+      if (len[u]) atomicAdd(&S.js[j + 1], 1);
     }
     loc += len[u];
+    ne += len[u] ? 1u : 0u;
   }
   uint32_t tot;
   uint32_t run = block_excl_scan<CT_THREADS>(loc, S.wtot, tot);
+  uint32_t netot;
+  uint32_t pos = block_excl_scan<CT_THREADS>(ne, S.wtot, netot);
+  if (tid == 0) {
+    for (int j = 0; j < n_sub; ++j) S.js[j + 1] += S.js[j];
+  }
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
-    const int t = tid * PER + u;
-    S.pref[t] = run;
-    if (t < nb) S.dl[t] -= (int32_t)run;
+    if (len[u]) {
+      S.pref[pos] = run;
+      S.dl[pos] = (int32_t)st[u] - (int32_t)run;
+      ++pos;
+    }
     run += len[u];
   }
-  if (tid == 0) S.pref[CT_PB] = tot;
+  if (tid == 0) S.pref[netot] = tot;
   __syncthreads();
-  return nb;
 }
 
 // One (subspace, round) step of a warp: fetch up to 32*CT_E ids into idv
-// (lane-major: idv[i] is flattened id ws + 32 i + lane).  Returns the count of
-// valid steps for this lane through `nval`.
+// (idv[i] is flattened id ws + 32 i + lane).  The slice of each lane is found
+// by counting, uniformly across the warp, the slice starts inside the 32-id
+// window (no divergent walk).
 __device__ __forceinline__ void fetch_round(const uint32_t* __restrict__ ids, int64_t n, const CountSmem& S,
                                             int j, int lo_s, int hi_s, uint32_t ws, uint32_t we,
                                             uint32_t* idv, int& nval) {
   const int lane = threadIdx.x & 31;
   nval = 0;
   if (ws >= we) return;
-  int t = slice_in(S.pref, lo_s, hi_s, ws);
+  int t0 = slice_in(S.pref, lo_s, hi_s, ws);
   const uint32_t* src = ids + (size_t)j * n;
 #pragma unroll
   for (int i = 0; i < CT_E; ++i) {
-    const uint32_t f = ws + (uint32_t)(i * 32 + lane);
-    if (f < we) {
-      while (f >= S.pref[t + 1]) ++t;
-      idv[i] = __ldg(src + (int64_t)S.dl[t] + f);
-      nval = i + 1;
+    const uint32_t F = ws + (uint32_t)(i * 32);
+    if (F < we) {
+      while (t0 + 1 < hi_s && S.pref[t0 + 1] <= F) ++t0;           // uniform
+      const uint32_t f = F + (uint32_t)lane;
+      int tl = t0;
+      for (int k = t0 + 1; k < hi_s && S.pref[k] < F + 32u; ++k)   // uniform trip count
+        tl += S.pref[k] <= f ? 1 : 0;
+      if (f < we) {
+        idv[i] = __ldg(src + (int64_t)S.dl[tl] + f);
+        nval = i + 1;
+      }
     }
   }
 }
@@ -361,23 +378,21 @@ __device__ __forceinline__ void apply_round(uint8_t* table, uint32_t base, const
   }
 }
 
-// Iterates the (subspace, round) steps of the current batch in order; calls
-// body(j, lo_s, hi_s, ws, we) per warp-step, `sep()` between subspaces.
+// Iterates the (subspace, round) steps of the staged batch in order.
 template <typename Body>
-__device__ __forceinline__ void for_each_round(const CountSmem& S, int n_sub, int b0, int nb, Body body) {
+__device__ __forceinline__ void for_each_round(const CountSmem& S, int n_sub, Body body) {
   const int w = threadIdx.x >> 5;
   for (int j = 0; j < n_sub; ++j) {
-    const int lo_s = max(S.jpref[j], b0) - b0, hi_s = min(S.jpref[j + 1], b0 + nb) - b0;
+    const int lo_s = S.js[j], hi_s = S.js[j + 1];
     if (hi_s <= lo_s) continue;
     const uint32_t A = S.pref[lo_s], B = S.pref[hi_s];
-    if (B <= A) continue;
     const uint32_t per = (B - A + CT_WARPS - 1) / CT_WARPS;
     const uint32_t Lw = (per + 31u) & ~31u;
     const uint32_t w0 = A + (uint32_t)w * Lw, w1 = min(B, w0 + Lw);
     const int rounds = (int)((Lw + 32u * CT_E - 1) / (32u * CT_E));
     for (int r = 0; r < rounds; ++r) {
       const uint32_t ws = w0 + (uint32_t)r * 32u * CT_E;
-      body(j, lo_s, hi_s, ws, min(w1, ws + 32u * CT_E), r == rounds - 1);
+      body(j, lo_s, hi_s, ws, min(w1, ws + 32u * CT_E));
     }
   }
 }
@@ -400,12 +415,11 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
   __syncthreads();
   const int P_all = S.jpref[n_sub];
   for (int b0 = 0; b0 < P_all; b0 += CT_PB) {
-    const int nb = stage_slices(pops, cap, offs, offs_len, n_sub, K2, c, q, b0, S);
-    // software pipeline over the (subspace, round) steps
+    stage_slices(pops, cap, offs, offs_len, n_sub, K2, c, q, b0, S);
     uint32_t idA[CT_E], idB[CT_E];
     int nA = 0, jA = -1;
     bool haveA = false;
-    auto run_step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we, bool last_of_j) {
+    auto run_step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we) {
       int nB;
       fetch_round(ids, n, S, j, lo_s, hi_s, ws, we, idB, nB);
       if (haveA) {
@@ -418,9 +432,8 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       nA = nB;
       jA = j;
       haveA = true;
-      (void)last_of_j;
     };
-    for_each_round(S, n_sub, b0, nb, run_step);
+    for_each_round(S, n_sub, run_step);
     if (haveA) {
       if (n_sub <= 8) apply_round<true>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
       else apply_round<false>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
@@ -445,43 +458,6 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
     }
   }
   __syncthreads();
-}
-
-// Candidates of the last staged batch by re-walking its id lists: the first
-// time an id with score >= L is seen it is emitted and flagged (bit 7), so
-// every candidate is written exactly once (order irrelevant: ties break by id).
-__device__ void emit_candidates(const uint32_t* __restrict__ ids, int64_t n, int n_sub, uint8_t* table,
-                                uint32_t base, uint32_t L, uint32_t* dst, CountSmem& S) {
-  const int lane = threadIdx.x & 31;
-  const int nb = S.jpref[n_sub];   // single batch
-  auto step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we, bool last_of_j) {
-    uint32_t idv[CT_E];
-    int nv;
-    fetch_round(ids, n, S, j, lo_s, hi_s, ws, we, idv, nv);
-#pragma unroll
-    for (int i = 0; i < CT_E; ++i) {
-      bool e = false;
-      uint32_t x = 0;
-      if (i < nv) {
-        x = idv[i];
-        uint8_t* p = table + (x - base);
-        const uint32_t v = *p;
-        if (v >= L && v < 0x80u) {
-          *p = (uint8_t)(v | 0x80u);
-          e = true;
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, e);
-      if (m) {
-        uint32_t b = 0;
-        if (lane == 0) b = atomicAdd(&S.cursor, (uint32_t)__popc(m));
-        b = __shfl_sync(0xffffffffu, b, 0);
-        if (e) dst[b + __popc(m & ((1u << lane) - 1u))] = x;
-      }
-    }
-    if (last_of_j) __syncthreads();
-  };
-  for_each_round(S, n_sub, 0, nb, step);
 }
 
 // Level histogram of a chunk table.  n_sub <= 16: from the tallies; else by a
@@ -639,13 +615,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
   }
   cluster.sync();   // remote histograms no longer needed by anyone after this point
   if (s_base + s_cnt > cand_cap) return;
-  if (s_L >= 1 && S.batches == 1 && n_sub <= 127) {
-    if (tid == 0) S.cursor = 0;
-    __syncthreads();
-    emit_candidates(ids, n, n_sub, table, (uint32_t)base, (uint32_t)s_L, cand + s_base, S);
-  } else {
-    compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
-  }
+  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
 }
 
 // ------------------------------------------------------- global-mode count
