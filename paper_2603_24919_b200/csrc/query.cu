@@ -249,9 +249,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // 16-bit counters), which gives the level histogram without rescanning:
 // #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
-constexpr int CT_WARPS = CT_THREADS / 32;
 constexpr int CT_PB = 4096;   // slices staged per batch
-constexpr int CT_E = 8;       // 32-id steps per warp per round
+constexpr int CT_E = 16;      // ids fetched per thread per group
 
 struct CountSmem {
   int32_t dl[CT_PB];          // slice delta: the slice's id at flattened f is ids[j*n + dl + f]
@@ -327,73 +326,22 @@ __device__ void stage_slices(const uint16_t* __restrict__ pops, int cap, const u
   __syncthreads();
 }
 
-// One (subspace, round) step of a warp: fetch up to 32*CT_E ids into idv
-// (idv[i] is flattened id ws + 32 i + lane).  The slice of each lane is found
-// by counting, uniformly across the warp, the slice starts inside the 32-id
-// window (no divergent walk).
-__device__ __forceinline__ void fetch_round(const uint32_t* __restrict__ ids, int64_t n, const CountSmem& S,
-                                            int j, int lo_s, int hi_s, uint32_t ws, uint32_t we,
-                                            uint32_t* idv, int& nval) {
-  const int lane = threadIdx.x & 31;
-  nval = 0;
-  if (ws >= we) return;
-  int t0 = slice_in(S.pref, lo_s, hi_s, ws);
-  const uint32_t* src = ids + (size_t)j * n;
-#pragma unroll
-  for (int i = 0; i < CT_E; ++i) {
-    const uint32_t F = ws + (uint32_t)(i * 32);
-    if (F < we) {
-      while (t0 + 1 < hi_s && S.pref[t0 + 1] <= F) ++t0;           // uniform
-      const uint32_t f = F + (uint32_t)lane;
-      int tl = t0;
-      for (int k = t0 + 1; k < hi_s && S.pref[k] < F + 32u; ++k)   // uniform trip count
-        tl += S.pref[k] <= f ? 1 : 0;
-      if (f < we) {
-        idv[i] = __ldg(src + (int64_t)S.dl[tl] + f);
-        nval = i + 1;
-      }
-    }
-  }
-}
-
-template <bool SMALL>
-__device__ __forceinline__ void apply_round(uint8_t* table, uint32_t base, const uint32_t* idv, int nval,
-                                            uint64_t& lv0, uint64_t& lv1, uint64_t& lv2, uint64_t& lv3) {
-#pragma unroll
-  for (int i = 0; i < CT_E; ++i) {
-    if (i < nval) {
-      uint8_t* p = table + (idv[i] - base);
-      const uint32_t old = *p;
-      *p = (uint8_t)(old + 1);
-      const uint64_t inc = 1ull << ((old & 3u) << 4);
-      if (SMALL) {
-        if (old < 4) lv0 += inc; else lv1 += inc;
-      } else {
-        if (old < 4) lv0 += inc;
-        else if (old < 8) lv1 += inc;
-        else if (old < 12) lv2 += inc;
-        else lv3 += inc;
-      }
-    }
-  }
-}
-
-// Iterates the (subspace, round) steps of the staged batch in order.
-template <typename Body>
-__device__ __forceinline__ void for_each_round(const CountSmem& S, int n_sub, Body body) {
-  const int w = threadIdx.x >> 5;
-  for (int j = 0; j < n_sub; ++j) {
-    const int lo_s = S.js[j], hi_s = S.js[j + 1];
-    if (hi_s <= lo_s) continue;
-    const uint32_t A = S.pref[lo_s], B = S.pref[hi_s];
-    const uint32_t per = (B - A + CT_WARPS - 1) / CT_WARPS;
-    const uint32_t Lw = (per + 31u) & ~31u;
-    const uint32_t w0 = A + (uint32_t)w * Lw, w1 = min(B, w0 + Lw);
-    const int rounds = (int)((Lw + 32u * CT_E - 1) / (32u * CT_E));
-    for (int r = 0; r < rounds; ++r) {
-      const uint32_t ws = w0 + (uint32_t)r * 32u * CT_E;
-      body(j, lo_s, hi_s, ws, min(w1, ws + 32u * CT_E));
-    }
+// Phase B: the ids of ALL staged slices form one flattened list; every thread
+// owns a contiguous range of it, fetches CT_E ids at a time (the next group in
+// flight while the current one is applied) and increments the byte counters
+// with shared-memory atomics on their 32-bit word (byte lanes never carry:
+// scores <= n_sub <= 255).  Atomics make subspace ordering unnecessary -- no
+// barriers inside the count -- and return the old byte for the level tally.
+__device__ __forceinline__ void tally(uint32_t old, bool small, uint64_t& lv0, uint64_t& lv1,
+                                      uint64_t& lv2, uint64_t& lv3) {
+  const uint64_t inc = 1ull << ((old & 3u) << 4);
+  if (small) {
+    if (old < 4) lv0 += inc; else lv1 += inc;
+  } else {
+    if (old < 4) lv0 += inc;
+    else if (old < 8) lv1 += inc;
+    else if (old < 12) lv2 += inc;
+    else lv3 += inc;
   }
 }
 
@@ -402,6 +350,8 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
                             int64_t base, uint8_t* table, CountSmem& S) {
   const int tid = threadIdx.x;
+  const bool small = n_sub <= 8;
+  uint32_t* tw = reinterpret_cast<uint32_t*>(table);
   uint64_t lv0 = 0, lv1 = 0, lv2 = 0, lv3 = 0;   // packed per-level increment tallies
   if (tid == 0) {
     int acc = 0;
@@ -416,27 +366,56 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
   const int P_all = S.jpref[n_sub];
   for (int b0 = 0; b0 < P_all; b0 += CT_PB) {
     stage_slices(pops, cap, offs, offs_len, n_sub, K2, c, q, b0, S);
-    uint32_t idA[CT_E], idB[CT_E];
-    int nA = 0, jA = -1;
-    bool haveA = false;
-    auto run_step = [&](int j, int lo_s, int hi_s, uint32_t ws, uint32_t we) {
-      int nB;
-      fetch_round(ids, n, S, j, lo_s, hi_s, ws, we, idB, nB);
-      if (haveA) {
-        if (n_sub <= 8) apply_round<true>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
-        else apply_round<false>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
-        if (jA != j) __syncthreads();   // increments of a new subspace wait for the previous one
-      }
+    const int ns = S.js[n_sub];
+    const uint32_t total = S.pref[ns];
+    const uint32_t per = (total + CT_THREADS - 1) / CT_THREADS;
+    uint32_t f = per * tid;
+    const uint32_t fe = min(total, f + per);
+    if (f < fe) {
+      // slice of f, then walk forward with the bounds cached in registers
+      int t = slice_in(S.pref, 0, ns, f);
+      int jt = 0;
+      while (S.js[jt + 1] <= t) ++jt;
+      uint32_t nextb = S.pref[t + 1];
+      const uint32_t* src = ids + (size_t)jt * n + S.dl[t];
+      auto fetch = [&](uint32_t* idv, int& cnt) {
+        cnt = 0;
 #pragma unroll
-      for (int i = 0; i < CT_E; ++i) idA[i] = idB[i];
-      nA = nB;
-      jA = j;
-      haveA = true;
-    };
-    for_each_round(S, n_sub, run_step);
-    if (haveA) {
-      if (n_sub <= 8) apply_round<true>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
-      else apply_round<false>(table, (uint32_t)base, idA, nA, lv0, lv1, lv2, lv3);
+        for (int e = 0; e < CT_E; ++e) {
+          if (f < fe) {
+            while (f >= nextb) {
+              ++t;
+              while (S.js[jt + 1] <= t) ++jt;
+              nextb = S.pref[t + 1];
+              src = ids + (size_t)jt * n + S.dl[t];
+            }
+            idv[e] = __ldg(src + f);
+            ++f;
+            cnt = e + 1;
+          }
+        }
+      };
+      auto apply = [&](const uint32_t* idv, int cnt) {
+#pragma unroll
+        for (int e = 0; e < CT_E; ++e) {
+          if (e < cnt) {
+            const uint32_t x = idv[e] - (uint32_t)base;
+            const uint32_t sh = (x & 3u) << 3;
+            const uint32_t old = (atomicAdd(tw + (x >> 2), 1u << sh) >> sh) & 0xFFu;
+            tally(old, small, lv0, lv1, lv2, lv3);
+          }
+        }
+      };
+      uint32_t idA[CT_E], idB[CT_E];
+      int nA, nB;
+      fetch(idA, nA);
+      while (nA > 0) {
+        fetch(idB, nB);
+        apply(idA, nA);
+#pragma unroll
+        for (int e = 0; e < CT_E; ++e) idA[e] = idB[e];
+        nA = nB;
+      }
     }
     __syncthreads();
   }
