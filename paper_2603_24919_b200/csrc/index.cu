@@ -169,7 +169,7 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
   idx->D = n_subspaces * subspace_dim;
   idx->iters = kmeans_iters;
   if (n_global == n && n <= kClusterMaxN) {
-    const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, 131072)));
+    const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, 65536)));
     idx->chunk = ceil_div(ceil_div(n, ctas), 1024) * 1024;
     idx->cluster_mode = true;
   } else {

@@ -19,12 +19,12 @@
 namespace taco {
 
 // Score-table chunk: the id range one CTA counts in shared memory.
-//  cluster mode (single GPU, n <= kClusterMaxN): n is split over <= 8 CTAs of
-//    one thread-block cluster, chunk = ceil(n / ctas) rounded to 1 KiB;
+//  cluster mode (single GPU, n <= kClusterMaxN): n is split over <= 16 CTAs of
+//    one thread-block cluster (~64 KiB each), chunk = ceil(n / ctas) rounded to 1 KiB;
 //  global mode (larger shards / multi-GPU): chunk = 64 KiB, tables in HBM.
 constexpr int64_t kGlobalChunk = 65536;
-constexpr int64_t kClusterMaxChunk = 184320;   // + ~40 KiB static smem <= 227 KiB
-constexpr int kClusterMaxCtas = 8;
+constexpr int64_t kClusterMaxChunk = 98304;    // 2 CTAs (+ ~20 KiB static smem each) per SM
+constexpr int kClusterMaxCtas = 16;             // non-portable cluster size
 constexpr int64_t kClusterMaxN = kClusterMaxChunk * kClusterMaxCtas;
 
 struct DevBuf {

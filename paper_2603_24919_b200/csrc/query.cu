@@ -249,8 +249,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // 16-bit counters), which gives the level histogram without rescanning:
 // #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
-constexpr int CT_PB = 4096;   // slices staged per batch
-constexpr int CT_E = 16;      // ids fetched per thread per group
+constexpr int CT_PB = 2048;   // slices staged per batch
+constexpr int CT_E = 8;       // ids fetched per thread per group
 
 struct CountSmem {
   int32_t dl[CT_PB];          // slice delta: the slice's id at flattened f is ids[j*n + dl + f]
@@ -545,7 +545,7 @@ __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& 
 // ------------------------------------------------- cluster-fused count/select
 // Candidates of a query live in per-CTA segments (segment q*S + rank); the
 // final top-k breaks distance ties by id, so segment order is irrelevant.
-__global__ void __launch_bounds__(CT_THREADS, 1) k_count_cluster(
+__global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
@@ -1452,6 +1452,7 @@ static int set_count_attrs(taco_index* idx) {
   if (idx->cluster_mode && cur_c < idx->chunk) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kClusterMaxChunk));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cur_c = kClusterMaxChunk;
   }
   if (cur_g < kClusterMaxChunk) {
