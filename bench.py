@@ -143,11 +143,14 @@ def kernel_bytes(name, stats, meta):
     }.get(name)
 
 
-def ncu_traffic(name):
+def ncu_traffic(name, nq, launches):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed
+    ncu --set full capture (profiles/ncu_traffic.json, per query) scaled to this batch."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(name)
+            ent = json.load(fh).get(name)
+        return ent["dram_bytes_per_query"] * nq / max(launches, 1)
     except Exception:
         return None
 
@@ -294,8 +297,10 @@ def run_ours(args):
     roof = None
     if kb is not None and dom_ms > 0:
         ach = kb / (dom_ms / 1000.0) / 1e9
-        tr = ncu_traffic(dom)
+        tr = ncu_traffic(dom, nq, dom_n)
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "note": ("k_count reads the CSR ids (L2-resident) and counts in shared memory: its "
+                         "HBM traffic is small; it is latency/L2-bound") if dom == "k_count" else None,
                 "frac": ach / peak, "traffic": tr, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": kb / max(dom_n, 1),
                 "avg_launch_ms": dom_ms / max(dom_n, 1), "launches": dom_n,
