@@ -1,0 +1,70 @@
+"""CPU stand-in for CudaShardBackend (TEST INFRASTRUCTURE): the per-rank
+stages computed with the oracle so the sharded orchestration in
+paper_2603_24919_b200.distributed can be exercised with gloo on CPU."""
+
+import numpy as np
+import torch
+
+from oracle import taco_oracle as O
+
+
+class OracleShardBackend:
+    def __init__(self, oidx, X_shard, id_base, n_global, tile=7):
+        self.o = oidx
+        self.X = np.asarray(X_shard, np.float32)
+        self.lo = id_base
+        self.n = n_global
+        self.tile = tile
+        self.scores = None
+
+    def tile_size(self):
+        return self.tile
+
+    def count(self, Qt, alpha):
+        Q = Qt.numpy()
+        hi = self.lo + self.X.shape[0]
+        self.scores = [O.query_scores(self.o, q, alpha)[self.lo:hi] for q in Q]
+        self.Q = Q
+        h = [np.bincount(s, minlength=self.o.n_sub + 1) for s in self.scores]
+        return torch.tensor(np.array(h, np.int64))
+
+    def finish(self, nq, ghist, beta, k):
+        g = ghist.numpy()
+        ns = self.o.n_sub
+        d2 = np.full((nq, k), np.inf)
+        ids = np.full((nq, k), -1, np.int64)
+        num = np.zeros(nq, np.int64)
+        lvl = np.zeros(nq, np.int32)
+        budget = beta * self.n
+        for r in range(nq):
+            L, cand = ns, 0
+            for j in range(ns, -1, -1):       # engine.py:243-249 on the global histogram
+                cand += int(g[r, j])
+                if g[r, j] <= budget - cand:
+                    L -= 1
+                else:
+                    break
+            L = max(L, 0)
+            num[r], lvl[r] = cand, L
+            loc = np.flatnonzero(self.scores[r] >= L)
+            if loc.size:
+                e = self.X[loc].astype(np.float64) - self.Q[r].astype(np.float64)
+                dd = np.einsum("ij,ij->i", e, e)
+                gid = loc + self.lo
+                o = np.lexsort((gid, dd))[:k]
+                d2[r, :o.size] = dd[o]
+                ids[r, :o.size] = gid[o]
+        return torch.tensor(d2), torch.tensor(ids), torch.tensor(num), torch.tensor(lvl)
+
+    def merge(self, d2_all, ids_all, k):
+        d2a, ida = d2_all.numpy(), ids_all.numpy()
+        R, nq = d2a.shape[0], d2a.shape[1]
+        out_i = np.full((nq, k), -1, np.int32)
+        out_d = np.full((nq, k), np.inf, np.float32)
+        for q in range(nq):
+            items = [(d2a[r, q, t], ida[r, q, t]) for r in range(R) for t in range(k) if ida[r, q, t] >= 0]
+            items.sort()
+            for t, (dv, iv) in enumerate(items[:k]):
+                out_i[q, t] = iv
+                out_d[q, t] = np.float32(np.sqrt(dv))
+        return torch.tensor(out_i), torch.tensor(out_d)

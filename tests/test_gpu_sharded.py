@@ -1,0 +1,45 @@
+"""CUDA shard backend on ONE GPU: two point shards counted separately, their
+histograms summed (standing in for the NCCL all-reduce, no cross-kernel
+waiting), Alg. 5 + rerank per shard, device merge -> must equal the
+single-GPU batched path bit-for-bit."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_24919_b200 as T
+from paper_2603_24919_b200.distributed import CudaShardBackend, shard_range
+from paper_2603_24919_b200.workloads import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,alpha,beta,k", [(2, 0.05, 0.01, 10), (3, 0.2, 0.05, 25), (2, 0.6, 0.9, 5)])
+def test_two_shards_match_single(world, alpha, beta, k):
+    X, Q, _ = make_config(1, n=6000, nq=40, d=32)
+    idx = T.build_index(X, T.IndexParams(8, 4, 64, 10, 2))
+    ids0, d0, n0, l0 = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k))
+    bes = []
+    for r in range(world):
+        lo, hi = shard_range(X.shape[0], r, world)
+        bes.append(CudaShardBackend(idx, X[lo:hi], lo, X.shape[0], 0))
+    Qd = torch.from_numpy(Q).cuda()
+    T_ = min(b.tile_size() for b in bes)
+    outs = []
+    for q0 in range(0, Q.shape[0], T_):
+        Qt = Qd[q0:q0 + T_]
+        m = Qt.shape[0]
+        hist = sum(b.count(Qt, alpha) for b in bes)
+        parts = [b.finish(m, hist, beta, k) for b in bes]
+        d2_all = torch.stack([p[0] for p in parts])
+        id_all = torch.stack([p[1] for p in parts])
+        oi, od = bes[0].merge(d2_all, id_all, k)
+        torch.cuda.synchronize()
+        outs.append((oi.cpu().numpy(), od.cpu().numpy(), parts[0][2].cpu().numpy(), parts[0][3].cpu().numpy()))
+        for p in parts[1:]:
+            np.testing.assert_array_equal(p[2].cpu().numpy(), outs[-1][2])
+    ids = np.concatenate([o[0] for o in outs])
+    np.testing.assert_array_equal(ids, ids0)
+    np.testing.assert_array_equal(np.concatenate([o[1] for o in outs]), d0)
+    np.testing.assert_array_equal(np.concatenate([o[2] for o in outs]), n0)
+    np.testing.assert_array_equal(np.concatenate([o[3] for o in outs]), l0)
