@@ -178,3 +178,14 @@ def profile_read(reset=True):
     names = [lib().taco_profile_name(i).decode() for i in range(nk)]
     keys = ("sum_retrieved", "sum_candidates", "sum_pops", "queries", "tiles", "score_bytes")
     return {n: (float(m), int(c)) for n, m, c in zip(names, ms, cnt)}, dict(zip(keys, map(int, st)))
+
+
+CUDA_STREAM_LEGACY = 0x1   # cudaStreamLegacy
+
+
+def torch_stream(torch, device=None) -> int:
+    """Handle of torch's current stream for the C ABI.  torch reports the legacy
+    default stream as 0, which the C ABI reads as "the index's own stream";
+    map it to cudaStreamLegacy so library work is ordered with torch's."""
+    h = torch.cuda.current_stream(device).cuda_stream
+    return h if h else CUDA_STREAM_LEGACY

@@ -85,7 +85,7 @@ class CudaShardBackend:
         return self.tile
 
     def _stream(self):
-        return self.torch.cuda.current_stream(self.device).cuda_stream
+        return nat.torch_stream(self.torch, self.device)
 
     def count(self, Qt, alpha: float):
         torch = self.torch
