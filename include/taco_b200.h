@@ -13,7 +13,8 @@
  *
  * Pointers suffixed _h are host memory, _d device memory (cuda:device of
  * the index).  Stream arguments are cudaStream_t passed as void*; NULL is
- * the index's own stream.
+ * the index's own (non-blocking) stream -- pass cudaStreamLegacy ((void*)1)
+ * to order work with the legacy default stream.
  */
 #ifndef TACO_B200_H
 #define TACO_B200_H
