@@ -133,6 +133,9 @@ int taco_topk_merge_device(int32_t ranks, int64_t nq, int32_t k, const double* d
                            const int64_t* ids_d, int32_t* ids_out_d, float* dists_out_d,
                            void* stream);
 
+/* Test hook: 1 forces every k-means++ draw through the exact numpy replay. */
+int taco_debug_force_replay(int on);
+
 /* --------------------------------------------------------------- profiling */
 /* Per-kernel CUDA-event timing of the query path on its launching stream. */
 int taco_profile_enable(int on);

@@ -62,6 +62,7 @@ _SIGS = {
     "taco_centroid_order": [_c_int, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_traverse": [_c_int, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp],
     "taco_transform_points": [_c_int, _vp, _vp, _c_i32, _c_i32, _vp, _c_i64, _vp],
+    "taco_debug_force_replay": [_c_int],
     "taco_profile_enable": [_c_int],
     "taco_profile_read": [_vp, _vp, _vp, _c_int],
     "taco_profile_name": [_c_int],

@@ -118,6 +118,8 @@ constexpr int PP_PPT = 4;                       // points per thread in one bloc
 constexpr int PP_BLOCK = PP_THREADS * PP_PPT;   // points per block-sum
 constexpr double U0 = 1.1102230246251565e-16;   // 2^-53
 
+static int g_force_replay = 0;   // test hook: always take the exact replay
+
 struct HalfView {
   const float* X;   // dimension-major: X[t*n + i]
   int64_t n;
@@ -192,43 +194,63 @@ __global__ void __launch_bounds__(PP_THREADS) k_pp_update(HalfView h, const doub
   }
 }
 
-// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) of a
-// contiguous double array, restated for the exact fallback path.
-__device__ double np_pairwise(const double* a, int64_t n) {
-  // explicit stack of (ptr offset, len, state)
-  struct Fr { int64_t off, len; double left; int state; };
+// numpy pairwise summation (loops_utils.h.src, as measured in DESIGN.md §4):
+// n < 8 sequential; n <= 128 eight strided accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail; else split at
+// n2 = n/2 - (n/2)%8 and add the halves.  The leaves (ranges <= 128) depend
+// only on n and are listed once on the host in depth-first order.
+static void pairwise_leaves(int64_t off, int64_t len, std::vector<int64_t>& out) {
+  if (len <= 128) {
+    out.push_back(off);
+    out.push_back(len);
+    return;
+  }
+  int64_t n2 = len / 2;
+  n2 -= n2 % 8;
+  pairwise_leaves(off, n2, out);
+  pairwise_leaves(off + n2, len - n2, out);
+}
+
+__device__ double np_leaf(const double* a, int64_t len) {
+  if (len < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int64_t i = 8;
+  for (; i < len - (len % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < len; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// Combines the leaf sums (in depth-first order) exactly as the recursion does.
+__device__ double np_combine(const double* leaf, int64_t n) {
+  struct Fr { int64_t len; double left; int state; };
   Fr st[64];
   int sp = 0;
-  st[sp++] = {0, n, 0.0, 0};
+  int64_t li = 0;
+  st[sp++] = {n, 0.0, 0};
   double ret = 0.0;
   while (sp > 0) {
     Fr& f = st[sp - 1];
-    if (f.len < 8) {
-      double r = 0.0;
-      for (int64_t i = 0; i < f.len; ++i) r = __dadd_rn(r, a[f.off + i]);
-      ret = r;
-      --sp;
-    } else if (f.len <= 128) {
-      double r[8];
-      for (int j = 0; j < 8; ++j) r[j] = a[f.off + j];
-      int64_t i = 8;
-      for (; i < f.len - (f.len % 8); i += 8)
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[f.off + i + j]);
-      double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-      for (; i < f.len; ++i) res = __dadd_rn(res, a[f.off + i]);
-      ret = res;
+    if (f.len <= 128) {
+      ret = leaf[li++];
       --sp;
     } else {
       int64_t n2 = f.len / 2;
       n2 -= n2 % 8;
       if (f.state == 0) {
         f.state = 1;
-        st[sp++] = {f.off, n2, 0.0, 0};
+        st[sp++] = {n2, 0.0, 0};
       } else if (f.state == 1) {
         f.left = ret;
         f.state = 2;
-        st[sp++] = {f.off + n2, f.len - n2, 0.0, 0};
+        st[sp++] = {f.len - n2, 0.0, 0};
       } else {
         ret = __dadd_rn(f.left, ret);
         --sp;
@@ -250,9 +272,12 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
                                                           const int64_t* __restrict__ forced,
                                                           double xsqmax, int ci,
                                                           int64_t* __restrict__ picks,
-                                                          int64_t* __restrict__ status) {
+                                                          int64_t* __restrict__ status,
+                                                          const int64_t* __restrict__ leaves, int64_t nleaves,
+                                                          double* __restrict__ lsum, double* __restrict__ pbuf,
+                                                          double* __restrict__ cbuf, int force_replay) {
   __shared__ double wsum[32];
-  __shared__ double s_total;
+  __shared__ double s_S;
   __shared__ int64_t s_blk;
   __shared__ double s_before;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -280,11 +305,11 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
       if (lane >= o) w = __dadd_rn(w, x);
     }
     wsum[lane] = w;
-    if (lane == 31) s_total = w;
+    if (lane == 31) s_S = w;
   }
   if (tid == 0) s_blk = -1;
   __syncthreads();
-  const double S = s_total;
+  const double S = s_S;
   if (!(S > 0.0)) {
     // reference: total == 0 -> rng.integers(n); the host replays this draw
     if (tid == 0) {
@@ -309,14 +334,14 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
     }
   }
   __syncthreads();
+  __shared__ int s_ok;
+  __shared__ double s_total;
   int64_t blk = s_blk;
   if (tid == 0) {
     int64_t kstar = -1;
     double Pk = 0.0, Pkm1 = 0.0;
-    if (blk < 0) {  // rounding put the target at/after the end: take the last positive point
-      blk = nb - 1;
-    }
-    double pre = blk >= 0 && s_blk >= 0 ? s_before : S - bsum[blk];
+    if (blk < 0) blk = nb - 1;   // rounding put the target at/after the end
+    double pre = s_blk >= 0 ? s_before : S - bsum[blk];
     const int64_t i0 = blk * PP_BLOCK, i1 = min(h.n, i0 + PP_BLOCK);
     for (int64_t i = i0; i < i1; ++i) {
       const double nx = __dadd_rn(pre, best[i]);
@@ -331,25 +356,56 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
     const double rel = (2.0 * n + 4.0 * log2(n + 2.0) + 4.0 * PP_BLOCK + 256.0) * U0;
     const double absU = 32.0 * U0 * n * xsqmax;
     const double margin = 3.0 * rel * S + 2.0 * absU;
-    bool ok = (Pk - target > margin) && (target - Pkm1 >= margin);
-    if (ok) {
-      picks[draw] = kstar;
-    } else {
-      // exact replay of Generator.choice(n, p=best/total)
-      const double total = np_pairwise(best, h.n);
-      double cdf = 0.0;
-      // cdf_last first (sequential cumsum of p = best/total)
-      for (int64_t i = 0; i < h.n; ++i) cdf = __dadd_rn(cdf, __ddiv_rn(best[i], total));
-      const double last = cdf;
-      cdf = 0.0;
-      int64_t idx = h.n - 1;
-      for (int64_t i = 0; i < h.n; ++i) {
-        cdf = __dadd_rn(cdf, __ddiv_rn(best[i], total));
-        if (__ddiv_rn(cdf, last) > u) { idx = i; break; }
+    s_ok = !force_replay && (Pk - target > margin) && (target - Pkm1 >= margin);
+    if (s_ok) picks[draw] = kstar;
+  }
+  __syncthreads();
+  if (s_ok) return;
+  // ---- exact replay of Generator.choice(n, p=best/total) (clustering.py:48):
+  // total = numpy pairwise sum; p = best/total; cdf = sequential cumsum;
+  // idx = first i with fl(cdf_i / cdf_last) > u.  Everything but the cumsum
+  // chain runs on all threads of the block.
+  for (int64_t l = tid; l < nleaves; l += PS_THREADS) lsum[l] = np_leaf(best + leaves[2 * l], leaves[2 * l + 1]);
+  __syncthreads();
+  if (tid == 0) s_total = np_combine(lsum, h.n);
+  __syncthreads();
+  const double total = s_total;
+  for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(best[i], total);
+  __syncthreads();
+  if (tid == 0) {
+    double c = 0.0;
+    int64_t i = 0;
+    for (; i + 8 <= h.n; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = pbuf[i + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        c = __dadd_rn(c, v[t]);
+        cbuf[i + t] = c;
       }
-      picks[draw] = idx;
-      status[1] += 1;
     }
+    for (; i < h.n; ++i) {
+      c = __dadd_rn(c, pbuf[i]);
+      cbuf[i] = c;
+    }
+    s_total = c;   // cdf[-1]
+  }
+  __syncthreads();
+  const double last = s_total;
+  __shared__ unsigned long long s_first;
+  if (tid == 0) s_first = (unsigned long long)(h.n - 1);
+  __syncthreads();
+  for (int64_t i = tid; i < h.n; i += PS_THREADS) {
+    if (__ddiv_rn(cbuf[i], last) > u) {
+      atomicMin(&s_first, (unsigned long long)i);
+      break;   // later i of this thread are larger
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    picks[draw] = (int64_t)s_first;
+    status[1] += 1;
   }
 }
 
@@ -537,7 +593,6 @@ __global__ void k_reseed(HalfView h, const int64_t* __restrict__ status,
   if (status[2]) return;
   __shared__ double bv[32];
   __shared__ int64_t bi[32];
-  __shared__ int64_t s_p;
   for (int c = 0; c < h.k; ++c) {
     if (counts[c] != 0) continue;
     double v = -INFINITY;
@@ -558,7 +613,6 @@ __global__ void k_reseed(HalfView h, const int64_t* __restrict__ status,
       int64_t wi = bi[0];
       for (int k2 = 1; k2 < (int)(blockDim.x >> 5); ++k2)
         if (bv[k2] > w || (bv[k2] == w && bi[k2] < wi)) { w = bv[k2]; wi = bi[k2]; }
-      s_p = wi;
       for (int t = 0; t < h.m; ++t) C64[(size_t)c * h.m + t] = (double)h.X[(size_t)t * h.n + wi];
       lab[wi] = c;
       far[wi] = -1.0;
@@ -619,6 +673,16 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
   TACO_TRY(s.ctl.ensure(8 * k));       // counts
   TACO_TRY(s.hsum.ensure(8 * nba));
   TACO_TRY(s.draws.ensure(8 * nbx));   // xsq block maxima
+  if (s.leaves_n != n) {                // numpy pairwise leaves of an n-array (exact replay)
+    std::vector<int64_t> lv;
+    pairwise_leaves(0, n, lv);
+    s.nleaves = (int64_t)lv.size() / 2;
+    TACO_TRY(s.leaves.ensure(8 * lv.size()));
+    TACO_CHECK_CUDA(cudaMemcpy(s.leaves.p, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice));
+    s.leaves_n = n;
+  }
+  TACO_TRY(s.pbuf.ensure(8 * std::max<int64_t>(n, s.nleaves)));
+  TACO_TRY(s.cbuf.ensure(8 * n));
   // xsq + its maximum (bound for the certified draw)
   k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.draws.as<double>());
   TACO_LAUNCHED();
@@ -643,7 +707,9 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
     if (ci + 1 < k) {
       k_pp_search<<<1, PS_THREADS, 0, st>>>(h, s.best.as<double>(), s.bsum.as<double>(), nbp,
                                             s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
-                                            xsqmax, ci, s.picks.as<int64_t>(), s.status.as<int64_t>());
+                                            xsqmax, ci, s.picks.as<int64_t>(), s.status.as<int64_t>(),
+                                            s.leaves.as<int64_t>(), s.nleaves, s.cbuf.as<double>(),
+                                            s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
       TACO_LAUNCHED();
     }
   }
@@ -944,6 +1010,12 @@ int taco_get_local_sizes(taco_index* idx, int64_t* sizes_h) {
   return TACO_OK;
 }
 
+// Test hook: 1 = every k-means++ draw takes the exact numpy replay path.
+int taco_debug_force_replay(int on) {
+  g_force_replay = on ? 1 : 0;
+  return TACO_OK;
+}
+
 int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, int32_t max_iter,
                 int64_t first, const double* uniforms_h, const int64_t* forced_h, float* centroids_h,
                 int32_t* labels_h, double* history_h, int32_t* n_iter_h, int32_t* degenerate_h) {
@@ -987,7 +1059,8 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
   } while (0);
   X.release(); lab.release(); hist.release(); nit.release(); cent.release();
   DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
-                  &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws};
+                  &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws,
+                  &s.leaves, &s.pbuf, &s.cbuf};
   for (auto* b : sb) b->release();
   return rc;
 }

@@ -45,7 +45,8 @@ struct QueryTile {
 
 struct BuildScratch {
   DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
-      loff, ctl, hsum, draws;
+      loff, ctl, hsum, draws, leaves, pbuf, cbuf;
+  int64_t nleaves = 0, leaves_n = -1;
 };
 
 }  // namespace taco

@@ -134,3 +134,19 @@ def test_build_validation():
     one = T.build_index(X, T.IndexParams(n_subspaces=1, subspace_dim=4, clusters=1, kmeans_iters=3))
     (cells,) = [s.cells for s in one.subspaces]
     assert list(cells) == [(0, 0)] and cells[(0, 0)].size == 50
+
+
+def test_kmeans_exact_replay_path():
+    """Force every k-means++ draw through the exact numpy replay (taken in
+    production only when the certified fast path is ambiguous)."""
+    from paper_2603_24919_b200 import _native as nat
+    nat.call("taco_debug_force_replay", 1)
+    try:
+        for shape, k, seed in [((5000, 8), 64, 1), ((3001, 5), 17, 4), ((1000, 3), 40, 13)]:
+            X = np.random.default_rng(seed).normal(size=shape).astype(np.float32)
+            r = T.kmeans(X, k, 10, seed)
+            o = O.kmeans(X, k, 10, seed)
+            np.testing.assert_array_equal(r.assignments, o.labels)
+            np.testing.assert_array_equal(r.centroids, o.centroids)
+    finally:
+        nat.call("taco_debug_force_replay", 0)
