@@ -13,6 +13,7 @@
 //               counting sort by (l1,l2) into the chunk-major CSR     imi.py:70-81
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -349,13 +350,16 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
       pre = nx;
     }
     if (kstar < 0) { kstar = i1 - 1; Pk = pre; Pkm1 = pre - best[kstar]; }
-    // error budget: numpy cumsum (n terms) + normalisation, our tree sums,
-    // and the reference's best[] differing from ours by rounding of the
-    // (dgemv-ordered) dot products: |delta d2| <= 8u0 (|x| + |c|)^2.
+    // Error budget (rigorous, first order + slack): the reference's
+    // cdf_k / cdf_last deviates from B_k/B_n by at most (k + n + 3)u
+    // (sequential cumsum of k and n terms, p = b/T roundings, the division);
+    // our fp64 prefix has <= ~1100u relative error (block tree + the final
+    // in-block chain); the reference's best[] may differ from ours by the
+    // rounding of its dgemv-ordered dot products: |delta d2| <= 8u(|x|+|c|)^2.
     const double n = (double)h.n;
-    const double rel = (2.0 * n + 4.0 * log2(n + 2.0) + 4.0 * PP_BLOCK + 256.0) * U0;
+    const double rel = ((double)kstar + n + 1200.0) * U0 * 1.05;
     const double absU = 32.0 * U0 * n * xsqmax;
-    const double margin = 3.0 * rel * S + 2.0 * absU;
+    const double margin = rel * S + 2.0 * absU;
     s_ok = !force_replay && (Pk - target > margin) && (target - Pkm1 >= margin);
     if (s_ok) picks[draw] = kstar;
   }
@@ -372,39 +376,47 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   const double total = s_total;
   for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(best[i], total);
   __syncthreads();
-  if (tid == 0) {
+  // cdf_last: the sequential chain (loads double-buffered 32 ahead)
+  auto chain = [&](double c_stop, int64_t& stop_at) -> double {
     double c = 0.0;
     int64_t i = 0;
-    for (; i + 8 <= h.n; i += 8) {
-      double v[8];
+    double va[32], vb[32];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = pbuf[i + t];
+    for (int t = 0; t < 32; ++t) va[t] = i + t < h.n ? pbuf[i + t] : 0.0;
+    while (i < h.n) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        c = __dadd_rn(c, v[t]);
-        cbuf[i + t] = c;
+      for (int t = 0; t < 32; ++t) vb[t] = i + 32 + t < h.n ? pbuf[i + 32 + t] : 0.0;
+      const int lim = (int)min((int64_t)32, h.n - i);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (t < lim) {
+          c = __dadd_rn(c, va[t]);
+          if (c > c_stop) { stop_at = i + t; return c; }
+        }
       }
+      i += 32;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) va[t] = vb[t];
     }
-    for (; i < h.n; ++i) {
-      c = __dadd_rn(c, pbuf[i]);
-      cbuf[i] = c;
-    }
-    s_total = c;   // cdf[-1]
-  }
-  __syncthreads();
-  const double last = s_total;
-  __shared__ unsigned long long s_first;
-  if (tid == 0) s_first = (unsigned long long)(h.n - 1);
-  __syncthreads();
-  for (int64_t i = tid; i < h.n; i += PS_THREADS) {
-    if (__ddiv_rn(cbuf[i], last) > u) {
-      atomicMin(&s_first, (unsigned long long)i);
-      break;   // later i of this thread are larger
-    }
-  }
-  __syncthreads();
+    stop_at = h.n - 1;
+    return c;
+  };
   if (tid == 0) {
-    picks[draw] = (int64_t)s_first;
+    int64_t dummy;
+    const double last = chain(INFINITY, dummy);          // cdf[-1]
+    // largest c with fl(c / last) <= u: searchsorted(cdf / last, u, 'right')
+    // == first i with cdf_i > c_thr (fl(c/last) is monotone in c)
+    double c_thr = __dmul_rn(u, last);
+    // c_thr >= 0: neighbouring doubles are the bit patterns -1 / +1
+    while (__ddiv_rn(c_thr, last) > u) c_thr = __longlong_as_double(__double_as_longlong(c_thr) - 1);
+    while (true) {
+      const double nx = __longlong_as_double(__double_as_longlong(c_thr) + 1);
+      if (__ddiv_rn(nx, last) > u) break;
+      c_thr = nx;
+    }
+    int64_t idx = h.n - 1;
+    chain(c_thr, idx);
+    picks[draw] = idx;
     status[1] += 1;
   }
 }
@@ -559,9 +571,22 @@ __global__ void k_label_scatter(int64_t n, int k, const int64_t* __restrict__ st
   }
 }
 
+// xs[t][k] = X[t][perm[k]]: every cluster's values become one contiguous run
+// (label-sorted, index order inside a label) for the sequential sums below.
+__global__ void k_gather_sorted(HalfView h, const int64_t* __restrict__ status, const int64_t* __restrict__ perm,
+                                float* __restrict__ xs) {
+  if (status[2]) return;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= h.n) return;
+  const int64_t p = perm[k];
+  for (int t = 0; t < h.m; ++t) xs[(size_t)t * h.n + k] = h.X[(size_t)t * h.n + p];
+}
+
 // centroid = (sequential fp64 sum over the cluster's points in index order) / count
+// -- np.add.at order (clustering.py:96).  One thread per (cluster, dim) runs
+// the dependent add chain over a contiguous, prefetchable run of xs.
 __global__ void k_cluster_sums(HalfView h, const int64_t* __restrict__ status,
-                               const int64_t* __restrict__ perm, const int64_t* __restrict__ counts,
+                               const float* __restrict__ xs, const int64_t* __restrict__ counts,
                                double* __restrict__ C64) {
   if (status[2]) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -571,17 +596,17 @@ __global__ void k_cluster_sums(HalfView h, const int64_t* __restrict__ status,
   if (cnt == 0) return;
   int64_t start = 0;
   for (int c2 = 0; c2 < c; ++c2) start += counts[c2];
-  const float* xt = h.X + (size_t)t * h.n;
+  const float* x = xs + (size_t)t * h.n + start;
   double acc = 0.0;
   int64_t p = 0;
-  for (; p + 8 <= cnt; p += 8) {
-    float v[8];
+  for (; p + 16 <= cnt; p += 16) {
+    float v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(xt + perm[start + p + u]);
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(x + p + u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+    for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, (double)v[u]);
   }
-  for (; p < cnt; ++p) acc = __dadd_rn(acc, (double)xt[perm[start + p]]);
+  for (; p < cnt; ++p) acc = __dadd_rn(acc, (double)x[p]);
   C64[(size_t)c * h.m + t] = __ddiv_rn(acc, (double)cnt);
 }
 
@@ -682,7 +707,7 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
     s.leaves_n = n;
   }
   TACO_TRY(s.pbuf.ensure(8 * std::max<int64_t>(n, s.nleaves)));
-  TACO_TRY(s.cbuf.ensure(8 * n));
+  TACO_TRY(s.cbuf.ensure(std::max<size_t>(8 * n, 4 * (size_t)n * m)));   // replay cdf / sorted X
   // xsq + its maximum (bound for the certified draw)
   k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.draws.as<double>());
   TACO_LAUNCHED();
@@ -699,6 +724,11 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
   }
   k_status_init<<<1, 1, 0, st>>>(s.status.as<int64_t>(), k);
   TACO_LAUNCHED();
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (getenv("TACO_DEBUG_TIMING")) {
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[0], st);
+  }
   for (int ci = 0; ci < k; ++ci) {
     k_pp_update<<<(unsigned)nbp, PP_THREADS, 0, st>>>(h, s.xsq.as<double>(), s.picks.as<int64_t>(), ci,
                                                       s.best.as<double>(), s.C64.as<double>(),
@@ -713,6 +743,7 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
       TACO_LAUNCHED();
     }
   }
+  if (ev[1]) cudaEventRecord(ev[1], st);
   const size_t ash = sizeof(double) * ((size_t)k * m + k);
   auto* kas = m <= 8 ? k_assign<8> : m <= 16 ? k_assign<16> : k_assign<32>;
   if (ash > 48 * 1024)
@@ -734,8 +765,11 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
     k_label_scatter<<<(unsigned)ntile, 32, 0, st>>>(n, k, s.status.as<int64_t>(), r.labels,
                                                     s.loff.as<int64_t>(), s.perm.as<int64_t>());
     TACO_LAUNCHED();
-    k_cluster_sums<<<(unsigned)ceil_div((int64_t)k * m, 128), 128, 0, st>>>(
-        h, s.status.as<int64_t>(), s.perm.as<int64_t>(), s.ctl.as<int64_t>(), s.C64.as<double>());
+    k_gather_sorted<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(h, s.status.as<int64_t>(), s.perm.as<int64_t>(),
+                                                               s.cbuf.as<float>());
+    TACO_LAUNCHED();
+    k_cluster_sums<<<(unsigned)ceil_div((int64_t)k * m, 32), 32, 0, st>>>(
+        h, s.status.as<int64_t>(), s.cbuf.as<float>(), s.ctl.as<int64_t>(), s.C64.as<double>());
     TACO_LAUNCHED();
     k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), s.ctl.as<int64_t>(), s.pd.as<double>(),
                                  r.labels, s.C64.as<double>());
@@ -744,6 +778,10 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
   k_centroids_out<<<(unsigned)ceil_div((int64_t)k * m, 256), 256, 0, st>>>(s.C64.as<double>(), k * m,
                                                                             r.cent_out);
   TACO_LAUNCHED();
+  if (ev[2]) {
+    cudaEventRecord(ev[2], st);
+    s.ev[0] = ev[0]; s.ev[1] = ev[1]; s.ev[2] = ev[2];
+  }
   return TACO_OK;
 }
 
@@ -940,6 +978,15 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
       TACO_CHECK_CUDA(cudaMemcpyAsync(status_h.data(), idx->bs[hh - w0].status.p, 8 * 5, cudaMemcpyDeviceToHost, st));
       TACO_CHECK_CUDA(cudaStreamSynchronize(st));
       degenerate_h[hh] = (int32_t)status_h[0];
+      BuildScratch& bs = idx->bs[hh - w0];
+      if (bs.ev[2]) {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, bs.ev[0], bs.ev[1]);
+        cudaEventElapsedTime(&b, bs.ev[1], bs.ev[2]);
+        fprintf(stderr, "[taco] half %d: k-means++ %.1f ms (replays %lld), Lloyd %.1f ms (iters %lld)\n", hh, a,
+                (long long)status_h[1], b, (long long)status_h[3]);
+        for (auto& e : bs.ev) { cudaEventDestroy(e); e = nullptr; }
+      }
     }
   }
   idx->has_cb = true;
