@@ -31,21 +31,43 @@ __global__ void k_nonfinite(const float* __restrict__ X, int64_t total, int d,
 }
 
 // numpy mean(axis=0) of a C-contiguous matrix: out = X[0]; out += X[r] for
-// r = 1..n-1 (row-sequential), then / n.  One thread per column.
-__global__ void k_colmean_seq(const float* __restrict__ X, int64_t n, int d, double* __restrict__ mean) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  double acc = (double)X[c];
-  int64_t r = 1;
-  for (; r + 8 <= n; r += 8) {
-    float v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (r + u) * d + c);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+// r = 1..n-1 (row-sequential), then / n.  Each of the block's first d
+// threads runs one column's add chain over row tiles that the whole block
+// stages in shared memory (double buffered).  One block per 1024 columns.
+constexpr int CM_THREADS = 1024;
+constexpr int CM_TILE_BYTES = 48 * 1024;
+__global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restrict__ X, int64_t n, int d,
+                                                            double* __restrict__ mean) {
+  extern __shared__ float cm[];
+  const int c0 = blockIdx.x * CM_THREADS;
+  const int nc = min(CM_THREADS, d - c0);
+  const int rows = max(1, CM_TILE_BYTES / (4 * nc));
+  float* buf[2] = {cm, cm + (size_t)rows * nc};
+  const int tid = threadIdx.x;
+  const int64_t ntile = (n + rows - 1) / rows;
+  auto load = [&](int64_t tb, float* dst) {
+    const int64_t r0 = tb * rows;
+    const int rr = (int)min((int64_t)rows, n - r0);
+    for (int e = tid; e < rr * nc; e += CM_THREADS) {
+      const int r = e / nc, c = e % nc;
+      dst[e] = X[(r0 + r) * d + c0 + c];
+    }
+  };
+  load(0, buf[0]);
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t tb = 0; tb < ntile; ++tb) {
+    if (tb + 1 < ntile) load(tb + 1, buf[(tb + 1) & 1]);
+    if (tid < nc) {
+      const float* tv = buf[tb & 1];
+      const int rr = (int)min((int64_t)rows, n - tb * rows);
+      int r = 0;
+      if (tb == 0) { acc = (double)tv[tid]; r = 1; }
+      for (; r < rr; ++r) acc = __dadd_rn(acc, (double)tv[r * nc + tid]);
+    }
+    __syncthreads();
   }
-  for (; r < n; ++r) acc = __dadd_rn(acc, (double)X[r * d + c]);
-  mean[c] = __ddiv_rn(acc, (double)n);
+  if (tid < nc) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
 }
 
 constexpr int GT = 64, GK = 16;
@@ -267,6 +289,7 @@ __device__ double np_combine(const double* leaf, int64_t n) {
 // Generator.choice, clustering.py:48) cannot land elsewhere.  Otherwise
 // replay numpy's arithmetic exactly (single thread).
 constexpr int PS_THREADS = 1024;
+constexpr int PS_TILE = 2048;   // doubles per staged tile of the replay chain
 __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const double* __restrict__ best,
                                                           const double* __restrict__ bsum, int64_t nb,
                                                           const double* __restrict__ uni,
@@ -376,34 +399,55 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   const double total = s_total;
   for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(best[i], total);
   __syncthreads();
-  // cdf_last: the sequential chain (loads double-buffered 32 ahead)
-  auto chain = [&](double c_stop, int64_t& stop_at) -> double {
-    double c = 0.0;
-    int64_t i = 0;
-    double va[32], vb[32];
+  // The sequential cumsum chain (cdf_last, then the crossing) runs on thread 0
+  // over shared-memory tiles that the whole block streams in (double
+  // buffered), so the chain only waits on LDS latency.
+  __shared__ double tile[2][PS_TILE];
+  __shared__ double s_c;
+  __shared__ int64_t s_stop;
+  auto chain = [&](double c_stop) {   // -> s_c (final or crossing value), s_stop
+    const int64_t ntile = (h.n + PS_TILE - 1) / PS_TILE;
+    for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += PS_THREADS) tile[0][i] = pbuf[i];
+    if (tid == 0) { s_c = 0.0; s_stop = -1; }
+    __syncthreads();
+    for (int64_t tb = 0; tb < ntile; ++tb) {
+      const int64_t nb0 = (tb + 1) * PS_TILE;
+      if (tid >= 32) {                       // warps 1.. prefetch the next tile
+        for (int64_t i = tid - 32; i < PS_TILE && nb0 + i < h.n; i += PS_THREADS - 32)
+          tile[(tb + 1) & 1][i] = pbuf[nb0 + i];
+      } else if (tid == 0 && s_stop < 0) {
+        const double* tv = tile[tb & 1];
+        const int lim = (int)min((int64_t)PS_TILE, h.n - tb * PS_TILE);
+        double c = s_c;
+        int t = 0;
+        for (; t + 8 <= lim; t += 8) {
+          double v[8];
 #pragma unroll
-    for (int t = 0; t < 32; ++t) va[t] = i + t < h.n ? pbuf[i + t] : 0.0;
-    while (i < h.n) {
+          for (int e = 0; e < 8; ++e) v[e] = tv[t + e];
+          bool hit = false;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) vb[t] = i + 32 + t < h.n ? pbuf[i + 32 + t] : 0.0;
-      const int lim = (int)min((int64_t)32, h.n - i);
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (t < lim) {
-          c = __dadd_rn(c, va[t]);
-          if (c > c_stop) { stop_at = i + t; return c; }
+          for (int e = 0; e < 8; ++e) {
+            if (!hit) {
+              c = __dadd_rn(c, v[e]);
+              if (c > c_stop) { hit = true; s_stop = tb * PS_TILE + t + e; }
+            }
+          }
+          if (hit) break;
         }
+        if (s_stop < 0)
+          for (; t < lim; ++t) {
+            c = __dadd_rn(c, tv[t]);
+            if (c > c_stop) { s_stop = tb * PS_TILE + t; break; }
+          }
+        s_c = c;
       }
-      i += 32;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) va[t] = vb[t];
+      __syncthreads();
+      if (s_stop >= 0) break;
     }
-    stop_at = h.n - 1;
-    return c;
   };
+  chain(INFINITY);
+  const double last = s_c;                               // cdf[-1]
   if (tid == 0) {
-    int64_t dummy;
-    const double last = chain(INFINITY, dummy);          // cdf[-1]
     // largest c with fl(c / last) <= u: searchsorted(cdf / last, u, 'right')
     // == first i with cdf_i > c_thr (fl(c/last) is monotone in c)
     double c_thr = __dmul_rn(u, last);
@@ -414,9 +458,13 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
       if (__ddiv_rn(nx, last) > u) break;
       c_thr = nx;
     }
-    int64_t idx = h.n - 1;
-    chain(c_thr, idx);
-    picks[draw] = idx;
+    s_c = c_thr;
+  }
+  __syncthreads();
+  const double c_thr = s_c;
+  chain(c_thr);
+  if (tid == 0) {
+    picks[draw] = s_stop >= 0 ? s_stop : h.n - 1;
     status[1] += 1;
   }
 }
@@ -895,7 +943,10 @@ static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, d
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
     *bad_row = b == ~0ull ? -1 : (int64_t)b;
     if (b != ~0ull) break;
-    k_colmean_seq<<<(unsigned)ceil_div(d, 32), 32, 0, st>>>(Xd, n, d, mean.as<double>());
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_colmean_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * CM_TILE_BYTES));
+    k_colmean_seq<<<(unsigned)ceil_div(d, CM_THREADS), CM_THREADS, 2 * CM_TILE_BYTES, st>>>(Xd, n, d,
+                                                                                          mean.as<double>());
     count_launch();
     const int tiles = (int)ceil_div(d, GT);
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(592, tiles * tiles), ceil_div(n, 256)));
