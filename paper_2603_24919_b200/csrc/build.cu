@@ -420,19 +420,22 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
         const int lim = (int)min((int64_t)PS_TILE, h.n - tb * PS_TILE);
         double c = s_c;
         int t = 0;
+        // pure add chain per group of 8; the cdf is non-decreasing, so a
+        // crossing inside the group shows at its last element
         for (; t + 8 <= lim; t += 8) {
-          double v[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = tv[t + e];
-          bool hit = false;
+          double cs[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            if (!hit) {
-              c = __dadd_rn(c, v[e]);
-              if (c > c_stop) { hit = true; s_stop = tb * PS_TILE + t + e; }
-            }
+            c = __dadd_rn(c, tv[t + e]);
+            cs[e] = c;
           }
-          if (hit) break;
+          if (cs[7] > c_stop) {
+            int e = 0;
+            while (!(cs[e] > c_stop)) ++e;
+            s_stop = tb * PS_TILE + t + e;
+            c = cs[e];
+            break;
+          }
         }
         if (s_stop < 0)
           for (; t < lim; ++t) {
