@@ -399,59 +399,55 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   const double total = s_total;
   for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(best[i], total);
   __syncthreads();
-  // The sequential cumsum chain (cdf_last, then the crossing) runs on thread 0
-  // over shared-memory tiles that the whole block streams in (double
-  // buffered), so the chain only waits on LDS latency.
+  // The sequential cumsum chain runs once on thread 0 over shared-memory tiles
+  // that the rest of the block streams in (double buffered) and writes back
+  // (cdf values -> cbuf); the crossing is then found by binary search.
   __shared__ double tile[2][PS_TILE];
   __shared__ double s_c;
-  __shared__ int64_t s_stop;
-  auto chain = [&](double c_stop) {   // -> s_c (final or crossing value), s_stop
-    const int64_t ntile = (h.n + PS_TILE - 1) / PS_TILE;
-    for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += PS_THREADS) tile[0][i] = pbuf[i];
-    if (tid == 0) { s_c = 0.0; s_stop = -1; }
-    __syncthreads();
-    for (int64_t tb = 0; tb < ntile; ++tb) {
-      const int64_t nb0 = (tb + 1) * PS_TILE;
-      if (tid >= 32) {                       // warps 1.. prefetch the next tile
-        for (int64_t i = tid - 32; i < PS_TILE && nb0 + i < h.n; i += PS_THREADS - 32)
-          tile[(tb + 1) & 1][i] = pbuf[nb0 + i];
-      } else if (tid == 0 && s_stop < 0) {
-        const double* tv = tile[tb & 1];
-        const int lim = (int)min((int64_t)PS_TILE, h.n - tb * PS_TILE);
-        double c = s_c;
-        int t = 0;
-        // pure add chain per group of 8; the cdf is non-decreasing, so a
-        // crossing inside the group shows at its last element
-        for (; t + 8 <= lim; t += 8) {
-          double cs[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            c = __dadd_rn(c, tv[t + e]);
-            cs[e] = c;
-          }
-          if (cs[7] > c_stop) {
-            int e = 0;
-            while (!(cs[e] > c_stop)) ++e;
-            s_stop = tb * PS_TILE + t + e;
-            c = cs[e];
-            break;
-          }
-        }
-        if (s_stop < 0)
-          for (; t < lim; ++t) {
-            c = __dadd_rn(c, tv[t]);
-            if (c > c_stop) { s_stop = tb * PS_TILE + t; break; }
-          }
-        s_c = c;
+  const int64_t ntile = (h.n + PS_TILE - 1) / PS_TILE;
+  for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += PS_THREADS) tile[0][i] = pbuf[i];
+  if (tid == 0) s_c = 0.0;
+  __syncthreads();
+  for (int64_t tb = 0; tb < ntile; ++tb) {
+    const int64_t nb0 = (tb + 1) * PS_TILE;
+    if (tid >= 32) {
+      // write back the previous tile's cdf, prefetch the next tile
+      if (tb > 0) {
+        const int64_t pb0 = (tb - 1) * PS_TILE;
+        for (int64_t i = tid - 32; i < PS_TILE && pb0 + i < h.n; i += PS_THREADS - 32)
+          cbuf[pb0 + i] = tile[(tb + 1) & 1][i];
       }
-      __syncthreads();
-      if (s_stop >= 0) break;
+      __syncwarp();
+      for (int64_t i = tid - 32; i < PS_TILE && nb0 + i < h.n; i += PS_THREADS - 32)
+        tile[(tb + 1) & 1][i] = pbuf[nb0 + i];
+    } else if (tid == 0) {
+      double* tv = tile[tb & 1];
+      const int lim = (int)min((int64_t)PS_TILE, h.n - tb * PS_TILE);
+      double c = s_c;
+      int t = 0;
+      for (; t + 8 <= lim; t += 8) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          c = __dadd_rn(c, tv[t + e]);
+          tv[t + e] = c;
+        }
+      }
+      for (; t < lim; ++t) {
+        c = __dadd_rn(c, tv[t]);
+        tv[t] = c;
+      }
+      s_c = c;
     }
-  };
-  chain(INFINITY);
-  const double last = s_c;                               // cdf[-1]
+    __syncthreads();
+  }
+  {
+    const int64_t pb0 = (ntile - 1) * PS_TILE;
+    for (int64_t i = tid; i < PS_TILE && pb0 + i < h.n; i += PS_THREADS) cbuf[pb0 + i] = tile[(ntile - 1) & 1][i];
+  }
+  __syncthreads();
   if (tid == 0) {
-    // largest c with fl(c / last) <= u: searchsorted(cdf / last, u, 'right')
+    const double last = s_c;                             // cdf[-1]
+    // largest c with fl(c / last) <= u; searchsorted(cdf / last, u, 'right')
     // == first i with cdf_i > c_thr (fl(c/last) is monotone in c)
     double c_thr = __dmul_rn(u, last);
     // c_thr >= 0: neighbouring doubles are the bit patterns -1 / +1
@@ -461,13 +457,12 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
       if (__ddiv_rn(nx, last) > u) break;
       c_thr = nx;
     }
-    s_c = c_thr;
-  }
-  __syncthreads();
-  const double c_thr = s_c;
-  chain(c_thr);
-  if (tid == 0) {
-    picks[draw] = s_stop >= 0 ? s_stop : h.n - 1;
+    int64_t lo = -1, hi = h.n - 1;   // cbuf[hi] = last > c_thr; find first index > c_thr
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cbuf[mid] > c_thr) hi = mid; else lo = mid;
+    }
+    picks[draw] = hi;
     status[1] += 1;
   }
 }
