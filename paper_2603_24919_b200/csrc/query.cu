@@ -598,26 +598,46 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
 }
 
 // ------------------------------------------------------- global-mode count
+// One CTA per (id chunk, query) over a whole super-tile.  Two sweeps replace
+// HBM score tables: sweep 1 (CNT_HIST) writes the chunk's level histogram,
+// Alg. 5 runs on the (all-reduced) per-query histogram, sweep 2 (CNT_EMIT)
+// recounts the chunk in shared memory and compacts its candidates straight
+// into the query's candidate segment.  CNT_TABLE stores the table itself
+// (count_collisions tap).
+enum { CNT_TABLE = 0, CNT_HIST = 1, CNT_EMIT = 2 };
 __global__ void __launch_bounds__(CT_THREADS) k_count(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
-    int64_t nchunks, int64_t chunk, int64_t q0, uint8_t* __restrict__ scores, int32_t* __restrict__ part) {
+    int64_t nchunks, int64_t chunk, int mode, uint8_t* __restrict__ scores, int32_t* __restrict__ part,
+    const int32_t* __restrict__ lvl, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
+    const int64_t* __restrict__ coff, int64_t cand_cap, uint32_t* __restrict__ cand) {
   extern __shared__ __align__(16) uint8_t table[];
   __shared__ CountSmem S;
   const int64_t c = blockIdx.x;
-  const int64_t qt = blockIdx.y;          // query within the tile
-  const int64_t q = q0 + qt;              // query within the super-tile
+  const int64_t q = blockIdx.y;
   const int tid = threadIdx.x;
   const int64_t base = c * chunk;
   const int valid = (int)min(chunk, n - base);
+  if (mode == CNT_EMIT) {
+    if (sbase[q] + scnt[q] > cand_cap) return;
+    const int64_t hi = c + 1 < nchunks ? coff[q * nchunks + c + 1] : scnt[q];
+    if (hi == coff[q * nchunks + c]) return;   // no candidate of this query in this chunk
+  }
   uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
-  uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)qt * nchunks + c) * chunk);
-  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
+  if (mode == CNT_EMIT) {
+    compact_table<CT_THREADS>(table, valid, (uint32_t)lvl[q], base, cand + sbase[q] + coff[q * nchunks + c],
+                              S.wtot);
+    return;
+  }
+  if (mode == CNT_TABLE) {
+    uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * chunk);
+    for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
+  }
   chunk_levels(table, valid, n_sub, S);
-  int32_t* pp = part + ((size_t)qt * nchunks + c) * (n_sub + 1);
+  int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
   for (int l = tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
 }
 
@@ -663,34 +683,46 @@ __global__ void k_hist_reduce(const int32_t* __restrict__ part, int64_t nchunks,
   }
 }
 
-// Global mode: one thread per query of the tile.  Alg. 5 on the (global)
-// histogram, local candidate offsets per chunk, one segment per query reserved
-// in the super-tile candidate buffer through the cursor flags[3].
-__global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __restrict__ part, int Q,
-                         int64_t q0, int64_t nchunks, int n_sub, double budget,
-                         int64_t* __restrict__ coff, int64_t cand_cap, int64_t* __restrict__ flags,
-                         int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
-                         int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
-  const int qt = blockIdx.x * blockDim.x + threadIdx.x;
-  if (qt >= Q) return;
-  const int64_t* h = ghist + (size_t)qt * (n_sub + 1);
+// Global mode: one warp per query.  Alg. 5 on the (global) histogram, local
+// candidate offsets per chunk (warp scan), one candidate segment per query
+// reserved in the super-tile candidate buffer through the cursor flags[3].
+__global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __restrict__ part, int64_t Q,
+                         int64_t nchunks, int n_sub, double budget, int64_t* __restrict__ coff,
+                         int64_t cand_cap, int64_t* __restrict__ flags, int64_t* __restrict__ sbase,
+                         int64_t* __restrict__ scnt, int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= Q) return;
+  const int64_t* h = ghist + (size_t)q * (n_sub + 1);
   int64_t cands = 0;
-  const int L = alg5([&](int l) { return h[l]; }, n_sub, budget, cands);
-  int64_t local = 0;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int32_t* pp = part + ((size_t)qt * nchunks + c) * (n_sub + 1);
+  int L = 0;
+  if (lane == 0) L = alg5([&](int l) { return h[l]; }, n_sub, budget, cands);
+  L = __shfl_sync(0xffffffffu, L, 0);
+  int64_t run = 0;
+  for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
+    const int64_t c = c0 + lane;
     int64_t cc = 0;
-    for (int l = L; l <= n_sub; ++l) cc += pp[l];
-    coff[(size_t)qt * nchunks + c] = local;
-    local += cc;
+    if (c < nchunks) {
+      const int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
+      for (int l = L; l <= n_sub; ++l) cc += pp[l];
+    }
+    int64_t v = cc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += x;
+    }
+    if (c < nchunks) coff[q * nchunks + c] = run + v - cc;
+    run += __shfl_sync(0xffffffffu, v, 31);
   }
-  const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)local);
-  if (b + local > cand_cap) flags[1] = 1;
-  const int64_t q = q0 + qt;
-  sbase[q] = b;
-  scnt[q] = local;
-  cnum[q] = cands;
-  lvl[q] = L;
+  if (lane == 0) {
+    const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)run);
+    if (b + run > cand_cap) flags[1] = 1;
+    sbase[q] = b;
+    scnt[q] = run;
+    cnum[q] = cands;
+    lvl[q] = L;
+  }
 }
 
 constexpr int CMP_THREADS = 256;
@@ -1346,12 +1378,6 @@ static int64_t super_tile(const taco_index* idx, int cap) {
   return std::max<int64_t>(64, std::min<int64_t>(Q, kSuperTile));
 }
 
-static int global_tile(const taco_index* idx) {
-  const int64_t per = idx->nchunks * idx->chunk;
-  const int64_t Q = (int64_t)(96ll << 20) / per;
-  return (int)std::max<int64_t>(8, std::min<int64_t>(Q, 1024));
-}
-
 static int ensure_front(taco_index* idx, int64_t QS, int k) {
   QueryTile& t = idx->qt;
   if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
@@ -1375,11 +1401,9 @@ static int ensure_front(taco_index* idx, int64_t QS, int k) {
   TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.out_d.ensure(sizeof(float) * (size_t)QS * std::max(k, 1)));
   if (!idx->cluster_mode) {
-    const int Qt = global_tile(idx);
-    TACO_TRY(t.scores.ensure((size_t)Qt * idx->nchunks * idx->chunk));
-    TACO_TRY(t.part.ensure(sizeof(int32_t) * (size_t)Qt * idx->nchunks * (idx->n_sub + 1)));
-    TACO_TRY(t.hist.ensure(sizeof(int64_t) * (size_t)Qt * (idx->n_sub + 1)));
-    TACO_TRY(t.coff.ensure(sizeof(int64_t) * (size_t)Qt * idx->nchunks));
+    TACO_TRY(t.part.ensure(sizeof(int32_t) * (size_t)QS * idx->nchunks * (idx->n_sub + 1)));
+    TACO_TRY(t.hist.ensure(sizeof(int64_t) * (size_t)QS * (idx->n_sub + 1)));
+    TACO_TRY(t.coff.ensure(sizeof(int64_t) * (size_t)QS * idx->nchunks));
   }
   return TACO_OK;
 }
@@ -1463,46 +1487,46 @@ static int set_count_attrs(taco_index* idx) {
   return TACO_OK;
 }
 
-// global-mode counting of queries [q0, q0+Q) of the super-tile: tables + histograms
-static int global_count_tile(taco_index* idx, int64_t q0, int Q, cudaStream_t st) {
+// global mode, sweep 1: level histograms of every (chunk, query) -> t.hist
+static int global_count(taco_index* idx, int64_t QS, cudaStream_t st) {
   QueryTile& t = idx->qt;
   TACO_TRY(set_count_attrs(idx));
   {
-    dim3 g((unsigned)idx->nchunks, (unsigned)Q);
+    dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COUNT, st);
-    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap,
-                                                       idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-                                                       idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, q0,
-                                                       t.scores.as<uint8_t>(), t.part.as<int32_t>());
+    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_HIST, nullptr, t.part.as<int32_t>(), nullptr,
+        nullptr, nullptr, nullptr, 0, nullptr);
     TACO_LAUNCHED();
   }
   {
     ProfScope ps(K_HIST, st);
-    k_hist_reduce<<<Q, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub, t.hist.as<int64_t>());
+    k_hist_reduce<<<(unsigned)QS, 64, 0, st>>>(t.part.as<int32_t>(), idx->nchunks, idx->n_sub, t.hist.as<int64_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
 }
 
-static int global_select_tile(taco_index* idx, int64_t q0, int Q, const int64_t* ghist, double beta,
-                              cudaStream_t st) {
+// global mode: Alg. 5 on `ghist`, then sweep 2 recounts and compacts
+static int global_select(taco_index* idx, int64_t QS, const int64_t* ghist, double beta, cudaStream_t st) {
   QueryTile& t = idx->qt;
   const double budget = beta * (double)idx->n_global;   // engine.py:240
   {
     ProfScope ps(K_SELECT, st);
-    k_select<<<(unsigned)ceil_div(Q, 128), 128, 0, st>>>(ghist, t.part.as<int32_t>(), Q, q0, idx->nchunks,
-                                                          idx->n_sub, budget, t.coff.as<int64_t>(), t.cand_cap,
-                                                          t.flags.as<int64_t>(), t.qbase.as<int64_t>(),
-                                                          t.clocal.as<int64_t>(), t.cnum.as<int64_t>(),
-                                                          t.lvl.as<int32_t>());  // qbase/clocal = segment base/count
+    k_select<<<(unsigned)ceil_div(QS * 32, 256), 256, 0, st>>>(
+        ghist, t.part.as<int32_t>(), QS, idx->nchunks, idx->n_sub, budget, t.coff.as<int64_t>(), t.cand_cap,
+        t.flags.as<int64_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cnum.as<int64_t>(),
+        t.lvl.as<int32_t>());
     TACO_LAUNCHED();
   }
   {
-    dim3 g((unsigned)idx->nchunks, (unsigned)Q);
+    dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COMPACT, st);
-    k_compact<<<g, CMP_THREADS, 0, st>>>(t.scores.as<uint8_t>(), idx->n, idx->nchunks, idx->chunk, q0,
-                                         t.lvl.as<int32_t>(), t.coff.as<int64_t>(), t.qbase.as<int64_t>(),
-                                         t.clocal.as<int64_t>(), t.cand_cap, t.cand.as<uint32_t>());
+    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, nullptr, nullptr, t.lvl.as<int32_t>(),
+        t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap, t.cand.as<uint32_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
@@ -1637,12 +1661,8 @@ static int run_super_tile(taco_index* idx, int64_t QS, double alpha, double beta
     if (idx->cluster_mode) {
       TACO_TRY(cluster_count(idx, QS, beta, st));
     } else {
-      const int Qt = global_tile(idx);
-      for (int64_t q0 = 0; q0 < QS; q0 += Qt) {
-        const int Q = (int)std::min<int64_t>(Qt, QS - q0);
-        TACO_TRY(global_count_tile(idx, q0, Q, st));
-        TACO_TRY(global_select_tile(idx, q0, Q, t.hist.as<int64_t>(), beta, st));
-      }
+      TACO_TRY(global_count(idx, QS, st));
+      TACO_TRY(global_select(idx, QS, t.hist.as<int64_t>(), beta, st));
     }
     int64_t fl[4];
     TACO_TRY(plan_and_read(idx, QS, st, fl));
@@ -1719,7 +1739,7 @@ int taco_query_batch_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
 
 int taco_query_tile_size(taco_index* idx) {
   if (!idx) return 0;
-  return idx->cluster_mode ? (int)kSuperTile : global_tile(idx);
+  return (int)super_tile(idx, idx->qt.pop_cap ? idx->qt.pop_cap : std::min(idx->K, 1024));
 }
 
 // Split query (multi-GPU): only global-mode (sharded) indexes.
@@ -1728,9 +1748,10 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
   TACO_TRY(check_query_ready(idx, alpha, 1));
   if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
-  const int Qt = global_tile(idx);
-  if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %d", (long long)nq, Qt);
   QueryTile& t = idx->qt;
+  if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
+  const int64_t Qt = super_tile(idx, t.pop_cap);
+  if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)nq, (long long)Qt);
   TACO_TRY(ensure_front(idx, Qt, 1));
   TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1743,7 +1764,7 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
     t.pop_cap = idx->K;
     TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)Qt * idx->n_sub * t.pop_cap));
   }
-  TACO_TRY(global_count_tile(idx, 0, (int)nq, st));
+  TACO_TRY(global_count(idx, nq, st));
   TACO_CHECK_CUDA(cudaMemcpyAsync(hist_d, t.hist.p, sizeof(int64_t) * (size_t)nq * (idx->n_sub + 1),
                                   cudaMemcpyDeviceToDevice, st));
   return TACO_OK;
@@ -1754,20 +1775,22 @@ int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d
                              int64_t* cand_num_d, int32_t* last_coll_d, void* stream) {
   TACO_TRY(index_check(idx));
   if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "base vectors are not resident");
+  if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
   if (!(beta > 0.0 && beta < 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "re-rank ratio %g outside (0, 1)", beta);
   if (k < 1 || k > TK_MAX) TACO_FAIL(TACO_ERR_PARAMETER, "result count %d outside [1, %d]", k, TK_MAX);
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
-  const int Qt = global_tile(idx);
-  if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %d", (long long)nq, Qt);
-  TACO_TRY(ensure_front(idx, Qt, k));
   QueryTile& t = idx->qt;
+  if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
+  const int64_t Qt = super_tile(idx, t.pop_cap);
+  if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)nq, (long long)Qt);
+  TACO_TRY(ensure_front(idx, Qt, k));
   if (t.cand_cap == 0)
-    TACO_TRY(ensure_cand(idx, Qt * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n_global)) + (1 << 20)));
+    TACO_TRY(ensure_cand(idx, Qt * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n)) + (1 << 20)));
   for (int attempt = 0; attempt < 3; ++attempt) {
-    int64_t zero[2] = {0, 0};
-    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 1, zero, 8, cudaMemcpyHostToDevice, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 3, zero, 8, cudaMemcpyHostToDevice, st));
-    TACO_TRY(global_select_tile(idx, 0, (int)nq, ghist_d, beta, st));
+    int64_t zero = 0;
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 1, &zero, 8, cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 3, &zero, 8, cudaMemcpyHostToDevice, st));
+    TACO_TRY(global_select(idx, nq, ghist_d, beta, st));
     int64_t fl[4];
     TACO_TRY(plan_and_read(idx, nq, st, fl));
     if (fl[1]) {
@@ -1824,7 +1847,8 @@ int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* 
     if ((rc = set_count_attrs(idx))) break;
     k_count<<<dim3((unsigned)idx->nchunks, 1), CT_THREADS, (size_t)idx->chunk, st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, 0, sc.as<uint8_t>(), part.as<int32_t>());
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_TABLE, sc.as<uint8_t>(), part.as<int32_t>(),
+        nullptr, nullptr, nullptr, nullptr, 0, nullptr);
     count_launch();
     cudaMemcpyAsync(scores_h, sc.p, idx->n, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
@@ -1893,7 +1917,7 @@ int taco_select_candidates(int device, const uint8_t* scores_h, int64_t n, int32
     count_launch();
     k_hist_reduce<<<1, 64>>>(part.as<int32_t>(), nc, n_sub, hist.as<int64_t>());
     count_launch();
-    k_select<<<1, 32>>>(hist.as<int64_t>(), part.as<int32_t>(), 1, 0, nc, n_sub, beta * (double)n,
+    k_select<<<1, 32>>>(hist.as<int64_t>(), part.as<int32_t>(), 1, nc, n_sub, beta * (double)n,
                         coff.as<int64_t>(), n, flags.as<int64_t>(), qbase.as<int64_t>(), clocal.as<int64_t>(),
                         cnum.as<int64_t>(), lvl.as<int32_t>());
     count_launch();
