@@ -152,6 +152,9 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
     TACO_FAIL(TACO_ERR_PARAMETER, "subspace budget %d (%d x %d) exceeds data dimension %d",
               n_subspaces * subspace_dim, n_subspaces, subspace_dim, d);
   if (n > 0xFFFFFFFFLL) TACO_FAIL(TACO_ERR_PARAMETER, "shard of %lld points exceeds 2^32", (long long)n);
+  if ((int64_t)n_subspaces * n > 0xFFFFFFFFLL)
+    TACO_FAIL(TACO_ERR_PARAMETER, "shard of %lld points x %d subspaces exceeds the 2^32 CSR index range",
+              (long long)n, n_subspaces);
   if (n_global < n) n_global = n;
   TACO_TRY(with_device(device));
   auto* idx = new taco_index();

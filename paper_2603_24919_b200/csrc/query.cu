@@ -250,101 +250,51 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // #(score >= l) = #(increments leaving level l-1).
 constexpr int CT_THREADS = 512;
 constexpr int CT_PB = 2048;   // slices staged per batch
-constexpr int CT_E = 8;       // ids fetched per thread per group
+
+constexpr int CT_UC = 4096;   // units (<= 8 consecutive ids of one slice) staged per round
 
 struct CountSmem {
-  int32_t dl[CT_PB];          // slice delta: the slice's id at flattened f is ids[j*n + dl + f]
-  uint32_t pref[CT_PB + 1];   // flattened start of each (non-empty) slice
+  uint32_t uidx[CT_UC];       // absolute index into ids[] of the unit's first id
+  uint8_t ulen[CT_UC];        // ids in the unit (1..8)
   uint32_t wtot[CT_THREADS / 32];
   int jpref[257];             // pop prefix over subspaces
-  int js[257];                // non-empty slices of subspace j: [js[j], js[j+1])
   int ge[257];                // ge[l] = #ids of the chunk with score >= l  (l >= 1)
   int lh[256];                // level histogram (lh[0] = ids at score 0)
-  int batches;                // number of slice batches the query needed
+  int batches;                // number of pop batches the query needed
 };
 
-__device__ __forceinline__ int slice_in(const uint32_t* pref, int lo, int hi, uint32_t f) {
-  while (hi - lo > 1) {       // largest t in [lo, hi) with pref[t] <= f
-    const int mid = (lo + hi) >> 1;
-    if (pref[mid] <= f) lo = mid; else hi = mid;
+// Per-thread tallies of "increment left level v": n_sub <= 8 packs levels
+// 0..7 as 8-bit fields (flushed per unit into 16-bit fields), else 16-bit
+// fields in four words.
+struct Tally {
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  __device__ __forceinline__ void add_small(uint64_t unit8) {   // 8 x 8-bit fields
+    a0 += unit8 & 0x00FF00FF00FF00FFull;           // levels 0,2,4,6
+    a1 += (unit8 >> 8) & 0x00FF00FF00FF00FFull;    // levels 1,3,5,7
   }
-  return lo;
-}
-
-// Stages batch b0 of the popped slices (phase A), keeping only the slices
-// that hold ids of this chunk (most popped cells have none in a given chunk).
-__device__ void stage_slices(const uint16_t* __restrict__ pops, int cap, const uint32_t* __restrict__ offs,
-                             size_t offs_len, int n_sub, int K2, int64_t c, int64_t q, int b0, CountSmem& S) {
-  const int tid = threadIdx.x;
-  const int P_all = S.jpref[n_sub];
-  const int nb = min(CT_PB, P_all - b0);
-  constexpr int PER = CT_PB / CT_THREADS;
-  uint32_t len[PER], st[PER];
-  uint32_t loc = 0, ne = 0;
-  for (int j = tid; j <= n_sub; j += CT_THREADS) S.js[j] = 0;
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int t = tid * PER + u;
-    len[u] = 0;
-    st[u] = 0;
-    if (t < nb) {
-      const int g = b0 + t;
-      int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (S.jpref[mid] <= g) lo = mid; else hi = mid;
-      }
-      const int j = lo;
-      const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
-      const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
-      const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
-      st[u] = s0;
-      len[u] = s1 - s0;
-      if (len[u]) atomicAdd(&S.js[j + 1], 1);
+  __device__ __forceinline__ void add_wide(uint32_t old) {
+    const uint64_t inc = 1ull << ((old & 3u) << 4);
+    if (old < 4) a0 += inc;
+    else if (old < 8) a1 += inc;
+    else if (old < 12) a2 += inc;
+    else a3 += inc;
+  }
+  __device__ __forceinline__ int level(int l, bool small) const {   // tally of level l
+    if (small) {
+      const uint64_t w = (l & 1) ? a1 : a0;
+      return (int)((w >> (16 * (l >> 1))) & 0xFFFFull);
     }
-    loc += len[u];
-    ne += len[u] ? 1u : 0u;
+    const uint64_t w = l < 4 ? a0 : l < 8 ? a1 : l < 12 ? a2 : a3;
+    return (int)((w >> (16 * (l & 3))) & 0xFFFFull);
   }
-  uint32_t tot;
-  uint32_t run = block_excl_scan<CT_THREADS>(loc, S.wtot, tot);
-  uint32_t netot;
-  uint32_t pos = block_excl_scan<CT_THREADS>(ne, S.wtot, netot);
-  if (tid == 0) {
-    for (int j = 0; j < n_sub; ++j) S.js[j + 1] += S.js[j];
-  }
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    if (len[u]) {
-      S.pref[pos] = run;
-      S.dl[pos] = (int32_t)st[u] - (int32_t)run;
-      ++pos;
-    }
-    run += len[u];
-  }
-  if (tid == 0) S.pref[netot] = tot;
-  __syncthreads();
-}
+};
 
-// Phase B: the ids of ALL staged slices form one flattened list; every thread
-// owns a contiguous range of it, fetches CT_E ids at a time (the next group in
-// flight while the current one is applied) and increments the byte counters
-// with shared-memory atomics on their 32-bit word (byte lanes never carry:
-// scores <= n_sub <= 255).  Atomics make subspace ordering unnecessary -- no
-// barriers inside the count -- and return the old byte for the level tally.
-__device__ __forceinline__ void tally(uint32_t old, bool small, uint64_t& lv0, uint64_t& lv1,
-                                      uint64_t& lv2, uint64_t& lv3) {
-  const uint64_t inc = 1ull << ((old & 3u) << 4);
-  if (small) {
-    if (old < 4) lv0 += inc; else lv1 += inc;
-  } else {
-    if (old < 4) lv0 += inc;
-    else if (old < 8) lv1 += inc;
-    else if (old < 12) lv2 += inc;
-    else lv3 += inc;
-  }
-}
-
+// Phase A + B for one (query, chunk): the popped cells' slices of this chunk
+// are cut into units of <= 8 consecutive ids (CSR order), units are staged
+// CT_UC at a time and consumed round-robin by the threads: no per-id search
+// or walk, 8 independent loads per unit, the next unit's loads in flight
+// while the current one is applied with shared-memory byte-lane atomics
+// (scores <= n_sub <= 255 never carry into the next byte).
 __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
                             const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs,
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
@@ -352,7 +302,7 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
   const int tid = threadIdx.x;
   const bool small = n_sub <= 8;
   uint32_t* tw = reinterpret_cast<uint32_t*>(table);
-  uint64_t lv0 = 0, lv1 = 0, lv2 = 0, lv3 = 0;   // packed per-level increment tallies
+  Tally T;
   if (tid == 0) {
     int acc = 0;
     for (int j = 0; j < n_sub; ++j) {
@@ -364,76 +314,102 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
   }
   __syncthreads();
   const int P_all = S.jpref[n_sub];
+  constexpr int PER = CT_PB / CT_THREADS;
   for (int b0 = 0; b0 < P_all; b0 += CT_PB) {
-    stage_slices(pops, cap, offs, offs_len, n_sub, K2, c, q, b0, S);
-    const int ns = S.js[n_sub];
-    const uint32_t total = S.pref[ns];
-    const uint32_t per = (total + CT_THREADS - 1) / CT_THREADS;
-    uint32_t f = per * tid;
-    const uint32_t fe = min(total, f + per);
-    if (f < fe) {
-      // slice of f, then walk forward with the bounds cached in registers
-      int t = slice_in(S.pref, 0, ns, f);
-      int jt = 0;
-      while (S.js[jt + 1] <= t) ++jt;
-      uint32_t nextb = S.pref[t + 1];
-      const uint32_t* src = ids + (size_t)jt * n + S.dl[t];
-      auto fetch = [&](uint32_t* idv, int& cnt) {
-        cnt = 0;
+    const int nb = min(CT_PB, P_all - b0);
+    uint32_t sa[PER], ln[PER], ub[PER];
+    uint32_t myu = 0;
 #pragma unroll
-        for (int e = 0; e < CT_E; ++e) {
-          if (f < fe) {
-            while (f >= nextb) {
-              ++t;
-              while (S.js[jt + 1] <= t) ++jt;
-              nextb = S.pref[t + 1];
-              src = ids + (size_t)jt * n + S.dl[t];
-            }
-            idv[e] = __ldg(src + f);
-            ++f;
-            cnt = e + 1;
-          }
+    for (int u = 0; u < PER; ++u) {
+      const int t = tid * PER + u;
+      sa[u] = 0;
+      ln[u] = 0;
+      if (t < nb) {
+        const int g = b0 + t;
+        int lo = 0, hi = n_sub;  // largest j with jpref[j] <= g
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.jpref[mid] <= g) lo = mid; else hi = mid;
+        }
+        const int j = lo;
+        const int cell = pops[((size_t)q * n_sub + j) * cap + (g - S.jpref[j])];
+        const uint32_t* O = offs + (size_t)j * offs_len + (size_t)c * K2;
+        const uint32_t s0 = __ldg(O + cell), s1 = __ldg(O + cell + 1);
+        sa[u] = (uint32_t)((size_t)j * n + s0);
+        ln[u] = s1 - s0;
+      }
+      myu += (ln[u] + 7u) >> 3;
+    }
+    uint32_t utot;
+    uint32_t run = block_excl_scan<CT_THREADS>(myu, S.wtot, utot);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      ub[u] = run;
+      run += (ln[u] + 7u) >> 3;
+    }
+    for (uint32_t r0 = 0; r0 < utot; r0 += CT_UC) {
+      const uint32_t r1 = min(utot, r0 + (uint32_t)CT_UC);
+      // scatter my slices' units of this round into the table
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const uint32_t nu = (ln[u] + 7u) >> 3;
+        const uint32_t k0 = max(ub[u], r0), k1 = min(ub[u] + nu, r1);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint32_t off = (k - ub[u]) << 3;
+          S.uidx[k - r0] = sa[u] + off;
+          S.ulen[k - r0] = (uint8_t)min(8u, ln[u] - off);
+        }
+      }
+      __syncthreads();
+      // consume: units tid, tid + CT_THREADS, ... with one unit of lookahead
+      const int nr = (int)(r1 - r0);
+      uint32_t va[8], vb[8];
+      int la = 0, lb = 0;
+      auto fetch = [&](int k, uint32_t* v, int& l) {
+        l = 0;
+        if (k < nr) {
+          const uint32_t* src = ids + S.uidx[k];
+          l = S.ulen[k];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (e < l) v[e] = __ldg(src + e);
         }
       };
-      auto apply = [&](const uint32_t* idv, int cnt) {
+      auto apply = [&](const uint32_t* v, int l) {
+        uint64_t u8 = 0;
 #pragma unroll
-        for (int e = 0; e < CT_E; ++e) {
-          if (e < cnt) {
-            const uint32_t x = idv[e] - (uint32_t)base;
+        for (int e = 0; e < 8; ++e) {
+          if (e < l) {
+            const uint32_t x = v[e] - (uint32_t)base;
             const uint32_t sh = (x & 3u) << 3;
             const uint32_t old = (atomicAdd(tw + (x >> 2), 1u << sh) >> sh) & 0xFFu;
-            tally(old, small, lv0, lv1, lv2, lv3);
+            if (small) u8 += 1ull << (old << 3);
+            else T.add_wide(old);
           }
         }
+        if (small) T.add_small(u8);
       };
-      uint32_t idA[CT_E], idB[CT_E];
-      int nA, nB;
-      fetch(idA, nA);
-      while (nA > 0) {
-        fetch(idB, nB);
-        apply(idA, nA);
+      int k = tid;
+      fetch(k, va, la);
+      while (k < nr) {
+        fetch(k + CT_THREADS, vb, lb);
+        apply(va, la);
 #pragma unroll
-        for (int e = 0; e < CT_E; ++e) idA[e] = idB[e];
-        nA = nB;
+        for (int e = 0; e < 8; ++e) va[e] = vb[e];
+        la = lb;
+        k += CT_THREADS;
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   for (int i = tid; i < 257; i += CT_THREADS) S.ge[i] = 0;
   __syncthreads();
   if (n_sub <= 16) {
-    uint64_t v[4] = {lv0, lv1, lv2, lv3};
+    for (int l = 1; l <= n_sub; ++l) {
+      int x = T.level(l - 1, small);
 #pragma unroll
-    for (int wv = 0; wv < 4; ++wv) {
-      if (wv * 4 >= n_sub) break;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        int x = (int)((v[wv] >> (16 * s)) & 0xFFFFull);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        const int l = wv * 4 + s + 1;
-        if ((tid & 31) == 0 && x && l <= n_sub) atomicAdd(&S.ge[l], x);
-      }
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if ((tid & 31) == 0 && x) atomicAdd(&S.ge[l], x);
     }
   }
   __syncthreads();
@@ -477,13 +453,14 @@ __device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSm
 // run of 16-byte vectors, one block scan places the runs.
 // 16-bit mask of the bytes of v that are >= L (bit i = byte i).
 __device__ __forceinline__ uint32_t ge_mask16(const uint4 v, uint32_t Lrep) {
-  uint32_t m = 0;
   const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+  uint32_t m = 0;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x01010101u;   // bit 0 of each byte
-    g = (g | (g >> 7) | (g >> 14) | (g >> 21)) & 0xFu;     // compress to 4 bits
-    m |= g << (4 * u);
+    // bytes are 0x00/0xFF; picking bit i of byte i and summing the bytes by a
+    // multiply gathers the 4 flags into the top byte
+    const uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x08040201u;
+    m |= ((g * 0x01010101u) >> 24) << (4 * u);
   }
   return m;
 }
