@@ -248,10 +248,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
 // separates subspaces.  Every increment leaving level v is tallied (packed
 // 16-bit counters), which gives the level histogram without rescanning:
 // #(score >= l) = #(increments leaving level l-1).
-constexpr int CT_THREADS = 512;
-constexpr int CT_PB = 2048;   // slices staged per batch
+constexpr int CT_THREADS = 256;
+constexpr int CT_PB = 1024;   // slices staged per batch
 
-constexpr int CT_UC = 4096;   // units (<= 8 consecutive ids of one slice) staged per round
+constexpr int CT_UC = 2048;   // units (<= 8 consecutive ids of one slice) staged per round
 
 struct CountSmem {
   uint32_t uidx[CT_UC];       // absolute index into ids[] of the unit's first id
@@ -295,6 +295,7 @@ struct Tally {
 // or walk, 8 independent loads per unit, the next unit's loads in flight
 // while the current one is applied with shared-memory byte-lane atomics
 // (scores <= n_sub <= 255 never carry into the next byte).
+template <bool NIB>
 __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
                             const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs,
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
@@ -381,8 +382,14 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
         for (int e = 0; e < 8; ++e) {
           if (e < l) {
             const uint32_t x = v[e] - (uint32_t)base;
-            const uint32_t sh = (x & 3u) << 3;
-            const uint32_t old = (atomicAdd(tw + (x >> 2), 1u << sh) >> sh) & 0xFFu;
+            uint32_t old;
+            if (NIB) {   // 4-bit counters: scores <= n_sub <= 15 never carry
+              const uint32_t sh = (x & 7u) << 2;
+              old = (atomicAdd(tw + (x >> 3), 1u << sh) >> sh) & 0xFu;
+            } else {
+              const uint32_t sh = (x & 3u) << 3;
+              old = (atomicAdd(tw + (x >> 2), 1u << sh) >> sh) & 0xFFu;
+            }
             if (small) u8 += 1ull << (old << 3);
             else T.add_wide(old);
           }
@@ -451,40 +458,64 @@ __device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSm
 // Ordered compaction of ids (id0 + position) whose score >= L from a table of
 // `valid` bytes (16-byte aligned, zero padded): every thread owns a contiguous
 // run of 16-byte vectors, one block scan places the runs.
-// 16-bit mask of the bytes of v that are >= L (bit i = byte i).
-__device__ __forceinline__ uint32_t ge_mask16(const uint4 v, uint32_t Lrep) {
+// flags of 4 bytes (0x00/0xFF) -> 4 bits at positions 0,2,4,6 (multiply-gather)
+__device__ __forceinline__ uint32_t flags_even4(uint32_t g) {
+  return ((g & 0x40100401u) * 0x01010101u) >> 24;
+}
+
+// mask of the ids of vector v (16 table bytes) whose score >= L: 16 ids for
+// byte tables, 32 ids for nibble tables (bit i = id i of the vector).
+template <bool NIB>
+__device__ __forceinline__ uint32_t vec_mask(const uint4 v, uint32_t Lrep) {
   const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
   uint32_t m = 0;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    // bytes are 0x00/0xFF; picking bit i of byte i and summing the bytes by a
-    // multiply gathers the 4 flags into the top byte
-    const uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x08040201u;
-    m |= ((g * 0x01010101u) >> 24) << (4 * u);
+    if (NIB) {
+      const uint32_t ge = __vcmpgeu4(ws[u] & 0x0F0F0F0Fu, Lrep);          // even ids
+      const uint32_t go = __vcmpgeu4((ws[u] >> 4) & 0x0F0F0F0Fu, Lrep);   // odd ids
+      m |= (flags_even4(ge) | (flags_even4(go) << 1)) << (8 * u);
+    } else {
+      const uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x08040201u;
+      m |= ((g * 0x01010101u) >> 24) << (4 * u);
+    }
   }
   return m;
 }
 
-template <int NT>
+template <bool NIB>
+__device__ __forceinline__ bool vec_any(const uint4 v, uint32_t Lrep) {
+  if (NIB) {
+    return (__vcmpgeu4(v.x & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.x >> 4) & 0x0F0F0F0Fu, Lrep) |
+            __vcmpgeu4(v.y & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.y >> 4) & 0x0F0F0F0Fu, Lrep) |
+            __vcmpgeu4(v.z & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.z >> 4) & 0x0F0F0F0Fu, Lrep) |
+            __vcmpgeu4(v.w & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.w >> 4) & 0x0F0F0F0Fu, Lrep)) != 0u;
+  }
+  return (__vcmpgeu4(v.x, Lrep) | __vcmpgeu4(v.y, Lrep) | __vcmpgeu4(v.z, Lrep) | __vcmpgeu4(v.w, Lrep)) != 0u;
+}
+
+// Ordered compaction of ids (id0 + position) whose score >= L from a table of
+// `valid` counters (byte or nibble, 16-byte aligned, zero padded): every
+// thread owns a contiguous run of 16-byte vectors, one block scan places them.
+template <int NT, bool NIB = false>
 __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                               uint32_t* wtot) {
+  constexpr int IDS = NIB ? 32 : 16;             // ids per 16-byte vector
   const uint32_t Lrep = 0x01010101u * L;
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
-  const int nvec = (valid + 15) >> 4;
+  const int nvec = (valid + IDS - 1) / IDS;
   const int per = (nvec + NT - 1) / NT;          // vectors per thread
   const int v0 = threadIdx.x * per, v1 = min(nvec, v0 + per);
   const int nv = max(v1 - v0, 0);
   uint32_t cnt = 0;
-  uint32_t hit = 0;                              // which of my first 32 vectors hold matches
+  uint32_t hit = 0;                              // which of my first 31 vectors hold matches
   for (int i = 0; i < nv; ++i) {
     const int vi = v0 + (i + threadIdx.x) % nv;  // rotated start: bank-conflict free
     const uint4 v = t4[vi];
-    const uint32_t g0 = __vcmpgeu4(v.x, Lrep), g1 = __vcmpgeu4(v.y, Lrep);
-    const uint32_t g2 = __vcmpgeu4(v.z, Lrep), g3 = __vcmpgeu4(v.w, Lrep);
-    if (g0 | g1 | g2 | g3) {
-      uint32_t m = ge_mask16(v, Lrep);
-      const int lim = valid - (vi << 4);
-      if (lim < 16) m &= (1u << lim) - 1u;
+    if (vec_any<NIB>(v, Lrep)) {
+      uint32_t m = vec_mask<NIB>(v, Lrep);
+      const int lim = valid - vi * IDS;
+      if (lim < IDS) m &= (1u << lim) - 1u;
       cnt += __popc(m);
       if (m) hit |= vi - v0 < 31 ? 1u << (vi - v0) : 0x80000000u;
     }
@@ -494,10 +525,10 @@ __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t
   for (int i = 0; i < nv; ++i) {
     if (i < 31 ? !((hit >> i) & 1u) : !(hit >> 31)) continue;
     const int vi = v0 + i;
-    uint32_t m = ge_mask16(t4[vi], Lrep);
-    const int lim = valid - (vi << 4);
-    if (lim < 16) m &= (1u << lim) - 1u;
-    const int64_t idb = id0 + ((int64_t)vi << 4);
+    uint32_t m = vec_mask<NIB>(t4[vi], Lrep);
+    const int lim = valid - vi * IDS;
+    if (lim < IDS) m &= (1u << lim) - 1u;
+    const int64_t idb = id0 + (int64_t)vi * IDS;
     while (m) {
       const int bb = __ffs(m) - 1;
       dst[pos++] = (uint32_t)(idb + bb);
@@ -522,7 +553,8 @@ __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& 
 // ------------------------------------------------- cluster-fused count/select
 // Candidates of a query live in per-CTA segments (segment q*S + rank); the
 // final top-k breaks distance ties by id, so segment order is irrelevant.
-__global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
+template <bool NIB>
+__global__ void __launch_bounds__(CT_THREADS, 4) k_count_cluster(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
@@ -541,9 +573,10 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
   const int64_t base = c * chunk;
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
   uint4* t4 = reinterpret_cast<uint4*>(table);
-  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  for (int i = tid; i < tbytes / 16; i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
   chunk_levels(table, valid, n_sub, S);
   cluster.sync();
   if (tid == 0) {
@@ -571,7 +604,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
   }
   cluster.sync();   // remote histograms no longer needed by anyone after this point
   if (s_base + s_cnt > cand_cap) return;
-  compact_table<CT_THREADS>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
+  compact_table<CT_THREADS, NIB>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
 }
 
 // ------------------------------------------------------- global-mode count
@@ -582,7 +615,8 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
 // into the query's candidate segment.  CNT_TABLE stores the table itself
 // (count_collisions tap).
 enum { CNT_TABLE = 0, CNT_HIST = 1, CNT_EMIT = 2 };
-__global__ void __launch_bounds__(CT_THREADS) k_count(
+template <bool NIB>
+__global__ void __launch_bounds__(CT_THREADS, 4) k_count(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, int mode, uint8_t* __restrict__ scores, int32_t* __restrict__ part,
@@ -601,15 +635,16 @@ __global__ void __launch_bounds__(CT_THREADS) k_count(
     if (hi == coff[q * nchunks + c]) return;   // no candidate of this query in this chunk
   }
   uint4* t4 = reinterpret_cast<uint4*>(table);
-  for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  for (int i = tid; i < tbytes / 16; i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  count_chunk(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
   if (mode == CNT_EMIT) {
-    compact_table<CT_THREADS>(table, valid, (uint32_t)lvl[q], base, cand + sbase[q] + coff[q * nchunks + c],
-                              S.wtot);
+    compact_table<CT_THREADS, NIB>(table, valid, (uint32_t)lvl[q], base, cand + sbase[q] + coff[q * nchunks + c],
+                                   S.wtot);
     return;
   }
-  if (mode == CNT_TABLE) {
+  if (mode == CNT_TABLE && !NIB) {
     uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * chunk);
     for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
   }
@@ -1448,18 +1483,24 @@ static int stage_front(taco_index* idx, int64_t QS, double alpha, cudaStream_t s
   return TACO_OK;
 }
 
-static int set_count_attrs(taco_index* idx) {
-  static int64_t cur_c = -1, cur_g = -1;
-  if (idx->cluster_mode && cur_c < idx->chunk) {
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kClusterMaxChunk));
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cur_c = kClusterMaxChunk;
-  }
-  if (cur_g < kClusterMaxChunk) {
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kClusterMaxChunk));
-    cur_g = kClusterMaxChunk;
+// 4-bit score tables whenever a score (<= n_sub) fits a nibble: half the
+// shared memory per CTA, so 4 CTAs of 256 threads share an SM.
+static inline bool nib_tables(const taco_index* idx) { return idx->n_sub <= 15; }
+static inline size_t table_bytes(const taco_index* idx) {
+  return (size_t)(nib_tables(idx) ? idx->chunk / 2 : idx->chunk);
+}
+
+static int set_count_attrs(taco_index*) {
+  static bool done = false;
+  if (!done) {
+    const int mx = (int)kClusterMaxChunk;
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    done = true;
   }
   return TACO_OK;
 }
@@ -1471,7 +1512,8 @@ static int global_count(taco_index* idx, int64_t QS, cudaStream_t st) {
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COUNT, st);
-    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(
+    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
+    kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
         idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_HIST, nullptr, t.part.as<int32_t>(), nullptr,
         nullptr, nullptr, nullptr, 0, nullptr);
@@ -1500,7 +1542,8 @@ static int global_select(taco_index* idx, int64_t QS, const int64_t* ghist, doub
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COMPACT, st);
-    k_count<<<g, CT_THREADS, (size_t)idx->chunk, st>>>(
+    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
+    kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
         idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, nullptr, nullptr, t.lvl.as<int32_t>(),
         t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap, t.cand.as<uint32_t>());
@@ -1516,7 +1559,7 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)idx->nchunks, (unsigned)QS, 1);
   cfg.blockDim = dim3(CT_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = (size_t)idx->chunk;
+  cfg.dynamicSmemBytes = table_bytes(idx);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1526,7 +1569,8 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ProfScope ps(K_COUNT, st);
-  TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_count_cluster, (const uint16_t*)t.pops.as<uint16_t>(),
+  TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, nib_tables(idx) ? k_count_cluster<true> : k_count_cluster<false>,
+                                     (const uint16_t*)t.pops.as<uint16_t>(),
                                      (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
                                      (const uint32_t*)idx->ids.as<uint32_t>(),
                                      (const uint32_t*)idx->offs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
@@ -1822,7 +1866,7 @@ int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* 
     }
     if (rc) break;
     if ((rc = set_count_attrs(idx))) break;
-    k_count<<<dim3((unsigned)idx->nchunks, 1), CT_THREADS, (size_t)idx->chunk, st>>>(
+    k_count<false><<<dim3((unsigned)idx->nchunks, 1), CT_THREADS, (size_t)idx->chunk, st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
         idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_TABLE, sc.as<uint8_t>(), part.as<int32_t>(),
         nullptr, nullptr, nullptr, nullptr, 0, nullptr);
