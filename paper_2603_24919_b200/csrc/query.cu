@@ -264,13 +264,20 @@ struct CountSmem {
 };
 
 // Per-thread tallies of "increment left level v": n_sub <= 8 packs levels
-// 0..7 as 8-bit fields (flushed per unit into 16-bit fields), else 16-bit
-// fields in four words.
+// 0..7 as 4-bit fields per unit, 8-bit fields per round and 16-bit fields per
+// chunk; else 16-bit fields in four words.
+
+__device__ __forceinline__ uint32_t smem_atomic_add(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
 struct Tally {
   uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  __device__ __forceinline__ void add_small(uint64_t unit8) {   // 8 x 8-bit fields
-    a0 += unit8 & 0x00FF00FF00FF00FFull;           // levels 0,2,4,6
-    a1 += (unit8 >> 8) & 0x00FF00FF00FF00FFull;    // levels 1,3,5,7
+  // ev / od: 8-bit fields of levels 0,2,4,6 / 1,3,5,7 -> 16-bit fields
+  __device__ __forceinline__ void add_round(uint32_t ev, uint32_t od) {
+    a0 += ((uint64_t)__byte_perm(ev, 0, 0x4342) << 32) | __byte_perm(ev, 0, 0x4140);
+    a1 += ((uint64_t)__byte_perm(od, 0, 0x4342) << 32) | __byte_perm(od, 0, 0x4140);
   }
   __device__ __forceinline__ void add_wide(uint32_t old) {
     const uint64_t inc = 1ull << ((old & 3u) << 4);
@@ -295,14 +302,17 @@ struct Tally {
 // or walk, 8 independent loads per unit, the next unit's loads in flight
 // while the current one is applied with shared-memory byte-lane atomics
 // (scores <= n_sub <= 255 never carry into the next byte).
-template <bool NIB>
-__device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+template <bool NIB, bool SMALL>
+__device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
                             const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs,
                             size_t offs_len, int n_sub, int K2, int64_t n, int64_t c, int64_t q,
                             int64_t base, uint8_t* table, CountSmem& S) {
   const int tid = threadIdx.x;
-  const bool small = n_sub <= 8;
-  uint32_t* tw = reinterpret_cast<uint32_t*>(table);
+  constexpr bool small = SMALL;   // n_sub <= 8
+  static_assert(CT_UC / CT_THREADS * 8 <= 255, "per-round tally fields are 8-bit");
+  uint32_t tsm = (uint32_t)__cvta_generic_to_shared(table);
+  asm volatile("mov.u32 %0, %0;" : "+r"(tsm));   // keep it in a register (no per-atomic rematerialisation)
+  const uint32_t base32 = (uint32_t)base;
   Tally T;
   if (tid == 0) {
     int acc = 0;
@@ -364,6 +374,7 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
       __syncthreads();
       // consume: units tid, tid + CT_THREADS, ... with one unit of lookahead
       const int nr = (int)(r1 - r0);
+      uint32_t ev = 0, od = 0;   // per-round level tallies (small), 8-bit fields
       uint32_t va[8], vb[8];
       int la = 0, lb = 0;
       auto fetch = [&](int k, uint32_t* v, int& l) {
@@ -377,24 +388,27 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
         }
       };
       auto apply = [&](const uint32_t* v, int l) {
-        uint64_t u8 = 0;
+        uint32_t u4 = 0;   // small: 8 x 4-bit fields "left level v" (<= 8 ids per unit)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           if (e < l) {
-            const uint32_t x = v[e] - (uint32_t)base;
-            uint32_t old;
+            const uint32_t x = v[e] - base32;
+            uint32_t r;
             if (NIB) {   // 4-bit counters: scores <= n_sub <= 15 never carry
-              const uint32_t sh = (x & 7u) << 2;
-              old = (atomicAdd(tw + (x >> 3), 1u << sh) >> sh) & 0xFu;
+              const uint32_t sh = (x << 2) & 28u;
+              r = smem_atomic_add(tsm + ((x >> 1) & ~3u), 1u << sh) >> sh;
             } else {
-              const uint32_t sh = (x & 3u) << 3;
-              old = (atomicAdd(tw + (x >> 2), 1u << sh) >> sh) & 0xFFu;
+              const uint32_t sh = (x << 3) & 24u;
+              r = smem_atomic_add(tsm + (x & ~3u), 1u << sh) >> sh;
             }
-            if (small) u8 += 1ull << (old << 3);
-            else T.add_wide(old);
+            if (small) u4 += 1u << ((r << 2) & 28u);
+            else T.add_wide(r & (NIB ? 0xFu : 0xFFu));
           }
         }
-        if (small) T.add_small(u8);
+        if (small) {   // <= CT_UC / CT_THREADS units per round: 8-bit fields cannot overflow
+          ev += u4 & 0x0F0F0F0Fu;
+          od += (u4 >> 4) & 0x0F0F0F0Fu;
+        }
       };
       int k = tid;
       fetch(k, va, la);
@@ -406,6 +420,7 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
         la = lb;
         k += CT_THREADS;
       }
+      if (small) T.add_round(ev, od);
       __syncthreads();
     }
   }
@@ -420,6 +435,16 @@ __device__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __
     }
   }
   __syncthreads();
+}
+
+template <bool NIB>
+__device__ __forceinline__ void count_chunk(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop,
+                                            int cap, const uint32_t* __restrict__ ids,
+                                            const uint32_t* __restrict__ offs, size_t offs_len, int n_sub, int K2,
+                                            int64_t n, int64_t c, int64_t q, int64_t base, uint8_t* table,
+                                            CountSmem& S) {
+  if (n_sub <= 8) count_chunk_impl<NIB, true>(pops, npop, cap, ids, offs, offs_len, n_sub, K2, n, c, q, base, table, S);
+  else count_chunk_impl<NIB, false>(pops, npop, cap, ids, offs, offs_len, n_sub, K2, n, c, q, base, table, S);
 }
 
 // Level histogram of a chunk table.  n_sub <= 16: from the tallies; else by a
@@ -455,69 +480,59 @@ __device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSm
   __syncthreads();
 }
 
-// Ordered compaction of ids (id0 + position) whose score >= L from a table of
-// `valid` bytes (16-byte aligned, zero padded): every thread owns a contiguous
-// run of 16-byte vectors, one block scan places the runs.
-// flags of 4 bytes (0x00/0xFF) -> 4 bits at positions 0,2,4,6 (multiply-gather)
-__device__ __forceinline__ uint32_t flags_even4(uint32_t g) {
-  return ((g & 0x40100401u) * 0x01010101u) >> 24;
-}
-
-// mask of the ids of vector v (16 table bytes) whose score >= L: 16 ids for
-// byte tables, 32 ids for nibble tables (bit i = id i of the vector).
+// Lanes (4-bit or 8-bit counters) of w that are >= L, as the lane's top bit:
+// the carry out of lane + (2^W - L), computed without cross-lane carries
+// (s holds each lane's carry into its top bit).  D = (2^W - L) per lane, L >= 1.
 template <bool NIB>
-__device__ __forceinline__ uint32_t vec_mask(const uint4 v, uint32_t Lrep) {
-  const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-  uint32_t m = 0;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    if (NIB) {
-      const uint32_t ge = __vcmpgeu4(ws[u] & 0x0F0F0F0Fu, Lrep);          // even ids
-      const uint32_t go = __vcmpgeu4((ws[u] >> 4) & 0x0F0F0F0Fu, Lrep);   // odd ids
-      m |= (flags_even4(ge) | (flags_even4(go) << 1)) << (8 * u);
-    } else {
-      const uint32_t g = __vcmpgeu4(ws[u], Lrep) & 0x08040201u;
-      m |= ((g * 0x01010101u) >> 24) << (4 * u);
-    }
-  }
-  return m;
-}
-
-template <bool NIB>
-__device__ __forceinline__ bool vec_any(const uint4 v, uint32_t Lrep) {
-  if (NIB) {
-    return (__vcmpgeu4(v.x & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.x >> 4) & 0x0F0F0F0Fu, Lrep) |
-            __vcmpgeu4(v.y & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.y >> 4) & 0x0F0F0F0Fu, Lrep) |
-            __vcmpgeu4(v.z & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.z >> 4) & 0x0F0F0F0Fu, Lrep) |
-            __vcmpgeu4(v.w & 0x0F0F0F0Fu, Lrep) | __vcmpgeu4((v.w >> 4) & 0x0F0F0F0Fu, Lrep)) != 0u;
-  }
-  return (__vcmpgeu4(v.x, Lrep) | __vcmpgeu4(v.y, Lrep) | __vcmpgeu4(v.z, Lrep) | __vcmpgeu4(v.w, Lrep)) != 0u;
+__device__ __forceinline__ uint32_t lanes_ge(uint32_t w, uint32_t D) {
+  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
+  const uint32_t s = (w & ~H) + (D & ~H);
+  return ((w & D) | ((w | D) & s)) & H;
 }
 
 // Ordered compaction of ids (id0 + position) whose score >= L from a table of
-// `valid` counters (byte or nibble, 16-byte aligned, zero padded): every
+// `valid` counters (4-bit or 8-bit, 16-byte aligned, zero padded): every
 // thread owns a contiguous run of 16-byte vectors, one block scan places them.
 template <int NT, bool NIB = false>
 __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                               uint32_t* wtot) {
-  constexpr int IDS = NIB ? 32 : 16;             // ids per 16-byte vector
-  const uint32_t Lrep = 0x01010101u * L;
+  constexpr int LW = NIB ? 4 : 8;                // lane width (bits)
+  constexpr int LPW = 32 / LW;                   // lanes per word
+  constexpr int IDS = 4 * LPW;                   // ids per 16-byte vector
+  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
+  const uint32_t D = L == 0 ? 0u : (NIB ? (16u - L) * 0x11111111u : (256u - L) * 0x01010101u);
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
   const int nvec = (valid + IDS - 1) / IDS;
   const int per = (nvec + NT - 1) / NT;          // vectors per thread
   const int v0 = threadIdx.x * per, v1 = min(nvec, v0 + per);
   const int nv = max(v1 - v0, 0);
+  // lane top bits of vector vi with score >= L, lanes past `valid` cleared
+  auto vec_bits = [&](int vi, uint32_t (&g)[4]) {
+    const uint4 v = t4[vi];
+    if (L == 0) {
+      g[0] = g[1] = g[2] = g[3] = H;
+    } else {
+      g[0] = lanes_ge<NIB>(v.x, D); g[1] = lanes_ge<NIB>(v.y, D);
+      g[2] = lanes_ge<NIB>(v.z, D); g[3] = lanes_ge<NIB>(v.w, D);
+    }
+    const int lim = valid - vi * IDS;
+    if (lim < IDS) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int al = min(max(lim - u * LPW, 0), LPW);
+        g[u] &= al >= LPW ? 0xFFFFFFFFu : (1u << (al * LW)) - 1u;
+      }
+    }
+  };
   uint32_t cnt = 0;
   uint32_t hit = 0;                              // which of my first 31 vectors hold matches
   for (int i = 0; i < nv; ++i) {
     const int vi = v0 + (i + threadIdx.x) % nv;  // rotated start: bank-conflict free
-    const uint4 v = t4[vi];
-    if (vec_any<NIB>(v, Lrep)) {
-      uint32_t m = vec_mask<NIB>(v, Lrep);
-      const int lim = valid - vi * IDS;
-      if (lim < IDS) m &= (1u << lim) - 1u;
-      cnt += __popc(m);
-      if (m) hit |= vi - v0 < 31 ? 1u << (vi - v0) : 0x80000000u;
+    uint32_t g[4];
+    vec_bits(vi, g);
+    if (g[0] | g[1] | g[2] | g[3]) {
+      cnt += __popc(g[0]) + __popc(g[1]) + __popc(g[2]) + __popc(g[3]);
+      hit |= vi - v0 < 31 ? 1u << (vi - v0) : 0x80000000u;
     }
   }
   uint32_t tot;
@@ -525,14 +540,17 @@ __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t
   for (int i = 0; i < nv; ++i) {
     if (i < 31 ? !((hit >> i) & 1u) : !(hit >> 31)) continue;
     const int vi = v0 + i;
-    uint32_t m = vec_mask<NIB>(t4[vi], Lrep);
-    const int lim = valid - vi * IDS;
-    if (lim < IDS) m &= (1u << lim) - 1u;
-    const int64_t idb = id0 + (int64_t)vi * IDS;
-    while (m) {
-      const int bb = __ffs(m) - 1;
-      dst[pos++] = (uint32_t)(idb + bb);
-      m &= m - 1u;
+    uint32_t g[4];
+    vec_bits(vi, g);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t idb = id0 + (int64_t)vi * IDS + u * LPW;
+      uint32_t m = g[u];
+      while (m) {
+        const int bb = __ffs(m) - 1;
+        dst[pos++] = (uint32_t)(idb + bb / LW);
+        m &= m - 1u;
+      }
     }
   }
 }
