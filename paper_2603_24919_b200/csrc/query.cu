@@ -777,15 +777,21 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
 
 // ------------------------------------------------------------ rerank plan
 constexpr int GR = 32;    // candidate rows per rerank tile (one warp: lane = row)
-// tiles per segment -> exclusive prefix tpref[0..nseg], total in flags[2]
-__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ scnt, int64_t nseg,
-                                                  int64_t* __restrict__ tpref, int64_t* __restrict__ flags) {
+// Tiles are enumerated in processing order: query slot p = 0..QS-1 runs query
+// order[p] (identity if order is null), its S segments consecutively.
+// tstart[sg] = first tile of segment sg, total in flags[2].
+__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ scnt, int64_t nseg, int S,
+                                                  const int32_t* __restrict__ order,
+                                                  int64_t* __restrict__ tstart, int64_t* __restrict__ flags) {
   __shared__ int64_t wsum[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t per = (nseg + 1023) / 1024;
   const int64_t a0 = threadIdx.x * per, a1 = min(nseg, a0 + per);
+  auto seg_of = [&](int64_t p) -> int64_t {
+    return order ? (int64_t)order[p / S] * S + p % S : p;
+  };
   int64_t loc = 0;
-  for (int64_t s = a0; s < a1; ++s) loc += (scnt[s] + GR - 1) / GR;
+  for (int64_t p = a0; p < a1; ++p) loc += (scnt[seg_of(p)] + GR - 1) / GR;
   int64_t v = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -805,14 +811,71 @@ __global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ sc
   }
   __syncthreads();
   int64_t run = (wid ? wsum[wid - 1] : 0) + v - loc;
-  for (int64_t s = a0; s < a1; ++s) {
-    tpref[s] = run;
-    run += (scnt[s] + GR - 1) / GR;
+  for (int64_t p = a0; p < a1; ++p) {
+    const int64_t sg = seg_of(p);
+    tstart[sg] = run;
+    run += (scnt[sg] + GR - 1) / GR;
   }
-  if (threadIdx.x == 1023) {
-    tpref[nseg] = run;
-    flags[2] = run;
+  if (threadIdx.x == 1023) flags[2] = run;
+}
+
+// tile descriptors in processing order (one warp per segment):
+// {candidate offset lo, hi, query, rows}
+__global__ void k_tile_map(const int64_t* __restrict__ scnt, const int64_t* __restrict__ tstart,
+                           const int64_t* __restrict__ sbase, int64_t nseg, int S, int4* __restrict__ desc) {
+  const int64_t sg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sg >= nseg) return;
+  const int64_t cnt = scnt[sg], nt = (cnt + GR - 1) / GR, t0 = tstart[sg], b = sbase[sg];
+  for (int64_t i = threadIdx.x & 31; i < nt; i += 32) {
+    const int64_t cb = b + i * GR;
+    desc[t0 + i] = make_int4((int)(uint32_t)cb, (int)(cb >> 32), (int)(sg / S), (int)min((int64_t)GR, cnt - i * GR));
   }
+}
+
+// Query processing order for the rerank (L2 reuse between queries that share
+// candidates): queries sorted by a locality key, ties by query index.
+//   mode 1: first popped IMI cell of subspaces 0 and 1
+//   mode 2: smallest candidate id
+// One CTA, bitonic sort of (key << 32 | q) in shared memory (QS <= 16384).
+__global__ void __launch_bounds__(1024) k_qorder(int mode, int64_t QS, const uint16_t* __restrict__ pops,
+                                                 const int32_t* __restrict__ npop, int n_sub, int cap,
+                                                 const uint32_t* __restrict__ cand,
+                                                 const int64_t* __restrict__ sbase,
+                                                 const int64_t* __restrict__ scnt, int S,
+                                                 int32_t* __restrict__ order) {
+  extern __shared__ unsigned long long qk[];
+  int P = 1;
+  while (P < QS) P <<= 1;
+  for (int64_t q = threadIdx.x; q < P; q += blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (q < QS) {
+      uint32_t k32 = 0xFFFFFFFFu;
+      if (mode == 1) {
+        const uint32_t c0 = npop[q * n_sub] > 0 ? pops[(size_t)q * n_sub * cap] : 0xFFFFu;
+        const uint32_t c1 = n_sub > 1 && npop[q * n_sub + 1] > 0 ? pops[((size_t)q * n_sub + 1) * cap] : 0xFFFFu;
+        k32 = (c0 << 16) | c1;
+      } else {
+        for (int r = 0; r < S; ++r)
+          if (scnt[q * S + r] > 0) { k32 = cand[sbase[q * S + r]]; break; }
+      }
+      key = ((unsigned long long)k32 << 32) | (unsigned long long)q;
+    }
+    qk[q] = key;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long x = qk[lo], y = qk[hi];
+        if ((x > y) == up) { qk[lo] = y; qk[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int64_t i = threadIdx.x; i < QS; i += blockDim.x) order[i] = (int32_t)(qk[i] & 0xFFFFFFFFull);
 }
 
 // ---------------------------------------------------- warp top-k helpers
@@ -835,15 +898,6 @@ __device__ __forceinline__ void warp_sort_pairs(unsigned long long& key, uint32_
   }
 }
 
-__device__ __forceinline__ int64_t tile_segment(const int64_t* tpref, int64_t nseg, int64_t tile) {
-  int64_t lo = 0, hi = nseg;  // largest s with tpref[s] <= tile
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (tpref[mid] <= tile) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // fold 8 products of a block into numpy's two einsum lanes (engine.py:273)
 __device__ __forceinline__ void einsum_block8(const float* xv, const float* qv8, double& a0, double& a1) {
   double p[8];
@@ -858,191 +912,29 @@ __device__ __forceinline__ void einsum_block8(const float* xv, const float* qv8,
   a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
 }
 
-// ------------------------------------------ rerank: TMA bulk-copy gather
-// Persistent, warp-specialised (one producer warp, RW consumer warps).  Work
-// unit = (tile of 32 candidate rows, 128-dim segment).  The producer warp's
-// lane r issues cp.async.bulk for row r's segment (plus lane 0 the query
-// segment) into a ring of RS shared-memory stages guarded by full/empty
-// mbarriers; consumer lane r folds row r into the einsum lanes.  After the last
-// segment the warp sorts its 32 (d2, id) pairs and emits the first min(k,32).
-constexpr int RSEG = 128;
-constexpr int RPITCH = RSEG + 4;       // 528 B rows: float4 reads are bank-conflict free
-constexpr int RS = 8;                  // stages
-constexpr int RW = 4;                  // consumer warps
-struct RStage {
-  float rows[GR][RPITCH];
-  float q[RSEG];
-};
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n LAB_WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }\n" ::"r"(smem_u32(b)), "r"(parity));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes));
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 struct TileRef {
-  int64_t sg, off, q;
+  int64_t q;
   int m;
   uint32_t cid;   // this lane's candidate id (valid if lane < m)
 };
 
-// Walks tiles in increasing order: segment pointer only moves forward.
-struct TileWalker {
-  const int64_t* tpref;
-  const int64_t* sbase;
-  const int64_t* scnt;
-  const uint32_t* cand;
-  int64_t nseg, sg, seg_lo, seg_hi, base, cnt;
-  int S;
-  __device__ void init(int64_t tile) {
-    sg = tile_segment(tpref, nseg, tile);
-    load_seg();
-  }
-  __device__ void load_seg() {
-    seg_lo = tpref[sg];
-    seg_hi = tpref[sg + 1];
-    base = sbase[sg];
-    cnt = scnt[sg];
-  }
-  __device__ TileRef at(int64_t tile, int lane) {
-    while (tile >= seg_hi) {
-      ++sg;
-      load_seg();
-    }
-    TileRef r;
-    r.sg = sg;
-    r.off = (tile - seg_lo) * GR;
-    r.m = (int)min((int64_t)GR, cnt - r.off);
-    r.q = sg / S;
-    r.cid = lane < r.m ? cand[base + r.off + lane] : 0xFFFFFFFFu;
-    return r;
-  }
-};
-
-__global__ void __launch_bounds__(32 * (RW + 1), 1) k_rerank_tma(
-    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int64_t* __restrict__ tpref,
-    int64_t nseg, int S, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
-    const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
-    uint32_t* __restrict__ pid) {
-  extern __shared__ __align__(128) unsigned char rsm[];
-  RStage* stg = reinterpret_cast<RStage*>(rsm);
-  __shared__ __align__(8) uint64_t full[RS], empty[RS];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nsg = (d + RSEG - 1) / RSEG;
-  const int64_t t0 = ntiles * blockIdx.x / gridDim.x;
-  const int64_t t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < RS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  __syncthreads();
-  if (t0 >= t1) return;
-  TileWalker W{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};
-  if (wid == 0) {
-    // ---------------- producer warp: one tile of lookahead on the id loads
-    W.init(t0);
-    TileRef cur = W.at(t0, lane);
-    int64_t u = 0;
-    for (int64_t tile = t0; tile < t1; ++tile) {
-      TileRef nxt = cur;
-      if (tile + 1 < t1) nxt = W.at(tile + 1, lane);
-      for (int g = 0; g < nsg; ++g, ++u) {
-        const int slot = (int)(u % RS);
-        const uint32_t par = (uint32_t)((u / RS) & 1);
-        const int s0 = g * RSEG;
-        const int len = min(RSEG, d - s0);
-        if (lane == 0) {
-          mbar_wait(&empty[slot], par ^ 1u);
-          mbar_expect_tx(&full[slot], (uint32_t)((cur.m + 1) * len * 4));
-        }
-        __syncwarp();
-        if (lane < cur.m)
-          bulk_g2s(stg[slot].rows[lane], X + (size_t)cur.cid * d + s0, (uint32_t)(len * 4), &full[slot]);
-        if (lane == 0) bulk_g2s(stg[slot].q, Qf + (size_t)cur.q * d + s0, (uint32_t)(len * 4), &full[slot]);
-        __syncwarp();
-      }
-      cur = nxt;
-    }
-  } else {
-    // ---------------- consumer warps: local tiles cw, cw + RW, ...
-    const int cw = wid - 1;
-    if (t0 + cw >= t1) return;
-    W.init(t0 + cw);
-    for (int64_t i = cw; t0 + i < t1; i += RW) {
-      const int64_t tile = t0 + i;
-      const TileRef tr = W.at(tile, lane);
-      double a0 = 0.0, a1 = 0.0;
-      const int64_t ubase = i * nsg;
-      for (int g = 0; g < nsg; ++g) {
-        const int64_t u = ubase + g;
-        const int slot = (int)(u % RS);
-        mbar_wait(&full[slot], (uint32_t)((u / RS) & 1));
-        const float* row = stg[slot].rows[lane];
-        const float* qv = stg[slot].q;
-        const int s0 = g * RSEG;
-        const int len = min(RSEG, d - s0);
-        const bool last = g == nsg - 1;
-        const int full8 = last ? (len & ~7) : len;
-        for (int b = 0; b < full8; b += 8) {
-          const float4 x0 = *reinterpret_cast<const float4*>(row + b);
-          const float4 x1 = *reinterpret_cast<const float4*>(row + b + 4);
-          const float4 q0 = *reinterpret_cast<const float4*>(qv + b);
-          const float4 q1 = *reinterpret_cast<const float4*>(qv + b + 4);
-          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-          const float q8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-          einsum_block8(xv, q8, a0, a1);
-        }
-        if (last) {
-          for (int b = full8; b < len; b += 2) {
-            const double e0 = __dsub_rn((double)row[b], (double)qv[b]);
-            a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
-            if (b + 1 < len) {
-              const double e1 = __dsub_rn((double)row[b + 1], (double)qv[b + 1]);
-              a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-      }
-      double v = __dadd_rn(a0, a1);
-      v = v >= 0.0 ? v : 0.0;
-      unsigned long long key = lane < tr.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
-      uint32_t id = tr.cid;
-      warp_sort_pairs(key, id);
-      if (lane < kk) {
-        pkey[tile * kk + lane] = key;
-        pid[tile * kk + lane] = id;
-      }
-    }
-  }
+__device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint32_t* __restrict__ cand) {
+  TileRef r;
+  r.m = dsc.w;
+  r.q = dsc.z;
+  const int64_t cb = (int64_t)(((uint64_t)(uint32_t)dsc.y << 32) | (uint32_t)dsc.x);
+  r.cid = lane < r.m ? cand[cb + lane] : 0xFFFFFFFFu;
+  return r;
 }
 
 // ----------------------------------------- rerank: cp.async warp pipelines
-// Each warp owns a contiguous range of 32-row candidate tiles and streams
+// Warp w of W takes tiles w, w + W, w + 2W, ... of the plan's processing
+// order, so all warps sweep the (locality-ordered) queries together and rows
+// shared by neighbouring queries are served from L2.  Each warp streams
 // (tile, 64-dim segment) units through its own ring of AST shared-memory
 // stages with cp.async (LDGSTS, 16 B per lane, L2-only; one instruction moves
 // two 256-byte row segments): the next AST-1 units are in flight while lane r
@@ -1070,42 +962,49 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
-    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int64_t* __restrict__ tpref,
-    int64_t nseg, int S, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
+    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
     const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
     uint32_t* __restrict__ pid) {
   extern __shared__ __align__(128) unsigned char asm_[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   AWarpSmem& W = reinterpret_cast<AWarpSmem*>(asm_)[wid];
-  const int64_t gw = (int64_t)blockIdx.x * AWARPS + wid, nw = (int64_t)gridDim.x * AWARPS;
-  const int64_t t0 = ntiles * gw / nw, t1 = ntiles * (gw + 1) / nw;
-  if (t0 >= t1) return;
+  // warps interleaved across CTAs: concurrently running warps hold adjacent tiles
+  const int64_t gw = (int64_t)wid * gridDim.x + blockIdx.x, nw = (int64_t)gridDim.x * AWARPS;
+  if (gw >= ntiles) return;
+  const int64_t t0 = gw;
+  const int64_t nt = (ntiles - gw + nw - 1) / nw;        // my tiles: t0 + i * nw
   const int nsg = (d + ASEG - 1) / ASEG;
-  const int64_t U = (t1 - t0) * nsg;
-  TileWalker Wi{tpref, sbase, scnt, cand, nseg, 0, 0, 0, 0, 0, S};
-  Wi.init(t0);
-  TileRef tcur = Wi.at(t0, lane);                         // tile being issued
-  TileRef tnext = t0 + 1 < t1 ? Wi.at(t0 + 1, lane) : tcur;  // its successor (ids prefetched)
-  int64_t tcur_tile = t0;
+  const int64_t U = nt * nsg;
+  // descriptors run two tiles ahead of the issue, candidate ids one tile ahead
+  auto dsc = [&](int64_t i) { return i < nt ? __ldg(desc + t0 + i * nw) : make_int4(0, 0, 0, 0); };
+  TileRef tcur = tile_ref(dsc(0), lane, cand);           // tile being issued
+  TileRef tnext = tile_ref(dsc(1), lane, cand);          // its successor (ids in flight)
+  int4 dpre = dsc(2);                                    // the one after
+  int64_t tcur_i = 0;
+  const float* rp = X + (size_t)(lane < tcur.m ? tcur.cid : 0u) * d;   // my row of the issued tile
   TileRef tcomp = tcur;                                   // tile being computed
   const int half = lane >> 4, hl = lane & 15;
   auto issue = [&](int64_t u) {
-    const int64_t tile = t0 + u / nsg;
+    const int64_t i = u / nsg;
     const int g = (int)(u % nsg);
-    if (tile != tcur_tile) {
+    if (i != tcur_i) {
       tcur = tnext;
-      tcur_tile = tile;
-      if (tile + 1 < t1) tnext = Wi.at(tile + 1, lane);
+      tcur_i = i;
+      rp = X + (size_t)(lane < tcur.m ? tcur.cid : 0u) * d;
+      tnext = tile_ref(dpre, lane, cand);
+      dpre = dsc(i + 2);
     }
     AStage& st = W.st[u % AST];
     const int s0 = g * ASEG;
     const int len = min(ASEG, d - s0);
     const int nv = len >> 2;                              // float4 per row segment (<= 16)
-    const float* xs = X + s0 + hl * 4;
-    for (int r = 0; r < tcur.m; r += 2) {
-      const int rr = r + half;
-      const uint32_t cid = __shfl_sync(0xffffffffu, tcur.cid, rr & 31);
-      if (hl < nv && rr < tcur.m) cp_async16(&st.rows[rr][hl * 4], xs + (size_t)cid * d);
+    const int cofs = s0 + hl * 4;
+#pragma unroll
+    for (int j = 0; j < GR / 2; ++j) {                    // rows 2j + half
+      const int rr = 2 * j + half;
+      const float* src = reinterpret_cast<const float*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rp), rr));
+      if (hl < nv && rr < tcur.m) cp_async16(&st.rows[rr][hl * 4], src + cofs);
     }
     if (lane < nv) cp_async16(&st.q[lane * 4], Qf + (size_t)tcur.q * d + s0 + lane * 4);
   };
@@ -1115,9 +1014,10 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
   }
   double a0 = 0.0, a1 = 0.0;
   for (int64_t u = 0; u < U; ++u) {
-    const int64_t tile = t0 + u / nsg;
+    const int64_t i = u / nsg;
+    const int64_t tile = t0 + i * nw;
     const int g = (int)(u % nsg);
-    if (g == 0) tcomp = (tile == tcur_tile) ? tcur : tnext;   // ids of the tile computed now
+    if (g == 0) tcomp = (i == tcur_i) ? tcur : tnext;     // ids of the tile computed now
     if (u + AST - 1 < U) issue(u + AST - 1);
     cp_async_commit();
     cp_async_wait<AST - 1>();
@@ -1175,20 +1075,17 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
 // Generic rerank for d % 4 != 0: lane = row, direct loads.
 __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ X, int d,
                                                       const float* __restrict__ Qf,
-                                                      const int64_t* __restrict__ tpref, int64_t nseg, int S,
-                                                      const int64_t* __restrict__ sbase,
-                                                      const int64_t* __restrict__ scnt,
+                                                      const int4* __restrict__ desc,
                                                       const uint32_t* __restrict__ cand, int64_t ntiles, int kk,
                                                       unsigned long long* __restrict__ pkey,
                                                       uint32_t* __restrict__ pid) {
   const int lane = threadIdx.x & 31;
   const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (tile >= ntiles) return;
-  const int64_t sg = tile_segment(tpref, nseg, tile);
-  const int64_t off = (tile - tpref[sg]) * GR;
-  const int m = (int)min((int64_t)GR, scnt[sg] - off);
-  const int64_t q = sg / S;
-  const uint32_t cid = lane < m ? cand[sbase[sg] + off + lane] : 0xFFFFFFFFu;
+  const TileRef tr = tile_ref(desc[tile], lane, cand);
+  const int m = tr.m;
+  const int64_t q = tr.q;
+  const uint32_t cid = tr.cid;
   const float* row = X + (size_t)(lane < m ? cid : 0u) * d;
   const float* qv = Qf + (size_t)q * d;
   double a0 = 0.0, a1 = 0.0;
@@ -1291,28 +1188,33 @@ __device__ __forceinline__ void bitonic_pairs(unsigned long long* key, uint32_t*
 
 __global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* __restrict__ pkey,
                                                       const uint32_t* __restrict__ pid,
-                                                      const int64_t* __restrict__ tpref, int S, int kk_part,
+                                                      const int64_t* __restrict__ tstart, int S, int kk_part,
                                                       const int64_t* __restrict__ scnt, int k, int64_t id_base,
                                                       double* __restrict__ out_d2,
                                                       int64_t* __restrict__ out_ids) {
   __shared__ unsigned hist[256];
   __shared__ unsigned long long s_pre;
   __shared__ int s_rem, s_fill;
-  __shared__ int64_t s_ties, s_m;
+  __shared__ int64_t s_ties, s_m, s_nt;
   __shared__ unsigned long long skey[TK_MAX];
   __shared__ uint32_t sid[TK_MAX];
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    int64_t c = 0;
-    for (int r = 0; r < S; ++r) c += scnt[q * S + r];
+    int64_t c = 0, nt = 0;
+    for (int r = 0; r < S; ++r) {
+      c += scnt[q * S + r];
+      nt += (scnt[q * S + r] + GR - 1) / GR;
+    }
     s_m = c;
+    s_nt = nt;
     s_fill = 0;
     s_ties = 0;
   }
   __syncthreads();
-  const int64_t lo = tpref[q * S] * kk_part;
-  const int64_t m = (tpref[(q + 1) * S] - tpref[q * S]) * kk_part;
+  // the query's tiles are consecutive in the plan's processing order
+  const int64_t lo = tstart[q * S] * kk_part;
+  const int64_t m = s_nt * kk_part;
   const int kk = (int)min((int64_t)k, s_m);
   const unsigned long long* keys = pkey + lo;
   const uint32_t* ids = pid + lo;
@@ -1599,12 +1501,47 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
   return TACO_OK;
 }
 
+// TACO_QORDER: 0 = batch order, 1 = IMI-cell key, 2 = smallest-candidate key
+static int qorder_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("TACO_QORDER");
+    mode = e ? atoi(e) : 0;
+    if (mode < 0 || mode > 2) mode = 0;
+  }
+  return mode;
+}
+
+static int set_qorder_attrs() {
+  static bool done = false;
+  if (!done) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_qorder, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(unsigned long long) * kSuperTile)));
+    done = true;
+  }
+  return TACO_OK;
+}
+
 static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t fl[4]) {
   QueryTile& t = idx->qt;
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
+  const int mode = qorder_mode();
+  if (mode && QS > 1) {
+    ProfScope ps(K_PLAN, st);
+    TACO_TRY(t.qord.ensure(sizeof(int32_t) * (size_t)QS));
+    int P = 1;
+    while (P < QS) P <<= 1;
+    TACO_TRY(set_qorder_attrs());
+    k_qorder<<<1, 1024, sizeof(unsigned long long) * (size_t)P, st>>>(
+        mode, QS, t.pops.as<uint16_t>(), t.npop.as<int32_t>(), idx->n_sub, t.pop_cap, t.cand.as<uint32_t>(),
+        t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), (int)S, t.qord.as<int32_t>());
+    TACO_LAUNCHED();
+  }
   {
     ProfScope ps(K_PLAN, st);
-    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, t.bpref.as<int64_t>(), t.flags.as<int64_t>());
+    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S,
+                                  mode && QS > 1 ? t.qord.as<int32_t>() : nullptr, t.bpref.as<int64_t>(),
+                                  t.flags.as<int64_t>());
     TACO_LAUNCHED();
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
@@ -1633,23 +1570,30 @@ static int set_rerank_attrs() {
 }
 
 // rows of candidates -> CTA partial top-k -> per-query top-k (t.tk_d2 / t.tk_ids)
-static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64_t S, const int64_t* tpref,
+static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64_t S, const int64_t* tstart,
                        const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
-                       int64_t id_base, DevBuf& pkey, DevBuf& pid, double* out_d2, int64_t* out_ids,
-                       cudaStream_t st) {
+                       int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, double* out_d2,
+                       int64_t* out_ids, cudaStream_t st) {
   const int kk = std::min(k, GR);
   TACO_TRY(pkey.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
   TACO_TRY(pid.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
+  TACO_TRY(tsegb.ensure(sizeof(int4) * (size_t)std::max<int64_t>(ntiles, 1)));
+  const int4* desc = tsegb.as<int4>();
+  if (ntiles > 0) {
+    ProfScope ps(K_PLAN, st);
+    k_tile_map<<<(unsigned)ceil_div(QS * S * 32, 256), 256, 0, st>>>(scnt, tstart, sbase, QS * S, (int)S,
+                                                                    tsegb.as<int4>());
+    TACO_LAUNCHED();
+  }
   if (ntiles > 0) {
     ProfScope ps(K_RERANK, st);
     if (d % 4 == 0) {
       TACO_TRY(set_rerank_attrs());
       const int64_t grid = std::min<int64_t>(ceil_div(ntiles, AWARPS), (int64_t)num_sms());
       k_rerank_async<<<(unsigned)grid, 32 * AWARPS, sizeof(AWarpSmem) * AWARPS, st>>>(
-          X, d, Qf, tpref, QS * S, (int)S, sbase, scnt, cand, ntiles, kk, pkey.as<unsigned long long>(),
-          pid.as<uint32_t>());
+          X, d, Qf, desc, cand, ntiles, kk, pkey.as<unsigned long long>(), pid.as<uint32_t>());
     } else {
-      k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, tpref, QS * S, (int)S, sbase, scnt,
+      k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, desc,
                                                                    cand, ntiles, kk, pkey.as<unsigned long long>(),
                                                                    pid.as<uint32_t>());
     }
@@ -1657,7 +1601,7 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
   }
   {
     ProfScope ps(K_TOPK, st);
-    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tpref, (int)S,
+    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart, (int)S,
                                                 kk, scnt, k, id_base, out_d2, out_ids);
     TACO_LAUNCHED();
   }
@@ -1669,7 +1613,7 @@ static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cuda
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   return rerank_core(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
-                     t.pd2, t.ppos, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
+                     t.pd2, t.ppos, t.tseg, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
 }
 
 static void prof_stats(taco_index* idx, int64_t QS, int64_t total) {
@@ -2005,7 +1949,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
   for (int64_t i = 0; i < m; ++i)
     std::copy(X_h + (size_t)c32[i] * d, X_h + (size_t)c32[i] * d + d, rowsv.begin() + (size_t)i * d);
   const int64_t ntiles = ceil_div(m, GR);
-  DevBuf Xd, Qd, sb, sc, tp, cd, pk, pi, tkd, tki, fl;
+  DevBuf Xd, Qd, sb, sc, tp, cd, pk, pi, ts, tkd, tki, fl;
   int rc = TACO_OK;
   do {
     if ((rc = Xd.ensure(sizeof(float) * rowsv.size())) || (rc = Qd.ensure(sizeof(float) * d)) ||
@@ -2020,10 +1964,10 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     cudaMemcpy(sb.p, &zero, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(sc.p, &m, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
-    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, tp.as<int64_t>(), fl.as<int64_t>());
+    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, 1, nullptr, tp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
     if ((rc = rerank_core(Xd.as<float>(), d, Qd.as<float>(), 1, 1, tp.as<int64_t>(), sb.as<int64_t>(),
-                          sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, tkd.as<double>(),
+                          sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, ts, tkd.as<double>(),
                           tki.as<int64_t>(), nullptr)))
       break;
     std::vector<double> td(k);
@@ -2040,7 +1984,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     }
   } while (0);
   Xd.release(); Qd.release(); sb.release(); sc.release(); tp.release(); cd.release(); pk.release();
-  pi.release(); tkd.release(); tki.release(); fl.release();
+  pi.release(); ts.release(); tkd.release(); tki.release(); fl.release();
   return rc;
 }
 
