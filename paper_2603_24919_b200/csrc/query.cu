@@ -777,19 +777,17 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
 
 // ------------------------------------------------------------ rerank plan
 constexpr int GR = 32;    // candidate rows per rerank tile (one warp: lane = row)
-// Tiles are enumerated in processing order: query slot p = 0..QS-1 runs query
-// order[p] (identity if order is null), its S segments consecutively.
-// tstart[sg] = first tile of segment sg, total in flags[2].
+// Exclusive prefix of the tiles per segment, enumerated query-major
+// (segment p) or chunk-major (p = r * QS + q -> segment q * S + r):
+// tstart[segment] = its first tile in that order, total in flags[2].
 __global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ scnt, int64_t nseg, int S,
-                                                  const int32_t* __restrict__ order,
-                                                  int64_t* __restrict__ tstart, int64_t* __restrict__ flags) {
+                                                  int64_t QS, int chunk_major, int64_t* __restrict__ tstart,
+                                                  int64_t* __restrict__ flags) {
   __shared__ int64_t wsum[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t per = (nseg + 1023) / 1024;
   const int64_t a0 = threadIdx.x * per, a1 = min(nseg, a0 + per);
-  auto seg_of = [&](int64_t p) -> int64_t {
-    return order ? (int64_t)order[p / S] * S + p % S : p;
-  };
+  auto seg_of = [&](int64_t p) -> int64_t { return chunk_major ? (p % QS) * S + p / QS : p; };
   int64_t loc = 0;
   for (int64_t p = a0; p < a1; ++p) loc += (scnt[seg_of(p)] + GR - 1) / GR;
   int64_t v = loc;
@@ -816,66 +814,22 @@ __global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ sc
     tstart[sg] = run;
     run += (scnt[sg] + GR - 1) / GR;
   }
-  if (threadIdx.x == 1023) flags[2] = run;
+  if (threadIdx.x == 1023 && flags) flags[2] = run;
 }
 
-// tile descriptors in processing order (one warp per segment):
-// {candidate offset lo, hi, query, rows}
-__global__ void k_tile_map(const int64_t* __restrict__ scnt, const int64_t* __restrict__ tstart,
-                           const int64_t* __restrict__ sbase, int64_t nseg, int S, int4* __restrict__ desc) {
+// Tile descriptors in processing order (one warp per segment):
+// {candidate offset lo, hi, query << 6 | rows, output tile (query-major)}.
+__global__ void k_tile_map(const int64_t* __restrict__ scnt, const int64_t* __restrict__ tproc,
+                           const int64_t* __restrict__ tout, const int64_t* __restrict__ sbase, int64_t nseg,
+                           int S, int4* __restrict__ desc) {
   const int64_t sg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (sg >= nseg) return;
-  const int64_t cnt = scnt[sg], nt = (cnt + GR - 1) / GR, t0 = tstart[sg], b = sbase[sg];
+  const int64_t cnt = scnt[sg], nt = (cnt + GR - 1) / GR, tp = tproc[sg], to = tout[sg], b = sbase[sg];
   for (int64_t i = threadIdx.x & 31; i < nt; i += 32) {
     const int64_t cb = b + i * GR;
-    desc[t0 + i] = make_int4((int)(uint32_t)cb, (int)(cb >> 32), (int)(sg / S), (int)min((int64_t)GR, cnt - i * GR));
+    const int m = (int)min((int64_t)GR, cnt - i * GR);
+    desc[tp + i] = make_int4((int)(uint32_t)cb, (int)(cb >> 32), (int)((sg / S) << 6) | m, (int)(to + i));
   }
-}
-
-// Query processing order for the rerank (L2 reuse between queries that share
-// candidates): queries sorted by a locality key, ties by query index.
-//   mode 1: first popped IMI cell of subspaces 0 and 1
-//   mode 2: smallest candidate id
-// One CTA, bitonic sort of (key << 32 | q) in shared memory (QS <= 16384).
-__global__ void __launch_bounds__(1024) k_qorder(int mode, int64_t QS, const uint16_t* __restrict__ pops,
-                                                 const int32_t* __restrict__ npop, int n_sub, int cap,
-                                                 const uint32_t* __restrict__ cand,
-                                                 const int64_t* __restrict__ sbase,
-                                                 const int64_t* __restrict__ scnt, int S,
-                                                 int32_t* __restrict__ order) {
-  extern __shared__ unsigned long long qk[];
-  int P = 1;
-  while (P < QS) P <<= 1;
-  for (int64_t q = threadIdx.x; q < P; q += blockDim.x) {
-    unsigned long long key = ~0ull;
-    if (q < QS) {
-      uint32_t k32 = 0xFFFFFFFFu;
-      if (mode == 1) {
-        const uint32_t c0 = npop[q * n_sub] > 0 ? pops[(size_t)q * n_sub * cap] : 0xFFFFu;
-        const uint32_t c1 = n_sub > 1 && npop[q * n_sub + 1] > 0 ? pops[((size_t)q * n_sub + 1) * cap] : 0xFFFFu;
-        k32 = (c0 << 16) | c1;
-      } else {
-        for (int r = 0; r < S; ++r)
-          if (scnt[q * S + r] > 0) { k32 = cand[sbase[q * S + r]]; break; }
-      }
-      key = ((unsigned long long)k32 << 32) | (unsigned long long)q;
-    }
-    qk[q] = key;
-  }
-  __syncthreads();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long x = qk[lo], y = qk[hi];
-        if ((x > y) == up) { qk[lo] = y; qk[hi] = x; }
-      }
-      __syncthreads();
-    }
-  }
-  for (int64_t i = threadIdx.x; i < QS; i += blockDim.x) order[i] = (int32_t)(qk[i] & 0xFFFFFFFFull);
 }
 
 // ---------------------------------------------------- warp top-k helpers
@@ -919,13 +873,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 struct TileRef {
   int64_t q;
   int m;
+  int out;        // output tile (query-major)
   uint32_t cid;   // this lane's candidate id (valid if lane < m)
 };
 
 __device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint32_t* __restrict__ cand) {
   TileRef r;
-  r.m = dsc.w;
-  r.q = dsc.z;
+  r.m = dsc.z & 63;
+  r.q = dsc.z >> 6;
+  r.out = dsc.w;
   const int64_t cb = (int64_t)(((uint64_t)(uint32_t)dsc.y << 32) | (uint32_t)dsc.x);
   r.cid = lane < r.m ? cand[cb + lane] : 0xFFFFFFFFu;
   return r;
@@ -1015,7 +971,6 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
   double a0 = 0.0, a1 = 0.0;
   for (int64_t u = 0; u < U; ++u) {
     const int64_t i = u / nsg;
-    const int64_t tile = t0 + i * nw;
     const int g = (int)(u % nsg);
     if (g == 0) tcomp = (i == tcur_i) ? tcur : tnext;     // ids of the tile computed now
     if (u + AST - 1 < U) issue(u + AST - 1);
@@ -1061,8 +1016,8 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
       uint32_t id = tcomp.cid;
       warp_sort_pairs(key, id);
       if (lane < kk) {
-        pkey[tile * kk + lane] = key;
-        pid[tile * kk + lane] = id;
+        pkey[(int64_t)tcomp.out * kk + lane] = key;
+        pid[(int64_t)tcomp.out * kk + lane] = id;
       }
       a0 = 0.0;
       a1 = 0.0;
@@ -1110,8 +1065,8 @@ __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ 
   uint32_t id = cid;
   warp_sort_pairs(key, id);
   if (lane < kk) {
-    pkey[tile * kk + lane] = key;
-    pid[tile * kk + lane] = id;
+    pkey[(int64_t)tr.out * kk + lane] = key;
+    pid[(int64_t)tr.out * kk + lane] = id;
   }
 }
 
@@ -1501,48 +1456,25 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
   return TACO_OK;
 }
 
-// TACO_QORDER: 0 = batch order, 1 = IMI-cell key, 2 = smallest-candidate key
-static int qorder_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("TACO_QORDER");
-    mode = e ? atoi(e) : 0;
-    if (mode < 0 || mode > 2) mode = 0;
-  }
-  return mode;
-}
-
-static int set_qorder_attrs() {
-  static bool done = false;
-  if (!done) {
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_qorder, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(unsigned long long) * kSuperTile)));
-    done = true;
-  }
-  return TACO_OK;
-}
-
+// Tile plans: query-major output positions (t.bpref, for the top-k) and, in
+// cluster mode, the chunk-major processing order (t.ppref): all queries'
+// candidates in one id chunk are re-ranked before the next chunk, so the
+// rows they share (each row is a candidate of ~beta*alpha-proportional many
+// queries of a batch) are read from HBM about once and then served by L2.
 static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t fl[4]) {
   QueryTile& t = idx->qt;
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
-  const int mode = qorder_mode();
-  if (mode && QS > 1) {
-    ProfScope ps(K_PLAN, st);
-    TACO_TRY(t.qord.ensure(sizeof(int32_t) * (size_t)QS));
-    int P = 1;
-    while (P < QS) P <<= 1;
-    TACO_TRY(set_qorder_attrs());
-    k_qorder<<<1, 1024, sizeof(unsigned long long) * (size_t)P, st>>>(
-        mode, QS, t.pops.as<uint16_t>(), t.npop.as<int32_t>(), idx->n_sub, t.pop_cap, t.cand.as<uint32_t>(),
-        t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), (int)S, t.qord.as<int32_t>());
-    TACO_LAUNCHED();
-  }
   {
     ProfScope ps(K_PLAN, st);
-    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S,
-                                  mode && QS > 1 ? t.qord.as<int32_t>() : nullptr, t.bpref.as<int64_t>(),
+    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S, QS, 0, t.bpref.as<int64_t>(),
                                   t.flags.as<int64_t>());
     TACO_LAUNCHED();
+    if (S > 1) {
+      TACO_TRY(t.ppref.ensure(sizeof(int64_t) * (size_t)(QS * S + 1)));
+      k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S, QS, 1, t.ppref.as<int64_t>(),
+                                    nullptr);
+      TACO_LAUNCHED();
+    }
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1571,7 +1503,7 @@ static int set_rerank_attrs() {
 
 // rows of candidates -> CTA partial top-k -> per-query top-k (t.tk_d2 / t.tk_ids)
 static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64_t S, const int64_t* tstart,
-                       const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
+                       const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
                        int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, double* out_d2,
                        int64_t* out_ids, cudaStream_t st) {
   const int kk = std::min(k, GR);
@@ -1581,8 +1513,8 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
   const int4* desc = tsegb.as<int4>();
   if (ntiles > 0) {
     ProfScope ps(K_PLAN, st);
-    k_tile_map<<<(unsigned)ceil_div(QS * S * 32, 256), 256, 0, st>>>(scnt, tstart, sbase, QS * S, (int)S,
-                                                                    tsegb.as<int4>());
+    k_tile_map<<<(unsigned)ceil_div(QS * S * 32, 256), 256, 0, st>>>(scnt, tproc, tstart, sbase, QS * S,
+                                                                    (int)S, tsegb.as<int4>());
     TACO_LAUNCHED();
   }
   if (ntiles > 0) {
@@ -1612,6 +1544,7 @@ static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cuda
   QueryTile& t = idx->qt;
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   return rerank_core(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
+                     S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
                      t.pd2, t.ppos, t.tseg, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
 }
@@ -1964,9 +1897,10 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     cudaMemcpy(sb.p, &zero, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(sc.p, &m, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
-    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, 1, nullptr, tp.as<int64_t>(), fl.as<int64_t>());
+    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, 1, 1, 0, tp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
-    if ((rc = rerank_core(Xd.as<float>(), d, Qd.as<float>(), 1, 1, tp.as<int64_t>(), sb.as<int64_t>(),
+    if ((rc = rerank_core(Xd.as<float>(), d, Qd.as<float>(), 1, 1, tp.as<int64_t>(), tp.as<int64_t>(),
+                          sb.as<int64_t>(),
                           sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, ts, tkd.as<double>(),
                           tki.as<int64_t>(), nullptr)))
       break;

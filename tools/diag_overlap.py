@@ -26,6 +26,7 @@ for i in range(NQ):
     sets.append(cs.ids)
 print("collected", NQ, "sets in", round(time.time() - t0, 1), "s; mean size", np.mean([s.size for s in sets]))
 M = torch.zeros((NQ, n), dtype=torch.bfloat16, device="cuda")
+print("all-batch union/sum", round(torch.unique(torch.cat([torch.from_numpy(x).cuda() for x in sets])).numel() / sum(x.size for x in sets), 4))
 for i, s in enumerate(sets):
     M[i, torch.from_numpy(s).cuda()] = 1
 sizes = M.float().sum(1)
@@ -64,5 +65,14 @@ while left:
     left.remove(nxt)
     cur = nxt
 keys["greedy"] = chain
+def group_union(order, G):
+    tot = uni = 0
+    for g0 in range(0, NQ, G):
+        qs = order[g0:g0 + G]
+        u = torch.unique(torch.cat([torch.from_numpy(sets[q]).cuda() for q in qs]))
+        uni += u.numel()
+        tot += sum(sets[q].size for q in qs)
+    return uni / tot
 for name, order in keys.items():
-    print(name, {w: round(reuse(order, w), 3) for w in (1, 4, 16)})
+    print(name, {w: round(reuse(order, w), 3) for w in (1, 4, 16)},
+          "union/sum", {G: round(group_union(order, G), 3) for G in (16, 64, 256, 1024)})
