@@ -52,9 +52,17 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces,
                       int32_t subspace_dim, int32_t clusters, int32_t kmeans_iters,
                       int64_t n_global, int64_t id_base, taco_index** out);
 int taco_index_destroy(taco_index* idx);
-/* Uploads the base vectors (owned device copy, used by build + rerank). */
+/* Uploads the base vectors (owned device copy, used by build + rerank).
+ * The rerank additionally keeps a lossless narrower copy of the rows when
+ * EVERY value converts exactly (u8: integers 0..255, f16: exactly
+ * representable halves; d a multiple of 16 / 8), so it reads 4x / 2x fewer
+ * bytes per candidate with bit-identical distances.  TACO_ROWS=f32 in the
+ * environment disables it. */
 int taco_index_set_data(taco_index* idx, const float* X_h);
 int taco_index_set_data_device(taco_index* idx, const float* X_d);
+enum { TACO_ROWS_F32 = 0, TACO_ROWS_F16 = 1, TACO_ROWS_U8 = 2 };
+/* Storage format the rerank reads rows in (TACO_ROWS_*), or -1 without data. */
+int32_t taco_index_row_format(const taco_index* idx);
 
 /* ------------------------------------------------------------------ build */
 /* spectral.fit_covariance (spectral.py:94-111): fp64 row mean (sequential,

@@ -30,6 +30,7 @@ _SIGS = {
     "taco_index_destroy": [_vp],
     "taco_index_set_data": [_vp, _vp],
     "taco_index_set_data_device": [_vp, _vp],
+    "taco_index_row_format": [_vp],
     "taco_fit_covariance": [_vp, _vp, _vp, _vp],
     "taco_covariance": [_c_int, _vp, _c_i64, _c_i32, _vp, _vp, _vp],
     "taco_jacobi_sweeps": [_vp, _vp, _c_i32, _c_dbl, _c_i32, _vp, _vp],

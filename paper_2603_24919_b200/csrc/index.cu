@@ -193,7 +193,7 @@ int taco_index_destroy(taco_index* idx) {
   if (!idx) return TACO_OK;
   cudaSetDevice(idx->device);
   cudaStreamSynchronize(idx->stream);
-  DevBuf* bufs[] = {&idx->X, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
+  DevBuf* bufs[] = {&idx->X, &idx->Xn, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
                     &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
   for (auto* b : bufs) b->release();
   QueryTile& q = idx->qt;
@@ -213,6 +213,64 @@ int taco_index_destroy(taco_index* idx) {
   return TACO_OK;
 }
 
+namespace taco {
+// ok[0] &= every value is an integer 0..255 (bit-exact round trip through u8),
+// ok[1] &= every value round-trips exactly through f16
+__global__ void k_row_formats(const float* __restrict__ X, size_t N, int* __restrict__ ok) {
+  bool u8 = true, f16 = true;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x) {
+    const float x = X[i];
+    const uint32_t b = __float_as_uint(x);
+    const bool in = x >= 0.0f && x <= 255.0f;
+    u8 = u8 && in && __float_as_uint((float)(uint32_t)x) == b;
+    f16 = f16 && __float_as_uint(__half2float(__float2half_rn(x))) == b;
+  }
+  if (!__all_sync(0xffffffffu, u8) && (threadIdx.x & 31) == 0) atomicAnd(ok, 0);
+  if (!__all_sync(0xffffffffu, f16) && (threadIdx.x & 31) == 0) atomicAnd(ok + 1, 0);
+}
+__global__ void k_rows_u8(const float* __restrict__ X, size_t N, uint8_t* __restrict__ out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)(uint32_t)X[i];
+}
+__global__ void k_rows_f16(const float* __restrict__ X, size_t N, __half* __restrict__ out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __float2half_rn(X[i]);
+}
+
+// choose the rerank's row storage (lossless only) after X changed
+static int narrow_rows(taco_index* idx) {
+  idx->xfmt = TACO_ROWS_F32;
+  idx->Xn.release();
+  const char* env = getenv("TACO_ROWS");
+  if (env && strcmp(env, "f32") == 0) return TACO_OK;
+  const size_t N = (size_t)idx->n * idx->d;
+  if (N == 0) return TACO_OK;
+  DevBuf ok;
+  TACO_TRY(ok.ensure(2 * sizeof(int)));
+  const int ones[2] = {1, 1};
+  int res[2] = {0, 0};
+  TACO_CHECK_CUDA(cudaMemcpyAsync(ok.p, ones, sizeof(ones), cudaMemcpyHostToDevice, idx->stream));
+  k_row_formats<<<1184, 256, 0, idx->stream>>>(idx->X.as<float>(), N, ok.as<int>());
+  count_launch();
+  TACO_CHECK_CUDA(cudaMemcpyAsync(res, ok.p, sizeof(res), cudaMemcpyDeviceToHost, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  ok.release();
+  if (res[0] && idx->d % 16 == 0) {
+    TACO_TRY(idx->Xn.ensure(N));
+    k_rows_u8<<<1184, 256, 0, idx->stream>>>(idx->X.as<float>(), N, idx->Xn.as<uint8_t>());
+    count_launch();
+    idx->xfmt = TACO_ROWS_U8;
+  } else if (res[1] && idx->d % 8 == 0) {
+    TACO_TRY(idx->Xn.ensure(2 * N));
+    k_rows_f16<<<1184, 256, 0, idx->stream>>>(idx->X.as<float>(), N, idx->Xn.as<__half>());
+    count_launch();
+    idx->xfmt = TACO_ROWS_F16;
+  }
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  return TACO_OK;
+}
+}  // namespace taco
+
 int taco_index_set_data(taco_index* idx, const float* X_h) {
   TACO_TRY(index_check(idx));
   size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
@@ -220,7 +278,12 @@ int taco_index_set_data(taco_index* idx, const float* X_h) {
   TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_h, bytes, cudaMemcpyHostToDevice, idx->stream));
   TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
   idx->has_X = true;
-  return TACO_OK;
+  return narrow_rows(idx);
+}
+
+int32_t taco_index_row_format(const taco_index* idx) {
+  if (!idx || !idx->has_X) return -1;
+  return idx->xfmt;
 }
 
 int taco_index_set_data_device(taco_index* idx, const float* X_d) {
@@ -230,7 +293,7 @@ int taco_index_set_data_device(taco_index* idx, const float* X_d) {
   TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_d, bytes, cudaMemcpyDeviceToDevice, idx->stream));
   TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
   idx->has_X = true;
-  return TACO_OK;
+  return narrow_rows(idx);
 }
 
 int taco_index_set_transform(taco_index* idx, const float* mean_h, const float* matrix_h) {

@@ -59,6 +59,8 @@ struct taco_index {
   bool cluster_mode = false;
   int d = 0, n_sub = 0, s = 0, K = 0, kp = 0, m1 = 0, m2 = 0, D = 0, iters = 0;
   taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
+  taco::DevBuf Xn;            // lossless narrow copy of X for the rerank (xfmt != TACO_ROWS_F32)
+  int xfmt = 0;               // TACO_ROWS_*
   bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,
        has_cells = false, has_gsize = false;
   std::vector<cudaStream_t> half_streams;

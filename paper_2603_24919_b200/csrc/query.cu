@@ -897,18 +897,62 @@ __device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint
 // folds row r of the current unit into numpy's two einsum lanes against the
 // query segment (pre-converted to fp64 in shared memory).  Warp top-k of the
 // 32 (d2, id) pairs per tile.
-constexpr int ASEG = 64;               // dims per unit
-constexpr int APITCH = ASEG + 4;       // 272 B rows: float4 reads are bank-conflict free
+// Rows are staged in the index's storage format (row_format.cuh): f32, or a
+// lossless narrower copy (f16 / u8) when every value of X converts exactly,
+// so the staged bytes per row shrink 2x / 4x and the fp64 arithmetic on the
+// widened values is unchanged.
+template <typename T> struct RowFmt;
+template <> struct RowFmt<float> {    // 64 dims (256 B) per unit, 16 lanes per row segment
+  static constexpr int UD = 64, LPR = 16, PITCH = 272, WARPS = 12;
+};
+template <> struct RowFmt<__half> {   // 128 dims (256 B) per unit
+  static constexpr int UD = 128, LPR = 16, PITCH = 272, WARPS = 11;
+};
+template <> struct RowFmt<uint8_t> {  // 128 dims (128 B) per unit, 8 lanes per row segment
+  static constexpr int UD = 128, LPR = 8, PITCH = 144, WARPS = 20;
+};
 constexpr int AST = 2;                 // stages per warp (the id lookahead assumes 2)
-constexpr int AWARPS = 12;             // warps per CTA
+template <typename T>
 struct AStage {
-  float rows[GR][APITCH];
-  float q[ASEG];
+  uint8_t rows[GR][RowFmt<T>::PITCH];  // pitch = 16 B mod 128: 16-byte row reads are conflict free
+  float q[RowFmt<T>::UD];
 };
+template <typename T>
 struct AWarpSmem {
-  AStage st[AST];
-  double qd[ASEG];
+  AStage<T> st[AST];
+  double qd[RowFmt<T>::UD];
 };
+
+// 8 consecutive row values (exact) as f32
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], float) {
+  const float4 x0 = *reinterpret_cast<const float4*>(rb + 4 * b);
+  const float4 x1 = *reinterpret_cast<const float4*>(rb + 4 * b + 16);
+  xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
+  xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
+}
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], __half) {
+  const uint4 w = *reinterpret_cast<const uint4*>(rb + 2 * b);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws[t]));
+    xv[2 * t] = f.x;
+    xv[2 * t + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], uint8_t) {
+  const uint2 w = *reinterpret_cast<const uint2*>(rb + b);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {   // 2^23 + byte, exactly, then minus 2^23
+    const uint32_t bits = __byte_perm(t < 4 ? w.x : w.y, 0x4B000000u, 0x7650u + (t & 3));
+    xv[t] = __fsub_rn(__uint_as_float(bits), 8388608.0f);
+  }
+}
+__device__ __forceinline__ float elem(const uint8_t* rb, int b, float) { return reinterpret_cast<const float*>(rb)[b]; }
+__device__ __forceinline__ float elem(const uint8_t* rb, int b, __half) {
+  return __half2float(reinterpret_cast<const __half*>(rb)[b]);
+}
+__device__ __forceinline__ float elem(const uint8_t* rb, int b, uint8_t) { return (float)rb[b]; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -917,52 +961,58 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
-    const float* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
+template <typename T>
+__global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, 1) k_rerank_async(
+    const T* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
     const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
     uint32_t* __restrict__ pid) {
+  using F = RowFmt<T>;
+  constexpr int UD = F::UD, LPR = F::LPR, RPI = 32 / F::LPR;
   extern __shared__ __align__(128) unsigned char asm_[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  AWarpSmem& W = reinterpret_cast<AWarpSmem*>(asm_)[wid];
+  AWarpSmem<T>& W = reinterpret_cast<AWarpSmem<T>*>(asm_)[wid];
   // warps interleaved across CTAs: concurrently running warps hold adjacent tiles
-  const int64_t gw = (int64_t)wid * gridDim.x + blockIdx.x, nw = (int64_t)gridDim.x * AWARPS;
+  const int64_t gw = (int64_t)wid * gridDim.x + blockIdx.x, nw = (int64_t)gridDim.x * F::WARPS;
   if (gw >= ntiles) return;
   const int64_t t0 = gw;
   const int64_t nt = (ntiles - gw + nw - 1) / nw;        // my tiles: t0 + i * nw
-  const int nsg = (d + ASEG - 1) / ASEG;
+  const int nsg = (d + UD - 1) / UD;
   const int64_t U = nt * nsg;
   // descriptors run two tiles ahead of the issue, candidate ids one tile ahead
   auto dsc = [&](int64_t i) { return i < nt ? __ldg(desc + t0 + i * nw) : make_int4(0, 0, 0, 0); };
+  auto row_of = [&](const TileRef& r) {
+    return reinterpret_cast<const uint8_t*>(X + (size_t)(lane < r.m ? r.cid : 0u) * d);
+  };
   TileRef tcur = tile_ref(dsc(0), lane, cand);           // tile being issued
   TileRef tnext = tile_ref(dsc(1), lane, cand);          // its successor (ids in flight)
   int4 dpre = dsc(2);                                    // the one after
   int64_t tcur_i = 0;
-  const float* rp = X + (size_t)(lane < tcur.m ? tcur.cid : 0u) * d;   // my row of the issued tile
+  const uint8_t* rp = row_of(tcur);                      // my row of the issued tile
   TileRef tcomp = tcur;                                   // tile being computed
-  const int half = lane >> 4, hl = lane & 15;
+  const int r0 = lane / LPR, cl = lane % LPR;
   auto issue = [&](int64_t u) {
     const int64_t i = u / nsg;
     const int g = (int)(u % nsg);
     if (i != tcur_i) {
       tcur = tnext;
       tcur_i = i;
-      rp = X + (size_t)(lane < tcur.m ? tcur.cid : 0u) * d;
+      rp = row_of(tcur);
       tnext = tile_ref(dpre, lane, cand);
       dpre = dsc(i + 2);
     }
-    AStage& st = W.st[u % AST];
-    const int s0 = g * ASEG;
-    const int len = min(ASEG, d - s0);
-    const int nv = len >> 2;                              // float4 per row segment (<= 16)
-    const int cofs = s0 + hl * 4;
+    AStage<T>& st = W.st[u % AST];
+    const int s0 = g * UD;
+    const int len = min(UD, d - s0);
+    const int nch = (int)(len * sizeof(T)) / 16;          // 16-byte chunks per row segment (<= LPR)
+    const int cofs = s0 * (int)sizeof(T) + cl * 16;
 #pragma unroll
-    for (int j = 0; j < GR / 2; ++j) {                    // rows 2j + half
-      const int rr = 2 * j + half;
-      const float* src = reinterpret_cast<const float*>(
+    for (int j = 0; j < GR / RPI; ++j) {                  // rows j * RPI + r0
+      const int rr = j * RPI + r0;
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(
           __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rp), rr));
-      if (hl < nv && rr < tcur.m) cp_async16(&st.rows[rr][hl * 4], src + cofs);
+      if (cl < nch && rr < tcur.m) cp_async16(&st.rows[rr][cl * 16], src + cofs);
     }
-    if (lane < nv) cp_async16(&st.q[lane * 4], Qf + (size_t)tcur.q * d + s0 + lane * 4);
+    for (int c = lane; c < len / 4; c += 32) cp_async16(&st.q[c * 4], Qf + (size_t)tcur.q * d + s0 + c * 4);
   };
   for (int64_t u = 0; u < AST - 1; ++u) {
     if (u < U) issue(u);
@@ -977,19 +1027,18 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
     cp_async_commit();
     cp_async_wait<AST - 1>();
     __syncwarp();
-    const AStage& st = W.st[u % AST];
-    const int s0 = g * ASEG;
-    const int len = min(ASEG, d - s0);
+    const AStage<T>& st = W.st[u % AST];
+    const int s0 = g * UD;
+    const int len = min(UD, d - s0);
     for (int t = lane; t < len; t += 32) W.qd[t] = (double)st.q[t];
     __syncwarp();
-    const float* row = st.rows[lane];
+    const uint8_t* row = st.rows[lane];
     const double* qv = W.qd;
     const bool last = g == nsg - 1;
     const int full8 = last ? (len & ~7) : len;
     for (int b = 0; b < full8; b += 8) {
-      const float4 x0 = *reinterpret_cast<const float4*>(row + b);
-      const float4 x1 = *reinterpret_cast<const float4*>(row + b + 4);
-      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      float xv[8];
+      load8(row, b, xv, T());
       double p[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -1003,10 +1052,10 @@ __global__ void __launch_bounds__(32 * AWARPS, 1) k_rerank_async(
     }
     if (last) {
       for (int b = full8; b < len; b += 2) {
-        const double e0 = __dsub_rn((double)row[b], qv[b]);
+        const double e0 = __dsub_rn((double)elem(row, b, T()), qv[b]);
         a0 = __dadd_rn(__dmul_rn(e0, e0), a0);
         if (b + 1 < len) {
-          const double e1 = __dsub_rn((double)row[b + 1], qv[b + 1]);
+          const double e1 = __dsub_rn((double)elem(row, b + 1, T()), qv[b + 1]);
           a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
         }
       }
@@ -1491,18 +1540,25 @@ static int num_sms() {
   return g_num_sms;
 }
 
-static int set_rerank_attrs() {
-  static bool done = false;
-  if (!done) {
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(AWarpSmem) * AWARPS)));
-    done = true;
+template <typename T>
+static int launch_rerank_async(const void* X, int d, const float* Qf, const int4* desc, const uint32_t* cand,
+                               int64_t ntiles, int kk, unsigned long long* pkey, uint32_t* pid, cudaStream_t st) {
+  constexpr int WARPS = RowFmt<T>::WARPS;
+  const size_t smem = sizeof(AWarpSmem<T>) * WARPS;
+  static bool attr = false;
+  if (!attr) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_async<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
   }
+  const int64_t grid = std::min<int64_t>(ceil_div(ntiles, WARPS), (int64_t)num_sms());
+  k_rerank_async<T><<<(unsigned)grid, 32 * WARPS, smem, st>>>(static_cast<const T*>(X), d, Qf, desc, cand, ntiles,
+                                                              kk, pkey, pid);
   return TACO_OK;
 }
 
 // rows of candidates -> CTA partial top-k -> per-query top-k (t.tk_d2 / t.tk_ids)
-static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64_t S, const int64_t* tstart,
+static int rerank_core(const float* X, const void* Xn, int fmt, int d, const float* Qf, int64_t QS, int64_t S,
+                       const int64_t* tstart,
                        const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
                        int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, double* out_d2,
                        int64_t* out_ids, cudaStream_t st) {
@@ -1519,11 +1575,13 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
   }
   if (ntiles > 0) {
     ProfScope ps(K_RERANK, st);
-    if (d % 4 == 0) {
-      TACO_TRY(set_rerank_attrs());
-      const int64_t grid = std::min<int64_t>(ceil_div(ntiles, AWARPS), (int64_t)num_sms());
-      k_rerank_async<<<(unsigned)grid, 32 * AWARPS, sizeof(AWarpSmem) * AWARPS, st>>>(
-          X, d, Qf, desc, cand, ntiles, kk, pkey.as<unsigned long long>(), pid.as<uint32_t>());
+    unsigned long long* pk = pkey.as<unsigned long long>();
+    if (fmt == TACO_ROWS_U8) {
+      TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
+    } else if (fmt == TACO_ROWS_F16) {
+      TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
+    } else if (d % 4 == 0) {
+      TACO_TRY(launch_rerank_async<float>(X, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
     } else {
       k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, desc,
                                                                    cand, ntiles, kk, pkey.as<unsigned long long>(),
@@ -1543,7 +1601,7 @@ static int rerank_core(const float* X, int d, const float* Qf, int64_t QS, int64
 static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
   QueryTile& t = idx->qt;
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
-  return rerank_core(idx->X.as<float>(), idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
+  return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
                      t.pd2, t.ppos, t.tseg, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
@@ -1899,7 +1957,8 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
     k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, 1, 1, 0, tp.as<int64_t>(), fl.as<int64_t>());
     count_launch();
-    if ((rc = rerank_core(Xd.as<float>(), d, Qd.as<float>(), 1, 1, tp.as<int64_t>(), tp.as<int64_t>(),
+    if ((rc = rerank_core(Xd.as<float>(), nullptr, TACO_ROWS_F32, d, Qd.as<float>(), 1, 1, tp.as<int64_t>(),
+                          tp.as<int64_t>(),
                           sb.as<int64_t>(),
                           sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, ts, tkd.as<double>(),
                           tki.as<int64_t>(), nullptr)))

@@ -21,7 +21,7 @@ HEADER = "include/taco_b200.h"
 
 
 def test_library_exports_every_declared_symbol():
-    decl = set(re.findall(r"^(?:int|int64_t|const char\*|void\*)\s+(taco_\w+)\(",
+    decl = set(re.findall(r"^(?:int|int32_t|int64_t|const char\*|void\*)\s+(taco_\w+)\(",
                           open(HEADER).read(), flags=re.M))
     assert len(decl) >= 30
     lib = nat.lib()

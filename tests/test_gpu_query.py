@@ -155,3 +155,31 @@ def test_traversal_units(golden):
         np.testing.assert_array_equal(np.array([(a, b) for _, a, b in act.pop_trace]).reshape(-1, 2),
                                       u[f"tr{c}_pops"].reshape(-1, 2))
         assert act.retrieved_num == int(u[f"tr{c}_ret"][0])
+
+
+@pytest.mark.parametrize("fmt", [2, 1, 0])
+def test_row_formats_bit_identical(fmt):
+    """Lossless narrow row storage (u8 / f16 / f32, taco_b200.h) must not change
+    a single bit of the answers: checked against the oracle on data that is
+    exactly representable in each format, with non-representable queries."""
+    from paper_2603_24919_b200 import _native as nat
+    from paper_2603_24919_b200.engine import _device_of
+
+    rng = np.random.default_rng(40 + fmt)
+    n, d, nq = 4000, 32, 40
+    if fmt == 2:
+        X = rng.integers(0, 256, (n, d)).astype(np.float32)
+    elif fmt == 1:
+        X = (rng.integers(-1024, 1024, (n, d)) / 64.0).astype(np.float32)
+    else:
+        X = rng.standard_normal((n, d)).astype(np.float32) * 30
+    Q = (X[rng.integers(0, n, nq)] + rng.standard_normal((nq, d)) * 3).astype(np.float32)
+    idx = T.build_index(X, T.IndexParams(4, 8, 16, 10, 1 + fmt))
+    assert nat.lib().taco_index_row_format(_device_of(idx).h) == fmt
+    oidx = O.deserialize(T.serialize_index(idx))
+    for a, b, k in [(0.05, 0.01, 10), (0.3, 0.2, 25)]:
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(a, b, k))
+        oi, od, on, ol = O.knn_batch(oidx, X, Q, a, b, k)
+        np.testing.assert_array_equal(num, on)
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(dists, od)
