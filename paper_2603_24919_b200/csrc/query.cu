@@ -555,6 +555,70 @@ __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t
   }
 }
 
+// Unordered single-pass compaction (the batch paths: a segment's candidates
+// are re-ranked as a set, ties are broken by id, so their order is free).
+// Thread t scans vectors t, t + NT, ... (conflict-free 16-byte reads); each
+// warp step scans its lanes' hit counts and reserves one run of slots with a
+// shared-memory atomic, so stores stay warp-contiguous.  *fill ends = count.
+template <int NT, bool NIB>
+__device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
+                                  int* fill) {
+  constexpr int LW = NIB ? 4 : 8;
+  constexpr int LPW = 32 / LW;
+  constexpr int IDS = 4 * LPW;
+  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
+  const uint32_t D = L == 0 ? 0u : (NIB ? (16u - L) * 0x11111111u : (256u - L) * 0x01010101u);
+  const uint4* t4 = reinterpret_cast<const uint4*>(tab);
+  const int nvec = (valid + IDS - 1) / IDS;
+  const int lane = threadIdx.x & 31;
+  for (int v0 = threadIdx.x - lane; v0 < nvec; v0 += NT) {
+    const int vi = v0 + lane;
+    uint32_t g[4] = {0u, 0u, 0u, 0u};
+    if (vi < nvec) {
+      const uint4 v = t4[vi];
+      if (L == 0) {
+        g[0] = g[1] = g[2] = g[3] = H;
+      } else {
+        g[0] = lanes_ge<NIB>(v.x, D); g[1] = lanes_ge<NIB>(v.y, D);
+        g[2] = lanes_ge<NIB>(v.z, D); g[3] = lanes_ge<NIB>(v.w, D);
+      }
+      const int lim = valid - vi * IDS;
+      if (lim < IDS) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int al = min(max(lim - u * LPW, 0), LPW);
+          g[u] &= al >= LPW ? 0xFFFFFFFFu : (1u << (al * LW)) - 1u;
+        }
+      }
+    }
+    const uint32_t any = g[0] | g[1] | g[2] | g[3];
+    if (__ballot_sync(0xffffffffu, any != 0u) == 0u) continue;
+    const int c = __popc(g[0]) + __popc(g[1]) + __popc(g[2]) + __popc(g[3]);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    int base = 0;
+    if (lane == 31) base = atomicAdd(fill, incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - c;
+    if (any) {
+      const int64_t idb = id0 + (int64_t)vi * IDS;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t m = g[u];
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          dst[pos++] = (uint32_t)(idb + u * LPW + bb / LW);
+          m &= m - 1u;
+        }
+      }
+    }
+  }
+}
+
 // Alg. 5 (engine.py:239-249) on a histogram fetched through `get(level)`.
 template <typename Get>
 __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& cand) {
@@ -596,16 +660,19 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count_cluster(
   __syncthreads();
   count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
   chunk_levels(table, valid, n_sub, S);
-  cluster.sync();
+  cluster.sync();   // every CTA's level histogram is final
+  // cluster-wide histogram: one level per thread, the csz remote reads in parallel
+  for (int l = tid; l <= n_sub; l += CT_THREADS) {
+    int h = 0;
+    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
+    S.ge[l] = h;
+  }
+  // done reading remote shared memory: arrive now, wait only before exiting
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
   if (tid == 0) {
-    int* rl[kClusterMaxCtas];
-    for (int r = 0; r < csz; ++r) rl[r] = cluster.map_shared_rank(S.lh, r);
     int64_t cands = 0;
-    const int L = alg5([&](int l) {
-      int64_t h = 0;
-      for (int r = 0; r < csz; ++r) h += rl[r][l];
-      return h;
-    }, n_sub, budget, cands);
+    const int L = alg5([&](int l) { return (int64_t)S.ge[l]; }, n_sub, budget, cands);
     int64_t mine = 0;
     for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
     const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
@@ -613,6 +680,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count_cluster(
     s_L = L;
     s_base = b;
     s_cnt = mine;
+    S.batches = 0;   // fill counter of the compaction
     sbase[q * csz + rank] = b;
     scnt[q * csz + rank] = mine;
     if (rank == 0) {
@@ -620,9 +688,10 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count_cluster(
       lvl[q] = L;
     }
   }
-  cluster.sync();   // remote histograms no longer needed by anyone after this point
-  if (s_base + s_cnt > cand_cap) return;
-  compact_table<CT_THREADS, NIB>(table, valid, (uint32_t)s_L, base, cand + s_base, S.wtot);
+  __syncthreads();
+  if (s_base + s_cnt <= cand_cap)
+    compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)s_L, base, cand + s_base, &S.batches);
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // nobody reads my histogram any more
 }
 
 // ------------------------------------------------------- global-mode count
@@ -658,8 +727,10 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
   __syncthreads();
   count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
   if (mode == CNT_EMIT) {
-    compact_table<CT_THREADS, NIB>(table, valid, (uint32_t)lvl[q], base, cand + sbase[q] + coff[q * nchunks + c],
-                                   S.wtot);
+    if (tid == 0) S.batches = 0;
+    __syncthreads();
+    compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)lvl[q], base,
+                                       cand + sbase[q] + coff[q * nchunks + c], &S.batches);
     return;
   }
   if (mode == CNT_TABLE && !NIB) {
@@ -923,14 +994,14 @@ struct AWarpSmem {
   double qd[RowFmt<T>::UD];
 };
 
-// 8 consecutive row values (exact) as f32
-__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], float) {
+// 8 consecutive row values (exact) widened to f64
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, double (&xv)[8], float) {
   const float4 x0 = *reinterpret_cast<const float4*>(rb + 4 * b);
   const float4 x1 = *reinterpret_cast<const float4*>(rb + 4 * b + 16);
   xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
   xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
 }
-__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], __half) {
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, double (&xv)[8], __half) {
   const uint4 w = *reinterpret_cast<const uint4*>(rb + 2 * b);
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -940,13 +1011,10 @@ __device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], 
     xv[2 * t + 1] = f.y;
   }
 }
-__device__ __forceinline__ void load8(const uint8_t* rb, int b, float (&xv)[8], uint8_t) {
+__device__ __forceinline__ void load8(const uint8_t* rb, int b, double (&xv)[8], uint8_t) {
   const uint2 w = *reinterpret_cast<const uint2*>(rb + b);
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {   // 2^23 + byte, exactly, then minus 2^23
-    const uint32_t bits = __byte_perm(t < 4 ? w.x : w.y, 0x4B000000u, 0x7650u + (t & 3));
-    xv[t] = __fsub_rn(__uint_as_float(bits), 8388608.0f);
-  }
+  for (int t = 0; t < 8; ++t) xv[t] = __uint2double_rn(__byte_perm(t < 4 ? w.x : w.y, 0, 0x4440u + (t & 3)));
 }
 __device__ __forceinline__ float elem(const uint8_t* rb, int b, float) { return reinterpret_cast<const float*>(rb)[b]; }
 __device__ __forceinline__ float elem(const uint8_t* rb, int b, __half) {
@@ -1037,12 +1105,12 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, 1) k_rerank_async(
     const bool last = g == nsg - 1;
     const int full8 = last ? (len & ~7) : len;
     for (int b = 0; b < full8; b += 8) {
-      float xv[8];
+      double xv[8];
       load8(row, b, xv, T());
       double p[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const double e = __dsub_rn((double)xv[t], qv[b + t]);
+        const double e = __dsub_rn(xv[t], qv[b + t]);
         p[t] = __dmul_rn(e, e);
       }
       a0 = __dadd_rn(p[6], a0); a1 = __dadd_rn(p[7], a1);
