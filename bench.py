@@ -114,8 +114,14 @@ def workload_name(meta):
 
 
 def build(X, meta):
+    """Cold build (first CUDA work of the process: context, module load, first H2D),
+    then the timed warm build whose index is used."""
     import paper_2603_24919_b200 as T
     params = T.IndexParams(meta["n_sub"], meta["s"], meta["clusters"], meta["kmeans_iters"], meta["seed"])
+    t = time.perf_counter()
+    cold = T.build_index(X, params)
+    meta["build_seconds_cold"] = time.perf_counter() - t
+    del cold
     t = time.perf_counter()
     index = T.build_index(X, params)
     wall = time.perf_counter() - t
@@ -132,10 +138,10 @@ def path_bytes(stats, meta, nq_total):
 ROW_BYTES = {0: 4, 1: 2, 2: 1}   # TACO_ROWS_F32 / F16 / U8 (taco_b200.h): bytes per stored value
 
 
-def chunking(n):
+def chunking(n, n_sub=8):
     """index.cu's id chunking: (chunk, nchunks, cluster mode)."""
     if n <= 16 * 98304:
-        ctas = min(16, max(1, -(-n // 65536)))
+        ctas = min(16, max(1, -(-n // (131072 if n_sub <= 15 else 65536))))
         chunk = -(-(-(-n // ctas)) // 1024) * 1024
         return chunk, -(-n // chunk), True
     return 65536, -(-n // 65536), False
@@ -300,7 +306,7 @@ def run_ours(args):
     device_step()
     torch.cuda.synchronize()
     prof, stats = nat.profile_read(reset=True)
-    stats["nchunks"] = chunking(meta["n"])[1]
+    stats["nchunks"] = chunking(meta["n"], meta["n_sub"])[1]
     stats["row_format"] = int(nat.lib().taco_index_row_format(dev.h))
     nat.profile_enable(False)
     total_prof = sum(v[0] for v in prof.values())
@@ -358,7 +364,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8(d) generator, seeded)",
         "config": {"workload": workload_name(meta), "n": meta["n"], "d": d, "batch": nq,
                    "l2": "256 MiB buffer written between timed steps; X (512 MB) > L2",
-                   "build_seconds": build_wall, "build_breakdown": {
+                   "build_seconds": build_wall, "build_seconds_cold": meta["build_seconds_cold"],
+                   "build_breakdown": {
                        kk: index.metadata[kk] for kk in ("covariance_seconds", "eigensolve_seconds",
                                                          "transform_seconds", "kmeans_seconds")},
                    "recall@10_sample100": rec},

@@ -172,11 +172,18 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
   idx->D = n_subspaces * subspace_dim;
   idx->iters = kmeans_iters;
   if (n_global == n && n <= kClusterMaxN) {
-    const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, 65536)));
+    // ids per CTA: 4-bit tables (n_sub <= 15) 128K = 64 KiB, 8-bit tables 64K (TACO_CLUSTER_IDS overrides)
+    int64_t target = n_subspaces <= 15 ? 131072 : 65536;
+    if (const char* e = getenv("TACO_CLUSTER_IDS")) target = std::max<int64_t>(1024, atoll(e));
+    target = std::min(target, n_subspaces <= 15 ? kClusterMaxChunk : kClusterMaxChunk8);
+    const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, target)));
     idx->chunk = ceil_div(ceil_div(n, ctas), 1024) * 1024;
     idx->cluster_mode = true;
   } else {
-    idx->chunk = kGlobalChunk;
+    idx->chunk = kGlobalChunk;   // 4-bit tables: TACO_GLOBAL_CHUNK may raise it to 131072
+    if (const char* e = getenv("TACO_GLOBAL_CHUNK"))
+      idx->chunk = std::min<int64_t>(n_subspaces <= 15 ? kClusterMaxChunk : kClusterMaxChunk8,
+                                     std::max<int64_t>(1024, atoll(e) / 1024 * 1024));
     idx->cluster_mode = false;
   }
   idx->nchunks = ceil_div(n, idx->chunk);

@@ -23,9 +23,10 @@ namespace taco {
 //    one thread-block cluster (~64 KiB each), chunk = ceil(n / ctas) rounded to 1 KiB;
 //  global mode (larger shards / multi-GPU): chunk = 64 KiB, tables in HBM.
 constexpr int64_t kGlobalChunk = 65536;
-constexpr int64_t kClusterMaxChunk = 98304;    // 2 CTAs (+ ~20 KiB static smem each) per SM
+constexpr int64_t kClusterMaxChunk = 131072;   // 4-bit tables: 64 KiB; 8-bit tables are capped at 98304
+constexpr int64_t kClusterMaxChunk8 = 98304;
 constexpr int kClusterMaxCtas = 16;             // non-portable cluster size
-constexpr int64_t kClusterMaxN = kClusterMaxChunk * kClusterMaxCtas;
+constexpr int64_t kClusterMaxN = kClusterMaxChunk8 * kClusterMaxCtas;
 
 struct DevBuf {
   void* p = nullptr;
