@@ -591,9 +591,10 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
         }
       }
     }
-    const uint32_t any = g[0] | g[1] | g[2] | g[3];
-    if (__ballot_sync(0xffffffffu, any != 0u) == 0u) continue;
-    const int c = __popc(g[0]) + __popc(g[1]) + __popc(g[2]) + __popc(g[3]);
+    // word u's hits sit at lane tops (bit LW*i + LW-1); shifted by u they are disjoint
+    uint32_t m = g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
+    if (__ballot_sync(0xffffffffu, m != 0u) == 0u) continue;
+    const int c = __popc(m);
     int incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -603,18 +604,13 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
     int base = 0;
     if (lane == 31) base = atomicAdd(fill, incl);
     base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - c;
-    if (any) {
-      const int64_t idb = id0 + (int64_t)vi * IDS;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint32_t m = g[u];
-        while (m) {
-          const int bb = __ffs(m) - 1;
-          dst[pos++] = (uint32_t)(idb + u * LPW + bb / LW);
-          m &= m - 1u;
-        }
-      }
+    uint32_t* out = dst + (base + incl - c);
+    const uint32_t idb = (uint32_t)(id0 + (int64_t)vi * IDS);
+    while (m) {
+      const int b = 31 - __clz(m);                 // highest hit first (order is free)
+      m ^= 1u << b;
+      const int u = LW - 1 - (b & (LW - 1));        // word
+      *out++ = idb + (uint32_t)(u * LPW + b / LW);  // lane b / LW of word u
     }
   }
 }
