@@ -310,9 +310,9 @@ __device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_
   const int tid = threadIdx.x;
   constexpr bool small = SMALL;   // n_sub <= 8
   static_assert(CT_UC / CT_THREADS * 8 <= 255, "per-round tally fields are 8-bit");
-  uint32_t tsm = (uint32_t)__cvta_generic_to_shared(table);
-  asm volatile("mov.u32 %0, %0;" : "+r"(tsm));   // keep it in a register (no per-atomic rematerialisation)
-  const uint32_t base32 = (uint32_t)base;
+  // 32-bit smem address of the table, biased by the chunk base (mod 2^32 arithmetic)
+  uint32_t tsg = (uint32_t)__cvta_generic_to_shared(table) - (NIB ? ((uint32_t)base >> 1) : (uint32_t)base);
+  asm volatile("mov.u32 %0, %0;" : "+r"(tsg));   // keep it in a register (no per-atomic rematerialisation)
   Tally T;
   if (tid == 0) {
     int acc = 0;
@@ -392,14 +392,16 @@ __device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           if (e < l) {
-            const uint32_t x = v[e] - base32;
+            // table word of id x lives at tsg + (x >> 1 or x) & ~3: tsg absorbs the chunk base
+            // (a multiple of 1024, so the lane position within the word is x's own low bits)
+            const uint32_t x = v[e];
             uint32_t r;
             if (NIB) {   // 4-bit counters: scores <= n_sub <= 15 never carry
               const uint32_t sh = (x << 2) & 28u;
-              r = smem_atomic_add(tsm + ((x >> 1) & ~3u), 1u << sh) >> sh;
+              r = smem_atomic_add(tsg + ((x >> 1) & ~3u), 1u << sh) >> sh;
             } else {
               const uint32_t sh = (x << 3) & 24u;
-              r = smem_atomic_add(tsm + (x & ~3u), 1u << sh) >> sh;
+              r = smem_atomic_add(tsg + (x & ~3u), 1u << sh) >> sh;
             }
             if (small) u4 += 1u << ((r << 2) & 28u);
             else T.add_wide(r & (NIB ? 0xFu : 0xFFu));
