@@ -206,7 +206,7 @@ int taco_index_destroy(taco_index* idx) {
   QueryTile& q = idx->qt;
   DevBuf* qb[] = {&q.Q, &q.qt, &q.sd, &q.sl, &q.pops, &q.npop, &q.ret, &q.flags, &q.scores, &q.part,
                   &q.hist, &q.lvl, &q.cnum, &q.clocal, &q.coff, &q.qbase, &q.cursor, &q.cand,
-                  &q.bpref, &q.pd2, &q.ppos, &q.tseg, &q.ppref, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d};
+                  &q.bpref, &q.pd2, &q.ppos, &q.tseg, &q.ppref, &q.psum, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d};
   for (auto* b : qb) b->release();
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,

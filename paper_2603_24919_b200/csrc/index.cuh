@@ -39,7 +39,7 @@ struct DevBuf {
 
 struct QueryTile {
   DevBuf Q, qt, sd, sl, pops, npop, ret, flags, scores, part, hist, lvl, cnum, clocal, coff, qbase,
-      cursor, cand, bpref, pd2, ppos, tseg, ppref, tk_d2, tk_ids, out_ids, out_d;
+      cursor, cand, bpref, pd2, ppos, tseg, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   int64_t cand_cap = 0;
   int pop_cap = 0;
 };

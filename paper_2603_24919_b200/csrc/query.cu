@@ -14,7 +14,7 @@
 //   k_count           per (query, 64 Ki chunk) smem counting -> HBM tables +
 //                     per-chunk histograms;  k_hist_reduce -> (all-reduce across
 //                     ranks) -> k_select (Alg. 5) -> k_compact
-//   k_rr_plan         32-candidate tiles per candidate segment
+//   k_plan_*          32-candidate tiles per candidate segment (two orders)
 //   k_rerank_tma      persistent warp-specialised gather: cp.async.bulk (TMA
 //                     bulk copies) of candidate row segments into an mbarrier
 //                     ring, fp64 einsum-order distances, warp top-k  engine.py:272-275
@@ -846,44 +846,74 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
 
 // ------------------------------------------------------------ rerank plan
 constexpr int GR = 32;    // candidate rows per rerank tile (one warp: lane = row)
-// Exclusive prefix of the tiles per segment, enumerated query-major
-// (segment p) or chunk-major (p = r * QS + q -> segment q * S + r):
-// tstart[segment] = its first tile in that order, total in flags[2].
-__global__ void __launch_bounds__(1024) k_rr_plan(const int64_t* __restrict__ scnt, int64_t nseg, int S,
-                                                  int64_t QS, int chunk_major, int64_t* __restrict__ tstart,
-                                                  int64_t* __restrict__ flags) {
-  __shared__ int64_t wsum[32];
+// Tile plans: exclusive prefixes of the tiles per segment in two orders,
+// query-major (segment p) and chunk-major (p = r * QS + q -> segment q * S + r);
+// tq/tp[segment] = its first tile in that order, total in flags[2].  Two
+// launches: per-1024-segment block sums, then block offsets + in-block scans.
+constexpr int PLAN_NT = 1024;
+__device__ __forceinline__ int64_t seg_cm(int64_t p, int64_t QS, int S) { return (p % QS) * S + p / QS; }
+__device__ __forceinline__ int64_t seg_tiles(const int64_t* scnt, int64_t sg) { return (scnt[sg] + GR - 1) / GR; }
+
+// inclusive block scan of two int64 values (PLAN_NT threads)
+__device__ __forceinline__ void block_scan2(int64_t& a, int64_t& b, int64_t* ws /* [2][32] */) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t per = (nseg + 1023) / 1024;
-  const int64_t a0 = threadIdx.x * per, a1 = min(nseg, a0 + per);
-  auto seg_of = [&](int64_t p) -> int64_t { return chunk_major ? (p % QS) * S + p / QS : p; };
-  int64_t loc = 0;
-  for (int64_t p = a0; p < a1; ++p) loc += (scnt[seg_of(p)] + GR - 1) / GR;
-  int64_t v = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int64_t x = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += x;
+    const int64_t x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) { a += x; b += y; }
   }
-  if (lane == 31) wsum[wid] = v;
+  if (lane == 31) { ws[wid] = a; ws[32 + wid] = b; }
   __syncthreads();
   if (wid == 0) {
-    int64_t w = wsum[lane];
+    int64_t x = ws[lane], y = ws[32 + lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int64_t x = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += x;
+      const int64_t u = __shfl_up_sync(0xffffffffu, x, o), v = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) { x += u; y += v; }
     }
-    wsum[lane] = w;
+    ws[lane] = x;
+    ws[32 + lane] = y;
   }
   __syncthreads();
-  int64_t run = (wid ? wsum[wid - 1] : 0) + v - loc;
-  for (int64_t p = a0; p < a1; ++p) {
-    const int64_t sg = seg_of(p);
-    tstart[sg] = run;
-    run += (scnt[sg] + GR - 1) / GR;
+  if (wid) { a += ws[wid - 1]; b += ws[32 + wid - 1]; }
+}
+
+__global__ void __launch_bounds__(PLAN_NT) k_plan_sums(const int64_t* __restrict__ scnt, int64_t nseg, int S,
+                                                       int64_t QS, int64_t* __restrict__ bsum) {
+  __shared__ int64_t ws[64];
+  const int64_t p = (int64_t)blockIdx.x * PLAN_NT + threadIdx.x;
+  int64_t a = p < nseg ? seg_tiles(scnt, p) : 0, b = p < nseg ? seg_tiles(scnt, seg_cm(p, QS, S)) : 0;
+  block_scan2(a, b, ws);
+  if (threadIdx.x == PLAN_NT - 1) {
+    bsum[blockIdx.x] = a;
+    bsum[gridDim.x + blockIdx.x] = b;
   }
-  if (threadIdx.x == 1023 && flags) flags[2] = run;
+}
+
+__global__ void __launch_bounds__(PLAN_NT) k_plan_scan(const int64_t* __restrict__ scnt, int64_t nseg, int S,
+                                                       int64_t QS, const int64_t* __restrict__ bsum,
+                                                       int64_t* __restrict__ tq, int64_t* __restrict__ tp,
+                                                       int64_t* __restrict__ flags) {
+  __shared__ int64_t ws[64];
+  __shared__ int64_t off[2];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {   // this block's offsets: sums of the earlier blocks
+    int64_t x = 0, y = 0;
+    for (int i = lane; i < (int)blockIdx.x; i += 32) { x += bsum[i]; y += bsum[gridDim.x + i]; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { x += __shfl_xor_sync(0xffffffffu, x, o); y += __shfl_xor_sync(0xffffffffu, y, o); }
+    if (lane == 0) { off[0] = x; off[1] = y; }
+  }
+  const int64_t p = (int64_t)blockIdx.x * PLAN_NT + threadIdx.x;
+  const int64_t sq = p, sc = p < nseg ? seg_cm(p, QS, S) : 0;
+  const int64_t ta = p < nseg ? seg_tiles(scnt, sq) : 0, tb = p < nseg ? seg_tiles(scnt, sc) : 0;
+  int64_t a = ta, b = tb;
+  block_scan2(a, b, ws);   // (syncs make off[] visible)
+  if (p < nseg) {
+    tq[sq] = off[0] + a - ta;
+    if (tp) tp[sc] = off[1] + b - tb;
+  }
+  if (p == nseg - 1 && flags) flags[2] = off[0] + a;
 }
 
 // Tile descriptors in processing order (one warp per segment):
@@ -1581,15 +1611,15 @@ static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t f
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   {
     ProfScope ps(K_PLAN, st);
-    k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S, QS, 0, t.bpref.as<int64_t>(),
-                                  t.flags.as<int64_t>());
+    const int64_t nseg = QS * S, nb = ceil_div(nseg, PLAN_NT);
+    TACO_TRY(t.psum.ensure(sizeof(int64_t) * 2 * (size_t)nb));
+    if (S > 1) TACO_TRY(t.ppref.ensure(sizeof(int64_t) * (size_t)(nseg + 1)));
+    k_plan_sums<<<(unsigned)nb, PLAN_NT, 0, st>>>(t.clocal.as<int64_t>(), nseg, (int)S, QS, t.psum.as<int64_t>());
     TACO_LAUNCHED();
-    if (S > 1) {
-      TACO_TRY(t.ppref.ensure(sizeof(int64_t) * (size_t)(QS * S + 1)));
-      k_rr_plan<<<1, 1024, 0, st>>>(t.clocal.as<int64_t>(), QS * S, (int)S, QS, 1, t.ppref.as<int64_t>(),
-                                    nullptr);
-      TACO_LAUNCHED();
-    }
+    k_plan_scan<<<(unsigned)nb, PLAN_NT, 0, st>>>(t.clocal.as<int64_t>(), nseg, (int)S, QS, t.psum.as<int64_t>(),
+                                                  t.bpref.as<int64_t>(), S > 1 ? t.ppref.as<int64_t>() : nullptr,
+                                                  t.flags.as<int64_t>());
+    TACO_LAUNCHED();
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -2006,11 +2036,12 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
   for (int64_t i = 0; i < m; ++i)
     std::copy(X_h + (size_t)c32[i] * d, X_h + (size_t)c32[i] * d + d, rowsv.begin() + (size_t)i * d);
   const int64_t ntiles = ceil_div(m, GR);
-  DevBuf Xd, Qd, sb, sc, tp, cd, pk, pi, ts, tkd, tki, fl;
+  DevBuf Xd, Qd, sb, sc, tp, ps, cd, pk, pi, ts, tkd, tki, fl;
   int rc = TACO_OK;
   do {
     if ((rc = Xd.ensure(sizeof(float) * rowsv.size())) || (rc = Qd.ensure(sizeof(float) * d)) ||
-        (rc = sb.ensure(8)) || (rc = sc.ensure(8)) || (rc = tp.ensure(16)) || (rc = cd.ensure(4 * m)) ||
+        (rc = sb.ensure(8)) || (rc = sc.ensure(8)) || (rc = tp.ensure(16)) || (rc = ps.ensure(16)) ||
+        (rc = cd.ensure(4 * m)) ||
         (rc = tkd.ensure(8 * k)) || (rc = tki.ensure(8 * k)) || (rc = fl.ensure(64)))
       break;
     std::vector<uint32_t> local(m);
@@ -2021,7 +2052,10 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     cudaMemcpy(sb.p, &zero, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(sc.p, &m, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(cd.p, local.data(), 4 * m, cudaMemcpyHostToDevice);
-    k_rr_plan<<<1, 1024>>>(sc.as<int64_t>(), 1, 1, 1, 0, tp.as<int64_t>(), fl.as<int64_t>());
+    k_plan_sums<<<1, PLAN_NT>>>(sc.as<int64_t>(), 1, 1, 1, ps.as<int64_t>());
+    k_plan_scan<<<1, PLAN_NT>>>(sc.as<int64_t>(), 1, 1, 1, ps.as<int64_t>(), tp.as<int64_t>(), nullptr,
+                                fl.as<int64_t>());
+    count_launch();
     count_launch();
     if ((rc = rerank_core(Xd.as<float>(), nullptr, TACO_ROWS_F32, d, Qd.as<float>(), 1, 1, tp.as<int64_t>(),
                           tp.as<int64_t>(),
@@ -2043,7 +2077,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     }
   } while (0);
   Xd.release(); Qd.release(); sb.release(); sc.release(); tp.release(); cd.release(); pk.release();
-  pi.release(); ts.release(); tkd.release(); tki.release(); fl.release();
+  pi.release(); ts.release(); ps.release(); tkd.release(); tki.release(); fl.release();
   return rc;
 }
 
