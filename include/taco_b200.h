@@ -144,6 +144,17 @@ int taco_topk_merge_device(int32_t ranks, int64_t nq, int32_t k, const double* d
 /* Test hook: 1 forces every k-means++ draw through the exact numpy replay. */
 int taco_debug_force_replay(int on);
 
+/* --------------------------------------------------------- ground truth */
+/* Exact k-NN (dataio.compute_ground_truth, dataio.py:142-172): fp64
+ * d2 = max((xsq - 2 q.x) + qsq, 0) with numpy's einsum / dgemm orders, the k
+ * smallest (d2, id), dists = f32(sqrt(d2)).  k <= 1024, d <= 25600.
+ * ids_h int32 [nq][k], dists_h f32 [nq][k], host buffers. */
+int taco_ground_truth(int device, const float* X_h, int64_t n, int32_t d, const float* Q_h, int64_t nq,
+                      int32_t k, int32_t* ids_h, float* dists_h);
+/* Same over the index's resident base vectors (whole dataset, not a shard). */
+int taco_ground_truth_index(taco_index* idx, const float* Q_h, int64_t nq, int32_t k, int32_t* ids_h,
+                            float* dists_h);
+
 /* --------------------------------------------------------------- profiling */
 /* Per-kernel CUDA-event timing of the query path on its launching stream. */
 int taco_profile_enable(int on);
