@@ -155,6 +155,15 @@ int taco_ground_truth(int device, const float* X_h, int64_t n, int32_t d, const 
 int taco_ground_truth_index(taco_index* idx, const float* Q_h, int64_t nq, int32_t k, int32_t* ids_h,
                             float* dists_h);
 
+/* SC-Linear exact collision counting (engine.sc_linear_scores, engine.py:290-321):
+ * per subspace, the ceil(alpha n) nearest points by (einsum fp64 d2, id) collide.
+ * T_h row-major n x (n_sub*s) f32, qt_h the transformed query (n_sub*s f32),
+ * scores_h uint8[n]. */
+int taco_sc_linear_scores(int device, const float* T_h, int64_t n, int32_t n_sub, int32_t s, const float* qt_h,
+                          double alpha, uint8_t* scores_h);
+/* Same over the index's resident transformed matrix. */
+int taco_sc_linear_scores_index(taco_index* idx, const float* qt_h, double alpha, uint8_t* scores_h);
+
 /* --------------------------------------------------------------- profiling */
 /* Per-kernel CUDA-event timing of the query path on its launching stream. */
 int taco_profile_enable(int on);

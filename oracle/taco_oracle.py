@@ -485,6 +485,22 @@ def knn_batch(index, X, Q, alpha, beta, k, threads=1):
     return out_i, out_d, num, lvl
 
 
+def sc_linear_scores(T, qt, n_sub, s, alpha):
+    """engine.py:290-321 -- exact collisions: per subspace, the ceil(alpha n)
+    nearest rows by (fp64 einsum d2, id) collide."""
+    T = np.asarray(T)
+    qt = np.asarray(qt, dtype=np.float64).ravel()
+    n = T.shape[0]
+    collide = min(n, math.ceil(alpha * n))
+    scores = np.zeros(n, np.uint8)
+    ids = np.arange(n)
+    for j in range(n_sub):
+        diff = T[:, j * s:(j + 1) * s].astype(np.float64) - qt[j * s:(j + 1) * s]
+        dd = np.einsum("ij,ij->i", diff, diff)
+        scores[np.lexsort((ids, dd))[:collide]] += 1
+    return scores
+
+
 def ground_truth(base, queries, k):
     """dataio.py:142-172 -- exact k-NN, fp64 expansion form, ties by id."""
     X = np.asarray(base).astype(np.float64)

@@ -58,6 +58,8 @@ _SIGS = {
     "taco_topk_merge_device": [_c_i32, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_ground_truth": [_c_int, _vp, _c_i64, _c_i32, _vp, _c_i64, _c_i32, _vp, _vp],
     "taco_ground_truth_index": [_vp, _vp, _c_i64, _c_i32, _vp, _vp],
+    "taco_sc_linear_scores": [_c_int, _vp, _c_i64, _c_i32, _c_i32, _vp, _c_dbl, _vp],
+    "taco_sc_linear_scores_index": [_vp, _vp, _c_dbl, _vp],
     "taco_count_scores": [_vp, _vp, _c_dbl, _vp],
     "taco_activation_trace": [_vp, _vp, _c_i32, _c_dbl, _c_i32, _vp, _vp, _vp, _vp],
     "taco_select_candidates": [_c_int, _vp, _c_i64, _c_i32, _c_dbl, _vp, _vp, _vp],

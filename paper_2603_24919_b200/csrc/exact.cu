@@ -1,4 +1,6 @@
-// Exact k-NN ground truth on the device: the reference's
+// Index-free exact paths on the device.
+//
+// 1. Exact k-NN ground truth: the reference's
 // dataio.compute_ground_truth (dataio.py:142-172) with its arithmetic --
 //   xsq = einsum('ij,ij->i', X, X)            (numpy 2-lane einsum order)
 //   G   = Q @ X.T                             (dgemm: one FMA chain over d)
@@ -8,6 +10,7 @@
 // full fp64 distance rows (each X row read once per tile, GT_QT FMA chains per
 // thread), then one CTA per query radix-selects its k smallest (d2, id).
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "index.cuh"
@@ -239,6 +242,86 @@ static int ground_truth_impl(int device, const float* X_d, int64_t n, int d, con
   return rc;
 }
 
+// 2. SC-Linear exact collision counting (engine.py:290-321):
+// per subspace j, d2_j(i) = einsum((f64 T[i, js:js+s] - f64 qt[js:js+s])^2);
+// the ceil(alpha n) smallest (d2_j, id) collide; scores[i] = #subspaces.
+// T element (i, c) lives at T[i * rs + c * cs] (row-major host copy or the
+// index's dimension-major resident matrix).
+__global__ void k_sc_d2(const float* __restrict__ T, int64_t n, int64_t rs, int64_t cs, int s,
+                        const double* __restrict__ qt, double* __restrict__ D2) {
+  const int j = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float* base = T + i * rs + (int64_t)j * s * cs;
+    const double* qj = qt + (int64_t)j * s;
+    const double v = einsum_sq([&](int t) { return __dsub_rn((double)base[t * cs], qj[t]); }, s);
+    D2[(int64_t)j * n + i] = v;   // a sum of squares: >= +0, bit patterns order like values
+  }
+}
+
+__global__ void __launch_bounds__(GS_NT) k_sc_select(const double* __restrict__ D2, int64_t n, int collide,
+                                                      unsigned long long* __restrict__ cut) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long s_pre;
+  __shared__ int s_rem;
+  __shared__ unsigned s_ties;
+  const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(D2 + (int64_t)blockIdx.x * n);
+  unsigned long long tau, pi = ~0ull;
+  int take;
+  unsigned ties;
+  gt_radix(keys, n, collide, false, 0ull, tau, take, ties, hist, &s_pre, &s_rem, &s_ties);
+  if (ties > (unsigned)take) {
+    int dummy;
+    unsigned t2;
+    gt_radix(keys, n, take, true, tau, pi, dummy, t2, hist, &s_pre, &s_rem, &s_ties);
+  }
+  if (threadIdx.x == 0) {
+    cut[2 * blockIdx.x] = tau;
+    cut[2 * blockIdx.x + 1] = pi;
+  }
+}
+
+__global__ void k_sc_mark(const double* __restrict__ D2, int64_t n, int n_sub,
+                          const unsigned long long* __restrict__ cut, uint8_t* __restrict__ scores) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int j = 0; j < n_sub; ++j) {
+      const unsigned long long kv = (unsigned long long)__double_as_longlong(D2[(int64_t)j * n + i]);
+      c += kv < cut[2 * j] || (kv == cut[2 * j] && (unsigned long long)i <= cut[2 * j + 1]);
+    }
+    scores[i] = (uint8_t)c;
+  }
+}
+
+static int sc_linear_impl(int device, const float* T_d, int64_t n, int64_t rs, int64_t cs, int n_sub, int s,
+                          const float* qt_h, double alpha, uint8_t* scores_h) {
+  if (n < 1) TACO_FAIL(TACO_ERR_PARAMETER, "empty transformed matrix");
+  if (n_sub < 1 || n_sub > 255 || s < 1) TACO_FAIL(TACO_ERR_PARAMETER, "bad subspace layout %d x %d", n_sub, s);
+  if (!(alpha > 0.0 && alpha <= 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "collision ratio %g outside (0, 1]", alpha);
+  const int64_t collide = std::min<int64_t>(n, (int64_t)std::ceil(alpha * (double)n));   // engine.py:309
+  std::vector<double> q64((size_t)n_sub * s);
+  for (size_t t = 0; t < q64.size(); ++t) q64[t] = (double)qt_h[t];
+  DevBuf qd, D2, cut, sc;
+  int rc = TACO_OK;
+  do {
+    if ((rc = qd.ensure(sizeof(double) * q64.size())) || (rc = D2.ensure(sizeof(double) * (size_t)n_sub * n)) ||
+        (rc = cut.ensure(16 * (size_t)n_sub)) || (rc = sc.ensure((size_t)n)))
+      break;
+    cudaMemcpy(qd.p, q64.data(), sizeof(double) * q64.size(), cudaMemcpyHostToDevice);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(n, 256), (int64_t)sms * 8);
+    k_sc_d2<<<dim3(gx, (unsigned)n_sub), 256>>>(T_d, n, rs, cs, s, qd.as<double>(), D2.as<double>());
+    k_sc_select<<<(unsigned)n_sub, GS_NT>>>(D2.as<double>(), n, (int)collide, cut.as<unsigned long long>());
+    k_sc_mark<<<gx, 256>>>(D2.as<double>(), n, n_sub, cut.as<unsigned long long>(), sc.as<uint8_t>());
+    count_launch(3);
+    cudaMemcpy(scores_h, sc.p, (size_t)n, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; }
+  } while (0);
+  qd.release(); D2.release(); cut.release(); sc.release();
+  return rc;
+}
+
 }  // namespace taco
 
 using namespace taco;
@@ -256,6 +339,27 @@ int taco_ground_truth(int device, const float* X_h, int64_t n, int32_t d, const 
                             : (set_error("%s", cudaGetErrorString(e)), TACO_ERR_CUDA);
   X.release();
   return rc;
+}
+
+int taco_sc_linear_scores(int device, const float* T_h, int64_t n, int32_t n_sub, int32_t s, const float* qt_h,
+                          double alpha, uint8_t* scores_h) {
+  TACO_TRY(with_device(device));
+  if (n < 1 || n_sub < 1 || s < 1) TACO_FAIL(TACO_ERR_PARAMETER, "empty transformed matrix");
+  DevBuf T;
+  TACO_TRY(T.ensure(sizeof(float) * (size_t)n * n_sub * s));
+  cudaError_t e = cudaMemcpy(T.p, T_h, sizeof(float) * (size_t)n * n_sub * s, cudaMemcpyHostToDevice);
+  int rc = e == cudaSuccess ? sc_linear_impl(device, T.as<float>(), n, (int64_t)n_sub * s, 1, n_sub, s, qt_h, alpha,
+                                             scores_h)
+                            : (set_error("%s", cudaGetErrorString(e)), TACO_ERR_CUDA);
+  T.release();
+  return rc;
+}
+
+int taco_sc_linear_scores_index(taco_index* idx, const float* qt_h, double alpha, uint8_t* scores_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_T) TACO_FAIL(TACO_ERR_STATE, "transformed matrix not resident");
+  return sc_linear_impl(idx->device, idx->T.as<float>(), idx->n, 1, idx->n, idx->n_sub, idx->s, qt_h, alpha,
+                        scores_h);
 }
 
 int taco_ground_truth_index(taco_index* idx, const float* Q_h, int64_t nq, int32_t k, int32_t* ids_h,

@@ -37,6 +37,7 @@ from .errors import (
     InsufficientDataError,
     NumericError,
     ParameterError,
+    StateError,
     UnsupportedVersionError,
 )
 from .imi import DeviceCells, InvertedMultiIndex, run_kmeans_all
@@ -260,10 +261,12 @@ def build_index(data, params: IndexParams, keep_transformed: bool = False) -> Ta
         "warnings": list(model.warnings),
         "device": dev.device,
     }
+    dev.has_T = True   # the device keeps the transformed matrix it built from
     transformed = None
     if keep_transformed:
         transformed = np.empty((n, params.output_dim), np.float32)
         nat.call("taco_get_transformed", dev.h, nat.ptr(transformed))
+        dev.transformed_key = _data_key(transformed)
     return TacoIndex(params=params, transform=model, subspaces=subspaces, n=n, metadata=metadata,
                      transformed=transformed, device=dev)
 
@@ -275,6 +278,9 @@ def attach_transformed(index: TacoIndex, data) -> TacoIndex:
         raise ParameterError(
             f"data shape {np.shape(data)} does not match index ({index.n}, {index.d})")
     index.transformed = transform_points(index.transform, X)
+    dev = index.device
+    if dev is not None and getattr(dev, "has_T", False) and dev.data_key == _data_key(X):
+        dev.transformed_key = _data_key(index.transformed)   # same rows as the resident matrix
     return index
 
 
@@ -381,6 +387,57 @@ def knn_query(index: TacoIndex, data, query, qp: QueryParams,
     ids, dists, _, _ = knn_query_batch(index, data, q[None, :], qp)
     keep = ids[0] >= 0
     return SearchResult(ids=ids[0][keep].copy(), dists=dists[0][keep].copy())
+
+
+def sc_linear_scores(transformed, query_t, n_subspaces: int, subspace_dim: int,
+                     alpha: float) -> np.ndarray:
+    """Exact collision counting without the index (engine.py:290-321), on the
+    GPU: per subspace the ceil(alpha*n) nearest points by (fp64 einsum d2, id)
+    collide; scores[i] = number of subspaces where i collides."""
+    Tm = np.asarray(transformed)
+    qt = np.asarray(query_t).ravel()
+    if Tm.ndim != 2:
+        raise ParameterError(f"expected a 2-D matrix, got shape {Tm.shape}")
+    n = Tm.shape[0]
+    if qt.shape[0] != Tm.shape[1]:
+        raise DimensionMismatchError(
+            f"query has dimension {qt.shape[0]}, transformed data has {Tm.shape[1]}")
+    if n_subspaces * subspace_dim != Tm.shape[1]:
+        raise ParameterError(f"{n_subspaces} x {subspace_dim} does not cover {Tm.shape[1]} columns")
+    if not 0.0 < alpha <= 1.0:
+        raise ParameterError(f"collision ratio {alpha} outside (0, 1]")
+    scores = np.zeros(n, np.uint8)
+    if n == 0:
+        return scores
+    T32 = as_f32_exact(Tm, "transformed")
+    q32 = as_f32_exact(qt, "query_t")
+    nat.call("taco_sc_linear_scores", nat.device_id(), nat.ptr(T32), n, int(n_subspaces), int(subspace_dim),
+             nat.ptr(q32), float(alpha), nat.ptr(scores))
+    return scores
+
+
+def sc_linear_query(index: TacoIndex, data, query, qp: QueryParams) -> SearchResult:
+    """Query through exact collision counting over the retained transformed
+    matrix (engine.py:324-342).  The scores come from the index's resident
+    transformed matrix when it holds the same rows, else from the host copy."""
+    if index.transformed is None:
+        raise StateError(
+            "transformed matrix was not retained at build time; rebuild with "
+            "keep_transformed=True or call attach_transformed()")
+    q = np.asarray(query, dtype=np.float32).ravel()
+    if q.shape[0] != index.d:
+        raise DimensionMismatchError(f"query has dimension {q.shape[0]}, index expects {index.d}")
+    qt = np.ascontiguousarray(transform_points(index.transform, q[None, :])[0], dtype=np.float32)
+    p = index.params
+    scores = None
+    dev = index.device
+    if dev is not None and getattr(dev, "transformed_key", None) == _data_key(index.transformed):
+        scores = np.zeros(index.n, np.uint8)
+        nat.call("taco_sc_linear_scores_index", dev.h, nat.ptr(qt), float(qp.alpha), nat.ptr(scores))
+    if scores is None:
+        scores = sc_linear_scores(index.transformed, qt, p.n_subspaces, p.subspace_dim, qp.alpha)
+    cand = select_candidates(scores, qp.beta, p.n_subspaces, index.n)
+    return rerank(data, query, cand, qp.k)
 
 
 # --------------------------------------------------------------- persistence

@@ -181,11 +181,61 @@ def unit_fixture(ref):
     print("units", len(out))
 
 
+SC_CASES = [  # (seed, n, n_sub, s, integer-valued T)
+    (11, 3000, 4, 8, False),
+    (12, 2500, 8, 4, True),     # integer coordinates: many distance ties, decided by id
+]
+SC_ALPHAS = [0.01, 0.05, 0.3, 1.0]
+
+
+def sc_inputs(seed, n, n_sub, s, ints):
+    rng = np.random.default_rng([77, seed])
+    if ints:
+        T = rng.integers(-3, 4, (n, n_sub * s)).astype(np.float32)
+        q = rng.integers(-3, 4, (6, n_sub * s)).astype(np.float32)
+    else:
+        T = rng.standard_normal((n, n_sub * s)).astype(np.float32)
+        q = rng.standard_normal((6, n_sub * s)).astype(np.float32)
+    return T, q
+
+
+def sc_fixture(ref):
+    """engine.sc_linear_scores on seeded transformed matrices, and
+    sc_linear_query on the rig1 index (reference-built, transformed attached)."""
+    out = {}
+    for ci, (seed, n, n_sub, s, ints) in enumerate(SC_CASES):
+        T, q = sc_inputs(seed, n, n_sub, s, ints)
+        for qi in range(q.shape[0]):
+            for ai, a in enumerate(SC_ALPHAS):
+                out[f"sc_{ci}_{qi}_{ai}"] = ref.engine.sc_linear_scores(T, q[qi], n_sub, s, a)
+    name, cfg, n, nq, d, n_sub, s, kp, iters, seed, grid = RIGS[0]
+    X, Q, _ = make_config(cfg, n=n, nq=nq, d=d)
+    blob = np.load(os.path.join(HERE, f"{name}.npz"))["blob"].tobytes()
+    index = ref.engine.deserialize_index(blob) if hasattr(ref.engine, "deserialize_index") else None
+    if index is None:
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".taco") as fh:
+            fh.write(blob)
+            fh.flush()
+            index = ref.load_index(fh.name)
+    ref.attach_transformed(index, X)
+    for qi in range(8):
+        for gi, (a, b, k) in enumerate([(0.05, 0.01, 10), (0.2, 0.05, 15)]):
+            r = ref.engine.sc_linear_query(index, X, Q[qi], ref.QueryParams(alpha=a, beta=b, k=k))
+            out[f"q_{qi}_{gi}_ids"] = r.ids
+            out[f"q_{qi}_{gi}_dists"] = r.dists
+    np.savez_compressed(os.path.join(HERE, "sclinear.npz"), **out)
+
+
 def main():
     ref = load_reference()
+    if sys.argv[1:] == ["sclinear"]:
+        sc_fixture(ref)
+        return
     unit_fixture(ref)
     for rig in RIGS:
         rig_fixture(ref, *rig)
+    sc_fixture(ref)
 
 
 if __name__ == "__main__":

@@ -183,3 +183,49 @@ def test_row_formats_bit_identical(fmt):
         np.testing.assert_array_equal(num, on)
         np.testing.assert_array_equal(ids, oi)
         np.testing.assert_array_equal(dists, od)
+
+
+def test_sc_linear_scores_vs_reference():
+    """SC-Linear exact collision counting on the GPU
+    against the reference's engine.sc_linear_scores (tests/golden/sclinear.npz)."""
+    import sys
+    sys.path.insert(0, "tests/golden")
+    from make_golden import SC_ALPHAS, SC_CASES, sc_inputs
+    g = np.load("tests/golden/sclinear.npz")
+    for ci, (seed, n, n_sub, s, ints) in enumerate(SC_CASES):
+        T_, q = sc_inputs(seed, n, n_sub, s, ints)
+        for qi in range(q.shape[0]):
+            for ai, a in enumerate(SC_ALPHAS):
+                np.testing.assert_array_equal(T.sc_linear_scores(T_, q[qi], n_sub, s, a), g[f"sc_{ci}_{qi}_{ai}"])
+
+
+def test_sc_linear_query_vs_reference(golden):
+    g = golden("rig1")
+    cfg, n, nq, d, ns, s, kp, it, seed = (int(v) for v in g["params"])
+    X, Q, _ = make_config(cfg, n=n, nq=nq, d=d)
+    idx = T.deserialize_index(g["blob"].tobytes())
+    with pytest.raises(T.StateError):
+        T.sc_linear_query(idx, X, Q[0], T.QueryParams(0.05, 0.01, 10))
+    T.attach_transformed(idx, X)
+    gs = np.load("tests/golden/sclinear.npz")
+    for qi in range(8):
+        for gi, (a, b, k) in enumerate([(0.05, 0.01, 10), (0.2, 0.05, 15)]):
+            r = T.sc_linear_query(idx, X, Q[qi], T.QueryParams(a, b, k))
+            np.testing.assert_array_equal(r.ids, gs[f"q_{qi}_{gi}_ids"])
+            np.testing.assert_array_equal(r.dists, gs[f"q_{qi}_{gi}_dists"])
+
+
+def test_sc_linear_resident_matches_host():
+    """The resident-matrix path (built index, keep_transformed) equals the
+    host-matrix path."""
+    X, Q, _ = make_config(1, n=3000, nq=4, d=32)
+    idx = T.build_index(X, T.IndexParams(4, 8, 16, 5, 1), keep_transformed=True)
+    assert getattr(idx.device, "transformed_key", None) is not None
+    for qi in range(4):
+        r1 = T.sc_linear_query(idx, X, Q[qi], T.QueryParams(0.1, 0.02, 10))
+        qt = T.transform_points(idx.transform, Q[qi][None, :])[0]
+        sc = T.sc_linear_scores(idx.transformed, qt, 4, 8, 0.1)
+        cand = T.select_candidates(sc, 0.02, 4, 3000)
+        r2 = T.rerank(X, Q[qi], cand, 10)
+        np.testing.assert_array_equal(r1.ids, r2.ids)
+        np.testing.assert_array_equal(r1.dists, r2.dists)

@@ -131,3 +131,16 @@ def test_select_hand_traces():
 def test_seeds(golden):
     for r, p, want in golden("units")["seeds"]:
         assert O.derive_seed(int(r), int(p)) == int(want)
+
+
+def test_sc_linear_scores_vs_reference():
+    """oracle.sc_linear_scores pinned to the reference's engine.sc_linear_scores."""
+    import sys
+    sys.path.insert(0, "tests/golden")
+    from make_golden import SC_ALPHAS, SC_CASES, sc_inputs
+    g = np.load("tests/golden/sclinear.npz")
+    for ci, (seed, n, n_sub, s, ints) in enumerate(SC_CASES):
+        T, q = sc_inputs(seed, n, n_sub, s, ints)
+        for qi in range(q.shape[0]):
+            for ai, a in enumerate(SC_ALPHAS):
+                np.testing.assert_array_equal(O.sc_linear_scores(T, q[qi], n_sub, s, a), g[f"sc_{ci}_{qi}_{ai}"])
