@@ -33,6 +33,16 @@ int DevBuf::ensure(size_t want) {
   return TACO_OK;
 }
 
+void QueryTile::release() {
+  DevBuf* qb[] = {&Q, &qt, &sd, &sl, &pops, &npop, &ret, &flags, &scores, &part, &hist, &lvl, &cnum, &clocal,
+                  &coff, &qbase, &cursor, &cand, &bpref, &pd2, &ppos, &tseg, &ppref, &psum, &tk_d2, &tk_ids,
+                  &out_ids, &out_d};
+  for (auto* b : qb) b->release();
+  if (flags_h) cudaFreeHost(flags_h);
+  flags_h = nullptr;
+  cand_cap = 0;
+}
+
 void DevBuf::release() {
   if (p) cudaFree(p);
   p = nullptr;
@@ -203,11 +213,8 @@ int taco_index_destroy(taco_index* idx) {
   DevBuf* bufs[] = {&idx->X, &idx->Xn, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
                     &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
   for (auto* b : bufs) b->release();
-  QueryTile& q = idx->qt;
-  DevBuf* qb[] = {&q.Q, &q.qt, &q.sd, &q.sl, &q.pops, &q.npop, &q.ret, &q.flags, &q.scores, &q.part,
-                  &q.hist, &q.lvl, &q.cnum, &q.clocal, &q.coff, &q.qbase, &q.cursor, &q.cand,
-                  &q.bpref, &q.pd2, &q.ppos, &q.tseg, &q.ppref, &q.psum, &q.tk_d2, &q.tk_ids, &q.out_ids, &q.out_d};
-  for (auto* b : qb) b->release();
+  idx->qt.release();
+  idx->qt2.release();
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
                     &s.csq, &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl,
@@ -215,6 +222,9 @@ int taco_index_destroy(taco_index* idx) {
     for (auto* b : sb) b->release();
   }
   for (auto st : idx->half_streams) cudaStreamDestroy(st);
+  if (idx->stream2) cudaStreamDestroy(idx->stream2);
+  if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
+  if (idx->ev_join) cudaEventDestroy(idx->ev_join);
   cudaStreamDestroy(idx->stream);
   delete idx;
   return TACO_OK;

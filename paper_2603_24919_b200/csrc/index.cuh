@@ -42,6 +42,8 @@ struct QueryTile {
       cursor, cand, bpref, pd2, ppos, tseg, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   int64_t cand_cap = 0;
   int pop_cap = 0;
+  int64_t* flags_h = nullptr;   // pinned copy of flags[0..3] (async read-back)
+  void release();
 };
 
 struct BuildScratch {
@@ -65,7 +67,9 @@ struct taco_index {
   bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,
        has_cells = false, has_gsize = false;
   std::vector<cudaStream_t> half_streams;
-  taco::QueryTile qt;
+  taco::QueryTile qt, qt2;      // two query tiles: the batch loop pipelines them on two streams
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<taco::BuildScratch> bs;
 };
 

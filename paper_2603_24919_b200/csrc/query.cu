@@ -1002,13 +1002,13 @@ __device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint
 // widened values is unchanged.
 template <typename T> struct RowFmt;
 template <> struct RowFmt<float> {    // 64 dims (256 B) per unit, 16 lanes per row segment
-  static constexpr int UD = 64, LPR = 16, PITCH = 272, WARPS = 12;
+  static constexpr int UD = 64, LPR = 16, PITCH = 272, WARPS = 12, CTAS = 1;
 };
 template <> struct RowFmt<__half> {   // 128 dims (256 B) per unit
-  static constexpr int UD = 128, LPR = 16, PITCH = 272, WARPS = 11;
+  static constexpr int UD = 128, LPR = 16, PITCH = 272, WARPS = 11, CTAS = 1;
 };
 template <> struct RowFmt<uint8_t> {  // 128 dims (128 B) per unit, 8 lanes per row segment
-  static constexpr int UD = 128, LPR = 8, PITCH = 144, WARPS = 20;
+  static constexpr int UD = 128, LPR = 8, PITCH = 144, WARPS = 20, CTAS = 1;
 };
 constexpr int AST = 2;                 // stages per warp (the id lookahead assumes 2)
 template <typename T>
@@ -1058,7 +1058,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <typename T>
-__global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, 1) k_rerank_async(
+__global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rerank_async(
     const T* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
     const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
     uint32_t* __restrict__ pid) {
@@ -1410,8 +1410,7 @@ static int64_t super_tile(const taco_index* idx, int cap) {
   return std::max<int64_t>(64, std::min<int64_t>(Q, kSuperTile));
 }
 
-static int ensure_front(taco_index* idx, int64_t QS, int k) {
-  QueryTile& t = idx->qt;
+static int ensure_front(taco_index* idx, QueryTile& t, int64_t QS, int k) {
   if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
   const size_t QN = (size_t)QS * idx->n_sub;
   TACO_TRY(t.Q.ensure(sizeof(float) * (size_t)QS * idx->d));
@@ -1422,6 +1421,7 @@ static int ensure_front(taco_index* idx, int64_t QS, int k) {
   TACO_TRY(t.npop.ensure(sizeof(int32_t) * QN));
   TACO_TRY(t.ret.ensure(sizeof(int64_t) * QN));
   TACO_TRY(t.flags.ensure(sizeof(int64_t) * 8));
+  if (!t.flags_h) TACO_CHECK_CUDA(cudaMallocHost(&t.flags_h, sizeof(int64_t) * 4));
   TACO_TRY(t.lvl.ensure(sizeof(int32_t) * QS));
   TACO_TRY(t.cnum.ensure(sizeof(int64_t) * QS));
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;   // candidate segments per query
@@ -1440,8 +1440,7 @@ static int ensure_front(taco_index* idx, int64_t QS, int k) {
   return TACO_OK;
 }
 
-static int ensure_cand(taco_index* idx, int64_t want) {
-  QueryTile& t = idx->qt;
+static int ensure_cand(QueryTile& t, int64_t want) {
   if (want > t.cand_cap) {
     TACO_TRY(t.cand.ensure(sizeof(uint32_t) * (size_t)want));
     t.cand_cap = want;
@@ -1466,8 +1465,8 @@ static int64_t retrieval_target(double alpha, int64_t n) {
 }
 
 // transform + centroid ranks + traversal for QS queries resident in t.Q
-static int stage_front(taco_index* idx, int64_t QS, double alpha, cudaStream_t st, double* keys_out) {
-  QueryTile& t = idx->qt;
+static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, cudaStream_t st,
+                       double* keys_out) {
   const int kp = idx->kp;
   {
     ProfScope ps(K_TRANSFORM, st);
@@ -1526,8 +1525,7 @@ static int set_count_attrs(taco_index*) {
 }
 
 // global mode, sweep 1: level histograms of every (chunk, query) -> t.hist
-static int global_count(taco_index* idx, int64_t QS, cudaStream_t st) {
-  QueryTile& t = idx->qt;
+static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
   TACO_TRY(set_count_attrs(idx));
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
@@ -1548,8 +1546,8 @@ static int global_count(taco_index* idx, int64_t QS, cudaStream_t st) {
 }
 
 // global mode: Alg. 5 on `ghist`, then sweep 2 recounts and compacts
-static int global_select(taco_index* idx, int64_t QS, const int64_t* ghist, double beta, cudaStream_t st) {
-  QueryTile& t = idx->qt;
+static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_t* ghist, double beta,
+                         cudaStream_t st) {
   const double budget = beta * (double)idx->n_global;   // engine.py:240
   {
     ProfScope ps(K_SELECT, st);
@@ -1572,8 +1570,7 @@ static int global_select(taco_index* idx, int64_t QS, const int64_t* ghist, doub
   return TACO_OK;
 }
 
-static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t st) {
-  QueryTile& t = idx->qt;
+static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta, cudaStream_t st) {
   TACO_TRY(set_count_attrs(idx));
   const double budget = beta * (double)idx->n_global;
   cudaLaunchConfig_t cfg = {};
@@ -1606,8 +1603,8 @@ static int cluster_count(taco_index* idx, int64_t QS, double beta, cudaStream_t 
 // candidates in one id chunk are re-ranked before the next chunk, so the
 // rows they share (each row is a candidate of ~beta*alpha-proportional many
 // queries of a batch) are read from HBM about once and then served by L2.
-static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t fl[4]) {
-  QueryTile& t = idx->qt;
+// launches the plans and an async copy of flags[0..3] into t.flags_h (read after a stream sync)
+static int plan_async(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   {
     ProfScope ps(K_PLAN, st);
@@ -1621,8 +1618,14 @@ static int plan_and_read(taco_index* idx, int64_t QS, cudaStream_t st, int64_t f
                                                   t.flags.as<int64_t>());
     TACO_LAUNCHED();
   }
-  TACO_CHECK_CUDA(cudaMemcpyAsync(fl, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  return TACO_OK;
+}
+
+static int plan_and_read(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st, int64_t fl[4]) {
+  TACO_TRY(plan_async(idx, t, QS, st));
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < 4; ++i) fl[i] = t.flags_h[i];
   return TACO_OK;
 }
 
@@ -1646,7 +1649,7 @@ static int launch_rerank_async(const void* X, int d, const float* Qf, const int4
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_async<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t grid = std::min<int64_t>(ceil_div(ntiles, WARPS), (int64_t)num_sms());
+  const int64_t grid = std::min<int64_t>(ceil_div(ntiles, WARPS), (int64_t)num_sms() * RowFmt<T>::CTAS);
   k_rerank_async<T><<<(unsigned)grid, 32 * WARPS, smem, st>>>(static_cast<const T*>(X), d, Qf, desc, cand, ntiles,
                                                               kk, pkey, pid);
   return TACO_OK;
@@ -1694,8 +1697,7 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
   return TACO_OK;
 }
 
-static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
-  QueryTile& t = idx->qt;
+static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
   return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
@@ -1703,9 +1705,8 @@ static int rerank_stage(taco_index* idx, int64_t QS, int k, int64_t ntiles, cuda
                      t.pd2, t.ppos, t.tseg, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
 }
 
-static void prof_stats(taco_index* idx, int64_t QS, int64_t total) {
+static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total) {
   if (!g_prof.on) return;
-  QueryTile& t = idx->qt;
   std::vector<int64_t> r((size_t)QS * idx->n_sub);
   std::vector<int32_t> np((size_t)QS * idx->n_sub);
   cudaMemcpy(r.data(), t.ret.p, 8 * r.size(), cudaMemcpyDeviceToHost);
@@ -1718,38 +1719,53 @@ static void prof_stats(taco_index* idx, int64_t QS, int64_t total) {
   g_prof.bytes_scores += idx->cluster_mode ? 0 : QS * idx->nchunks * idx->chunk;
 }
 
-// Full single-GPU pipeline for QS queries already in t.Q -> t.tk_d2 / t.tk_ids (+ cnum, lvl).
-static int run_super_tile(taco_index* idx, int64_t QS, double alpha, double beta, int k, cudaStream_t st) {
-  QueryTile& t = idx->qt;
+// Front half of a tile (queries already in t.Q): transform, ranks, traversal,
+// counting, Alg. 5, plans; flags read back asynchronously.
+static int tile_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, double beta, cudaStream_t st) {
   if (t.cand_cap == 0) {
     const int64_t est = QS * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n_global)) + (1 << 20);
-    TACO_TRY(ensure_cand(idx, std::min<int64_t>(est, (int64_t)1 << 31)));
+    TACO_TRY(ensure_cand(t, std::min<int64_t>(est, (int64_t)1 << 31)));
   }
+  TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
+  TACO_TRY(stage_front(idx, t, QS, alpha, st, nullptr));
+  if (idx->cluster_mode) {
+    TACO_TRY(cluster_count(idx, t, QS, beta, st));
+  } else {
+    TACO_TRY(global_count(idx, t, QS, st));
+    TACO_TRY(global_select(idx, t, QS, t.hist.as<int64_t>(), beta, st));
+  }
+  return plan_async(idx, t, QS, st);
+}
+
+// Back half, after tile_front's stream work: re-run the front with larger
+// scratch if a traversal or the candidate buffer overflowed, then re-rank.
+static int tile_back(taco_index* idx, QueryTile& t, int64_t QS, double alpha, double beta, int k, cudaStream_t st) {
   for (int attempt = 0; attempt < 4; ++attempt) {
-    TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
-    TACO_TRY(stage_front(idx, QS, alpha, st, nullptr));
-    if (idx->cluster_mode) {
-      TACO_TRY(cluster_count(idx, QS, beta, st));
-    } else {
-      TACO_TRY(global_count(idx, QS, st));
-      TACO_TRY(global_select(idx, QS, t.hist.as<int64_t>(), beta, st));
-    }
-    int64_t fl[4];
-    TACO_TRY(plan_and_read(idx, QS, st, fl));
+    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+    const int64_t* fl = t.flags_h;
     if (fl[0] > t.pop_cap) {           // a traversal popped more cells than stored
       t.pop_cap = idx->K;
       TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)QS * idx->n_sub * t.pop_cap));
+      TACO_TRY(tile_front(idx, t, QS, alpha, beta, st));
       continue;
     }
     if (fl[1]) {                       // candidate buffer too small: grow to what was asked
-      TACO_TRY(ensure_cand(idx, fl[3] + fl[3] / 4 + 1024));
+      TACO_TRY(ensure_cand(t, fl[3] + fl[3] / 4 + 1024));
+      TACO_TRY(tile_front(idx, t, QS, alpha, beta, st));
       continue;
     }
-    prof_stats(idx, QS, fl[3]);
-    return rerank_stage(idx, QS, k, fl[2], st);
+    prof_stats(idx, t, QS, fl[3]);
+    return rerank_stage(idx, t, QS, k, fl[2], st);
   }
   TACO_FAIL(TACO_ERR_CUDA, "query scratch did not converge");
 }
+
+// Batches of >= 2 * kPipeMin queries run as tiles alternating between two
+// buffers and two streams: tile i+1's front (transform .. count, issued
+// before tile i's flags are read) overlaps tile i's re-rank on the other
+// stream, and the latency-bound front kernels (ranks, traversal) overlap
+// the other tile's counting.
+constexpr int64_t kPipeMin = 2048;
 
 static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, int64_t nq, double alpha,
                             double beta, int k, int32_t* ids_o, float* dists_o, int64_t* cnum_o,
@@ -1758,27 +1774,63 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
   if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "base vectors are not resident");
   if (!(beta > 0.0 && beta < 1.0)) TACO_FAIL(TACO_ERR_PARAMETER, "re-rank ratio %g outside (0, 1)", beta);
   if (nq == 0) return TACO_OK;
-  QueryTile& t = idx->qt;
-  if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
-  const int64_t QSmax = std::min<int64_t>(nq, super_tile(idx, t.pop_cap));
-  TACO_TRY(ensure_front(idx, QSmax, k));
+  QueryTile* tiles[2] = {&idx->qt, &idx->qt2};
+  for (QueryTile* t : tiles)
+    if (t->pop_cap == 0) t->pop_cap = std::min(idx->K, 1024);
+  const int64_t QSmax = std::min<int64_t>(nq, super_tile(idx, idx->qt.pop_cap));
+  static int ptiles = -1;   // tiles a pipelined batch is cut into (TACO_PIPE_TILES, default 2; 1 = off)
+  if (ptiles < 0) {
+    const char* e = getenv("TACO_PIPE_TILES");
+    ptiles = e ? std::max(1, atoi(e)) : 2;
+  }
+  const bool pipe = ptiles > 1 && nq >= 2 * kPipeMin;
+  int64_t QT = QSmax;
+  if (pipe) QT = std::min<int64_t>(QSmax, std::max<int64_t>(kPipeMin, ceil_div(nq, ptiles)));
+  const int64_t ntile = ceil_div(nq, QT);
+  cudaStream_t sts[2] = {st, st};
+  if (pipe) {
+    if (!idx->stream2) {
+      TACO_CHECK_CUDA(cudaStreamCreateWithFlags(&idx->stream2, cudaStreamNonBlocking));
+      TACO_CHECK_CUDA(cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming));
+      TACO_CHECK_CUDA(cudaEventCreateWithFlags(&idx->ev_join, cudaEventDisableTiming));
+    }
+    sts[1] = idx->stream2;
+    TACO_CHECK_CUDA(cudaEventRecord(idx->ev_fork, st));             // stream 2 starts after the caller's work
+    TACO_CHECK_CUDA(cudaStreamWaitEvent(idx->stream2, idx->ev_fork, 0));
+  }
+  for (int b = 0; b < (pipe ? 2 : 1); ++b) TACO_TRY(ensure_front(idx, *tiles[b], QT, k));
   const cudaMemcpyKind kin = src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind kout = dst_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  for (int64_t q0 = 0; q0 < nq; q0 += QSmax) {
-    const int64_t QS = std::min<int64_t>(QSmax, nq - q0);
-    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_src + (size_t)q0 * idx->d, sizeof(float) * (size_t)QS * idx->d, kin, st));
-    TACO_TRY(run_super_tile(idx, QS, alpha, beta, k, st));
+  auto front = [&](int64_t i) -> int {
+    QueryTile& t = *tiles[pipe ? i & 1 : 0];
+    cudaStream_t s = sts[pipe ? i & 1 : 0];
+    const int64_t q0 = i * QT, QS = std::min<int64_t>(QT, nq - q0);
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_src + (size_t)q0 * idx->d, sizeof(float) * (size_t)QS * idx->d, kin, s));
+    return tile_front(idx, t, QS, alpha, beta, s);
+  };
+  TACO_TRY(front(0));
+  for (int64_t i = 0; i < ntile; ++i) {
+    if (pipe && i + 1 < ntile) TACO_TRY(front(i + 1));
+    QueryTile& t = *tiles[pipe ? i & 1 : 0];
+    cudaStream_t s = sts[pipe ? i & 1 : 0];
+    const int64_t q0 = i * QT, QS = std::min<int64_t>(QT, nq - q0);
+    TACO_TRY(tile_back(idx, t, QS, alpha, beta, k, s));
     const int64_t tot = QS * k;
     {
-      ProfScope ps(K_FINAL, st);
-      k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), tot,
-                                                               t.out_ids.as<int32_t>(), t.out_d.as<float>());
+      ProfScope ps(K_FINAL, s);
+      k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), tot,
+                                                              t.out_ids.as<int32_t>(), t.out_d.as<float>());
       TACO_LAUNCHED();
     }
-    TACO_CHECK_CUDA(cudaMemcpyAsync(ids_o + q0 * k, t.out_ids.p, sizeof(int32_t) * tot, kout, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(dists_o + q0 * k, t.out_d.p, sizeof(float) * tot, kout, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(cnum_o + q0, t.cnum.p, sizeof(int64_t) * QS, kout, st));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(lvl_o + q0, t.lvl.p, sizeof(int32_t) * QS, kout, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(ids_o + q0 * k, t.out_ids.p, sizeof(int32_t) * tot, kout, s));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(dists_o + q0 * k, t.out_d.p, sizeof(float) * tot, kout, s));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(cnum_o + q0, t.cnum.p, sizeof(int64_t) * QS, kout, s));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(lvl_o + q0, t.lvl.p, sizeof(int32_t) * QS, kout, s));
+    if (!pipe && i + 1 < ntile) TACO_TRY(front(i + 1));
+  }
+  if (pipe) {   // the caller's stream resumes after both tiles' work
+    TACO_CHECK_CUDA(cudaEventRecord(idx->ev_join, idx->stream2));
+    TACO_CHECK_CUDA(cudaStreamWaitEvent(st, idx->ev_join, 0));
   }
   if (dst_host) TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   return TACO_OK;
@@ -1822,11 +1874,11 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
   if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
   const int64_t Qt = super_tile(idx, t.pop_cap);
   if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)nq, (long long)Qt);
-  TACO_TRY(ensure_front(idx, Qt, 1));
+  TACO_TRY(ensure_front(idx, t, Qt, 1));
   TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
   for (int attempt = 0; attempt < 2; ++attempt) {
     TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
-    TACO_TRY(stage_front(idx, nq, alpha, st, nullptr));
+    TACO_TRY(stage_front(idx, t, nq, alpha, st, nullptr));
     int64_t f0 = 0;
     TACO_CHECK_CUDA(cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st));
     TACO_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1834,7 +1886,7 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
     t.pop_cap = idx->K;
     TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)Qt * idx->n_sub * t.pop_cap));
   }
-  TACO_TRY(global_count(idx, nq, st));
+  TACO_TRY(global_count(idx, t, nq, st));
   TACO_CHECK_CUDA(cudaMemcpyAsync(hist_d, t.hist.p, sizeof(int64_t) * (size_t)nq * (idx->n_sub + 1),
                                   cudaMemcpyDeviceToDevice, st));
   return TACO_OK;
@@ -1853,22 +1905,22 @@ int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d
   if (t.pop_cap == 0) t.pop_cap = std::min(idx->K, 1024);
   const int64_t Qt = super_tile(idx, t.pop_cap);
   if (nq > Qt) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)nq, (long long)Qt);
-  TACO_TRY(ensure_front(idx, Qt, k));
+  TACO_TRY(ensure_front(idx, t, Qt, k));
   if (t.cand_cap == 0)
-    TACO_TRY(ensure_cand(idx, Qt * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n)) + (1 << 20)));
+    TACO_TRY(ensure_cand(t, Qt * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n)) + (1 << 20)));
   for (int attempt = 0; attempt < 3; ++attempt) {
     int64_t zero = 0;
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 1, &zero, 8, cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 3, &zero, 8, cudaMemcpyHostToDevice, st));
-    TACO_TRY(global_select(idx, nq, ghist_d, beta, st));
+    TACO_TRY(global_select(idx, t, nq, ghist_d, beta, st));
     int64_t fl[4];
-    TACO_TRY(plan_and_read(idx, nq, st, fl));
+    TACO_TRY(plan_and_read(idx, t, nq, st, fl));
     if (fl[1]) {
-      TACO_TRY(ensure_cand(idx, fl[3] + fl[3] / 4 + 1024));
+      TACO_TRY(ensure_cand(t, fl[3] + fl[3] / 4 + 1024));
       continue;
     }
-    prof_stats(idx, nq, fl[3]);
-    TACO_TRY(rerank_stage(idx, nq, k, fl[2], st));
+    prof_stats(idx, t, nq, fl[3]);
+    TACO_TRY(rerank_stage(idx, t, nq, k, fl[2], st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(topk_d2_d, t.tk_d2.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(topk_ids_d, t.tk_ids.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(cand_num_d, t.cnum.p, sizeof(int64_t) * nq, cudaMemcpyDeviceToDevice, st));
@@ -1894,7 +1946,7 @@ int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* 
   TACO_TRY(check_query_ready(idx, alpha, 1));
   QueryTile& t = idx->qt;
   cudaStream_t st = idx->stream;
-  TACO_TRY(ensure_front(idx, 1, 1));
+  TACO_TRY(ensure_front(idx, t, 1, 1));
   DevBuf sc, part, hist;
   TACO_TRY(sc.ensure((size_t)idx->nchunks * idx->chunk));
   TACO_TRY(part.ensure(sizeof(int32_t) * idx->nchunks * (idx->n_sub + 1)));
@@ -1905,7 +1957,7 @@ int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* 
     }
     for (int attempt = 0; attempt < 2; ++attempt) {
       cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st);
-      if ((rc = stage_front(idx, 1, alpha, st, nullptr))) break;
+      if ((rc = stage_front(idx, t, 1, alpha, st, nullptr))) break;
       int64_t f0 = 0;
       cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
@@ -1936,11 +1988,11 @@ int taco_activation_trace(taco_index* idx, const float* q_h, int32_t j, double a
   cudaStream_t st = idx->stream;
   const int saved = t.pop_cap;
   t.pop_cap = idx->K;
-  TACO_TRY(ensure_front(idx, 1, 1));
+  TACO_TRY(ensure_front(idx, t, 1, 1));
   DevBuf keys;
   TACO_TRY(keys.ensure(sizeof(double) * (size_t)idx->n_sub * idx->K));
   TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, q_h, sizeof(float) * idx->d, cudaMemcpyHostToDevice, st));
-  int rc = stage_front(idx, 1, alpha, st, keys.as<double>());
+  int rc = stage_front(idx, t, 1, alpha, st, keys.as<double>());
   t.pop_cap = saved;
   if (rc != TACO_OK) { keys.release(); return rc; }
   int32_t np = 0;
