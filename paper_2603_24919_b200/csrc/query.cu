@@ -1783,7 +1783,8 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
     const char* e = getenv("TACO_PIPE_TILES");
     ptiles = e ? std::max(1, atoi(e)) : 2;
   }
-  const bool pipe = ptiles > 1 && nq >= 2 * kPipeMin;
+  // profiled passes run unpipelined so per-kernel event times do not overlap
+  const bool pipe = ptiles > 1 && nq >= 2 * kPipeMin && !g_prof.on;
   int64_t QT = QSmax;
   if (pipe) QT = std::min<int64_t>(QSmax, std::max<int64_t>(kPipeMin, ceil_div(nq, ptiles)));
   const int64_t ntile = ceil_div(nq, QT);
