@@ -1061,7 +1061,7 @@ template <typename T>
 __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rerank_async(
     const T* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
     const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
-    uint32_t* __restrict__ pid) {
+    uint32_t* __restrict__ pid, unsigned long long* __restrict__ qthr) {
   using F = RowFmt<T>;
   constexpr int UD = F::UD, LPR = F::LPR, RPI = 32 / F::LPR;
   extern __shared__ __align__(128) unsigned char asm_[];
@@ -1159,10 +1159,33 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
       v = v >= 0.0 ? v : 0.0;
       unsigned long long key = lane < tcomp.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
       uint32_t id = tcomp.cid;
-      warp_sort_pairs(key, id);
-      if (lane < kk) {
-        pkey[(int64_t)tcomp.out * kk + lane] = key;
-        pid[(int64_t)tcomp.out * kk + lane] = id;
+      // qthr[q] bounds the query's final kk-th best from above (some earlier tile's kk-th
+      // best), so rows above it cannot make the top-kk: when at most kk rows survive they
+      // are written unsorted (k_topk selects), else the tile is sorted and tightens qthr.
+      const unsigned long long thr = __ldcg(qthr + tcomp.q);
+      const bool keep = key != ~0ull && key <= thr;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      const int ns = __popc(bal);
+      unsigned long long* ok = pkey + (int64_t)tcomp.out * kk;
+      uint32_t* oi = pid + (int64_t)tcomp.out * kk;
+      if (ns <= kk) {
+        if (keep) {
+          const int slot = __popc(bal & ((1u << lane) - 1u));
+          ok[slot] = key;
+          oi[slot] = id;
+        }
+        if (lane >= ns && lane < kk) {
+          ok[lane] = ~0ull;
+          oi[lane] = 0xFFFFFFFFu;
+        }
+      } else {
+        warp_sort_pairs(key, id);
+        if (lane < kk) {
+          ok[lane] = key;
+          oi[lane] = id;
+        }
+        const unsigned long long kth = __shfl_sync(0xffffffffu, key, kk - 1);
+        if (lane == 0 && kth != ~0ull) atomicMin(qthr + tcomp.q, kth);
       }
       a0 = 0.0;
       a1 = 0.0;
@@ -1641,7 +1664,8 @@ static int num_sms() {
 
 template <typename T>
 static int launch_rerank_async(const void* X, int d, const float* Qf, const int4* desc, const uint32_t* cand,
-                               int64_t ntiles, int kk, unsigned long long* pkey, uint32_t* pid, cudaStream_t st) {
+                               int64_t ntiles, int kk, unsigned long long* pkey, uint32_t* pid,
+                               unsigned long long* qthr, cudaStream_t st) {
   constexpr int WARPS = RowFmt<T>::WARPS;
   const size_t smem = sizeof(AWarpSmem<T>) * WARPS;
   static bool attr = false;
@@ -1651,7 +1675,7 @@ static int launch_rerank_async(const void* X, int d, const float* Qf, const int4
   }
   const int64_t grid = std::min<int64_t>(ceil_div(ntiles, WARPS), (int64_t)num_sms() * RowFmt<T>::CTAS);
   k_rerank_async<T><<<(unsigned)grid, 32 * WARPS, smem, st>>>(static_cast<const T*>(X), d, Qf, desc, cand, ntiles,
-                                                              kk, pkey, pid);
+                                                              kk, pkey, pid, qthr);
   return TACO_OK;
 }
 
@@ -1659,9 +1683,12 @@ static int launch_rerank_async(const void* X, int d, const float* Qf, const int4
 static int rerank_core(const float* X, const void* Xn, int fmt, int d, const float* Qf, int64_t QS, int64_t S,
                        const int64_t* tstart,
                        const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
-                       int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, double* out_d2,
+                       int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, DevBuf& qthrb, double* out_d2,
                        int64_t* out_ids, cudaStream_t st) {
   const int kk = std::min(k, GR);
+  TACO_TRY(qthrb.ensure(sizeof(unsigned long long) * (size_t)QS));
+  TACO_CHECK_CUDA(cudaMemsetAsync(qthrb.p, 0xFF, sizeof(unsigned long long) * (size_t)QS, st));
+  unsigned long long* qthr = qthrb.as<unsigned long long>();
   TACO_TRY(pkey.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
   TACO_TRY(pid.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(ntiles, 1) * kk));
   TACO_TRY(tsegb.ensure(sizeof(int4) * (size_t)std::max<int64_t>(ntiles, 1)));
@@ -1676,11 +1703,11 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
     ProfScope ps(K_RERANK, st);
     unsigned long long* pk = pkey.as<unsigned long long>();
     if (fmt == TACO_ROWS_U8) {
-      TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
+      TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
     } else if (fmt == TACO_ROWS_F16) {
-      TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
+      TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
     } else if (d % 4 == 0) {
-      TACO_TRY(launch_rerank_async<float>(X, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), st));
+      TACO_TRY(launch_rerank_async<float>(X, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
     } else {
       k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, desc,
                                                                    cand, ntiles, kk, pkey.as<unsigned long long>(),
@@ -1702,7 +1729,7 @@ static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_
   return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
-                     t.pd2, t.ppos, t.tseg, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
+                     t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
 }
 
 static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total) {
@@ -2089,7 +2116,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
   for (int64_t i = 0; i < m; ++i)
     std::copy(X_h + (size_t)c32[i] * d, X_h + (size_t)c32[i] * d + d, rowsv.begin() + (size_t)i * d);
   const int64_t ntiles = ceil_div(m, GR);
-  DevBuf Xd, Qd, sb, sc, tp, ps, cd, pk, pi, ts, tkd, tki, fl;
+  DevBuf Xd, Qd, sb, sc, tp, ps, cd, pk, pi, ts, qh, tkd, tki, fl;
   int rc = TACO_OK;
   do {
     if ((rc = Xd.ensure(sizeof(float) * rowsv.size())) || (rc = Qd.ensure(sizeof(float) * d)) ||
@@ -2113,7 +2140,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     if ((rc = rerank_core(Xd.as<float>(), nullptr, TACO_ROWS_F32, d, Qd.as<float>(), 1, 1, tp.as<int64_t>(),
                           tp.as<int64_t>(),
                           sb.as<int64_t>(),
-                          sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, ts, tkd.as<double>(),
+                          sc.as<int64_t>(), cd.as<uint32_t>(), ntiles, k, 0, pk, pi, ts, qh, tkd.as<double>(),
                           tki.as<int64_t>(), nullptr)))
       break;
     std::vector<double> td(k);
@@ -2130,7 +2157,7 @@ int taco_rerank(int device, const float* X_h, int64_t n, int32_t d, const float*
     }
   } while (0);
   Xd.release(); Qd.release(); sb.release(); sc.release(); tp.release(); cd.release(); pk.release();
-  pi.release(); ts.release(); ps.release(); tkd.release(); tki.release(); fl.release();
+  pi.release(); ts.release(); qh.release(); ps.release(); tkd.release(); tki.release(); fl.release();
   return rc;
 }
 
