@@ -301,6 +301,9 @@ def run_ours(args):
 
     # one profiled pass: per-kernel CUDA-event times on the launching stream
     nat.profile_enable(True)
+    device_step()   # profiled passes run as one tile: let its scratch settle first
+    torch.cuda.synchronize()
+    nat.profile_read(reset=True)
     flush.zero_()
     torch.cuda.synchronize()
     device_step()
@@ -323,8 +326,8 @@ def run_ours(args):
                         "candidate ids; the 4 B/point-per-subspace CSR (32 MB here) stays L2-resident, "
                         "so the kernel is bound by shared-memory atomics and instruction issue, not HBM"),
             "k_rerank": ("algorithmic bytes = stored candidate rows + ids; chunk-major order keeps "
-                         "the rows L2-resident (HBM reads ~1.4 GB per 10k batch), the bound is the "
-                         "fp64 pipe (3 DP ops per candidate-dimension)"),
+                         "the rows L2-resident; u8 rows with u8-exact queries use the exact DP4A "
+                         "integer path, otherwise the fp64 pipe bounds it"),
         }
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "note": notes.get(dom),

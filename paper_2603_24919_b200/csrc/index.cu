@@ -34,10 +34,10 @@ int DevBuf::ensure(size_t want) {
 }
 
 void QueryTile::release() {
-  DevBuf* qb[] = {&Q, &qt, &sd, &sl, &pops, &npop, &ret, &flags, &scores, &part, &hist, &lvl, &cnum, &clocal,
-                  &coff, &qbase, &cursor, &cand, &bpref, &pd2, &ppos, &tseg, &qthr, &ppref, &psum, &tk_d2, &tk_ids,
+  DevBuf* all[] = {&Q, &qt, &sd, &sl, &pops, &npop, &ret, &flags, &scores, &part, &hist, &lvl, &cnum, &clocal,
+                  &coff, &qbase, &cursor, &cand, &bpref, &pd2, &ppos, &tseg, &qthr, &qb, &qsq, &qok, &ppref, &psum, &tk_d2, &tk_ids,
                   &out_ids, &out_d};
-  for (auto* b : qb) b->release();
+  for (auto* b : all) b->release();
   if (flags_h) cudaFreeHost(flags_h);
   flags_h = nullptr;
   cand_cap = 0;
@@ -210,7 +210,7 @@ int taco_index_destroy(taco_index* idx) {
   if (!idx) return TACO_OK;
   cudaSetDevice(idx->device);
   cudaStreamSynchronize(idx->stream);
-  DevBuf* bufs[] = {&idx->X, &idx->Xn, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
+  DevBuf* bufs[] = {&idx->X, &idx->Xn, &idx->Xsq, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
                     &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
   for (auto* b : bufs) b->release();
   idx->qt.release();
@@ -249,6 +249,14 @@ __global__ void k_rows_u8(const float* __restrict__ X, size_t N, uint8_t* __rest
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
     out[i] = (uint8_t)(uint32_t)X[i];
 }
+__global__ void k_rows_sq(const uint8_t* __restrict__ Xn, int64_t n, int d, int32_t* __restrict__ sq) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(Xn + i * d);
+    uint32_t acc = 0;
+    for (int w = 0; w < d / 4; ++w) acc = __dp4a(r[w], r[w], acc);
+    sq[i] = (int32_t)acc;
+  }
+}
 __global__ void k_rows_f16(const float* __restrict__ X, size_t N, __half* __restrict__ out) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
     out[i] = __float2half_rn(X[i]);
@@ -258,6 +266,7 @@ __global__ void k_rows_f16(const float* __restrict__ X, size_t N, __half* __rest
 static int narrow_rows(taco_index* idx) {
   idx->xfmt = TACO_ROWS_F32;
   idx->Xn.release();
+  idx->Xsq.release();
   const char* env = getenv("TACO_ROWS");
   if (env && strcmp(env, "f32") == 0) return TACO_OK;
   const size_t N = (size_t)idx->n * idx->d;
@@ -275,7 +284,9 @@ static int narrow_rows(taco_index* idx) {
   if (res[0] && idx->d % 16 == 0) {
     TACO_TRY(idx->Xn.ensure(N));
     k_rows_u8<<<1184, 256, 0, idx->stream>>>(idx->X.as<float>(), N, idx->Xn.as<uint8_t>());
-    count_launch();
+    TACO_TRY(idx->Xsq.ensure(sizeof(int32_t) * (size_t)idx->n));
+    k_rows_sq<<<1184, 256, 0, idx->stream>>>(idx->Xn.as<uint8_t>(), idx->n, idx->d, idx->Xsq.as<int32_t>());
+    count_launch(2);
     idx->xfmt = TACO_ROWS_U8;
   } else if (res[1] && idx->d % 8 == 0) {
     TACO_TRY(idx->Xn.ensure(2 * N));

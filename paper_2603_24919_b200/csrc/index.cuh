@@ -39,7 +39,7 @@ struct DevBuf {
 
 struct QueryTile {
   DevBuf Q, qt, sd, sl, pops, npop, ret, flags, scores, part, hist, lvl, cnum, clocal, coff, qbase,
-      cursor, cand, bpref, pd2, ppos, tseg, qthr, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
+      cursor, cand, bpref, pd2, ppos, tseg, qthr, qb, qsq, qok, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   int64_t cand_cap = 0;
   int pop_cap = 0;
   int64_t* flags_h = nullptr;   // pinned copy of flags[0..3] (async read-back)
@@ -63,6 +63,7 @@ struct taco_index {
   int d = 0, n_sub = 0, s = 0, K = 0, kp = 0, m1 = 0, m2 = 0, D = 0, iters = 0;
   taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
   taco::DevBuf Xn;            // lossless narrow copy of X for the rerank (xfmt != TACO_ROWS_F32)
+  taco::DevBuf Xsq;           // u8 rows: int32 sum of squares per row (integer rerank path)
   int xfmt = 0;               // TACO_ROWS_*
   bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,
        has_cells = false, has_gsize = false;

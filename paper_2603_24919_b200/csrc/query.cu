@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "index.cuh"
@@ -974,6 +975,8 @@ struct TileRef {
   int m;
   int out;        // output tile (query-major)
   uint32_t cid;   // this lane's candidate id (valid if lane < m)
+  int iq = 0;     // integer path: u8 rows and a u8-exact query
+  int32_t xs = 0; // integer path: this lane's row sum of squares
 };
 
 __device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint32_t* __restrict__ cand) {
@@ -1061,8 +1064,10 @@ template <typename T>
 __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rerank_async(
     const T* __restrict__ X, int d, const float* __restrict__ Qf, const int4* __restrict__ desc,
     const uint32_t* __restrict__ cand, int64_t ntiles, int kk, unsigned long long* __restrict__ pkey,
-    uint32_t* __restrict__ pid, unsigned long long* __restrict__ qthr) {
+    uint32_t* __restrict__ pid, unsigned long long* __restrict__ qthr, const uint8_t* __restrict__ Qb,
+    const uint8_t* __restrict__ qok, const int32_t* __restrict__ qsq, const int32_t* __restrict__ xsq) {
   using F = RowFmt<T>;
+  constexpr bool U8 = std::is_same<T, uint8_t>::value;
   constexpr int UD = F::UD, LPR = F::LPR, RPI = 32 / F::LPR;
   extern __shared__ __align__(128) unsigned char asm_[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1079,8 +1084,17 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
   auto row_of = [&](const TileRef& r) {
     return reinterpret_cast<const uint8_t*>(X + (size_t)(lane < r.m ? r.cid : 0u) * d);
   };
-  TileRef tcur = tile_ref(dsc(0), lane, cand);           // tile being issued
-  TileRef tnext = tile_ref(dsc(1), lane, cand);          // its successor (ids in flight)
+  // integer path (U8 rows, qok[q]): d2 = sum x^2 - 2 sum x q + sum q^2 in exact integers
+  auto ref_of = [&](const int4 dd) {
+    TileRef r = tile_ref(dd, lane, cand);
+    if (U8 && qok) {
+      r.iq = r.m > 0 ? qok[r.q] : 0;
+      r.xs = r.iq && lane < r.m ? __ldg(xsq + r.cid) : 0;
+    }
+    return r;
+  };
+  TileRef tcur = ref_of(dsc(0));                         // tile being issued
+  TileRef tnext = ref_of(dsc(1));                        // its successor (ids in flight)
   int4 dpre = dsc(2);                                    // the one after
   int64_t tcur_i = 0;
   const uint8_t* rp = row_of(tcur);                      // my row of the issued tile
@@ -1093,7 +1107,7 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
       tcur = tnext;
       tcur_i = i;
       rp = row_of(tcur);
-      tnext = tile_ref(dpre, lane, cand);
+      tnext = ref_of(dpre);
       dpre = dsc(i + 2);
     }
     AStage<T>& st = W.st[u % AST];
@@ -1108,13 +1122,19 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
           __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rp), rr));
       if (cl < nch && rr < tcur.m) cp_async16(&st.rows[rr][cl * 16], src + cofs);
     }
-    for (int c = lane; c < len / 4; c += 32) cp_async16(&st.q[c * 4], Qf + (size_t)tcur.q * d + s0 + c * 4);
+    if (U8 && tcur.iq) {   // the query's bytes (len is a multiple of 16 for u8 rows)
+      if (lane < len / 16)
+        cp_async16(reinterpret_cast<uint8_t*>(st.q) + lane * 16, Qb + (size_t)tcur.q * d + s0 + lane * 16);
+    } else {
+      for (int c = lane; c < len / 4; c += 32) cp_async16(&st.q[c * 4], Qf + (size_t)tcur.q * d + s0 + c * 4);
+    }
   };
   for (int64_t u = 0; u < AST - 1; ++u) {
     if (u < U) issue(u);
     cp_async_commit();
   }
   double a0 = 0.0, a1 = 0.0;
+  uint32_t iacc = 0;   // integer path: sum of x * q
   for (int64_t u = 0; u < U; ++u) {
     const int64_t i = u / nsg;
     const int g = (int)(u % nsg);
@@ -1126,11 +1146,23 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
     const AStage<T>& st = W.st[u % AST];
     const int s0 = g * UD;
     const int len = min(UD, d - s0);
+    const bool last = g == nsg - 1;
+    if (U8 && tcomp.iq) {
+      const uint8_t* row = st.rows[lane];
+      const uint8_t* qb = reinterpret_cast<const uint8_t*>(st.q);
+      for (int b = 0; b < len; b += 16) {
+        const uint4 xw = *reinterpret_cast<const uint4*>(row + b);
+        const uint4 qw = *reinterpret_cast<const uint4*>(qb + b);
+        iacc = __dp4a(xw.x, qw.x, iacc);
+        iacc = __dp4a(xw.y, qw.y, iacc);
+        iacc = __dp4a(xw.z, qw.z, iacc);
+        iacc = __dp4a(xw.w, qw.w, iacc);
+      }
+    } else {
     for (int t = lane; t < len; t += 32) W.qd[t] = (double)st.q[t];
     __syncwarp();
     const uint8_t* row = st.rows[lane];
     const double* qv = W.qd;
-    const bool last = g == nsg - 1;
     const int full8 = last ? (len & ~7) : len;
     for (int b = 0; b < full8; b += 8) {
       double xv[8];
@@ -1155,8 +1187,17 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
           a1 = __dadd_rn(__dmul_rn(e1, e1), a1);
         }
       }
-      double v = __dadd_rn(a0, a1);
-      v = v >= 0.0 ? v : 0.0;
+    }
+    }   // fp64 path
+    if (last) {
+      double v;
+      if (U8 && tcomp.iq) {   // every step of the reference's fp64 sum is exact on these integers
+        v = (double)((int64_t)tcomp.xs - 2 * (int64_t)iacc + (int64_t)__ldg(qsq + tcomp.q));
+        iacc = 0;
+      } else {
+        v = __dadd_rn(a0, a1);
+        v = v >= 0.0 ? v : 0.0;
+      }
       unsigned long long key = lane < tcomp.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
       uint32_t id = tcomp.cid;
       // qthr[q] bounds the query's final kk-th best from above (some earlier tile's kk-th
@@ -1662,10 +1703,17 @@ static int num_sms() {
   return g_num_sms;
 }
 
+struct IntRerank {   // integer path inputs (u8 rows only); all null = off
+  const uint8_t* Qb = nullptr;
+  const uint8_t* qok = nullptr;
+  const int32_t* qsq = nullptr;
+  const int32_t* xsq = nullptr;
+};
+
 template <typename T>
 static int launch_rerank_async(const void* X, int d, const float* Qf, const int4* desc, const uint32_t* cand,
                                int64_t ntiles, int kk, unsigned long long* pkey, uint32_t* pid,
-                               unsigned long long* qthr, cudaStream_t st) {
+                               unsigned long long* qthr, const IntRerank& ir, cudaStream_t st) {
   constexpr int WARPS = RowFmt<T>::WARPS;
   const size_t smem = sizeof(AWarpSmem<T>) * WARPS;
   static bool attr = false;
@@ -1675,8 +1723,47 @@ static int launch_rerank_async(const void* X, int d, const float* Qf, const int4
   }
   const int64_t grid = std::min<int64_t>(ceil_div(ntiles, WARPS), (int64_t)num_sms() * RowFmt<T>::CTAS);
   k_rerank_async<T><<<(unsigned)grid, 32 * WARPS, smem, st>>>(static_cast<const T*>(X), d, Qf, desc, cand, ntiles,
-                                                              kk, pkey, pid, qthr);
+                                                              kk, pkey, pid, qthr, ir.Qb, ir.qok, ir.qsq,
+                                                              ir.xsq);
   return TACO_OK;
+}
+
+// Integer re-rank eligibility of each query (u8 rows only): every value an
+// integer in [0, 255] (bit-exact f32 round trip; -0 counts as 0, which gives
+// the same differences).  Then for rows and query in [0, 255] and d <= 4096,
+// each step of the reference's fp64 einsum -- the difference, its square and
+// every partial sum (< 2^31) -- is exact, so the fp64 d2 equals the integer
+// sum x^2 - 2 sum x q + sum q^2, computed with DP4A.
+__global__ void k_q_u8(const float* __restrict__ Q, int64_t nq, int d, uint8_t* __restrict__ Qb,
+                       int32_t* __restrict__ qsq, uint8_t* __restrict__ qok) {
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  bool ok = true;
+  uint32_t sq = 0;
+  for (int t = lane; t < d; t += 32) {
+    const float v = Q[q * d + t];
+    const bool in = v >= 0.0f && v <= 255.0f && v == rintf(v);
+    ok = ok && in;
+    const uint32_t b = in ? (uint32_t)v : 0u;
+    Qb[q * d + t] = (uint8_t)b;
+    sq += b * b;
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) {
+    qsq[q] = (int32_t)sq;
+    qok[q] = ok ? 1 : 0;
+  }
+}
+
+static bool int_rerank_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("TACO_INT_RERANK");
+    on = !(e && e[0] == '0');
+  }
+  return on;
 }
 
 // rows of candidates -> CTA partial top-k -> per-query top-k (t.tk_d2 / t.tk_ids)
@@ -1684,7 +1771,7 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
                        const int64_t* tstart,
                        const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
                        int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, DevBuf& qthrb, double* out_d2,
-                       int64_t* out_ids, cudaStream_t st) {
+                       int64_t* out_ids, cudaStream_t st, const IntRerank& ir = IntRerank()) {
   const int kk = std::min(k, GR);
   TACO_TRY(qthrb.ensure(sizeof(unsigned long long) * (size_t)QS));
   TACO_CHECK_CUDA(cudaMemsetAsync(qthrb.p, 0xFF, sizeof(unsigned long long) * (size_t)QS, st));
@@ -1703,11 +1790,11 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
     ProfScope ps(K_RERANK, st);
     unsigned long long* pk = pkey.as<unsigned long long>();
     if (fmt == TACO_ROWS_U8) {
-      TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
+      TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, ir, st));
     } else if (fmt == TACO_ROWS_F16) {
-      TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
+      TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, ir, st));
     } else if (d % 4 == 0) {
-      TACO_TRY(launch_rerank_async<float>(X, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, st));
+      TACO_TRY(launch_rerank_async<float>(X, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, ir, st));
     } else {
       k_rerank_plain<<<(unsigned)ceil_div(ntiles, 4), 128, 0, st>>>(X, d, Qf, desc,
                                                                    cand, ntiles, kk, pkey.as<unsigned long long>(),
@@ -1726,10 +1813,26 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
 
 static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
   const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
+  IntRerank ir;
+  if (idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled()) {
+    TACO_TRY(t.qb.ensure((size_t)QS * idx->d));
+    TACO_TRY(t.qsq.ensure(sizeof(int32_t) * (size_t)QS));
+    TACO_TRY(t.qok.ensure((size_t)QS));
+    {
+      ProfScope ps(K_PLAN, st);
+      k_q_u8<<<(unsigned)ceil_div(QS * 32, 256), 256, 0, st>>>(t.Q.as<float>(), QS, idx->d, t.qb.as<uint8_t>(),
+                                                                t.qsq.as<int32_t>(), t.qok.as<uint8_t>());
+      TACO_LAUNCHED();
+    }
+    ir.Qb = t.qb.as<uint8_t>();
+    ir.qok = t.qok.as<uint8_t>();
+    ir.qsq = t.qsq.as<int32_t>();
+    ir.xsq = idx->Xsq.as<int32_t>();
+  }
   return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
-                     t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st);
+                     t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st, ir);
 }
 
 static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total) {

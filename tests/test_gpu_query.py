@@ -229,3 +229,25 @@ def test_sc_linear_resident_matches_host():
         r2 = T.rerank(X, Q[qi], cand, 10)
         np.testing.assert_array_equal(r1.ids, r2.ids)
         np.testing.assert_array_equal(r1.dists, r2.dists)
+
+
+@pytest.mark.parametrize("int_queries", [True, False])
+def test_integer_rerank_path(int_queries, monkeypatch):
+    """u8 rows + u8-exact queries take the DP4A integer re-rank (exact by
+    construction); it must agree bit-for-bit with the oracle, and so must the
+    fp64 path on the same rows with non-integer queries."""
+    rng = np.random.default_rng(77)
+    n, d, nq = 5000, 64, 64
+    X = rng.integers(0, 256, (n, d)).astype(np.float32)
+    Q = X[rng.integers(0, n, nq)] + rng.integers(-6, 7, (nq, d))
+    Q = np.clip(Q, 0, 255).astype(np.float32)
+    if not int_queries:
+        Q = (Q + rng.uniform(-0.5, 0.5, Q.shape)).astype(np.float32)
+    Q[:3] = X[:3]   # exact duplicates: d2 == 0 ties broken by id
+    idx = T.build_index(X, T.IndexParams(4, 16, 64, 5, 3))
+    oidx = O.deserialize(T.serialize_index(idx))
+    for a, b, k in [(0.05, 0.01, 10), (0.2, 0.05, 40)]:
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(a, b, k))
+        oi, od, on, ol = O.knn_batch(oidx, X, Q, a, b, k)
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(dists, od)
