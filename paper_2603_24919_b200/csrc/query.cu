@@ -789,7 +789,8 @@ __global__ void k_hist_reduce(const int32_t* __restrict__ part, int64_t nchunks,
 __global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __restrict__ part, int64_t Q,
                          int64_t nchunks, int n_sub, double budget, int64_t* __restrict__ coff,
                          int64_t cand_cap, int64_t* __restrict__ flags, int64_t* __restrict__ sbase,
-                         int64_t* __restrict__ scnt, int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+                         int64_t* __restrict__ scnt, int64_t* __restrict__ cnum, int32_t* __restrict__ lvl,
+                         int64_t* __restrict__ gsb = nullptr, int64_t* __restrict__ gsc = nullptr) {
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (q >= Q) return;
@@ -815,13 +816,22 @@ __global__ void k_select(const int64_t* __restrict__ ghist, const int32_t* __res
     if (c < nchunks) coff[q * nchunks + c] = run + v - cc;
     run += __shfl_sync(0xffffffffu, v, 31);
   }
+  int64_t b = 0;
   if (lane == 0) {
-    const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)run);
+    b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)run);
     if (b + run > cand_cap) flags[1] = 1;
     sbase[q] = b;
     scnt[q] = run;
     cnum[q] = cands;
     lvl[q] = L;
+  }
+  if (gsb) {   // per-(query, chunk) candidate segments: the re-rank's chunk-major plan
+    b = __shfl_sync(0xffffffffu, b, 0);
+    for (int64_t c = lane; c < nchunks; c += 32) {
+      const int64_t o = coff[q * nchunks + c];
+      gsb[q * nchunks + c] = b + o;
+      gsc[q * nchunks + c] = (c + 1 < nchunks ? coff[q * nchunks + c + 1] : run) - o;
+    }
   }
 }
 
@@ -1488,10 +1498,15 @@ static int ensure_front(taco_index* idx, QueryTile& t, int64_t QS, int k) {
   if (!t.flags_h) TACO_CHECK_CUDA(cudaMallocHost(&t.flags_h, sizeof(int64_t) * 4));
   TACO_TRY(t.lvl.ensure(sizeof(int32_t) * QS));
   TACO_TRY(t.cnum.ensure(sizeof(int64_t) * QS));
-  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;   // candidate segments per query
-  TACO_TRY(t.clocal.ensure(sizeof(int64_t) * QS * S));
-  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * QS * S));
+  const int64_t S = idx->nchunks;   // candidate segments per query (re-rank plan)
+  const int64_t SC = idx->cluster_mode ? idx->nchunks : 1;   // count-side segments (clocal / qbase)
+  TACO_TRY(t.clocal.ensure(sizeof(int64_t) * QS * SC));
+  TACO_TRY(t.qbase.ensure(sizeof(int64_t) * QS * SC));
   TACO_TRY(t.bpref.ensure(sizeof(int64_t) * (QS * S + 1)));
+  if (!idx->cluster_mode) {
+    TACO_TRY(t.gsb.ensure(sizeof(int64_t) * QS * S));
+    TACO_TRY(t.gsc.ensure(sizeof(int64_t) * QS * S));
+  }
   TACO_TRY(t.tk_d2.ensure(sizeof(double) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.tk_ids.ensure(sizeof(int64_t) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)QS * std::max(k, 1)));
@@ -1618,7 +1633,7 @@ static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_
     k_select<<<(unsigned)ceil_div(QS * 32, 256), 256, 0, st>>>(
         ghist, t.part.as<int32_t>(), QS, idx->nchunks, idx->n_sub, budget, t.coff.as<int64_t>(), t.cand_cap,
         t.flags.as<int64_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cnum.as<int64_t>(),
-        t.lvl.as<int32_t>());
+        t.lvl.as<int32_t>(), t.gsb.as<int64_t>(), t.gsc.as<int64_t>());
     TACO_LAUNCHED();
   }
   {
@@ -1668,16 +1683,26 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
 // rows they share (each row is a candidate of ~beta*alpha-proportional many
 // queries of a batch) are read from HBM about once and then served by L2.
 // launches the plans and an async copy of flags[0..3] into t.flags_h (read after a stream sync)
+// candidate segments per query: cluster mode (q, rank) in qbase/clocal; global
+// mode (q, chunk) in gsb/gsc (k_select) -- both re-ranked chunk-major
+static inline int64_t seg_per_query(const taco_index* idx) { return idx->nchunks; }
+static inline const int64_t* seg_base(const taco_index* idx, const QueryTile& t) {
+  return idx->cluster_mode ? t.qbase.as<int64_t>() : t.gsb.as<int64_t>();
+}
+static inline const int64_t* seg_cnt(const taco_index* idx, const QueryTile& t) {
+  return idx->cluster_mode ? t.clocal.as<int64_t>() : t.gsc.as<int64_t>();
+}
+
 static int plan_async(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
-  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
+  const int64_t S = seg_per_query(idx);
   {
     ProfScope ps(K_PLAN, st);
     const int64_t nseg = QS * S, nb = ceil_div(nseg, PLAN_NT);
     TACO_TRY(t.psum.ensure(sizeof(int64_t) * 2 * (size_t)nb));
     if (S > 1) TACO_TRY(t.ppref.ensure(sizeof(int64_t) * (size_t)(nseg + 1)));
-    k_plan_sums<<<(unsigned)nb, PLAN_NT, 0, st>>>(t.clocal.as<int64_t>(), nseg, (int)S, QS, t.psum.as<int64_t>());
+    k_plan_sums<<<(unsigned)nb, PLAN_NT, 0, st>>>(seg_cnt(idx, t), nseg, (int)S, QS, t.psum.as<int64_t>());
     TACO_LAUNCHED();
-    k_plan_scan<<<(unsigned)nb, PLAN_NT, 0, st>>>(t.clocal.as<int64_t>(), nseg, (int)S, QS, t.psum.as<int64_t>(),
+    k_plan_scan<<<(unsigned)nb, PLAN_NT, 0, st>>>(seg_cnt(idx, t), nseg, (int)S, QS, t.psum.as<int64_t>(),
                                                   t.bpref.as<int64_t>(), S > 1 ? t.ppref.as<int64_t>() : nullptr,
                                                   t.flags.as<int64_t>());
     TACO_LAUNCHED();
@@ -1812,7 +1837,7 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
 }
 
 static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
-  const int64_t S = idx->cluster_mode ? idx->nchunks : 1;
+  const int64_t S = seg_per_query(idx);
   IntRerank ir;
   if (idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled()) {
     TACO_TRY(t.qb.ensure((size_t)QS * idx->d));
@@ -1831,7 +1856,7 @@ static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_
   }
   return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
-                     t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
+                     seg_base(idx, t), seg_cnt(idx, t), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
                      t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st, ir);
 }
 
