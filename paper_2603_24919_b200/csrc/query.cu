@@ -732,13 +732,37 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
                                        cand + sbase[q] + coff[q * nchunks + c], &S.batches);
     return;
   }
-  if (mode == CNT_TABLE && !NIB) {
-    uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * chunk);
-    for (int i = tid; i < (int)(chunk / 16); i += CT_THREADS) dst[i] = t4[i];
+  if ((mode == CNT_TABLE && !NIB) || (mode == CNT_HIST && scores)) {   // HIST: spill the table for the emit sweep
+    uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * tbytes);
+    for (int i = tid; i < tbytes / 16; i += CT_THREADS) dst[i] = t4[i];
   }
   chunk_levels(table, valid, n_sub, S);
   int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
   for (int l = tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
+}
+
+// Global-mode emit sweep: compact each (chunk, query) table spilled by the
+// count sweep (coalesced 16-byte reads from HBM) at the query's level L.
+template <bool NIB>
+__global__ void __launch_bounds__(CT_THREADS) k_emit_table(const uint8_t* __restrict__ tables, int64_t n,
+                                                           int64_t nchunks, int64_t chunk,
+                                                           const int32_t* __restrict__ lvl,
+                                                           const int64_t* __restrict__ sbase,
+                                                           const int64_t* __restrict__ scnt,
+                                                           const int64_t* __restrict__ coff, int64_t cand_cap,
+                                                           uint32_t* __restrict__ cand) {
+  __shared__ int fill;
+  const int64_t c = blockIdx.x, q = blockIdx.y;
+  if (sbase[q] + scnt[q] > cand_cap) return;
+  const int64_t hi = c + 1 < nchunks ? coff[q * nchunks + c + 1] : scnt[q];
+  if (hi == coff[q * nchunks + c]) return;   // no candidate of this query in this chunk
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  const int64_t tbytes = NIB ? chunk / 2 : chunk;
+  if (threadIdx.x == 0) fill = 0;
+  __syncthreads();
+  compact_unordered<CT_THREADS, NIB>(tables + ((size_t)q * nchunks + c) * tbytes, valid, (uint32_t)lvl[q], base,
+                                     cand + sbase[q] + coff[q * nchunks + c], &fill);
 }
 
 // Level histograms of externally provided score chunks (select_candidates tap).
@@ -1478,9 +1502,20 @@ __global__ void k_merge(int R, int k, int64_t nq, const double* __restrict__ d2,
 // ===================================================================== host
 constexpr int64_t kSuperTile = 16384;
 
+// 4-bit score tables whenever a score (<= n_sub) fits a nibble: half the
+// shared memory per CTA, so 4 CTAs of 256 threads share an SM.
+static inline bool nib_tables(const taco_index* idx) { return idx->n_sub <= 15; }
+static inline size_t table_bytes(const taco_index* idx) {
+  return (size_t)(nib_tables(idx) ? idx->chunk / 2 : idx->chunk);
+}
+
 static int64_t super_tile(const taco_index* idx, int cap) {
   const int64_t per = (int64_t)idx->n_sub * (2LL * cap + 20LL * idx->kp + 16) + 8LL * (idx->d + idx->D) + 64;
-  const int64_t Q = (int64_t)(1ll << 30) / std::max<int64_t>(per, 1);
+  int64_t Q = (int64_t)(1ll << 30) / std::max<int64_t>(per, 1);
+  if (!idx->cluster_mode) {   // + the spilled count tables: 8 GiB per tile
+    const int64_t tb = (idx->n_sub <= 15 ? idx->chunk / 2 : idx->chunk) * idx->nchunks;
+    Q = std::min<int64_t>(Q, (int64_t)(8ll << 30) / std::max<int64_t>(tb, 1));
+  }
   return std::max<int64_t>(64, std::min<int64_t>(Q, kSuperTile));
 }
 
@@ -1512,6 +1547,7 @@ static int ensure_front(taco_index* idx, QueryTile& t, int64_t QS, int k) {
   TACO_TRY(t.out_ids.ensure(sizeof(int32_t) * (size_t)QS * std::max(k, 1)));
   TACO_TRY(t.out_d.ensure(sizeof(float) * (size_t)QS * std::max(k, 1)));
   if (!idx->cluster_mode) {
+    TACO_TRY(t.gtab.ensure(table_bytes(idx) * (size_t)QS * idx->nchunks));   // spilled count tables
     TACO_TRY(t.part.ensure(sizeof(int32_t) * (size_t)QS * idx->nchunks * (idx->n_sub + 1)));
     TACO_TRY(t.hist.ensure(sizeof(int64_t) * (size_t)QS * (idx->n_sub + 1)));
     TACO_TRY(t.coff.ensure(sizeof(int64_t) * (size_t)QS * idx->nchunks));
@@ -1581,12 +1617,6 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
   return TACO_OK;
 }
 
-// 4-bit score tables whenever a score (<= n_sub) fits a nibble: half the
-// shared memory per CTA, so 4 CTAs of 256 threads share an SM.
-static inline bool nib_tables(const taco_index* idx) { return idx->n_sub <= 15; }
-static inline size_t table_bytes(const taco_index* idx) {
-  return (size_t)(nib_tables(idx) ? idx->chunk / 2 : idx->chunk);
-}
 
 static int set_count_attrs(taco_index*) {
   static bool done = false;
@@ -1612,8 +1642,8 @@ static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t 
     auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
     kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_HIST, nullptr, t.part.as<int32_t>(), nullptr,
-        nullptr, nullptr, nullptr, 0, nullptr);
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_HIST, t.gtab.as<uint8_t>(), t.part.as<int32_t>(),
+        nullptr, nullptr, nullptr, nullptr, 0, nullptr);
     TACO_LAUNCHED();
   }
   {
@@ -1639,11 +1669,10 @@ static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COMPACT, st);
-    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
-    kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
-        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, nullptr, nullptr, t.lvl.as<int32_t>(),
-        t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap, t.cand.as<uint32_t>());
+    auto kern = nib_tables(idx) ? k_emit_table<true> : k_emit_table<false>;
+    kern<<<g, CT_THREADS, 0, st>>>(t.gtab.as<uint8_t>(), idx->n, idx->nchunks, idx->chunk, t.lvl.as<int32_t>(),
+                                   t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap,
+                                   t.cand.as<uint32_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
