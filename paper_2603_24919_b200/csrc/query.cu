@@ -635,7 +635,7 @@ __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& 
 // Candidates of a query live in per-CTA segments (segment q*S + rank); the
 // final top-k breaks distance ties by id, so segment order is irrelevant.
 template <bool NIB>
-__global__ void __launch_bounds__(CT_THREADS, 2) k_count_cluster(
+__global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
