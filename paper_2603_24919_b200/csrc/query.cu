@@ -1530,7 +1530,7 @@ static int ensure_front(taco_index* idx, QueryTile& t, int64_t QS, int k) {
   TACO_TRY(t.npop.ensure(sizeof(int32_t) * QN));
   TACO_TRY(t.ret.ensure(sizeof(int64_t) * QN));
   TACO_TRY(t.flags.ensure(sizeof(int64_t) * 8));
-  if (!t.flags_h) TACO_CHECK_CUDA(cudaMallocHost(&t.flags_h, sizeof(int64_t) * 4));
+  if (!t.flags_h) TACO_CHECK_CUDA(cudaMallocHost(&t.flags_h, sizeof(int64_t) * 8));
   TACO_TRY(t.lvl.ensure(sizeof(int32_t) * QS));
   TACO_TRY(t.cnum.ensure(sizeof(int64_t) * QS));
   const int64_t S = idx->nchunks;   // candidate segments per query (re-rank plan)
@@ -1736,7 +1736,7 @@ static int plan_async(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st
                                                   t.flags.as<int64_t>());
     TACO_LAUNCHED();
   }
-  TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, st));
   return TACO_OK;
 }
 
@@ -1789,7 +1789,7 @@ static int launch_rerank_async(const void* X, int d, const float* Qf, const int4
 // every partial sum (< 2^31) -- is exact, so the fp64 d2 equals the integer
 // sum x^2 - 2 sum x q + sum q^2, computed with DP4A.
 __global__ void k_q_u8(const float* __restrict__ Q, int64_t nq, int d, uint8_t* __restrict__ Qb,
-                       int32_t* __restrict__ qsq, uint8_t* __restrict__ qok) {
+                       int32_t* __restrict__ qsq, uint8_t* __restrict__ qok, int64_t* __restrict__ any_fp) {
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (q >= nq) return;
@@ -1808,6 +1808,7 @@ __global__ void k_q_u8(const float* __restrict__ Q, int64_t nq, int d, uint8_t* 
   if (lane == 0) {
     qsq[q] = (int32_t)sq;
     qok[q] = ok ? 1 : 0;
+    if (!ok) any_fp[0] = 1;   // some query of the batch takes the fp64 path
   }
 }
 
@@ -1865,19 +1866,26 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
   return TACO_OK;
 }
 
-static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_t ntiles, cudaStream_t st) {
+static int q_u8_prep(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
+  TACO_TRY(t.qb.ensure((size_t)QS * idx->d));
+  TACO_TRY(t.qsq.ensure(sizeof(int32_t) * (size_t)QS));
+  TACO_TRY(t.qok.ensure((size_t)QS));
+  ProfScope ps(K_PLAN, st);
+  k_q_u8<<<(unsigned)ceil_div(QS * 32, 256), 256, 0, st>>>(t.Q.as<float>(), QS, idx->d, t.qb.as<uint8_t>(),
+                                                            t.qsq.as<int32_t>(), t.qok.as<uint8_t>(),
+                                                            t.flags.as<int64_t>() + 4);
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
+// prepped: tile_front already ran q_u8_prep (the split API has not)
+static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_t ntiles, cudaStream_t st,
+                        bool prepped = false) {
   const int64_t S = seg_per_query(idx);
   IntRerank ir;
-  if (idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled()) {
-    TACO_TRY(t.qb.ensure((size_t)QS * idx->d));
-    TACO_TRY(t.qsq.ensure(sizeof(int32_t) * (size_t)QS));
-    TACO_TRY(t.qok.ensure((size_t)QS));
-    {
-      ProfScope ps(K_PLAN, st);
-      k_q_u8<<<(unsigned)ceil_div(QS * 32, 256), 256, 0, st>>>(t.Q.as<float>(), QS, idx->d, t.qb.as<uint8_t>(),
-                                                                t.qsq.as<int32_t>(), t.qok.as<uint8_t>());
-      TACO_LAUNCHED();
-    }
+  const bool intp = idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled();
+  if (intp && !prepped) TACO_TRY(q_u8_prep(idx, t, QS, st));
+  if (intp) {
     ir.Qb = t.qb.as<uint8_t>();
     ir.qok = t.qok.as<uint8_t>();
     ir.qsq = t.qsq.as<int32_t>();
@@ -1918,6 +1926,8 @@ static int tile_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, d
     TACO_TRY(global_count(idx, t, QS, st));
     TACO_TRY(global_select(idx, t, QS, t.hist.as<int64_t>(), beta, st));
   }
+  if (idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled())   // integer re-rank eligibility -> flags[4]
+    TACO_TRY(q_u8_prep(idx, t, QS, st));
   return plan_async(idx, t, QS, st);
 }
 
@@ -1939,7 +1949,7 @@ static int tile_back(taco_index* idx, QueryTile& t, int64_t QS, double alpha, do
       continue;
     }
     prof_stats(idx, t, QS, fl[3]);
-    return rerank_stage(idx, t, QS, k, fl[2], st);
+    return rerank_stage(idx, t, QS, k, fl[2], st, true);
   }
   TACO_FAIL(TACO_ERR_CUDA, "query scratch did not converge");
 }
