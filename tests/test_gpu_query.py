@@ -251,3 +251,21 @@ def test_integer_rerank_path(int_queries, monkeypatch):
         oi, od, on, ol = O.knn_batch(oidx, X, Q, a, b, k)
         np.testing.assert_array_equal(ids, oi)
         np.testing.assert_array_equal(dists, od)
+
+
+def test_pipelined_batch_matches_oracle():
+    """A batch >= 2 x 2048 queries runs as two tiles on two streams; every
+    query's answer must still be the oracle's (and the same as unbatched)."""
+    X, Q, _ = make_config(1, n=20000, nq=4500, d=32)
+    idx = T.build_index(X, T.IndexParams(8, 4, 64, 5, 4))
+    qp = T.QueryParams(0.05, 0.01, 10)
+    ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+    oidx = O.deserialize(T.serialize_index(idx))
+    sel = np.r_[0:40, 2240:2280, 4460:4500]   # both tiles and their seams
+    oi, od, on, ol = O.knn_batch(oidx, X, Q[sel], qp.alpha, qp.beta, qp.k)
+    np.testing.assert_array_equal(ids[sel], oi)
+    np.testing.assert_array_equal(dists[sel], od)
+    np.testing.assert_array_equal(num[sel], on)
+    np.testing.assert_array_equal(lvl[sel], ol)
+    i2, d2, n2, l2 = T.knn_query_batch(idx, X, Q[2250:2260], qp)   # a small unpipelined batch
+    np.testing.assert_array_equal(i2, ids[2250:2260])
