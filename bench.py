@@ -342,6 +342,7 @@ def run_ours(args):
             "mean_candidates": stats["sum_candidates"] / nq,
             "mean_retrieved_per_subspace": stats["sum_retrieved"] / nq / meta["n_sub"],
             "mean_pops_per_subspace": stats["sum_pops"] / nq / meta["n_sub"],
+            "max_pops_per_subspace": stats.get("max_pops"),
             "row_format": {0: "f32", 1: "f16", 2: "u8"}.get(stats["row_format"]),
             "kernels": {kname: {"ms": round(v[0], 4), "launches": v[1],
                                 "algorithmic_GBps": (round(kernel_bytes(kname, stats, meta) / (v[0] / 1e3) / 1e9, 1)

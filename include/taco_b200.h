@@ -165,7 +165,9 @@ int taco_sc_linear_scores(int device, const float* T_h, int64_t n, int32_t n_sub
 int taco_sc_linear_scores_index(taco_index* idx, const float* qt_h, double alpha, uint8_t* scores_h);
 
 /* --------------------------------------------------------------- profiling */
-/* Per-kernel CUDA-event timing of the query path on its launching stream. */
+/* Per-kernel CUDA-event timing of the query path on its launching stream.
+ * stats_out[7]: sum retrieved ids, sum candidates, sum pops, queries, tiles,
+ * score-table bytes, max pops of one (query, subspace). */
 int taco_profile_enable(int on);
 int taco_profile_read(double* ms_out, int64_t* cnt_out, int64_t* stats_out, int reset);
 const char* taco_profile_name(int i);

@@ -179,10 +179,10 @@ def profile_read(reset=True):
     nk = lib().taco_profile_kernels()
     ms = np.zeros(nk)
     cnt = np.zeros(nk, np.int64)
-    st = np.zeros(6, np.int64)
+    st = np.zeros(7, np.int64)
     check(lib().taco_profile_read(ptr(ms), ptr(cnt), ptr(st), 1 if reset else 0))
     names = [lib().taco_profile_name(i).decode() for i in range(nk)]
-    keys = ("sum_retrieved", "sum_candidates", "sum_pops", "queries", "tiles", "score_bytes")
+    keys = ("sum_retrieved", "sum_candidates", "sum_pops", "queries", "tiles", "score_bytes", "max_pops")
     return {n: (float(m), int(c)) for n, m, c in zip(names, ms, cnt)}, dict(zip(keys, map(int, st)))
 
 

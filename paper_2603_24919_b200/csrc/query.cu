@@ -49,7 +49,7 @@ struct Prof {
   std::vector<P> pend;
   double ms[K_NKIDS] = {};
   int64_t cnt[K_NKIDS] = {};
-  int64_t sumR = 0, sumC = 0, sumPops = 0, queries = 0, tiles = 0, bytes_scores = 0;
+  int64_t sumR = 0, sumC = 0, sumPops = 0, queries = 0, tiles = 0, bytes_scores = 0, maxPops = 0;
 };
 static Prof g_prof;
 static cudaEvent_t prof_event() {
@@ -1904,7 +1904,10 @@ static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total)
   cudaMemcpy(r.data(), t.ret.p, 8 * r.size(), cudaMemcpyDeviceToHost);
   cudaMemcpy(np.data(), t.npop.p, 4 * np.size(), cudaMemcpyDeviceToHost);
   for (auto v : r) g_prof.sumR += v;
-  for (auto v : np) g_prof.sumPops += v;
+  for (auto v : np) {
+    g_prof.sumPops += v;
+    g_prof.maxPops = std::max<int64_t>(g_prof.maxPops, v);
+  }
   g_prof.sumC += total;
   g_prof.queries += QS;
   g_prof.tiles += 1;
@@ -2435,10 +2438,11 @@ int taco_profile_read(double* ms_out, int64_t* cnt_out, int64_t* stats_out, int 
   for (int i = 0; i < taco::K_NKIDS; ++i) { ms_out[i] = taco::g_prof.ms[i]; cnt_out[i] = taco::g_prof.cnt[i]; }
   stats_out[0] = taco::g_prof.sumR; stats_out[1] = taco::g_prof.sumC; stats_out[2] = taco::g_prof.sumPops;
   stats_out[3] = taco::g_prof.queries; stats_out[4] = taco::g_prof.tiles; stats_out[5] = taco::g_prof.bytes_scores;
+  stats_out[6] = taco::g_prof.maxPops;
   if (reset) {
     for (int i = 0; i < taco::K_NKIDS; ++i) { taco::g_prof.ms[i] = 0; taco::g_prof.cnt[i] = 0; }
     taco::g_prof.sumR = taco::g_prof.sumC = taco::g_prof.sumPops = 0;
-    taco::g_prof.queries = taco::g_prof.tiles = taco::g_prof.bytes_scores = 0;
+    taco::g_prof.queries = taco::g_prof.tiles = taco::g_prof.bytes_scores = taco::g_prof.maxPops = 0;
   }
   return TACO_OK;
 }
