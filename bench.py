@@ -65,8 +65,11 @@ class Clocks:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
+            t0 = time.time()   # wait (bounded) until the sampler is actually sampling
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -260,12 +263,12 @@ def run_ours(args):
         nat.call("taco_query_batch_device", dev.h, Qd.data_ptr(), nq, qp.alpha, qp.beta, k,
                  ids_d.data_ptr(), dist_d.data_ptr(), num_d.data_ptr(), lvl_d.data_ptr(), stream_ptr)
 
-    for _ in range(args.warmup):
-        device_step()
-    torch.cuda.synchronize()
     times = []
-    launches0 = nat.launch_count()
     with Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0)) as clk:
+        for _ in range(args.warmup):
+            device_step()
+        torch.cuda.synchronize()
+        launches0 = nat.launch_count()
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
