@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "index.cuh"
 
 namespace taco {
@@ -31,41 +33,82 @@ __global__ void k_nonfinite(const float* __restrict__ X, int64_t total, int d,
 }
 
 // numpy mean(axis=0) of a C-contiguous matrix: out = X[0]; out += X[r] for
-// r = 1..n-1 (row-sequential), then / n.  Each of the block's first d
-// threads runs one column's add chain over row tiles that the whole block
-// stages in shared memory (double buffered).  One block per 1024 columns.
-constexpr int CM_THREADS = 1024;
-constexpr int CM_TILE_BYTES = 48 * 1024;
+// r = 1..n-1 (row-sequential), then / n.  The add chain is inherently
+// sequential per column, so the kernel is built to run at the dependent-DADD
+// latency floor: one CTA per 32-column slab, warp 0 = the 32 chains (lane =
+// column), warps 1..3 stream the slab's rows into an 8-stage shared-memory
+// ring with cp.async (16-byte pieces when the slab is 16-byte aligned) so the
+// chain never waits on HBM.  One __syncthreads per 128-row stage.
+constexpr int CM_W = 32;          // columns per CTA
+constexpr int CM_ROWS = 128;      // rows per stage
+constexpr int CM_STAGES = 8;
+constexpr int CM_THREADS = 128;   // 1 consumer warp + 3 producer warps
+constexpr size_t CM_SMEM = sizeof(float) * CM_STAGES * CM_ROWS * CM_W;
+
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restrict__ X, int64_t n, int d,
                                                             double* __restrict__ mean) {
-  extern __shared__ float cm[];
-  const int c0 = blockIdx.x * CM_THREADS;
-  const int nc = min(CM_THREADS, d - c0);
-  const int rows = max(1, CM_TILE_BYTES / (4 * nc));
-  float* buf[2] = {cm, cm + (size_t)rows * nc};
+  extern __shared__ __align__(16) float cm[];
+  const int c0 = blockIdx.x * CM_W;
+  const int nc = min(CM_W, d - c0);
   const int tid = threadIdx.x;
-  const int64_t ntile = (n + rows - 1) / rows;
-  auto load = [&](int64_t tb, float* dst) {
-    const int64_t r0 = tb * rows;
-    const int rr = (int)min((int64_t)rows, n - r0);
-    for (int e = tid; e < rr * nc; e += CM_THREADS) {
-      const int r = e / nc, c = e % nc;
-      dst[e] = X[(r0 + r) * d + c0 + c];
+  const int64_t ntile = (n + CM_ROWS - 1) / CM_ROWS;
+  const bool vec = (d % 4 == 0) && (nc % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  const int ptid = tid - 32;   // producer index (warps 1..3)
+  auto load = [&](int64_t tb) {
+    if (tb < ntile) {
+      float* dst = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W;
+      const int64_t r0 = tb * CM_ROWS;
+      const int rr = (int)min((int64_t)CM_ROWS, n - r0);
+      if (vec) {
+        const int per = nc / 4;
+        for (int e = ptid; e < rr * per; e += CM_THREADS - 32) {
+          const int r = e / per, q = e - r * per;
+          cp_async16(dst + r * CM_W + 4 * q, X + (r0 + r) * d + c0 + 4 * q);
+        }
+      } else {
+        for (int e = ptid; e < rr * nc; e += CM_THREADS - 32) {
+          const int r = e / nc, c = e - r * nc;
+          cp_async4(dst + r * CM_W + c, X + (r0 + r) * d + c0 + c);
+        }
+      }
     }
+    cp_commit();
   };
-  load(0, buf[0]);
-  __syncthreads();
+  if (tid >= 32)
+    for (int s = 0; s < CM_STAGES - 1; ++s) load(s);
   double acc = 0.0;
   for (int64_t tb = 0; tb < ntile; ++tb) {
-    if (tb + 1 < ntile) load(tb + 1, buf[(tb + 1) & 1]);
-    if (tid < nc) {
-      const float* tv = buf[tb & 1];
-      const int rr = (int)min((int64_t)rows, n - tb * rows);
+    if (tid >= 32) cp_wait<CM_STAGES - 2>();   // tile tb has landed (this thread's pieces)
+    __syncthreads();                             // ... everyone's; slot (tb-1)%S is free
+    if (tid >= 32) {
+      load(tb + CM_STAGES - 1);
+    } else if (tid < nc) {
+      const float* tv = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W + tid;
+      const int rr = (int)min((int64_t)CM_ROWS, n - tb * CM_ROWS);
       int r = 0;
-      if (tb == 0) { acc = (double)tv[tid]; r = 1; }
-      for (; r < rr; ++r) acc = __dadd_rn(acc, (double)tv[r * nc + tid]);
+      if (tb == 0) { acc = (double)tv[0]; r = 1; }
+      if (rr == CM_ROWS) {
+        for (; r < CM_ROWS; r += 8) {   // r = 0 or 1 at entry: the 8-blocks may start at 1
+          if (r + 8 > CM_ROWS) break;
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = tv[(r + u) * CM_W];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+        }
+      }
+      for (; r < rr; ++r) acc = __dadd_rn(acc, (double)tv[r * CM_W]);
     }
-    __syncthreads();
   }
   if (tid < nc) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
 }
@@ -136,8 +179,8 @@ __global__ void k_gram_reduce(const double* __restrict__ partial, int splits, in
 }
 
 // ================================================================ k-means
-constexpr int PP_THREADS = 256;
-constexpr int PP_PPT = 4;                       // points per thread in one block
+constexpr int PP_THREADS = 1024;
+constexpr int PP_PPT = 1;                       // points per thread in one block
 constexpr int PP_BLOCK = PP_THREADS * PP_PPT;   // points per block-sum
 constexpr double U0 = 1.1102230246251565e-16;   // 2^-53
 
@@ -150,7 +193,7 @@ struct HalfView {
   int k;
 };
 
-__global__ void k_xsq(HalfView h, double* __restrict__ xsq, double* __restrict__ xsqmax_blk) {
+__global__ void k_xsq(HalfView h, double* __restrict__ xsq, int64_t* __restrict__ status) {
   __shared__ double red[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
@@ -164,59 +207,14 @@ __global__ void k_xsq(HalfView h, double* __restrict__ xsq, double* __restrict__
   if (threadIdx.x < 32) {
     double w = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
-    if (threadIdx.x == 0) xsqmax_blk[blockIdx.x] = w;
+    // non-negative doubles order like their bit patterns
+    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(status + 5),
+                                    (unsigned long long)__double_as_longlong(w));
   }
 }
 
 // status layout (int64): [0] degenerate draw index (k if none), [1] fallbacks,
-// [2] converged flag, [3] n_iter, [4] changed count
-// D^2 update for centroid `ci` (= picks[ci]) and per-block sums of best.
-__global__ void __launch_bounds__(PP_THREADS) k_pp_update(HalfView h, const double* __restrict__ xsq,
-                                                          const int64_t* __restrict__ picks, int ci,
-                                                          double* __restrict__ best,
-                                                          double* __restrict__ C64,
-                                                          double* __restrict__ bsum) {
-  __shared__ double cv[64];
-  __shared__ double red[PP_THREADS / 32];
-  __shared__ double s_csq;
-  const int64_t p = picks[ci];
-  if (threadIdx.x < h.m) cv[threadIdx.x] = (double)h.X[(size_t)threadIdx.x * h.n + p];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_csq = einsum_sq([&](int t) { return cv[t]; }, h.m);
-    if (blockIdx.x == 0)
-      for (int t = 0; t < h.m; ++t) C64[(size_t)ci * h.m + t] = cv[t];
-  }
-  __syncthreads();
-  const double csq = s_csq;
-  const int64_t b0 = (int64_t)blockIdx.x * PP_BLOCK + threadIdx.x;
-  double s = 0.0;
-#pragma unroll
-  for (int u = 0; u < PP_PPT; ++u) {
-    const int64_t i = b0 + (int64_t)u * PP_THREADS;
-    if (i < h.n) {
-      const double dot = dot_fma([&](int t) { return (double)h.X[(size_t)t * h.n + i]; },
-                                 [&](int t) { return cv[t]; }, h.m);
-      const double d2 = sq_dist_expand(xsq[i], dot, csq);
-      double b = d2;
-      if (ci > 0) {
-        const double old = best[i];
-        b = d2 < old ? d2 : old;
-      }
-      best[i] = b;
-      s = __dadd_rn(s, b);
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
-    bsum[blockIdx.x] = t;
-  }
-}
-
+// [2] converged flag, [3] n_iter, [4] changed count, [5] max xsq (double bits)
 // numpy pairwise summation (loops_utils.h.src, as measured in DESIGN.md §4):
 // n < 8 sequential; n <= 128 eight strided accumulators combined
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail; else split at
@@ -237,17 +235,17 @@ static void pairwise_leaves(int64_t off, int64_t len, std::vector<int64_t>& out)
 __device__ double np_leaf(const double* a, int64_t len) {
   if (len < 8) {
     double r = 0.0;
-    for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, a[i]);
+    for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, __ldcg(a + i));
     return r;
   }
   double r[8];
-  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  for (int j = 0; j < 8; ++j) r[j] = __ldcg(a + j);
   int64_t i = 8;
   for (; i < len - (len % 8); i += 8)
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __ldcg(a + i + j));
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < len; ++i) res = __dadd_rn(res, a[i]);
+  for (; i < len; ++i) res = __dadd_rn(res, __ldcg(a + i));
   return res;
 }
 
@@ -290,11 +288,11 @@ __device__ double np_combine(const double* leaf, int64_t n) {
 // replay numpy's arithmetic exactly (single thread).
 constexpr int PS_THREADS = 1024;
 constexpr int PS_TILE = 2048;   // doubles per staged tile of the replay chain
-__global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const double* __restrict__ best,
+__device__ __forceinline__ void pp_search_body(HalfView h, const double* __restrict__ best,
                                                           const double* __restrict__ bsum, int64_t nb,
                                                           const double* __restrict__ uni,
                                                           const int64_t* __restrict__ forced,
-                                                          double xsqmax, int ci,
+                                                          int ci,
                                                           int64_t* __restrict__ picks,
                                                           int64_t* __restrict__ status,
                                                           const int64_t* __restrict__ leaves, int64_t nleaves,
@@ -314,7 +312,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   const int64_t per = (nb + PS_THREADS - 1) / PS_THREADS;
   const int64_t a0 = (int64_t)tid * per, a1 = min(nb, a0 + per);
   double loc = 0.0;
-  for (int64_t b = a0; b < a1; ++b) loc = __dadd_rn(loc, bsum[b]);
+  for (int64_t b = a0; b < a1; ++b) loc = __dadd_rn(loc, __ldcg(bsum + b));
   double v = loc;
   for (int o = 1; o < 32; o <<= 1) {
     double x = __shfl_up_sync(0xffffffffu, v, o);
@@ -349,7 +347,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   {
     double pre = run;
     for (int64_t b = a0; b < a1; ++b) {
-      const double nx = __dadd_rn(pre, bsum[b]);
+      const double nx = __dadd_rn(pre, __ldcg(bsum + b));
       if (nx > target && pre <= target) {
         s_blk = b;
         s_before = pre;
@@ -360,19 +358,54 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   __syncthreads();
   __shared__ int s_ok;
   __shared__ double s_total;
+  __shared__ double s_scan[PP_BLOCK];
+  __shared__ int s_k;
   int64_t blk = s_blk;
+  if (blk < 0) blk = nb - 1;   // rounding put the target at/after the end
+  const double pre = s_blk >= 0 ? s_before : S - __ldcg(bsum + blk);
+  const int64_t i0 = blk * PP_BLOCK, i1 = min(h.n, i0 + PP_BLOCK);
+  {
+    // in-block inclusive prefix of best[] (a fp64 tree scan: error well
+    // inside the certified budget below), then the first crossing
+    static_assert(PS_THREADS == PP_BLOCK, "one thread per point of the block");
+    const double x = i0 + tid < i1 ? __ldcg(best + i0 + tid) : 0.0;
+    double sv = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, sv, o);
+      if (lane >= o) sv = __dadd_rn(sv, y);
+    }
+    __syncthreads();   // wsum reuse
+    if (lane == 31) wsum[wid] = sv;
+    if (tid == 0) s_k = PP_BLOCK;
+    __syncthreads();
+    if (wid == 0) {
+      double w = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w = __dadd_rn(w, y);
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    if (wid) sv = __dadd_rn(sv, wsum[wid - 1]);
+    s_scan[tid] = sv;
+    if (i0 + tid < i1 && __dadd_rn(pre, sv) > target) atomicMin(&s_k, tid);
+    __syncthreads();
+  }
   if (tid == 0) {
     int64_t kstar = -1;
     double Pk = 0.0, Pkm1 = 0.0;
-    if (blk < 0) blk = nb - 1;   // rounding put the target at/after the end
-    double pre = s_blk >= 0 ? s_before : S - bsum[blk];
-    const int64_t i0 = blk * PP_BLOCK, i1 = min(h.n, i0 + PP_BLOCK);
-    for (int64_t i = i0; i < i1; ++i) {
-      const double nx = __dadd_rn(pre, best[i]);
-      if (nx > target) { kstar = i; Pk = nx; Pkm1 = pre; break; }
-      pre = nx;
+    const int kk = s_k;
+    if (kk < PP_BLOCK) {
+      kstar = i0 + kk;
+      Pk = __dadd_rn(pre, s_scan[kk]);
+      Pkm1 = kk ? __dadd_rn(pre, s_scan[kk - 1]) : pre;
+    } else {
+      const int last = (int)(i1 - i0 - 1);
+      kstar = i1 - 1;
+      Pk = __dadd_rn(pre, s_scan[last]);
+      Pkm1 = last ? __dadd_rn(pre, s_scan[last - 1]) : pre;
     }
-    if (kstar < 0) { kstar = i1 - 1; Pk = pre; Pkm1 = pre - best[kstar]; }
     // Error budget (rigorous, first order + slack): the reference's
     // cdf_k / cdf_last deviates from B_k/B_n by at most (k + n + 3)u
     // (sequential cumsum of k and n terms, p = b/T roundings, the division);
@@ -381,6 +414,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
     // rounding of its dgemv-ordered dot products: |delta d2| <= 8u(|x|+|c|)^2.
     const double n = (double)h.n;
     const double rel = ((double)kstar + n + 1200.0) * U0 * 1.05;
+    const double xsqmax = __longlong_as_double((long long)status[5]);
     const double absU = 32.0 * U0 * n * xsqmax;
     const double margin = rel * S + 2.0 * absU;
     s_ok = !force_replay && (Pk - target > margin) && (target - Pkm1 >= margin);
@@ -397,7 +431,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   if (tid == 0) s_total = np_combine(lsum, h.n);
   __syncthreads();
   const double total = s_total;
-  for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(best[i], total);
+  for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(__ldcg(best + i), total);
   __syncthreads();
   // The sequential cumsum chain runs once on thread 0 over shared-memory tiles
   // that the rest of the block streams in (double buffered) and writes back
@@ -467,18 +501,89 @@ __global__ void __launch_bounds__(PS_THREADS) k_pp_search(HalfView h, const doub
   }
 }
 
+// One k-means++ draw in one launch: the D^2 update for centroid ci and the
+// block sums (every block), then the last block to finish (atomic ticket in
+// status[6]) chooses picks[ci+1] with the certified search above.
+__global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const double* __restrict__ xsq, int ci,
+                                                        double* __restrict__ best, double* __restrict__ C64,
+                                                        double* __restrict__ bsum, int64_t nb,
+                                                        const double* __restrict__ uni,
+                                                        const int64_t* __restrict__ forced,
+                                                        int64_t* __restrict__ picks, int64_t* __restrict__ status,
+                                                        const int64_t* __restrict__ leaves, int64_t nleaves,
+                                                        double* __restrict__ lsum, double* __restrict__ pbuf,
+                                                        double* __restrict__ cbuf, int force_replay) {
+  __shared__ double cv[64];
+  __shared__ double red[PP_THREADS / 32];
+  __shared__ double s_csq;
+  __shared__ int s_last;
+  const int64_t p = __ldcg(picks + ci);
+  if (threadIdx.x < h.m) cv[threadIdx.x] = (double)h.X[(size_t)threadIdx.x * h.n + p];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_csq = einsum_sq([&](int t) { return cv[t]; }, h.m);
+    if (blockIdx.x == 0)
+      for (int t = 0; t < h.m; ++t) C64[(size_t)ci * h.m + t] = cv[t];
+  }
+  __syncthreads();
+  const double csq = s_csq;
+  const int64_t i = (int64_t)blockIdx.x * PP_BLOCK + threadIdx.x;
+  double s = 0.0;
+  if (i < h.n) {
+    const double dot = dot_fma([&](int t) { return (double)h.X[(size_t)t * h.n + i]; },
+                               [&](int t) { return cv[t]; }, h.m);
+    const double d2 = sq_dist_expand(xsq[i], dot, csq);
+    double b = d2;
+    if (ci > 0) {
+      const double old = best[i];
+      b = d2 < old ? d2 : old;
+      if (d2 < old) best[i] = b;
+    } else {
+      best[i] = b;
+    }
+    s = b;
+  }
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
+    bsum[blockIdx.x] = t;
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 6), 1ull) == (unsigned long long)(nb - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) status[6] = 0;   // ticket for the next draw (stream-ordered launch)
+  if (ci + 1 < h.k)
+    pp_search_body(h, best, bsum, nb, uni, forced, ci, picks, status, leaves, nleaves, lsum, pbuf, cbuf,
+                   force_replay);
+}
+
 // ------------------------------------------------------------------ Lloyd
 constexpr int AS_THREADS = 256;
-template <int MM>
+// Lloyd assignment (clustering.py:86-89): d2 = max((xsq - 2 x.c) + csq, 0)
+// with x.c one FMA chain over t (dgemm order), first argmin.  Each thread
+// owns PPT points so every centroid coordinate read from shared memory feeds
+// PPT independent FMA chains (the kernel is fp64-issue bound).
+template <int MM, int PPT>
 __global__ void __launch_bounds__(AS_THREADS) k_assign(HalfView h, const double* __restrict__ xsq,
                                                        const double* __restrict__ C64,
                                                        const int32_t* __restrict__ lab,
                                                        int32_t* __restrict__ newlab,
                                                        double* __restrict__ pd, int iter,
                                                        int64_t* __restrict__ status,
-                                                       double* __restrict__ hsum) {
+                                                       double* __restrict__ hsum,
+                                                       unsigned long long* __restrict__ cnt_cur,
+                                                       unsigned long long* __restrict__ cnt_next) {
   extern __shared__ double ash[];
+  __shared__ int lhist[256];
   if (status[2]) return;
+  for (int c = threadIdx.x; c < h.k; c += AS_THREADS) lhist[c] = 0;
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < h.k; c += AS_THREADS) cnt_next[c] = 0ull;
   const int m = h.m;
   double* C = ash;                    // k*m
   double* csq = ash + (size_t)h.k * m; // k
@@ -490,34 +595,58 @@ __global__ void __launch_bounds__(AS_THREADS) k_assign(HalfView h, const double*
   for (int c = threadIdx.x; c < h.k; c += AS_THREADS)
     csq[c] = einsum_sq([&](int t) { return C[c * m + t]; }, m);
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * AS_THREADS + threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * AS_THREADS * PPT + threadIdx.x;
+  double x[PPT][MM], xs[PPT], bd[PPT];
+  int bl[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int64_t i = i0 + (int64_t)j * AS_THREADS;
+    const bool live = i < h.n;
+#pragma unroll
+    for (int t = 0; t < MM; ++t) x[j][t] = (t < m && live) ? (double)h.X[(size_t)t * h.n + i] : 0.0;
+    xs[j] = live ? xsq[i] : 0.0;
+    bd[j] = 0.0;
+    bl[j] = 0;
+  }
+  for (int c = 0; c < h.k; ++c) {
+    const double* cr = C + c * m;
+    double acc[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int t = 0; t < MM; ++t) {
+      if (t < m) {
+        const double cv = cr[t];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) acc[j] = __fma_rn(x[j][t], cv, acc[j]);
+      }
+    }
+    const double cs = csq[c];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const double d2 = sq_dist_expand(xs[j], acc[j], cs);
+      if (c == 0 || d2 < bd[j]) { bd[j] = d2; bl[j] = c; }
+    }
+  }
   double my = 0.0;
   int changed = 0;
-  if (i < h.n) {
-    double x[MM];
 #pragma unroll
-    for (int t = 0; t < MM; ++t) x[t] = t < m ? (double)h.X[(size_t)t * h.n + i] : 0.0;
-    const double xs = xsq[i];
-    double bd = 0.0;
-    int bl = 0;
-    for (int c = 0; c < h.k; ++c) {
-      const double* cr = C + c * m;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t < MM; ++t)
-        if (t < m) acc = __fma_rn(x[t], cr[t], acc);
-      const double d2 = sq_dist_expand(xs, acc, csq[c]);
-      if (c == 0 || d2 < bd) { bd = d2; bl = c; }
+  for (int j = 0; j < PPT; ++j) {
+    const int64_t i = i0 + (int64_t)j * AS_THREADS;
+    if (i < h.n) {
+      newlab[i] = bl[j];
+      atomicAdd(&lhist[bl[j]], 1);
+      pd[i] = bd[j];
+      my = __dadd_rn(my, bd[j]);
+      if (iter > 0 && lab[i] != bl[j]) changed = 1;
     }
-    newlab[i] = bl;
-    pd[i] = bd;
-    my = bd;
-    if (iter > 0 && lab[i] != bl) changed = 1;
   }
   if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) atomicOr(&chg, 1);
   for (int o = 16; o > 0; o >>= 1) my = __dadd_rn(my, __shfl_xor_sync(0xffffffffu, my, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = my;
   __syncthreads();
+  for (int c = threadIdx.x; c < h.k; c += AS_THREADS)
+    if (lhist[c]) atomicAdd(&cnt_cur[c], (unsigned long long)lhist[c]);
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < AS_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
@@ -548,118 +677,96 @@ __global__ void k_lloyd_ctl(const double* __restrict__ hsum, int64_t nb, int ite
   }
 }
 
-constexpr int LT = 4096;  // points per label tile
-__global__ void k_label_hist(int64_t n, int k, const int64_t* __restrict__ status,
-                             const int32_t* __restrict__ newlab, int32_t* __restrict__ lab,
-                             int32_t* __restrict__ lhist) {
+// centroid = (sequential fp64 sum over the cluster's points in index order) /
+// count -- the np.add.at order (clustering.py:95-99).  perm lists every
+// cluster's points in ascending index order (a stable radix sort of the
+// labels).  One CTA per cluster: warp 0's first m lanes run the m dependent
+// add chains; warps 1..3 gather the cluster's coordinates through perm into an
+// 8-stage shared-memory ring with cp.async, so each chain runs at the DADD
+// latency floor.  The producers also commit the new labels (lab[p] = c).
+constexpr int CS_R = 128, CS_ST = 8, CS_THREADS = 32 + CS_R;
+__global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const float* __restrict__ xp, int mp,
+                                                             const int64_t* __restrict__ status,
+                                                             const uint32_t* __restrict__ perm,
+                                                             const unsigned long long* __restrict__ counts,
+                                                             int32_t* __restrict__ lab,
+                                                             double* __restrict__ C64) {
   if (status[2]) return;
-  __shared__ int cnt[256];
-  for (int c = threadIdx.x; c < k; c += blockDim.x) cnt[c] = 0;
-  __syncthreads();
-  const int64_t i0 = (int64_t)blockIdx.x * LT;
-  const int64_t i1 = min(n, i0 + LT);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const int32_t l = newlab[i];
-    lab[i] = l;
-    atomicAdd(&cnt[l], 1);
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < k; c += blockDim.x) lhist[(size_t)blockIdx.x * k + c] = cnt[c];
-}
-
-// loff[tile][c] = start of (cluster c, tile) in the label-sorted order; counts[c]
-__global__ void k_label_offsets(int64_t ntiles, int k, const int64_t* __restrict__ status,
-                                const int32_t* __restrict__ lhist, int64_t* __restrict__ loff,
-                                int64_t* __restrict__ counts) {
-  if (status[2]) return;
-  __shared__ int64_t tot[256];
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    int64_t s = 0;
-    for (int64_t t = 0; t < ntiles; ++t) s += lhist[(size_t)t * k + c];
-    tot[c] = s;
-    counts[c] = s;
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    int64_t base = 0;
-    for (int c2 = 0; c2 < c; ++c2) base += tot[c2];
-    for (int64_t t = 0; t < ntiles; ++t) {
-      loff[(size_t)t * k + c] = base;
-      base += lhist[(size_t)t * k + c];
-    }
-  }
-}
-
-// one warp per tile, rounds of 32 ascending points: stable ranks via match_any
-__global__ void k_label_scatter(int64_t n, int k, const int64_t* __restrict__ status,
-                                const int32_t* __restrict__ lab, const int64_t* __restrict__ loff,
-                                int64_t* __restrict__ perm) {
-  if (status[2]) return;
-  __shared__ int64_t cur[256];
-  for (int c = threadIdx.x; c < k; c += 32) cur[c] = loff[(size_t)blockIdx.x * k + c];
-  __syncwarp();
-  const int lane = threadIdx.x;
-  const int64_t i0 = (int64_t)blockIdx.x * LT;
-  const int64_t i1 = min(n, i0 + LT);
-  for (int64_t r = i0; r < i1; r += 32) {
-    const int64_t i = r + lane;
-    const bool live = i < i1;
-    const int l = live ? lab[i] : -1;
-    const unsigned act = __ballot_sync(0xffffffffu, live);
-    const unsigned grp = __match_any_sync(0xffffffffu, l) & act;
-    if (live) {
-      const int rank = __popc(grp & ((1u << lane) - 1u));
-      perm[cur[l] + rank] = i;
-    }
-    __syncwarp();
-    if (live && lane == __ffs(grp) - 1) cur[l] += __popc(grp);
-    __syncwarp();
-  }
-}
-
-// xs[t][k] = X[t][perm[k]]: every cluster's values become one contiguous run
-// (label-sorted, index order inside a label) for the sequential sums below.
-__global__ void k_gather_sorted(HalfView h, const int64_t* __restrict__ status, const int64_t* __restrict__ perm,
-                                float* __restrict__ xs) {
-  if (status[2]) return;
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= h.n) return;
-  const int64_t p = perm[k];
-  for (int t = 0; t < h.m; ++t) xs[(size_t)t * h.n + k] = h.X[(size_t)t * h.n + p];
-}
-
-// centroid = (sequential fp64 sum over the cluster's points in index order) / count
-// -- np.add.at order (clustering.py:96).  One thread per (cluster, dim) runs
-// the dependent add chain over a contiguous, prefetchable run of xs.
-__global__ void k_cluster_sums(HalfView h, const int64_t* __restrict__ status,
-                               const float* __restrict__ xs, const int64_t* __restrict__ counts,
-                               double* __restrict__ C64) {
-  if (status[2]) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= h.k * h.m) return;
-  const int c = e / h.m, t = e % h.m;
-  const int64_t cnt = counts[c];
+  extern __shared__ __align__(16) float cs[];   // [CS_ST][CS_R][mp]
+  const int c = blockIdx.x, m = h.m, tid = threadIdx.x;
+  const int64_t cnt = (int64_t)counts[c];
   if (cnt == 0) return;
-  int64_t start = 0;
-  for (int c2 = 0; c2 < c; ++c2) start += counts[c2];
-  const float* x = xs + (size_t)t * h.n + start;
-  double acc = 0.0;
-  int64_t p = 0;
-  for (; p + 16 <= cnt; p += 16) {
-    float v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = __ldg(x + p + u);
-#pragma unroll
-    for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, (double)v[u]);
+  __shared__ int64_t s_start;
+  if (tid < 32) {
+    int64_t v = 0;
+    for (int c2 = tid; c2 < c; c2 += 32) v += (int64_t)counts[c2];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (tid == 0) s_start = v;
   }
-  for (; p < cnt; ++p) acc = __dadd_rn(acc, (double)x[p]);
-  C64[(size_t)c * h.m + t] = __ddiv_rn(acc, (double)cnt);
+  __syncthreads();
+  const uint32_t* pp = perm + s_start;
+  const int64_t ntile = (cnt + CS_R - 1) / CS_R;
+  const int SL = CS_R * mp;
+  const int r = tid - 32;   // producer: point r of every stage
+  auto load = [&](int64_t tb) {
+    if (tb < ntile && tb * CS_R + r < cnt) {
+      float* dst = cs + (size_t)(tb % CS_ST) * SL + r * mp;
+      const uint32_t p = pp[tb * CS_R + r];
+      const float* src = xp + (size_t)p * mp;   // the point's m coordinates: one 32-byte sector for m <= 8
+      for (int q = 0; q < mp; q += 4) cp_async16(dst + q, src + q);
+      lab[p] = c;
+    }
+    cp_commit();
+  };
+  if (tid >= 32)
+    for (int st = 0; st < CS_ST - 1; ++st) load(st);
+  double acc = 0.0;
+  for (int64_t tb = 0; tb < ntile; ++tb) {
+    if (tid >= 32) cp_wait<CS_ST - 2>();
+    __syncthreads();
+    if (tid >= 32) {
+      load(tb + CS_ST - 1);
+    } else if (tid < m) {
+      const float* tv = cs + (size_t)(tb % CS_ST) * SL + tid;
+      const int rr = (int)min((int64_t)CS_R, cnt - tb * CS_R);
+      int q = 0;
+      for (; q + 8 <= rr; q += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tv[(q + u) * mp];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
+      }
+      for (; q < rr; ++q) acc = __dadd_rn(acc, (double)tv[q * mp]);
+    }
+  }
+  if (tid < m) C64[(size_t)c * m + tid] = __ddiv_rn(acc, (double)cnt);
+}
+
+// point-major copy of a half (xp[i][t], t padded to mp = 4*ceil(m/4)) so a
+// point's coordinates are one contiguous 16-byte-aligned run for the gathers
+__global__ void k_point_major(HalfView h, int mp, float* __restrict__ xp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= h.n) return;
+  for (int q = 0; q < mp; q += 4) {
+    float4 v;
+    v.x = q + 0 < h.m ? h.X[(size_t)(q + 0) * h.n + i] : 0.f;
+    v.y = q + 1 < h.m ? h.X[(size_t)(q + 1) * h.n + i] : 0.f;
+    v.z = q + 2 < h.m ? h.X[(size_t)(q + 2) * h.n + i] : 0.f;
+    v.w = q + 3 < h.m ? h.X[(size_t)(q + 3) * h.n + i] : 0.f;
+    *reinterpret_cast<float4*>(xp + (size_t)i * mp + q) = v;
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
 }
 
 // empty clusters (ascending): farthest point (first argmax of point_d2 with
 // already-taken points at -1) becomes the centroid and moves its label.
 __global__ void k_reseed(HalfView h, const int64_t* __restrict__ status,
-                         const int64_t* __restrict__ counts, double* __restrict__ far,
+                         const unsigned long long* __restrict__ counts, double* __restrict__ far,
                          int32_t* __restrict__ lab, double* __restrict__ C64) {
   if (status[2]) return;
   __shared__ double bv[32];
@@ -698,6 +805,8 @@ __global__ void k_centroids_out(const double* __restrict__ C64, int km, float* _
 }
 
 __global__ void k_status_init(int64_t* status, int k) {
+  status[5] = 0;
+  status[6] = 0;
   status[0] = k;
   status[1] = 0;
   status[2] = 0;
@@ -715,8 +824,10 @@ struct KMeansRun {
   int iters;
 };
 
-static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h,
-                          const int64_t* forced_h, cudaStream_t st) {
+// All allocations of one k-means run (no stream work): done for every half
+// before any half is enqueued, so the enqueue loop never blocks in cudaMalloc.
+static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h, const int64_t* forced_h,
+                          cudaStream_t st) {
   BuildScratch& s = *r.s;
   const HalfView h = r.h;
   const int64_t n = h.n;
@@ -726,8 +837,7 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
   if (k > 256) TACO_FAIL(TACO_ERR_PARAMETER, "codebook size %d exceeds 256", k);
   const int64_t nbx = ceil_div(n, 256);
   const int64_t nbp = ceil_div(n, PP_BLOCK);
-  const int64_t nba = ceil_div(n, AS_THREADS);
-  const int64_t ntile = ceil_div(n, LT);
+  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
   TACO_TRY(s.xsq.ensure(8 * n));
   TACO_TRY(s.best.ensure(8 * n));
   TACO_TRY(s.bsum.ensure(8 * std::max(nbp, nbx)));
@@ -738,86 +848,114 @@ static int kmeans_enqueue(const KMeansRun& r, int64_t first, const double* uni_h
   TACO_TRY(s.C64.ensure(8 * (size_t)k * m));
   TACO_TRY(s.newlab.ensure(4 * n));
   TACO_TRY(s.pd.ensure(8 * n));
-  TACO_TRY(s.perm.ensure(8 * n));
-  TACO_TRY(s.lhist.ensure(4 * (size_t)ntile * k));
-  TACO_TRY(s.loff.ensure(8 * (size_t)ntile * k));
-  TACO_TRY(s.ctl.ensure(8 * k));       // counts
+  TACO_TRY(s.perm.ensure(4 * n));
+  TACO_TRY(s.keys2.ensure(4 * n));
+  TACO_TRY(s.ctl.ensure(8 * 2 * (size_t)k));   // per-cluster counts, double buffered by iteration parity
   TACO_TRY(s.hsum.ensure(8 * nba));
-  TACO_TRY(s.draws.ensure(8 * nbx));   // xsq block maxima
+  const int mp = (m + 3) & ~3;
+  TACO_TRY(s.xp.ensure(4 * (size_t)n * mp));
+  int lbits = 1;
+  while ((1 << lbits) < k) ++lbits;
+  size_t cub_bytes = 0;
+  TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
+                                                  lbits, st));
+  TACO_TRY(s.cubtmp.ensure(std::max<size_t>(cub_bytes, 16)));
+  if (s.iota.bytes < 4 * (size_t)n) {
+    TACO_TRY(s.iota.ensure(4 * n));
+    k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
+    TACO_LAUNCHED();
+  }
   if (s.leaves_n != n) {                // numpy pairwise leaves of an n-array (exact replay)
     std::vector<int64_t> lv;
     pairwise_leaves(0, n, lv);
     s.nleaves = (int64_t)lv.size() / 2;
     TACO_TRY(s.leaves.ensure(8 * lv.size()));
-    TACO_CHECK_CUDA(cudaMemcpy(s.leaves.p, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
     s.leaves_n = n;
   }
   TACO_TRY(s.pbuf.ensure(8 * std::max<int64_t>(n, s.nleaves)));
-  TACO_TRY(s.cbuf.ensure(std::max<size_t>(8 * n, 4 * (size_t)n * m)));   // replay cdf / sorted X
-  // xsq + its maximum (bound for the certified draw)
-  k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.draws.as<double>());
-  TACO_LAUNCHED();
-  std::vector<double> bm(nbx);
-  TACO_CHECK_CUDA(cudaMemcpyAsync(bm.data(), s.draws.p, 8 * nbx, cudaMemcpyDeviceToHost, st));
-  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
-  double xsqmax = 0.0;
-  for (double v : bm) xsqmax = std::max(xsqmax, v);
+  TACO_TRY(s.cbuf.ensure(8 * n));   // replay cdf
+  const size_t ash = sizeof(double) * ((size_t)k * m + k);
+  auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
+  if (ash > 48 * 1024)
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
+  const size_t css = sizeof(float) * CS_ST * CS_R * mp;
+  if (css > 48 * 1024)
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
+  // the draw plan (first pick, uniforms, forced draws) goes up before any
+  // kernel of the run is enqueued (the enqueue may be a graph capture)
   TACO_CHECK_CUDA(cudaMemcpyAsync(s.picks.p, &first, 8, cudaMemcpyHostToDevice, st));
   if (k > 1) {
     TACO_CHECK_CUDA(cudaMemcpyAsync(s.uni.p, uni_h, 8 * (k - 1), cudaMemcpyHostToDevice, st));
     if (forced_h)
       TACO_CHECK_CUDA(cudaMemcpyAsync(s.forced.p, forced_h, 8 * (k - 1), cudaMemcpyHostToDevice, st));
   }
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  return TACO_OK;
+}
+
+static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStream_t st, bool timing) {
+  BuildScratch& s = *r.s;
+  const HalfView h = r.h;
+  const int64_t n = h.n;
+  const int k = h.k;
+  const int m = h.m;
+  const int64_t nbx = ceil_div(n, 256);
+  const int64_t nbp = ceil_div(n, PP_BLOCK);
+  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
+  int lbits = 1;
+  while ((1 << lbits) < k) ++lbits;
   k_status_init<<<1, 1, 0, st>>>(s.status.as<int64_t>(), k);
   TACO_LAUNCHED();
+  // xsq + its maximum (bound for the certified draw)
+  k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.status.as<int64_t>());
+  TACO_LAUNCHED();
+  const int mp = (m + 3) & ~3;
+  k_point_major<<<(unsigned)nbx, 256, 0, st>>>(h, mp, s.xp.as<float>());
+  TACO_LAUNCHED();
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  if (getenv("TACO_DEBUG_TIMING")) {
+  if (timing) {
     for (auto& e : ev) cudaEventCreate(&e);
     cudaEventRecord(ev[0], st);
   }
   for (int ci = 0; ci < k; ++ci) {
-    k_pp_update<<<(unsigned)nbp, PP_THREADS, 0, st>>>(h, s.xsq.as<double>(), s.picks.as<int64_t>(), ci,
-                                                      s.best.as<double>(), s.C64.as<double>(),
-                                                      s.bsum.as<double>());
+    k_pp_step<<<(unsigned)nbp, PP_THREADS, 0, st>>>(h, s.xsq.as<double>(), ci, s.best.as<double>(),
+                                                    s.C64.as<double>(), s.bsum.as<double>(), nbp,
+                                                    s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
+                                                    s.picks.as<int64_t>(), s.status.as<int64_t>(),
+                                                    s.leaves.as<int64_t>(), s.nleaves, s.cbuf.as<double>(),
+                                                    s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
     TACO_LAUNCHED();
-    if (ci + 1 < k) {
-      k_pp_search<<<1, PS_THREADS, 0, st>>>(h, s.best.as<double>(), s.bsum.as<double>(), nbp,
-                                            s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
-                                            xsqmax, ci, s.picks.as<int64_t>(), s.status.as<int64_t>(),
-                                            s.leaves.as<int64_t>(), s.nleaves, s.cbuf.as<double>(),
-                                            s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
-      TACO_LAUNCHED();
-    }
   }
   if (ev[1]) cudaEventRecord(ev[1], st);
   const size_t ash = sizeof(double) * ((size_t)k * m + k);
-  auto* kas = m <= 8 ? k_assign<8> : m <= 16 ? k_assign<16> : k_assign<32>;
-  if (ash > 48 * 1024)
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
+  auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
+  unsigned long long* cnt = s.ctl.as<unsigned long long>();
+  TACO_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8 * 2 * (size_t)k, st));
+  const size_t css = sizeof(float) * CS_ST * CS_R * mp;
   for (int it = 0; it < r.iters; ++it) {
+    unsigned long long* cc = cnt + (size_t)(it & 1) * k;
+    unsigned long long* cn = cnt + (size_t)((it + 1) & 1) * k;
     kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,
                                                 s.newlab.as<int32_t>(), s.pd.as<double>(), it,
-                                                s.status.as<int64_t>(), s.hsum.as<double>());
+                                                s.status.as<int64_t>(), s.hsum.as<double>(), cc, cn);
     TACO_LAUNCHED();
     k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nba, it, s.status.as<int64_t>(), r.history,
                                     r.n_iter);
     TACO_LAUNCHED();
-    k_label_hist<<<(unsigned)ntile, 256, 0, st>>>(n, k, s.status.as<int64_t>(), s.newlab.as<int32_t>(),
-                                                  r.labels, s.lhist.as<int32_t>());
+    // stable sort of the point indices by label (index order inside a label)
+    size_t cb = s.cubtmp.bytes;
+    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(s.cubtmp.p, cb, reinterpret_cast<const uint32_t*>(s.newlab.p),
+                                                    s.keys2.as<uint32_t>(), s.iota.as<uint32_t>(),
+                                                    s.perm.as<uint32_t>(), (int64_t)n, 0, lbits, st));
+    count_launch(2);
+    k_cluster_sums<<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xp.as<float>(), mp, s.status.as<int64_t>(),
+                                                         s.perm.as<uint32_t>(), cc,
+                                                         r.labels, s.C64.as<double>());
     TACO_LAUNCHED();
-    k_label_offsets<<<1, 256, 0, st>>>(ntile, k, s.status.as<int64_t>(), s.lhist.as<int32_t>(),
-                                       s.loff.as<int64_t>(), s.ctl.as<int64_t>());
-    TACO_LAUNCHED();
-    k_label_scatter<<<(unsigned)ntile, 32, 0, st>>>(n, k, s.status.as<int64_t>(), r.labels,
-                                                    s.loff.as<int64_t>(), s.perm.as<int64_t>());
-    TACO_LAUNCHED();
-    k_gather_sorted<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(h, s.status.as<int64_t>(), s.perm.as<int64_t>(),
-                                                               s.cbuf.as<float>());
-    TACO_LAUNCHED();
-    k_cluster_sums<<<(unsigned)ceil_div((int64_t)k * m, 32), 32, 0, st>>>(
-        h, s.status.as<int64_t>(), s.cbuf.as<float>(), s.ctl.as<int64_t>(), s.C64.as<double>());
-    TACO_LAUNCHED();
-    k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), s.ctl.as<int64_t>(), s.pd.as<double>(),
+    k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), cc, s.pd.as<double>(),
                                  r.labels, s.C64.as<double>());
     TACO_LAUNCHED();
   }
@@ -884,28 +1022,16 @@ __global__ void k_cell_sizes(const uint32_t* __restrict__ chist, int K2, int64_t
   gsize[e] = s;
 }
 
-// one warp per chunk: stable scatter of ascending ids into their cells
-__global__ void k_cell_scatter(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2,
-                               int64_t n, int kp, int64_t chunk, uint32_t* __restrict__ cursor,
-                               uint32_t* __restrict__ ids) {
-  const int lane = threadIdx.x;
-  const int64_t c = blockIdx.x;
-  const int K2 = kp * kp;
-  uint32_t* cur = cursor + (size_t)c * K2;
-  const int64_t i0 = c * chunk;
-  const int64_t i1 = min(n, i0 + chunk);
-  for (int64_t r = i0; r < i1; r += 32) {
-    const int64_t i = r + lane;
-    const bool live = i < i1;
-    const int key = live ? l1[i] * kp + l2[i] : -1;
-    const unsigned act = __ballot_sync(0xffffffffu, live);
-    const unsigned grp = __match_any_sync(0xffffffffu, key) & act;
-    uint32_t base = 0;
-    const int leader = live ? __ffs(grp) - 1 : 0;
-    if (live && lane == leader) base = atomicAdd(&cur[key], (uint32_t)__popc(grp));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (live) ids[base + __popc(grp & ((1u << lane) - 1u))] = (uint32_t)i;
-  }
+// sort keys for the CSR: (chunk, cell) of every local id; values = the id.
+// A stable radix sort of ascending ids by this key is the (chunk, cell, id)
+// order the counting kernels read (imi.py:72-81 lexsort((arange, l2, l1)),
+// chunk-major).
+__global__ void k_cell_keys(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2, int64_t n,
+                            int kp, int64_t chunk, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (uint32_t)((i / chunk) * kp * kp + l1[i] * kp + l2[i]);
+  vals[i] = (uint32_t)i;
 }
 
 }  // namespace taco
@@ -918,7 +1044,11 @@ int ensure_half_streams(taco_index* idx, int want) {
     cudaStream_t s;
     TACO_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     idx->half_streams.push_back(s);
+    cudaEvent_t e;
+    TACO_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    idx->half_ev.push_back(e);
   }
+  if (!idx->km_fork) TACO_CHECK_CUDA(cudaEventCreateWithFlags(&idx->km_fork, cudaEventDisableTiming));
   return TACO_OK;
 }
 }  // namespace
@@ -942,9 +1072,8 @@ static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, d
     *bad_row = b == ~0ull ? -1 : (int64_t)b;
     if (b != ~0ull) break;
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_colmean_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * CM_TILE_BYTES));
-    k_colmean_seq<<<(unsigned)ceil_div(d, CM_THREADS), CM_THREADS, 2 * CM_TILE_BYTES, st>>>(Xd, n, d,
-                                                                                          mean.as<double>());
+                                         (int)CM_SMEM));
+    k_colmean_seq<<<(unsigned)ceil_div(d, CM_W), CM_THREADS, CM_SMEM, st>>>(Xd, n, d, mean.as<double>());
     count_launch();
     const int tiles = (int)ceil_div(d, GT);
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(592, tiles * tiles), ceil_div(n, 256)));
@@ -1004,6 +1133,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   std::vector<int64_t> status_h(8);
   for (int w0 = 0; w0 < H; w0 += NS) {
     const int w1 = std::min(H, w0 + NS);
+    std::vector<KMeansRun> runs;
     for (int hh = w0; hh < w1; ++hh) {
       const int j = hh / 2, b = hh % 2;
       KMeansRun r;
@@ -1018,10 +1148,49 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
       r.n_iter = idx->niter.as<int32_t>() + hh;
       r.cent_out = b ? idx->cb2.as<float>() + (size_t)j * kp * idx->m2 : idx->cb1.as<float>() + (size_t)j * kp * idx->m1;
       r.iters = idx->iters;
-      TACO_TRY(kmeans_enqueue(r, first_h[hh], uniforms_h + (size_t)hh * std::max(kp - 1, 0),
+      TACO_TRY(kmeans_prepare(r, first_h[hh], uniforms_h + (size_t)hh * std::max(kp - 1, 0),
                               forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr,
                               idx->half_streams[hh - w0]));
+      runs.push_back(r);
     }
+    // All halves of the wave are independent: their ~300 launches each are
+    // captured once into one graph with a branch per half (fork/join through
+    // events), so the host enqueue cost is paid at capture speed and the GPU
+    // sees every half at once.  TACO_KM_GRAPH=0 launches them directly.
+    const char* ge = getenv("TACO_KM_GRAPH");
+    const bool timing = getenv("TACO_DEBUG_TIMING") != nullptr;
+    const bool graph = !(ge && ge[0] == '0') && !timing;
+    cudaStream_t origin = idx->stream;
+    cudaGraph_t g = nullptr;
+    if (graph) {
+      TACO_CHECK_CUDA(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
+      TACO_CHECK_CUDA(cudaEventRecord(idx->km_fork, origin));
+    }
+    int erc = TACO_OK;
+    for (int hh = w0; hh < w1 && erc == TACO_OK; ++hh) {
+      cudaStream_t hs = idx->half_streams[hh - w0];
+      if (graph) cudaStreamWaitEvent(hs, idx->km_fork, 0);
+      erc = kmeans_enqueue(runs[hh - w0], forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr, hs,
+                           timing);
+      if (graph) {
+        cudaEventRecord(idx->half_ev[hh - w0], hs);
+        cudaStreamWaitEvent(origin, idx->half_ev[hh - w0], 0);
+      }
+    }
+    if (graph) {
+      cudaError_t ce = cudaStreamEndCapture(origin, &g);
+      if (erc != TACO_OK) { if (g) cudaGraphDestroy(g); return erc; }
+      if (ce != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "k-means graph capture: %s", cudaGetErrorString(ce));
+      cudaGraphExec_t ex = nullptr;
+      TACO_CHECK_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      cudaError_t le = cudaGraphLaunch(ex, origin);
+      cudaError_t se = cudaStreamSynchronize(origin);
+      cudaGraphExecDestroy(ex);
+      if (le != cudaSuccess || se != cudaSuccess)
+        TACO_FAIL(TACO_ERR_CUDA, "k-means graph: %s", cudaGetErrorString(le != cudaSuccess ? le : se));
+    }
+    TACO_TRY(erc);
     for (int hh = w0; hh < w1; ++hh) {
       cudaStream_t st = idx->half_streams[hh - w0];
       TACO_CHECK_CUDA(cudaMemcpyAsync(status_h.data(), idx->bs[hh - w0].status.p, 8 * 5, cudaMemcpyDeviceToHost, st));
@@ -1037,6 +1206,14 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
         for (auto& e : bs.ev) { cudaEventDestroy(e); e = nullptr; }
       }
     }
+  }
+  // the scratch goes back to the device pool (a later build reuses it)
+  for (auto& bs : idx->bs) {
+    DevBuf* sb[] = {&bs.xsq, &bs.best, &bs.bsum, &bs.picks, &bs.uni, &bs.forced, &bs.status, &bs.C64, &bs.csq,
+                    &bs.newlab, &bs.pd, &bs.changed, &bs.perm, &bs.lhist, &bs.loff, &bs.ctl, &bs.hsum, &bs.draws,
+                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp};
+    for (auto* b : sb) b->release();
+    bs.leaves_n = -1;
   }
   idx->has_cb = true;
   idx->has_labels = true;
@@ -1054,9 +1231,18 @@ int taco_build_cells(taco_index* idx) {
   TACO_TRY(idx->ids.ensure(sizeof(uint32_t) * (size_t)n * idx->n_sub));
   TACO_TRY(idx->offs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
   TACO_TRY(idx->gsize.ensure(sizeof(int64_t) * (size_t)K2 * idx->n_sub));
-  DevBuf chist, cursor;
+  DevBuf chist, keys, keys2, vals, tmp;
   TACO_TRY(chist.ensure(sizeof(uint32_t) * (size_t)nc * K2));
-  TACO_TRY(cursor.ensure(sizeof(uint32_t) * (size_t)nc * K2));
+  TACO_TRY(keys.ensure(sizeof(uint32_t) * (size_t)n));
+  TACO_TRY(keys2.ensure(sizeof(uint32_t) * (size_t)n));
+  TACO_TRY(vals.ensure(sizeof(uint32_t) * (size_t)n));
+  int bits = 1;
+  while (bits < 32 && ((uint64_t)1 << bits) < (uint64_t)nc * K2) ++bits;
+  size_t tmp_bytes = 0;
+  TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                                  vals.as<uint32_t>(), idx->ids.as<uint32_t>(), (int64_t)n, 0,
+                                                  bits, st));
+  TACO_TRY(tmp.ensure(std::max<size_t>(tmp_bytes, 16)));
   for (int j = 0; j < idx->n_sub; ++j) {
     const int32_t* l1 = idx->labels.as<int32_t>() + (size_t)(2 * j) * n;
     const int32_t* l2 = idx->labels.as<int32_t>() + (size_t)(2 * j + 1) * n;
@@ -1071,14 +1257,18 @@ int taco_build_cells(taco_index* idx) {
                                                                idx->gsize.as<int64_t>() + (size_t)j * K2);
       TACO_LAUNCHED();
     }
-    TACO_CHECK_CUDA(cudaMemcpyAsync(cursor.p, offs, sizeof(uint32_t) * (size_t)nc * K2, cudaMemcpyDeviceToDevice, st));
-    k_cell_scatter<<<(unsigned)nc, 32, 0, st>>>(l1, l2, n, kp, idx->chunk, cursor.as<uint32_t>(),
-                                                idx->ids.as<uint32_t>() + (size_t)j * n);
+    k_cell_keys<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(l1, l2, n, kp, idx->chunk, keys.as<uint32_t>(),
+                                                            vals.as<uint32_t>());
     TACO_LAUNCHED();
+    size_t tb = tmp.bytes;
+    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                                    vals.as<uint32_t>(), idx->ids.as<uint32_t>() + (size_t)j * n,
+                                                    (int64_t)n, 0, bits, st));
+    count_launch(bits <= 8 ? 2 : 1 + (bits + 7) / 8);
   }
   cudaError_t e = cudaStreamSynchronize(st);
   chist.release();
-  cursor.release();
+  keys.release(); keys2.release(); vals.release(); tmp.release();
   if (e != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e));
   idx->has_cells = true;
   if (idx->n_global == idx->n) idx->has_gsize = true;
@@ -1143,7 +1333,8 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
     r.n_iter = nit.as<int32_t>();
     r.cent_out = cent.as<float>();
     r.iters = max_iter;
-    if ((rc = kmeans_enqueue(r, first, uniforms_h, forced_h, st))) break;
+    if ((rc = kmeans_prepare(r, first, uniforms_h, forced_h, st)) || (rc = kmeans_enqueue(r, forced_h, st, false)))
+      break;
     std::vector<int64_t> status(5);
     cudaMemcpy(status.data(), s.status.p, 8 * 5, cudaMemcpyDeviceToHost);
     cudaMemcpy(centroids_h, cent.p, 4 * (size_t)k * m, cudaMemcpyDeviceToHost);
@@ -1156,7 +1347,7 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
   X.release(); lab.release(); hist.release(); nit.release(); cent.release();
   DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
                   &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws,
-                  &s.leaves, &s.pbuf, &s.cbuf};
+                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp};
   for (auto* b : sb) b->release();
   return rc;
 }

@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <mutex>
+#include <omp.h>
 #include <vector>
 
 #include "index.cuh"
@@ -22,13 +24,33 @@ void set_error(const char* fmt, ...) {
 
 void count_launch(int n) { g_launches += n; }
 
+// Device memory comes from the device's stream-ordered pool with an unbounded
+// release threshold: freed blocks stay cached in the pool, so the scratch of a
+// second build (or a resized query tile) is a pool hit instead of a
+// cudaMalloc.  Allocation and free are issued on the legacy stream and
+// completed before returning; release() first waits for all device work, which
+// is the guarantee cudaFree gave the callers.
+static void pool_setup() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done_dev = dev;
+}
+
 int DevBuf::ensure(size_t want) {
   if (want <= bytes && p) return TACO_OK;
-  if (p) cudaFree(p);
-  p = nullptr;
-  bytes = 0;
+  release();
   size_t b = want < 256 ? 256 : want;
-  TACO_CHECK_CUDA(cudaMalloc(&p, b));
+  pool_setup();
+  TACO_CHECK_CUDA(cudaMallocAsync(&p, b, cudaStreamLegacy));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   bytes = b;
   return TACO_OK;
 }
@@ -44,7 +66,11 @@ void QueryTile::release() {
 }
 
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) {
+    cudaDeviceSynchronize();
+    cudaFreeAsync(p, cudaStreamLegacy);
+    cudaStreamSynchronize(cudaStreamLegacy);
+  }
   p = nullptr;
   bytes = 0;
 }
@@ -218,10 +244,12 @@ int taco_index_destroy(taco_index* idx) {
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
                     &s.csq, &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl,
-                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf};
+                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp};
     for (auto* b : sb) b->release();
   }
   for (auto st : idx->half_streams) cudaStreamDestroy(st);
+  for (auto e : idx->half_ev) cudaEventDestroy(e);
+  if (idx->km_fork) cudaEventDestroy(idx->km_fork);
   if (idx->stream2) cudaStreamDestroy(idx->stream2);
   if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
   if (idx->ev_join) cudaEventDestroy(idx->ev_join);
@@ -299,12 +327,60 @@ static int narrow_rows(taco_index* idx) {
 }
 }  // namespace taco
 
+namespace taco {
+// Host -> device upload of a pageable buffer (the numpy base vectors) through
+// a ring of pinned staging buffers: the host threads copy chunk i+1 into one
+// buffer while the DMA engine drains chunk i from another, so the upload runs
+// at min(host memcpy, PCIe) instead of the driver's single-threaded pageable
+// path.  Already-pinned sources go straight to cudaMemcpyAsync.
+constexpr size_t kStageBytes = 32u << 20;
+constexpr int kStages = 3;
+static std::mutex g_stage_mu;
+static char* g_stage[kStages] = {nullptr, nullptr, nullptr};
+static cudaEvent_t g_stage_ev[kStages] = {nullptr, nullptr, nullptr};
+
+int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaPointerAttributes pa;
+  const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned || bytes <= 2 * kStageBytes) {
+    TACO_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+    return TACO_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (int b = 0; b < kStages; ++b) {
+    if (!g_stage[b]) {
+      TACO_CHECK_CUDA(cudaHostAlloc((void**)&g_stage[b], kStageBytes, cudaHostAllocDefault));
+      TACO_CHECK_CUDA(cudaEventCreateWithFlags(&g_stage_ev[b], cudaEventDisableTiming));
+    }
+  }
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  int nthr = std::min(16, omp_get_num_procs());
+  for (size_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
+    const int b = (int)(i % kStages);
+    const size_t len = std::min(kStageBytes, bytes - off);
+    TACO_CHECK_CUDA(cudaEventSynchronize(g_stage_ev[b]));   // buffer b drained
+    char* stg = g_stage[b];
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (int t = 0; t < 64; ++t) {
+      const size_t a0 = len * t / 64, a1 = len * (t + 1) / 64;
+      memcpy(stg + a0, s + off + a0, a1 - a0);
+    }
+    TACO_CHECK_CUDA(cudaMemcpyAsync(d + off, stg, len, cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaEventRecord(g_stage_ev[b], st));
+  }
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  return TACO_OK;
+}
+}  // namespace taco
+
 int taco_index_set_data(taco_index* idx, const float* X_h) {
   TACO_TRY(index_check(idx));
   size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
   TACO_TRY(idx->X.ensure(bytes));
-  TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_h, bytes, cudaMemcpyHostToDevice, idx->stream));
-  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  TACO_TRY(upload_h2d(idx->X.p, X_h, bytes, idx->stream));
   idx->has_X = true;
   return narrow_rows(idx);
 }

@@ -48,7 +48,7 @@ struct QueryTile {
 
 struct BuildScratch {
   DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
-      loff, ctl, hsum, draws, leaves, pbuf, cbuf;
+      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp;
   int64_t nleaves = 0, leaves_n = -1;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // TACO_DEBUG_TIMING
 };
@@ -68,6 +68,8 @@ struct taco_index {
   bool has_X = false, has_T = false, has_model = false, has_cb = false, has_labels = false,
        has_cells = false, has_gsize = false;
   std::vector<cudaStream_t> half_streams;
+  std::vector<cudaEvent_t> half_ev;   // k-means graph join, one per half stream
+  cudaEvent_t km_fork = nullptr;
   taco::QueryTile qt, qt2;      // two query tiles: the batch loop pipelines them on two streams
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
