@@ -10,8 +10,6 @@ sequential per-cluster sums (build.cu).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
 import numpy as np
 
 from . import _native as nat
@@ -21,13 +19,30 @@ MAX_HALF_DIM = 32
 MAX_CLUSTERS = 256
 
 
-@dataclass(frozen=True)
 class KMeansModel:
-    centroids: np.ndarray             # (k, m) float32
-    assignments: np.ndarray | None    # (n,) int32; None for models loaded from disk
-    inertia: float
-    inertia_history: tuple = ()
-    n_iter: int = 0
+    """Fitted codebook (reference clustering.py:17-31).
+
+    ``assignments`` may be supplied lazily through ``loader`` (a callable
+    returning the int32 labels): a device-built index keeps its labels in HBM
+    and copies them to the host only when a caller first reads them."""
+
+    __slots__ = ("centroids", "_assignments", "_loader", "inertia", "inertia_history", "n_iter")
+
+    def __init__(self, centroids, assignments=None, inertia: float = float("nan"),
+                 inertia_history: tuple = (), n_iter: int = 0, *, loader=None):
+        self.centroids = centroids
+        self._assignments = assignments
+        self._loader = loader
+        self.inertia = inertia
+        self.inertia_history = inertia_history
+        self.n_iter = n_iter
+
+    @property
+    def assignments(self):
+        if self._assignments is None and self._loader is not None:
+            self._assignments = self._loader()
+            self._loader = None
+        return self._assignments
 
     @property
     def n_clusters(self) -> int:
@@ -36,6 +51,10 @@ class KMeansModel:
     @property
     def dim(self) -> int:
         return self.centroids.shape[1]
+
+    def __repr__(self):
+        return (f"KMeansModel(n_clusters={self.n_clusters}, dim={self.dim}, inertia={self.inertia!r}, "
+                f"n_iter={self.n_iter})")
 
 
 def draw_plan(n: int, k: int, seed: int):

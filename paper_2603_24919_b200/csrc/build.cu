@@ -39,6 +39,36 @@ __global__ void k_nonfinite(const float* __restrict__ X, int64_t total, int d,
 // column), warps 1..3 stream the slab's rows into an 8-stage shared-memory
 // ring with cp.async (16-byte pieces when the slab is 16-byte aligned) so the
 // chain never waits on HBM.  One __syncthreads per 128-row stage.
+// One dependent fp64 add chain over rr floats at stride `st` in shared memory
+// (acc += x_0, acc += x_1, ... in order).  Values are pulled into registers
+// 64 at a time (both 32-halves issued before the first add), so the chain
+// waits on LDS latency once per 64 adds and otherwise runs at the DADD
+// latency (11 cycles on B200).
+__device__ __forceinline__ double chain_add(double acc, const float* __restrict__ tv, int rr, int st) {
+  int q = 0;
+  for (; q + 64 <= rr; q += 64) {
+    float a[32], b[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) a[u] = tv[(q + u) * st];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) b[u] = tv[(q + 32 + u) * st];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, (double)a[u]);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, (double)b[u]);
+  }
+  if (q + 32 <= rr) {
+    float a[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) a[u] = tv[(q + u) * st];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, (double)a[u]);
+    q += 32;
+  }
+  for (; q < rr; ++q) acc = __dadd_rn(acc, (double)tv[q * st]);
+  return acc;
+}
+
 constexpr int CM_W = 32;          // columns per CTA
 constexpr int CM_ROWS = 128;      // rows per stage
 constexpr int CM_STAGES = 8;
@@ -95,19 +125,8 @@ __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restr
     } else if (tid < nc) {
       const float* tv = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W + tid;
       const int rr = (int)min((int64_t)CM_ROWS, n - tb * CM_ROWS);
-      int r = 0;
-      if (tb == 0) { acc = (double)tv[0]; r = 1; }
-      if (rr == CM_ROWS) {
-        for (; r < CM_ROWS; r += 8) {   // r = 0 or 1 at entry: the 8-blocks may start at 1
-          if (r + 8 > CM_ROWS) break;
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = tv[(r + u) * CM_W];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
-        }
-      }
-      for (; r < rr; ++r) acc = __dadd_rn(acc, (double)tv[r * CM_W]);
+      if (tb == 0) acc = chain_add((double)tv[0], tv + CM_W, rr - 1, CM_W);
+      else acc = chain_add(acc, tv, rr, CM_W);
     }
   }
   if (tid < nc) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
@@ -179,12 +198,23 @@ __global__ void k_gram_reduce(const double* __restrict__ partial, int splits, in
 }
 
 // ================================================================ k-means
-constexpr int PP_THREADS = 1024;
-constexpr int PP_PPT = 1;                       // points per thread in one block
+constexpr int PP_THREADS = 256;
+constexpr int PP_PPT = 4;                       // points per thread in one block
 constexpr int PP_BLOCK = PP_THREADS * PP_PPT;   // points per block-sum
 constexpr double U0 = 1.1102230246251565e-16;   // 2^-53
 
 static int g_force_replay = 0;   // test hook: always take the exact replay
+
+static int g_num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 struct HalfView {
   const float* X;   // dimension-major: X[t*n + i]
@@ -286,7 +316,6 @@ __device__ double np_combine(const double* leaf, int64_t n) {
 // that numpy's sequential cumsum/normalise/searchsorted (the reference's
 // Generator.choice, clustering.py:48) cannot land elsewhere.  Otherwise
 // replay numpy's arithmetic exactly (single thread).
-constexpr int PS_THREADS = 1024;
 constexpr int PS_TILE = 2048;   // doubles per staged tile of the replay chain
 __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restrict__ best,
                                                           const double* __restrict__ bsum, int64_t nb,
@@ -303,13 +332,14 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   __shared__ int64_t s_blk;
   __shared__ double s_before;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
   const int draw = ci + 1;                 // centroid index being chosen
   if (forced && forced[ci] >= 0) {
     if (tid == 0) picks[draw] = forced[ci];
     return;
   }
   // per-thread contiguous block-sum ranges, then a block scan (fixed order)
-  const int64_t per = (nb + PS_THREADS - 1) / PS_THREADS;
+  const int64_t per = (nb + NT - 1) / NT;
   const int64_t a0 = (int64_t)tid * per, a1 = min(nb, a0 + per);
   double loc = 0.0;
   for (int64_t b = a0; b < a1; ++b) loc = __dadd_rn(loc, __ldcg(bsum + b));
@@ -321,7 +351,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   if (lane == 31) wsum[wid] = v;
   __syncthreads();
   if (wid == 0) {
-    double w = wsum[lane];
+    double w = lane < NW ? wsum[lane] : 0.0;
     for (int o = 1; o < 32; o <<= 1) {
       double x = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w = __dadd_rn(w, x);
@@ -365,11 +395,22 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   const double pre = s_blk >= 0 ? s_before : S - __ldcg(bsum + blk);
   const int64_t i0 = blk * PP_BLOCK, i1 = min(h.n, i0 + PP_BLOCK);
   {
-    // in-block inclusive prefix of best[] (a fp64 tree scan: error well
-    // inside the certified budget below), then the first crossing
-    static_assert(PS_THREADS == PP_BLOCK, "one thread per point of the block");
-    const double x = i0 + tid < i1 ? __ldcg(best + i0 + tid) : 0.0;
-    double sv = x;
+    // in-block inclusive prefix of best[] (PP_BLOCK / NT consecutive values
+    // per thread, then a block scan of the thread totals: a fp64 tree whose
+    // error is far inside the certified budget below), then the first crossing
+    constexpr int VPT_MAX = 8;
+    const int vpt = PP_BLOCK / NT;
+    double loc2[VPT_MAX];
+    double tsum = 0.0;
+#pragma unroll
+    for (int e = 0; e < VPT_MAX; ++e) {
+      if (e < vpt) {
+        const int64_t i = i0 + (int64_t)tid * vpt + e;
+        tsum = __dadd_rn(tsum, i < i1 ? __ldcg(best + i) : 0.0);
+        loc2[e] = tsum;
+      }
+    }
+    double sv = tsum;
     for (int o = 1; o < 32; o <<= 1) {
       const double y = __shfl_up_sync(0xffffffffu, sv, o);
       if (lane >= o) sv = __dadd_rn(sv, y);
@@ -379,7 +420,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
     if (tid == 0) s_k = PP_BLOCK;
     __syncthreads();
     if (wid == 0) {
-      double w = wsum[lane];
+      double w = lane < NW ? wsum[lane] : 0.0;
       for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_up_sync(0xffffffffu, w, o);
         if (lane >= o) w = __dadd_rn(w, y);
@@ -387,9 +428,18 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
       wsum[lane] = w;
     }
     __syncthreads();
-    if (wid) sv = __dadd_rn(sv, wsum[wid - 1]);
-    s_scan[tid] = sv;
-    if (i0 + tid < i1 && __dadd_rn(pre, sv) > target) atomicMin(&s_k, tid);
+    const double prevlane = __shfl_up_sync(0xffffffffu, sv, 1);   // warp-inclusive prefix of lane - 1
+    const double wbase = wid ? wsum[wid - 1] : 0.0;
+    const double base = lane ? __dadd_rn(wbase, prevlane) : wbase;
+#pragma unroll
+    for (int e = 0; e < VPT_MAX; ++e) {
+      if (e < vpt) {
+        const int j = tid * vpt + e;
+        const double pv = __dadd_rn(base, loc2[e]);
+        s_scan[j] = pv;
+        if (i0 + j < i1 && __dadd_rn(pre, pv) > target) atomicMin(&s_k, j);
+      }
+    }
     __syncthreads();
   }
   if (tid == 0) {
@@ -426,12 +476,12 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   // total = numpy pairwise sum; p = best/total; cdf = sequential cumsum;
   // idx = first i with fl(cdf_i / cdf_last) > u.  Everything but the cumsum
   // chain runs on all threads of the block.
-  for (int64_t l = tid; l < nleaves; l += PS_THREADS) lsum[l] = np_leaf(best + leaves[2 * l], leaves[2 * l + 1]);
+  for (int64_t l = tid; l < nleaves; l += NT) lsum[l] = np_leaf(best + leaves[2 * l], leaves[2 * l + 1]);
   __syncthreads();
   if (tid == 0) s_total = np_combine(lsum, h.n);
   __syncthreads();
   const double total = s_total;
-  for (int64_t i = tid; i < h.n; i += PS_THREADS) pbuf[i] = __ddiv_rn(__ldcg(best + i), total);
+  for (int64_t i = tid; i < h.n; i += NT) pbuf[i] = __ddiv_rn(__ldcg(best + i), total);
   __syncthreads();
   // The sequential cumsum chain runs once on thread 0 over shared-memory tiles
   // that the rest of the block streams in (double buffered) and writes back
@@ -439,7 +489,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   __shared__ double tile[2][PS_TILE];
   __shared__ double s_c;
   const int64_t ntile = (h.n + PS_TILE - 1) / PS_TILE;
-  for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += PS_THREADS) tile[0][i] = pbuf[i];
+  for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += NT) tile[0][i] = pbuf[i];
   if (tid == 0) s_c = 0.0;
   __syncthreads();
   for (int64_t tb = 0; tb < ntile; ++tb) {
@@ -448,11 +498,11 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
       // write back the previous tile's cdf, prefetch the next tile
       if (tb > 0) {
         const int64_t pb0 = (tb - 1) * PS_TILE;
-        for (int64_t i = tid - 32; i < PS_TILE && pb0 + i < h.n; i += PS_THREADS - 32)
+        for (int64_t i = tid - 32; i < PS_TILE && pb0 + i < h.n; i += NT - 32)
           cbuf[pb0 + i] = tile[(tb + 1) & 1][i];
       }
       __syncwarp();
-      for (int64_t i = tid - 32; i < PS_TILE && nb0 + i < h.n; i += PS_THREADS - 32)
+      for (int64_t i = tid - 32; i < PS_TILE && nb0 + i < h.n; i += NT - 32)
         tile[(tb + 1) & 1][i] = pbuf[nb0 + i];
     } else if (tid == 0) {
       double* tv = tile[tb & 1];
@@ -476,7 +526,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   }
   {
     const int64_t pb0 = (ntile - 1) * PS_TILE;
-    for (int64_t i = tid; i < PS_TILE && pb0 + i < h.n; i += PS_THREADS) cbuf[pb0 + i] = tile[(ntile - 1) & 1][i];
+    for (int64_t i = tid; i < PS_TILE && pb0 + i < h.n; i += NT) cbuf[pb0 + i] = tile[(ntile - 1) & 1][i];
   }
   __syncthreads();
   if (tid == 0) {
@@ -502,9 +552,14 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
 }
 
 // One k-means++ draw in one launch: the D^2 update for centroid ci and the
-// block sums (every block), then the last block to finish (atomic ticket in
-// status[6]) chooses picks[ci+1] with the certified search above.
-__global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const double* __restrict__ xsq, int ci,
+// per-1024-point block sums, then the last CTA to finish (atomic ticket in
+// status[6]) chooses picks[ci+1] with the certified search above.  The grid
+// is persistent and sized so the concurrent halves share the SMs; a CTA of
+// 256 threads walks its 1024-point blocks, 4 points per thread, reading each
+// point's coordinates as float4s from the point-major copy.
+template <int MP>
+__global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const float* __restrict__ xp,
+                                                        const double* __restrict__ xsq, int ci,
                                                         double* __restrict__ best, double* __restrict__ C64,
                                                         double* __restrict__ bsum, int64_t nb,
                                                         const double* __restrict__ uni,
@@ -513,50 +568,71 @@ __global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const double
                                                         const int64_t* __restrict__ leaves, int64_t nleaves,
                                                         double* __restrict__ lsum, double* __restrict__ pbuf,
                                                         double* __restrict__ cbuf, int force_replay) {
-  __shared__ double cv[64];
+  __shared__ double cv[MP];
   __shared__ double red[PP_THREADS / 32];
   __shared__ double s_csq;
   __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int m = h.m;
   const int64_t p = __ldcg(picks + ci);
-  if (threadIdx.x < h.m) cv[threadIdx.x] = (double)h.X[(size_t)threadIdx.x * h.n + p];
+  if (tid < MP) cv[tid] = tid < m ? (double)xp[(size_t)p * MP + tid] : 0.0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    s_csq = einsum_sq([&](int t) { return cv[t]; }, h.m);
+  if (tid == 0) {
+    s_csq = einsum_sq([&](int t) { return cv[t]; }, m);
     if (blockIdx.x == 0)
-      for (int t = 0; t < h.m; ++t) C64[(size_t)ci * h.m + t] = cv[t];
+      for (int t = 0; t < m; ++t) C64[(size_t)ci * m + t] = cv[t];
   }
   __syncthreads();
   const double csq = s_csq;
-  const int64_t i = (int64_t)blockIdx.x * PP_BLOCK + threadIdx.x;
-  double s = 0.0;
-  if (i < h.n) {
-    const double dot = dot_fma([&](int t) { return (double)h.X[(size_t)t * h.n + i]; },
-                               [&](int t) { return cv[t]; }, h.m);
-    const double d2 = sq_dist_expand(xsq[i], dot, csq);
-    double b = d2;
-    if (ci > 0) {
-      const double old = best[i];
-      b = d2 < old ? d2 : old;
-      if (d2 < old) best[i] = b;
-    } else {
-      best[i] = b;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    double part = 0.0;
+#pragma unroll
+    for (int u = 0; u < PP_PPT; ++u) {
+      const int64_t i = b * PP_BLOCK + (int64_t)u * PP_THREADS + tid;
+      if (i < h.n) {
+        const float4* src = reinterpret_cast<const float4*>(xp + (size_t)i * MP);
+        float xv[MP];
+#pragma unroll
+        for (int q = 0; q < MP / 4; ++q) {
+          const float4 v = __ldcs(src + q);
+          xv[4 * q] = v.x; xv[4 * q + 1] = v.y; xv[4 * q + 2] = v.z; xv[4 * q + 3] = v.w;
+        }
+        double dot = 0.0;
+#pragma unroll
+        for (int t = 0; t < MP; ++t)
+          if (t < m) dot = __fma_rn((double)xv[t], cv[t], dot);
+        // xsq recomputed in the einsum order of k_xsq (bit-identical) instead of an 8 B/point read
+        const double xs = einsum_sq([&](int t) { return (double)xv[t]; }, m);
+        const double d2 = sq_dist_expand(xs, dot, csq);
+        double bb = d2;
+        if (ci > 0) {
+          const double old = best[i];
+          if (d2 < old) best[i] = d2; else bb = old;
+        } else {
+          best[i] = d2;
+        }
+        part = __dadd_rn(part, bb);
+      }
     }
-    s = b;
+    for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if (lane == 0) red[wid] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
+      bsum[b] = t;
+    }
+    __syncthreads();
   }
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
-    bsum[blockIdx.x] = t;
+  if (tid == 0) {
     __threadfence();
-    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 6), 1ull) == (unsigned long long)(nb - 1);
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 6), 1ull) ==
+             (unsigned long long)(gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x == 0) status[6] = 0;   // ticket for the next draw (stream-ordered launch)
+  if (tid == 0) status[6] = 0;   // ticket for the next draw (stream-ordered launch)
   if (ci + 1 < h.k)
     pp_search_body(h, best, bsum, nb, uni, forced, ci, picks, status, leaves, nleaves, lsum, pbuf, cbuf,
                    force_replay);
@@ -708,36 +784,41 @@ __global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const f
   const int64_t ntile = (cnt + CS_R - 1) / CS_R;
   const int SL = CS_R * mp;
   const int r = tid - 32;   // producer: point r of every stage
-  auto load = [&](int64_t tb) {
+  // perm index of this producer's point in tile tb (issued one stage before
+  // its gather, so the gather never waits on the index load)
+  auto pidx = [&](int64_t tb) -> uint32_t {
+    return (tb < ntile && tb * CS_R + r < cnt) ? pp[tb * CS_R + r] : 0u;
+  };
+  uint32_t pnext = 0;
+  auto load = [&](int64_t tb, uint32_t p) {
     if (tb < ntile && tb * CS_R + r < cnt) {
       float* dst = cs + (size_t)(tb % CS_ST) * SL + r * mp;
-      const uint32_t p = pp[tb * CS_R + r];
       const float* src = xp + (size_t)p * mp;   // the point's m coordinates: one 32-byte sector for m <= 8
       for (int q = 0; q < mp; q += 4) cp_async16(dst + q, src + q);
       lab[p] = c;
     }
     cp_commit();
   };
-  if (tid >= 32)
-    for (int st = 0; st < CS_ST - 1; ++st) load(st);
+  if (tid >= 32) {
+    uint32_t pi[CS_ST - 1];
+#pragma unroll
+    for (int st = 0; st < CS_ST - 1; ++st) pi[st] = pidx(st);
+#pragma unroll
+    for (int st = 0; st < CS_ST - 1; ++st) load(st, pi[st]);
+    pnext = pidx(CS_ST - 1);
+  }
   double acc = 0.0;
   for (int64_t tb = 0; tb < ntile; ++tb) {
     if (tid >= 32) cp_wait<CS_ST - 2>();
     __syncthreads();
     if (tid >= 32) {
-      load(tb + CS_ST - 1);
+      const uint32_t pcur = pnext;
+      pnext = pidx(tb + CS_ST);
+      load(tb + CS_ST - 1, pcur);
     } else if (tid < m) {
       const float* tv = cs + (size_t)(tb % CS_ST) * SL + tid;
       const int rr = (int)min((int64_t)CS_R, cnt - tb * CS_R);
-      int q = 0;
-      for (; q + 8 <= rr; q += 8) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = tv[(q + u) * mp];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, (double)v[u]);
-      }
-      for (; q < rr; ++q) acc = __dadd_rn(acc, (double)tv[q * mp]);
+      acc = chain_add(acc, tv, rr, mp);
     }
   }
   if (tid < m) C64[(size_t)c * m + tid] = __ddiv_rn(acc, (double)cnt);
@@ -822,6 +903,7 @@ struct KMeansRun {
   int32_t* n_iter;     // 1 (device)
   float* cent_out;     // k*m (device)
   int iters;
+  int concurrent = 1;  // halves running at once: each k-means++ draw takes sms/concurrent CTAs
 };
 
 // All allocations of one k-means run (no stream work): done for every half
@@ -852,7 +934,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   TACO_TRY(s.keys2.ensure(4 * n));
   TACO_TRY(s.ctl.ensure(8 * 2 * (size_t)k));   // per-cluster counts, double buffered by iteration parity
   TACO_TRY(s.hsum.ensure(8 * nba));
-  const int mp = (m + 3) & ~3;
+  const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
   TACO_TRY(s.xp.ensure(4 * (size_t)n * mp));
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
@@ -912,7 +994,7 @@ static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStrea
   // xsq + its maximum (bound for the certified draw)
   k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.status.as<int64_t>());
   TACO_LAUNCHED();
-  const int mp = (m + 3) & ~3;
+  const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
   k_point_major<<<(unsigned)nbx, 256, 0, st>>>(h, mp, s.xp.as<float>());
   TACO_LAUNCHED();
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -921,12 +1003,12 @@ static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStrea
     cudaEventRecord(ev[0], st);
   }
   for (int ci = 0; ci < k; ++ci) {
-    k_pp_step<<<(unsigned)nbp, PP_THREADS, 0, st>>>(h, s.xsq.as<double>(), ci, s.best.as<double>(),
-                                                    s.C64.as<double>(), s.bsum.as<double>(), nbp,
-                                                    s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
-                                                    s.picks.as<int64_t>(), s.status.as<int64_t>(),
-                                                    s.leaves.as<int64_t>(), s.nleaves, s.cbuf.as<double>(),
-                                                    s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
+    auto* kpp = mp <= 8 ? k_pp_step<8> : mp <= 16 ? k_pp_step<16> : k_pp_step<32>;
+    kpp<<<(unsigned)std::min<int64_t>(nbp, std::max(1, 4 * g_num_sms() / std::max(1, r.concurrent))), PP_THREADS,
+          0, st>>>(h, s.xp.as<float>(), s.xsq.as<double>(), ci, s.best.as<double>(), s.C64.as<double>(),
+                   s.bsum.as<double>(), nbp, s.uni.as<double>(), forced_h ? s.forced.as<int64_t>() : nullptr,
+                   s.picks.as<int64_t>(), s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
+                   s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
     TACO_LAUNCHED();
   }
   if (ev[1]) cudaEventRecord(ev[1], st);
@@ -1148,6 +1230,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
       r.n_iter = idx->niter.as<int32_t>() + hh;
       r.cent_out = b ? idx->cb2.as<float>() + (size_t)j * kp * idx->m2 : idx->cb1.as<float>() + (size_t)j * kp * idx->m1;
       r.iters = idx->iters;
+      r.concurrent = w1 - w0;
       TACO_TRY(kmeans_prepare(r, first_h[hh], uniforms_h + (size_t)hh * std::max(kp - 1, 0),
                               forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr,
                               idx->half_streams[hh - w0]));

@@ -241,9 +241,12 @@ def build_index(data, params: IndexParams, keep_transformed: bool = False) -> Ta
     nat.call("taco_index_set_transform", dev.h, nat.ptr(model.mean), nat.ptr(M))
     nat.call("taco_transform_data", dev.h)
     t_transform = time.perf_counter() - t0
+    t_km0 = time.perf_counter()
     models = run_kmeans_all(dev, n, params.n_subspaces, s, kp, params.kmeans_iters,
                             lambda j, h: derive_seed(derive_seed(params.seed, j), h))
+    t_km1 = time.perf_counter()
     nat.call("taco_build_cells", dev.h)
+    t_cells = time.perf_counter()
     subspaces = [InvertedMultiIndex(codebook1=c1, codebook2=c2, cells=DeviceCells(dev, j, kp),
                                     codebook_size=kp, split=(s + 1) // 2)
                  for j, (c1, c2) in enumerate(models)]
@@ -258,6 +261,9 @@ def build_index(data, params: IndexParams, keep_transformed: bool = False) -> Ta
         "build_seconds": total,
         "covariance_seconds": t_cov - t0,
         "eigensolve_seconds": t_eig - t_cov,
+        "transform_only_seconds": t_km0 - t_eig,
+        "kmeans_only_seconds": t_km1 - t_km0,
+        "cells_seconds": t_cells - t_km1,
         "warnings": list(model.warnings),
         "device": dev.device,
     }

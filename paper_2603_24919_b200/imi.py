@@ -121,20 +121,28 @@ def run_kmeans_all(dev, n, n_sub, s, kprime, iters, seed_of):
     cb1 = np.empty((n_sub, kprime, m1), np.float32)
     cb2 = np.empty((n_sub, kprime, m2), np.float32)
     nat.call("taco_get_codebooks", dev.h, nat.ptr(cb1), nat.ptr(cb2))
-    lab1 = np.empty((n_sub, n), np.int32)
-    lab2 = np.empty((n_sub, n), np.int32)
-    nat.call("taco_get_labels", dev.h, nat.ptr(lab1), nat.ptr(lab2))
+    labels = {}
+
+    def fetch_labels():   # one device -> host copy of all 2*N_s label vectors, on first use
+        if not labels:
+            lab1 = np.empty((n_sub, n), np.int32)
+            lab2 = np.empty((n_sub, n), np.int32)
+            nat.call("taco_get_labels", dev.h, nat.ptr(lab1), nat.ptr(lab2))
+            labels["v"] = (lab1, lab2)
+        return labels["v"]
+
     hist = np.zeros((H, iters))
     nit = np.zeros(H, np.int32)
     nat.call("taco_get_history", dev.h, nat.ptr(hist), nat.ptr(nit))
     out = []
     for j in range(n_sub):
         pair = []
-        for b, (cb, lab) in enumerate(((cb1[j], lab1[j]), (cb2[j], lab2[j]))):
+        for b, cb in enumerate((cb1[j], cb2[j])):
             h = hist[2 * j + b][: nit[2 * j + b]]
-            pair.append(KMeansModel(centroids=cb.copy(), assignments=lab.copy(),
+            pair.append(KMeansModel(centroids=cb.copy(), assignments=None,
                                     inertia=float(h[-1]), inertia_history=tuple(map(float, h)),
-                                    n_iter=int(nit[2 * j + b])))
+                                    n_iter=int(nit[2 * j + b]),
+                                    loader=lambda j=j, b=b: fetch_labels()[b][j].copy()))
         out.append(tuple(pair))
     return out
 
