@@ -40,6 +40,8 @@ enum {
 typedef struct taco_index taco_index;
 
 const char* taco_last_error(void);
+/* Number of visible CUDA devices (0 when there is no usable GPU). */
+int taco_device_count(void);
 int taco_version(void);
 /* Number of kernel launches issued by this process so far (bench evidence). */
 int64_t taco_launch_count(void);
@@ -74,6 +76,10 @@ int taco_fit_covariance(taco_index* idx, double* mean_h, double* gram_h, int64_t
  * eigenvectors (columns).  Returns TACO_ERR_CONVERGENCE past max_sweeps. */
 int taco_jacobi_sweeps(double* A_h, double* V_h, int32_t d, double tol, int32_t max_sweeps,
                        int32_t* sweeps_out, double* residual_out);
+/* The same sweeps on `device` (one cooperative kernel, eigen.cu); bit-identical
+ * to taco_jacobi_sweeps (same IEEE operation sequence per element). */
+int taco_jacobi_sweeps_device(int device, double* A_h, double* V_h, int32_t d, double tol, int32_t max_sweeps,
+                              int32_t* sweeps_out, double* residual_out);
 /* TransformModel (spectral.py:64-91): mean f32[d], matrix f32[d x D] row-major
  * (blocks concatenated column-wise). */
 int taco_index_set_transform(taco_index* idx, const float* mean_h, const float* matrix_h);

@@ -34,6 +34,8 @@ _SIGS = {
     "taco_fit_covariance": [_vp, _vp, _vp, _vp],
     "taco_covariance": [_c_int, _vp, _c_i64, _c_i32, _vp, _vp, _vp],
     "taco_jacobi_sweeps": [_vp, _vp, _c_i32, _c_dbl, _c_i32, _vp, _vp],
+    "taco_device_count": [],
+    "taco_jacobi_sweeps_device": [_c_int, _vp, _vp, _c_i32, _c_dbl, _c_i32, _vp, _vp],
     "taco_index_set_transform": [_vp, _vp, _vp],
     "taco_transform_data": [_vp],
     "taco_index_set_transformed": [_vp, _vp],
@@ -130,6 +132,11 @@ def ptr(a: np.ndarray | None):
     if not a.flags["C_CONTIGUOUS"]:
         raise ValueError("native call needs a C-contiguous array")
     return a.ctypes.data
+
+
+def gpu_available() -> bool:
+    """True when the library sees at least one CUDA device."""
+    return int(lib().taco_device_count()) > 0
 
 
 def device_id() -> int:

@@ -169,6 +169,15 @@ extern "C" {
 
 const char* taco_last_error(void) { return g_err.c_str(); }
 int taco_version(void) { return 1; }
+
+int taco_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 int64_t taco_launch_count(void) { return g_launches.load(); }
 
 int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int32_t subspace_dim,

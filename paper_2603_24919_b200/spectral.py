@@ -14,6 +14,7 @@
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -126,6 +127,14 @@ def fit_covariance(data) -> CovarianceModel:
     return covariance_from_gram(mean, gram, n)
 
 
+def _eig_on_device() -> bool:
+    """The sweeps run on the GPU (eigen.cu) unless TACO_EIG=host selects the
+    bit-identical host restatement (jacobi.cpp), e.g. on a machine without a GPU."""
+    if os.environ.get("TACO_EIG", "") == "host":
+        return False
+    return nat.gpu_available()
+
+
 def jacobi_eigh(matrix, tol_rel: float = JACOBI_TOL_REL, max_sweeps: int = JACOBI_MAX_SWEEPS):
     """Eigensystem via cyclic Jacobi rotations (spectral.py:139-195)."""
     A = np.array(matrix, dtype=np.float64)
@@ -142,8 +151,12 @@ def jacobi_eigh(matrix, tol_rel: float = JACOBI_TOL_REL, max_sweeps: int = JACOB
     V = np.empty((d, d))
     sweeps = np.zeros(1, np.int32)
     resid = np.zeros(1)
-    rc = nat.lib().taco_jacobi_sweeps(nat.ptr(A), nat.ptr(V), d, tol, int(max_sweeps),
-                                      nat.ptr(sweeps), nat.ptr(resid))
+    if _eig_on_device():
+        rc = nat.lib().taco_jacobi_sweeps_device(nat.device_id(), nat.ptr(A), nat.ptr(V), d, tol,
+                                                 int(max_sweeps), nat.ptr(sweeps), nat.ptr(resid))
+    else:
+        rc = nat.lib().taco_jacobi_sweeps(nat.ptr(A), nat.ptr(V), d, tol, int(max_sweeps),
+                                          nat.ptr(sweeps), nat.ptr(resid))
     if rc == 5:
         raise ConvergenceError(nat.lib().taco_last_error().decode())
     nat.check(rc)
