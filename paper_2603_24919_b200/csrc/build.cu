@@ -12,6 +12,7 @@
 //  cells        k_cell_hist / k_cell_offsets / k_cell_scatter: stable
 //               counting sort by (l1,l2) into the chunk-major CSR     imi.py:70-81
 #include <algorithm>
+#include <ctime>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -753,75 +754,125 @@ __global__ void k_lloyd_ctl(const double* __restrict__ hsum, int64_t nb, int ite
   }
 }
 
+// A point's coordinates as one record of MP floats (the point-major copy);
+// the label sort moves whole records, so every cluster ends up as one
+// contiguous run of records in index order.
+template <int MP>
+struct __align__(16) PointRec {
+  float v[MP];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+// 1-D TMA: `bytes` (multiple of 16) from global to shared, completion counted on bar
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // centroid = (sequential fp64 sum over the cluster's points in index order) /
-// count -- the np.add.at order (clustering.py:95-99).  perm lists every
-// cluster's points in ascending index order (a stable radix sort of the
-// labels).  One CTA per cluster: warp 0's first m lanes run the m dependent
-// add chains; warps 1..3 gather the cluster's coordinates through perm into an
-// 8-stage shared-memory ring with cp.async, so each chain runs at the DADD
-// latency floor.  The producers also commit the new labels (lab[p] = c).
-constexpr int CS_R = 128, CS_ST = 8, CS_THREADS = 32 + CS_R;
-__global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const float* __restrict__ xp, int mp,
+// count -- the np.add.at order (clustering.py:95-99).  The label sort leaves
+// cluster c's records contiguous (index order inside the cluster), so one CTA
+// per cluster streams its run with 1-D TMA bulk copies into a CS_ST-stage
+// shared-memory ring (full/empty mbarriers), and the first m lanes of the
+// consumer warp run the m dependent add chains at the DADD latency.  The
+// producer warp's other lanes commit the new labels (lab = newlab).
+constexpr int CS_R = 64, CS_ST = 8, CS_THREADS = 64;
+template <int MP>
+__global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const PointRec<MP>* __restrict__ xs,
                                                              const int64_t* __restrict__ status,
-                                                             const uint32_t* __restrict__ perm,
                                                              const unsigned long long* __restrict__ counts,
+                                                             const int32_t* __restrict__ newlab,
                                                              int32_t* __restrict__ lab,
                                                              double* __restrict__ C64) {
   if (status[2]) return;
-  extern __shared__ __align__(16) float cs[];   // [CS_ST][CS_R][mp]
-  const int c = blockIdx.x, m = h.m, tid = threadIdx.x;
-  const int64_t cnt = (int64_t)counts[c];
-  if (cnt == 0) return;
+  extern __shared__ __align__(128) float cs[];   // [CS_ST][CS_R][MP]
+  __shared__ __align__(8) uint64_t full[CS_ST], empty[CS_ST];
   __shared__ int64_t s_start;
+  const int c = blockIdx.x, m = h.m, tid = threadIdx.x, lane = tid & 31;
+  const int64_t cnt = (int64_t)counts[c];
   if (tid < 32) {
     int64_t v = 0;
     for (int c2 = tid; c2 < c; c2 += 32) v += (int64_t)counts[c2];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (tid == 0) s_start = v;
+    if (tid == 0) {
+      s_start = v;
+      for (int st = 0; st < CS_ST; ++st) {
+        mbar_init(&full[st], 1);
+        mbar_init(&empty[st], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
   }
   __syncthreads();
-  const uint32_t* pp = perm + s_start;
+  const PointRec<MP>* run = xs + s_start;
   const int64_t ntile = (cnt + CS_R - 1) / CS_R;
-  const int SL = CS_R * mp;
-  const int r = tid - 32;   // producer: point r of every stage
-  // perm index of this producer's point in tile tb (issued one stage before
-  // its gather, so the gather never waits on the index load)
-  auto pidx = [&](int64_t tb) -> uint32_t {
-    return (tb < ntile && tb * CS_R + r < cnt) ? pp[tb * CS_R + r] : 0u;
-  };
-  uint32_t pnext = 0;
-  auto load = [&](int64_t tb, uint32_t p) {
-    if (tb < ntile && tb * CS_R + r < cnt) {
-      float* dst = cs + (size_t)(tb % CS_ST) * SL + r * mp;
-      const float* src = xp + (size_t)p * mp;   // the point's m coordinates: one 32-byte sector for m <= 8
-      for (int q = 0; q < mp; q += 4) cp_async16(dst + q, src + q);
-      lab[p] = c;
+  if (tid > 32) {
+    // commit the labels of this iteration (lab = newlab) while the chains run:
+    // CTA c copies its slice with 16-byte accesses, 8 in flight per lane
+    const int64_t per = ((h.n + gridDim.x - 1) / gridDim.x + 3) & ~(int64_t)3;
+    const int64_t i0 = min(h.n, (int64_t)c * per), i1 = min(h.n, i0 + per);
+    const bool al = ((reinterpret_cast<uintptr_t>(newlab) | reinterpret_cast<uintptr_t>(lab)) & 15) == 0;
+    const int64_t v0 = i0 >> 2, v1 = al ? i1 >> 2 : v0;   // whole int4s (i0 is a multiple of 4)
+    const int4* src = reinterpret_cast<const int4*>(newlab);
+    int4* dst = reinterpret_cast<int4*>(lab);
+    for (int64_t b = v0 + (tid - 33); b < v1; b += 31 * 8) {
+      int4 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b + u * 31 < v1) t[u] = __ldcs(src + b + u * 31);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b + u * 31 < v1) dst[b + u * 31] = t[u];
     }
-    cp_commit();
-  };
-  if (tid >= 32) {
-    uint32_t pi[CS_ST - 1];
-#pragma unroll
-    for (int st = 0; st < CS_ST - 1; ++st) pi[st] = pidx(st);
-#pragma unroll
-    for (int st = 0; st < CS_ST - 1; ++st) load(st, pi[st]);
-    pnext = pidx(CS_ST - 1);
-  }
-  double acc = 0.0;
-  for (int64_t tb = 0; tb < ntile; ++tb) {
-    if (tid >= 32) cp_wait<CS_ST - 2>();
-    __syncthreads();
-    if (tid >= 32) {
-      const uint32_t pcur = pnext;
-      pnext = pidx(tb + CS_ST);
-      load(tb + CS_ST - 1, pcur);
-    } else if (tid < m) {
-      const float* tv = cs + (size_t)(tb % CS_ST) * SL + tid;
+    for (int64_t i = (al ? v1 << 2 : i0) + (tid - 33); i < i1; i += 31) lab[i] = newlab[i];
+  } else if (tid == 32 && cnt > 0) {
+    // producer: one elected thread streams the run
+    for (int64_t tb = 0; tb < ntile; ++tb) {
+      const int slot = (int)(tb % CS_ST);
+      if (tb >= CS_ST) mbar_wait(&empty[slot], (unsigned)(((tb / CS_ST) - 1) & 1));
       const int rr = (int)min((int64_t)CS_R, cnt - tb * CS_R);
-      acc = chain_add(acc, tv, rr, mp);
+      const unsigned bytes = (unsigned)(rr * MP * sizeof(float));
+      mbar_expect_tx(&full[slot], bytes);
+      tma_g2s(cs + (size_t)slot * CS_R * MP, run + tb * CS_R, bytes, &full[slot]);
     }
+  } else if (tid < 32 && cnt > 0) {
+    double acc = 0.0;
+    for (int64_t tb = 0; tb < ntile; ++tb) {
+      const int slot = (int)(tb % CS_ST);
+      mbar_wait(&full[slot], (unsigned)((tb / CS_ST) & 1));
+      if (lane < m) {
+        const int rr = (int)min((int64_t)CS_R, cnt - tb * CS_R);
+        acc = chain_add(acc, cs + (size_t)slot * CS_R * MP + lane, rr, MP);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    if (lane < m) C64[(size_t)c * m + lane] = __ddiv_rn(acc, (double)cnt);
   }
-  if (tid < m) C64[(size_t)c * m + tid] = __ddiv_rn(acc, (double)cnt);
 }
 
 // point-major copy of a half (xp[i][t], t padded to mp = 4*ceil(m/4)) so a
@@ -906,6 +957,39 @@ struct KMeansRun {
   int concurrent = 1;  // halves running at once: each k-means++ draw takes sms/concurrent CTAs
 };
 
+// CUB onesweep radix sort of the point records (values) by label (keys);
+// stable, so index order is kept inside every label.
+// (128-byte records exceed CUB's onesweep shared memory: MP = 32 sorts the
+// point indices instead and gathers the records, 128 B per point.)
+__global__ void k_gather_rec32(const PointRec<32>* __restrict__ in, const uint32_t* __restrict__ perm, int64_t n,
+                               PointRec<32>* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one float4 per thread
+  if (t >= n * 8) return;
+  const int64_t k = t >> 3;
+  const int q = (int)(t & 7);
+  reinterpret_cast<float4*>(out + k)[q] = __ldg(reinterpret_cast<const float4*>(in + perm[k]) + q);
+}
+
+template <int MP>
+static int label_sort(void* tmp, size_t& tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out, const void* rec_in,
+                      void* rec_out, int64_t n, int bits, cudaStream_t st, const uint32_t* iota = nullptr,
+                      uint32_t* perm = nullptr) {
+  if constexpr (MP == 32) {
+    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, iota, perm, n, 0, bits, st));
+    if (tmp) {
+      k_gather_rec32<<<(unsigned)ceil_div(n * 8, 256), 256, 0, st>>>(static_cast<const PointRec<32>*>(rec_in), perm, n,
+                                                                     static_cast<PointRec<32>*>(rec_out));
+      TACO_LAUNCHED();
+    }
+    return TACO_OK;
+  } else {
+    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out,
+                                                    static_cast<const PointRec<MP>*>(rec_in),
+                                                    static_cast<PointRec<MP>*>(rec_out), n, 0, bits, st));
+    return TACO_OK;
+  }
+}
+
 // All allocations of one k-means run (no stream work): done for every half
 // before any half is enqueued, so the enqueue loop never blocks in cudaMalloc.
 static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h, const int64_t* forced_h,
@@ -930,7 +1014,6 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   TACO_TRY(s.C64.ensure(8 * (size_t)k * m));
   TACO_TRY(s.newlab.ensure(4 * n));
   TACO_TRY(s.pd.ensure(8 * n));
-  TACO_TRY(s.perm.ensure(4 * n));
   TACO_TRY(s.keys2.ensure(4 * n));
   TACO_TRY(s.ctl.ensure(8 * 2 * (size_t)k));   // per-cluster counts, double buffered by iteration parity
   TACO_TRY(s.hsum.ensure(8 * nba));
@@ -939,15 +1022,19 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
   size_t cub_bytes = 0;
-  TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
-                                                  lbits, st));
+  if (mp == 8) TACO_TRY(label_sort<8>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
+  else if (mp == 16) TACO_TRY(label_sort<16>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
+  else TACO_TRY(label_sort<32>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
   TACO_TRY(s.cubtmp.ensure(std::max<size_t>(cub_bytes, 16)));
-  if (s.iota.bytes < 4 * (size_t)n) {
-    TACO_TRY(s.iota.ensure(4 * n));
-    k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
-    TACO_LAUNCHED();
+  if (mp == 32) {
+    TACO_TRY(s.perm.ensure(4 * n));
+    if (s.iota.bytes < 4 * (size_t)n) {
+      TACO_TRY(s.iota.ensure(4 * n));
+      k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
+      TACO_LAUNCHED();
+    }
   }
+  TACO_TRY(s.xs.ensure(4 * (size_t)n * mp));
   if (s.leaves_n != n) {                // numpy pairwise leaves of an n-array (exact replay)
     std::vector<int64_t> lv;
     pairwise_leaves(0, n, lv);
@@ -964,8 +1051,11 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   if (ash > 48 * 1024)
     TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
   const size_t css = sizeof(float) * CS_ST * CS_R * mp;
-  if (css > 48 * 1024)
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
+  if (css > 48 * 1024) {
+    if (mp == 8) TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
+    else if (mp == 16) TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
+    else TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
+  }
   // the draw plan (first pick, uniforms, forced draws) goes up before any
   // kernel of the run is enqueued (the enqueue may be a graph capture)
   TACO_CHECK_CUDA(cudaMemcpyAsync(s.picks.p, &first, 8, cudaMemcpyHostToDevice, st));
@@ -978,7 +1068,14 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   return TACO_OK;
 }
 
-static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStream_t st, bool timing) {
+// The enqueue of one k-means run is cut into steps -- 0: xsq and the
+// point-major copy; 1..k: one k-means++ draw each; then one Lloyd iteration
+// each; last: the centroid export -- so the caller can interleave the steps of
+// all concurrent halves (every half's first draw is queued before any half's
+// second) and the GPU never waits for a host enqueue that is busy elsewhere.
+static int kmeans_steps(const KMeansRun& r) { return 1 + r.h.k + r.iters + 1; }
+
+static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t st, bool timing, int step) {
   BuildScratch& s = *r.s;
   const HalfView h = r.h;
   const int64_t n = h.n;
@@ -989,20 +1086,25 @@ static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStrea
   const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
-  k_status_init<<<1, 1, 0, st>>>(s.status.as<int64_t>(), k);
-  TACO_LAUNCHED();
-  // xsq + its maximum (bound for the certified draw)
-  k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.status.as<int64_t>());
-  TACO_LAUNCHED();
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
-  k_point_major<<<(unsigned)nbx, 256, 0, st>>>(h, mp, s.xp.as<float>());
-  TACO_LAUNCHED();
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  if (timing) {
-    for (auto& e : ev) cudaEventCreate(&e);
-    cudaEventRecord(ev[0], st);
+  unsigned long long* cnt = s.ctl.as<unsigned long long>();
+  if (step == 0) {
+    k_status_init<<<1, 1, 0, st>>>(s.status.as<int64_t>(), k);
+    TACO_LAUNCHED();
+    // xsq + its maximum (bound for the certified draw)
+    k_xsq<<<(unsigned)nbx, 256, 0, st>>>(h, s.xsq.as<double>(), s.status.as<int64_t>());
+    TACO_LAUNCHED();
+    k_point_major<<<(unsigned)nbx, 256, 0, st>>>(h, mp, s.xp.as<float>());
+    TACO_LAUNCHED();
+    TACO_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8 * 2 * (size_t)k, st));
+    if (timing) {
+      for (auto& e : s.ev) cudaEventCreate(&e);
+      cudaEventRecord(s.ev[0], st);
+    }
+    return TACO_OK;
   }
-  for (int ci = 0; ci < k; ++ci) {
+  if (step <= k) {
+    const int ci = step - 1;
     auto* kpp = mp <= 8 ? k_pp_step<8> : mp <= 16 ? k_pp_step<16> : k_pp_step<32>;
     kpp<<<(unsigned)std::min<int64_t>(nbp, std::max(1, 4 * g_num_sms() / std::max(1, r.concurrent))), PP_THREADS,
           0, st>>>(h, s.xp.as<float>(), s.xsq.as<double>(), ci, s.best.as<double>(), s.C64.as<double>(),
@@ -1010,14 +1112,14 @@ static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStrea
                    s.picks.as<int64_t>(), s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
                    s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
     TACO_LAUNCHED();
+    if (ci == k - 1 && timing) cudaEventRecord(s.ev[1], st);
+    return TACO_OK;
   }
-  if (ev[1]) cudaEventRecord(ev[1], st);
-  const size_t ash = sizeof(double) * ((size_t)k * m + k);
-  auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
-  unsigned long long* cnt = s.ctl.as<unsigned long long>();
-  TACO_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8 * 2 * (size_t)k, st));
-  const size_t css = sizeof(float) * CS_ST * CS_R * mp;
-  for (int it = 0; it < r.iters; ++it) {
+  if (step <= k + r.iters) {
+    const int it = step - k - 1;
+    const size_t ash = sizeof(double) * ((size_t)k * m + k);
+    auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
+    const size_t css = sizeof(float) * CS_ST * CS_R * mp;
     unsigned long long* cc = cnt + (size_t)(it & 1) * k;
     unsigned long long* cn = cnt + (size_t)((it + 1) & 1) * k;
     kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,
@@ -1027,27 +1129,41 @@ static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStrea
     k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nba, it, s.status.as<int64_t>(), r.history,
                                     r.n_iter);
     TACO_LAUNCHED();
-    // stable sort of the point indices by label (index order inside a label)
+    // stable radix sort of the point records by label (index order inside a label)
     size_t cb = s.cubtmp.bytes;
-    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(s.cubtmp.p, cb, reinterpret_cast<const uint32_t*>(s.newlab.p),
-                                                    s.keys2.as<uint32_t>(), s.iota.as<uint32_t>(),
-                                                    s.perm.as<uint32_t>(), (int64_t)n, 0, lbits, st));
-    count_launch(2);
-    k_cluster_sums<<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xp.as<float>(), mp, s.status.as<int64_t>(),
-                                                         s.perm.as<uint32_t>(), cc,
-                                                         r.labels, s.C64.as<double>());
-    TACO_LAUNCHED();
+    const uint32_t* nl = reinterpret_cast<const uint32_t*>(s.newlab.p);
+    if (mp == 8) {
+      TACO_TRY(label_sort<8>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st));
+      k_cluster_sums<8><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<8>>(), s.status.as<int64_t>(), cc,
+                                                              s.newlab.as<int32_t>(), r.labels, s.C64.as<double>());
+    } else if (mp == 16) {
+      TACO_TRY(label_sort<16>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st));
+      k_cluster_sums<16><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<16>>(), s.status.as<int64_t>(),
+                                                               cc, s.newlab.as<int32_t>(), r.labels,
+                                                               s.C64.as<double>());
+    } else {
+      TACO_TRY(label_sort<32>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st,
+                              s.iota.as<uint32_t>(), s.perm.as<uint32_t>()));
+      k_cluster_sums<32><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<32>>(), s.status.as<int64_t>(),
+                                                               cc, s.newlab.as<int32_t>(), r.labels,
+                                                               s.C64.as<double>());
+    }
+    count_launch(3);
+    TACO_CHECK_CUDA(cudaGetLastError());
     k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), cc, s.pd.as<double>(),
                                  r.labels, s.C64.as<double>());
     TACO_LAUNCHED();
+    return TACO_OK;
   }
   k_centroids_out<<<(unsigned)ceil_div((int64_t)k * m, 256), 256, 0, st>>>(s.C64.as<double>(), k * m,
                                                                             r.cent_out);
   TACO_LAUNCHED();
-  if (ev[2]) {
-    cudaEventRecord(ev[2], st);
-    s.ev[0] = ev[0]; s.ev[1] = ev[1]; s.ev[2] = ev[2];
-  }
+  if (timing) cudaEventRecord(s.ev[2], st);
+  return TACO_OK;
+}
+
+static int kmeans_enqueue(const KMeansRun& r, const int64_t* forced_h, cudaStream_t st, bool timing) {
+  for (int i = 0; i < kmeans_steps(r); ++i) TACO_TRY(kmeans_step(r, forced_h, st, timing, i));
   return TACO_OK;
 }
 
@@ -1236,42 +1352,61 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
                               idx->half_streams[hh - w0]));
       runs.push_back(r);
     }
-    // All halves of the wave are independent: their ~300 launches each are
-    // captured once into one graph with a branch per half (fork/join through
-    // events), so the host enqueue cost is paid at capture speed and the GPU
-    // sees every half at once.  TACO_KM_GRAPH=0 launches them directly.
+    // All halves of the wave are independent.  Default: direct launches,
+    // interleaved step by step across the halves (every half's draw i is
+    // queued before any half's draw i+1), so the GPU starts on all halves at
+    // once and the host enqueue (~2 us per launch) overlaps the execution.
+    // TACO_KM_GRAPH=1 captures the same work into one graph instead (a branch
+    // per half; instantiation costs more than it saves for a single build).
     const char* ge = getenv("TACO_KM_GRAPH");
     const bool timing = getenv("TACO_DEBUG_TIMING") != nullptr;
-    const bool graph = !(ge && ge[0] == '0') && !timing;
+    const bool graph = ge && ge[0] == '1' && !timing;
     cudaStream_t origin = idx->stream;
     cudaGraph_t g = nullptr;
+    const bool gdbg = getenv("TACO_DEBUG_GRAPH") != nullptr;
+    auto now_ms = []() {
+      timespec ts;
+      clock_gettime(CLOCK_MONOTONIC, &ts);
+      return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    };
+    const double tg0 = now_ms();
+    int erc = TACO_OK;
+    auto forced_of = [&](int hh) { return forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr; };
     if (graph) {
       TACO_CHECK_CUDA(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
       TACO_CHECK_CUDA(cudaEventRecord(idx->km_fork, origin));
-    }
-    int erc = TACO_OK;
-    for (int hh = w0; hh < w1 && erc == TACO_OK; ++hh) {
-      cudaStream_t hs = idx->half_streams[hh - w0];
-      if (graph) cudaStreamWaitEvent(hs, idx->km_fork, 0);
-      erc = kmeans_enqueue(runs[hh - w0], forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr, hs,
-                           timing);
-      if (graph) {
+      for (int hh = w0; hh < w1 && erc == TACO_OK; ++hh) {
+        cudaStream_t hs = idx->half_streams[hh - w0];
+        cudaStreamWaitEvent(hs, idx->km_fork, 0);
+        erc = kmeans_enqueue(runs[hh - w0], forced_of(hh), hs, false);
         cudaEventRecord(idx->half_ev[hh - w0], hs);
         cudaStreamWaitEvent(origin, idx->half_ev[hh - w0], 0);
       }
-    }
-    if (graph) {
       cudaError_t ce = cudaStreamEndCapture(origin, &g);
       if (erc != TACO_OK) { if (g) cudaGraphDestroy(g); return erc; }
       if (ce != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "k-means graph capture: %s", cudaGetErrorString(ce));
+      const double tg1 = now_ms();
       cudaGraphExec_t ex = nullptr;
       TACO_CHECK_CUDA(cudaGraphInstantiate(&ex, g, 0));
       cudaGraphDestroy(g);
+      const double tg2 = now_ms();
       cudaError_t le = cudaGraphLaunch(ex, origin);
+      const double tg3 = now_ms();
       cudaError_t se = cudaStreamSynchronize(origin);
+      if (gdbg)
+        fprintf(stderr, "[taco] k-means graph: prepare+capture %.2f ms, instantiate %.2f ms, launch %.2f ms, run %.2f ms\n",
+                tg1 - tg0, tg2 - tg1, tg3 - tg2, now_ms() - tg3);
       cudaGraphExecDestroy(ex);
       if (le != cudaSuccess || se != cudaSuccess)
         TACO_FAIL(TACO_ERR_CUDA, "k-means graph: %s", cudaGetErrorString(le != cudaSuccess ? le : se));
+    } else {
+      int maxs = 0;
+      for (auto& r : runs) maxs = std::max(maxs, kmeans_steps(r));
+      for (int i = 0; i < maxs && erc == TACO_OK; ++i)
+        for (int hh = w0; hh < w1 && erc == TACO_OK; ++hh)
+          if (i < kmeans_steps(runs[hh - w0]))
+            erc = kmeans_step(runs[hh - w0], forced_of(hh), idx->half_streams[hh - w0], timing, i);
+      if (gdbg) fprintf(stderr, "[taco] k-means direct enqueue %.2f ms\n", now_ms() - tg0);
     }
     TACO_TRY(erc);
     for (int hh = w0; hh < w1; ++hh) {
@@ -1294,7 +1429,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   for (auto& bs : idx->bs) {
     DevBuf* sb[] = {&bs.xsq, &bs.best, &bs.bsum, &bs.picks, &bs.uni, &bs.forced, &bs.status, &bs.C64, &bs.csq,
                     &bs.newlab, &bs.pd, &bs.changed, &bs.perm, &bs.lhist, &bs.loff, &bs.ctl, &bs.hsum, &bs.draws,
-                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp};
+                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp, &bs.xs};
     for (auto* b : sb) b->release();
     bs.leaves_n = -1;
   }
@@ -1430,7 +1565,7 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
   X.release(); lab.release(); hist.release(); nit.release(); cent.release();
   DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
                   &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws,
-                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp};
+                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs};
   for (auto* b : sb) b->release();
   return rc;
 }

@@ -48,7 +48,7 @@ struct QueryTile {
 
 struct BuildScratch {
   DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
-      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp;
+      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp, xs;
   int64_t nleaves = 0, leaves_n = -1;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // TACO_DEBUG_TIMING
 };
