@@ -131,6 +131,38 @@ def build(X, meta):
     return index, wall
 
 
+DADD_NS = 5.6   # dependent fp64 add latency on B200 (11 cycles at 1965 MHz, tools/mb_dadd.cu)
+
+
+def build_roofline(index, meta, build_wall, peak):
+    """SURVEY 8(d) algorithmic build bytes:
+    8nd (mean + Gram reads) + 4nd + 4nD (transform) + sum over the 2 N_s halves of
+    (K'-1) n (4m+16) (k-means++ passes) + t_h n (8m+8) (Lloyd) + 48 n N_s (CSR),
+    with t_h each half's own Lloyd iteration count.  Reported with and without
+    the eigensolve, plus the floors of the reference's strictly sequential fp64
+    add chains (column mean: n adds; Lloyd centroid sums: the largest cluster's
+    chain every iteration), which no parallel schedule can beat."""
+    n, d, ns, s, kp = meta["n"], meta["d"], meta["n_sub"], meta["s"], meta["kprime"]
+    D = ns * s
+    b = 8 * n * d + 4 * n * d + 4 * n * D + 48 * n * ns
+    chain_ms = 0.0
+    for sub in index.subspaces:
+        for cb in (sub.codebook1, sub.codebook2):
+            m = cb.dim
+            b += (kp - 1) * n * (4 * m + 16) + cb.n_iter * n * (8 * m + 8)
+            sizes = np.bincount(np.asarray(cb.assignments), minlength=kp)
+            chain_ms = max(chain_ms, cb.n_iter * int(sizes.max()) * DADD_NS * 1e-6)
+    eig = index.metadata.get("eigensolve_seconds", 0.0)
+    return {"algorithmic_bytes": int(b), "seconds": build_wall,
+            "achieved_GBps": b / build_wall / 1e9, "peak": peak, "frac": b / build_wall / 1e9 / peak,
+            "frac_excl_eigensolve": b / max(build_wall - eig, 1e-9) / 1e9 / peak,
+            "hbm_time_ms": b / peak / 1e6,
+            "sequential_floor_ms": {"column_mean_chain": n * DADD_NS * 1e-6, "lloyd_sum_chains": chain_ms},
+            "stages_seconds": {kk: index.metadata[kk] for kk in (
+                "covariance_seconds", "eigensolve_seconds", "transform_only_seconds", "kmeans_only_seconds",
+                "cells_seconds") if kk in index.metadata}}
+
+
 def path_bytes(stats, meta, nq_total):
     """B_q = 4*sum_j R_j + n + (4d+4)|C| + 4d + 8 min(k,|C|)."""
     d, n, k = meta["d"], meta["n"], meta["k"]
@@ -368,6 +400,7 @@ def run_ours(args):
     o_ids, _ = O.ground_truth(X, Q[:2], k)
     gt_checked = bool(np.array_equal(o_ids, gt.ids[:2]))
 
+    broof = build_roofline(index, meta, build_wall, peak)
     cpu = None if args.no_cpu_baseline else cpu_baseline(index, X, Q, meta, ids_gpu, args.cpu_budget)
     h2d = nq * d * 4
     d2h = nq * k * 8 + nq * 12
@@ -378,12 +411,11 @@ def run_ours(args):
         "config": {"workload": workload_name(meta), "n": meta["n"], "d": d, "batch": nq,
                    "l2": "256 MiB buffer written between timed steps; X (512 MB) > L2",
                    "build_seconds": build_wall, "build_seconds_cold": meta["build_seconds_cold"],
-                   "build_breakdown": {
-                       kk: index.metadata[kk] for kk in ("covariance_seconds", "eigensolve_seconds",
-                                                         "transform_seconds", "kmeans_seconds")},
+                   "build_breakdown": broof["stages_seconds"],
                    "recall@10": rec, "recall_queries": nq, "ground_truth": "GPU exact (fp64, ties by id)",
                    "ground_truth_seconds": gt_seconds, "ground_truth_oracle_spotcheck": gt_checked},
         "build_seconds": build_wall,
+        "build_roofline": broof,
         "e2e": {"value": nq / (e2e_ms / 1000.0), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),

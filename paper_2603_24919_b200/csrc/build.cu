@@ -1319,7 +1319,25 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   const int kp = idx->kp;
   const int64_t n = idx->n;
   if (n < kp) TACO_FAIL(TACO_ERR_INSUFFICIENT, "%lld points cannot fill %d clusters", (long long)n, kp);
-  const int NS = std::min(H, 16);
+  // Halves in flight: up to 16, fewer when their scratch would not fit in the
+  // free device memory (n = 1e8 needs ~15 GB per half).  Cached pool memory
+  // is returned to the device first if that is what stands in the way.
+  const int mpx = std::max(idx->m1, idx->m2) <= 8 ? 8 : std::max(idx->m1, idx->m2) <= 16 ? 16 : 32;
+  const size_t per_half = (size_t)n * (64 + 12 * (size_t)mpx) + ((size_t)64 << 20);
+  auto fit = [&]() {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    return (int)std::max<size_t>(1, (size_t)(0.85 * (double)fr) / per_half);
+  };
+  int NS = std::min({H, 16, fit()});
+  if (NS < std::min(H, 16)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    NS = std::min({H, 16, fit()});
+  }
   TACO_TRY(ensure_half_streams(idx, NS));
   if ((int)idx->bs.size() < NS) idx->bs.resize(NS);
   TACO_TRY(idx->labels.ensure(sizeof(int32_t) * (size_t)n * H));
