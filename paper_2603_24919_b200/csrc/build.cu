@@ -12,6 +12,9 @@
 //  cells        k_cell_hist / k_cell_offsets / k_cell_scatter: stable
 //               counting sort by (l1,l2) into the chunk-major CSR     imi.py:70-81
 #include <algorithm>
+#include <cstring>
+#include <array>
+#include <climits>
 #include <ctime>
 #include <cmath>
 #include <cstdlib>
@@ -251,6 +254,46 @@ __global__ void k_xsq(HalfView h, double* __restrict__ xsq, int64_t* __restrict_
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail; else split at
 // n2 = n/2 - (n/2)%8 and add the halves.  The leaves (ranges <= 128) depend
 // only on n and are listed once on the host in depth-first order.
+// The combine tree of that recursion: internal node = (left, right) ids over
+// [0, nleaves) = leaves (DFS order) and nleaves + i = internal node i; nodes
+// are ordered by height so a level-synchronous pass meets children first.
+struct PwTree {
+  std::vector<int32_t> left, right, level_start;
+};
+static int pw_build(int64_t len, int& leaf_ctr, std::vector<std::array<int32_t, 3>>& tmp) {
+  // returns the node's temporary id: leaves -> (leaf index), internal -> -(1 + tmp index)
+  if (len <= 128) return leaf_ctr++;
+  int64_t n2 = len / 2;
+  n2 -= n2 % 8;
+  const int l = pw_build(n2, leaf_ctr, tmp);
+  const int r = pw_build(len - n2, leaf_ctr, tmp);
+  auto height = [&](int id) { return id >= 0 ? 0 : tmp[-1 - id][2]; };
+  tmp.push_back({l, r, 1 + std::max(height(l), height(r))});
+  return -(int)tmp.size();
+}
+static PwTree pairwise_tree(int64_t n) {
+  PwTree t;
+  std::vector<std::array<int32_t, 3>> tmp;
+  int leaves = 0;
+  pw_build(n, leaves, tmp);
+  const int ni = (int)tmp.size();
+  std::vector<int> order(ni);
+  for (int i = 0; i < ni; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tmp[a][2] < tmp[b][2]; });
+  std::vector<int> rank(ni);
+  for (int i = 0; i < ni; ++i) rank[order[i]] = i;
+  auto final_id = [&](int id) { return id >= 0 ? id : leaves + rank[-1 - id]; };
+  int cur = 0;
+  for (int i = 0; i < ni; ++i) {
+    const auto& nd = tmp[order[i]];
+    if (i == 0 || nd[2] != cur) { t.level_start.push_back(i); cur = nd[2]; }
+    t.left.push_back(final_id(nd[0]));
+    t.right.push_back(final_id(nd[1]));
+  }
+  t.level_start.push_back(ni);
+  return t;
+}
+
 static void pairwise_leaves(int64_t off, int64_t len, std::vector<int64_t>& out) {
   if (len <= 128) {
     out.push_back(off);
@@ -310,6 +353,123 @@ __device__ double np_combine(const double* leaf, int64_t n) {
     }
   }
   return ret;
+}
+
+// numpy's sequential cumsum (np.add.accumulate) of p[0..n) reproduced
+// bit-exactly by one CTA without the n-step dependent chain.  While the
+// running value c stays in one binade [2^e, 2^(e+1)), every step
+// fl(c + p_k) = c + g * round(p_k / g) with g = ulp = 2^(e-52) (c is a multiple
+// of g), so the chain inside a binade is an exact int64 prefix sum of the
+// rounded quotients q_k.  A parallel scan finds the first element that leaves
+// the binade (c + g*Q_k >= 2^(e+1)) or whose quotient is an exact tie (round to
+// even depends on the running value); that one element is added with a real
+// fp64 add and the scan resumes from it.  There are ~log2(S / c_0) binade
+// changes, so the work is one pass over p plus O(log n) short restarts.
+constexpr int CX_V = 16;   // elements per thread per chunk
+__device__ void cumsum_exact_block(const double* __restrict__ best, double total, int64_t n, double* __restrict__ cdf) {
+  // p_k = best_k / total (numpy's elementwise division), formed on the fly
+  auto P = [&](int64_t k) { return __ddiv_rn(__ldcg(best + k), total); };
+  __shared__ double s_crun;
+  __shared__ long long s_i, s_stop;
+  __shared__ long long s_wq[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+  if (tid == 0) {
+    // head: sequential until the running value is a normal double well above underflow
+    double c = P(0);
+    cdf[0] = c;
+    int64_t i = 1;
+    while (i < n && !(c >= 0x1p-900)) {
+      c = __dadd_rn(c, P(i));
+      cdf[i] = c;
+      ++i;
+    }
+    s_crun = c;
+    s_i = i;
+    s_stop = LLONG_MAX;
+  }
+  __syncthreads();
+  while (true) {
+    const int64_t i0 = s_i;
+    if (i0 >= n) break;
+    const double crun = s_crun;
+    const int e = ilogb(crun);
+    const double g = scalbn(1.0, e - 52), inv = scalbn(1.0, 52 - e);
+    const long long Qlim = (long long)__dmul_rn(__dsub_rn(scalbn(1.0, e + 1), crun), inv);   // exact
+    long long Qbase = 0;
+    long long stop = LLONG_MAX;
+    for (int64_t j0 = i0; j0 < n; j0 += (int64_t)NT * CX_V) {
+      long long lp[CX_V];
+      long long tsum = 0;
+      int tie = CX_V;
+#pragma unroll
+      for (int v = 0; v < CX_V; ++v) {
+        const int64_t k = j0 + (int64_t)tid * CX_V + v;
+        long long q = 0;
+        if (k < n) {
+          const double t = __dmul_rn(P(k), inv);   // exact power-of-two scaling
+          if (t >= 0x1p60) {
+            q = 1LL << 60;                         // certainly leaves the binade
+          } else {
+            const double fl = floor(t), fr = __dsub_rn(t, fl);
+            q = (long long)fl + (fr > 0.5 ? 1 : 0);
+            if (fr == 0.5 && tie == CX_V) tie = v;
+          }
+        }
+        tsum += q;
+        lp[v] = tsum;
+      }
+      // block exclusive scan of the thread totals
+      long long incl = tsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wq[wid] = incl;
+      __syncthreads();
+      if (wid == 0) {
+        long long w = lane < NW ? s_wq[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += y;
+        }
+        s_wq[lane] = w;
+      }
+      __syncthreads();
+      const long long excl = Qbase + (wid ? s_wq[wid - 1] : 0) + (incl - tsum);
+      const long long chunk_tot = s_wq[NW - 1];
+#pragma unroll
+      for (int v = 0; v < CX_V; ++v) {
+        const int64_t k = j0 + (int64_t)tid * CX_V + v;
+        if (k < n && (excl + lp[v] >= Qlim || v == tie)) {
+          atomicMin(&s_stop, (long long)k);
+          break;
+        }
+      }
+      __syncthreads();
+      stop = s_stop;
+#pragma unroll
+      for (int v = 0; v < CX_V; ++v) {
+        const int64_t k = j0 + (int64_t)tid * CX_V + v;
+        if (k < n && k < stop) cdf[k] = __dadd_rn(crun, __dmul_rn((double)(excl + lp[v]), g));   // exact
+      }
+      __syncthreads();   // s_wq / s_stop reuse, cdf visible
+      if (stop != LLONG_MAX) break;
+      Qbase += chunk_tot;
+    }
+    if (stop == LLONG_MAX) break;   // ran to the end inside this binade
+    if (tid == 0) {
+      const double prev = stop == i0 ? crun : cdf[stop - 1];
+      const double c = __dadd_rn(prev, P(stop));   // the element that leaves the binade (or ties)
+      cdf[stop] = c;
+      s_crun = c;
+      s_i = stop + 1;
+      s_stop = LLONG_MAX;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
 }
 
 // One CTA: chooses picks[ci+1] from best (after centroids 0..ci) and u.
@@ -477,18 +637,66 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   // total = numpy pairwise sum; p = best/total; cdf = sequential cumsum;
   // idx = first i with fl(cdf_i / cdf_last) > u.  Everything but the cumsum
   // chain runs on all threads of the block.
-  for (int64_t l = tid; l < nleaves; l += NT) lsum[l] = np_leaf(best + leaves[2 * l], leaves[2 * l + 1]);
-  __syncthreads();
-  if (tid == 0) s_total = np_combine(lsum, h.n);
-  __syncthreads();
+  // numpy pairwise total: 8 lanes per leaf (one per strided accumulator, the
+  // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree by xor shuffles, then the tail),
+  // then the combine tree level by level (node lists from the host)
+  {
+    const int j = tid & 7;
+    for (int64_t l0 = 0; l0 < nleaves; l0 += NT / 8) {
+      const int64_t l = l0 + (tid >> 3);
+      double r = 0.0;
+      int64_t off = 0, len = 0;
+      if (l < nleaves) {
+        off = leaves[2 * l];
+        len = leaves[2 * l + 1];
+        if (len >= 8) {
+          const double* a = best + off;
+          r = __ldcg(a + j);
+          const int64_t full = len - (len % 8);
+#pragma unroll 4
+          for (int64_t i = 8; i < full; i += 8) r = __dadd_rn(r, __ldcg(a + i + j));
+        }
+      }
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+      if (l < nleaves && j == 0) {
+        if (len < 8) {
+          r = 0.0;
+          for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
+        } else {
+          for (int64_t i = len - (len % 8); i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
+        }
+        lsum[l] = r;
+      }
+    }
+    __syncthreads();
+    const int32_t* tl = reinterpret_cast<const int32_t*>(leaves + 2 * nleaves);   // left[ni], right[ni], level_start[]
+    const int ni = (int)(nleaves - 1);
+    const int32_t* tr = tl + ni;
+    const int32_t* lvs = tr + ni;
+    for (int lv = 0; ni > 0; ++lv) {
+      const int b0 = lvs[lv], b1 = lvs[lv + 1];
+      for (int i = b0 + tid; i < b1; i += NT) lsum[nleaves + i] = __dadd_rn(lsum[tl[i]], lsum[tr[i]]);
+      __syncthreads();
+      if (b1 == ni) break;
+    }
+    if (tid == 0) s_total = ni > 0 ? lsum[nleaves + ni - 1] : lsum[0];
+    __syncthreads();
+  }
   const double total = s_total;
-  for (int64_t i = tid; i < h.n; i += NT) pbuf[i] = __ddiv_rn(__ldcg(best + i), total);
-  __syncthreads();
-  // The sequential cumsum chain runs once on thread 0 over shared-memory tiles
-  // that the rest of the block streams in (double buffered) and writes back
-  // (cdf values -> cbuf); the crossing is then found by binary search.
   __shared__ double tile[2][PS_TILE];
   __shared__ double s_c;
+  if (force_replay != 2) {
+    cumsum_exact_block(best, total, h.n, cbuf);
+    if (tid == 0) s_c = cbuf[h.n - 1];
+    __syncthreads();
+  } else {
+  for (int64_t i = tid; i < h.n; i += NT) pbuf[i] = __ddiv_rn(__ldcg(best + i), total);
+  __syncthreads();
+  // (test hook force_replay == 2) the sequential cumsum chain on thread 0 over
+  // shared-memory tiles the rest of the block streams in (double buffered)
+  // and writes back (cdf values -> cbuf)
   const int64_t ntile = (h.n + PS_TILE - 1) / PS_TILE;
   for (int64_t i = tid; i < min((int64_t)PS_TILE, h.n); i += NT) tile[0][i] = pbuf[i];
   if (tid == 0) s_c = 0.0;
@@ -530,6 +738,8 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
     for (int64_t i = tid; i < PS_TILE && pb0 + i < h.n; i += NT) cbuf[pb0 + i] = tile[(ntile - 1) & 1][i];
   }
   __syncthreads();
+  }   // sequential chain
+  // the crossing is then found by binary search over cbuf
   if (tid == 0) {
     const double last = s_c;                             // cdf[-1]
     // largest c with fl(c / last) <= u; searchsorted(cdf / last, u, 'right')
@@ -1039,13 +1249,24 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
     std::vector<int64_t> lv;
     pairwise_leaves(0, n, lv);
     s.nleaves = (int64_t)lv.size() / 2;
-    TACO_TRY(s.leaves.ensure(8 * lv.size()));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice, st));
+    const PwTree tree = pairwise_tree(n);
+    // layout: (off, len) per leaf as int64, then left[ni], right[ni], level_start[] as int32
+    std::vector<char> blob(8 * lv.size() + 4 * (tree.left.size() + tree.right.size() + tree.level_start.size()));
+    char* bp = blob.data();
+    memcpy(bp, lv.data(), 8 * lv.size());
+    bp += 8 * lv.size();
+    memcpy(bp, tree.left.data(), 4 * tree.left.size());
+    bp += 4 * tree.left.size();
+    memcpy(bp, tree.right.data(), 4 * tree.right.size());
+    bp += 4 * tree.right.size();
+    memcpy(bp, tree.level_start.data(), 4 * tree.level_start.size());
+    TACO_TRY(s.leaves.ensure(blob.size()));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaStreamSynchronize(st));
     s.leaves_n = n;
   }
   TACO_TRY(s.pbuf.ensure(8 * std::max<int64_t>(n, s.nleaves)));
-  TACO_TRY(s.cbuf.ensure(8 * n));   // replay cdf
+  TACO_TRY(s.cbuf.ensure(8 * std::max<int64_t>(n, 2 * s.nleaves)));   // replay cdf / leaf + node sums
   const size_t ash = sizeof(double) * ((size_t)k * m + k);
   auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
   if (ash > 48 * 1024)
@@ -1330,6 +1551,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
     return (int)std::max<size_t>(1, (size_t)(0.85 * (double)fr) / per_half);
   };
   int NS = std::min({H, 16, fit()});
+  if (const char* e = getenv("TACO_KM_HALVES")) NS = std::max(1, std::min(NS, atoi(e)));   // experiments
   if (NS < std::min(H, 16)) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) {
@@ -1534,7 +1756,7 @@ int taco_get_local_sizes(taco_index* idx, int64_t* sizes_h) {
 
 // Test hook: 1 = every k-means++ draw takes the exact numpy replay path.
 int taco_debug_force_replay(int on) {
-  g_force_replay = on ? 1 : 0;
+  g_force_replay = on;   // 1: every draw replays (parallel exact cumsum); 2: replays with the sequential chain
   return TACO_OK;
 }
 

@@ -142,12 +142,21 @@ def test_kmeans_exact_replay_path():
     from paper_2603_24919_b200 import _native as nat
     nat.call("taco_debug_force_replay", 1)
     try:
-        for shape, k, seed in [((5000, 8), 64, 1), ((3001, 5), 17, 4), ((1000, 3), 40, 13)]:
+        for shape, k, seed in [((5000, 8), 64, 1), ((3001, 5), 17, 4), ((1000, 3), 40, 13),
+                               ((200_000, 6), 16, 7)]:
             X = np.random.default_rng(seed).normal(size=shape).astype(np.float32)
+            if shape[0] > 100_000:
+                X[::3] *= 1e-3   # wide value range: many binade changes inside the cumsum
             r = T.kmeans(X, k, 10, seed)
             o = O.kmeans(X, k, 10, seed)
             np.testing.assert_array_equal(r.assignments, o.labels)
             np.testing.assert_array_equal(r.centroids, o.centroids)
+            # the parallel exact cumsum (mode 1) == the sequential chain (mode 2)
+            nat.call("taco_debug_force_replay", 2)
+            r2 = T.kmeans(X, k, 10, seed)
+            nat.call("taco_debug_force_replay", 1)
+            np.testing.assert_array_equal(r.assignments, r2.assignments)
+            np.testing.assert_array_equal(r.centroids, r2.centroids)
     finally:
         nat.call("taco_debug_force_replay", 0)
 
