@@ -769,7 +769,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
 // 256 threads walks its 1024-point blocks, 4 points per thread, reading each
 // point's coordinates as float4s from the point-major copy.
 template <int MP>
-__global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const float* __restrict__ xp,
+__global__ void __launch_bounds__(PP_THREADS, 3) k_pp_step(HalfView h, const float* __restrict__ xp,
                                                         const double* __restrict__ xsq, int ci,
                                                         double* __restrict__ best, double* __restrict__ C64,
                                                         double* __restrict__ bsum, int64_t nb,
@@ -780,7 +780,6 @@ __global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const float*
                                                         double* __restrict__ lsum, double* __restrict__ pbuf,
                                                         double* __restrict__ cbuf, int force_replay) {
   __shared__ double cv[MP];
-  __shared__ double red[PP_THREADS / 32];
   __shared__ double s_csq;
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -795,46 +794,54 @@ __global__ void __launch_bounds__(PP_THREADS) k_pp_step(HalfView h, const float*
   }
   __syncthreads();
   const double csq = s_csq;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+  // Warp-granular: each warp owns whole 1024-point blocks (32 points per lane,
+  // in batches with all loads in flight) and reduces them with shuffles, so no
+  // CTA barrier sits between a block's loads and the next block's.
+  const int64_t nwarps = (int64_t)gridDim.x * (PP_THREADS / 32);
+  const int64_t gw = (int64_t)blockIdx.x * (PP_THREADS / 32) + wid;
+  constexpr int UB = MP <= 8 ? 4 : MP <= 16 ? 2 : 1;   // points per lane per batch
+  for (int64_t b = gw; b < nb; b += nwarps) {
     double part = 0.0;
+    for (int u0 = 0; u0 < PP_BLOCK / 32; u0 += UB) {
+      float xv[UB][MP];
+      double ob[UB];
+      int64_t ii[UB];
 #pragma unroll
-    for (int u = 0; u < PP_PPT; ++u) {
-      const int64_t i = b * PP_BLOCK + (int64_t)u * PP_THREADS + tid;
-      if (i < h.n) {
-        const float4* src = reinterpret_cast<const float4*>(xp + (size_t)i * MP);
-        float xv[MP];
+      for (int u = 0; u < UB; ++u) {
+        ii[u] = b * PP_BLOCK + (int64_t)(u0 + u) * 32 + lane;
+        const bool live = ii[u] < h.n;
+        const float4* src = reinterpret_cast<const float4*>(xp + (size_t)(live ? ii[u] : 0) * MP);
 #pragma unroll
         for (int q = 0; q < MP / 4; ++q) {
-          const float4 v = __ldcs(src + q);
-          xv[4 * q] = v.x; xv[4 * q + 1] = v.y; xv[4 * q + 2] = v.z; xv[4 * q + 3] = v.w;
+          const float4 v = live ? __ldcs(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          xv[u][4 * q] = v.x; xv[u][4 * q + 1] = v.y; xv[u][4 * q + 2] = v.z; xv[u][4 * q + 3] = v.w;
         }
-        double dot = 0.0;
+        ob[u] = (live && ci > 0) ? best[ii[u]] : 0.0;
+      }
 #pragma unroll
-        for (int t = 0; t < MP; ++t)
-          if (t < m) dot = __fma_rn((double)xv[t], cv[t], dot);
-        // xsq recomputed in the einsum order of k_xsq (bit-identical) instead of an 8 B/point read
-        const double xs = einsum_sq([&](int t) { return (double)xv[t]; }, m);
-        const double d2 = sq_dist_expand(xs, dot, csq);
-        double bb = d2;
-        if (ci > 0) {
-          const double old = best[i];
-          if (d2 < old) best[i] = d2; else bb = old;
-        } else {
-          best[i] = d2;
+      for (int u = 0; u < UB; ++u) {
+        if (ii[u] < h.n) {
+          double dot = 0.0;
+#pragma unroll
+          for (int t = 0; t < MP; ++t)
+            if (t < m) dot = __fma_rn((double)xv[u][t], cv[t], dot);
+          // xsq recomputed in the einsum order of k_xsq (bit-identical) instead of an 8 B/point read
+          const double xs = einsum_sq([&](int t) { return (double)xv[u][t]; }, m);
+          const double d2 = sq_dist_expand(xs, dot, csq);
+          double bb = d2;
+          if (ci > 0) {
+            if (d2 < ob[u]) best[ii[u]] = d2; else bb = ob[u];
+          } else {
+            best[ii[u]] = d2;
+          }
+          part = __dadd_rn(part, bb);
         }
-        part = __dadd_rn(part, bb);
       }
     }
     for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-    if (lane == 0) red[wid] = part;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < PP_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
-      bsum[b] = t;
-    }
-    __syncthreads();
+    if (lane == 0) bsum[b] = part;
   }
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
     s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 6), 1ull) ==
@@ -1010,7 +1017,7 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned byt
 // shared-memory ring (full/empty mbarriers), and the first m lanes of the
 // consumer warp run the m dependent add chains at the DADD latency.  The
 // producer warp's other lanes commit the new labels (lab = newlab).
-constexpr int CS_R = 64, CS_ST = 8, CS_THREADS = 64;
+constexpr int CS_R = 64, CS_ST = 8, CS_THREADS = 96;   // warp 0 chains, warp 1 (one lane) TMA, warp 2 labels
 template <int MP>
 __global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const PointRec<MP>* __restrict__ xs,
                                                              const int64_t* __restrict__ status,
@@ -1040,25 +1047,26 @@ __global__ void __launch_bounds__(CS_THREADS) k_cluster_sums(HalfView h, const P
   __syncthreads();
   const PointRec<MP>* run = xs + s_start;
   const int64_t ntile = (cnt + CS_R - 1) / CS_R;
-  if (tid > 32) {
-    // commit the labels of this iteration (lab = newlab) while the chains run:
-    // CTA c copies its slice with 16-byte accesses, 8 in flight per lane
+  if (tid >= 64) {
+    // commit the labels of this iteration (lab = newlab) while the chains run
+    // (own warp, so the TMA producer lane never waits behind it): CTA c copies
+    // its slice with 16-byte accesses, 8 in flight per lane
     const int64_t per = ((h.n + gridDim.x - 1) / gridDim.x + 3) & ~(int64_t)3;
     const int64_t i0 = min(h.n, (int64_t)c * per), i1 = min(h.n, i0 + per);
     const bool al = ((reinterpret_cast<uintptr_t>(newlab) | reinterpret_cast<uintptr_t>(lab)) & 15) == 0;
     const int64_t v0 = i0 >> 2, v1 = al ? i1 >> 2 : v0;   // whole int4s (i0 is a multiple of 4)
     const int4* src = reinterpret_cast<const int4*>(newlab);
     int4* dst = reinterpret_cast<int4*>(lab);
-    for (int64_t b = v0 + (tid - 33); b < v1; b += 31 * 8) {
+    for (int64_t b = v0 + (tid - 64); b < v1; b += 32 * 8) {
       int4 t[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (b + u * 31 < v1) t[u] = __ldcs(src + b + u * 31);
+        if (b + u * 32 < v1) t[u] = __ldcs(src + b + u * 32);
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (b + u * 31 < v1) dst[b + u * 31] = t[u];
+        if (b + u * 32 < v1) dst[b + u * 32] = t[u];
     }
-    for (int64_t i = (al ? v1 << 2 : i0) + (tid - 33); i < i1; i += 31) lab[i] = newlab[i];
+    for (int64_t i = (al ? v1 << 2 : i0) + (tid - 64); i < i1; i += 32) lab[i] = newlab[i];
   } else if (tid == 32 && cnt > 0) {
     // producer: one elected thread streams the run
     for (int64_t tb = 0; tb < ntile; ++tb) {
@@ -1214,44 +1222,22 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   const int64_t nbx = ceil_div(n, 256);
   const int64_t nbp = ceil_div(n, PP_BLOCK);
   const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
-  TACO_TRY(s.xsq.ensure(8 * n));
-  TACO_TRY(s.best.ensure(8 * n));
-  TACO_TRY(s.bsum.ensure(8 * std::max(nbp, nbx)));
-  TACO_TRY(s.picks.ensure(8 * k));
-  TACO_TRY(s.uni.ensure(8 * std::max(k, 1)));
-  TACO_TRY(s.forced.ensure(8 * std::max(k, 1)));
-  TACO_TRY(s.status.ensure(8 * 8));
-  TACO_TRY(s.C64.ensure(8 * (size_t)k * m));
-  TACO_TRY(s.newlab.ensure(4 * n));
-  TACO_TRY(s.pd.ensure(8 * n));
-  TACO_TRY(s.keys2.ensure(4 * n));
-  TACO_TRY(s.ctl.ensure(8 * 2 * (size_t)k));   // per-cluster counts, double buffered by iteration parity
-  TACO_TRY(s.hsum.ensure(8 * nba));
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
-  TACO_TRY(s.xp.ensure(4 * (size_t)n * mp));
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
   size_t cub_bytes = 0;
   if (mp == 8) TACO_TRY(label_sort<8>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
   else if (mp == 16) TACO_TRY(label_sort<16>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
   else TACO_TRY(label_sort<32>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
-  TACO_TRY(s.cubtmp.ensure(std::max<size_t>(cub_bytes, 16)));
-  if (mp == 32) {
-    TACO_TRY(s.perm.ensure(4 * n));
-    if (s.iota.bytes < 4 * (size_t)n) {
-      TACO_TRY(s.iota.ensure(4 * n));
-      k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
-      TACO_LAUNCHED();
-    }
-  }
-  TACO_TRY(s.xs.ensure(4 * (size_t)n * mp));
-  if (s.leaves_n != n) {                // numpy pairwise leaves of an n-array (exact replay)
+  // host side of the exact replay: numpy's pairwise leaves and combine tree for n
+  std::vector<char> blob;
+  if (s.leaves_n != n || s.leaf_blob.empty()) {
     std::vector<int64_t> lv;
     pairwise_leaves(0, n, lv);
     s.nleaves = (int64_t)lv.size() / 2;
     const PwTree tree = pairwise_tree(n);
     // layout: (off, len) per leaf as int64, then left[ni], right[ni], level_start[] as int32
-    std::vector<char> blob(8 * lv.size() + 4 * (tree.left.size() + tree.right.size() + tree.level_start.size()));
+    blob.resize(8 * lv.size() + 4 * (tree.left.size() + tree.right.size() + tree.level_start.size()));
     char* bp = blob.data();
     memcpy(bp, lv.data(), 8 * lv.size());
     bp += 8 * lv.size();
@@ -1260,13 +1246,37 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
     memcpy(bp, tree.right.data(), 4 * tree.right.size());
     bp += 4 * tree.right.size();
     memcpy(bp, tree.level_start.data(), 4 * tree.level_start.size());
-    TACO_TRY(s.leaves.ensure(blob.size()));
-    TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+    s.leaf_blob.swap(blob);
     s.leaves_n = n;
   }
-  TACO_TRY(s.pbuf.ensure(8 * std::max<int64_t>(n, s.nleaves)));
-  TACO_TRY(s.cbuf.ensure(8 * std::max<int64_t>(n, 2 * s.nleaves)));   // replay cdf / leaf + node sums
+  // One arena per half (a single pool allocation: the ~20 scratch buffers
+  // used to cost ~20 allocations each, which dominated the warm build's
+  // host time when the pool had to map memory)
+  struct Cut { DevBuf* b; size_t bytes; };
+  const Cut cuts[] = {
+      {&s.xsq, 8 * (size_t)n}, {&s.best, 8 * (size_t)n}, {&s.bsum, 8 * (size_t)std::max(nbp, nbx)},
+      {&s.picks, 8 * (size_t)k}, {&s.uni, 8 * (size_t)std::max(k, 1)}, {&s.forced, 8 * (size_t)std::max(k, 1)},
+      {&s.status, 8 * 8}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
+      {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)nba},
+      {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.cubtmp, std::max<size_t>(cub_bytes, 16)},
+      {&s.perm, mp == 32 ? 4 * (size_t)n : 0}, {&s.iota, mp == 32 ? 4 * (size_t)n : 0},
+      {&s.leaves, s.leaf_blob.size()}, {&s.pbuf, 8 * (size_t)std::max<int64_t>(n, s.nleaves)},
+      {&s.cbuf, 8 * (size_t)std::max<int64_t>(n, 2 * s.nleaves)}};
+  size_t total = 0;
+  for (const Cut& c : cuts) total += (c.bytes + 255) & ~(size_t)255;
+  TACO_TRY(s.arena.ensure(total));
+  {
+    char* base = s.arena.as<char>();
+    for (const Cut& c : cuts) {
+      c.b->view_of(base, c.bytes);
+      base += (c.bytes + 255) & ~(size_t)255;
+    }
+  }
+  if (mp == 32) {
+    k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
+    TACO_LAUNCHED();
+  }
+  TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, s.leaf_blob.data(), s.leaf_blob.size(), cudaMemcpyHostToDevice, st));
   const size_t ash = sizeof(double) * ((size_t)k * m + k);
   auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
   if (ash > 48 * 1024)
@@ -1572,6 +1582,8 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   for (int w0 = 0; w0 < H; w0 += NS) {
     const int w1 = std::min(H, w0 + NS);
     std::vector<KMeansRun> runs;
+    timespec tp0;
+    clock_gettime(CLOCK_MONOTONIC, &tp0);
     for (int hh = w0; hh < w1; ++hh) {
       const int j = hh / 2, b = hh % 2;
       KMeansRun r;
@@ -1610,6 +1622,9 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
       return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
     };
     const double tg0 = now_ms();
+    if (gdbg)
+      fprintf(stderr, "[taco] k-means prepare (allocations, draw-plan upload) %.2f ms\n",
+              tg0 - (tp0.tv_sec * 1e3 + tp0.tv_nsec * 1e-6));
     int erc = TACO_OK;
     auto forced_of = [&](int hh) { return forced_h ? forced_h + (size_t)hh * std::max(kp - 1, 0) : nullptr; };
     if (graph) {
@@ -1669,7 +1684,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   for (auto& bs : idx->bs) {
     DevBuf* sb[] = {&bs.xsq, &bs.best, &bs.bsum, &bs.picks, &bs.uni, &bs.forced, &bs.status, &bs.C64, &bs.csq,
                     &bs.newlab, &bs.pd, &bs.changed, &bs.perm, &bs.lhist, &bs.loff, &bs.ctl, &bs.hsum, &bs.draws,
-                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp, &bs.xs};
+                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp, &bs.xs, &bs.arena};
     for (auto* b : sb) b->release();
     bs.leaves_n = -1;
   }
@@ -1805,7 +1820,7 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
   X.release(); lab.release(); hist.release(); nit.release(); cent.release();
   DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
                   &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws,
-                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs};
+                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs, &s.arena};
   for (auto* b : sb) b->release();
   return rc;
 }

@@ -3,7 +3,9 @@
 #include <atomic>
 #include <cstring>
 #include <mutex>
-#include <omp.h>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <vector>
 
 #include "index.cuh"
@@ -66,6 +68,12 @@ void QueryTile::release() {
 }
 
 void DevBuf::release() {
+  if (view) {
+    p = nullptr;
+    bytes = 0;
+    view = false;
+    return;
+  }
   if (p) {
     cudaDeviceSynchronize();
     cudaFreeAsync(p, cudaStreamLegacy);
@@ -253,7 +261,7 @@ int taco_index_destroy(taco_index* idx) {
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
                     &s.csq, &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl,
-                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs};
+                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs, &s.arena};
     for (auto* b : sb) b->release();
   }
   for (auto st : idx->half_streams) cudaStreamDestroy(st);
@@ -348,6 +356,65 @@ static std::mutex g_stage_mu;
 static char* g_stage[kStages] = {nullptr, nullptr, nullptr};
 static cudaEvent_t g_stage_ev[kStages] = {nullptr, nullptr, nullptr};
 
+// Host copy workers for the staged upload: plain threads that BLOCK between
+// jobs (an OpenMP team would spin for ~100 ms after each region and starve
+// the launch thread of the build that follows).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    // never destroyed: the workers block on cv_ for the life of the process, and
+    // destroying a condition variable with waiters at exit can hang the exit
+    static CopyPool* p = new CopyPool();
+    return *p;
+  }
+  // dst[0, len) = src[0, len) split over the workers; returns when done
+  void copy(char* dst, const char* src, size_t len) {
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = dst;
+    src_ = src;
+    len_ = len;
+    pending_ = (int)workers_.size();
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  CopyPool() {
+    const int n = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+    for (int t = 0; t < n; ++t) workers_.emplace_back([this, t, n] { run(t, n); });
+    for (auto& w : workers_) w.detach();
+  }
+  void run(int t, int n) {
+    uint64_t seen = 0;
+    for (;;) {
+      char* d;
+      const char* s;
+      size_t len;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        d = dst_;
+        s = src_;
+        len = len_;
+      }
+      const size_t a0 = len * t / n, a1 = len * (t + 1) / n;
+      memcpy(d + a0, s + a0, a1 - a0);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> workers_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t len_ = 0;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
 int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   cudaPointerAttributes pa;
   const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
@@ -366,17 +433,13 @@ int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   }
   const char* s = static_cast<const char*>(src);
   char* d = static_cast<char*>(dst);
-  int nthr = std::min(16, omp_get_num_procs());
+  CopyPool& pool = CopyPool::get();
   for (size_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
     const int b = (int)(i % kStages);
     const size_t len = std::min(kStageBytes, bytes - off);
     TACO_CHECK_CUDA(cudaEventSynchronize(g_stage_ev[b]));   // buffer b drained
     char* stg = g_stage[b];
-#pragma omp parallel for num_threads(nthr) schedule(static)
-    for (int t = 0; t < 64; ++t) {
-      const size_t a0 = len * t / 64, a1 = len * (t + 1) / 64;
-      memcpy(stg + a0, s + off + a0, a1 - a0);
-    }
+    pool.copy(stg, s + off, len);
     TACO_CHECK_CUDA(cudaMemcpyAsync(d + off, stg, len, cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaEventRecord(g_stage_ev[b], st));
   }

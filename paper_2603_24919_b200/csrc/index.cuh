@@ -31,8 +31,15 @@ constexpr int64_t kClusterMaxN = kClusterMaxChunk8 * kClusterMaxCtas;
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool view = false;   // a window into another buffer (an arena): release() only forgets it
   int ensure(size_t want);
   void release();
+  void view_of(void* base, size_t b) {
+    release();
+    p = b ? base : nullptr;
+    bytes = b;
+    view = b != 0;
+  }
   template <typename T>
   T* as() const { return static_cast<T*>(p); }
 };
@@ -48,7 +55,8 @@ struct QueryTile {
 
 struct BuildScratch {
   DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
-      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp, xs;
+      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp, xs, arena;
+  std::vector<char> leaf_blob;   // host copy of the pairwise leaves + combine tree (exact replay)
   int64_t nleaves = 0, leaves_n = -1;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // TACO_DEBUG_TIMING
 };
