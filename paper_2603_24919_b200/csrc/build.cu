@@ -858,6 +858,7 @@ __global__ void __launch_bounds__(PP_THREADS, 3) k_pp_step(HalfView h, const flo
 
 // ------------------------------------------------------------------ Lloyd
 constexpr int AS_THREADS = 256;
+constexpr int AS_CU = 4;   // centroids in flight per thread in k_assign
 // Lloyd assignment (clustering.py:86-89): d2 = max((xsq - 2 x.c) + csq, 0)
 // with x.c one FMA chain over t (dgemm order), first argmin.  Each thread
 // owns PPT points so every centroid coordinate read from shared memory feeds
@@ -872,26 +873,33 @@ __global__ void __launch_bounds__(AS_THREADS) k_assign(HalfView h, const double*
                                                        double* __restrict__ hsum,
                                                        unsigned long long* __restrict__ cnt_cur,
                                                        unsigned long long* __restrict__ cnt_next) {
-  extern __shared__ double ash[];
+  extern __shared__ __align__(16) double ash[];
   __shared__ int lhist[256];
   if (status[2]) return;
   for (int c = threadIdx.x; c < h.k; c += AS_THREADS) lhist[c] = 0;
   if (blockIdx.x == 0)
     for (int c = threadIdx.x; c < h.k; c += AS_THREADS) cnt_next[c] = 0ull;
   const int m = h.m;
-  double* C = ash;                    // k*m
-  double* csq = ash + (size_t)h.k * m; // k
+  // centroids at a compile-time stride MM, zero padded: a padded coordinate
+  // adds fma(0, 0, acc) = acc exactly (up to the sign of a zero, which the
+  // distance cannot see), so the inner loop has no bounds checks
+  double* C = ash;                       // k*MM
+  double* csq = ash + (size_t)h.k * MM;  // k
   __shared__ double red[AS_THREADS / 32];
   __shared__ int chg;
-  for (int e = threadIdx.x; e < h.k * m; e += AS_THREADS) C[e] = C64[e];
+  for (int e = threadIdx.x; e < h.k * MM; e += AS_THREADS) {
+    const int c = e / MM, t = e - c * MM;
+    C[e] = t < m ? C64[(size_t)c * m + t] : 0.0;
+  }
   if (threadIdx.x == 0) chg = 0;
   __syncthreads();
   for (int c = threadIdx.x; c < h.k; c += AS_THREADS)
-    csq[c] = einsum_sq([&](int t) { return C[c * m + t]; }, m);
+    csq[c] = einsum_sq([&](int t) { return C[c * MM + t]; }, m);
   __syncthreads();
   const int64_t i0 = (int64_t)blockIdx.x * AS_THREADS * PPT + threadIdx.x;
   double x[PPT][MM], xs[PPT], bd[PPT];
   int bl[PPT];
+  bool pos[PPT];   // bd > 0: while false (bd == 0) no later centroid can win (strict <)
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
     const int64_t i = i0 + (int64_t)j * AS_THREADS;
@@ -899,28 +907,59 @@ __global__ void __launch_bounds__(AS_THREADS) k_assign(HalfView h, const double*
 #pragma unroll
     for (int t = 0; t < MM; ++t) x[j][t] = (t < m && live) ? (double)h.X[(size_t)t * h.n + i] : 0.0;
     xs[j] = live ? xsq[i] : 0.0;
-    bd[j] = 0.0;
+    bd[j] = INFINITY;
     bl[j] = 0;
+    pos[j] = true;
   }
-  for (int c = 0; c < h.k; ++c) {
-    const double* cr = C + c * m;
-    double acc[PPT];
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
-#pragma unroll
-    for (int t = 0; t < MM; ++t) {
-      if (t < m) {
-        const double cv = cr[t];
-#pragma unroll
-        for (int j = 0; j < PPT; ++j) acc[j] = __fma_rn(x[j][t], cv, acc[j]);
-      }
-    }
+  // AS_CU centroids at a time: AS_CU x PPT independent FMA chains per thread
+  // (the latency of one dgemm-order chain is hidden by the others), compared
+  // in ascending centroid order so the first argmin still wins
+  auto visit = [&](int c, const double (&acc)[PPT]) {
     const double cs = csq[c];
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const double d2 = sq_dist_expand(xs[j], acc[j], cs);
-      if (c == 0 || d2 < bd[j]) { bd[j] = d2; bl[j] = c; }
+      // clustering._sq_dists: (xsq - 2 dot) + csq, clamped at 0; xsq - 2 dot is
+      // one FMA (2 dot is exact), the clamp is applied only on an update:
+      // max(v, 0) < bd  <=>  v < bd  whenever bd > 0
+      const double v = __dadd_rn(__fma_rn(-2.0, acc[j], xs[j]), cs);
+      if (v < bd[j] && pos[j]) {
+        bd[j] = v > 0.0 ? v : 0.0;
+        pos[j] = v > 0.0;
+        bl[j] = c;
+      }
     }
+  };
+  int c0 = 0;
+  for (; c0 + AS_CU <= h.k; c0 += AS_CU) {
+    double acc[AS_CU][PPT];
+#pragma unroll
+    for (int t2 = 0; t2 < MM / 2; ++t2) {
+#pragma unroll
+      for (int u = 0; u < AS_CU; ++u) {
+        const double2 cv = reinterpret_cast<const double2*>(C + (c0 + u) * MM)[t2];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          // dgemm order: one FMA chain over t from 0 (fma(x0, c0, 0) = x0 * c0)
+          acc[u][j] = t2 == 0 ? __dmul_rn(x[j][0], cv.x) : __fma_rn(x[j][2 * t2], cv.x, acc[u][j]);
+          acc[u][j] = __fma_rn(x[j][2 * t2 + 1], cv.y, acc[u][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < AS_CU; ++u) visit(c0 + u, acc[u]);
+  }
+  for (; c0 < h.k; ++c0) {
+    double acc[PPT];
+#pragma unroll
+    for (int t2 = 0; t2 < MM / 2; ++t2) {
+      const double2 cv = reinterpret_cast<const double2*>(C + c0 * MM)[t2];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        acc[j] = t2 == 0 ? __dmul_rn(x[j][0], cv.x) : __fma_rn(x[j][2 * t2], cv.x, acc[j]);
+        acc[j] = __fma_rn(x[j][2 * t2 + 1], cv.y, acc[j]);
+      }
+    }
+    visit(c0, acc);
   }
   double my = 0.0;
   int changed = 0;
@@ -1221,7 +1260,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   if (k > 256) TACO_FAIL(TACO_ERR_PARAMETER, "codebook size %d exceeds 256", k);
   const int64_t nbx = ceil_div(n, 256);
   const int64_t nbp = ceil_div(n, PP_BLOCK);
-  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
+  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS);
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
@@ -1277,8 +1316,8 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
     TACO_LAUNCHED();
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, s.leaf_blob.data(), s.leaf_blob.size(), cudaMemcpyHostToDevice, st));
-  const size_t ash = sizeof(double) * ((size_t)k * m + k);
-  auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
+  const size_t ash = sizeof(double) * ((size_t)k * (m <= 8 ? 8 : m <= 16 ? 16 : 32) + k);
+  auto* kas = m <= 8 ? k_assign<8, 1> : m <= 16 ? k_assign<16, 1> : k_assign<32, 1>;
   if (ash > 48 * 1024)
     TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
   const size_t css = sizeof(float) * CS_ST * CS_R * mp;
@@ -1314,7 +1353,7 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
   const int m = h.m;
   const int64_t nbx = ceil_div(n, 256);
   const int64_t nbp = ceil_div(n, PP_BLOCK);
-  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS * (m <= 8 ? 4 : m <= 16 ? 2 : 1));
+  const int64_t nba = ceil_div(n, (int64_t)AS_THREADS);
   int lbits = 1;
   while ((1 << lbits) < k) ++lbits;
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
@@ -1348,8 +1387,8 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
   }
   if (step <= k + r.iters) {
     const int it = step - k - 1;
-    const size_t ash = sizeof(double) * ((size_t)k * m + k);
-    auto* kas = m <= 8 ? k_assign<8, 4> : m <= 16 ? k_assign<16, 2> : k_assign<32, 1>;
+    const size_t ash = sizeof(double) * ((size_t)k * (m <= 8 ? 8 : m <= 16 ? 16 : 32) + k);
+    auto* kas = m <= 8 ? k_assign<8, 1> : m <= 16 ? k_assign<16, 1> : k_assign<32, 1>;
     const size_t css = sizeof(float) * CS_ST * CS_R * mp;
     unsigned long long* cc = cnt + (size_t)(it & 1) * k;
     unsigned long long* cn = cnt + (size_t)((it + 1) & 1) * k;
