@@ -376,7 +376,9 @@ __device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_
       // consume: units tid, tid + CT_THREADS, ... with one unit of lookahead
       const int nr = (int)(r1 - r0);
       uint32_t ev = 0, od = 0;   // per-round level tallies (small), 8-bit fields
-      uint32_t va[8], vb[8];
+      uint32_t va[8], vb[8];   // lanes past a unit's length keep a valid id of this chunk (+0 atomics)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) va[e] = vb[e] = (uint32_t)base;
       int la = 0, lb = 0;
       auto fetch = [&](int k, uint32_t* v, int& l) {
         l = 0;
@@ -388,25 +390,27 @@ __device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_
             if (e < l) v[e] = __ldg(src + e);
         }
       };
+      // All of a unit's atomics are issued before any returned word is used
+      // (they are independent: the latencies overlap), lanes past the unit's
+      // length add 0 to a word they already own (no branches, no effect).
       auto apply = [&](const uint32_t* v, int l) {
+        uint32_t sh[8], ad[8], old[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          // table word of id x lives at tsg + (x >> 1 or x) & ~3: tsg absorbs the chunk base
+          // (a multiple of 1024, so the lane position within the word is x's own low bits)
+          const uint32_t x = v[e];
+          sh[e] = NIB ? (x << 2) & 28u : (x << 3) & 24u;
+          ad[e] = tsg + (NIB ? ((x >> 1) & ~3u) : (x & ~3u));
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) old[e] = smem_atomic_add(ad[e], e < l ? 1u << sh[e] : 0u);
         uint32_t u4 = 0;   // small: 8 x 4-bit fields "left level v" (<= 8 ids per unit)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          if (e < l) {
-            // table word of id x lives at tsg + (x >> 1 or x) & ~3: tsg absorbs the chunk base
-            // (a multiple of 1024, so the lane position within the word is x's own low bits)
-            const uint32_t x = v[e];
-            uint32_t r;
-            if (NIB) {   // 4-bit counters: scores <= n_sub <= 15 never carry
-              const uint32_t sh = (x << 2) & 28u;
-              r = smem_atomic_add(tsg + ((x >> 1) & ~3u), 1u << sh) >> sh;
-            } else {
-              const uint32_t sh = (x << 3) & 24u;
-              r = smem_atomic_add(tsg + (x & ~3u), 1u << sh) >> sh;
-            }
-            if (small) u4 += 1u << ((r << 2) & 28u);
-            else T.add_wide(r & (NIB ? 0xFu : 0xFFu));
-          }
+          const uint32_t r = old[e] >> sh[e];
+          if (small) u4 += e < l ? 1u << ((r << 2) & 28u) : 0u;
+          else if (e < l) T.add_wide(r & (NIB ? 0xFu : 0xFFu));
         }
         if (small) {   // <= CT_UC / CT_THREADS units per round: 8-bit fields cannot overflow
           ev += u4 & 0x0F0F0F0Fu;
@@ -415,12 +419,13 @@ __device__ void count_chunk_impl(const uint16_t* __restrict__ pops, const int32_
       };
       int k = tid;
       fetch(k, va, la);
-      while (k < nr) {
+      while (k < nr) {   // ping-pong buffers: no register moves between units
         fetch(k + CT_THREADS, vb, lb);
         apply(va, la);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) va[e] = vb[e];
-        la = lb;
+        k += CT_THREADS;
+        if (k >= nr) break;
+        fetch(k + CT_THREADS, va, la);
+        apply(vb, lb);
         k += CT_THREADS;
       }
       if (small) T.add_round(ev, od);
