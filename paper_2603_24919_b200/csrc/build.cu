@@ -1049,6 +1049,257 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned byt
       : "memory");
 }
 
+// ---- Lloyd assignment on the tensor cores (m <= 8): the distance GEMM
+// X[128 x 8] . C^T[8 x N] of each 128-point tile runs as three tcgen05 TF32
+// MMAs (x_hi c_hi + x_hi c_lo + x_lo c_hi, hi = tf32(x), lo = tf32(x - hi):
+// ~fp32-accurate products, fp32 accumulation in TMEM).  Thread r of the CTA
+// owns TMEM lane r (point r): it reads the N approximate dot products, forms
+// d2f = (xsq - 2 dot) + csq in fp32 and a bound e = 2^-14 (xsq + max csq) on
+// |d2f - d2_ref| (TF32x3 products and accumulation <= 2^-17 A, A <= (xsq +
+// csq)/2; fp32 formation <= 2^-22 (xsq + csq)), then re-evaluates in the
+// reference's fp64 formula only the centroids whose interval can still hold
+// the minimum -- the first exact argmin is the reference's label and point_d2.
+constexpr int TC_THREADS = 128;
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// K-major, no swizzle: 8-row x 16-byte core matrices; the two K halves of an
+// 8-row group 128 B apart (LBO), 8-row groups 256 B apart (SBO)
+__device__ __forceinline__ int tc_off(int row, int k) {   // float index inside an operand tile
+  return (row >> 3) * 64 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t tc_desc(const void* smem) {
+  const uint64_t a = (uint64_t)((smem_u32(smem) >> 4) & 0x3FFF);
+  const uint64_t lbo = 128 >> 4, sbo = 256 >> 4;
+  return a | (lbo << 16) | (sbo << 32) | (1ull << 46);   // version 1 (sm_100), SWIZZLE_NONE, base offset 0
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const float* __restrict__ xp,
+                                                          const double* __restrict__ xsq,
+                                                          const double* __restrict__ C64,
+                                                          const int32_t* __restrict__ lab,
+                                                          int32_t* __restrict__ newlab,
+                                                          double* __restrict__ pd, int iter,
+                                                          int64_t* __restrict__ status,
+                                                          double* __restrict__ hsum,
+                                                          unsigned long long* __restrict__ cnt_cur,
+                                                          unsigned long long* __restrict__ cnt_next, int npad) {
+  extern __shared__ __align__(128) float tsm[];
+  float* Ahi = tsm;                       // 128 x 8
+  float* Alo = Ahi + TC_THREADS * 8;
+  float* Bhi = Alo + TC_THREADS * 8;      // npad x 8
+  float* Blo = Bhi + npad * 8;
+  double* C = reinterpret_cast<double*>(Blo + npad * 8);   // k x 8 (fp64, zero padded)
+  double* csq = C + (size_t)h.k * 8;
+  float* ca = reinterpret_cast<float*>(csq + h.k + (h.k & 1));   // [npad] RU(csq (1 + K)) (+inf for pads), 16-B aligned
+  float* cb_ = ca + npad;                              // [npad] RD(csq (1 - K))
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  __shared__ int lhist[256];
+  __shared__ double red[TC_THREADS / 32];
+  __shared__ int chg;
+  if (status[2]) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, m = h.m, k = h.k;
+  for (int c = tid; c < k; c += TC_THREADS) lhist[c] = 0;
+  if (blockIdx.x == 0)
+    for (int c = tid; c < k; c += TC_THREADS) cnt_next[c] = 0ull;
+  for (int e = tid; e < npad * 8; e += TC_THREADS) {
+    const int c = e >> 3, t = e & 7;
+    const double cv = (c < k && t < m) ? C64[(size_t)c * m + t] : 0.0;
+    if (c < k) C[e] = cv;
+    const float cf = __double2float_rn(cv);
+    const float hi = tf32_rna(cf);
+    Bhi[tc_off(c, t)] = hi;
+    Blo[tc_off(c, t)] = tf32_rna(cf - hi);
+  }
+  if (tid == 0) {
+    chg = 0;
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (wid == 0) {
+    uint32_t ncols = 32;
+    while ((int)ncols < npad) ncols <<= 1;
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  __syncthreads();
+  // |d2_fp32 - d2_ref| <= K (xsq + csq_c), K = 2^-14 (see above): the
+  // centroid part is folded into per-centroid constants, the point part K xsq
+  // is added to the threshold
+  constexpr float KB = 6.103515625e-05f;
+  for (int c = tid; c < npad; c += TC_THREADS) {
+    if (c < k) {
+      const double v = einsum_sq([&](int t) { return C[c * 8 + t]; }, m);
+      csq[c] = v;
+      ca[c] = __double2float_ru(v * (1.0 + 6.103515625e-05));
+      cb_[c] = __double2float_rd(v * (1.0 - 6.103515625e-05));
+    } else {
+      ca[c] = INFINITY;
+      cb_[c] = INFINITY;
+    }
+  }
+  __syncthreads();
+  const uint32_t tmem = tmem_base;
+  // tf32 . tf32 -> f32, both operands K-major, M = 128, N = npad
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(npad >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint64_t dAhi = tc_desc(Ahi), dAlo = tc_desc(Alo), dBhi = tc_desc(Bhi), dBlo = tc_desc(Blo);
+  const int64_t ntiles = (h.n + TC_THREADS - 1) / TC_THREADS;
+  double my = 0.0;
+  int changed = 0;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TC_THREADS + tid;
+    const bool live = i < h.n;
+    float x[8];
+    {
+      const float4* src = reinterpret_cast<const float4*>(xp + (size_t)(live ? i : 0) * 8);
+      const float4 a = live ? __ldg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 b = live ? __ldg(src + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+    const double xs = live ? xsq[i] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float hi = tf32_rna(x[t]);
+      Ahi[tc_off(tid, t)] = hi;
+      Alo[tc_off(tid, t)] = tf32_rna(x[t] - hi);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy smem writes -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      tc_mma(tmem, dAhi, dBhi, idesc, 0u);
+      tc_mma(tmem, dAhi, dBlo, idesc, 1u);
+      tc_mma(tmem, dAlo, dBhi, idesc, 1u);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar))
+                   : "memory");
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // this thread's row: TMEM lane tid, columns [0, npad).  With g = csq - 2 dot
+    // (xsq is common to every centroid): pass 1 takes min_c RU(a_c - 2 dot),
+    // pass 2 keeps the centroids with RD(b_c - 2 dot) <= that + 2 K xsq.
+    const uint32_t trow = tmem + ((uint32_t)(wid * 32) << 16);
+    auto tld = [&](int cb, float (&v)[16]) {
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(trow + (uint32_t)(cb * 16)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __uint_as_float(r[u]);
+    };
+    float gmin = INFINITY;
+    for (int cb = 0; cb * 16 < npad; ++cb) {
+      float v[16];
+      tld(cb, v);
+      const float4* a4 = reinterpret_cast<const float4*>(ca + cb * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 a = a4[q];
+        gmin = fminf(gmin, __fmaf_ru(-2.f, v[4 * q + 0], a.x));
+        gmin = fminf(gmin, __fmaf_ru(-2.f, v[4 * q + 1], a.y));
+        gmin = fminf(gmin, __fmaf_ru(-2.f, v[4 * q + 2], a.z));
+        gmin = fminf(gmin, __fmaf_ru(-2.f, v[4 * q + 3], a.w));
+      }
+    }
+    const float xsu = __double2float_ru(xs);
+    const float thr = __fadd_ru(gmin, __fmul_ru(2.f * KB, xsu));
+    // pass 2: candidate masks (16 centroids per block) and the least lower bound
+    uint32_t cm[8];   // npad <= 256: 16 blocks of 16 bits
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cm[q] = 0u;
+    float lmin = INFINITY;
+#pragma unroll
+    for (int cb = 0; cb < 16; ++cb) {
+      if (cb * 16 < npad) {
+        float v[16];
+        tld(cb, v);
+        const float4* b4 = reinterpret_cast<const float4*>(cb_ + cb * 16);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 bq = b4[q];
+          const float l0 = __fmaf_rd(-2.f, v[4 * q + 0], bq.x), l1 = __fmaf_rd(-2.f, v[4 * q + 1], bq.y);
+          const float l2 = __fmaf_rd(-2.f, v[4 * q + 2], bq.z), l3 = __fmaf_rd(-2.f, v[4 * q + 3], bq.w);
+          mask |= ((uint32_t)(l0 <= thr) << (4 * q)) | ((uint32_t)(l1 <= thr) << (4 * q + 1)) |
+                  ((uint32_t)(l2 <= thr) << (4 * q + 2)) | ((uint32_t)(l3 <= thr) << (4 * q + 3));
+          lmin = fminf(lmin, fminf(fminf(l0, l1), fminf(l2, l3)));
+        }
+        cm[cb >> 1] |= mask << ((cb & 1) * 16);
+      }
+    }
+    // every reference value provably > 0 unless xs (1 - K) + lmin <= 0: then the
+    // clamp at 0 may tie several centroids and all of them are evaluated
+    const bool clampy = !(__fadd_rd(__fmul_rd(__double2float_rd(xs), 1.f - KB), lmin) > 0.f);
+    double bd = INFINITY;
+    int bl = 0;
+    bool pos = true;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q * 32 < npad) {
+        uint32_t mask = clampy ? 0xFFFFFFFFu : cm[q];
+        while (mask) {
+          const int u = __ffs(mask) - 1;
+          mask &= mask - 1u;
+          const int c = q * 32 + u;
+          if (c >= k) break;
+          const double* cr = C + c * 8;
+          double acc = __dmul_rn((double)x[0], cr[0]);
+#pragma unroll
+          for (int t = 1; t < 8; ++t) acc = __fma_rn((double)x[t], cr[t], acc);   // padded t >= m add exact zeros
+          const double dv = __dadd_rn(__fma_rn(-2.0, acc, xs), csq[c]);
+          if (dv < bd && pos) {
+            bd = dv > 0.0 ? dv : 0.0;
+            pos = dv > 0.0;
+            bl = c;
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    if (live) {
+      newlab[i] = bl;
+      atomicAdd(&lhist[bl], 1);
+      pd[i] = bd;
+      my = __dadd_rn(my, bd);
+      if (iter > 0 && lab[i] != bl) changed = 1;
+    }
+    __syncthreads();   // A tiles and TMEM free for the next tile
+  }
+  if (__any_sync(0xffffffffu, changed) && lane == 0) atomicOr(&chg, 1);
+  for (int o = 16; o > 0; o >>= 1) my = __dadd_rn(my, __shfl_xor_sync(0xffffffffu, my, o));
+  if (lane == 0) red[wid] = my;
+  __syncthreads();
+  for (int c = tid; c < k; c += TC_THREADS)
+    if (lhist[c]) atomicAdd(&cnt_cur[c], (unsigned long long)lhist[c]);
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < TC_THREADS / 32; ++w) t = __dadd_rn(t, red[w]);
+    hsum[blockIdx.x] = t;
+    if (chg) atomicAdd((unsigned long long*)&status[4], 1ull);
+  }
+  if (wid == 0) {
+    uint32_t ncols = 32;
+    while ((int)ncols < npad) ncols <<= 1;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+  }
+}
+
 // centroid = (sequential fp64 sum over the cluster's points in index order) /
 // count -- the np.add.at order (clustering.py:95-99).  The label sort leaves
 // cluster c's records contiguous (index order inside the cluster), so one CTA
@@ -1296,7 +1547,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
       {&s.xsq, 8 * (size_t)n}, {&s.best, 8 * (size_t)n}, {&s.bsum, 8 * (size_t)std::max(nbp, nbx)},
       {&s.picks, 8 * (size_t)k}, {&s.uni, 8 * (size_t)std::max(k, 1)}, {&s.forced, 8 * (size_t)std::max(k, 1)},
       {&s.status, 8 * 8}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
-      {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)nba},
+      {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)std::max<int64_t>(nba, ceil_div(n, TC_THREADS))},   // fp64 or tensor-core assign partials
       {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.cubtmp, std::max<size_t>(cub_bytes, 16)},
       {&s.perm, mp == 32 ? 4 * (size_t)n : 0}, {&s.iota, mp == 32 ? 4 * (size_t)n : 0},
       {&s.leaves, s.leaf_blob.size()}, {&s.pbuf, 8 * (size_t)std::max<int64_t>(n, s.nleaves)},
@@ -1320,6 +1571,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   auto* kas = m <= 8 ? k_assign<8, 1> : m <= 16 ? k_assign<16, 1> : k_assign<32, 1>;
   if (ash > 48 * 1024)
     TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
+  TACO_CHECK_CUDA(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
   const size_t css = sizeof(float) * CS_ST * CS_R * mp;
   if (css > 48 * 1024) {
     if (mp == 8) TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
@@ -1336,6 +1588,17 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   }
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   return TACO_OK;
+}
+
+// Lloyd assignment on the tensor cores (k_assign_tc) for half widths <= 8;
+// TACO_TC_ASSIGN=0 keeps the all-fp64 k_assign (both give the same labels).
+static bool use_tc_assign(int m, int k) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("TACO_TC_ASSIGN");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env && m <= 8 && k <= 256;
 }
 
 // The enqueue of one k-means run is cut into steps -- 0: xsq and the
@@ -1392,11 +1655,29 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
     const size_t css = sizeof(float) * CS_ST * CS_R * mp;
     unsigned long long* cc = cnt + (size_t)(it & 1) * k;
     unsigned long long* cn = cnt + (size_t)((it + 1) & 1) * k;
-    kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,
-                                                s.newlab.as<int32_t>(), s.pd.as<double>(), it,
-                                                s.status.as<int64_t>(), s.hsum.as<double>(), cc, cn);
+    int64_t nb_h = nba;   // hsum entries written by the assignment
+    if (use_tc_assign(m, k)) {
+      const int npad = (k + 15) & ~15;
+      const int64_t ntiles = ceil_div(n, TC_THREADS);
+      const int G = (int)std::min<int64_t>(ntiles, 4 * g_num_sms());
+      // at most 7 of these CTAs per SM (smem-limited), so their TMEM columns
+      // (<= 64 each for K' <= 64) never exceed the SM's 512 and no CTA blocks in
+      // tcgen05.alloc behind another half's kernel
+      const size_t tsmem = sizeof(float) * (2 * TC_THREADS * 8 + 2 * (size_t)npad * 8) +
+                           sizeof(double) * ((size_t)k * 8 + k + 1) + sizeof(float) * 2 * npad;
+      const int ncols = npad <= 32 ? 32 : npad <= 64 ? 64 : npad <= 128 ? 128 : 256;
+      const size_t tsm_launch = std::max(tsmem, (size_t)(228 * 1024) / (size_t)(512 / ncols) + 1024);
+      k_assign_tc<<<G, TC_THREADS, tsm_launch, st>>>(h, s.xp.as<float>(), s.xsq.as<double>(), s.C64.as<double>(),
+                                               r.labels, s.newlab.as<int32_t>(), s.pd.as<double>(), it,
+                                               s.status.as<int64_t>(), s.hsum.as<double>(), cc, cn, npad);
+      nb_h = G;
+    } else {
+      kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,
+                                                  s.newlab.as<int32_t>(), s.pd.as<double>(), it,
+                                                  s.status.as<int64_t>(), s.hsum.as<double>(), cc, cn);
+    }
     TACO_LAUNCHED();
-    k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nba, it, s.status.as<int64_t>(), r.history,
+    k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nb_h, it, s.status.as<int64_t>(), r.history,
                                     r.n_iter);
     TACO_LAUNCHED();
     // stable radix sort of the point records by label (index order inside a label)

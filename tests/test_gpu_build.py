@@ -208,3 +208,29 @@ def test_device_jacobi_golden_and_cap(golden):
     A = np.random.default_rng(0).normal(size=(12, 12))
     rc, *_ , res = _jac(A + A.T, True, max_sweeps=1)
     assert rc == 5 and res > 0
+
+
+def test_tensor_core_assign_matches_fp64_assign(tmp_path):
+    """k_assign_tc (tcgen05 TF32x3 bound + exact fp64 recheck) and the
+    all-fp64 k_assign (TACO_TC_ASSIGN=0) give bit-identical k-means runs,
+    including duplicate points (seeds that clamp at distance 0) and K' not a
+    multiple of 16 (padded tensor-core N)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); import paper_2603_24919_b200 as T\n"
+        "rng = np.random.default_rng(3); X = (rng.normal(size=(20000, 7)) * 40).astype(np.float32)\n"
+        "X[500:900] = X[0]; X[900:950] = X[7]\n"
+        "out = []\n"
+        "for k, it in ((50, 6), (64, 4), (100, 3)):\n"
+        "    r = T.kmeans(X, k, it, 11)\n"
+        "    out += [r.assignments.astype(np.float64), r.centroids.ravel().astype(np.float64), np.array(r.inertia_history)]\n"
+        "np.save(sys.argv[1], np.concatenate(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = {}
+    for tc in ("0", "1"):
+        f = tmp_path / f"r{tc}.npy"
+        subprocess.run([sys.executable, "-c", code, str(f)], check=True,
+                       env=dict(os.environ, TACO_TC_ASSIGN=tc))
+        res[tc] = np.load(f)
+    np.testing.assert_array_equal(res["0"], res["1"])
