@@ -89,20 +89,25 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restrict__ X, int64_t n, int d,
+// Rows [r0, r1) of the chain; state[] carries each column's running sum
+// between launches (r0 == 0 starts from X[0]), and the launch that reaches
+// row n divides (the staged upload runs one launch per landed chunk).
+__global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restrict__ X, int64_t r0g, int64_t r1g,
+                                                            int64_t n, int d, double* __restrict__ state,
                                                             double* __restrict__ mean) {
   extern __shared__ __align__(16) float cm[];
   const int c0 = blockIdx.x * CM_W;
   const int nc = min(CM_W, d - c0);
   const int tid = threadIdx.x;
-  const int64_t ntile = (n + CM_ROWS - 1) / CM_ROWS;
+  const int64_t nrow = r1g - r0g;
+  const int64_t ntile = (nrow + CM_ROWS - 1) / CM_ROWS;
   const bool vec = (d % 4 == 0) && (nc % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   const int ptid = tid - 32;   // producer index (warps 1..3)
   auto load = [&](int64_t tb) {
     if (tb < ntile) {
       float* dst = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W;
-      const int64_t r0 = tb * CM_ROWS;
-      const int rr = (int)min((int64_t)CM_ROWS, n - r0);
+      const int64_t r0 = r0g + tb * CM_ROWS;
+      const int rr = (int)min((int64_t)CM_ROWS, r1g - r0);
       if (vec) {
         const int per = nc / 4;
         for (int e = ptid; e < rr * per; e += CM_THREADS - 32) {
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restr
   };
   if (tid >= 32)
     for (int s = 0; s < CM_STAGES - 1; ++s) load(s);
-  double acc = 0.0;
+  double acc = (r0g > 0 && tid < nc) ? state[c0 + tid] : 0.0;
   for (int64_t tb = 0; tb < ntile; ++tb) {
     if (tid >= 32) cp_wait<CM_STAGES - 2>();   // tile tb has landed (this thread's pieces)
     __syncthreads();                             // ... everyone's; slot (tb-1)%S is free
@@ -128,12 +133,28 @@ __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restr
       load(tb + CM_STAGES - 1);
     } else if (tid < nc) {
       const float* tv = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W + tid;
-      const int rr = (int)min((int64_t)CM_ROWS, n - tb * CM_ROWS);
-      if (tb == 0) acc = chain_add((double)tv[0], tv + CM_W, rr - 1, CM_W);
+      const int rr = (int)min((int64_t)CM_ROWS, nrow - tb * CM_ROWS);
+      if (tb == 0 && r0g == 0) acc = chain_add((double)tv[0], tv + CM_W, rr - 1, CM_W);
       else acc = chain_add(acc, tv, rr, CM_W);
     }
   }
-  if (tid < nc) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
+  if (tid < nc) {
+    state[c0 + tid] = acc;
+    if (r1g == n) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
+  }
+}
+
+int launch_colmean(cudaStream_t st, const float* X, int64_t r0, int64_t r1, int64_t n, int d, double* state,
+                   double* mean) {
+  static bool attr = false;
+  if (!attr) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_colmean_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM));
+    attr = true;
+  }
+  if (r1 <= r0) return TACO_OK;
+  k_colmean_seq<<<(unsigned)ceil_div(d, CM_W), CM_THREADS, CM_SMEM, st>>>(X, r0, r1, n, d, state, mean);
+  TACO_LAUNCHED();
+  return TACO_OK;
 }
 
 constexpr int GT = 64, GK = 16;
@@ -1805,8 +1826,8 @@ int ensure_half_streams(taco_index* idx, int want) {
 extern "C" {
 
 static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, double* mean_h,
-                           double* gram_h, int64_t* bad_row) {
-  DevBuf bad, mean, part, G;
+                           double* gram_h, int64_t* bad_row, const double* mean_ready = nullptr) {
+  DevBuf bad, mean, part, G, cstate;
   int rc = TACO_OK;
   do {
     if ((rc = bad.ensure(8)) || (rc = mean.ensure(8 * d)) || (rc = G.ensure(8 * (size_t)d * d))) break;
@@ -1820,10 +1841,12 @@ static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, d
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; break; }
     *bad_row = b == ~0ull ? -1 : (int64_t)b;
     if (b != ~0ull) break;
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_colmean_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)CM_SMEM));
-    k_colmean_seq<<<(unsigned)ceil_div(d, CM_W), CM_THREADS, CM_SMEM, st>>>(Xd, n, d, mean.as<double>());
-    count_launch();
+    if (mean_ready) {   // the column mean was chained while X was being uploaded
+      TACO_CHECK_CUDA(cudaMemcpyAsync(mean.p, mean_ready, 8 * (size_t)d, cudaMemcpyDeviceToDevice, st));
+    } else {
+      if ((rc = cstate.ensure(8 * (size_t)d))) break;
+      if ((rc = launch_colmean(st, Xd, 0, n, n, d, cstate.as<double>(), mean.as<double>()))) break;
+    }
     const int tiles = (int)ceil_div(d, GT);
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(592, tiles * tiles), ceil_div(n, 256)));
     const int64_t rows_per = ceil_div(ceil_div(n, splits), GK) * GK;
@@ -1840,14 +1863,19 @@ static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, d
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; }
   } while (0);
-  bad.release(); mean.release(); part.release(); G.release();
+  bad.release(); mean.release(); part.release(); G.release(); cstate.release();
   return rc;
 }
 
 int taco_fit_covariance(taco_index* idx, double* mean_h, double* gram_h, int64_t* bad_row) {
   TACO_TRY(index_check(idx));
   if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "no data uploaded");
-  return covariance_impl(idx->X.as<float>(), idx->n, idx->d, idx->stream, mean_h, gram_h, bad_row);
+  const double* mr = nullptr;
+  if (idx->mean_ready) {   // chained during the staged upload on the aux stream
+    TACO_CHECK_CUDA(cudaStreamSynchronize(idx->aux));
+    mr = idx->colmean.as<double>();
+  }
+  return covariance_impl(idx->X.as<float>(), idx->n, idx->d, idx->stream, mean_h, gram_h, bad_row, mr);
 }
 
 int taco_covariance(int device, const float* X_h, int64_t n, int32_t d, double* mean_h, double* gram_h,

@@ -268,6 +268,9 @@ int taco_index_destroy(taco_index* idx) {
   for (auto e : idx->half_ev) cudaEventDestroy(e);
   if (idx->km_fork) cudaEventDestroy(idx->km_fork);
   if (idx->stream2) cudaStreamDestroy(idx->stream2);
+  if (idx->aux) cudaStreamDestroy(idx->aux);
+  idx->colstate.release();
+  idx->colmean.release();
   if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
   if (idx->ev_join) cudaEventDestroy(idx->ev_join);
   cudaStreamDestroy(idx->stream);
@@ -415,7 +418,8 @@ class CopyPool {
   uint64_t gen_ = 0;
 };
 
-int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st,
+               const std::function<int(size_t, cudaEvent_t)>& on_chunk) {
   cudaPointerAttributes pa;
   const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
@@ -442,6 +446,7 @@ int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     pool.copy(stg, s + off, len);
     TACO_CHECK_CUDA(cudaMemcpyAsync(d + off, stg, len, cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaEventRecord(g_stage_ev[b], st));
+    if (on_chunk) TACO_TRY(on_chunk(off + len, g_stage_ev[b]));   // bytes [0, off + len) have landed once ev fires
   }
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   return TACO_OK;
@@ -452,7 +457,26 @@ int taco_index_set_data(taco_index* idx, const float* X_h) {
   TACO_TRY(index_check(idx));
   size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
   TACO_TRY(idx->X.ensure(bytes));
-  TACO_TRY(upload_h2d(idx->X.p, X_h, bytes, idx->stream));
+  // the sequential column-mean chain of fit_covariance follows the staged
+  // upload chunk by chunk on the aux stream (it is bound by the DADD latency,
+  // the upload by PCIe: run together they overlap)
+  idx->mean_ready = false;
+  if (!idx->aux) TACO_CHECK_CUDA(cudaStreamCreateWithFlags(&idx->aux, cudaStreamNonBlocking));
+  TACO_TRY(idx->colstate.ensure(8 * (size_t)idx->d));
+  TACO_TRY(idx->colmean.ensure(8 * (size_t)idx->d));
+  int64_t rows_done = 0;
+  const size_t row_bytes = sizeof(float) * (size_t)idx->d;
+  auto on_chunk = [&](size_t landed, cudaEvent_t ev) -> int {
+    const int64_t rows = (int64_t)(landed / row_bytes);
+    if (rows <= rows_done) return TACO_OK;
+    TACO_CHECK_CUDA(cudaStreamWaitEvent(idx->aux, ev, 0));
+    TACO_TRY(launch_colmean(idx->aux, idx->X.as<float>(), rows_done, rows, idx->n, idx->d,
+                            idx->colstate.as<double>(), idx->colmean.as<double>()));
+    rows_done = rows;
+    return TACO_OK;
+  };
+  TACO_TRY(upload_h2d(idx->X.p, X_h, bytes, idx->stream, on_chunk));
+  idx->mean_ready = rows_done == idx->n;
   idx->has_X = true;
   return narrow_rows(idx);
 }
@@ -464,6 +488,7 @@ int32_t taco_index_row_format(const taco_index* idx) {
 
 int taco_index_set_data_device(taco_index* idx, const float* X_d) {
   TACO_TRY(index_check(idx));
+  idx->mean_ready = false;
   size_t bytes = (size_t)idx->n * idx->d * sizeof(float);
   TACO_TRY(idx->X.ensure(bytes));
   TACO_CHECK_CUDA(cudaMemcpyAsync(idx->X.p, X_d, bytes, cudaMemcpyDeviceToDevice, idx->stream));

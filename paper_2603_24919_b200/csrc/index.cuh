@@ -82,6 +82,9 @@ struct taco_index {
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<taco::BuildScratch> bs;
+  cudaStream_t aux = nullptr;          // column-mean chain that runs behind the staged upload
+  taco::DevBuf colstate, colmean;
+  bool mean_ready = false;
 };
 
 namespace taco {
@@ -90,4 +93,6 @@ int index_check(taco_index* idx);
 // kernels shared between translation units
 int launch_transform(cudaStream_t st, const float* P, int64_t np_, int d, int D,
                      const float* mean, const float* M, float* out, bool dim_major);
+int launch_colmean(cudaStream_t st, const float* X, int64_t r0, int64_t r1, int64_t n, int d, double* state,
+                   double* mean);
 }  // namespace taco

@@ -222,15 +222,19 @@ def test_tensor_core_assign_matches_fp64_assign(tmp_path):
         "import sys, numpy as np; sys.path.insert(0, %r); import paper_2603_24919_b200 as T\n"
         "rng = np.random.default_rng(3); X = (rng.normal(size=(20000, 7)) * 40).astype(np.float32)\n"
         "X[500:900] = X[0]; X[900:950] = X[7]\n"
-        "out = []\n"
+        "out, hist = [], []\n"
         "for k, it in ((50, 6), (64, 4), (100, 3)):\n"
         "    r = T.kmeans(X, k, it, 11)\n"
-        "    out += [r.assignments.astype(np.float64), r.centroids.ravel().astype(np.float64), np.array(r.inertia_history)]\n"
-        "np.save(sys.argv[1], np.concatenate(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        "    out += [r.assignments.astype(np.float64), r.centroids.ravel().astype(np.float64)]\n"
+        "    hist.append(np.array(r.inertia_history))\n"
+        "np.save(sys.argv[1], np.concatenate(out)); np.save(sys.argv[1] + '.h.npy', np.concatenate(hist))\n"
+        % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     res = {}
     for tc in ("0", "1"):
         f = tmp_path / f"r{tc}.npy"
         subprocess.run([sys.executable, "-c", code, str(f)], check=True,
                        env=dict(os.environ, TACO_TC_ASSIGN=tc))
-        res[tc] = np.load(f)
-    np.testing.assert_array_equal(res["0"], res["1"])
+        res[tc] = (np.load(f), np.load(str(f) + ".h.npy"))
+    np.testing.assert_array_equal(res["0"][0], res["1"][0])   # labels and centroids: bit-identical
+    # the inertia history is a tree sum whose grouping follows the kernel's grid
+    np.testing.assert_allclose(res["0"][1], res["1"][1], rtol=1e-12)
