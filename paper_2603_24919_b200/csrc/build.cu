@@ -422,12 +422,18 @@ __device__ void cumsum_exact_block(const double* __restrict__ best, double total
       long long lp[CX_V];
       long long tsum = 0;
       int tie = CX_V;
+      double bv[CX_V];   // this thread's values: loads first (all in flight), then the quotients
+#pragma unroll
+      for (int v = 0; v < CX_V; ++v) {
+        const int64_t k = j0 + (int64_t)tid * CX_V + v;
+        bv[v] = k < n ? __ldcg(best + k) : 0.0;
+      }
 #pragma unroll
       for (int v = 0; v < CX_V; ++v) {
         const int64_t k = j0 + (int64_t)tid * CX_V + v;
         long long q = 0;
         if (k < n) {
-          const double t = __dmul_rn(P(k), inv);   // exact power-of-two scaling
+          const double t = __dmul_rn(__ddiv_rn(bv[v], total), inv);   // p_k, then exact power-of-two scaling
           if (t >= 0x1p60) {
             q = 1LL << 60;                         // certainly leaves the binade
           } else {
@@ -569,7 +575,6 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   }
   __syncthreads();
   __shared__ int s_ok;
-  __shared__ double s_total;
   __shared__ double s_scan[PP_BLOCK];
   __shared__ int s_k;
   int64_t blk = s_blk;
@@ -653,7 +658,26 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
     if (s_ok) picks[draw] = kstar;
   }
   __syncthreads();
-  if (s_ok) return;
+  if (!s_ok && tid == 0) status[7] = draw;   // undecided: k_pp_replay (next launch) replays numpy exactly
+}
+
+// The exact replay of Generator.choice(n, p=best/total) for draw ci + 1 when
+// the certified search could not decide (status[7] == draw): its own launch of
+// one 1024-thread CTA (4x the warps of a k_pp_step CTA to hide the latencies
+// of the division / scan chain), a no-op otherwise.
+constexpr int RP_THREADS = 1024;
+__global__ void __launch_bounds__(RP_THREADS) k_pp_replay(HalfView h, const double* __restrict__ best,
+                                                          const double* __restrict__ uni, int ci,
+                                                          int64_t* __restrict__ picks, int64_t* __restrict__ status,
+                                                          const int64_t* __restrict__ leaves, int64_t nleaves,
+                                                          double* __restrict__ lsum, double* __restrict__ pbuf,
+                                                          double* __restrict__ cbuf, int force_replay) {
+  const int draw = ci + 1;
+  if (__ldcg(status + 7) != draw) return;
+  const int tid = threadIdx.x;
+  const int NT = blockDim.x;
+  const double u = uni[ci];
+  __shared__ double s_total;
   // ---- exact replay of Generator.choice(n, p=best/total) (clustering.py:48):
   // total = numpy pairwise sum; p = best/total; cdf = sequential cumsum;
   // idx = first i with fl(cdf_i / cdf_last) > u.  Everything but the cumsum
@@ -671,11 +695,16 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
         off = leaves[2 * l];
         len = leaves[2 * l + 1];
         if (len >= 8) {
+          // this lane's strided accumulator: all (<= 16) loads in flight, then the adds
           const double* a = best + off;
-          r = __ldcg(a + j);
-          const int64_t full = len - (len % 8);
-#pragma unroll 4
-          for (int64_t i = 8; i < full; i += 8) r = __dadd_rn(r, __ldcg(a + i + j));
+          const int nb8 = (int)(len / 8);
+          double v[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) v[t] = t < nb8 ? __ldcg(a + 8 * t + j) : 0.0;
+          r = v[0];
+#pragma unroll
+          for (int t = 1; t < 16; ++t)
+            if (t < nb8) r = __dadd_rn(r, v[t]);
         }
       }
       r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
@@ -780,6 +809,7 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
     }
     picks[draw] = hi;
     status[1] += 1;
+    status[7] = 0;
   }
 }
 
@@ -1468,6 +1498,7 @@ __global__ void k_centroids_out(const double* __restrict__ C64, int km, float* _
 __global__ void k_status_init(int64_t* status, int k) {
   status[5] = 0;
   status[6] = 0;
+  status[7] = 0;
   status[0] = k;
   status[1] = 0;
   status[2] = 0;
@@ -1666,6 +1697,13 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
                    s.picks.as<int64_t>(), s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
                    s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
     TACO_LAUNCHED();
+    if (ci + 1 < k) {
+      k_pp_replay<<<1, RP_THREADS, 0, st>>>(h, s.best.as<double>(), s.uni.as<double>(), ci, s.picks.as<int64_t>(),
+                                            s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
+                                            s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(),
+                                            g_force_replay);
+      TACO_LAUNCHED();
+    }
     if (ci == k - 1 && timing) cudaEventRecord(s.ev[1], st);
     return TACO_OK;
   }
