@@ -249,22 +249,36 @@ struct HalfView {
 };
 
 __global__ void k_xsq(HalfView h, double* __restrict__ xsq, int64_t* __restrict__ status) {
-  __shared__ double red[32];
+  __shared__ double red[32], reds[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (i < h.n) {
     v = einsum_sq([&](int t) { return (double)h.X[(size_t)t * h.n + i]; }, h.m);
     xsq[i] = v;
   }
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  double sv = v;
+  for (int o = 16; o > 0; o >>= 1) {
+    v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = v;
+    reds[threadIdx.x >> 5] = sv;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
     double w = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
-    // non-negative doubles order like their bit patterns
-    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(status + 5),
-                                    (unsigned long long)__double_as_longlong(w));
+    double ws = threadIdx.x < (blockDim.x >> 5) ? reds[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+      ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    }
+    // non-negative doubles order like their bit patterns; the sum of xsq (a
+    // bound input, any order) for the k-means++ certificate
+    if (threadIdx.x == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(status + 5), (unsigned long long)__double_as_longlong(w));
+      atomicAdd(reinterpret_cast<double*>(status + 8), ws);
+    }
   }
 }
 
@@ -651,8 +665,13 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
     // rounding of its dgemv-ordered dot products: |delta d2| <= 8u(|x|+|c|)^2.
     const double n = (double)h.n;
     const double rel = ((double)kstar + n + 1200.0) * U0 * 1.05;
-    const double xsqmax = __longlong_as_double((long long)status[5]);
-    const double absU = 32.0 * U0 * n * xsqmax;
+    // |best_i(ours) - best_i(reference)| <= 16u (xsq_i + max csq of the chosen
+    // centroids) (dgemv vs FMA-chain dot products, (|x|+|c|)^2 <= 2(xsq + csq)),
+    // summed over the points: 16u (sum xsq + n csqmax); the sum of xsq carries a
+    // 1e-9 relative slack for its own (order-free) rounding
+    const double xsqsum = __longlong_as_double((long long)__ldcg(status + 8)) * (1.0 + 1e-9);
+    const double csqmax = __longlong_as_double((long long)__ldcg(status + 9));
+    const double absU = 16.0 * U0 * (xsqsum + n * csqmax);
     const double margin = rel * S + 2.0 * absU;
     s_ok = !force_replay && (Pk - target > margin) && (target - Pkm1 >= margin);
     if (s_ok) picks[draw] = kstar;
@@ -840,8 +859,10 @@ __global__ void __launch_bounds__(PP_THREADS, 3) k_pp_step(HalfView h, const flo
   __syncthreads();
   if (tid == 0) {
     s_csq = einsum_sq([&](int t) { return cv[t]; }, m);
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0) {
       for (int t = 0; t < m; ++t) C64[(size_t)ci * m + t] = cv[t];
+      atomicMax(reinterpret_cast<unsigned long long*>(status + 9), (unsigned long long)__double_as_longlong(s_csq));
+    }
   }
   __syncthreads();
   const double csq = s_csq;
@@ -1499,6 +1520,8 @@ __global__ void k_status_init(int64_t* status, int k) {
   status[5] = 0;
   status[6] = 0;
   status[7] = 0;
+  status[8] = 0;   // sum xsq (double bits)
+  status[9] = 0;   // max csq of the chosen centroids (double bits)
   status[0] = k;
   status[1] = 0;
   status[2] = 0;
@@ -1598,7 +1621,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   const Cut cuts[] = {
       {&s.xsq, 8 * (size_t)n}, {&s.best, 8 * (size_t)n}, {&s.bsum, 8 * (size_t)std::max(nbp, nbx)},
       {&s.picks, 8 * (size_t)k}, {&s.uni, 8 * (size_t)std::max(k, 1)}, {&s.forced, 8 * (size_t)std::max(k, 1)},
-      {&s.status, 8 * 8}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
+      {&s.status, 8 * 16}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
       {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)std::max<int64_t>(nba, ceil_div(n, TC_THREADS))},   // fp64 or tensor-core assign partials
       {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.cubtmp, std::max<size_t>(cub_bytes, 16)},
       {&s.perm, mp == 32 ? 4 * (size_t)n : 0}, {&s.iota, mp == 32 ? 4 * (size_t)n : 0},
