@@ -601,24 +601,26 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
     }
     // word u's hits sit at lane tops (bit LW*i + LW-1); shifted by u they are disjoint
     uint32_t m = g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
-    if (__ballot_sync(0xffffffffu, m != 0u) == 0u) continue;
-    const int c = __popc(m);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
+    // one reservation per warp step (total by a warp reduction), then the
+    // hits leave in rounds of one per lane: a ballot ranks the lanes that
+    // still hold one (most steps need 1-2 rounds; no per-lane prefix scan)
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(m));
+    if (tot == 0u) continue;
     int base = 0;
-    if (lane == 31) base = atomicAdd(fill, incl);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    uint32_t* out = dst + (base + incl - c);
+    if (lane == 0) base = atomicAdd(fill, (int)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
     const uint32_t idb = (uint32_t)(id0 + (int64_t)vi * IDS);
-    while (m) {
-      const int b = 31 - __clz(m);                 // highest hit first (order is free)
-      m ^= 1u << b;
-      const int u = LW - 1 - (b & (LW - 1));        // word
-      *out++ = idb + (uint32_t)(u * LPW + b / LW);  // lane b / LW of word u
+    const uint32_t lt = (1u << lane) - 1u;
+    while (true) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
+      if (bal == 0u) break;
+      if (m) {
+        const int b = 31 - __clz(m);                 // highest hit first (order is free)
+        m ^= 1u << b;
+        const int u = LW - 1 - (b & (LW - 1));        // word
+        dst[base + __popc(bal & lt)] = idb + (uint32_t)(u * LPW + b / LW);   // lane b / LW of word u
+      }
+      base += __popc(bal);
     }
   }
 }
