@@ -1137,14 +1137,16 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// K-major, no swizzle: 8-row x 16-byte core matrices; the two K halves of an
-// 8-row group 128 B apart (LBO), 8-row groups 256 B apart (SBO)
+// K-major, no swizzle: 8-row x 16-byte core matrices; the K chunks (4 tf32)
+// of an 8-row group 128 B apart (LBO), 8-row groups MP * 32 B apart (SBO)
+template <int MP>
 __device__ __forceinline__ int tc_off(int row, int k) {   // float index inside an operand tile
-  return (row >> 3) * 64 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+  return (row >> 3) * (MP * 8) + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
+template <int MP>
 __device__ __forceinline__ uint64_t tc_desc(const void* smem) {
   const uint64_t a = (uint64_t)((smem_u32(smem) >> 4) & 0x3FFF);
-  const uint64_t lbo = 128 >> 4, sbo = 256 >> 4;
+  const uint64_t lbo = 128 >> 4, sbo = (uint64_t)(MP * 32) >> 4;
   return a | (lbo << 16) | (sbo << 32) | (1ull << 46);   // version 1 (sm_100), SWIZZLE_NONE, base offset 0
 }
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -1154,6 +1156,7 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+template <int MP>
 __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const float* __restrict__ xp,
                                                           const double* __restrict__ xsq,
                                                           const double* __restrict__ C64,
@@ -1165,12 +1168,12 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
                                                           unsigned long long* __restrict__ cnt_cur,
                                                           unsigned long long* __restrict__ cnt_next, int npad) {
   extern __shared__ __align__(128) float tsm[];
-  float* Ahi = tsm;                       // 128 x 8
-  float* Alo = Ahi + TC_THREADS * 8;
-  float* Bhi = Alo + TC_THREADS * 8;      // npad x 8
-  float* Blo = Bhi + npad * 8;
-  double* C = reinterpret_cast<double*>(Blo + npad * 8);   // k x 8 (fp64, zero padded)
-  double* csq = C + (size_t)h.k * 8;
+  float* Ahi = tsm;                       // 128 x MP
+  float* Alo = Ahi + TC_THREADS * MP;
+  float* Bhi = Alo + TC_THREADS * MP;     // npad x MP
+  float* Blo = Bhi + npad * MP;
+  double* C = reinterpret_cast<double*>(Blo + npad * MP);   // k x MP (fp64, zero padded)
+  double* csq = C + (size_t)h.k * MP;
   float* ca = reinterpret_cast<float*>(csq + h.k + (h.k & 1));   // [npad] RU(csq (1 + K)) (+inf for pads), 16-B aligned
   float* cb_ = ca + npad;                              // [npad] RD(csq (1 - K))
   __shared__ __align__(8) uint64_t mbar;
@@ -1183,14 +1186,14 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
   for (int c = tid; c < k; c += TC_THREADS) lhist[c] = 0;
   if (blockIdx.x == 0)
     for (int c = tid; c < k; c += TC_THREADS) cnt_next[c] = 0ull;
-  for (int e = tid; e < npad * 8; e += TC_THREADS) {
-    const int c = e >> 3, t = e & 7;
+  for (int e = tid; e < npad * MP; e += TC_THREADS) {
+    const int c = e / MP, t = e % MP;
     const double cv = (c < k && t < m) ? C64[(size_t)c * m + t] : 0.0;
     if (c < k) C[e] = cv;
     const float cf = __double2float_rn(cv);
     const float hi = tf32_rna(cf);
-    Bhi[tc_off(c, t)] = hi;
-    Blo[tc_off(c, t)] = tf32_rna(cf - hi);
+    Bhi[tc_off<MP>(c, t)] = hi;
+    Blo[tc_off<MP>(c, t)] = tf32_rna(cf - hi);
   }
   if (tid == 0) {
     chg = 0;
@@ -1211,7 +1214,7 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
   constexpr float KB = 6.103515625e-05f;
   for (int c = tid; c < npad; c += TC_THREADS) {
     if (c < k) {
-      const double v = einsum_sq([&](int t) { return C[c * 8 + t]; }, m);
+      const double v = einsum_sq([&](int t) { return C[c * MP + t]; }, m);
       csq[c] = v;
       ca[c] = __double2float_ru(v * (1.0 + 6.103515625e-05));
       cb_[c] = __double2float_rd(v * (1.0 - 6.103515625e-05));
@@ -1224,7 +1227,8 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
   const uint32_t tmem = tmem_base;
   // tf32 . tf32 -> f32, both operands K-major, M = 128, N = npad
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(npad >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint64_t dAhi = tc_desc(Ahi), dAlo = tc_desc(Alo), dBhi = tc_desc(Bhi), dBlo = tc_desc(Blo);
+  // k-block kb (8 tf32 = two 16-byte chunks) starts 256 B further into each operand
+  const uint64_t dAhi = tc_desc<MP>(Ahi), dAlo = tc_desc<MP>(Alo), dBhi = tc_desc<MP>(Bhi), dBlo = tc_desc<MP>(Blo);
   const int64_t ntiles = (h.n + TC_THREADS - 1) / TC_THREADS;
   double my = 0.0;
   int changed = 0;
@@ -1232,28 +1236,34 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TC_THREADS + tid;
     const bool live = i < h.n;
-    float x[8];
+    float x[MP];
     {
-      const float4* src = reinterpret_cast<const float4*>(xp + (size_t)(live ? i : 0) * 8);
-      const float4 a = live ? __ldg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 b = live ? __ldg(src + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+      const float4* src = reinterpret_cast<const float4*>(xp + (size_t)(live ? i : 0) * MP);
+#pragma unroll
+      for (int q4 = 0; q4 < MP / 4; ++q4) {
+        const float4 a = live ? __ldg(src + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * q4] = a.x; x[4 * q4 + 1] = a.y; x[4 * q4 + 2] = a.z; x[4 * q4 + 3] = a.w;
+      }
     }
     const double xs = live ? xsq[i] : 0.0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < MP; ++t) {
       const float hi = tf32_rna(x[t]);
-      Ahi[tc_off(tid, t)] = hi;
-      Alo[tc_off(tid, t)] = tf32_rna(x[t] - hi);
+      Ahi[tc_off<MP>(tid, t)] = hi;
+      Alo[tc_off<MP>(tid, t)] = tf32_rna(x[t] - hi);
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy smem writes -> tensor core
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      tc_mma(tmem, dAhi, dBhi, idesc, 0u);
-      tc_mma(tmem, dAhi, dBlo, idesc, 1u);
-      tc_mma(tmem, dAlo, dBhi, idesc, 1u);
+#pragma unroll
+      for (int kb = 0; kb < MP / 8; ++kb) {
+        const uint64_t o = (uint64_t)(kb * 256) >> 4;   // descriptor start address is in 16 B units
+        tc_mma(tmem, dAhi + o, dBhi + o, idesc, kb > 0 ? 1u : 0u);
+        tc_mma(tmem, dAhi + o, dBlo + o, idesc, 1u);
+        tc_mma(tmem, dAlo + o, dBhi + o, idesc, 1u);
+      }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar))
                    : "memory");
     }
@@ -1330,10 +1340,10 @@ __global__ void __launch_bounds__(TC_THREADS) k_assign_tc(HalfView h, const floa
           mask &= mask - 1u;
           const int c = q * 32 + u;
           if (c >= k) break;
-          const double* cr = C + c * 8;
+          const double* cr = C + c * MP;
           double acc = __dmul_rn((double)x[0], cr[0]);
 #pragma unroll
-          for (int t = 1; t < 8; ++t) acc = __fma_rn((double)x[t], cr[t], acc);   // padded t >= m add exact zeros
+          for (int t = 1; t < MP; ++t) acc = __fma_rn((double)x[t], cr[t], acc);   // padded t >= m add exact zeros
           const double dv = __dadd_rn(__fma_rn(-2.0, acc, xs), csq[c]);
           if (dv < bd && pos) {
             bd = dv > 0.0 ? dv : 0.0;
@@ -1646,7 +1656,9 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   auto* kas = m <= 8 ? k_assign<8, 1> : m <= 16 ? k_assign<16, 1> : k_assign<32, 1>;
   if (ash > 48 * 1024)
     TACO_CHECK_CUDA(cudaFuncSetAttribute(kas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ash));
-  TACO_CHECK_CUDA(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+  TACO_CHECK_CUDA(cudaFuncSetAttribute(k_assign_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  TACO_CHECK_CUDA(cudaFuncSetAttribute(k_assign_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  TACO_CHECK_CUDA(cudaFuncSetAttribute(k_assign_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const size_t css = sizeof(float) * CS_ST * CS_R * mp;
   if (css > 48 * 1024) {
     if (mp == 8) TACO_CHECK_CUDA(cudaFuncSetAttribute(k_cluster_sums<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)css));
@@ -1673,7 +1685,7 @@ static bool use_tc_assign(int m, int k) {
     const char* e = getenv("TACO_TC_ASSIGN");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env && m <= 8 && k <= 256;
+  return env && m <= 32 && k <= 256;
 }
 
 // The enqueue of one k-means run is cut into steps -- 0: xsq and the
@@ -1745,13 +1757,15 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
       // at most 7 of these CTAs per SM (smem-limited), so their TMEM columns
       // (<= 64 each for K' <= 64) never exceed the SM's 512 and no CTA blocks in
       // tcgen05.alloc behind another half's kernel
-      const size_t tsmem = sizeof(float) * (2 * TC_THREADS * 8 + 2 * (size_t)npad * 8) +
-                           sizeof(double) * ((size_t)k * 8 + k + 1) + sizeof(float) * 2 * npad;
+      const size_t tsmem = sizeof(float) * (2 * TC_THREADS * (size_t)mp + 2 * (size_t)npad * mp) +
+                           sizeof(double) * ((size_t)k * mp + k + 1) + sizeof(float) * 2 * npad;
       const int ncols = npad <= 32 ? 32 : npad <= 64 ? 64 : npad <= 128 ? 128 : 256;
-      const size_t tsm_launch = std::max(tsmem, (size_t)(228 * 1024) / (size_t)(512 / ncols) + 1024);
-      k_assign_tc<<<G, TC_THREADS, tsm_launch, st>>>(h, s.xp.as<float>(), s.xsq.as<double>(), s.C64.as<double>(),
-                                               r.labels, s.newlab.as<int32_t>(), s.pd.as<double>(), it,
-                                               s.status.as<int64_t>(), s.hsum.as<double>(), cc, cn, npad);
+      const size_t tsm_launch =
+          std::min<size_t>(std::max(tsmem, (size_t)(228 * 1024) / (size_t)(512 / ncols) + 1024), 200 * 1024);
+      auto* ktc = mp == 8 ? k_assign_tc<8> : mp == 16 ? k_assign_tc<16> : k_assign_tc<32>;
+      ktc<<<G, TC_THREADS, tsm_launch, st>>>(h, s.xp.as<float>(), s.xsq.as<double>(), s.C64.as<double>(), r.labels,
+                                             s.newlab.as<int32_t>(), s.pd.as<double>(), it, s.status.as<int64_t>(),
+                                             s.hsum.as<double>(), cc, cn, npad);
       nb_h = G;
     } else {
       kas<<<(unsigned)nba, AS_THREADS, ash, st>>>(h, s.xsq.as<double>(), s.C64.as<double>(), r.labels,

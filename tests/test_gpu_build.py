@@ -213,17 +213,19 @@ def test_device_jacobi_golden_and_cap(golden):
 def test_tensor_core_assign_matches_fp64_assign(tmp_path):
     """k_assign_tc (tcgen05 TF32x3 bound + exact fp64 recheck) and the
     all-fp64 k_assign (TACO_TC_ASSIGN=0) give bit-identical k-means runs,
-    including duplicate points (seeds that clamp at distance 0) and K' not a
-    multiple of 16 (padded tensor-core N)."""
+    including duplicate points (seeds that clamp at distance 0), K' not a
+    multiple of 16 (padded tensor-core N) and half widths 7, 12, 16, 30 (one,
+    two and four TF32 k-blocks per product)."""
     import os
     import subprocess
     import sys
     code = (
         "import sys, numpy as np; sys.path.insert(0, %r); import paper_2603_24919_b200 as T\n"
-        "rng = np.random.default_rng(3); X = (rng.normal(size=(20000, 7)) * 40).astype(np.float32)\n"
-        "X[500:900] = X[0]; X[900:950] = X[7]\n"
+        "rng = np.random.default_rng(3)\n"
         "out, hist = [], []\n"
-        "for k, it in ((50, 6), (64, 4), (100, 3)):\n"
+        "for m, k, it in ((7, 50, 6), (7, 64, 4), (7, 100, 3), (12, 64, 3), (16, 40, 3), (30, 64, 3)):\n"
+        "    X = (rng.normal(size=(20000, m)) * 40).astype(np.float32)\n"
+        "    X[500:900] = X[0]; X[900:950] = X[7]\n"
         "    r = T.kmeans(X, k, it, 11)\n"
         "    out += [r.assignments.astype(np.float64), r.centroids.ravel().astype(np.float64)]\n"
         "    hist.append(np.array(r.inertia_history))\n"
