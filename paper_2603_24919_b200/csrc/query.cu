@@ -11,8 +11,8 @@
 //                     through DSMEM, Alg. 5 runs in-cluster and every CTA
 //                     compacts its candidates straight from smem   engine.py:201-251
 //   global mode (large shards / multi-GPU, query tiles):
-//   k_count           per (query, 64 Ki chunk) smem counting -> HBM tables +
-//                     per-chunk histograms;  k_hist_reduce -> (all-reduce across
+//   k_count           per (query, 64 Ki chunk) smem counting -> per-chunk
+//                     histograms + spilled score >= 2 records;  k_hist_reduce -> (all-reduce across
 //                     ranks) -> k_select (Alg. 5) -> k_compact
 //   k_plan_*          32-candidate tiles per candidate segment (two orders)
 //   k_rerank_tma      persistent warp-specialised gather: cp.async.bulk (TMA
@@ -625,6 +625,54 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
   }
 }
 
+// Global-mode spill: the ids of a chunk table with score >= 2 as packed
+// records (chunk position << 8 | score), unordered, warp-contiguous stores.
+// The emit sweep filters them at the query's level L >= 2 instead of
+// re-reading the whole table (a query's candidates are a small fraction of
+// the ids it touched).  *fill ends = record count.
+template <int NT, bool NIB>
+__device__ void compact_records(const uint8_t* tab, int valid, uint32_t* dst, int* fill) {
+  constexpr int LW = NIB ? 4 : 8;
+  constexpr int LPW = 32 / LW;
+  constexpr int IDS = 4 * LPW;
+  constexpr uint32_t MASK = (1u << LW) - 1u;
+  const uint32_t D = NIB ? 14u * 0x11111111u : 254u * 0x01010101u;   // lanes >= 2
+  const uint4* t4 = reinterpret_cast<const uint4*>(tab);
+  const int nvec = (valid + IDS - 1) / IDS;
+  const int lane = threadIdx.x & 31;
+  for (int v0 = threadIdx.x - lane; v0 < nvec; v0 += NT) {
+    const int vi = v0 + lane;
+    uint32_t w[4] = {0u, 0u, 0u, 0u}, g[4] = {0u, 0u, 0u, 0u};
+    if (vi < nvec) {
+      const uint4 v = t4[vi];
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) g[u] = lanes_ge<NIB>(w[u], D);   // tables are zero past `valid`
+    }
+    uint32_t m = g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(m));
+    if (tot == 0u) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(fill, (int)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t pos0 = (uint32_t)vi * IDS;
+    const uint32_t lt = (1u << lane) - 1u;
+    while (true) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
+      if (bal == 0u) break;
+      if (m) {
+        const int b = 31 - __clz(m);
+        m ^= 1u << b;
+        const int u = LW - 1 - (b & (LW - 1));
+        const int ln = b / LW;
+        const uint32_t sc = (w[u] >> (ln * LW)) & MASK;
+        dst[base + __popc(bal & lt)] = ((pos0 + (uint32_t)(u * LPW + ln)) << 8) | sc;
+      }
+      base += __popc(bal);
+    }
+  }
+}
+
 // Alg. 5 (engine.py:239-249) on a histogram fetched through `get(level)`.
 template <typename Get>
 __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& cand) {
@@ -701,12 +749,13 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 }
 
 // ------------------------------------------------------- global-mode count
-// One CTA per (id chunk, query) over a whole super-tile.  Two sweeps replace
-// HBM score tables: sweep 1 (CNT_HIST) writes the chunk's level histogram,
-// Alg. 5 runs on the (all-reduced) per-query histogram, sweep 2 (CNT_EMIT)
-// recounts the chunk in shared memory and compacts its candidates straight
-// into the query's candidate segment.  CNT_TABLE stores the table itself
-// (count_collisions tap).
+// One CTA per (id chunk, query) over a whole super-tile.  Sweep 1 (CNT_HIST)
+// writes the chunk's level histogram and spills its score >= 2 ids as packed
+// records (not the 32-64 KB table), Alg. 5 runs on the (all-reduced)
+// per-query histogram, sweep 2 (CNT_EMIT) filters the records at the level L
+// straight into the query's candidate segment -- or, when L < 2 or the
+// records overflowed their slot, recounts the chunk in shared memory and
+// compacts it.  CNT_TABLE stores the table itself (count_collisions tap).
 enum { CNT_TABLE = 0, CNT_HIST = 1, CNT_EMIT = 2 };
 template <bool NIB>
 __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
@@ -722,13 +771,42 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
   const int tid = threadIdx.x;
   const int64_t base = c * chunk;
   const int valid = (int)min(chunk, n - base);
+  __shared__ int s_fill;
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  const int rec_cap = tbytes / 4;                  // records per spilled (query, chunk) slot
   if (mode == CNT_EMIT) {
     if (sbase[q] + scnt[q] > cand_cap) return;
+    const int64_t lo = coff[q * nchunks + c];
     const int64_t hi = c + 1 < nchunks ? coff[q * nchunks + c + 1] : scnt[q];
-    if (hi == coff[q * nchunks + c]) return;   // no candidate of this query in this chunk
+    if (hi == lo) return;   // no candidate of this query in this chunk
+    const int L = lvl[q];
+    if (scores && L >= 2) {
+      // the count sweep spilled this chunk's score >= 2 ids unless they overflowed the slot
+      const int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
+      const int rc = valid - pp[0] - pp[1];
+      if (rc <= rec_cap) {
+        const uint32_t* rec = reinterpret_cast<const uint32_t*>(scores + ((size_t)q * nchunks + c) * tbytes);
+        uint32_t* dst = cand + sbase[q] + lo;
+        if (tid == 0) s_fill = 0;
+        __syncthreads();
+        const int lane = tid & 31;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int i0 = tid - lane; i0 < rc; i0 += CT_THREADS) {
+          const int i = i0 + lane;
+          const uint32_t r = i < rc ? rec[i] : 0u;
+          const bool hit = (int)(r & 0xFFu) >= L;
+          const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+          if (bal == 0u) continue;
+          int wb = 0;
+          if (lane == 0) wb = atomicAdd(&s_fill, __popc(bal));
+          wb = __shfl_sync(0xffffffffu, wb, 0);
+          if (hit) dst[wb + __popc(bal & lt)] = (uint32_t)base + (r >> 8);
+        }
+        return;
+      }
+    }
   }
   uint4* t4 = reinterpret_cast<uint4*>(table);
-  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
   for (int i = tid; i < tbytes / 16; i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
@@ -739,37 +817,18 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
                                        cand + sbase[q] + coff[q * nchunks + c], &S.batches);
     return;
   }
-  if ((mode == CNT_TABLE && !NIB) || (mode == CNT_HIST && scores)) {   // HIST: spill the table for the emit sweep
+  if (mode == CNT_TABLE && !NIB) {
     uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * tbytes);
     for (int i = tid; i < tbytes / 16; i += CT_THREADS) dst[i] = t4[i];
   }
-  chunk_levels(table, valid, n_sub, S);
+  if (tid == 0) s_fill = 0;
+  chunk_levels(table, valid, n_sub, S);   // ends with a barrier
+  if (mode == CNT_HIST && scores && n_sub >= 2 && valid - S.lh[0] - S.lh[1] <= rec_cap)
+    compact_records<CT_THREADS, NIB>(table, valid,
+                                     reinterpret_cast<uint32_t*>(scores + ((size_t)q * nchunks + c) * tbytes),
+                                     &s_fill);
   int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
   for (int l = tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
-}
-
-// Global-mode emit sweep: compact each (chunk, query) table spilled by the
-// count sweep (coalesced 16-byte reads from HBM) at the query's level L.
-template <bool NIB>
-__global__ void __launch_bounds__(CT_THREADS) k_emit_table(const uint8_t* __restrict__ tables, int64_t n,
-                                                           int64_t nchunks, int64_t chunk,
-                                                           const int32_t* __restrict__ lvl,
-                                                           const int64_t* __restrict__ sbase,
-                                                           const int64_t* __restrict__ scnt,
-                                                           const int64_t* __restrict__ coff, int64_t cand_cap,
-                                                           uint32_t* __restrict__ cand) {
-  __shared__ int fill;
-  const int64_t c = blockIdx.x, q = blockIdx.y;
-  if (sbase[q] + scnt[q] > cand_cap) return;
-  const int64_t hi = c + 1 < nchunks ? coff[q * nchunks + c + 1] : scnt[q];
-  if (hi == coff[q * nchunks + c]) return;   // no candidate of this query in this chunk
-  const int64_t base = c * chunk;
-  const int valid = (int)min(chunk, n - base);
-  const int64_t tbytes = NIB ? chunk / 2 : chunk;
-  if (threadIdx.x == 0) fill = 0;
-  __syncthreads();
-  compact_unordered<CT_THREADS, NIB>(tables + ((size_t)q * nchunks + c) * tbytes, valid, (uint32_t)lvl[q], base,
-                                     cand + sbase[q] + coff[q * nchunks + c], &fill);
 }
 
 // Level histograms of externally provided score chunks (select_candidates tap).
@@ -1661,7 +1720,7 @@ static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t 
   return TACO_OK;
 }
 
-// global mode: Alg. 5 on `ghist`, then sweep 2 recounts and compacts
+// global mode: Alg. 5 on `ghist`, then sweep 2 emits (records, else recount)
 static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_t* ghist, double beta,
                          cudaStream_t st) {
   const double budget = beta * (double)idx->n_global;   // engine.py:240
@@ -1676,10 +1735,12 @@ static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_
   {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COMPACT, st);
-    auto kern = nib_tables(idx) ? k_emit_table<true> : k_emit_table<false>;
-    kern<<<g, CT_THREADS, 0, st>>>(t.gtab.as<uint8_t>(), idx->n, idx->nchunks, idx->chunk, t.lvl.as<int32_t>(),
-                                   t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap,
-                                   t.cand.as<uint32_t>());
+    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
+    kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, t.gtab.as<uint8_t>(), t.part.as<int32_t>(),
+        t.lvl.as<int32_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap,
+        t.cand.as<uint32_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;

@@ -14,11 +14,18 @@ from paper_2603_24919_b200.workloads import make_config
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("chunk", [None, "1024"])
 @pytest.mark.parametrize("world,alpha,beta,k", [(2, 0.05, 0.01, 10), (3, 0.2, 0.05, 25), (2, 0.6, 0.9, 5)])
-def test_two_shards_match_single(world, alpha, beta, k):
+def test_two_shards_match_single(world, alpha, beta, k, chunk, monkeypatch):
+    """chunk=1024 cuts each shard into several id chunks whose spilled
+    score >= 2 records (slot = 128) overflow at the larger alphas, so the
+    emit sweep's record filter, its recount fallback and the L < 2 recount
+    all run."""
     X, Q, _ = make_config(1, n=6000, nq=40, d=32)
     idx = T.build_index(X, T.IndexParams(8, 4, 64, 10, 2))
     ids0, d0, n0, l0 = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k))
+    if chunk:
+        monkeypatch.setenv("TACO_GLOBAL_CHUNK", chunk)
     bes = []
     for r in range(world):
         lo, hi = shard_range(X.shape[0], r, world)
