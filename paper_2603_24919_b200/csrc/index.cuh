@@ -46,7 +46,7 @@ struct DevBuf {
 
 struct QueryTile {
   DevBuf Q, qt, sd, sl, pops, npop, ret, flags, scores, part, hist, lvl, cnum, clocal, coff, qbase,
-      cursor, cand, bpref, pd2, ppos, tseg, qthr, qb, qsq, qok, gsb, gsc, gtab, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
+      cursor, cand, bpref, pd2, ppos, tseg, qthr, qb, qsq, qok, gsb, gsc, gtab, rlist, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   int64_t cand_cap = 0;
   int pop_cap = 0;
   int64_t* flags_h = nullptr;   // pinned copy of flags[0..3] (async read-back)

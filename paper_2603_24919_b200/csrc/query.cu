@@ -751,72 +751,52 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 // ------------------------------------------------------- global-mode count
 // One CTA per (id chunk, query) over a whole super-tile.  Sweep 1 (CNT_HIST)
 // writes the chunk's level histogram and spills its score >= 2 ids as packed
-// records (not the 32-64 KB table), Alg. 5 runs on the (all-reduced)
-// per-query histogram, sweep 2 (CNT_EMIT) filters the records at the level L
-// straight into the query's candidate segment -- or, when L < 2 or the
-// records overflowed their slot, recounts the chunk in shared memory and
-// compacts it.  CNT_TABLE stores the table itself (count_collisions tap).
+// records (not the 32-64 KB table); Alg. 5 runs on the (all-reduced)
+// per-query histogram; sweep 2 is k_emit_rec (a warp per (query, chunk)
+// filters the records at the level L straight into the query's candidate
+// segment) plus, for the pairs it lists (L < 2, or records that overflowed
+// their slot), this kernel in CNT_EMIT mode: persistent CTAs recount those
+// chunks in shared memory and compact them.  CNT_TABLE stores the table
+// itself (count_collisions tap).
 enum { CNT_TABLE = 0, CNT_HIST = 1, CNT_EMIT = 2 };
 template <bool NIB>
 __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offs, int n_sub, int K2, int64_t n,
     int64_t nchunks, int64_t chunk, int mode, uint8_t* __restrict__ scores, int32_t* __restrict__ part,
-    const int32_t* __restrict__ lvl, const int64_t* __restrict__ sbase, const int64_t* __restrict__ scnt,
-    const int64_t* __restrict__ coff, int64_t cand_cap, uint32_t* __restrict__ cand) {
+    const int32_t* __restrict__ lvl, const int64_t* __restrict__ sbase, const int64_t* __restrict__ coff,
+    uint32_t* __restrict__ cand, const int64_t* __restrict__ rlist) {
   extern __shared__ __align__(16) uint8_t table[];
   __shared__ CountSmem S;
+  __shared__ int s_fill;
+  const int tid = threadIdx.x;
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  uint4* t4 = reinterpret_cast<uint4*>(table);
+  if (mode == CNT_EMIT) {
+    const int64_t cnt = rlist[0];
+    for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+      const int64_t p = rlist[1 + i];
+      const int64_t q = p / nchunks, c = p - q * nchunks;
+      const int64_t base = c * chunk;
+      const int valid = (int)min(chunk, n - base);
+      for (int v = tid; v < tbytes / 16; v += CT_THREADS) t4[v] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+      if (tid == 0) s_fill = 0;
+      __syncthreads();
+      compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)lvl[q], base, cand + sbase[q] + coff[p], &s_fill);
+      __syncthreads();   // table and S are reused by the next pair
+    }
+    return;
+  }
   const int64_t c = blockIdx.x;
   const int64_t q = blockIdx.y;
-  const int tid = threadIdx.x;
   const int64_t base = c * chunk;
   const int valid = (int)min(chunk, n - base);
-  __shared__ int s_fill;
-  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
   const int rec_cap = tbytes / 4;                  // records per spilled (query, chunk) slot
-  if (mode == CNT_EMIT) {
-    if (sbase[q] + scnt[q] > cand_cap) return;
-    const int64_t lo = coff[q * nchunks + c];
-    const int64_t hi = c + 1 < nchunks ? coff[q * nchunks + c + 1] : scnt[q];
-    if (hi == lo) return;   // no candidate of this query in this chunk
-    const int L = lvl[q];
-    if (scores && L >= 2) {
-      // the count sweep spilled this chunk's score >= 2 ids unless they overflowed the slot
-      const int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
-      const int rc = valid - pp[0] - pp[1];
-      if (rc <= rec_cap) {
-        const uint32_t* rec = reinterpret_cast<const uint32_t*>(scores + ((size_t)q * nchunks + c) * tbytes);
-        uint32_t* dst = cand + sbase[q] + lo;
-        if (tid == 0) s_fill = 0;
-        __syncthreads();
-        const int lane = tid & 31;
-        const uint32_t lt = (1u << lane) - 1u;
-        for (int i0 = tid - lane; i0 < rc; i0 += CT_THREADS) {
-          const int i = i0 + lane;
-          const uint32_t r = i < rc ? rec[i] : 0u;
-          const bool hit = (int)(r & 0xFFu) >= L;
-          const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-          if (bal == 0u) continue;
-          int wb = 0;
-          if (lane == 0) wb = atomicAdd(&s_fill, __popc(bal));
-          wb = __shfl_sync(0xffffffffu, wb, 0);
-          if (hit) dst[wb + __popc(bal & lt)] = (uint32_t)base + (r >> 8);
-        }
-        return;
-      }
-    }
-  }
-  uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < tbytes / 16; i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
-  if (mode == CNT_EMIT) {
-    if (tid == 0) S.batches = 0;
-    __syncthreads();
-    compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)lvl[q], base,
-                                       cand + sbase[q] + coff[q * nchunks + c], &S.batches);
-    return;
-  }
   if (mode == CNT_TABLE && !NIB) {
     uint4* dst = reinterpret_cast<uint4*>(scores + ((size_t)q * nchunks + c) * tbytes);
     for (int i = tid; i < tbytes / 16; i += CT_THREADS) dst[i] = t4[i];
@@ -829,6 +809,56 @@ __global__ void __launch_bounds__(CT_THREADS, 4) k_count(
                                      &s_fill);
   int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
   for (int l = tid; l <= n_sub; l += CT_THREADS) pp[l] = S.lh[l];
+}
+
+// Global-mode emit sweep: a warp per (query, chunk) pair filters the
+// chunk's spilled score >= 2 records at the query's level L into its
+// candidate slots; pairs without usable records (L < 2, overflowed slot) are
+// appended to rlist (rlist[0] = count) for the CNT_EMIT recount.
+constexpr int ER_WARPS = 8;
+template <bool NIB>
+__global__ void __launch_bounds__(32 * ER_WARPS) k_emit_rec(
+    const uint8_t* __restrict__ recs, int64_t n, int64_t nchunks, int64_t chunk, int n_sub, int64_t QS,
+    const int32_t* __restrict__ part, const int32_t* __restrict__ lvl, const int64_t* __restrict__ sbase,
+    const int64_t* __restrict__ scnt, const int64_t* __restrict__ coff, int64_t cand_cap,
+    uint32_t* __restrict__ cand, int64_t* __restrict__ rlist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * ER_WARPS + (threadIdx.x >> 5);
+  if (p >= QS * nchunks) return;
+  const int64_t q = p / nchunks, c = p - q * nchunks;
+  if (sbase[q] + scnt[q] > cand_cap) return;
+  const int64_t lo = coff[p];
+  const int64_t hi = c + 1 < nchunks ? coff[p + 1] : scnt[q];
+  if (hi == lo) return;   // no candidate of this query in this chunk
+  const int L = lvl[q];
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  const int64_t tbytes = NIB ? chunk / 2 : chunk;
+  int rc = 0;
+  if (L >= 2) {
+    const int32_t* pp = part + (size_t)p * (n_sub + 1);
+    rc = valid - pp[0] - pp[1];
+  }
+  if (L < 2 || rc > (int)(tbytes / 4)) {
+    if (lane == 0) {
+      const int64_t slot = (int64_t)atomicAdd((unsigned long long*)rlist, 1ull);
+      rlist[1 + slot] = p;
+    }
+    return;
+  }
+  const uint32_t* rec = reinterpret_cast<const uint32_t*>(recs + (size_t)p * tbytes);
+  uint32_t* dst = cand + sbase[q] + lo;
+  const uint32_t lt = (1u << lane) - 1u;
+  int w = 0;
+#pragma unroll 4
+  for (int i0 = 0; i0 < rc; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t r = i < rc ? __ldg(rec + i) : 0u;
+    const bool hit = (int)(r & 0xFFu) >= L;
+    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+    if (hit) dst[w + __popc(bal & lt)] = (uint32_t)base + (r >> 8);
+    w += __popc(bal);
+  }
 }
 
 // Level histograms of externally provided score chunks (select_candidates tap).
@@ -1709,7 +1739,7 @@ static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t 
     kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
         idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_HIST, t.gtab.as<uint8_t>(), t.part.as<int32_t>(),
-        nullptr, nullptr, nullptr, nullptr, 0, nullptr);
+        nullptr, nullptr, nullptr, nullptr, nullptr);
     TACO_LAUNCHED();
   }
   {
@@ -1719,6 +1749,8 @@ static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t 
   }
   return TACO_OK;
 }
+
+static int num_sms();
 
 // global mode: Alg. 5 on `ghist`, then sweep 2 emits (records, else recount)
 static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_t* ghist, double beta,
@@ -1733,14 +1765,23 @@ static int global_select(taco_index* idx, QueryTile& t, int64_t QS, const int64_
     TACO_LAUNCHED();
   }
   {
-    dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COMPACT, st);
-    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
-    kern<<<g, CT_THREADS, table_bytes(idx), st>>>(
-        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
-        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, t.gtab.as<uint8_t>(), t.part.as<int32_t>(),
+    const int64_t pairs = QS * idx->nchunks;
+    TACO_TRY(t.rlist.ensure(sizeof(int64_t) * (size_t)(pairs + 1)));
+    TACO_CHECK_CUDA(cudaMemsetAsync(t.rlist.p, 0, sizeof(int64_t), st));
+    auto ek = nib_tables(idx) ? k_emit_rec<true> : k_emit_rec<false>;
+    ek<<<(unsigned)ceil_div(pairs, ER_WARPS), 32 * ER_WARPS, 0, st>>>(
+        t.gtab.as<uint8_t>(), idx->n, idx->nchunks, idx->chunk, idx->n_sub, QS, t.part.as<int32_t>(),
         t.lvl.as<int32_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(), t.coff.as<int64_t>(), t.cand_cap,
-        t.cand.as<uint32_t>());
+        t.cand.as<uint32_t>(), t.rlist.as<int64_t>());
+    TACO_LAUNCHED();
+    // recount the listed pairs: persistent CTAs, as many as are co-resident
+    auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;
+    const int64_t ctas = std::min<int64_t>(pairs, (int64_t)num_sms() * 4);
+    kern<<<(unsigned)ctas, CT_THREADS, table_bytes(idx), st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
+        idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_EMIT, nullptr, nullptr, t.lvl.as<int32_t>(),
+        t.qbase.as<int64_t>(), t.coff.as<int64_t>(), t.cand.as<uint32_t>(), t.rlist.as<int64_t>());
     TACO_LAUNCHED();
   }
   return TACO_OK;
@@ -2236,7 +2277,7 @@ int taco_count_scores(taco_index* idx, const float* q_h, double alpha, uint8_t* 
     k_count<false><<<dim3((unsigned)idx->nchunks, 1), CT_THREADS, (size_t)idx->chunk, st>>>(
         t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(),
         idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, CNT_TABLE, sc.as<uint8_t>(), part.as<int32_t>(),
-        nullptr, nullptr, nullptr, nullptr, 0, nullptr);
+        nullptr, nullptr, nullptr, nullptr, nullptr);
     count_launch();
     cudaMemcpyAsync(scores_h, sc.p, idx->n, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
