@@ -34,3 +34,14 @@ for G in (2, 4, 8):
     ms = (time.perf_counter() - t) / 3 * 1000
     print(f"G={G} shard0 [{lo},{hi}) per-rank ms {ms:.2f}  (implied {Q.shape[0] / ms * 1000:.0f} QPS if ranks scale)")
     del be
+    # per-kernel split of one more pass (CUDA events on the launching stream)
+    from paper_2603_24919_b200 import _native as nat  # noqa: E402
+    be = CudaShardBackend(idx, X[lo:hi], lo, n, 0)
+    run(); torch.cuda.synchronize()
+    nat.profile_enable(True)
+    nat.profile_read(reset=True)
+    run(); torch.cuda.synchronize()
+    prof, _ = nat.profile_read(reset=True)
+    nat.profile_enable(False)
+    print("   ", {k: round(v[0], 3) for k, v in prof.items() if v[0] > 0.02})
+    del be
