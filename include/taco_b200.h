@@ -140,6 +140,20 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
 int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d, double beta,
                              int32_t k, double* topk_d2_d, int64_t* topk_ids_d,
                              int64_t* cand_num_d, int32_t* last_coll_d, void* stream);
+/* Split traversal: stage 1 as three calls so ranks can divide the replicated
+ * per-query traversal.  taco_query_front_device computes rows [q_lo, q_hi)
+ * of a tile of nq queries (Q_d; rows >= nq is the all-gather's padded row
+ * count) into the index's tile
+ * buffers; *need > 0 reports a traversal longer than pop_cap (all ranks then
+ * repeat with pop_cap = K'^2).  taco_query_pop_buffers exposes those buffers
+ * (pops u16 [rows][Ns][pop_cap], npop i32 [rows][Ns], ret i64 [rows][Ns]) for
+ * an in-place all-gather; taco_query_count_popped_device then counts the
+ * local shard for all nq queries.  Replaces the count half of
+ * engine.py:201-220 (popped cells shared, ids counted per shard). */
+int taco_query_front_device(taco_index* idx, const float* Q_d, int64_t nq, int64_t q_lo, int64_t q_hi,
+                            int64_t rows, double alpha, int32_t pop_cap, int64_t* need, void* stream);
+int taco_query_pop_buffers(taco_index* idx, void** pops, void** npop, void** ret, int32_t* pop_cap);
+int taco_query_count_popped_device(taco_index* idx, int64_t nq, int64_t* hist_d, void* stream);
 /* Largest nq accepted by the split count/finish calls for this index. */
 int taco_query_tile_size(taco_index* idx);
 /* Merge R sorted per-rank top-k lists [R][nq][k] on (d2, id), write ids/dists. */

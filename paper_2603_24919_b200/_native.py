@@ -55,6 +55,9 @@ _SIGS = {
     "taco_query_batch": [_vp, _vp, _c_i64, _c_dbl, _c_dbl, _c_i32, _vp, _vp, _vp, _vp],
     "taco_query_batch_device": [_vp, _vp, _c_i64, _c_dbl, _c_dbl, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_query_count_device": [_vp, _vp, _c_i64, _c_dbl, _vp, _vp],
+    "taco_query_front_device": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_i32, _vp, _vp],
+    "taco_query_pop_buffers": [_vp, _vp, _vp, _vp, _vp],
+    "taco_query_count_popped_device": [_vp, _c_i64, _vp, _vp],
     "taco_query_finish_device": [_vp, _c_i64, _vp, _c_dbl, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_query_tile_size": [_vp],
     "taco_topk_merge_device": [_c_i32, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp],

@@ -1676,21 +1676,28 @@ static int64_t retrieval_target(double alpha, int64_t n) {
 }
 
 // transform + centroid ranks + traversal for QS queries resident in t.Q
+// Queries [q0, q0 + QS) of the tile buffers (q0 > 0: one rank's slice of a
+// split traversal, taco_query_front_device).
 static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, cudaStream_t st,
-                       double* keys_out) {
+                       double* keys_out, int64_t q0 = 0) {
   const int kp = idx->kp;
+  if (QS == 0) return TACO_OK;
+  const size_t qn0 = (size_t)q0 * idx->n_sub;
+  float* qt = t.qt.as<float>() + (size_t)q0 * idx->D;
+  double* sd = t.sd.as<double>() + qn0 * 2 * kp;
+  uint16_t* sl = t.sl.as<uint16_t>() + qn0 * 2 * kp;
   {
     ProfScope ps(K_TRANSFORM, st);
-    TACO_TRY(launch_transform(st, t.Q.as<float>(), QS, idx->d, idx->D, idx->mean.as<float>(),
-                              idx->M.as<float>(), t.qt.as<float>(), false));
+    TACO_TRY(launch_transform(st, t.Q.as<float>() + (size_t)q0 * idx->d, QS, idx->d, idx->D,
+                              idx->mean.as<float>(), idx->M.as<float>(), qt, false));
   }
   {
     const int64_t warps = QS * idx->n_sub * 2;
     const int wpb = 8;
     ProfScope ps(K_CSORT, st);
     k_csort<<<(unsigned)ceil_div(warps, wpb), wpb * 32, sizeof(double) * kp * wpb, st>>>(
-        t.qt.as<float>(), (int)QS, idx->n_sub, idx->s, idx->m1, idx->m2, kp, idx->cb1.as<float>(),
-        idx->cb2.as<float>(), t.sd.as<double>(), t.sl.as<uint16_t>());
+        qt, (int)QS, idx->n_sub, idx->s, idx->m1, idx->m2, kp, idx->cb1.as<float>(),
+        idx->cb2.as<float>(), sd, sl);
     TACO_LAUNCHED();
   }
   {
@@ -1699,9 +1706,9 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
     const unsigned g = (unsigned)ceil_div(th, 128);
     ProfScope ps(K_TRAVERSE, st);
 #define TRAV(KM)                                                                                  \
-  k_traverse<KM><<<g, 128, 0, st>>>(t.sd.as<double>(), t.sl.as<uint16_t>(), idx->gsize.as<int64_t>(), \
-                                    QS, idx->n_sub, kp, target, t.pops.as<uint16_t>(), t.pop_cap,     \
-                                    keys_out, t.npop.as<int32_t>(), t.ret.as<int64_t>(),              \
+  k_traverse<KM><<<g, 128, 0, st>>>(sd, sl, idx->gsize.as<int64_t>(), QS, idx->n_sub, kp, target,    \
+                                    t.pops.as<uint16_t>() + qn0 * t.pop_cap, t.pop_cap, keys_out,     \
+                                    t.npop.as<int32_t>() + qn0, t.ret.as<int64_t>() + qn0,            \
                                     t.flags.as<int64_t>())
     if (kp <= 32) TRAV(32);
     else if (kp <= 64) TRAV(64);
@@ -2193,6 +2200,65 @@ int taco_query_count_device(taco_index* idx, const float* Q_d, int64_t nq, doubl
     t.pop_cap = idx->K;
     TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)Qt * idx->n_sub * t.pop_cap));
   }
+  TACO_TRY(global_count(idx, t, nq, st));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(hist_d, t.hist.p, sizeof(int64_t) * (size_t)nq * (idx->n_sub + 1),
+                                  cudaMemcpyDeviceToDevice, st));
+  return TACO_OK;
+}
+
+// Split traversal (multi-GPU): this rank's slice [q_lo, q_hi) of a tile of nq
+// queries (Q_d; rows >= nq is the all-gather's padded row count) -> popped
+// cells in rows [q_lo, q_hi) of the tile buffers, which the caller
+// all-gathers (taco_query_pop_buffers) before taco_query_count_popped_device.
+// *need = the longest traversal when it exceeded pop_cap (every rank must then
+// re-run with cap K'^2), else 0.
+int taco_query_front_device(taco_index* idx, const float* Q_d, int64_t nq, int64_t q_lo, int64_t q_hi,
+                            int64_t rows, double alpha, int32_t pop_cap, int64_t* need, void* stream) {
+  TACO_TRY(check_query_ready(idx, alpha, 1));
+  if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
+  if (pop_cap < 1 || pop_cap > idx->K) TACO_FAIL(TACO_ERR_PARAMETER, "pop cap %d outside [1, %lld]", pop_cap, (long long)idx->K);
+  if (!(q_lo >= 0 && q_lo <= q_hi && q_hi <= nq && nq <= rows))
+    TACO_FAIL(TACO_ERR_PARAMETER, "query slice [%lld, %lld) of %lld outside [0, %lld)", (long long)q_lo,
+              (long long)q_hi, (long long)nq, (long long)rows);
+  const int64_t Qt = super_tile(idx, pop_cap);
+  if (rows > Qt + 16) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)rows, (long long)Qt);
+  cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
+  QueryTile& t = idx->qt;
+  t.pop_cap = pop_cap;
+  TACO_TRY(ensure_front(idx, t, std::max(Qt, rows), 1));
+  // every query of the tile: the re-rank (taco_query_finish_device) reads them all
+  if (nq > 0)
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
+  TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
+  TACO_TRY(stage_front(idx, t, q_hi - q_lo, alpha, st, nullptr, q_lo));
+  int64_t f0 = 0;
+  TACO_CHECK_CUDA(cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  *need = f0 > pop_cap ? f0 : 0;
+  return TACO_OK;
+}
+
+int taco_query_pop_buffers(taco_index* idx, void** pops, void** npop, void** ret, int32_t* pop_cap) {
+  TACO_TRY(index_check(idx));
+  QueryTile& t = idx->qt;
+  if (!t.pops.p) TACO_FAIL(TACO_ERR_STATE, "no traversal buffers yet (call taco_query_front_device)");
+  *pops = t.pops.p;
+  *npop = t.npop.p;
+  *ret = t.ret.p;
+  *pop_cap = t.pop_cap;
+  return TACO_OK;
+}
+
+// Counting sweep over the (gathered) popped cells of nq tile queries -> the
+// local per-query level histograms, as taco_query_count_device.
+int taco_query_count_popped_device(taco_index* idx, int64_t nq, int64_t* hist_d, void* stream) {
+  TACO_TRY(index_check(idx));
+  if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
+  QueryTile& t = idx->qt;
+  if (!t.pops.p) TACO_FAIL(TACO_ERR_STATE, "no traversal buffers yet (call taco_query_front_device)");
+  if (nq > super_tile(idx, t.pop_cap) + 16) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile", (long long)nq);
+  if (nq == 0) return TACO_OK;
+  cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
   TACO_TRY(global_count(idx, t, nq, st));
   TACO_CHECK_CUDA(cudaMemcpyAsync(hist_d, t.hist.p, sizeof(int64_t) * (size_t)nq * (idx->n_sub + 1),
                                   cudaMemcpyDeviceToDevice, st));

@@ -37,6 +37,14 @@ def shard_range(n: int, rank: int, world: int):
     return lo, min(n, lo + per)
 
 
+class _DeviceBytes:
+    """Zero-copy handle on library-owned device memory (CUDA array interface)."""
+
+    def __init__(self, ptr: int, rows: int, row_bytes: int):
+        self.__cuda_array_interface__ = {"shape": (rows, row_bytes), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
 class CudaShardBackend:
     """One rank's shard on its GPU."""
 
@@ -80,9 +88,46 @@ class CudaShardBackend:
         Xs = np.ascontiguousarray(X_shard, dtype=np.float32)
         nat.call("taco_index_set_data", self.dev.h, nat.ptr(Xs))
         self.tile = int(nat.lib().taco_query_tile_size(self.dev.h))
+        self.k2 = K2
+        # popped cells per (query, subspace) slot: the all-gathered rows are
+        # nq * N_s * pop_cap * 2 bytes, so start small (config 2 pops <= ~310)
+        # and grow to the measured need (kept for later batches)
+        self.pop_cap = min(K2, 256)
 
     def tile_size(self) -> int:
         return self.tile
+
+    # ---- split traversal: each rank walks a slice of the tile's queries
+    def front(self, Qt, alpha: float, lo: int, hi: int, rows: int) -> int:
+        """Traverse queries [lo, hi) of the tile Qt into rows [lo, hi) of the
+        pop buffers; returns the longest traversal if it exceeded the cap."""
+        import ctypes
+        need = ctypes.c_int64(0)
+        nat.call("taco_query_front_device", self.dev.h, Qt.data_ptr(), Qt.shape[0], lo, hi, rows, float(alpha),
+                 self.pop_cap, ctypes.byref(need), self._stream())
+        return int(need.value)
+
+    def raise_pop_cap(self, need: int) -> None:
+        """Every rank gets the same all-reduced `need`, so caps stay equal."""
+        self.pop_cap = min(self.k2, -(-(need + need // 4) // 64) * 64)
+
+    def pop_views(self, rows: int):
+        """uint8 views [rows, bytes per query] of the popped cells, their
+        counts and retrieved sizes (rows are contiguous per query)."""
+        import ctypes
+        pp, pn, pr = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        cap = ctypes.c_int32(0)
+        nat.call("taco_query_pop_buffers", self.dev.h, ctypes.byref(pp), ctypes.byref(pn), ctypes.byref(pr),
+                 ctypes.byref(cap))
+        dev = f"cuda:{self.device}"
+        per_row = (2 * self.k_sub * cap.value, 4 * self.k_sub, 8 * self.k_sub)
+        return [self.torch.as_tensor(_DeviceBytes(p.value, rows, b), device=dev)
+                for p, b in zip((pp, pn, pr), per_row)]
+
+    def count_popped(self, nq: int):
+        hist = self.torch.empty((nq, self.k_sub + 1), dtype=self.torch.int64, device=f"cuda:{self.device}")
+        nat.call("taco_query_count_popped_device", self.dev.h, nq, hist.data_ptr(), self._stream())
+        return hist
 
     def _stream(self):
         return nat.torch_stream(self.torch, self.device)
@@ -116,6 +161,31 @@ class CudaShardBackend:
         return out_i, out_d
 
 
+def _split_count(backend, Qt, alpha: float, group=None):
+    """Stage 1 with the replicated traversal divided by query: rank r walks
+    rows [r*per, (r+1)*per) of the tile, an in-place all_gather gives every
+    rank all popped cells (identical to walking them itself: the traversal
+    reads only replicated state), then each rank counts its own ids."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m = Qt.shape[0]
+    per = -(-m // world)
+    rows = per * world
+    lo, hi = min(m, rank * per), min(m, rank * per + per)
+    for _ in range(2):
+        need = torch.tensor([backend.front(Qt, alpha, lo, hi, rows)], dtype=torch.int64, device=Qt.device)
+        dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
+        if int(need.item()) == 0:
+            break
+        backend.raise_pop_cap(int(need.item()))   # some rank's walk was longer than the cap: all redo
+    for buf in backend.pop_views(rows):
+        dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
+    return backend.count_popped(m)
+
+
 def sharded_query(backend, Q, alpha: float, beta: float, k: int, group=None):
     """Batched k-ANN over a point-sharded index; every rank returns the full,
     identical result (ids int32 [nq,k], dists f32 [nq,k], cand_num, last_coll)."""
@@ -129,7 +199,10 @@ def sharded_query(backend, Q, alpha: float, beta: float, k: int, group=None):
     for q0 in range(0, nq, T):
         Qt = Q[q0:q0 + T]
         m = Qt.shape[0]
-        hist = backend.count(Qt, alpha)
+        if hasattr(backend, "front"):
+            hist = _split_count(backend, Qt, alpha, group)
+        else:
+            hist = backend.count(Qt, alpha)
         dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
         d2, ids, num, lvl = backend.finish(m, hist, beta, k)
         d2_all = torch.empty((world * m, k), dtype=d2.dtype, device=d2.device)

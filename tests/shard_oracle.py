@@ -20,6 +20,57 @@ class OracleShardBackend:
     def tile_size(self):
         return self.tile
 
+    # ---- split traversal (distributed._split_count); small cap so the
+    # overflow -> re-run path is exercised too
+    pop_cap = 6
+
+    def front(self, Qt, alpha, lo, hi, rows):
+        o = self.o
+        Q = Qt.numpy()
+        self.Q = Q
+        if getattr(self, "_rows", None) != (rows, self.pop_cap):
+            self._rows = (rows, self.pop_cap)
+            self.pops = np.zeros((rows, o.n_sub, self.pop_cap), np.uint16)
+            self.npop = np.zeros((rows, o.n_sub), np.int32)
+            self.ret = np.zeros((rows, o.n_sub), np.int64)
+        need = 0
+        s, kp = o.s, o.kprime
+        for r in range(lo, hi):
+            qt = O.transform(o.mean, o.blocks, Q[r][None, :])[0]
+            for j in range(o.n_sub):
+                cells = o.cells[j]
+                d1, i1, d2, i2 = O.centroid_order(o.cb1[j], o.cb2[j], qt[j * s:(j + 1) * s], o.split)
+                pops, got = O.traverse(alpha, o.n, kp, d1, i1, d2, i2,
+                                       lambda a, b: cells[(a, b)].size if (a, b) in cells else 0)
+                self.npop[r, j] = len(pops)
+                self.ret[r, j] = got
+                if len(pops) > self.pop_cap:
+                    need = max(need, len(pops))
+                for t, (_, a, b) in enumerate(pops[:self.pop_cap]):
+                    self.pops[r, j, t] = a * kp + b
+        return need
+
+    def raise_pop_cap(self, need):
+        self.pop_cap = min(self.o.kprime ** 2, need + 1)
+
+    def pop_views(self, rows):
+        return [torch.from_numpy(a.reshape(rows, -1).view(np.uint8)) for a in (self.pops, self.npop, self.ret)]
+
+    def count_popped(self, nq):
+        o = self.o
+        hi = self.lo + self.X.shape[0]
+        self.scores = []
+        for r in range(nq):
+            sc = np.zeros(o.n, np.uint8)
+            for j in range(o.n_sub):
+                for cell in self.pops[r, j, :self.npop[r, j]]:
+                    key = divmod(int(cell), o.kprime)
+                    if key in o.cells[j]:
+                        sc[o.cells[j][key]] += 1
+            self.scores.append(sc[self.lo:hi])
+        h = [np.bincount(s, minlength=o.n_sub + 1) for s in self.scores]
+        return torch.tensor(np.array(h, np.int64))
+
     def count(self, Qt, alpha):
         Q = Qt.numpy()
         hi = self.lo + self.X.shape[0]

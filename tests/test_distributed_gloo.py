@@ -1,6 +1,7 @@
-"""world_size-2 gloo run of the sharded query orchestration (CPU): histogram
-all-reduce, Alg. 5 on the global histogram, top-k all-gather + merge must equal
-the single-process result bit-for-bit."""
+"""world_size-2 gloo run of the sharded query orchestration (CPU): traversal
+split by query + all-gather of the popped cells (with the cap-overflow
+re-run), histogram all-reduce, Alg. 5 on the global histogram, top-k
+all-gather + merge must equal the single-process result bit-for-bit."""
 
 import os
 import socket
@@ -34,7 +35,7 @@ def _worker(rank, world, port, cfg, out_q):
     lo, hi = shard_range(X.shape[0], rank, world)
     be = OracleShardBackend(oidx, X[lo:hi], lo, X.shape[0], tile=5)
     ids, dists, num, lvl = sharded_query(be, torch.from_numpy(Q), cfg["alpha"], cfg["beta"], cfg["k"])
-    out_q.put((rank, ids.numpy(), dists.numpy(), num.numpy(), lvl.numpy()))
+    out_q.put((rank, ids.numpy(), dists.numpy(), num.numpy(), lvl.numpy(), be.pop_cap))
     dist.destroy_process_group()
 
 
@@ -61,7 +62,9 @@ def test_sharded_equals_single(cfg):
     X, Q, _ = make_config(1, n=cfg["n"], nq=cfg["nq"], d=32)
     oidx = O.build_index(X, 8, 4, 64, 8, 3)
     oi, od, on, ol = O.knn_batch(oidx, X, Q, cfg["alpha"], cfg["beta"], cfg["k"])
-    for _, ids, dists, num, lvl in res:
+    # the split traversal's cap-overflow re-run (cap 6 -> the all-reduced need) ran with equal caps
+    assert all(r[5] > 6 for r in res) and len({r[5] for r in res}) == 1, [r[5] for r in res]
+    for _, ids, dists, num, lvl, _ in res:
         np.testing.assert_array_equal(ids, oi)
         np.testing.assert_array_equal(dists, od)
         np.testing.assert_array_equal(num, on)

@@ -50,3 +50,55 @@ def test_two_shards_match_single(world, alpha, beta, k, chunk, monkeypatch):
     np.testing.assert_array_equal(np.concatenate([o[1] for o in outs]), d0)
     np.testing.assert_array_equal(np.concatenate([o[2] for o in outs]), n0)
     np.testing.assert_array_equal(np.concatenate([o[3] for o in outs]), l0)
+
+
+@pytest.mark.parametrize("world,alpha,beta,k,cap", [(2, 0.05, 0.01, 10, 64), (3, 0.2, 0.05, 25, 4)])
+def test_split_traversal_matches_single(world, alpha, beta, k, cap):
+    """distributed._split_count on one GPU: every shard walks only its slice
+    of the tile's queries (taco_query_front_device), the slices are copied
+    into every shard's pop buffers (standing in for the in-place NCCL
+    all_gather), each shard counts its ids (taco_query_count_popped_device).
+    cap=4 forces the cap-overflow re-run at the measured need.  Must equal the
+    single-GPU batch bit-for-bit."""
+    X, Q, _ = make_config(1, n=6000, nq=40, d=32)
+    idx = T.build_index(X, T.IndexParams(8, 4, 64, 10, 2))
+    ids0, d0, n0, l0 = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k))
+    bes = []
+    for r in range(world):
+        lo, hi = shard_range(X.shape[0], r, world)
+        bes.append(CudaShardBackend(idx, X[lo:hi], lo, X.shape[0], 0))
+        bes[-1].pop_cap = cap
+    Qd = torch.from_numpy(Q).cuda()
+    T_ = min(b.tile_size() for b in bes)
+    outs = []
+    raised = False
+    for q0 in range(0, Q.shape[0], T_):
+        Qt = Qd[q0:q0 + T_]
+        m = Qt.shape[0]
+        per = -(-m // world)
+        rows = per * world
+        for _ in range(2):
+            need = max(b.front(Qt, alpha, min(m, r * per), min(m, r * per + per), rows) for r, b in enumerate(bes))
+            if need == 0:
+                break
+            raised = True
+            for b in bes:
+                b.raise_pop_cap(need)
+        views = [b.pop_views(rows) for b in bes]
+        for r in range(world):              # all_gather: rank r's rows to every rank
+            for dst in range(world):
+                if dst != r:
+                    for vd, vs in zip(views[dst], views[r]):
+                        vd[r * per:(r + 1) * per].copy_(vs[r * per:(r + 1) * per])
+        hist = sum(b.count_popped(m) for b in bes)
+        parts = [b.finish(m, hist, beta, k) for b in bes]
+        d2_all = torch.stack([p[0] for p in parts])
+        id_all = torch.stack([p[1] for p in parts])
+        oi, od = bes[0].merge(d2_all, id_all, k)
+        torch.cuda.synchronize()
+        outs.append((oi.cpu().numpy(), od.cpu().numpy(), parts[0][2].cpu().numpy(), parts[0][3].cpu().numpy()))
+    assert raised == (cap < 64)
+    np.testing.assert_array_equal(np.concatenate([o[0] for o in outs]), ids0)
+    np.testing.assert_array_equal(np.concatenate([o[1] for o in outs]), d0)
+    np.testing.assert_array_equal(np.concatenate([o[2] for o in outs]), n0)
+    np.testing.assert_array_equal(np.concatenate([o[3] for o in outs]), l0)
