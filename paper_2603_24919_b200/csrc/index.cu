@@ -224,7 +224,8 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
   idx->m2 = subspace_dim - idx->m1;
   idx->D = n_subspaces * subspace_dim;
   idx->iters = kmeans_iters;
-  if (n_global == n && n <= kClusterMaxN) {
+  const char* force_global = getenv("TACO_GLOBAL_MODE");   // =1: global mode at any size (sharded-path checks)
+  if (n_global == n && n <= kClusterMaxN && !(force_global && force_global[0] == '1')) {
     // ids per CTA: 4-bit tables (n_sub <= 15) 128K = 64 KiB, 8-bit tables 64K (TACO_CLUSTER_IDS overrides)
     int64_t target = n_subspaces <= 15 ? 131072 : 65536;
     if (const char* e = getenv("TACO_CLUSTER_IDS")) target = std::max<int64_t>(1024, atoll(e));

@@ -2027,7 +2027,19 @@ static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total)
   g_prof.sumC += total;
   g_prof.queries += QS;
   g_prof.tiles += 1;
-  g_prof.bytes_scores += idx->cluster_mode ? 0 : QS * idx->nchunks * idx->chunk;
+  if (!idx->cluster_mode && idx->n_sub >= 2) {   // spilled score >= 2 records (k_count CNT_HIST)
+    const size_t np1 = (size_t)idx->n_sub + 1;
+    std::vector<int32_t> part((size_t)QS * idx->nchunks * np1);
+    cudaMemcpy(part.data(), t.part.p, 4 * part.size(), cudaMemcpyDeviceToHost);
+    const int64_t cap = table_bytes(idx) / 4;
+    for (int64_t q = 0; q < QS; ++q)
+      for (int64_t c = 0; c < idx->nchunks; ++c) {
+        const int32_t* pp = part.data() + ((size_t)q * idx->nchunks + c) * np1;
+        const int64_t valid = std::min<int64_t>(idx->chunk, idx->n - c * idx->chunk);
+        const int64_t rc = valid - pp[0] - pp[1];
+        if (rc <= cap) g_prof.bytes_scores += 4 * rc;
+      }
+  }
 }
 
 // Front half of a tile (queries already in t.Q): transform, ranks, traversal,

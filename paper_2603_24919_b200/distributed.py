@@ -213,57 +213,3 @@ def sharded_query(backend, Q, alpha: float, beta: float, k: int, group=None):
         outs.append((oi, od, num, lvl))
     cat = lambda i: torch.cat([o[i] for o in outs]) if outs else None  # noqa: E731
     return cat(0), cat(1), cat(2), cat(3)
-
-
-def bench_main(args, metric):
-    """bench.py under torchrun (N > 1): strong scaling of config 2 over ranks."""
-    import json
-    import os
-    import statistics
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_2603_24919_b200 as T
-    from paper_2603_24919_b200.workloads import make_config
-
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    os.environ["TACO_DEVICE"] = str(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    X, Q, meta = make_config(args.config, n=args.n, nq=args.nq)
-    params = T.IndexParams(meta["n_sub"], meta["s"], meta["clusters"], meta["kmeans_iters"], meta["seed"])
-    index = T.build_index(X, params)            # replicated, deterministic build
-    lo, hi = shard_range(X.shape[0], rank, world)
-    backend = CudaShardBackend(index, X[lo:hi], lo, X.shape[0], local)
-    Qd = torch.from_numpy(Q).cuda()
-    a, b, k = meta["alpha"], meta["beta"], meta["k"]
-    for _ in range(max(args.warmup, 1)):
-        sharded_query(backend, Qd, a, b, k)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(args.steps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        ids, dists, num, lvl = sharded_query(backend, Qd, a, b, k)
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t.item()))
-    ms = statistics.mean(times)
-    if rank == 0:
-        line = {"metric": metric, "value": Q.shape[0] / (ms / 1000.0), "unit": "queries/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"cfg{meta['cfg']} n={meta['n']} batch={meta['nq']}",
-                           "parallelism": f"points sharded over {world} GPUs; NCCL all_reduce of "
-                                          "per-query histograms + all_gather of top-k"},
-                "step_ms": times}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
