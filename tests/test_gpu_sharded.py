@@ -102,3 +102,25 @@ def test_split_traversal_matches_single(world, alpha, beta, k, cap):
     np.testing.assert_array_equal(np.concatenate([o[1] for o in outs]), d0)
     np.testing.assert_array_equal(np.concatenate([o[2] for o in outs]), n0)
     np.testing.assert_array_equal(np.concatenate([o[3] for o in outs]), l0)
+
+
+@pytest.mark.parametrize("chunk", [None, "1024"])
+def test_global_mode_matches_cluster_mode(chunk, monkeypatch):
+    """One unsharded index counted both ways: cluster mode (DSMEM-fused
+    count/select) and global mode (TACO_GLOBAL_MODE=1: per-chunk histograms,
+    spilled score >= 2 records, warp record filter, persistent recount of the
+    listed chunks).  chunk=1024 makes record slots overflow; beta=0.9 drives
+    L below 2 (the recount path).  Results must be identical."""
+    X, Q, _ = make_config(1, n=7000, nq=48, d=32)
+    P = T.IndexParams(8, 4, 64, 10, 2)
+    idx_c = T.build_index(X, P)
+    monkeypatch.setenv("TACO_GLOBAL_MODE", "1")
+    if chunk:
+        monkeypatch.setenv("TACO_GLOBAL_CHUNK", chunk)
+    idx_g = T.build_index(X, P)
+    for alpha, beta, k in ((0.05, 0.01, 10), (0.3, 0.2, 16), (0.6, 0.9, 5)):
+        qp = T.QueryParams(alpha, beta, k)
+        a = T.knn_query_batch(idx_c, X, Q, qp)
+        b = T.knn_query_batch(idx_g, X, Q, qp)
+        for u, v in zip(a, b):
+            np.testing.assert_array_equal(u, v)
