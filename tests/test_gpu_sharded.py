@@ -124,3 +124,29 @@ def test_global_mode_matches_cluster_mode(chunk, monkeypatch):
         b = T.knn_query_batch(idx_g, X, Q, qp)
         for u, v in zip(a, b):
             np.testing.assert_array_equal(u, v)
+
+
+def test_split_traversal_errors():
+    """The split-traversal entry points fail loudly on bad slices / caps and on
+    an unsharded (cluster-mode) index, like the reference's ParameterError."""
+    import ctypes
+
+    from paper_2603_24919_b200 import _native as nat
+    from paper_2603_24919_b200.errors import ParameterError, StateError
+
+    X, Q, _ = make_config(1, n=3000, nq=8, d=32)
+    idx = T.build_index(X, T.IndexParams(8, 4, 64, 10, 2))
+    be = CudaShardBackend(idx, X[:1500], 0, X.shape[0], 0)
+    Qd = torch.from_numpy(Q).cuda()
+    with pytest.raises(ParameterError):
+        be.front(Qd, 0.1, 5, 3, 8)            # lo > hi
+    with pytest.raises(ParameterError):
+        be.front(Qd, 0.1, 0, 8, 4)            # rows < nq
+    be.pop_cap = 10_000                        # above K'^2
+    with pytest.raises(ParameterError):
+        be.front(Qd, 0.1, 0, 8, 8)
+    whole = T.build_index(X, T.IndexParams(8, 4, 64, 10, 2))   # unsharded: cluster mode
+    need = ctypes.c_int64(0)
+    with pytest.raises(StateError):
+        nat.call("taco_query_front_device", T.engine._device_of(whole).h, Qd.data_ptr(), 8, 0, 8, 8, 0.1, 64,
+                 ctypes.byref(need), None)
