@@ -274,6 +274,7 @@ int taco_index_destroy(taco_index* idx) {
   idx->colmean.release();
   if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
   if (idx->ev_join) cudaEventDestroy(idx->ev_join);
+  if (idx->hstage) cudaFreeHost(idx->hstage);
   cudaStreamDestroy(idx->stream);
   delete idx;
   return TACO_OK;

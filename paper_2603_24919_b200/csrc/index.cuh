@@ -81,6 +81,8 @@ struct taco_index {
   taco::QueryTile qt, qt2;      // two query tiles: the batch loop pipelines them on two streams
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void* hstage = nullptr;        // pinned host staging of host-API results (async per-tile D2H)
+  size_t hstage_bytes = 0;
   std::vector<taco::BuildScratch> bs;
   cudaStream_t aux = nullptr;          // column-mean chain that runs behind the staged upload
   taco::DevBuf colstate, colmean;

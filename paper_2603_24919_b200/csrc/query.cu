@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <type_traits>
 #include <vector>
@@ -2127,6 +2128,30 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
   for (int b = 0; b < (pipe ? 2 : 1); ++b) TACO_TRY(ensure_front(idx, *tiles[b], QT, k));
   const cudaMemcpyKind kin = src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind kout = dst_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  // host results land in pinned staging first: a D2H copy into pageable memory
+  // blocks the host until the tile is done, which would stall the enqueue of
+  // the next tiles (the pipeline); the caller's arrays are filled at the end
+  int32_t* ids_u = ids_o;
+  float* dists_u = dists_o;
+  int64_t* cnum_u = cnum_o;
+  int32_t* lvl_u = lvl_o;
+  const size_t sb_ids = sizeof(int32_t) * (size_t)nq * k, sb_d = sizeof(float) * (size_t)nq * k;
+  const size_t sb_c = sizeof(int64_t) * (size_t)nq, sb_l = sizeof(int32_t) * (size_t)nq;
+  if (dst_host) {
+    const size_t need = sb_ids + sb_d + sb_c + sb_l + 64;
+    if (idx->hstage_bytes < need) {
+      if (idx->hstage) TACO_CHECK_CUDA(cudaFreeHost(idx->hstage));
+      idx->hstage = nullptr;
+      idx->hstage_bytes = 0;
+      TACO_CHECK_CUDA(cudaMallocHost(&idx->hstage, need));
+      idx->hstage_bytes = need;
+    }
+    uint8_t* h = static_cast<uint8_t*>(idx->hstage);
+    cnum_o = reinterpret_cast<int64_t*>(h);
+    ids_o = reinterpret_cast<int32_t*>(h + sb_c);
+    dists_o = reinterpret_cast<float*>(h + sb_c + sb_ids);
+    lvl_o = reinterpret_cast<int32_t*>(h + sb_c + sb_ids + sb_d);
+  }
   auto front = [&](int64_t i) -> int {
     QueryTile& t = *tiles[pipe ? i & 1 : 0];
     cudaStream_t s = sts[pipe ? i & 1 : 0];
@@ -2158,7 +2183,13 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
     TACO_CHECK_CUDA(cudaEventRecord(idx->ev_join, idx->stream2));
     TACO_CHECK_CUDA(cudaStreamWaitEvent(st, idx->ev_join, 0));
   }
-  if (dst_host) TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (dst_host) {
+    TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(ids_u, ids_o, sb_ids);
+    std::memcpy(dists_u, dists_o, sb_d);
+    std::memcpy(cnum_u, cnum_o, sb_c);
+    std::memcpy(lvl_u, lvl_o, sb_l);
+  }
   return TACO_OK;
 }
 
