@@ -65,6 +65,10 @@ int taco_index_set_data_device(taco_index* idx, const float* X_d);
 enum { TACO_ROWS_F32 = 0, TACO_ROWS_F16 = 1, TACO_ROWS_U8 = 2 };
 /* Storage format the rerank reads rows in (TACO_ROWS_*), or -1 without data. */
 int32_t taco_index_row_format(const taco_index* idx);
+/* Id chunking of the count path: ids per chunk, the
+ * number of chunks, and whether the index counts in cluster mode (one
+ * thread-block cluster of nchunks CTAs per query) or global mode. */
+int taco_index_layout(const taco_index* idx, int64_t* chunk, int64_t* nchunks, int32_t* cluster_mode);
 
 /* ------------------------------------------------------------------ build */
 /* spectral.fit_covariance (spectral.py:94-111): fp64 row mean (sequential,
@@ -152,6 +156,12 @@ int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d
  * engine.py:201-220 (popped cells shared, ids counted per shard). */
 int taco_query_front_device(taco_index* idx, const float* Q_d, int64_t nq, int64_t q_lo, int64_t q_hi,
                             int64_t rows, double alpha, int32_t pop_cap, int64_t* need, void* stream);
+/* taco_query_front_async: the same walk without a host round trip; the
+ * slice's longest walk (pops) is copied to need_d[0] (device int64) on the
+ * stream, so a caller all-reduces it and checks every tile of a batch with one
+ * sync (the batch is re-run with a raised cap in the rare overflow case). */
+int taco_query_front_async(taco_index* idx, const float* Q_d, int64_t nq, int64_t q_lo, int64_t q_hi,
+                           int64_t rows, double alpha, int32_t pop_cap, int64_t* need_d, void* stream);
 int taco_query_pop_buffers(taco_index* idx, void** pops, void** npop, void** ret, int32_t* pop_cap);
 int taco_query_count_popped_device(taco_index* idx, int64_t nq, int64_t* hist_d, void* stream);
 /* Largest nq accepted by the split count/finish calls for this index. */

@@ -31,6 +31,7 @@ _SIGS = {
     "taco_index_set_data": [_vp, _vp],
     "taco_index_set_data_device": [_vp, _vp],
     "taco_index_row_format": [_vp],
+    "taco_index_layout": [_vp, _vp, _vp, _vp],
     "taco_fit_covariance": [_vp, _vp, _vp, _vp],
     "taco_covariance": [_c_int, _vp, _c_i64, _c_i32, _vp, _vp, _vp],
     "taco_jacobi_sweeps": [_vp, _vp, _c_i32, _c_dbl, _c_i32, _vp, _vp],
@@ -56,6 +57,7 @@ _SIGS = {
     "taco_query_batch_device": [_vp, _vp, _c_i64, _c_dbl, _c_dbl, _c_i32, _vp, _vp, _vp, _vp, _vp],
     "taco_query_count_device": [_vp, _vp, _c_i64, _c_dbl, _vp, _vp],
     "taco_query_front_device": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_i32, _vp, _vp],
+    "taco_query_front_async": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_i32, _vp, _vp],
     "taco_query_pop_buffers": [_vp, _vp, _vp, _vp, _vp],
     "taco_query_count_popped_device": [_vp, _c_i64, _vp, _vp],
     "taco_query_finish_device": [_vp, _c_i64, _vp, _c_dbl, _c_i32, _vp, _vp, _vp, _vp, _vp],
@@ -149,6 +151,13 @@ def device_id() -> int:
         if v not in (None, ""):
             return int(v)
     return 0
+
+
+def index_layout(h):
+    """(ids per chunk, chunks, cluster mode) of a device index (taco_index_layout)."""
+    chunk, nch, cm = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int32(0)
+    call("taco_index_layout", h, ctypes.byref(chunk), ctypes.byref(nch), ctypes.byref(cm))
+    return int(chunk.value), int(nch.value), bool(cm.value)
 
 
 def launch_count() -> int:

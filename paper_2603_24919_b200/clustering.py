@@ -122,4 +122,26 @@ def kmeans(data, n_clusters: int, max_iter: int = 20, seed: int = 0) -> KMeansMo
                        inertia_history=history, n_iter=len(history))
 
 
-__all__ = ["KMeansModel", "kmeans", "draw_plan", "forced_plan", "DimensionMismatchError"]
+def assign(model: KMeansModel, point) -> int:
+    """Index of the nearest centroid, ties to the lowest index
+    (clustering.py:118-127).  The device computes the reference's fp64
+    direct-form einsum distances and their stable rank (k_csort); the first
+    entry of a stable ascending argsort is numpy's first argmin."""
+    p = np.asarray(point, dtype=np.float64).ravel()
+    if p.shape[0] != model.dim:
+        raise DimensionMismatchError(
+            f"point has dimension {p.shape[0]}, centroids have {model.dim}")
+    p32 = p.astype(np.float32)
+    if not np.array_equal(p32.astype(np.float64), p):
+        raise ParameterError("assign: the B200 path takes float32-representable points")
+    C = np.ascontiguousarray(model.centroids, dtype=np.float32)
+    k, m = C.shape
+    q = np.ascontiguousarray(np.concatenate([p32, p32]))
+    d1s, d2s = np.empty(k), np.empty(k)
+    l1s, l2s = np.empty(k, np.int32), np.empty(k, np.int32)
+    nat.call("taco_centroid_order", nat.device_id(), nat.ptr(C), nat.ptr(C), k, m, m, nat.ptr(q),
+             nat.ptr(d1s), nat.ptr(l1s), nat.ptr(d2s), nat.ptr(l2s))
+    return int(l1s[0])
+
+
+__all__ = ["KMeansModel", "assign", "kmeans", "draw_plan", "forced_plan", "DimensionMismatchError"]

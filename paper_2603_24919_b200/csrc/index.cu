@@ -488,6 +488,14 @@ int32_t taco_index_row_format(const taco_index* idx) {
   return idx->xfmt;
 }
 
+int taco_index_layout(const taco_index* idx, int64_t* chunk, int64_t* nchunks, int32_t* cluster_mode) {
+  TACO_TRY(index_check(const_cast<taco_index*>(idx)));
+  if (chunk) *chunk = idx->chunk;
+  if (nchunks) *nchunks = idx->nchunks;
+  if (cluster_mode) *cluster_mode = idx->cluster_mode ? 1 : 0;
+  return TACO_OK;
+}
+
 int taco_index_set_data_device(taco_index* idx, const float* X_d) {
   TACO_TRY(index_check(idx));
   idx->mean_ready = false;

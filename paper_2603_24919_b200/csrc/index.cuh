@@ -49,6 +49,7 @@ struct QueryTile {
       cursor, cand, bpref, pd2, ppos, tseg, qthr, qb, qsq, qok, gsb, gsc, gtab, rlist, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   int64_t cand_cap = 0;
   int pop_cap = 0;
+  int64_t front_rows = 0;       // rows the split-traversal buffers were sized for
   int64_t* flags_h = nullptr;   // pinned copy of flags[0..3] (async read-back)
   void release();
 };

@@ -2264,11 +2264,11 @@ int taco_query_front_device(taco_index* idx, const float* Q_d, int64_t nq, int64
     TACO_FAIL(TACO_ERR_PARAMETER, "query slice [%lld, %lld) of %lld outside [0, %lld)", (long long)q_lo,
               (long long)q_hi, (long long)nq, (long long)rows);
   const int64_t Qt = super_tile(idx, pop_cap);
-  if (rows > Qt + 16) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile %lld", (long long)rows, (long long)Qt);
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
   QueryTile& t = idx->qt;
   t.pop_cap = pop_cap;
   TACO_TRY(ensure_front(idx, t, std::max(Qt, rows), 1));
+  t.front_rows = std::max(t.front_rows, rows);
   // every query of the tile: the re-rank (taco_query_finish_device) reads them all
   if (nq > 0)
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
@@ -2278,6 +2278,31 @@ int taco_query_front_device(taco_index* idx, const float* Q_d, int64_t nq, int64
   TACO_CHECK_CUDA(cudaMemcpyAsync(&f0, t.flags.p, 8, cudaMemcpyDeviceToHost, st));
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   *need = f0 > pop_cap ? f0 : 0;
+  return TACO_OK;
+}
+
+// As taco_query_front_device without the host round trip: the longest walk
+// of the slice (pops, capped or not) is copied to need_d[0] on the stream, so
+// a caller can all-reduce it and check all tiles of a batch with one sync.
+int taco_query_front_async(taco_index* idx, const float* Q_d, int64_t nq, int64_t q_lo, int64_t q_hi,
+                           int64_t rows, double alpha, int32_t pop_cap, int64_t* need_d, void* stream) {
+  TACO_TRY(check_query_ready(idx, alpha, 1));
+  if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
+  if (pop_cap < 1 || pop_cap > idx->K) TACO_FAIL(TACO_ERR_PARAMETER, "pop cap %d outside [1, %lld]", pop_cap, (long long)idx->K);
+  if (!(q_lo >= 0 && q_lo <= q_hi && q_hi <= nq && nq <= rows))
+    TACO_FAIL(TACO_ERR_PARAMETER, "query slice [%lld, %lld) of %lld outside [0, %lld)", (long long)q_lo,
+              (long long)q_hi, (long long)nq, (long long)rows);
+  if (!need_d) TACO_FAIL(TACO_ERR_PARAMETER, "need_d is null");
+  cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
+  QueryTile& t = idx->qt;
+  t.pop_cap = pop_cap;
+  TACO_TRY(ensure_front(idx, t, std::max(super_tile(idx, pop_cap), rows), 1));
+  t.front_rows = std::max(t.front_rows, rows);
+  if (nq > 0)
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_d, sizeof(float) * (size_t)nq * idx->d, cudaMemcpyDeviceToDevice, st));
+  TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
+  TACO_TRY(stage_front(idx, t, q_hi - q_lo, alpha, st, nullptr, q_lo));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(need_d, t.flags.p, 8, cudaMemcpyDeviceToDevice, st));
   return TACO_OK;
 }
 
@@ -2299,7 +2324,8 @@ int taco_query_count_popped_device(taco_index* idx, int64_t nq, int64_t* hist_d,
   if (idx->cluster_mode) TACO_FAIL(TACO_ERR_STATE, "split query needs a sharded (global-mode) index");
   QueryTile& t = idx->qt;
   if (!t.pops.p) TACO_FAIL(TACO_ERR_STATE, "no traversal buffers yet (call taco_query_front_device)");
-  if (nq > super_tile(idx, t.pop_cap) + 16) TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile", (long long)nq);
+  if (nq > std::max(t.front_rows, super_tile(idx, t.pop_cap) + 16))
+    TACO_FAIL(TACO_ERR_PARAMETER, "split query batch %lld exceeds tile", (long long)nq);
   if (nq == 0) return TACO_OK;
   cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
   TACO_TRY(global_count(idx, t, nq, st));

@@ -107,6 +107,14 @@ class CudaShardBackend:
                  self.pop_cap, ctypes.byref(need), self._stream())
         return int(need.value)
 
+    def front_async(self, Qt, alpha: float, lo: int, hi: int, rows: int):
+        """As ``front`` without a host sync: returns a device int64[1] holding
+        the slice's longest walk (checked once per batch by the caller)."""
+        need = self.torch.zeros(1, dtype=self.torch.int64, device=f"cuda:{self.device}")
+        nat.call("taco_query_front_async", self.dev.h, Qt.data_ptr(), Qt.shape[0], lo, hi, rows, float(alpha),
+                 self.pop_cap, need.data_ptr(), self._stream())
+        return need
+
     def raise_pop_cap(self, need: int) -> None:
         """Every rank gets the same all-reduced `need`, so caps stay equal."""
         self.pop_cap = min(self.k2, -(-(need + need // 4) // 64) * 64)
@@ -165,8 +173,11 @@ def _split_count(backend, Qt, alpha: float, group=None):
     """Stage 1 with the replicated traversal divided by query: rank r walks
     rows [r*per, (r+1)*per) of the tile, an in-place all_gather gives every
     rank all popped cells (identical to walking them itself: the traversal
-    reads only replicated state), then each rank counts its own ids."""
-    import torch
+    reads only replicated state), then each rank counts its own ids.
+
+    Returns (local histograms, the all-reduced longest walk as a device
+    tensor): no host sync here; the caller checks the walks of the whole
+    batch against the pop cap once (``sharded_query``)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -175,41 +186,66 @@ def _split_count(backend, Qt, alpha: float, group=None):
     per = -(-m // world)
     rows = per * world
     lo, hi = min(m, rank * per), min(m, rank * per + per)
-    for _ in range(2):
-        need = torch.tensor([backend.front(Qt, alpha, lo, hi, rows)], dtype=torch.int64, device=Qt.device)
-        dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
-        if int(need.item()) == 0:
-            break
-        backend.raise_pop_cap(int(need.item()))   # some rank's walk was longer than the cap: all redo
+    need = backend.front_async(Qt, alpha, lo, hi, rows)
+    dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
     for buf in backend.pop_views(rows):
         dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
-    return backend.count_popped(m)
+    return backend.count_popped(m), need
+
+
+def common_tile_size(backend, group=None, device=None) -> int:
+    """The query tile every rank uses: the MIN of the ranks' own tile sizes
+    (a rank's super-tile depends on its local chunk count, and the per-tile
+    collectives must have equal shapes on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([int(backend.tile_size())], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return int(t.item())
 
 
 def sharded_query(backend, Q, alpha: float, beta: float, k: int, group=None):
     """Batched k-ANN over a point-sharded index; every rank returns the full,
-    identical result (ids int32 [nq,k], dists f32 [nq,k], cand_num, last_coll)."""
+    identical result (ids int32 [nq,k], dists f32 [nq,k], cand_num, last_coll).
+
+    One host sync per batch: the tiles' all-reduced longest walks are checked
+    against the pop cap after the last tile; if any walk was truncated (rare:
+    the cap adapts to the workload and is kept), every rank raises its cap to
+    the same all-reduced need and the batch is re-run."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     nq = Q.shape[0]
-    T = backend.tile_size()
-    outs = []
-    for q0 in range(0, nq, T):
-        Qt = Q[q0:q0 + T]
-        m = Qt.shape[0]
-        if hasattr(backend, "front"):
-            hist = _split_count(backend, Qt, alpha, group)
-        else:
-            hist = backend.count(Qt, alpha)
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
-        d2, ids, num, lvl = backend.finish(m, hist, beta, k)
-        d2_all = torch.empty((world * m, k), dtype=d2.dtype, device=d2.device)
-        ids_all = torch.empty((world * m, k), dtype=ids.dtype, device=ids.device)
-        dist.all_gather_into_tensor(d2_all, d2.contiguous(), group=group)
-        dist.all_gather_into_tensor(ids_all, ids.contiguous(), group=group)
-        oi, od = backend.merge(d2_all.view(world, m, k), ids_all.view(world, m, k), k)
-        outs.append((oi, od, num, lvl))
+    split = hasattr(backend, "front_async")
+    T = getattr(backend, "common_tile", None)
+    if T is None:
+        T = common_tile_size(backend, group, Q.device)
+        backend.common_tile = T
+    for _attempt in range(2):
+        outs, needs = [], []
+        for q0 in range(0, nq, T):
+            Qt = Q[q0:q0 + T]
+            m = Qt.shape[0]
+            if split:
+                hist, need = _split_count(backend, Qt, alpha, group)
+                needs.append(need)
+            else:
+                hist = backend.count(Qt, alpha)
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+            d2, ids, num, lvl = backend.finish(m, hist, beta, k)
+            d2_all = torch.empty((world * m, k), dtype=d2.dtype, device=d2.device)
+            ids_all = torch.empty((world * m, k), dtype=ids.dtype, device=ids.device)
+            dist.all_gather_into_tensor(d2_all, d2.contiguous(), group=group)
+            dist.all_gather_into_tensor(ids_all, ids.contiguous(), group=group)
+            oi, od = backend.merge(d2_all.view(world, m, k), ids_all.view(world, m, k), k)
+            outs.append((oi, od, num, lvl))
+        if not needs:
+            break
+        longest = int(torch.cat(needs).max().item())   # the batch's one host sync
+        if longest <= backend.pop_cap:
+            break
+        backend.raise_pop_cap(longest)   # same all-reduced value on every rank: caps stay equal
     cat = lambda i: torch.cat([o[i] for o in outs]) if outs else None  # noqa: E731
     return cat(0), cat(1), cat(2), cat(3)

@@ -51,6 +51,7 @@ from .spectral import (
 )
 
 INDEX_MAGIC = b"TACO"
+TOPK_MAX = 2048   # query.cu TK_MAX: results per query the device top-k keeps
 INDEX_VERSION = 1
 _MAX_SUBSPACES = 255
 
@@ -132,6 +133,23 @@ def _data_key(X: np.ndarray):
     rows = np.unique(np.linspace(0, max(n - 1, 0), num=min(n, 64)).astype(np.int64)) if n else []
     dig = hashlib.blake2b(np.ascontiguousarray(X[rows]).tobytes(), digest_size=16).hexdigest()
     return (X.ctypes.data, X.shape, X.strides, X.dtype.str, dig)
+
+
+def refresh_data(index: TacoIndex, data) -> None:
+    """Re-upload ``data`` as the index's resident base matrix unconditionally.
+
+    The per-call identity check (``_data_key``: pointer, shape, strides,
+    dtype and a digest of 64 sampled rows) cannot see an in-place edit of
+    rows it does not sample; a caller that mutates ``data`` in place between
+    queries calls this."""
+    dev = _device_of(index)
+    X = as_f32_exact(np.asarray(data), "data")
+    if X.ndim != 2 or X.shape != (index.n, index.d):
+        raise DimensionMismatchError(
+            f"data shape {X.shape} does not match index ({index.n}, {index.d})")
+    X = np.ascontiguousarray(X)
+    nat.call("taco_index_set_data", dev.h, nat.ptr(X))
+    dev.data_key = _data_key(X)
 
 
 def _resident(index: TacoIndex, data) -> np.ndarray:
@@ -371,13 +389,24 @@ def knn_query_batch(index: TacoIndex, data, queries, qp: QueryParams):
     if Q.ndim != 2 or Q.shape[1] != index.d:
         raise DimensionMismatchError(f"queries have shape {Q.shape}, index expects (*, {index.d})")
     nq, k = Q.shape[0], int(qp.k)
-    ids = np.empty((nq, k), np.int32)
-    dists = np.empty((nq, k), np.float32)
+    # at most min(k, n) results exist: a k beyond the device top-k limit is
+    # served when n itself fits under it (the rest is padding)
+    kk = min(k, index.n) if k > TOPK_MAX else k
+    if kk > TOPK_MAX:
+        raise ParameterError(f"result count {k} exceeds the B200 top-k limit {TOPK_MAX} "
+                             f"(n = {index.n})")
+    ids = np.full((nq, k), -1, np.int32)
+    dists = np.full((nq, k), np.inf, np.float32)
     num = np.empty(nq, np.int64)
     lvl = np.empty(nq, np.int32)
     if nq:
+        oi = ids if kk == k else np.empty((nq, kk), np.int32)
+        od = dists if kk == k else np.empty((nq, kk), np.float32)
         nat.call("taco_query_batch", _device_of(index).h, nat.ptr(Q), nq, float(qp.alpha), float(qp.beta),
-                 k, nat.ptr(ids), nat.ptr(dists), nat.ptr(num), nat.ptr(lvl))
+                 kk, nat.ptr(oi), nat.ptr(od), nat.ptr(num), nat.ptr(lvl))
+        if kk != k:
+            ids[:, :kk] = oi
+            dists[:, :kk] = od
     return ids, dists, num, lvl
 
 
@@ -390,6 +419,8 @@ def knn_query(index: TacoIndex, data, query, qp: QueryParams,
     X = np.asarray(data)
     if X.ndim == 2 and X.shape[1] != q.shape[0]:
         raise DimensionMismatchError(f"query has dimension {q.shape[0]}, data has {X.shape[1]}")
+    if scratch is not None:   # engine.py:285: the reference counts into the caller's buffer
+        count_collisions(index, q, qp.alpha, out=scratch)
     ids, dists, _, _ = knn_query_batch(index, data, q[None, :], qp)
     keep = ids[0] >= 0
     return SearchResult(ids=ids[0][keep].copy(), dists=dists[0][keep].copy())

@@ -219,3 +219,12 @@ def scalable_dynamic_activation(alpha, n, n_cells, dists1, idx1, dists2, idx2,
         retrieved.append(cells.get((a, b), _EMPTY_IDS))
         trace.append((float(key), a, b))
     return ActivationResult(tuple(retrieved), int(got[0]), tuple(trace))
+
+
+def linear_dynamic_activation(alpha, n, n_cells, dists1, idx1, dists2, idx2,
+                              imi) -> ActivationResult:
+    """The reference's linear-frontier variant (imi.py:169-208).  Its contract
+    is the heap traversal's exact cell sequence (the reference asserts the two
+    traces are equal, bench.py:248-255), so it runs the same device walk
+    (k_traverse); only the reference's CPU cost model differs."""
+    return scalable_dynamic_activation(alpha, n, n_cells, dists1, idx1, dists2, idx2, imi)

@@ -34,6 +34,10 @@ RIGS = [
     ("rig1", 1, 3000, 24, 32, 8, 4, 8, 10, 5, [(0.05, 0.01, 10), (0.1, 0.05, 20)]),
     ("rig2", 2, 20000, 16, 128, 8, 16, 16, 20, 0, [(0.03, 0.01, 10)]),
     ("rig3", 3, 4000, 12, 60, 4, 15, 6, 20, 3, [(0.05, 0.02, 10)]),
+    # N_s = 16: 8-bit count tables with wide tallies (the config-3 count path)
+    ("rig4", 3, 20000, 16, 64, 16, 4, 8, 10, 7, [(0.05, 0.01, 10), (0.2, 0.05, 10)]),
+    # N_s = 20: levels above 16 (table-scan level histogram), half widths 2 / 1
+    ("rig5", 4, 12000, 12, 64, 20, 3, 6, 10, 9, [(0.05, 0.01, 10), (0.3, 0.1, 12)]),
 ]
 
 
@@ -231,6 +235,11 @@ def main():
     ref = load_reference()
     if sys.argv[1:] == ["sclinear"]:
         sc_fixture(ref)
+        return
+    if sys.argv[1:]:   # named rigs only, e.g. `make_golden.py rig4 rig5`
+        for rig in RIGS:
+            if rig[0] in sys.argv[1:]:
+                rig_fixture(ref, *rig)
         return
     unit_fixture(ref)
     for rig in RIGS:

@@ -50,6 +50,12 @@ class OracleShardBackend:
                     self.pops[r, j, t] = a * kp + b
         return need
 
+    def front_async(self, Qt, alpha, lo, hi, rows):
+        """distributed._split_count's protocol: the slice's longest walk as a
+        tensor (the caller checks it against the cap once per batch)."""
+        self.front(Qt, alpha, lo, hi, rows)
+        return torch.tensor([int(self.npop[lo:hi].max()) if hi > lo else 0], dtype=torch.int64)
+
     def raise_pop_cap(self, need):
         self.pop_cap = min(self.o.kprime ** 2, need + 1)
 

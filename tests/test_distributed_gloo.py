@@ -33,14 +33,16 @@ def _worker(rank, world, port, cfg, out_q):
     X, Q, _ = make_config(1, n=cfg["n"], nq=cfg["nq"], d=32)
     oidx = O.build_index(X, 8, 4, 64, 8, 3)
     lo, hi = shard_range(X.shape[0], rank, world)
-    be = OracleShardBackend(oidx, X[lo:hi], lo, X.shape[0], tile=5)
+    be = OracleShardBackend(oidx, X[lo:hi], lo, X.shape[0], tile=cfg.get("tiles", (5, 5))[rank])
     ids, dists, num, lvl = sharded_query(be, torch.from_numpy(Q), cfg["alpha"], cfg["beta"], cfg["k"])
     out_q.put((rank, ids.numpy(), dists.numpy(), num.numpy(), lvl.numpy(), be.pop_cap))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("cfg", [dict(n=1500, nq=12, alpha=0.05, beta=0.02, k=10),
-                                 dict(n=1201, nq=9, alpha=0.3, beta=0.9, k=7)])
+                                 dict(n=1201, nq=9, alpha=0.3, beta=0.9, k=7),
+                                 # ranks whose own tile sizes differ must agree on one
+                                 dict(n=1500, nq=11, alpha=0.05, beta=0.02, k=10, tiles=(5, 3))])
 def test_sharded_equals_single(cfg):
     world = 2
     ctx = mp.get_context("spawn")

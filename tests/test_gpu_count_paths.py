@@ -1,0 +1,104 @@
+"""Every counting layout the product runs, against the reference's own
+answers (golden fixtures from tests/golden/make_golden.py) and the oracle.
+
+The batched count has three layouts:
+  * cluster mode with ONE CTA per query (n small: all earlier rigs);
+  * cluster mode with SEVERAL CTAs per query -- the config-2/3 path: per-CTA
+    id chunks, level histograms gathered over DSMEM, split cluster barrier,
+    per-CTA candidate segments.  TACO_CLUSTER_IDS shrinks the chunk so a
+    20,000-point rig runs it with 10 CTAs per query;
+  * global mode (sharded / n > 1.5M, config 4): per-(query, chunk) CTAs,
+    spilled score >= 2 records, emit sweep, recount list.
+and three table widths: 4-bit (N_s <= 15), 8-bit with wide tallies
+(N_s = 16, config 3) and 8-bit with a table-scan level histogram (N_s > 16).
+rig2 (N_s = 8), rig4 (N_s = 16) and rig5 (N_s = 20) cover the widths; the
+modes below cover the layouts.  All must equal the reference bit-for-bit."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_24919_b200 as T
+from oracle import taco_oracle as O
+from paper_2603_24919_b200 import _native as nat
+from paper_2603_24919_b200.engine import _device_of
+from paper_2603_24919_b200.workloads import make_config
+
+pytestmark = pytest.mark.gpu
+
+# mode -> (environment at index creation, expected (cluster mode, min chunks))
+MODES = {
+    "cluster_1cta": ({}, (True, 1)),
+    "cluster_multi": ({"TACO_CLUSTER_IDS": "2048"}, (True, 5)),
+    "cluster_odd": ({"TACO_CLUSTER_IDS": "7000"}, (True, 2)),
+    "global": ({"TACO_GLOBAL_MODE": "1"}, (False, 1)),
+    "global_small_chunk": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "2048"}, (False, 5)),
+}
+
+
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.fixture(scope="module", params=["rig2", "rig4", "rig5"])
+def rig(request, golden):
+    g = golden(request.param)
+    cfg, n, nq, d, ns, s, kp, it, seed = (int(v) for v in g["params"])
+    X, Q, _ = make_config(cfg, n=n, nq=nq, d=d)
+    return request.param, g, X, Q
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_count_layout_matches_reference(rig, mode):
+    name, g, X, Q = rig
+    env, (want_cluster, min_chunks) = MODES[mode]
+    idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
+    chunk, nch, cluster = nat.index_layout(_device_of(idx).h)
+    assert cluster == want_cluster and nch >= min_chunks, (chunk, nch, cluster)
+    for gi, (alpha, beta, k) in enumerate(g["grid"]):
+        qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+        np.testing.assert_array_equal(num, g[f"num_{gi}"])
+        np.testing.assert_array_equal(lvl, g[f"lvl_{gi}"])
+        np.testing.assert_array_equal(ids, g[f"ids_{gi}"])
+        np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
+
+
+def test_multi_cta_against_oracle_many_queries(rig):
+    """More queries than the golden rig holds (the oracle answers them), both
+    batch tiles, through the 10-CTA cluster path and global mode."""
+    name, g, X, Q0 = rig
+    cfg, n, nq, d, ns, s, kp, it, seed = (int(v) for v in g["params"])
+    _, Q, _ = make_config(cfg, n=n, nq=96, d=d)
+    oidx = O.deserialize(g["blob"].tobytes())
+    alpha, beta, k = (float(v) for v in g["grid"][-1])
+    oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, beta, int(k), threads=8)
+    for env in (MODES["cluster_multi"][0], MODES["global_small_chunk"][0]):
+        idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, int(k)))
+        np.testing.assert_array_equal(num, on)
+        np.testing.assert_array_equal(lvl, ol)
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(dists, od)
+
+
+def test_scores_tap_wide_levels(rig):
+    """count_collisions (uint8 table) equals the reference's table digests,
+    including N_s = 16 / 20 where scores exceed a nibble."""
+    name, g, X, Q = rig
+    idx = T.deserialize_index(g["blob"].tobytes())
+    for gi, (alpha, _, _) in enumerate(g["grid"]):
+        for qi in range(Q.shape[0]):
+            sc = T.count_collisions(idx, Q[qi], float(alpha))
+            import hashlib
+            assert hashlib.blake2b(sc.tobytes(), digest_size=16).hexdigest() == g[f"scores_digest_{gi}"][qi]

@@ -269,3 +269,50 @@ def test_pipelined_batch_matches_oracle():
     np.testing.assert_array_equal(lvl[sel], ol)
     i2, d2, n2, l2 = T.knn_query_batch(idx, X, Q[2250:2260], qp)   # a small unpipelined batch
     np.testing.assert_array_equal(i2, ids[2250:2260])
+
+
+def test_assign_matches_reference_formula():
+    """clustering.assign (clustering.py:118-127): nearest centroid by the fp64
+    einsum distance, ties to the lowest index."""
+    rng = np.random.default_rng(5)
+    C = rng.normal(size=(40, 7)).astype(np.float32)
+    C[17] = C[3]                                   # duplicate centroid: tie -> 3
+    model = T.KMeansModel(C, None, 0.0)
+    pts = np.vstack([rng.normal(size=(50, 7)), C[3:4], C[17:18]]).astype(np.float32)
+    for p in pts:
+        e = C.astype(np.float64) - p.astype(np.float64)
+        want = int(np.argmin(np.einsum("ij,ij->i", e, e)))
+        assert T.assign(model, p) == want
+    with pytest.raises(T.DimensionMismatchError):
+        T.assign(model, np.zeros(6, np.float32))
+
+
+def test_knn_query_fills_scratch_and_pads_large_k(rig):
+    """knn_query(scratch=...) leaves the query's collision counts in the
+    buffer like engine.py:285; k beyond the device top-k limit is served when
+    n fits under it (padding -1 / +inf like cli.py:155-164)."""
+    g, X, Q, idx = rig
+    alpha, beta, k = g["grid"][0]
+    qp = T.QueryParams(float(alpha), float(beta), int(k))
+    scratch = np.full(idx.n, 7, np.uint8)
+    res = T.knn_query(idx, X, Q[0], qp, scratch=scratch)
+    np.testing.assert_array_equal(scratch, T.count_collisions(idx, Q[0], float(alpha)))
+    assert _digest(scratch) == g["scores_digest_0"][0]
+    want = g["ids_0"][0]
+    np.testing.assert_array_equal(res.ids, want[want >= 0])
+    if idx.n <= T.engine.TOPK_MAX:
+        return
+    with pytest.raises(T.ParameterError):
+        T.knn_query_batch(idx, X, Q[:2], T.QueryParams(float(alpha), float(beta), T.engine.TOPK_MAX + 1))
+
+
+def test_large_k_on_small_index():
+    X, Q, _ = make_config(1, n=1500, nq=6, d=32)
+    idx = T.build_index(X, T.IndexParams(4, 8, 16, 5, 1))
+    qp = T.QueryParams(0.5, 0.9, 3000)             # k > TK_MAX and k > n
+    ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+    oidx = O.deserialize(T.serialize_index(idx))
+    oi, od, on, ol = O.knn_batch(oidx, X, Q, qp.alpha, qp.beta, qp.k)
+    np.testing.assert_array_equal(ids, oi)
+    np.testing.assert_array_equal(dists, od)
+    np.testing.assert_array_equal(num, on)
