@@ -235,19 +235,37 @@ def cpu_baseline(index, X, Q, meta, ids_gpu, budget_s=15.0, threads=None):
             "seconds": el, "topk_identical_to_gpu": parity}
 
 
+def _workloads_module():
+    """paper_2603_24919_b200/workloads.py loaded on its own (plain numpy), so the
+    reference arm never imports the product package or loads its library."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_2603_24919_b200", "workloads.py")
+    spec = importlib.util.spec_from_file_location("taco_bench_workloads", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def run_reference(args):
-    """--impl reference: timed CPU oracle (rank 0 only)."""
+    """--impl reference: the reference's algorithm on the host cores (the
+    oracle port, rank 0 only), built AND queried on the CPU: the index comes
+    from the oracle's own build (engine.py:122-174 restated; the 2*N_s
+    independent k-means halves run in parallel processes), never from the
+    product library, which this arm does not load."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2603_24919_b200 as T
     from oracle import taco_oracle as O
-    X, Q, meta = workload(args)
-    index, _ = build(X, meta)
-    oidx = O.deserialize(T.serialize_index(index))
+    W = _workloads_module()
+    t = time.perf_counter()
+    X, Q, meta = W.make_config(args.config, n=args.n, nq=args.nq)
+    meta["gen_seconds"] = time.perf_counter() - t
     threads = os.cpu_count() or 1
+    tim = {}
+    oidx = O.build_index(X, meta["n_sub"], meta["s"], meta["clusters"], meta["kmeans_iters"], meta["seed"],
+                         workers=threads, timings=tim)
     a, b, k = meta["alpha"], meta["beta"], meta["k"]
-    per = args.ref_sample
+    per = max(args.ref_sample, -(-2560 // max(args.steps, 1)))   # >= 2,560 timed queries per run
     times = []
     for s in range(args.warmup + args.steps):
         lo = (s * per) % Q.shape[0]
@@ -263,11 +281,24 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(meta), "step": f"{per} queries of the batch"},
+            "data": "synthetic (SURVEY 8(d) generator, seeded)", "impl": "reference",
+            "config": {"workload": workload_name(meta), "step": f"{per} queries of the batch",
+                       "index": "built on the CPU by the oracle (reference algorithm), not by the GPU"},
+            "build_seconds": tim["build_seconds"],
+            "cpu_build_seconds": tim["build_seconds"],
+            "cpu_build_breakdown": {"transform_seconds": tim["transform_seconds"],
+                                    "kmeans_seconds": tim["kmeans_seconds"],
+                                    "kmeans_workers": min(threads, 2 * meta["n_sub"])},
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
-                             "sample": f"{per} queries per step, {args.steps} timed steps"},
+                             "sample": f"{per} queries per step, {args.steps} timed steps "
+                                       f"({nq} queries), index built by the oracle in "
+                                       f"{tim['build_seconds']:.1f} s"},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        with open("/proc/self/maps") as fh:
+            line["product_library_loaded"] = "libtaco_b200" in fh.read()
+    except OSError:
+        pass
     print(json.dumps(line), flush=True)
 
 
@@ -579,6 +610,16 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=256)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: relaunch this command under torchrun (rank 0 prints the line)
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

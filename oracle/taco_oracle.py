@@ -331,9 +331,64 @@ def cells_from_labels(l1, l2):
     return {(int(ka[x]), int(kb[x])): ids[x:y].copy() for x, y in zip(lo, hi)}
 
 
-def build_index(X, n_sub, s, clusters, iters=20, seed=0, T=None, model=None):
+def _kmeans_half_worker(job):
+    """One k-means half in a spawned process (``build_index(workers=...)``):
+    the transformed matrix is read from shared memory, BLAS runs one thread."""
+    from multiprocessing import shared_memory
+
+    name, shape, col0, col1, kp, iters, seed = job
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        T = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
+        r = kmeans(np.ascontiguousarray(T[:, col0:col1]), kp, iters, seed)
+    finally:
+        shm.close()
+    return r
+
+
+def _kmeans_halves(T, n_sub, s, kp, iters, seed, workers):
+    """The 2*N_s k-means runs of imi.py:68-69, in order; with workers > 1 they
+    run in parallel processes (independent problems: identical results)."""
+    split = (s + 1) // 2
+    jobs = []
+    for j in range(n_sub):
+        sj = derive_seed(seed, j)
+        jobs.append((j * s, j * s + split, kp, iters, derive_seed(sj, 0)))
+        jobs.append((j * s + split, (j + 1) * s, kp, iters, derive_seed(sj, 1)))
+    if workers <= 1:
+        return [kmeans(T[:, a:b], k, it, sd) for a, b, k, it, sd in jobs]
+    import multiprocessing as mp
+    import os
+    from multiprocessing import shared_memory
+
+    T = np.ascontiguousarray(T, dtype=np.float32)
+    shm = shared_memory.SharedMemory(create=True, size=max(T.nbytes, 1))
+    saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS")}
+    try:
+        np.ndarray(T.shape, np.float32, buffer=shm.buf)[:] = T
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"   # one BLAS thread per process (inherited at spawn)
+        os.environ["OMP_NUM_THREADS"] = "1"
+        with mp.get_context("spawn").Pool(min(workers, len(jobs))) as pool:
+            return pool.map(_kmeans_half_worker, [(shm.name, T.shape) + jb for jb in jobs], chunksize=1)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        shm.close()
+        shm.unlink()
+
+
+def build_index(X, n_sub, s, clusters, iters=20, seed=0, T=None, model=None, workers=1, timings=None):
     """engine.py:122-174 + imi.py:49-85.  ``model``/``T`` let stage-wise
-    parity tests inject a fixed transform."""
+    parity tests inject a fixed transform; ``workers`` > 1 runs the 2*N_s
+    independent k-means halves in parallel processes (the CPU baseline);
+    ``timings`` (a dict) receives transform / k-means seconds like
+    engine.py:156-166."""
+    import time as _time
+
+    t0 = _time.perf_counter()
     X = np.ascontiguousarray(X, dtype=np.float32)
     n, d = X.shape
     kp = math.isqrt(clusters)
@@ -344,19 +399,22 @@ def build_index(X, n_sub, s, clusters, iters=20, seed=0, T=None, model=None):
         warns = []
     if T is None:
         T = transform(mean, blocks, X)
+    t1 = _time.perf_counter()
     split = (s + 1) // 2
     idx = OracleIndex(n, d, n_sub, s, clusters, iters, seed, mean, list(blocks),
                       [], [], [], warnings=warns)
+    halves = _kmeans_halves(T, n_sub, s, kp, iters, seed, workers)
     for j in range(n_sub):
-        sj = derive_seed(seed, j)
-        blk = T[:, j * s:(j + 1) * s]
-        r1 = kmeans(blk[:, :split], kp, iters, derive_seed(sj, 0))
-        r2 = kmeans(blk[:, split:], kp, iters, derive_seed(sj, 1))
+        r1, r2 = halves[2 * j], halves[2 * j + 1]
         idx.cb1.append(r1.centroids)
         idx.cb2.append(r2.centroids)
         idx.labels.append((r1.labels, r2.labels))
         idx.seeds.append((r1.seeds, r2.seeds))
         idx.cells.append(cells_from_labels(r1.labels, r2.labels))
+    if timings is not None:
+        timings["transform_seconds"] = t1 - t0
+        timings["kmeans_seconds"] = _time.perf_counter() - t1
+        timings["build_seconds"] = _time.perf_counter() - t0
     return idx
 
 
