@@ -110,6 +110,29 @@ int taco_index_set_cells(taco_index* idx, const int64_t* offsets_h, const uint32
 /* Global cell sizes (u32[N_s*K'^2]) for a sharded index; single GPU derives them. */
 int taco_index_set_global_sizes(taco_index* idx, const int64_t* sizes_h);
 
+/* --------------------------------------------- point-sharded build (8(e)) */
+/* Column-sum chain of this shard's rows (spectral.py:107, sequential fp64):
+ * starts from carry_in_h[d] (the running sums after all earlier shards) or,
+ * when NULL, from the shard's first row; carry_out_h[d] = the sums after its
+ * last row.  *bad_row = first local row with a non-finite value, else -1
+ * (spectral.py:102-105).  Ranks run it as a rank-ordered chain. */
+int taco_shard_colsum(taco_index* idx, const double* carry_in_h, double* carry_out_h, int64_t* bad_row);
+/* Centred Gram chain (spectral.py:108-109): carry_out_h[d*d] = carry_in_h (or
+ * 0) + the Gram partials of this shard's rows in blocks of block_rows (<= 0:
+ * taco_gram_block_rows(), the single-GPU decomposition), added in block
+ * order.  Shards starting on multiples of block_rows, chained in rank order,
+ * give exactly the single-GPU Gram. */
+int taco_shard_gram(taco_index* idx, const double* mean_h, int64_t block_rows, const double* carry_in_h,
+                    double* carry_out_h);
+int taco_gram_block_rows(void);
+/* Device copies of the transformed matrix (dimension-major [D][n] f32) and of
+ * the k-means labels ([2 N_s][n] i32, half 2j / 2j+1 = codebook 1 / 2 of
+ * subspace j): the all-to-all exchanges of the sharded k-means. */
+int taco_index_set_transformed_device(taco_index* idx, const float* T_d);
+int taco_get_transformed_device(taco_index* idx, float* T_d);
+int taco_get_labels_device(taco_index* idx, int32_t* lab_d);
+int taco_index_set_labels_device(taco_index* idx, const int32_t* lab_d);
+
 /* ---------------------------------------------------------------- exports */
 int taco_get_codebooks(taco_index* idx, float* cb1_h, float* cb2_h);
 int taco_get_labels(taco_index* idx, int32_t* lab1_h, int32_t* lab2_h);

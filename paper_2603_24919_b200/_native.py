@@ -80,6 +80,13 @@ _SIGS = {
     "taco_profile_name": [_c_int],
     "taco_profile_kernels": [],
     "taco_index_stream": [_vp],
+    "taco_shard_colsum": [_vp, _vp, _vp, _vp],
+    "taco_shard_gram": [_vp, _vp, _c_i64, _vp, _vp],
+    "taco_gram_block_rows": [],
+    "taco_index_set_transformed_device": [_vp, _vp],
+    "taco_get_transformed_device": [_vp, _vp],
+    "taco_get_labels_device": [_vp, _vp],
+    "taco_index_set_labels_device": [_vp, _vp],
     "taco_kmeans": [_c_int, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp],
 }

@@ -94,7 +94,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // row n divides (the staged upload runs one launch per landed chunk).
 __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restrict__ X, int64_t r0g, int64_t r1g,
                                                             int64_t n, int d, double* __restrict__ state,
-                                                            double* __restrict__ mean) {
+                                                            double* __restrict__ mean, int chained) {
   extern __shared__ __align__(16) float cm[];
   const int c0 = blockIdx.x * CM_W;
   const int nc = min(CM_W, d - c0);
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restr
   };
   if (tid >= 32)
     for (int s = 0; s < CM_STAGES - 1; ++s) load(s);
-  double acc = (r0g > 0 && tid < nc) ? state[c0 + tid] : 0.0;
+  // chained: this device's row 0 continues a chain begun on an earlier shard
+  double acc = ((r0g > 0 || chained) && tid < nc) ? state[c0 + tid] : 0.0;
   for (int64_t tb = 0; tb < ntile; ++tb) {
     if (tid >= 32) cp_wait<CM_STAGES - 2>();   // tile tb has landed (this thread's pieces)
     __syncthreads();                             // ... everyone's; slot (tb-1)%S is free
@@ -134,25 +135,25 @@ __global__ void __launch_bounds__(CM_THREADS) k_colmean_seq(const float* __restr
     } else if (tid < nc) {
       const float* tv = cm + (size_t)(tb % CM_STAGES) * CM_ROWS * CM_W + tid;
       const int rr = (int)min((int64_t)CM_ROWS, nrow - tb * CM_ROWS);
-      if (tb == 0 && r0g == 0) acc = chain_add((double)tv[0], tv + CM_W, rr - 1, CM_W);
+      if (tb == 0 && r0g == 0 && !chained) acc = chain_add((double)tv[0], tv + CM_W, rr - 1, CM_W);
       else acc = chain_add(acc, tv, rr, CM_W);
     }
   }
   if (tid < nc) {
     state[c0 + tid] = acc;
-    if (r1g == n) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
+    if (r1g == n && mean) mean[c0 + tid] = __ddiv_rn(acc, (double)n);
   }
 }
 
 int launch_colmean(cudaStream_t st, const float* X, int64_t r0, int64_t r1, int64_t n, int d, double* state,
-                   double* mean) {
+                   double* mean, int chained) {
   static bool attr = false;
   if (!attr) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_colmean_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM));
     attr = true;
   }
   if (r1 <= r0) return TACO_OK;
-  k_colmean_seq<<<(unsigned)ceil_div(d, CM_W), CM_THREADS, CM_SMEM, st>>>(X, r0, r1, n, d, state, mean);
+  k_colmean_seq<<<(unsigned)ceil_div(d, CM_W), CM_THREADS, CM_SMEM, st>>>(X, r0, r1, n, d, state, mean, chained);
   TACO_LAUNCHED();
   return TACO_OK;
 }
@@ -213,13 +214,47 @@ __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ X, int64
   }
 }
 
-__global__ void k_gram_reduce(const double* __restrict__ partial, int splits, int64_t dd,
-                              double* __restrict__ G) {
+// G += partial[0] + partial[1] + ... (sequential, in block order).  The Gram
+// is a chain over fixed blocks of kGramBlock rows (the block partials are the
+// only parallel part), so a point-sharded build whose shards start on block
+// boundaries reproduces it exactly by carrying G from shard to shard.
+__global__ void k_gram_accum(const double* __restrict__ partial, int splits, int64_t dd,
+                             double* __restrict__ G) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= dd) return;
-  double acc = 0.0;
+  double acc = G[e];
   for (int s = 0; s < splits; ++s) acc = __dadd_rn(acc, partial[(size_t)s * dd + e]);
   G[e] = acc;
+}
+
+constexpr int64_t kGramBlock = 4096;   // rows per Gram partial (a multiple of GK)
+
+// G (device, d x d, holding the carried-in sum) += the centred Gram of rows
+// [0, n) of X, block by block; partial memory bounded by grouping blocks.
+static int gram_chain(const float* X, int64_t n, int d, const double* mean_d, int64_t block_rows, double* G,
+                      cudaStream_t st) {
+  if (n <= 0) return TACO_OK;
+  if (block_rows < GK || block_rows % GK) TACO_FAIL(TACO_ERR_PARAMETER, "Gram block of %lld rows", (long long)block_rows);
+  const int tiles = (int)ceil_div(d, GT);
+  const int64_t dd = (int64_t)d * d;
+  const int64_t nblocks = ceil_div(n, block_rows);
+  const int64_t group = std::max<int64_t>(1, std::min<int64_t>(nblocks, ((int64_t)1 << 30) / (8 * dd)));
+  DevBuf part;
+  TACO_TRY(part.ensure(8 * (size_t)group * dd));
+  for (int64_t b0 = 0; b0 < nblocks; b0 += group) {
+    const int64_t nb = std::min(group, nblocks - b0);
+    const int64_t r0 = b0 * block_rows;
+    const int64_t rows = std::min(n - r0, nb * block_rows);
+    k_gram<<<dim3(tiles, tiles, (unsigned)nb), 256, 0, st>>>(X + (size_t)r0 * d, rows, d, mean_d, block_rows,
+                                                            part.as<double>());
+    count_launch();
+    k_gram_accum<<<(unsigned)ceil_div(dd, 256), 256, 0, st>>>(part.as<double>(), (int)nb, dd, G);
+    count_launch();
+  }
+  cudaError_t e = cudaStreamSynchronize(st);   // part is released below
+  part.release();
+  if (e != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  return TACO_OK;
 }
 
 // ================================================================ k-means
@@ -1902,7 +1937,7 @@ extern "C" {
 
 static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, double* mean_h,
                            double* gram_h, int64_t* bad_row, const double* mean_ready = nullptr) {
-  DevBuf bad, mean, part, G, cstate;
+  DevBuf bad, mean, G, cstate;
   int rc = TACO_OK;
   do {
     if ((rc = bad.ensure(8)) || (rc = mean.ensure(8 * d)) || (rc = G.ensure(8 * (size_t)d * d))) break;
@@ -1920,25 +1955,17 @@ static int covariance_impl(const float* Xd, int64_t n, int d, cudaStream_t st, d
       TACO_CHECK_CUDA(cudaMemcpyAsync(mean.p, mean_ready, 8 * (size_t)d, cudaMemcpyDeviceToDevice, st));
     } else {
       if ((rc = cstate.ensure(8 * (size_t)d))) break;
-      if ((rc = launch_colmean(st, Xd, 0, n, n, d, cstate.as<double>(), mean.as<double>()))) break;
+      if ((rc = launch_colmean(st, Xd, 0, n, n, d, cstate.as<double>(), mean.as<double>(), 0))) break;
     }
-    const int tiles = (int)ceil_div(d, GT);
-    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(592, tiles * tiles), ceil_div(n, 256)));
-    const int64_t rows_per = ceil_div(ceil_div(n, splits), GK) * GK;
-    splits = (int)ceil_div(n, rows_per);
-    if ((rc = part.ensure(8 * (size_t)splits * d * d))) break;
-    k_gram<<<dim3(tiles, tiles, splits), 256, 0, st>>>(Xd, n, d, mean.as<double>(), rows_per,
-                                                      part.as<double>());
-    count_launch();
     const int64_t dd = (int64_t)d * d;
-    k_gram_reduce<<<(unsigned)ceil_div(dd, 256), 256, 0, st>>>(part.as<double>(), splits, dd, G.as<double>());
-    count_launch();
+    TACO_CHECK_CUDA(cudaMemsetAsync(G.p, 0, 8 * (size_t)dd, st));
+    if ((rc = gram_chain(Xd, n, d, mean.as<double>(), kGramBlock, G.as<double>(), st))) break;
     cudaMemcpyAsync(mean_h, mean.p, 8 * d, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(gram_h, G.p, 8 * dd, cudaMemcpyDeviceToHost, st);
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); rc = TACO_ERR_CUDA; }
   } while (0);
-  bad.release(); mean.release(); part.release(); G.release(); cstate.release();
+  bad.release(); mean.release(); G.release(); cstate.release();
   return rc;
 }
 
@@ -1952,6 +1979,62 @@ int taco_fit_covariance(taco_index* idx, double* mean_h, double* gram_h, int64_t
   }
   return covariance_impl(idx->X.as<float>(), idx->n, idx->d, idx->stream, mean_h, gram_h, bad_row, mr);
 }
+
+// ---------------------------------------------------- point-sharded build
+// Column-sum chain of this shard's rows (numpy mean(axis=0)'s sequential
+// per-column add, spectral.py:107): starts from carry_in (the running sums of
+// all earlier shards) or, without one, from this shard's first row; the
+// running sums after its last row go to carry_out.  *bad_row = the first
+// local row holding a non-finite value (-1 if none; nothing else is done).
+int taco_shard_colsum(taco_index* idx, const double* carry_in_h, double* carry_out_h, int64_t* bad_row) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "no data uploaded");
+  const int64_t n = idx->n;
+  const int d = idx->d;
+  cudaStream_t st = idx->stream;
+  if (idx->mean_ready) TACO_CHECK_CUDA(cudaStreamSynchronize(idx->aux));
+  DevBuf bad, state;
+  TACO_TRY(bad.ensure(8));
+  TACO_TRY(state.ensure(8 * (size_t)d));
+  unsigned long long init = ~0ull, b = 0;
+  TACO_CHECK_CUDA(cudaMemcpyAsync(bad.p, &init, 8, cudaMemcpyHostToDevice, st));
+  k_nonfinite<<<1184, 256, 0, st>>>(idx->X.as<float>(), n * d, d, bad.as<unsigned long long>());
+  count_launch();
+  TACO_CHECK_CUDA(cudaMemcpyAsync(&b, bad.p, 8, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  *bad_row = b == ~0ull ? -1 : (int64_t)b;
+  if (b != ~0ull) return TACO_OK;
+  if (carry_in_h) TACO_CHECK_CUDA(cudaMemcpyAsync(state.p, carry_in_h, 8 * (size_t)d, cudaMemcpyHostToDevice, st));
+  TACO_TRY(launch_colmean(st, idx->X.as<float>(), 0, n, -1, d, state.as<double>(), nullptr, carry_in_h ? 1 : 0));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(carry_out_h, state.p, 8 * (size_t)d, cudaMemcpyDeviceToHost, st));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  return TACO_OK;
+}
+
+// Centred Gram chain of this shard's rows (spectral.py:108-109): gram_out =
+// carry_in (or 0) + the kGramBlock-row block partials of its rows in order,
+// the same sequence taco_fit_covariance runs over all rows, so shards that
+// start on multiples of block_rows reproduce the single-GPU Gram exactly.
+int taco_shard_gram(taco_index* idx, const double* mean_h, int64_t block_rows, const double* carry_in_h,
+                    double* carry_out_h) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_X) TACO_FAIL(TACO_ERR_STATE, "no data uploaded");
+  if (block_rows <= 0) block_rows = kGramBlock;
+  const int d = idx->d;
+  const int64_t dd = (int64_t)d * d;
+  cudaStream_t st = idx->stream;
+  DevBuf mean, G;
+  TACO_TRY(mean.ensure(8 * (size_t)d));
+  TACO_TRY(G.ensure(8 * (size_t)dd));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(mean.p, mean_h, 8 * (size_t)d, cudaMemcpyHostToDevice, st));
+  if (carry_in_h) TACO_CHECK_CUDA(cudaMemcpyAsync(G.p, carry_in_h, 8 * (size_t)dd, cudaMemcpyHostToDevice, st));
+  else TACO_CHECK_CUDA(cudaMemsetAsync(G.p, 0, 8 * (size_t)dd, st));
+  TACO_TRY(gram_chain(idx->X.as<float>(), idx->n, d, mean.as<double>(), block_rows, G.as<double>(), st));
+  TACO_CHECK_CUDA(cudaMemcpy(carry_out_h, G.p, 8 * (size_t)dd, cudaMemcpyDeviceToHost));
+  return TACO_OK;
+}
+
+int taco_gram_block_rows(void) { return (int)kGramBlock; }
 
 int taco_covariance(int device, const float* X_h, int64_t n, int32_t d, double* mean_h, double* gram_h,
                     int64_t* bad_row) {

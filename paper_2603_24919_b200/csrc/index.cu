@@ -542,6 +542,48 @@ int taco_index_set_transformed(taco_index* idx, const float* T_h) {
   return TACO_OK;
 }
 
+// Device-resident exchange of the transformed matrix (point-sharded build):
+// dimension-major [D][n] f32, the index's own layout.
+int taco_index_set_transformed_device(taco_index* idx, const float* T_d) {
+  TACO_TRY(index_check(idx));
+  const size_t bytes = sizeof(float) * (size_t)idx->n * idx->D;
+  TACO_TRY(idx->T.ensure(bytes));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(idx->T.p, T_d, bytes, cudaMemcpyDeviceToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->has_T = true;
+  return TACO_OK;
+}
+
+int taco_get_transformed_device(taco_index* idx, float* T_d) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_T) TACO_FAIL(TACO_ERR_STATE, "transformed matrix not available");
+  TACO_CHECK_CUDA(cudaMemcpyAsync(T_d, idx->T.p, sizeof(float) * (size_t)idx->n * idx->D,
+                                  cudaMemcpyDeviceToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  return TACO_OK;
+}
+
+// labels [2 N_s][n] i32, half 2j = codebook 1 of subspace j, 2j+1 = codebook 2
+int taco_get_labels_device(taco_index* idx, int32_t* lab_d) {
+  TACO_TRY(index_check(idx));
+  if (!idx->has_labels) TACO_FAIL(TACO_ERR_STATE, "labels not available");
+  for (auto s : idx->half_streams) TACO_CHECK_CUDA(cudaStreamSynchronize(s));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(lab_d, idx->labels.p, sizeof(int32_t) * (size_t)idx->n * 2 * idx->n_sub,
+                                  cudaMemcpyDeviceToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  return TACO_OK;
+}
+
+int taco_index_set_labels_device(taco_index* idx, const int32_t* lab_d) {
+  TACO_TRY(index_check(idx));
+  const size_t bytes = sizeof(int32_t) * (size_t)idx->n * 2 * idx->n_sub;
+  TACO_TRY(idx->labels.ensure(bytes));
+  TACO_CHECK_CUDA(cudaMemcpyAsync(idx->labels.p, lab_d, bytes, cudaMemcpyDeviceToDevice, idx->stream));
+  TACO_CHECK_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->has_labels = true;
+  return TACO_OK;
+}
+
 int taco_get_transformed(taco_index* idx, float* T_h) {
   TACO_TRY(index_check(idx));
   if (!idx->has_T) TACO_FAIL(TACO_ERR_STATE, "transformed matrix not available");

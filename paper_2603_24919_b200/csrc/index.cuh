@@ -97,5 +97,5 @@ int index_check(taco_index* idx);
 int launch_transform(cudaStream_t st, const float* P, int64_t np_, int d, int D,
                      const float* mean, const float* M, float* out, bool dim_major);
 int launch_colmean(cudaStream_t st, const float* X, int64_t r0, int64_t r1, int64_t n, int d, double* state,
-                   double* mean);
+                   double* mean, int chained = 0);
 }  // namespace taco

@@ -45,8 +45,54 @@ class _DeviceBytes:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
+def _staged(t):
+    """gloo cannot move CUDA tensors: stage them through host memory."""
+    import torch.distributed as dist
+
+    return t.is_cuda and dist.get_backend() == "gloo"
+
+
+def _all_reduce(t, op, group=None):
+    import torch.distributed as dist
+
+    if _staged(t):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def _all_gather_into(out, inp, group=None):
+    import torch.distributed as dist
+
+    if _staged(out):
+        h = out.cpu()
+        dist.all_gather_into_tensor(h, inp.cpu().clone(), group=group)
+        out.copy_(h)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
 class CudaShardBackend:
     """One rank's shard on its GPU."""
+
+    @classmethod
+    def from_shard(cls, shard):
+        """Wrap the device shard a collective build produced
+        (distributed_build.sharded_build): its CSR, X, codebooks, transform and
+        global cell sizes are already resident."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.device = shard.backend.device
+        self.k_sub = shard.params.n_subspaces
+        self.dev = shard.backend.dev
+        self.tile = int(nat.lib().taco_query_tile_size(self.dev.h))
+        self.k2 = shard.params.clusters
+        self.pop_cap = min(self.k2, 256)
+        return self
 
     def __init__(self, index: TacoIndex, X_shard: np.ndarray, id_base: int, n_global: int, device: int):
         import torch
@@ -187,9 +233,9 @@ def _split_count(backend, Qt, alpha: float, group=None):
     rows = per * world
     lo, hi = min(m, rank * per), min(m, rank * per + per)
     need = backend.front_async(Qt, alpha, lo, hi, rows)
-    dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
+    _all_reduce(need, dist.ReduceOp.MAX, group)
     for buf in backend.pop_views(rows):
-        dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
+        _all_gather_into(buf, buf[rank * per:(rank + 1) * per], group)
     return backend.count_popped(m), need
 
 
@@ -201,7 +247,7 @@ def common_tile_size(backend, group=None, device=None) -> int:
     import torch.distributed as dist
 
     t = torch.tensor([int(backend.tile_size())], dtype=torch.int64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    _all_reduce(t, dist.ReduceOp.MIN, group)
     return int(t.item())
 
 
@@ -233,12 +279,12 @@ def sharded_query(backend, Q, alpha: float, beta: float, k: int, group=None):
                 needs.append(need)
             else:
                 hist = backend.count(Qt, alpha)
-            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+            _all_reduce(hist, dist.ReduceOp.SUM, group)
             d2, ids, num, lvl = backend.finish(m, hist, beta, k)
             d2_all = torch.empty((world * m, k), dtype=d2.dtype, device=d2.device)
             ids_all = torch.empty((world * m, k), dtype=ids.dtype, device=ids.device)
-            dist.all_gather_into_tensor(d2_all, d2.contiguous(), group=group)
-            dist.all_gather_into_tensor(ids_all, ids.contiguous(), group=group)
+            _all_gather_into(d2_all, d2.contiguous(), group)
+            _all_gather_into(ids_all, ids.contiguous(), group)
             oi, od = backend.merge(d2_all.view(world, m, k), ids_all.view(world, m, k), k)
             outs.append((oi, od, num, lvl))
         if not needs:

@@ -125,3 +125,84 @@ class OracleShardBackend:
                 out_i[q, t] = iv
                 out_d[q, t] = np.float32(np.sqrt(dv))
         return torch.tensor(out_i), torch.tensor(out_d)
+
+
+class OracleShardBuilder:
+    """CPU stand-in for distributed_build.CudaShardBuilder (TEST
+    INFRASTRUCTURE): each build stage of one rank restated with numpy /
+    the oracle, so the collective orchestration of
+    paper_2603_24919_b200.distributed_build runs with gloo on CPU.  The
+    covariance follows the same chains as the device (sequential column sums;
+    Gram partials over fixed row blocks added in order)."""
+
+    comm_device = "cpu"
+
+    def __init__(self, X_local, id_base, n_global, params, block=256):
+        self.X = np.ascontiguousarray(X_local, np.float32)
+        self.n_local, self.d = self.X.shape
+        self.id_base, self.n_global, self.params, self.block = id_base, n_global, params, block
+
+    def gram_block_rows(self):
+        return self.block
+
+    def colsum(self, carry):
+        X64 = self.X.astype(np.float64)
+        bad = np.flatnonzero(~np.isfinite(self.X).all(axis=1))
+        acc = X64[0].copy() if carry is None else np.array(carry, np.float64)
+        for row in (X64[1:] if carry is None else X64):
+            acc += row
+        return acc, int(bad[0]) if bad.size else -1
+
+    def gram(self, mean, block, carry):
+        acc = np.zeros((self.d, self.d)) if carry is None else np.array(carry, np.float64)
+        for b0 in range(0, self.n_local, block):
+            xc = self.X[b0:b0 + block].astype(np.float64) - mean
+            acc = acc + xc.T @ xc
+        return acc
+
+    def transform(self, model):
+        T = O.transform(np.asarray(model.mean, np.float32), list(model.blocks), self.X)
+        return torch.from_numpy(np.ascontiguousarray(T.T))
+
+    def kmeans(self, subspaces, T_cols, n_global, params):
+        p = params
+        s, sp = p.subspace_dim, (p.subspace_dim + 1) // 2
+        Tc = T_cols.numpy()
+        labs, cbs, hist = [], [], []
+        for jj, j in enumerate(subspaces):
+            blk = np.ascontiguousarray(Tc[jj * s:(jj + 1) * s].T)
+            sj = O.derive_seed(p.seed, j)
+            r1 = O.kmeans(blk[:, :sp], p.codebook_size, p.kmeans_iters, O.derive_seed(sj, 0))
+            r2 = O.kmeans(blk[:, sp:], p.codebook_size, p.kmeans_iters, O.derive_seed(sj, 1))
+            labs += [r1.labels, r2.labels]
+            cbs.append((r1.centroids, r2.centroids))
+            hist.append((tuple(r1.history), tuple(r2.history)))
+        return {"labels": torch.from_numpy(np.array(labs, np.int32)), "codebooks": cbs, "histories": hist}
+
+    def finish(self, codebooks, labels_loc):
+        p = self.params
+        L = labels_loc.numpy()
+        kp = p.codebook_size
+        self.cells = [O.cells_from_labels(L[2 * j], L[2 * j + 1]) for j in range(p.n_subspaces)]
+        sizes = np.zeros((p.n_subspaces, p.clusters), np.int64)
+        for j, cells in enumerate(self.cells):
+            for (a, b), ids in cells.items():
+                sizes[j, a * kp + b] = ids.size
+        return sizes
+
+    def set_global_sizes(self, sizes):
+        self.global_sizes = np.asarray(sizes)
+
+    def local_cells(self):
+        kp = self.params.codebook_size
+        out = []
+        for cells in self.cells:
+            off = np.zeros(kp * kp + 1, np.int64)
+            parts = []
+            for c in range(kp * kp):
+                ids = cells.get((c // kp, c % kp))
+                off[c + 1] = off[c] + (0 if ids is None else ids.size)
+                if ids is not None:
+                    parts.append(ids)
+            out.append((off, np.concatenate(parts) if parts else np.empty(0, np.uint32)))
+        return out
