@@ -314,7 +314,10 @@ def run_sharded(args):
 
     import paper_2603_24919_b200 as T
     from paper_2603_24919_b200 import _native as nat
-    from paper_2603_24919_b200.distributed import CudaShardBackend, shard_range, sharded_query
+    from paper_2603_24919_b200.distributed import CudaShardBackend, sharded_query
+    from paper_2603_24919_b200.distributed_build import (Comm, CudaShardBuilder, aligned_shard_range,
+                                                         sharded_build)
+    from paper_2603_24919_b200.workloads import CONFIGS, make_config, make_shard
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -324,15 +327,29 @@ def run_sharded(args):
     torch.cuda.set_device(local)
     os.environ["TACO_DEVICE"] = str(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    X, Q, meta = workload(args)
+    comm = Comm()
+    # each rank generates and uploads ONLY its own rows, then the ranks build
+    # the index collectively (distributed_build: column-sum / Gram chains,
+    # k-means by subspace owners over an all-to-all, cell-size all-reduce)
+    n = args.n or CONFIGS[args.config]["n"]
+    block = int(nat.lib().taco_gram_block_rows())
+    lo, hi = aligned_shard_range(n, rank, world, block)
+    t = time.perf_counter()
+    X_loc, Q, meta = make_shard(args.config, lo, hi, n=n, nq=args.nq)
+    gen_s = time.perf_counter() - t
     params = T.IndexParams(meta["n_sub"], meta["s"], meta["clusters"], meta["kmeans_iters"], meta["seed"])
+    torch.cuda.synchronize()
+    dist.barrier()
     t0 = time.perf_counter()
-    index = T.build_index(X, params)            # replicated, deterministic build
-    build_wall = time.perf_counter() - t0
-    n, nq, d, k = X.shape[0], Q.shape[0], meta["d"], meta["k"]
+    builder = CudaShardBuilder(X_loc, lo, n, params, device=local)
+    shard = sharded_build(builder, params, n, comm)
+    torch.cuda.synchronize()
+    bw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(bw, op=dist.ReduceOp.MAX)
+    build_wall = float(bw.item())
+    nq, d, k = Q.shape[0], meta["d"], meta["k"]
     a, b = meta["alpha"], meta["beta"]
-    lo, hi = shard_range(n, rank, world)
-    backend = CudaShardBackend(index, X[lo:hi], lo, n, local)
+    backend = CudaShardBackend.from_shard(shard)
     Qd = torch.from_numpy(Q).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
@@ -404,13 +421,20 @@ def run_sharded(args):
                     "launches": dom_n, "share_of_step": dom_ms / total_prof, "rank": rank,
                     "kernels_ms": {kname: round(v[0], 4) for kname, v in prof.items()}}
 
-    # parity of the sharded result with the single-GPU batch path, and recall@k
-    parity = rec = None
-    if rank == 0:
+    # parity with the single-GPU build + batch path on the whole matrix
+    # (rank 0: index bytes and answers), and recall@k
+    parity = rec = same_index = None
+    from paper_2603_24919_b200.distributed_build import gather_serialized
+    blob = gather_serialized(shard, comm) if not args.no_check else None
+    if rank == 0 and not args.no_check:
+        X, _, _ = make_config(args.config, n=n, nq=args.nq)
+        index = T.build_index(X, params)
+        same_index = T.serialize_index(index) == blob
         ids1, _, _, _ = T.knn_query_batch(index, X, Q, T.QueryParams(a, b, k))
         parity = bool(np.array_equal(ids1, ids_sh))
         gt = T.compute_ground_truth(X, Q, k, index=index)
         rec = float(np.mean([len(set(ids_sh[i]) & set(gt.ids[i])) / k for i in range(nq)]))
+        del index, X
     dist.barrier()
     if rank == 0:
         line = {"metric": METRIC, "value": nq / (ms / 1000.0), "unit": "queries/s", "n_gpus": world,
@@ -422,8 +446,12 @@ def run_sharded(args):
                                           "all_gather of popped cells, all_reduce of per-query histograms, "
                                           "all_gather of top-k",
                            "l2": "256 MiB buffer written between timed steps",
-                           "build_seconds_replicated": build_wall,
+                           "build": "point-sharded collective build (distributed_build.py), "
+                                    "each rank generates and holds only its rows",
+                           "shard_rows": [hi - lo], "gen_seconds_rank0": gen_s,
+                           "sharded_index_bytes_identical_to_single_gpu_build": same_index,
                            "matches_single_gpu_batch": parity, "recall@10": rec},
+                "build_seconds": build_wall,
                 "e2e": {"value": nq / (e2e_ms / 1000.0), "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
                         "d2h_bytes_per_step": nq * k * 8},
                 "gpu_launches": int(launches),
@@ -606,6 +634,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="N>1: skip the single-GPU parity check on rank 0")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=256)
     args = ap.parse_args()

@@ -66,6 +66,48 @@ def base_chunk(cfg: int, b: int, size: int, d: int | None = None):
     return _draw(cfg, np.random.default_rng([1000 + cfg, 0, b]), size, A, mu)
 
 
+def make_shard(cfg: int, lo: int, hi: int, n: int | None = None, nq: int | None = None,
+               d: int | None = None):
+    """(rows [lo, hi) of the base matrix, all queries, meta) -- what one rank
+    of a point-sharded run generates; equal to make_config's X[lo:hi] and Q."""
+    c = dict(CONFIGS[cfg])
+    n = c["n"] if n is None else n
+    nq = c["nq"] if nq is None else nq
+    d = c["d"] if d is None else d
+    A, mu = _mixture(cfg, d)
+    X = np.empty((hi - lo, d), np.float32)
+    for b in range(lo // CHUNK, math.ceil(hi / CHUNK)):
+        c0 = b * CHUNK
+        clen = min(CHUNK, n - c0)
+        a0, a1 = max(lo, c0), min(hi, c0 + clen)
+        X[a0 - lo:a1 - lo] = _draw(cfg, np.random.default_rng([1000 + cfg, 0, b]), clen, A, mu)[a0 - c0:a1 - c0]
+    qr = np.random.default_rng([1000 + cfg, 1])
+    if cfg in (1, 5):   # queries are base rows + noise: regenerate the chunks holding them
+        rows = qr.choice(n, size=nq, replace=False)
+        base = np.empty((nq, d), np.float32)
+        for b in np.unique(rows // CHUNK):
+            c0 = int(b) * CHUNK
+            clen = min(CHUNK, n - c0)
+            chunk = _draw(cfg, np.random.default_rng([1000 + cfg, 0, int(b)]), clen, A, mu)
+            sel = rows // CHUNK == b
+            base[sel] = chunk[rows[sel] - c0]
+        Q = (base.astype(np.float64) + 0.05 * qr.standard_normal((nq, d))).astype(np.float32)
+    else:
+        Q = _draw(cfg, qr, nq, A, mu)
+    return X, Q, _meta(cfg, n, nq, d)
+
+
+def _meta(cfg, n, nq, d):
+    c = CONFIGS[cfg]
+    s = c["s"] if d == c["d"] else max(2, d // c["n_sub"])
+    return dict(cfg=cfg, n=n, d=d, nq=nq, n_sub=c["n_sub"], s=s,
+                clusters=c["kprime"] ** 2, kprime=c["kprime"], kmeans_iters=20, seed=0,
+                alpha=c["alpha"], beta=c["beta"], k=c["k"], mixture=c["comps"],
+                power=c["power"], lam1=c["lam1"],
+                generator="SURVEY.md 8(d): rotated anisotropic Gaussian mixture, "
+                          "rng([1000+cfg,0,chunk]) base / rng([1000+cfg,1]) queries")
+
+
 def make_config(cfg: int, n: int | None = None, nq: int | None = None,
                 d: int | None = None):
     """Return (base f32[n,d], queries f32[nq,d], meta).
@@ -87,11 +129,5 @@ def make_config(cfg: int, n: int | None = None, nq: int | None = None,
         Q = (X[rows].astype(np.float64) + 0.05 * qr.standard_normal((nq, d))).astype(np.float32)
     else:
         Q = _draw(cfg, qr, nq, A, mu)
-    s = c["s"] if d == c["d"] else max(2, d // c["n_sub"])
-    meta = dict(cfg=cfg, n=n, d=d, nq=nq, n_sub=c["n_sub"], s=s,
-                clusters=c["kprime"] ** 2, kprime=c["kprime"], kmeans_iters=20, seed=0,
-                alpha=c["alpha"], beta=c["beta"], k=c["k"], mixture=c["comps"],
-                power=c["power"], lam1=c["lam1"],
-                generator="SURVEY.md 8(d): rotated anisotropic Gaussian mixture, "
-                          "rng([1000+cfg,0,chunk]) base / rng([1000+cfg,1]) queries")
+    meta = _meta(cfg, n, nq, d)
     return X, Q, meta
