@@ -566,71 +566,91 @@ __device__ void compact_table(const uint8_t* tab, int valid, uint32_t L, int64_t
 
 // Unordered single-pass compaction (the batch paths: a segment's candidates
 // are re-ranked as a set, ties are broken by id, so their order is free).
-// Thread t scans vectors t, t + NT, ... (conflict-free 16-byte reads); each
-// warp step scans its lanes' hit counts and reserves one run of slots with a
-// shared-memory atomic, so stores stay warp-contiguous.  *fill ends = count.
+// A warp step covers CP_VPL x 32 consecutive 16-byte vectors: lane l tests
+// vectors l, l + 32, ... (conflict-free 16-byte reads, CP_VPL independent
+// load/compare chains in flight), one warp prefix of the lanes' hit counts
+// and one shared-memory reservation place them, then each lane writes its
+// own hits.  *fill ends = count.
+constexpr int CP_VPL = 4;
+template <bool NIB>
+__device__ __forceinline__ uint32_t vec_hits(const uint4 v, uint32_t D, int lim) {
+  constexpr int LW = NIB ? 4 : 8;
+  constexpr int LPW = 32 / LW;
+  constexpr int IDS = 4 * LPW;
+  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
+  uint32_t g[4];
+  if (D == 0u) {
+    g[0] = g[1] = g[2] = g[3] = H;
+  } else {
+    g[0] = lanes_ge<NIB>(v.x, D); g[1] = lanes_ge<NIB>(v.y, D);
+    g[2] = lanes_ge<NIB>(v.z, D); g[3] = lanes_ge<NIB>(v.w, D);
+  }
+  if (lim < IDS) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int al = min(max(lim - u * LPW, 0), LPW);
+      g[u] &= al >= LPW ? 0xFFFFFFFFu : (1u << (al * LW)) - 1u;
+    }
+  }
+  // word u's hits sit at lane tops (bit LW*i + LW-1); shifted by u they are disjoint
+  return g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
+}
+
+// warp-inclusive prefix of c; lane 31 reserves the step's slots in *fill;
+// returns the lane's first slot
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t c, int* fill) {
+  const int lane = threadIdx.x & 31;
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int base = 0;
+  if (lane == 31) base = atomicAdd(fill, (int)x);
+  return (uint32_t)__shfl_sync(0xffffffffu, base, 31) + x - c;
+}
+
 template <int NT, bool NIB>
 __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                                   int* fill) {
   constexpr int LW = NIB ? 4 : 8;
   constexpr int LPW = 32 / LW;
   constexpr int IDS = 4 * LPW;
-  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
   const uint32_t D = L == 0 ? 0u : (NIB ? (16u - L) * 0x11111111u : (256u - L) * 0x01010101u);
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
   const int nvec = (valid + IDS - 1) / IDS;
   const int lane = threadIdx.x & 31;
-  for (int v0 = threadIdx.x - lane; v0 < nvec; v0 += NT) {
-    const int vi = v0 + lane;
-    uint32_t g[4] = {0u, 0u, 0u, 0u};
-    if (vi < nvec) {
-      const uint4 v = t4[vi];
-      if (L == 0) {
-        g[0] = g[1] = g[2] = g[3] = H;
-      } else {
-        g[0] = lanes_ge<NIB>(v.x, D); g[1] = lanes_ge<NIB>(v.y, D);
-        g[2] = lanes_ge<NIB>(v.z, D); g[3] = lanes_ge<NIB>(v.w, D);
-      }
-      const int lim = valid - vi * IDS;
-      if (lim < IDS) {
+  for (int v0 = (threadIdx.x - lane) * CP_VPL; v0 < nvec; v0 += NT * CP_VPL) {
+    uint32_t m[CP_VPL];
+    uint32_t c = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int al = min(max(lim - u * LPW, 0), LPW);
-          g[u] &= al >= LPW ? 0xFFFFFFFFu : (1u << (al * LW)) - 1u;
-        }
-      }
+    for (int e = 0; e < CP_VPL; ++e) {
+      const int vi = v0 + e * 32 + lane;
+      m[e] = vi < nvec ? vec_hits<NIB>(t4[vi], D, valid - vi * IDS) : 0u;
+      c += __popc(m[e]);
     }
-    // word u's hits sit at lane tops (bit LW*i + LW-1); shifted by u they are disjoint
-    uint32_t m = g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
-    // one reservation per warp step (total by a warp reduction), then the
-    // hits leave in rounds of one per lane: a ballot ranks the lanes that
-    // still hold one (most steps need 1-2 rounds; no per-lane prefix scan)
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(m));
-    if (tot == 0u) continue;
-    int base = 0;
-    if (lane == 0) base = atomicAdd(fill, (int)tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const uint32_t idb = (uint32_t)(id0 + (int64_t)vi * IDS);
-    const uint32_t lt = (1u << lane) - 1u;
-    while (true) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
-      if (bal == 0u) break;
-      if (m) {
-        const int b = 31 - __clz(m);                 // highest hit first (order is free)
-        m ^= 1u << b;
-        const int u = LW - 1 - (b & (LW - 1));        // word
-        dst[base + __popc(bal & lt)] = idb + (uint32_t)(u * LPW + b / LW);   // lane b / LW of word u
+    if (__ballot_sync(0xffffffffu, c != 0u) == 0u) continue;
+    uint32_t pos = warp_reserve(c, fill);
+#pragma unroll
+    for (int e = 0; e < CP_VPL; ++e) {
+      const uint32_t idb = (uint32_t)(id0 + (int64_t)(v0 + e * 32 + lane) * IDS);
+      uint32_t mm = m[e];
+      while (mm) {
+        const int b = 31 - __clz(mm);                  // highest hit first (order is free)
+        mm ^= 1u << b;
+        const int u = LW - 1 - (b & (LW - 1));          // word
+        dst[pos++] = idb + (uint32_t)(u * LPW + b / LW);   // lane b / LW of word u
       }
-      base += __popc(bal);
     }
   }
 }
 
 // Global-mode spill: the ids of a chunk table with score >= 2 as packed
-// records (chunk position << 8 | score), unordered, warp-contiguous stores.
-// The emit sweep filters them at the query's level L >= 2 instead of
-// re-reading the whole table (a query's candidates are a small fraction of
-// the ids it touched).  *fill ends = record count.
+// records (chunk position << 8 | score), unordered, CP_VPL vectors per lane
+// per warp step as above.  The emit sweep filters them at the query's level
+// L >= 2 instead of re-reading the whole table (a query's candidates are a
+// small fraction of the ids it touched).  *fill ends = record count.
 template <int NT, bool NIB>
 __device__ void compact_records(const uint8_t* tab, int valid, uint32_t* dst, int* fill) {
   constexpr int LW = NIB ? 4 : 8;
@@ -641,35 +661,31 @@ __device__ void compact_records(const uint8_t* tab, int valid, uint32_t* dst, in
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
   const int nvec = (valid + IDS - 1) / IDS;
   const int lane = threadIdx.x & 31;
-  for (int v0 = threadIdx.x - lane; v0 < nvec; v0 += NT) {
-    const int vi = v0 + lane;
-    uint32_t w[4] = {0u, 0u, 0u, 0u}, g[4] = {0u, 0u, 0u, 0u};
-    if (vi < nvec) {
-      const uint4 v = t4[vi];
-      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  for (int v0 = (threadIdx.x - lane) * CP_VPL; v0 < nvec; v0 += NT * CP_VPL) {
+    uint4 w[CP_VPL];
+    uint32_t m[CP_VPL];
+    uint32_t c = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) g[u] = lanes_ge<NIB>(w[u], D);   // tables are zero past `valid`
+    for (int e = 0; e < CP_VPL; ++e) {
+      const int vi = v0 + e * 32 + lane;
+      w[e] = vi < nvec ? t4[vi] : make_uint4(0, 0, 0, 0);   // tables are zero past `valid`
+      m[e] = vec_hits<NIB>(w[e], D, IDS);
+      c += __popc(m[e]);
     }
-    uint32_t m = g[0] | (g[1] >> 1) | (g[2] >> 2) | (g[3] >> 3);
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(m));
-    if (tot == 0u) continue;
-    int base = 0;
-    if (lane == 0) base = atomicAdd(fill, (int)tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const uint32_t pos0 = (uint32_t)vi * IDS;
-    const uint32_t lt = (1u << lane) - 1u;
-    while (true) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
-      if (bal == 0u) break;
-      if (m) {
-        const int b = 31 - __clz(m);
-        m ^= 1u << b;
+    if (__ballot_sync(0xffffffffu, c != 0u) == 0u) continue;
+    uint32_t pos = warp_reserve(c, fill);
+#pragma unroll
+    for (int e = 0; e < CP_VPL; ++e) {
+      const uint32_t pos0 = (uint32_t)(v0 + e * 32 + lane) * IDS;
+      uint32_t mm = m[e];
+      while (mm) {
+        const int b = 31 - __clz(mm);
+        mm ^= 1u << b;
         const int u = LW - 1 - (b & (LW - 1));
         const int ln = b / LW;
-        const uint32_t sc = (w[u] >> (ln * LW)) & MASK;
-        dst[base + __popc(bal & lt)] = ((pos0 + (uint32_t)(u * LPW + ln)) << 8) | sc;
+        const uint32_t wu = u == 0 ? w[e].x : u == 1 ? w[e].y : u == 2 ? w[e].z : w[e].w;
+        dst[pos++] = ((pos0 + (uint32_t)(u * LPW + ln)) << 8) | ((wu >> (ln * LW)) & MASK);
       }
-      base += __popc(bal);
     }
   }
 }
@@ -690,6 +706,8 @@ __device__ __forceinline__ int alg5(Get get, int n_sub, double budget, int64_t& 
 // ------------------------------------------------- cluster-fused count/select
 // Candidates of a query live in per-CTA segments (segment q*S + rank); the
 // final top-k breaks distance ties by id, so segment order is irrelevant.
+__device__ int g_count_dbg = 0;   // timing experiments only (TACO_COUNT_DBG): 1 skip counting, 2 skip compaction, 4 skip the cluster exchange
+
 template <bool NIB>
 __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
@@ -711,16 +729,26 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
   uint4* t4 = reinterpret_cast<uint4*>(table);
   const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  const int dbg = g_count_dbg;
   for (int i = tid; i < tbytes / 16; i += CT_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  if (!(dbg & 1))
+    count_chunk<NIB>(pops, npop, cap, ids, offs, (size_t)nchunks * K2 + 1, n_sub, K2, n, c, q, base, table, S);
+  else {
+    for (int i = tid; i < 257; i += CT_THREADS) S.ge[i] = 0;
+    __syncthreads();
+  }
   chunk_levels(table, valid, n_sub, S);
-  cluster.sync();   // every CTA's level histogram is final
-  // cluster-wide histogram: one level per thread, the csz remote reads in parallel
-  for (int l = tid; l <= n_sub; l += CT_THREADS) {
-    int h = 0;
-    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
-    S.ge[l] = h;
+  if (!(dbg & 4)) {
+    cluster.sync();   // every CTA's level histogram is final
+    // cluster-wide histogram: one level per thread, the csz remote reads in parallel
+    for (int l = tid; l <= n_sub; l += CT_THREADS) {
+      int h = 0;
+      for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
+      S.ge[l] = h;
+    }
+  } else {
+    for (int l = tid; l <= n_sub; l += CT_THREADS) S.ge[l] = S.lh[l] * csz;
   }
   // done reading remote shared memory: arrive now, wait only before exiting
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -730,6 +758,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
     const int L = alg5([&](int l) { return (int64_t)S.ge[l]; }, n_sub, budget, cands);
     int64_t mine = 0;
     for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
+    if (dbg & 3) mine = 0;   // timing experiment: no candidates
     const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
     if (b + mine > cand_cap) flags[1] = 1;
     s_L = L;
@@ -744,7 +773,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
     }
   }
   __syncthreads();
-  if (s_base + s_cnt <= cand_cap)
+  if (s_base + s_cnt <= cand_cap && !(dbg & 3))
     compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)s_L, base, cand + s_base, &S.batches);
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // nobody reads my histogram any more
 }
@@ -1811,6 +1840,14 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ProfScope ps(K_COUNT, st);
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("TACO_COUNT_DBG");
+      dbg = e ? atoi(e) : 0;
+      if (dbg) TACO_CHECK_CUDA(cudaMemcpyToSymbol(g_count_dbg, &dbg, sizeof(int)));
+    }
+  }
   TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, nib_tables(idx) ? k_count_cluster<true> : k_count_cluster<false>,
                                      (const uint16_t*)t.pops.as<uint16_t>(),
                                      (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
