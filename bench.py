@@ -186,29 +186,43 @@ def chunking(n, n_sub=8):
     return 65536, -(-n // 65536), False
 
 
-def kernel_bytes(name, stats, meta):
+def kernel_bytes(name, stats, meta, nq=None):
+    """Algorithmic bytes of one kernel over the batch.  k_count uses SURVEY
+    8(d)'s counting terms, 4*sum_j R_j + n per query (the popped cells' ids
+    plus one uint8 score-table pass); kernel_bytes_io gives the bytes the
+    kernel actually has to move with on-chip score tables."""
     d = meta["d"]
-    C, R, P = stats["sum_candidates"], stats["sum_retrieved"], stats["sum_pops"]
-    nch = stats.get("nchunks", 1)
+    C, R = stats["sum_candidates"], stats["sum_retrieved"]
     rb = ROW_BYTES.get(stats.get("row_format", 0), 4)
+    nq = stats.get("nq", 0) if nq is None else nq
     return {
-        # candidate rows gathered (stored format) + candidate ids + tile descriptors + partial top-k
+        # candidate rows gathered (stored format) + candidate ids
         "k_rerank": (rb * d + 4) * C,
-        # ids of popped cells + CSR bounds per (cell, chunk) + pop lists + candidate ids
-        # written (+ the spilled score >= 2 records in global mode)
-        "k_count": 4 * R + (8 * nch + 2) * P + 4 * C + stats["score_bytes"],
+        "k_count": 4 * R + meta["n"] * nq,
         # global mode: records read back + candidate ids written
         "k_compact": stats["score_bytes"] + 4 * C,
     }.get(name)
 
 
-def ncu_traffic(name, nq, launches):
+def kernel_bytes_io(name, stats, meta):
+    """k_count's own traffic with the score table in shared memory: ids of the
+    popped cells + CSR bounds per (cell, chunk) + pop lists + candidate ids
+    written (+ the spilled score >= 2 records in global mode)."""
+    if name != "k_count":
+        return None
+    C, R, P = stats["sum_candidates"], stats["sum_retrieved"], stats["sum_pops"]
+    nch = stats.get("nchunks", 1)
+    return 4 * R + (8 * nch + 2) * P + 4 * C + stats["score_bytes"]
+
+
+def ncu_traffic(name, nq, launches, cfg):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed
-    ncu --set full capture (profiles/ncu_traffic.json, per query) scaled to this batch."""
+    ncu --set full capture of THIS config (profiles/ncu_traffic.json, keyed by
+    config, per query) scaled to this batch; None when that config has no capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            ent = json.load(fh).get(name)
+            ent = json.load(fh)[f"cfg{cfg}"][name]
         return ent["dram_bytes_per_query"] * nq / max(launches, 1)
     except Exception:
         return None
@@ -412,6 +426,7 @@ def run_sharded(args):
         dom_ms, dom_n = prof[dom]
         stats["nchunks"] = -(-(hi - lo) // 65536)
         stats["row_format"] = 0
+        stats["nq"] = nq
         kb = kernel_bytes(dom, stats, dict(meta, n=hi - lo))
         if kb is not None and dom_ms > 0:
             ach = kb / (dom_ms / 1000.0) / 1e9
@@ -541,6 +556,7 @@ def run_ours(args):
     prof, stats = nat.profile_read(reset=True)
     stats["nchunks"] = chunking(meta["n"], meta["n_sub"])[1]
     stats["row_format"] = int(nat.lib().taco_index_row_format(dev.h))
+    stats["nq"] = nq
     nat.profile_enable(False)
     total_prof = sum(v[0] for v in prof.values())
     dom = max(prof, key=lambda kname: prof[kname][0])
@@ -550,7 +566,8 @@ def run_ours(args):
     roof = None
     if kb is not None and dom_ms > 0:
         ach = kb / (dom_ms / 1000.0) / 1e9
-        tr = ncu_traffic(dom, nq, dom_n)
+        tr = ncu_traffic(dom, nq, dom_n, meta["cfg"])
+        kio = kernel_bytes_io(dom, stats, meta)
         notes = {
             "k_count": ("algorithmic bytes = CSR ids of the popped cells + CSR bounds + pop lists + "
                         "candidate ids; the 4 B/point-per-subspace CSR (32 MB here) stays L2-resident, "
@@ -564,7 +581,14 @@ def run_ours(args):
                 "frac": ach / peak, "traffic": tr, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": kb / max(dom_n, 1),
                 "avg_launch_ms": dom_ms / max(dom_n, 1), "launches": dom_n,
-                "share_of_step": dom_ms / total_prof}
+                "share_of_step": dom_ms / total_prof,
+                "bytes_formula": ("SURVEY 8(d): 4*sum_j R_j + n per query" if dom == "k_count"
+                                  else "SURVEY 8(d): (b*d + 4)*|C|, b = bytes per stored value")}
+        if kio is not None:   # secondary: the bytes the kernel moves with on-chip tables
+            roof["secondary"] = {"bytes_formula": "4*sum R_j + (8*nchunks+2)*pops + 4*|C| (+ spilled records)",
+                                 "algorithmic_bytes_per_launch": kio / max(dom_n, 1),
+                                 "achieved": kio / (dom_ms / 1000.0) / 1e9,
+                                 "frac": kio / (dom_ms / 1000.0) / 1e9 / peak}
     pb = path_bytes(stats, meta, nq)
     path = {"algorithmic_bytes_per_step": pb, "achieved": pb / (ms / 1000.0) / 1e9, "peak": peak,
             "frac": pb / (ms / 1000.0) / 1e9 / peak, "unit": "GB/s",

@@ -1125,37 +1125,6 @@ struct __align__(16) PointRec {
   float v[MP];
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  while (!mbar_try(bar, parity)) {
-  }
-}
-// 1-D TMA: `bytes` (multiple of 16) from global to shared, completion counted on bar
-__device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // ---- Lloyd assignment on the tensor cores (m <= 8): the distance GEMM
 // X[128 x 8] . C^T[8 x N] of each 128-point tile runs as three tcgen05 TF32
 // MMAs (x_hi c_hi + x_hi c_lo + x_lo c_hi, hi = tf32(x), lo = tf32(x - hi):
@@ -2251,6 +2220,7 @@ int taco_build_cells(taco_index* idx) {
   if (e != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e));
   idx->has_cells = true;
   if (idx->n_global == idx->n) idx->has_gsize = true;
+  TACO_TRY(build_count_csr(idx));
   return TACO_OK;
 }
 

@@ -255,7 +255,7 @@ int taco_index_destroy(taco_index* idx) {
   cudaSetDevice(idx->device);
   cudaStreamSynchronize(idx->stream);
   DevBuf* bufs[] = {&idx->X, &idx->Xn, &idx->Xsq, &idx->mean, &idx->M, &idx->T, &idx->cb1, &idx->cb2, &idx->labels,
-                    &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize};
+                    &idx->hist, &idx->niter, &idx->ids, &idx->offs, &idx->gsize, &idx->cenc, &idx->coffs};
   for (auto* b : bufs) b->release();
   idx->qt.release();
   idx->qt2.release();
@@ -710,6 +710,7 @@ int taco_index_set_cells(taco_index* idx, const int64_t* offsets_h, const uint32
   }
   idx->has_cells = true;
   if (idx->n_global == idx->n) idx->has_gsize = true;
+  TACO_TRY(build_count_csr(idx));
   return TACO_OK;
 }
 

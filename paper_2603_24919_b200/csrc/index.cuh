@@ -71,6 +71,9 @@ struct taco_index {
   bool cluster_mode = false;
   int d = 0, n_sub = 0, s = 0, K = 0, kp = 0, m1 = 0, m2 = 0, D = 0, iters = 0;
   taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
+  taco::DevBuf cenc, coffs;   // encoded, group-padded CSR of the TMA count (build_count_csr)
+  size_t cstride = 0;         // entries per subspace in cenc
+  bool has_ccsr = false;
   taco::DevBuf Xn;            // lossless narrow copy of X for the rerank (xfmt != TACO_ROWS_F32)
   taco::DevBuf Xsq;           // u8 rows: int32 sum of squares per row (integer rerank path)
   int xfmt = 0;               // TACO_ROWS_*
@@ -96,6 +99,7 @@ int index_check(taco_index* idx);
 // kernels shared between translation units
 int launch_transform(cudaStream_t st, const float* P, int64_t np_, int d, int D,
                      const float* mean, const float* M, float* out, bool dim_major);
+int build_count_csr(taco_index* idx);   // after the cells change (query.cu)
 int launch_colmean(cudaStream_t st, const float* X, int64_t r0, int64_t r1, int64_t n, int d, double* state,
                    double* mean, int chained = 0);
 }  // namespace taco

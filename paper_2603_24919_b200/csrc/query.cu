@@ -458,7 +458,8 @@ __device__ __forceinline__ void count_chunk(const uint16_t* __restrict__ pops, c
 
 // Level histogram of a chunk table.  n_sub <= 16: from the tallies; else by a
 // scan of the table (atomics per nonzero byte).
-__device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, CountSmem& S) {
+template <typename SM>
+__device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, SM& S) {
   const int tid = threadIdx.x;
   if (n_sub <= 16) {
     for (int l = tid; l <= n_sub; l += blockDim.x) {
@@ -776,6 +777,432 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
   if (s_base + s_cnt <= cand_cap && !(dbg & 3))
     compact_unordered<CT_THREADS, NIB>(table, valid, (uint32_t)s_L, base, cand + s_base, &S.batches);
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // nobody reads my histogram any more
+}
+
+// ------------------------------------------- encoded-CSR cluster count (N_s <= 8)
+// Same contract as k_count_cluster (4-bit tables, one cluster of nchunks CTAs
+// per query), fed by the encoded CSR of build_count_csr: every (chunk, cell)
+// slice is a run of 16-byte groups of 4 entries, entry = table word byte
+// offset << 6 | nibble shift; padding entries (EC_SENT) have shift 32, so they
+// add 0 to word 0 and read level 0.  Per entry: and (shift), lea (address),
+// shl (increment), atom, shr (old nibble), shl + funnel shift (tally field),
+// add -- no predicates, no per-id address arithmetic.  Padding entries'
+// level-0 tallies are subtracted (their count rides in the top 2 bits of the
+// slice offsets).  Two feeds:
+//  - k_count_enc: all threads stage the popped slices' group addresses in
+//    shared memory (one store per 16-byte group), then consume them with
+//    direct 16-byte loads, two groups of lookahead per thread;
+//  - k_count_tma: a producer warp streams each slice with one cp.async.bulk
+//    into an mbarrier ring (TACO_COUNT_FEED=tma; measured slower: thousands
+//    of 100-200 byte bulk copies per CTA).
+constexpr uint32_t EC_SENT = 32u;
+constexpr uint32_t EC_GMASK = 0x3FFFFFFFu;
+
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
+  return r;
+}
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t v, uint32_t s) {
+  uint32_t r;
+  asm("shr.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
+  return r;
+}
+// one group of 4 encoded entries into the table at shared address tsg;
+// ev/od collect "left level r" in 8-bit fields (levels 0,2,4,6 / 1,3,5,7)
+__device__ __forceinline__ void apply_group(const uint4 e, uint32_t tsg, uint32_t& ev, uint32_t& od) {
+  const uint32_t s0 = e.x & 63u, s1 = e.y & 63u, s2 = e.z & 63u, s3 = e.w & 63u;
+  const uint32_t o0 = smem_atomic_add(tsg + (e.x >> 6), shl_clamp(1u, s0));
+  const uint32_t o1 = smem_atomic_add(tsg + (e.y >> 6), shl_clamp(1u, s1));
+  const uint32_t o2 = smem_atomic_add(tsg + (e.z >> 6), shl_clamp(1u, s2));
+  const uint32_t o3 = smem_atomic_add(tsg + (e.w >> 6), shl_clamp(1u, s3));
+  // 4-bit field r (r <= 7: the funnel shift wraps mod 32)
+  const uint32_t u4 = __funnelshift_l(0u, 1u, shr_clamp(o0, s0) << 2) + __funnelshift_l(0u, 1u, shr_clamp(o1, s1) << 2) +
+                      __funnelshift_l(0u, 1u, shr_clamp(o2, s2) << 2) + __funnelshift_l(0u, 1u, shr_clamp(o3, s3) << 2);
+  ev += u4 & 0x0F0F0F0Fu;
+  od += (u4 >> 4) & 0x0F0F0F0Fu;
+}
+
+template <int NT>
+struct EncSmem {
+  uint64_t full[8], empty[8];   // k_count_tma ring
+  int cnt[8];
+  int pads, fill, L, ptot;
+  int64_t sbase, scnt;
+  uint32_t wtot[NT / 32];
+  int jpref[17];
+  int ge[257];
+  int lh[256];
+};
+
+// tallies -> level histogram, cluster exchange, Alg. 5, compaction (the
+// k_count_cluster epilogue for NT threads)
+template <int NT>
+__device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
+                             cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
+                             uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
+                             int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
+                             int32_t* __restrict__ lvl) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int rank = (int)cluster.block_rank();
+  const int csz = (int)cluster.num_blocks();
+  for (int l = 1; l <= n_sub; ++l) {   // #score >= l = #increments leaving l - 1
+    int x = T.level(l - 1, true);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(&S.ge[l], x);
+  }
+  __syncthreads();
+  if (tid == 0) S.ge[1] -= S.pads;   // padding entries counted as leaving level 0
+  __syncthreads();
+  chunk_levels(table, valid, n_sub, S);
+  cluster.sync();   // every CTA's level histogram is final
+  for (int l = tid; l <= n_sub; l += NT) {
+    int h = 0;
+    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
+    S.ge[l] = h;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    int64_t cands = 0;
+    const int L = alg5([&](int l) { return (int64_t)S.ge[l]; }, n_sub, budget, cands);
+    int64_t mine = 0;
+    for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
+    const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
+    if (b + mine > cand_cap) flags[1] = 1;
+    S.L = L;
+    S.sbase = b;
+    S.scnt = mine;
+    S.fill = 0;
+    sbase[q * csz + rank] = b;
+    scnt[q * csz + rank] = mine;
+    if (rank == 0) {
+      cnum[q] = cands;
+      lvl[q] = L;
+    }
+  }
+  __syncthreads();
+  if (S.sbase + S.scnt <= cand_cap)
+    compact_unordered<NT, true>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// pop g of query q (flattened over subspaces, jpref in S): its slice's
+// (first group, group count, padding) in chunk c
+__device__ __forceinline__ void enc_slice(const uint16_t* __restrict__ pops, const uint32_t* __restrict__ coffs,
+                                          size_t offs_len, int cap, int n_sub, int K2, int64_t q, int64_t c,
+                                          const int* jpref, int g, uint32_t& g0, uint32_t& ng, uint32_t& pad,
+                                          uint32_t& jb) {
+  int j = 0;
+  for (int jj = 1; jj < n_sub; ++jj) j += g >= jpref[jj];
+  const int cell = pops[((size_t)q * n_sub + j) * cap + (g - jpref[j])];
+  const uint32_t* O = coffs + (size_t)j * offs_len + (size_t)c * K2;
+  const uint32_t a = __ldg(O + cell), b = __ldg(O + cell + 1);
+  g0 = a & EC_GMASK;
+  ng = (b & EC_GMASK) - g0;
+  pad = b >> 30;
+  jb = (uint32_t)j;
+}
+
+constexpr int EC_NT = 512;        // k_count_enc threads
+constexpr int EC_PER = 2;         // pops per thread per batch
+constexpr int EC_GC = 4096;       // staged group addresses per round (16 KB)
+
+__global__ void __launch_bounds__(EC_NT, 2) k_count_enc(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
+    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<EC_NT> S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t q = blockIdx.y;
+  const int64_t c = cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  const int tbytes = (int)(chunk / 2);
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [EC_GC]
+  const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
+  const uint32_t jstride = (uint32_t)(cstride / 4);                 // groups per subspace
+  const size_t offs_len = (size_t)nchunks * K2 + 1;
+  uint4* t4 = reinterpret_cast<uint4*>(table);
+  for (int i = tid; i < tbytes / 16; i += EC_NT) t4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < 257; i += EC_NT) S.ge[i] = 0;
+  if (tid < 32) {
+    const int np = tid < n_sub ? min(npop[q * n_sub + tid], cap) : 0;
+    int x = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (tid >= o) x += y;
+    }
+    if (tid <= n_sub) S.jpref[tid] = x - np;   // jpref[n_sub] = total
+    if (tid == 0) S.pads = 0;
+  }
+  __syncthreads();
+  const int P_all = S.jpref[n_sub];
+  const uint32_t tsg = smem_u32(table);
+  uint32_t ev = 0, od = 0;
+  Tally T;
+  int pads = 0;
+  for (int b0 = 0; b0 < P_all; b0 += EC_NT * EC_PER) {
+    uint32_t ga[EC_PER], ng[EC_PER];   // global group index of the slice start, group count
+    uint32_t my = 0;
+#pragma unroll
+    for (int u = 0; u < EC_PER; ++u) {
+      const int g = b0 + u * EC_NT + tid;
+      ga[u] = 0;
+      ng[u] = 0;
+      if (g < P_all) {
+        uint32_t g0, pad, j;
+        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, S.jpref, g, g0, ng[u], pad, j);
+        ga[u] = j * jstride + g0;
+        pads += (int)pad;
+      }
+      my += ng[u];
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan<EC_NT>(my, S.wtot, tot);
+    uint32_t gb[EC_PER];
+#pragma unroll
+    for (int u = 0; u < EC_PER; ++u) {
+      gb[u] = run;
+      run += ng[u];
+    }
+    for (uint32_t r0 = 0; r0 < tot; r0 += EC_GC) {
+      const uint32_t r1 = min(tot, r0 + (uint32_t)EC_GC);
+#pragma unroll
+      for (int u = 0; u < EC_PER; ++u) {
+        const uint32_t k0 = max(gb[u], r0), k1 = min(gb[u] + ng[u], r1);
+        for (uint32_t k = k0; k < k1; ++k) gaddr[k - r0] = ga[u] + (k - gb[u]);
+      }
+      __syncthreads();
+      const int nr = (int)(r1 - r0);
+      // two groups of lookahead: loads of k + NT and k + 2 NT in flight while k is applied
+      uint4 e0 = make_uint4(EC_SENT, EC_SENT, EC_SENT, EC_SENT), e1 = e0, e2 = e0;
+      int k = tid;
+      if (k < nr) e0 = E4[gaddr[k]];
+      if (k + EC_NT < nr) e1 = E4[gaddr[k + EC_NT]];
+      for (; k < nr; k += EC_NT) {
+        if (k + 2 * EC_NT < nr) e2 = E4[gaddr[k + 2 * EC_NT]];
+        apply_group(e0, tsg, ev, od);
+        e0 = e1;
+        e1 = e2;
+      }
+      T.add_round(ev, od);   // <= 4 per group, <= 8 groups per thread per round: 8-bit fields
+      ev = od = 0;
+      __syncthreads();
+    }
+  }
+  if (pads) atomicAdd(&S.pads, pads);
+  __syncthreads();
+  enc_epilogue<EC_NT>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt,
+                      cnum, lvl);
+}
+
+constexpr int TC_CW = 16;
+constexpr int TC_THREADS = 32 * (TC_CW + 1);
+constexpr int TC_SG = 32 * TC_CW;     // groups per stage: one per consumer thread
+constexpr int TC_RS = 4;              // ring stages (32 KB)
+
+__global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
+    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<TC_THREADS> S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t q = blockIdx.y;
+  const int64_t c = cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  const int tbytes = (int)(chunk / 2);
+  uint4* ring = reinterpret_cast<uint4*>(table + tbytes);   // [TC_RS][TC_SG]
+  if (tid == 0) {
+    for (int k = 0; k < TC_RS; ++k) {
+      mbar_init(&S.full[k], 1);
+      mbar_init(&S.empty[k], TC_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = tid; i < 257; i += TC_THREADS) S.ge[i] = 0;
+  if (tid < 32) {
+    const int np = tid < n_sub ? min(npop[q * n_sub + tid], cap) : 0;
+    int x = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (tid >= o) x += y;
+    }
+    if (tid <= n_sub) S.jpref[tid] = x - np;
+  }
+  __syncthreads();
+  Tally T;
+  if (wid == TC_CW) {
+    // producer: slices of batch b + 1 are looked up while batch b is issued
+    const int P_all = S.jpref[n_sub];
+    const size_t offs_len = (size_t)nchunks * K2 + 1;
+    const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
+    const uint32_t jstride = (uint32_t)(cstride / 4);
+    uint32_t pos = 0;   // groups issued so far
+    int opened = 0;     // ring stages [0, opened) are writable
+    int pads = 0;
+    auto open_until = [&](uint32_t end) {
+      while ((uint32_t)opened * TC_SG < end) {
+        if (opened >= TC_RS) mbar_wait(&S.empty[opened % TC_RS], (unsigned)((opened / TC_RS) - 1) & 1u);
+        ++opened;
+      }
+    };
+    auto lookup = [&](int b, uint32_t& ga, uint32_t& ng) {
+      const int g = b * 32 + lane;
+      ga = ng = 0;
+      if (g < P_all) {
+        uint32_t g0, pad, j;
+        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, S.jpref, g, g0, ng, pad, j);
+        ga = j * jstride + g0;
+        pads += (int)pad;
+      }
+    };
+    const int nbat = (P_all + 31) / 32;
+    uint32_t ga, ng, ga1, ng1;
+    lookup(0, ga, ng);
+    for (int b = 0; b < nbat; ++b) {
+      lookup(b + 1, ga1, ng1);
+      uint32_t x = ng;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t end = pos + __shfl_sync(0xffffffffu, x, 31);
+      const uint32_t my = pos + x - ng;
+      for (uint32_t k = pos / TC_SG; k * TC_SG < end; ++k) {
+        open_until(k * TC_SG + 1);
+        const uint32_t lo = max(my, k * TC_SG), hi = min(my + ng, (k + 1) * TC_SG);
+        if (lo < hi)
+          tma_g2s(ring + (size_t)(k % TC_RS) * TC_SG + (lo - k * TC_SG), E4 + ga + (lo - my), (hi - lo) * 16u,
+                  &S.full[k % TC_RS]);
+        __syncwarp();
+        if (lane == 0 && end >= (k + 1) * TC_SG) {
+          S.cnt[k % TC_RS] = TC_SG;
+          mbar_expect_tx(&S.full[k % TC_RS], TC_SG * 16u);
+        }
+      }
+      pos = end;
+      ga = ga1;
+      ng = ng1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pads += __shfl_xor_sync(0xffffffffu, pads, o);
+    uint32_t kend = pos / TC_SG;
+    if (pos % TC_SG) {   // last partial stage
+      if (lane == 0) {
+        S.cnt[kend % TC_RS] = (int)(pos % TC_SG);
+        mbar_expect_tx(&S.full[kend % TC_RS], (pos % TC_SG) * 16u);
+      }
+      ++kend;
+    }
+    open_until(kend * TC_SG + 1);   // the end marker's stage
+    if (lane == 0) {
+      S.pads = pads;
+      S.cnt[kend % TC_RS] = 0;
+      mbar_arrive(&S.full[kend % TC_RS]);
+    }
+  } else {
+    uint4* t4 = reinterpret_cast<uint4*>(table);
+    for (int i = tid; i < tbytes / 16; i += TC_CW * 32) t4[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("bar.sync 1, %0;" ::"r"(TC_CW * 32) : "memory");
+    const uint32_t tsg = smem_u32(table);
+    uint32_t ev = 0, od = 0;
+    for (int k = 0;; ++k) {
+      const int slot = k % TC_RS;
+      mbar_wait(&S.full[slot], (unsigned)(k / TC_RS) & 1u);
+      const int cnt = *(volatile int*)&S.cnt[slot];
+      if (cnt == 0) break;
+      if (tid < cnt) apply_group(ring[(size_t)slot * TC_SG + tid], tsg, ev, od);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[slot]);
+      if ((k & 31) == 31) {   // <= 4 per stage in 8-bit fields: flush before they can carry
+        T.add_round(ev, od);
+        ev = od = 0;
+      }
+    }
+    T.add_round(ev, od);
+  }
+  __syncthreads();
+  enc_epilogue<TC_THREADS>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase,
+                           scnt, cnum, lvl);
+}
+
+// Encoded CSR of the TMA count (cluster mode, 4-bit tables): per subspace,
+// slices (chunk, cell) of the (chunk, cell, id) CSR padded to whole 16-byte
+// groups; coffs = group offsets with the padding count of the slice ENDING
+// there in the top 2 bits.  Three launches: per-1024-slice group sums, a scan
+// of those sums, then per-slice offsets + the encoded fill.
+constexpr int CC_NT = 1024;
+__global__ void __launch_bounds__(CC_NT) k_ccsr_sums(const uint32_t* __restrict__ offs, size_t offs_len,
+                                                    int64_t nsl, uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t wtot[CC_NT / 32];
+  const int j = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
+  const uint32_t* O = offs + (size_t)j * offs_len;
+  const uint32_t g = i < nsl ? (O[i + 1] - O[i] + 3u) >> 2 : 0u;
+  uint32_t tot;
+  block_excl_scan<CC_NT>(g, wtot, tot);
+  if (threadIdx.x == 0) bsum[(size_t)j * gridDim.x + blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(CC_NT) k_ccsr_scan(uint32_t* __restrict__ bsum, int nb) {
+  __shared__ uint32_t wtot[CC_NT / 32];
+  const int j = blockIdx.x;
+  uint32_t carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += CC_NT) {
+    const int b = b0 + threadIdx.x;
+    const uint32_t v = b < nb ? bsum[(size_t)j * nb + b] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<CC_NT>(v, wtot, tot);
+    if (b < nb) bsum[(size_t)j * nb + b] = carry + ex;
+    carry += tot;
+  }
+}
+__global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict__ ids,
+                                                    const uint32_t* __restrict__ offs, size_t offs_len,
+                                                    int64_t nsl, int K2, int64_t n, int64_t chunk,
+                                                    const uint32_t* __restrict__ bsum, uint32_t* __restrict__ coffs,
+                                                    uint32_t* __restrict__ cenc, size_t cstride) {
+  __shared__ uint32_t wtot[CC_NT / 32];
+  const int j = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
+  const uint32_t* O = offs + (size_t)j * offs_len;
+  uint32_t s0 = 0, len = 0;
+  if (i < nsl) {
+    s0 = O[i];
+    len = O[i + 1] - s0;
+  }
+  const uint32_t g = (len + 3u) >> 2;
+  uint32_t tot;
+  const uint32_t g0 = bsum[(size_t)j * gridDim.x + blockIdx.x] + block_excl_scan<CC_NT>(g, wtot, tot);
+  uint32_t* C = coffs + (size_t)j * offs_len;
+  if (i < nsl) {   // coffs is zeroed first: the padding bits of slice i land in C[i + 1]
+    atomicOr(&C[i], g0);
+    atomicOr(&C[i + 1], ((4u * g - len) << 30) | (i + 1 == nsl ? g0 + g : 0u));
+    const int64_t cbase = (i / K2) * chunk;
+    const uint32_t* I = ids + (size_t)j * n + s0;
+    uint32_t* E = cenc + (size_t)j * cstride + 4 * (size_t)g0;
+    for (uint32_t e = 0; e < 4 * g; ++e) {
+      uint32_t v = EC_SENT;
+      if (e < len) {
+        const uint32_t p = (uint32_t)(I[e] - cbase);
+        v = ((p >> 3) << 8) | ((p & 7u) << 2);
+      }
+      E[e] = v;
+    }
+  }
 }
 
 // ------------------------------------------------------- global-mode count
@@ -1126,9 +1553,7 @@ __device__ __forceinline__ void einsum_block8(const float* xv, const float* qv8,
   a0 = __dadd_rn(p[0], a0); a1 = __dadd_rn(p[1], a1);
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+
 
 struct TileRef {
   int64_t q;
@@ -1751,6 +2176,45 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
 }
 
 
+// The TMA count runs in cluster mode with 4-bit tables and N_s <= 8
+// (TACO_COUNT_TMA=0 keeps the unit-staged k_count_cluster).
+static bool tma_count_enabled(const taco_index* idx) {
+  const char* e = getenv("TACO_COUNT_TMA");   // read per index (tests pin both kernels)
+  return !(e && e[0] == '0') && idx->cluster_mode && idx->n_sub <= 8 && idx->chunk <= kClusterMaxChunk;
+}
+
+int build_count_csr(taco_index* idx) {
+  idx->has_ccsr = false;
+  if (!tma_count_enabled(idx)) {
+    idx->cenc.release();
+    idx->coffs.release();
+    return TACO_OK;
+  }
+  const int64_t K2 = (int64_t)idx->kp * idx->kp, nsl = idx->nchunks * K2;
+  const size_t offs_len = (size_t)nsl + 1;
+  idx->cstride = (size_t)ceil_div(idx->n + 3 * nsl, 4) * 4;
+  TACO_TRY(idx->cenc.ensure(sizeof(uint32_t) * idx->cstride * idx->n_sub));
+  TACO_TRY(idx->coffs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
+  const int nb = (int)ceil_div(nsl, CC_NT);
+  DevBuf bsum;
+  TACO_TRY(bsum.ensure(sizeof(uint32_t) * (size_t)nb * idx->n_sub));
+  cudaStream_t st = idx->stream;
+  TACO_CHECK_CUDA(cudaMemsetAsync(idx->coffs.p, 0, sizeof(uint32_t) * offs_len * idx->n_sub, st));
+  k_ccsr_sums<<<dim3((unsigned)nb, (unsigned)idx->n_sub), CC_NT, 0, st>>>(idx->offs.as<uint32_t>(), offs_len, nsl,
+                                                                       bsum.as<uint32_t>());
+  TACO_LAUNCHED();
+  k_ccsr_scan<<<(unsigned)idx->n_sub, CC_NT, 0, st>>>(bsum.as<uint32_t>(), nb);
+  TACO_LAUNCHED();
+  k_ccsr_fill<<<dim3((unsigned)nb, (unsigned)idx->n_sub), CC_NT, 0, st>>>(
+      idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(), offs_len, nsl, (int)K2, idx->n, idx->chunk,
+      bsum.as<uint32_t>(), idx->coffs.as<uint32_t>(), idx->cenc.as<uint32_t>(), idx->cstride);
+  TACO_LAUNCHED();
+  TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  bsum.release();
+  idx->has_ccsr = true;
+  return TACO_OK;
+}
+
 static int set_count_attrs(taco_index*) {
   static bool done = false;
   if (!done) {
@@ -1759,6 +2223,12 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint4) * TC_RS * TC_SG)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_tma, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EC_GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     done = true;
@@ -1847,6 +2317,21 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
       dbg = e ? atoi(e) : 0;
       if (dbg) TACO_CHECK_CUDA(cudaMemcpyToSymbol(g_count_dbg, &dbg, sizeof(int)));
     }
+  }
+  if (idx->has_ccsr) {
+    const char* fe = getenv("TACO_COUNT_FEED");   // =tma: the cp.async.bulk ring feed
+    const int feed = (fe && !strcmp(fe, "tma")) ? 1 : 0;
+    cfg.blockDim = dim3(feed ? TC_THREADS : EC_NT, 1, 1);
+    cfg.dynamicSmemBytes = table_bytes(idx) + (feed ? sizeof(uint4) * TC_RS * TC_SG : sizeof(uint32_t) * EC_GC);
+    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma : k_count_enc, (const uint16_t*)t.pops.as<uint16_t>(),
+                                       (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
+                                       (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
+                                       (const uint32_t*)idx->coffs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
+                                       idx->nchunks, idx->chunk, budget, t.cand.as<uint32_t>(), t.cand_cap,
+                                       t.flags.as<int64_t>(), t.qbase.as<int64_t>(), t.clocal.as<int64_t>(),
+                                       t.cnum.as<int64_t>(), t.lvl.as<int32_t>()));
+    TACO_LAUNCHED();
+    return TACO_OK;
   }
   TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, nib_tables(idx) ? k_count_cluster<true> : k_count_cluster<false>,
                                      (const uint16_t*)t.pops.as<uint16_t>(),
