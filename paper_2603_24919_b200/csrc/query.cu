@@ -796,7 +796,8 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 //    into an mbarrier ring (TACO_COUNT_FEED=tma; measured slower: thousands
 //    of 100-200 byte bulk copies per CTA).
 constexpr uint32_t EC_SENT = 32u;
-constexpr uint32_t EC_GMASK = 0x3FFFFFFFu;
+constexpr int EC_U = 8;                  // entries per unit (32 bytes, one sector)
+constexpr uint32_t EC_GMASK = 0x1FFFFFFFu;   // unit offset bits of coffs (top 3 bits: padding count)
 
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t s) {
   uint32_t r;
@@ -836,21 +837,44 @@ struct EncSmem {
 };
 
 // tallies -> level histogram, cluster exchange, Alg. 5, compaction (the
-// k_count_cluster epilogue for NT threads)
+// k_count_cluster epilogue for NT threads).  Thread 0 reserves the CTA's
+// candidate segment with one global atomic; while it is in flight the CTA
+// compacts into `stage` (shared memory, scap ids) and copies the segment out
+// coalesced once the base is known (direct global writes when it is larger).
 template <int NT>
 __device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
                              cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
                              uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
                              int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
-                             int32_t* __restrict__ lvl) {
+                             int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int rank = (int)cluster.block_rank();
   const int csz = (int)cluster.num_blocks();
-  for (int l = 1; l <= n_sub; ++l) {   // #score >= l = #increments leaving l - 1
-    int x = T.level(l - 1, true);
+  // #score >= l = #increments leaving l - 1.  When every lane's packed 16-bit
+  // tallies are < 8192 they are summed packed over 8-lane groups (no carry
+  // between fields) and lanes 0, 8, 16, 24 add their levels; otherwise per
+  // level over the whole warp
+  uint64_t a0 = T.a0, a1 = T.a1;
+  constexpr uint64_t HI3 = 0xE000E000E000E000ull;
+  if (!__any_sync(0xffffffffu, ((a0 | a1) & HI3) != 0)) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && x) atomicAdd(&S.ge[l], x);
+    for (int o = 4; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if ((lane & 7) == 0)
+      for (int l = 1; l <= n_sub; ++l) {
+        const uint64_t w = ((l - 1) & 1) ? a1 : a0;
+        const int x = (int)((w >> (16 * ((l - 1) >> 1))) & 0xFFFFull);
+        if (x) atomicAdd(&S.ge[l], x);
+      }
+  } else {
+    for (int l = 1; l <= n_sub; ++l) {
+      int x = T.level(l - 1, true);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0 && x) atomicAdd(&S.ge[l], x);
+    }
   }
   __syncthreads();
   if (tid == 0) S.ge[1] -= S.pads;   // padding entries counted as leaving level 0
@@ -864,59 +888,87 @@ __device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_su
   }
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   __syncthreads();
+  int64_t b = 0;
   if (tid == 0) {
     int64_t cands = 0;
     const int L = alg5([&](int l) { return (int64_t)S.ge[l]; }, n_sub, budget, cands);
     int64_t mine = 0;
     for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
-    const int64_t b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
-    if (b + mine > cand_cap) flags[1] = 1;
+    b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);   // used after the scan
     S.L = L;
-    S.sbase = b;
     S.scnt = mine;
     S.fill = 0;
-    sbase[q * csz + rank] = b;
-    scnt[q * csz + rank] = mine;
     if (rank == 0) {
       cnum[q] = cands;
       lvl[q] = L;
     }
+    if (mine > scap) S.sbase = b;   // direct path: the base is needed before the scan
   }
   __syncthreads();
-  if (S.sbase + S.scnt <= cand_cap)
+  const int64_t mine = S.scnt;
+  if (mine <= scap) {
+    compact_unordered<NT, true>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
+    if (tid == 0) S.sbase = b;
+    __syncthreads();
+    const int64_t sb = S.sbase;
+    if (sb + mine <= cand_cap)
+      for (int i = tid; i < (int)mine; i += NT) cand[sb + i] = stage[i];
+  } else if (S.sbase + mine <= cand_cap) {
     compact_unordered<NT, true>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
+  }
+  if (tid == 0) {
+    if (S.sbase + mine > cand_cap) flags[1] = 1;
+    sbase[q * csz + rank] = S.sbase;
+    scnt[q * csz + rank] = mine;
+  }
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// pop g of query q (flattened over subspaces, jpref in S): its slice's
-// (first group, group count, padding) in chunk c
+// pop g of query q (flattened over subspaces; jpref = the subspaces' pop
+// prefix, in registers): its slice's (first unit, unit count, padding) in
+// chunk c and its subspace js
 __device__ __forceinline__ void enc_slice(const uint16_t* __restrict__ pops, const uint32_t* __restrict__ coffs,
                                           size_t offs_len, int cap, int n_sub, int K2, int64_t q, int64_t c,
-                                          const int* jpref, int g, uint32_t& g0, uint32_t& ng, uint32_t& pad,
-                                          uint32_t& jb) {
-  int j = 0;
-  for (int jj = 1; jj < n_sub; ++jj) j += g >= jpref[jj];
-  const int cell = pops[((size_t)q * n_sub + j) * cap + (g - jpref[j])];
+                                          const int (&jpref)[8], int g, uint32_t& g0, uint32_t& ng, uint32_t& pad,
+                                          uint32_t& js) {
+  int j = 0, jb = 0;
+#pragma unroll
+  for (int jj = 1; jj < 8; ++jj)
+    if (jj < n_sub && g >= jpref[jj]) {
+      j = jj;
+      jb = jpref[jj];
+    }
+  const int cell = pops[((size_t)q * n_sub + j) * cap + (g - jb)];
   const uint32_t* O = coffs + (size_t)j * offs_len + (size_t)c * K2;
   const uint32_t a = __ldg(O + cell), b = __ldg(O + cell + 1);
   g0 = a & EC_GMASK;
   ng = (b & EC_GMASK) - g0;
-  pad = b >> 30;
-  jb = (uint32_t)j;
+  pad = b >> 29;
+  js = (uint32_t)j;
 }
 
-constexpr int EC_NT = 512;        // k_count_enc threads
-constexpr int EC_PER = 2;         // pops per thread per batch
-constexpr int EC_GC = 4096;       // staged group addresses per round (16 KB)
+// k_count_enc<NT, MINB>: NT threads, MINB CTAs per SM.  Per batch of NT *
+// EC_PER popped slices: each thread looks up EC_PER slices (pops -> unit
+// range), one block scan places their units, and rounds of EC_GC(NT) unit
+// indices are staged in shared memory and consumed by all threads (unit t,
+// t + NT, ...; one unit of load lookahead).
+constexpr int EC_PER = 2;
+template <int NT>
+struct EcCfg {
+  static constexpr int PER = NT >= 512 ? 2 : 4;   // pops per thread per batch
+  static constexpr int GC = 8 * NT;               // staged units per round: 8 per thread (8-bit tallies)
+};
 
-__global__ void __launch_bounds__(EC_NT, 2) k_count_enc(
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_count_enc(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
     int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
     int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
     int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  constexpr int PER = EcCfg<NT>::PER, GC = EcCfg<NT>::GC;
   extern __shared__ __align__(16) uint8_t table[];
-  __shared__ EncSmem<EC_NT> S;
+  __shared__ EncSmem<NT> S;
   cg::cluster_group cluster = cg::this_cluster();
   const int64_t q = blockIdx.y;
   const int64_t c = cluster.block_rank();
@@ -924,13 +976,13 @@ __global__ void __launch_bounds__(EC_NT, 2) k_count_enc(
   const int64_t base = c * chunk;
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
   const int tbytes = (int)(chunk / 2);
-  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [EC_GC]
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
   const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
-  const uint32_t jstride = (uint32_t)(cstride / 4);                 // groups per subspace
+  const uint32_t jstride = (uint32_t)(cstride / EC_U);              // units per subspace
   const size_t offs_len = (size_t)nchunks * K2 + 1;
   uint4* t4 = reinterpret_cast<uint4*>(table);
-  for (int i = tid; i < tbytes / 16; i += EC_NT) t4[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 257; i += EC_NT) S.ge[i] = 0;
+  for (int i = tid; i < tbytes / 16; i += NT) t4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < 257; i += NT) S.ge[i] = 0;
   if (tid < 32) {
     const int np = tid < n_sub ? min(npop[q * n_sub + tid], cap) : 0;
     int x = np;
@@ -944,63 +996,75 @@ __global__ void __launch_bounds__(EC_NT, 2) k_count_enc(
   }
   __syncthreads();
   const int P_all = S.jpref[n_sub];
+  int jp[8];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) jp[jj] = S.jpref[jj];
   const uint32_t tsg = smem_u32(table);
   uint32_t ev = 0, od = 0;
   Tally T;
   int pads = 0;
-  for (int b0 = 0; b0 < P_all; b0 += EC_NT * EC_PER) {
-    uint32_t ga[EC_PER], ng[EC_PER];   // global group index of the slice start, group count
+  for (int b0 = 0; b0 < P_all; b0 += NT * PER) {
+    uint32_t ga[PER], ng[PER];   // unit index of the slice start, unit count
     uint32_t my = 0;
 #pragma unroll
-    for (int u = 0; u < EC_PER; ++u) {
-      const int g = b0 + u * EC_NT + tid;
+    for (int u = 0; u < PER; ++u) {
+      const int g = b0 + u * NT + tid;
       ga[u] = 0;
       ng[u] = 0;
       if (g < P_all) {
-        uint32_t g0, pad, j;
-        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, S.jpref, g, g0, ng[u], pad, j);
-        ga[u] = j * jstride + g0;
+        uint32_t u0, pad, j;
+        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, jp, g, u0, ng[u], pad, j);
+        ga[u] = j * jstride + u0;
         pads += (int)pad;
       }
       my += ng[u];
     }
     uint32_t tot;
-    uint32_t run = block_excl_scan<EC_NT>(my, S.wtot, tot);
-    uint32_t gb[EC_PER];
+    uint32_t run = block_excl_scan<NT>(my, S.wtot, tot);
+    uint32_t gb[PER];
 #pragma unroll
-    for (int u = 0; u < EC_PER; ++u) {
+    for (int u = 0; u < PER; ++u) {
       gb[u] = run;
       run += ng[u];
     }
-    for (uint32_t r0 = 0; r0 < tot; r0 += EC_GC) {
-      const uint32_t r1 = min(tot, r0 + (uint32_t)EC_GC);
+    for (uint32_t r0 = 0; r0 < tot; r0 += GC) {
+      const uint32_t r1 = min(tot, r0 + (uint32_t)GC);
 #pragma unroll
-      for (int u = 0; u < EC_PER; ++u) {
+      for (int u = 0; u < PER; ++u) {
         const uint32_t k0 = max(gb[u], r0), k1 = min(gb[u] + ng[u], r1);
         for (uint32_t k = k0; k < k1; ++k) gaddr[k - r0] = ga[u] + (k - gb[u]);
       }
       __syncthreads();
       const int nr = (int)(r1 - r0);
-      // two groups of lookahead: loads of k + NT and k + 2 NT in flight while k is applied
-      uint4 e0 = make_uint4(EC_SENT, EC_SENT, EC_SENT, EC_SENT), e1 = e0, e2 = e0;
+      // one unit (2 x 16 B) of lookahead: unit k + NT loads while unit k is applied
+      const uint4 sent = make_uint4(EC_SENT, EC_SENT, EC_SENT, EC_SENT);
+      uint4 a0 = sent, a1 = sent, b0v = sent, b1v = sent;
       int k = tid;
-      if (k < nr) e0 = E4[gaddr[k]];
-      if (k + EC_NT < nr) e1 = E4[gaddr[k + EC_NT]];
-      for (; k < nr; k += EC_NT) {
-        if (k + 2 * EC_NT < nr) e2 = E4[gaddr[k + 2 * EC_NT]];
-        apply_group(e0, tsg, ev, od);
-        e0 = e1;
-        e1 = e2;
+      if (k < nr) {
+        const uint4* src = E4 + 2 * (size_t)gaddr[k];
+        a0 = src[0];
+        a1 = src[1];
       }
-      T.add_round(ev, od);   // <= 4 per group, <= 8 groups per thread per round: 8-bit fields
+      for (; k < nr; k += NT) {
+        if (k + NT < nr) {
+          const uint4* src = E4 + 2 * (size_t)gaddr[k + NT];
+          b0v = src[0];
+          b1v = src[1];
+        }
+        apply_group(a0, tsg, ev, od);
+        apply_group(a1, tsg, ev, od);
+        a0 = b0v;
+        a1 = b1v;
+      }
+      T.add_round(ev, od);   // <= 8 per unit, <= 8 units per thread per round: 8-bit fields
       ev = od = 0;
       __syncthreads();
     }
   }
   if (pads) atomicAdd(&S.pads, pads);
   __syncthreads();
-  enc_epilogue<EC_NT>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt,
-                      cnum, lvl);
+  enc_epilogue<NT>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
+                   lvl, gaddr, GC);
 }
 
 constexpr int TC_CW = 16;
@@ -1049,7 +1113,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
     const int P_all = S.jpref[n_sub];
     const size_t offs_len = (size_t)nchunks * K2 + 1;
     const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
-    const uint32_t jstride = (uint32_t)(cstride / 4);
+    const uint32_t jstride = (uint32_t)(cstride / 4);   // groups per subspace
+    int jp[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) jp[jj] = S.jpref[jj];
     uint32_t pos = 0;   // groups issued so far
     int opened = 0;     // ring stages [0, opened) are writable
     int pads = 0;
@@ -1064,8 +1131,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
       ga = ng = 0;
       if (g < P_all) {
         uint32_t g0, pad, j;
-        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, S.jpref, g, g0, ng, pad, j);
-        ga = j * jstride + g0;
+        enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, jp, g, g0, ng, pad, j);
+        ga = j * jstride + 2 * g0;   // units -> 16-byte groups
+        ng *= 2;
         pads += (int)pad;
       }
     };
@@ -1137,7 +1205,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
   }
   __syncthreads();
   enc_epilogue<TC_THREADS>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase,
-                           scnt, cnum, lvl);
+                           scnt, cnum, lvl, reinterpret_cast<uint32_t*>(ring), TC_RS * TC_SG * 4);
 }
 
 // Encoded CSR of the TMA count (cluster mode, 4-bit tables): per subspace,
@@ -1152,7 +1220,7 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_sums(const uint32_t* __restrict_
   const int j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
   const uint32_t* O = offs + (size_t)j * offs_len;
-  const uint32_t g = i < nsl ? (O[i + 1] - O[i] + 3u) >> 2 : 0u;
+  const uint32_t g = i < nsl ? (O[i + 1] - O[i] + (EC_U - 1)) / EC_U : 0u;
   uint32_t tot;
   block_excl_scan<CC_NT>(g, wtot, tot);
   if (threadIdx.x == 0) bsum[(size_t)j * gridDim.x + blockIdx.x] = tot;
@@ -1184,17 +1252,17 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
     s0 = O[i];
     len = O[i + 1] - s0;
   }
-  const uint32_t g = (len + 3u) >> 2;
+  const uint32_t g = (len + (EC_U - 1)) / EC_U;
   uint32_t tot;
   const uint32_t g0 = bsum[(size_t)j * gridDim.x + blockIdx.x] + block_excl_scan<CC_NT>(g, wtot, tot);
   uint32_t* C = coffs + (size_t)j * offs_len;
   if (i < nsl) {   // coffs is zeroed first: the padding bits of slice i land in C[i + 1]
     atomicOr(&C[i], g0);
-    atomicOr(&C[i + 1], ((4u * g - len) << 30) | (i + 1 == nsl ? g0 + g : 0u));
+    atomicOr(&C[i + 1], ((EC_U * g - len) << 29) | (i + 1 == nsl ? g0 + g : 0u));
     const int64_t cbase = (i / K2) * chunk;
     const uint32_t* I = ids + (size_t)j * n + s0;
-    uint32_t* E = cenc + (size_t)j * cstride + 4 * (size_t)g0;
-    for (uint32_t e = 0; e < 4 * g; ++e) {
+    uint32_t* E = cenc + (size_t)j * cstride + EC_U * (size_t)g0;
+    for (uint32_t e = 0; e < EC_U * g; ++e) {
       uint32_t v = EC_SENT;
       if (e < len) {
         const uint32_t p = (uint32_t)(I[e] - cbase);
@@ -2180,7 +2248,11 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
 // (TACO_COUNT_TMA=0 keeps the unit-staged k_count_cluster).
 static bool tma_count_enabled(const taco_index* idx) {
   const char* e = getenv("TACO_COUNT_TMA");   // read per index (tests pin both kernels)
-  return !(e && e[0] == '0') && idx->cluster_mode && idx->n_sub <= 8 && idx->chunk <= kClusterMaxChunk;
+  // padding to whole units must stay below ~n entries per subspace (large K'
+  // with short slices keeps the unit-staged kernel)
+  const int64_t nsl = idx->nchunks * (int64_t)idx->kp * idx->kp;
+  return !(e && e[0] == '0') && idx->cluster_mode && idx->n_sub <= 8 && idx->chunk <= kClusterMaxChunk &&
+         (EC_U - 1) * nsl <= idx->n;
 }
 
 int build_count_csr(taco_index* idx) {
@@ -2192,7 +2264,7 @@ int build_count_csr(taco_index* idx) {
   }
   const int64_t K2 = (int64_t)idx->kp * idx->kp, nsl = idx->nchunks * K2;
   const size_t offs_len = (size_t)nsl + 1;
-  idx->cstride = (size_t)ceil_div(idx->n + 3 * nsl, 4) * 4;
+  idx->cstride = (size_t)ceil_div(idx->n + (EC_U - 1) * nsl, EC_U) * EC_U;
   TACO_TRY(idx->cenc.ensure(sizeof(uint32_t) * idx->cstride * idx->n_sub));
   TACO_TRY(idx->coffs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
   const int nb = (int)ceil_div(nsl, CC_NT);
@@ -2226,9 +2298,12 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint4) * TC_RS * TC_SG)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_tma, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EC_GC)));
-    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<512>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     done = true;
@@ -2321,9 +2396,13 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
   if (idx->has_ccsr) {
     const char* fe = getenv("TACO_COUNT_FEED");   // =tma: the cp.async.bulk ring feed
     const int feed = (fe && !strcmp(fe, "tma")) ? 1 : 0;
-    cfg.blockDim = dim3(feed ? TC_THREADS : EC_NT, 1, 1);
-    cfg.dynamicSmemBytes = table_bytes(idx) + (feed ? sizeof(uint4) * TC_RS * TC_SG : sizeof(uint32_t) * EC_GC);
-    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma : k_count_enc, (const uint16_t*)t.pops.as<uint16_t>(),
+    const char* ne = getenv("TACO_COUNT_NT");   // 256 (3 CTAs per SM, default) or 512 (2 per SM)
+    const bool wide = ne && atoi(ne) == 512;
+    cfg.blockDim = dim3(feed ? TC_THREADS : wide ? 512 : 256, 1, 1);
+    cfg.dynamicSmemBytes = table_bytes(idx) + (feed ? sizeof(uint4) * TC_RS * TC_SG
+                                                    : sizeof(uint32_t) * (wide ? EcCfg<512>::GC : EcCfg<256>::GC));
+    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma : wide ? k_count_enc<512, 2> : k_count_enc<256, 3>,
+                                       (const uint16_t*)t.pops.as<uint16_t>(),
                                        (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
                                        (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
                                        (const uint32_t*)idx->coffs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
