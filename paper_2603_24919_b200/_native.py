@@ -17,6 +17,9 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtaco_b200.so")
+# experiments only: a variant build of the same library (tools/variants.sh)
+if os.environ.get("TACO_LIB_VARIANT"):
+    LIB_PATH = os.path.abspath(os.environ["TACO_LIB_VARIANT"])
 
 _c_int, _c_i32, _c_i64, _c_dbl, _vp = ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 

@@ -612,13 +612,29 @@ __device__ __forceinline__ uint32_t warp_reserve(uint32_t c, int* fill) {
   return (uint32_t)__shfl_sync(0xffffffffu, base, 31) + x - c;
 }
 
-template <int NT, bool NIB>
+// SMALL (4-bit lanes holding scores <= 8, L >= 1): lane >= L <=> bit 3 of
+// lane + (8 - L), which cannot carry into the next lane (<= 15).
+__device__ __forceinline__ uint32_t vec_hits_small(const uint4 v, uint32_t K, int lim) {
+  constexpr uint32_t H = 0x88888888u;
+  uint32_t g0 = (v.x + K) & H, g1 = (v.y + K) & H, g2 = (v.z + K) & H, g3 = (v.w + K) & H;
+  if (lim < 32) {
+    const uint32_t m0 = lim >= 8 ? ~0u : (1u << (4 * lim)) - 1u;
+    const uint32_t m1 = lim >= 16 ? ~0u : lim <= 8 ? 0u : (1u << (4 * (lim - 8))) - 1u;
+    const uint32_t m2 = lim >= 24 ? ~0u : lim <= 16 ? 0u : (1u << (4 * (lim - 16))) - 1u;
+    const uint32_t m3 = lim <= 24 ? 0u : (1u << (4 * (lim - 24))) - 1u;
+    g0 &= m0; g1 &= m1; g2 &= m2; g3 &= m3;
+  }
+  return g0 | (g1 >> 1) | (g2 >> 2) | (g3 >> 3);
+}
+
+template <int NT, bool NIB, bool SMALL = false>
 __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst,
                                   int* fill) {
   constexpr int LW = NIB ? 4 : 8;
   constexpr int LPW = 32 / LW;
   constexpr int IDS = 4 * LPW;
   const uint32_t D = L == 0 ? 0u : (NIB ? (16u - L) * 0x11111111u : (256u - L) * 0x01010101u);
+  const uint32_t K = (8u - L) * 0x11111111u;
   const uint4* t4 = reinterpret_cast<const uint4*>(tab);
   const int nvec = (valid + IDS - 1) / IDS;
   const int lane = threadIdx.x & 31;
@@ -628,7 +644,10 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
 #pragma unroll
     for (int e = 0; e < CP_VPL; ++e) {
       const int vi = v0 + e * 32 + lane;
-      m[e] = vi < nvec ? vec_hits<NIB>(t4[vi], D, valid - vi * IDS) : 0u;
+      if (SMALL && L >= 1)
+        m[e] = vi < nvec ? vec_hits_small(t4[vi], K, valid - vi * IDS) : 0u;
+      else
+        m[e] = vi < nvec ? vec_hits<NIB>(t4[vi], D, valid - vi * IDS) : 0u;
       c += __popc(m[e]);
     }
     if (__ballot_sync(0xffffffffu, c != 0u) == 0u) continue;
@@ -795,6 +814,15 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 //  - k_count_tma: a producer warp streams each slice with one cp.async.bulk
 //    into an mbarrier ring (TACO_COUNT_FEED=tma; measured slower: thousands
 //    of 100-200 byte bulk copies per CTA).
+#ifndef EC_PP
+#define EC_PP 1      // ping-pong lookahead registers in the consume loop
+#endif
+#ifndef EC_FASTGE
+#define EC_FASTGE 1  // scores <= 8: lanes >= L as (w + (8 - L) * 0x11111111) & 0x88888888
+#endif
+#ifndef EC_RELAX
+#define EC_RELAX 1   // relaxed cluster arrive after the histogram gather
+#endif
 constexpr uint32_t EC_SENT = 32u;
 constexpr int EC_U = 8;                  // entries per unit (32 bytes, one sector)
 constexpr uint32_t EC_GMASK = 0x1FFFFFFFu;   // unit offset bits of coffs (top 3 bits: padding count)
@@ -886,7 +914,10 @@ __device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_su
     for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
     S.ge[l] = h;
   }
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (EC_RELAX)   // publishes nothing: only "done reading the remote histograms"
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  else
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   __syncthreads();
   int64_t b = 0;
   if (tid == 0) {
@@ -907,14 +938,14 @@ __device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_su
   __syncthreads();
   const int64_t mine = S.scnt;
   if (mine <= scap) {
-    compact_unordered<NT, true>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
+    compact_unordered<NT, true, EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
     if (tid == 0) S.sbase = b;
     __syncthreads();
     const int64_t sb = S.sbase;
     if (sb + mine <= cand_cap)
       for (int i = tid; i < (int)mine; i += NT) cand[sb + i] = stage[i];
   } else if (S.sbase + mine <= cand_cap) {
-    compact_unordered<NT, true>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
+    compact_unordered<NT, true, EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
   }
   if (tid == 0) {
     if (S.sbase + mine > cand_cap) flags[1] = 1;
@@ -952,7 +983,6 @@ __device__ __forceinline__ void enc_slice(const uint16_t* __restrict__ pops, con
 // range), one block scan places their units, and rounds of EC_GC(NT) unit
 // indices are staged in shared memory and consumed by all threads (unit t,
 // t + NT, ...; one unit of load lookahead).
-constexpr int EC_PER = 2;
 template <int NT>
 struct EcCfg {
   static constexpr int PER = NT >= 512 ? 2 : 4;   // pops per thread per batch
@@ -1037,24 +1067,36 @@ __global__ void __launch_bounds__(NT, MINB) k_count_enc(
       __syncthreads();
       const int nr = (int)(r1 - r0);
       // one unit (2 x 16 B) of lookahead: unit k + NT loads while unit k is applied
-      const uint4 sent = make_uint4(EC_SENT, EC_SENT, EC_SENT, EC_SENT);
-      uint4 a0 = sent, a1 = sent, b0v = sent, b1v = sent;
-      int k = tid;
-      if (k < nr) {
-        const uint4* src = E4 + 2 * (size_t)gaddr[k];
-        a0 = src[0];
-        a1 = src[1];
-      }
-      for (; k < nr; k += NT) {
-        if (k + NT < nr) {
-          const uint4* src = E4 + 2 * (size_t)gaddr[k + NT];
-          b0v = src[0];
-          b1v = src[1];
+      uint4 a0, a1, b0v, b1v;
+      auto fetch = [&](int kk, uint4& x0, uint4& x1) {
+        if (kk < nr) {
+          const uint4* src = E4 + 2 * (size_t)gaddr[kk];
+          x0 = src[0];
+          x1 = src[1];
         }
-        apply_group(a0, tsg, ev, od);
-        apply_group(a1, tsg, ev, od);
-        a0 = b0v;
-        a1 = b1v;
+      };
+      int k = tid;
+      fetch(k, a0, a1);
+      if (EC_PP) {   // ping-pong registers: no moves between units
+        while (k < nr) {
+          fetch(k + NT, b0v, b1v);
+          apply_group(a0, tsg, ev, od);
+          apply_group(a1, tsg, ev, od);
+          k += NT;
+          if (k >= nr) break;
+          fetch(k + NT, a0, a1);
+          apply_group(b0v, tsg, ev, od);
+          apply_group(b1v, tsg, ev, od);
+          k += NT;
+        }
+      } else {
+        for (; k < nr; k += NT) {
+          fetch(k + NT, b0v, b1v);
+          apply_group(a0, tsg, ev, od);
+          apply_group(a1, tsg, ev, od);
+          a0 = b0v;
+          a1 = b1v;
+        }
       }
       T.add_round(ev, od);   // <= 8 per unit, <= 8 units per thread per round: 8-bit fields
       ev = od = 0;
