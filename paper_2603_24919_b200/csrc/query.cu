@@ -1672,6 +1672,7 @@ struct TileRef {
   uint32_t cid;   // this lane's candidate id (valid if lane < m)
   int iq = 0;     // integer path: u8 rows and a u8-exact query
   int32_t xs = 0; // integer path: this lane's row sum of squares
+  int32_t qs = 0; // integer path: the query's sum of squares
 };
 
 __device__ __forceinline__ TileRef tile_ref(const int4 dsc, int lane, const uint32_t* __restrict__ cand) {
@@ -1708,7 +1709,7 @@ template <> struct RowFmt<__half> {   // 128 dims (256 B) per unit
 template <> struct RowFmt<uint8_t> {  // 128 dims (128 B) per unit, 8 lanes per row segment
   static constexpr int UD = 128, LPR = 8, PITCH = 144, WARPS = 20, CTAS = 1;
 };
-constexpr int AST = 2;                 // stages per warp (the id lookahead assumes 2)
+constexpr int AST = 2;                 // stages per warp (the id lookahead assumes 2; a power of 2)
 template <typename T>
 struct AStage {
   uint8_t rows[GR][RowFmt<T>::PITCH];  // pitch = 16 B mod 128: 16-byte row reads are conflict free
@@ -1779,33 +1780,47 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
   auto row_of = [&](const TileRef& r) {
     return reinterpret_cast<const uint8_t*>(X + (size_t)(lane < r.m ? r.cid : 0u) * d);
   };
-  // integer path (U8 rows, qok[q]): d2 = sum x^2 - 2 sum x q + sum q^2 in exact integers
+  // integer path (U8 rows, qok[q]): d2 = sum x^2 - 2 sum x q + sum q^2 in
+  // exact integers.  Loads are staged so none waits on another: descriptors
+  // two tiles ahead, candidate ids (and qok) one tile ahead, the row / query
+  // sums of squares when the tile starts issuing (its ids are resident then).
   auto ref_of = [&](const int4 dd) {
     TileRef r = tile_ref(dd, lane, cand);
-    if (U8 && qok) {
-      r.iq = r.m > 0 ? qok[r.q] : 0;
-      r.xs = r.iq && lane < r.m ? __ldg(xsq + r.cid) : 0;
-    }
+    if (U8 && qok) r.iq = r.m > 0 ? qok[r.q] : 0;
     return r;
   };
+  auto sums_of = [&](TileRef& r) {
+    if (U8 && r.iq) {
+      r.xs = lane < r.m ? __ldg(xsq + r.cid) : 0;
+      r.qs = __ldg(qsq + r.q);
+    }
+  };
   TileRef tcur = ref_of(dsc(0));                         // tile being issued
+  sums_of(tcur);
   TileRef tnext = ref_of(dsc(1));                        // its successor (ids in flight)
   int4 dpre = dsc(2);                                    // the one after
   int64_t tcur_i = 0;
   const uint8_t* rp = row_of(tcur);                      // my row of the issued tile
   TileRef tcomp = tcur;                                   // tile being computed
   const int r0 = lane / LPR, cl = lane % LPR;
+  int64_t iss_i = 0;   // (tile, segment) of the next unit to issue: units are issued in order
+  int iss_g = 0;
   auto issue = [&](int64_t u) {
-    const int64_t i = u / nsg;
-    const int g = (int)(u % nsg);
+    const int64_t i = iss_i;
+    const int g = iss_g;
+    if (++iss_g == nsg) {
+      iss_g = 0;
+      ++iss_i;
+    }
     if (i != tcur_i) {
       tcur = tnext;
       tcur_i = i;
+      sums_of(tcur);
       rp = row_of(tcur);
       tnext = ref_of(dpre);
       dpre = dsc(i + 2);
     }
-    AStage<T>& st = W.st[u % AST];
+    AStage<T>& st = W.st[(int)(u & (AST - 1))];
     const int s0 = g * UD;
     const int len = min(UD, d - s0);
     const int nch = (int)(len * sizeof(T)) / 16;          // 16-byte chunks per row segment (<= LPR)
@@ -1830,15 +1845,15 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
   }
   double a0 = 0.0, a1 = 0.0;
   uint32_t iacc = 0;   // integer path: sum of x * q
-  for (int64_t u = 0; u < U; ++u) {
-    const int64_t i = u / nsg;
-    const int g = (int)(u % nsg);
+  int64_t i = 0;       // (tile, segment) of unit u
+  int g = 0;
+  for (int64_t u = 0; u < U; ++u, (++g == nsg ? (g = 0, ++i) : 0)) {
     if (g == 0) tcomp = (i == tcur_i) ? tcur : tnext;     // ids of the tile computed now
     if (u + AST - 1 < U) issue(u + AST - 1);
     cp_async_commit();
     cp_async_wait<AST - 1>();
     __syncwarp();
-    const AStage<T>& st = W.st[u % AST];
+    const AStage<T>& st = W.st[(int)(u & (AST - 1))];
     const int s0 = g * UD;
     const int len = min(UD, d - s0);
     const bool last = g == nsg - 1;
@@ -1887,7 +1902,7 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
     if (last) {
       double v;
       if (U8 && tcomp.iq) {   // every step of the reference's fp64 sum is exact on these integers
-        v = (double)((int64_t)tcomp.xs - 2 * (int64_t)iacc + (int64_t)__ldg(qsq + tcomp.q));
+        v = (double)((int64_t)tcomp.xs - 2 * (int64_t)iacc + (int64_t)tcomp.qs);
         iacc = 0;
       } else {
         v = __dadd_rn(a0, a1);
