@@ -1,6 +1,9 @@
 """Summarise an ncu report into profiles/ (text + per-query DRAM traffic).
 
-    python tools/ncu_summary.py gpurun_out/prof_v10.ncu-rep --queries 2000 --tag r1_count
+    python tools/ncu_summary.py gpurun_out/prof_v10.ncu-rep --queries 2000 --tag r1_count [--config 2]
+
+--config N also records each kernel's DRAM bytes per query under "cfgN" in
+profiles/ncu_traffic.json (bench.py's roofline.traffic for that config).
 """
 import argparse
 import csv
@@ -33,6 +36,7 @@ def main():
     ap.add_argument("report")
     ap.add_argument("--queries", type=int, required=True)
     ap.add_argument("--tag", required=True)
+    ap.add_argument("--config", type=int, default=None)
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
@@ -55,13 +59,16 @@ def main():
         wb = float(vals["dram__bytes_write.sum"][0]) * UNIT.get(vals["dram__bytes_write.sum"][1], 1)
         out.append(f"- dram bytes per query    {(rb + wb) / a.queries:.1f} B")
         out.append("")
-        key = {"k_count_cluster": "k_count", "k_rerank_async": "k_rerank"}.get(name, name)
-        traffic[key] = {"dram_bytes_per_query": (rb + wb) / a.queries, "source": os.path.basename(a.report),
-                        "tag": a.tag}
+        key = {"k_count_cluster": "k_count", "k_count_enc": "k_count", "k_count_tma": "k_count",
+               "k_rerank_async": "k_rerank"}.get(name, name)
+        if a.config is not None:
+            traffic.setdefault(f"cfg{a.config}", {})[key] = {
+                "dram_bytes_per_query": (rb + wb) / a.queries, "source": os.path.basename(a.report), "tag": a.tag}
     with open(os.path.join(root, f"{a.tag}_ncu.md"), "w") as fh:
         fh.write("\n".join(out) + "\n")
-    with open(traffic_path, "w") as fh:
-        json.dump(traffic, fh, indent=1, sort_keys=True)
+    if a.config is not None:
+        with open(traffic_path, "w") as fh:
+            json.dump(traffic, fh, indent=1, sort_keys=True)
     print("\n".join(out))
 
 
