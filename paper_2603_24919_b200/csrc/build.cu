@@ -20,7 +20,6 @@
 #include <cstdlib>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "index.cuh"
 
@@ -1484,10 +1483,6 @@ __global__ void k_point_major(HalfView h, int mp, float* __restrict__ xp) {
   }
 }
 
-__global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
 
 // empty clusters (ascending): farthest point (first argmax of point_d2 with
 // already-taken points at -1) becomes the centroid and moves its label.
@@ -1554,37 +1549,171 @@ struct KMeansRun {
   int concurrent = 1;  // halves running at once: each k-means++ draw takes sms/concurrent CTAs
 };
 
-// CUB onesweep radix sort of the point records (values) by label (keys);
-// stable, so index order is kept inside every label.
-// (128-byte records exceed CUB's onesweep shared memory: MP = 32 sorts the
-// point indices instead and gathers the records, 128 B per point.)
-__global__ void k_gather_rec32(const PointRec<32>* __restrict__ in, const uint32_t* __restrict__ perm, int64_t n,
-                               PointRec<32>* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one float4 per thread
-  if (t >= n * 8) return;
-  const int64_t k = t >> 3;
-  const int q = (int)(t & 7);
-  reinterpret_cast<float4*>(out + k)[q] = __ldg(reinterpret_cast<const float4*>(in + perm[k]) + q);
+// ------------------------------------------------ stable counting sort
+// Stable sort of n items by a small key (< B <= 256 buckets), segmented into
+// independent segments of `seg` items (seg a multiple of the run length;
+// one segment for the Lloyd label sort, one per id chunk for the CSR).  A
+// warp owns a run of `run` consecutive items and handles them 32 at a time
+// in index order: __match_any_sync groups the lanes with equal keys, a
+// lane's rank among them is the popcount of the lower peers, the group's
+// lowest lane advances the warp's per-bucket cursor -- stable without any
+// cross-warp ordering.  Three launches per pass:
+//   k_ls_hist     per-run bucket counts, bh[b][run]
+//   k_ls_scan     one CTA per segment: bucket totals, bucket starts, and the
+//                 exclusive scan of each bucket's run counts -> item offsets
+//   k_ls_scatter  per-run cursors from bh, ranks by match_any, payload moves
+// With 2 N_s k-means halves in flight on their own streams, the narrow grids
+// (a warp per 4096 points) overlap across halves.
+constexpr int LS_WARPS = 4;
+constexpr int LS_SCAN_THREADS = 1024;
+
+struct LsLabelKey {   // key = label[i] (items in index order)
+  const int32_t* lab;
+  __device__ __forceinline__ uint32_t operator()(int64_t i, uint32_t) const { return (uint32_t)lab[i]; }
+};
+struct LsIdKey {      // key = label[id] (items carry point ids)
+  const int32_t* lab;
+  __device__ __forceinline__ uint32_t operator()(int64_t, uint32_t id) const { return (uint32_t)lab[id]; }
+};
+struct LsIota {       // payload id of item i = i
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const { return (uint32_t)i; }
+};
+struct LsIds {        // payload id of item i = ids[i]
+  const uint32_t* ids;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const { return ids[i]; }
+};
+struct LsIdOut {      // out[pos] = id
+  uint32_t* out;
+  __device__ __forceinline__ void operator()(int64_t pos, int64_t, uint32_t id) const { out[pos] = id; }
+};
+template <int MP>
+struct LsRecOut {     // out[pos] = record of point i
+  const PointRec<MP>* in;
+  PointRec<MP>* out;
+  __device__ __forceinline__ void operator()(int64_t pos, int64_t i, uint32_t) const {
+    const float4* s4 = reinterpret_cast<const float4*>(in + i);
+    float4* d4 = reinterpret_cast<float4*>(out + pos);
+#pragma unroll
+    for (int q = 0; q < MP / 4; ++q) d4[q] = __ldg(s4 + q);
+  }
+};
+
+template <class KeyF, class IdF>
+__global__ void __launch_bounds__(32 * LS_WARPS) k_ls_hist(KeyF key, IdF idf, int64_t n, int run, int64_t nruns,
+                                                           int B, uint32_t* __restrict__ bh,
+                                                           const int64_t* __restrict__ status) {
+  if (status && status[2]) return;   // k-means converged: nothing to sort
+  __shared__ uint32_t cnt_s[LS_WARPS][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * LS_WARPS + w;
+  if (r >= nruns) return;   // warp-private from here on
+  uint32_t* cnt = cnt_s[w];
+  for (int b = lane; b < B; b += 32) cnt[b] = 0;
+  __syncwarp();
+  const int64_t i0 = r * run, i1 = min(n, i0 + run);
+  for (int64_t base = i0; base < i1; base += 32) {
+    const int64_t i = base + lane;
+    const bool ok = i < i1;
+    const uint32_t k = ok ? key(i, idf(i)) : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (ok && lane == __ffs(peers) - 1) cnt[k] += __popc(peers);
+    __syncwarp();
+  }
+  for (int b = lane; b < B; b += 32) bh[(size_t)b * nruns + r] = cnt[b];
 }
 
-template <int MP>
-static int label_sort(void* tmp, size_t& tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out, const void* rec_in,
-                      void* rec_out, int64_t n, int bits, cudaStream_t st, const uint32_t* iota = nullptr,
-                      uint32_t* perm = nullptr) {
-  if constexpr (MP == 32) {
-    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, iota, perm, n, 0, bits, st));
-    if (tmp) {
-      k_gather_rec32<<<(unsigned)ceil_div(n * 8, 256), 256, 0, st>>>(static_cast<const PointRec<32>*>(rec_in), perm, n,
-                                                                     static_cast<PointRec<32>*>(rec_out));
-      TACO_LAUNCHED();
-    }
-    return TACO_OK;
-  } else {
-    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out,
-                                                    static_cast<const PointRec<MP>*>(rec_in),
-                                                    static_cast<PointRec<MP>*>(rec_out), n, 0, bits, st));
-    return TACO_OK;
+// one CTA per segment s (runs [s*rps, min(nruns, (s+1)*rps)), items from s*seg)
+__global__ void __launch_bounds__(LS_SCAN_THREADS) k_ls_scan(uint32_t* __restrict__ bh, int64_t nruns, int rps,
+                                                             int B, int64_t seg, const int64_t* __restrict__ status) {
+  if (status && status[2]) return;
+  __shared__ uint32_t tot[256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = LS_SCAN_THREADS / 32;
+  const int64_t s0 = blockIdx.x;
+  const int64_t r0 = s0 * rps, r1 = min(nruns, r0 + rps);
+  for (int b = w; b < B; b += nw) {
+    uint32_t v = 0;
+    for (int64_t r = r0 + lane; r < r1; r += 32) v += bh[(size_t)b * nruns + r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) tot[b] = v;
   }
+  __syncthreads();
+  for (int b = w; b < B; b += nw) {
+    uint32_t st = 0;   // items of this segment in buckets < b
+    for (int b2 = lane; b2 < b; b2 += 32) st += tot[b2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) st += __shfl_xor_sync(0xffffffffu, st, o);
+    int64_t carry = s0 * seg + st;
+    for (int64_t rb = r0; rb < r1; rb += 32) {
+      const int64_t r = rb + lane;
+      const uint32_t v = r < r1 ? bh[(size_t)b * nruns + r] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (r < r1) bh[(size_t)b * nruns + r] = (uint32_t)(carry + x - v);
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+}
+
+template <class KeyF, class IdF, class OutF>
+__global__ void __launch_bounds__(32 * LS_WARPS) k_ls_scatter(KeyF key, IdF idf, OutF out, int64_t n, int run,
+                                                              int64_t nruns, int B, const uint32_t* __restrict__ bh,
+                                                              const int64_t* __restrict__ status) {
+  if (status && status[2]) return;
+  __shared__ uint32_t cur_s[LS_WARPS][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * LS_WARPS + w;
+  if (r >= nruns) return;
+  uint32_t* cur = cur_s[w];
+  for (int b = lane; b < B; b += 32) cur[b] = bh[(size_t)b * nruns + r];
+  __syncwarp();
+  const int64_t i0 = r * run, i1 = min(n, i0 + run);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = i0; base < i1; base += 32) {
+    const int64_t i = base + lane;
+    const bool ok = i < i1;
+    const uint32_t id = ok ? idf(i) : 0u;
+    const uint32_t k = ok ? key(i, id) : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const uint32_t pos = ok ? cur[k] + __popc(peers & lt) : 0u;
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) cur[k] += __popc(peers);
+    __syncwarp();
+    if (ok) out((int64_t)pos, i, id);
+  }
+}
+
+// one stable counting-sort pass: hist, scan, scatter (bh: B * nruns u32)
+template <class KeyF, class IdF, class OutF>
+static int ls_pass(KeyF key, IdF idf, OutF out, int64_t n, int B, int run, int64_t seg, uint32_t* bh,
+                   const int64_t* status, cudaStream_t st) {
+  const int64_t nruns = ceil_div(n, run);
+  const int rps = (int)(seg / run);
+  const unsigned g = (unsigned)ceil_div(nruns, LS_WARPS);
+  k_ls_hist<<<g, 32 * LS_WARPS, 0, st>>>(key, idf, n, run, nruns, B, bh, status);
+  TACO_LAUNCHED();
+  k_ls_scan<<<(unsigned)ceil_div(nruns, rps), LS_SCAN_THREADS, 0, st>>>(bh, nruns, rps, B, seg, status);
+  TACO_LAUNCHED();
+  k_ls_scatter<<<g, 32 * LS_WARPS, 0, st>>>(key, idf, out, n, run, nruns, B, bh, status);
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
+constexpr int LS_LRUN = 4096;   // points per warp in the Lloyd label sort
+static size_t label_sort_bytes(int64_t n, int k) { return sizeof(uint32_t) * (size_t)k * ceil_div(n, LS_LRUN); }
+
+// Lloyd label sort: the point records (xp, index order) by new label into xs,
+// stable, so every cluster is one contiguous run in index order
+template <int MP>
+static int label_sort(const int32_t* newlab, const void* rec_in, void* rec_out, int64_t n, int k, uint32_t* bh,
+                      const int64_t* status, cudaStream_t st) {
+  return ls_pass(LsLabelKey{newlab}, LsIota{},
+                 LsRecOut<MP>{static_cast<const PointRec<MP>*>(rec_in), static_cast<PointRec<MP>*>(rec_out)}, n, k,
+                 LS_LRUN, ceil_div(n, LS_LRUN) * LS_LRUN, bh, status, st);
 }
 
 // All allocations of one k-means run (no stream work): done for every half
@@ -1602,12 +1731,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   const int64_t nbp = ceil_div(n, PP_BLOCK);
   const int64_t nba = ceil_div(n, (int64_t)AS_THREADS);
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
-  int lbits = 1;
-  while ((1 << lbits) < k) ++lbits;
-  size_t cub_bytes = 0;
-  if (mp == 8) TACO_TRY(label_sort<8>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
-  else if (mp == 16) TACO_TRY(label_sort<16>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
-  else TACO_TRY(label_sort<32>(nullptr, cub_bytes, nullptr, nullptr, nullptr, nullptr, n, lbits, st));
+  const size_t sort_bytes = label_sort_bytes(n, k);
   // host side of the exact replay: numpy's pairwise leaves and combine tree for n
   std::vector<char> blob;
   if (s.leaves_n != n || s.leaf_blob.empty()) {
@@ -1637,8 +1761,7 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
       {&s.picks, 8 * (size_t)k}, {&s.uni, 8 * (size_t)std::max(k, 1)}, {&s.forced, 8 * (size_t)std::max(k, 1)},
       {&s.status, 8 * 16}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
       {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)std::max<int64_t>(nba, ceil_div(n, TC_THREADS))},   // fp64 or tensor-core assign partials
-      {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.cubtmp, std::max<size_t>(cub_bytes, 16)},
-      {&s.perm, mp == 32 ? 4 * (size_t)n : 0}, {&s.iota, mp == 32 ? 4 * (size_t)n : 0},
+      {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.sorttmp, std::max<size_t>(sort_bytes, 16)},
       {&s.leaves, s.leaf_blob.size()}, {&s.pbuf, 8 * (size_t)std::max<int64_t>(n, s.nleaves)},
       {&s.cbuf, 8 * (size_t)std::max<int64_t>(n, 2 * s.nleaves)}};
   size_t total = 0;
@@ -1650,10 +1773,6 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
       c.b->view_of(base, c.bytes);
       base += (c.bytes + 255) & ~(size_t)255;
     }
-  }
-  if (mp == 32) {
-    k_iota<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(s.iota.as<uint32_t>(), n);
-    TACO_LAUNCHED();
   }
   TACO_CHECK_CUDA(cudaMemcpyAsync(s.leaves.p, s.leaf_blob.data(), s.leaf_blob.size(), cudaMemcpyHostToDevice, st));
   const size_t ash = sizeof(double) * ((size_t)k * (m <= 8 ? 8 : m <= 16 ? 16 : 32) + k);
@@ -1708,8 +1827,6 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
   const int64_t nbx = ceil_div(n, 256);
   const int64_t nbp = ceil_div(n, PP_BLOCK);
   const int64_t nba = ceil_div(n, (int64_t)AS_THREADS);
-  int lbits = 1;
-  while ((1 << lbits) < k) ++lbits;
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
   unsigned long long* cnt = s.ctl.as<unsigned long long>();
   if (step == 0) {
@@ -1780,26 +1897,26 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
     k_lloyd_ctl<<<1, 1024, 0, st>>>(s.hsum.as<double>(), nb_h, it, s.status.as<int64_t>(), r.history,
                                     r.n_iter);
     TACO_LAUNCHED();
-    // stable radix sort of the point records by label (index order inside a label)
-    size_t cb = s.cubtmp.bytes;
-    const uint32_t* nl = reinterpret_cast<const uint32_t*>(s.newlab.p);
+    // stable counting sort of the point records by label (index order inside a label)
+    const int32_t* nl = s.newlab.as<int32_t>();
+    uint32_t* bh = s.sorttmp.as<uint32_t>();
+    const int64_t* stt = s.status.as<int64_t>();
     if (mp == 8) {
-      TACO_TRY(label_sort<8>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st));
+      TACO_TRY(label_sort<8>(nl, s.xp.p, s.xs.p, n, k, bh, stt, st));
       k_cluster_sums<8><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<8>>(), s.status.as<int64_t>(), cc,
                                                               s.newlab.as<int32_t>(), r.labels, s.C64.as<double>());
     } else if (mp == 16) {
-      TACO_TRY(label_sort<16>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st));
+      TACO_TRY(label_sort<16>(nl, s.xp.p, s.xs.p, n, k, bh, stt, st));
       k_cluster_sums<16><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<16>>(), s.status.as<int64_t>(),
                                                                cc, s.newlab.as<int32_t>(), r.labels,
                                                                s.C64.as<double>());
     } else {
-      TACO_TRY(label_sort<32>(s.cubtmp.p, cb, nl, s.keys2.as<uint32_t>(), s.xp.p, s.xs.p, n, lbits, st,
-                              s.iota.as<uint32_t>(), s.perm.as<uint32_t>()));
+      TACO_TRY(label_sort<32>(nl, s.xp.p, s.xs.p, n, k, bh, stt, st));
       k_cluster_sums<32><<<(unsigned)k, CS_THREADS, css, st>>>(h, s.xs.as<PointRec<32>>(), s.status.as<int64_t>(),
                                                                cc, s.newlab.as<int32_t>(), r.labels,
                                                                s.C64.as<double>());
     }
-    count_launch(3);
+    count_launch(1);
     TACO_CHECK_CUDA(cudaGetLastError());
     k_reseed<<<1, 1024, 0, st>>>(h, s.status.as<int64_t>(), cc, s.pd.as<double>(),
                                  r.labels, s.C64.as<double>());
@@ -1875,13 +1992,6 @@ __global__ void k_cell_sizes(const uint32_t* __restrict__ chist, int K2, int64_t
 // A stable radix sort of ascending ids by this key is the (chunk, cell, id)
 // order the counting kernels read (imi.py:72-81 lexsort((arange, l2, l1)),
 // chunk-major).
-__global__ void k_cell_keys(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2, int64_t n,
-                            int kp, int64_t chunk, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  keys[i] = (uint32_t)((i / chunk) * kp * kp + l1[i] * kp + l2[i]);
-  vals[i] = (uint32_t)i;
-}
 
 }  // namespace taco
 
@@ -2159,7 +2269,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
   for (auto& bs : idx->bs) {
     DevBuf* sb[] = {&bs.xsq, &bs.best, &bs.bsum, &bs.picks, &bs.uni, &bs.forced, &bs.status, &bs.C64, &bs.csq,
                     &bs.newlab, &bs.pd, &bs.changed, &bs.perm, &bs.lhist, &bs.loff, &bs.ctl, &bs.hsum, &bs.draws,
-                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.cubtmp, &bs.xp, &bs.xs, &bs.arena};
+                    &bs.leaves, &bs.pbuf, &bs.cbuf, &bs.iota, &bs.keys2, &bs.sorttmp, &bs.xp, &bs.xs, &bs.arena};
     for (auto* b : sb) b->release();
     bs.leaves_n = -1;
   }
@@ -2179,18 +2289,14 @@ int taco_build_cells(taco_index* idx) {
   TACO_TRY(idx->ids.ensure(sizeof(uint32_t) * (size_t)n * idx->n_sub));
   TACO_TRY(idx->offs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
   TACO_TRY(idx->gsize.ensure(sizeof(int64_t) * (size_t)K2 * idx->n_sub));
-  DevBuf chist, keys, keys2, vals, tmp;
+  // (chunk, cell, id) order = inside every id chunk (a segment: chunk is a
+  // multiple of the run), a stable sort by l2 then a stable sort by l1
+  constexpr int CRUN = 1024;
+  DevBuf chist, ids1, bh;
   TACO_TRY(chist.ensure(sizeof(uint32_t) * (size_t)nc * K2));
-  TACO_TRY(keys.ensure(sizeof(uint32_t) * (size_t)n));
-  TACO_TRY(keys2.ensure(sizeof(uint32_t) * (size_t)n));
-  TACO_TRY(vals.ensure(sizeof(uint32_t) * (size_t)n));
-  int bits = 1;
-  while (bits < 32 && ((uint64_t)1 << bits) < (uint64_t)nc * K2) ++bits;
-  size_t tmp_bytes = 0;
-  TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                                  vals.as<uint32_t>(), idx->ids.as<uint32_t>(), (int64_t)n, 0,
-                                                  bits, st));
-  TACO_TRY(tmp.ensure(std::max<size_t>(tmp_bytes, 16)));
+  TACO_TRY(ids1.ensure(sizeof(uint32_t) * (size_t)n));
+  TACO_TRY(bh.ensure(sizeof(uint32_t) * (size_t)kp * ceil_div(n, CRUN)));
+  if (idx->chunk % CRUN) TACO_FAIL(TACO_ERR_STATE, "id chunk %lld is not a multiple of %d", (long long)idx->chunk, CRUN);
   for (int j = 0; j < idx->n_sub; ++j) {
     const int32_t* l1 = idx->labels.as<int32_t>() + (size_t)(2 * j) * n;
     const int32_t* l2 = idx->labels.as<int32_t>() + (size_t)(2 * j + 1) * n;
@@ -2205,18 +2311,15 @@ int taco_build_cells(taco_index* idx) {
                                                                idx->gsize.as<int64_t>() + (size_t)j * K2);
       TACO_LAUNCHED();
     }
-    k_cell_keys<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(l1, l2, n, kp, idx->chunk, keys.as<uint32_t>(),
-                                                            vals.as<uint32_t>());
-    TACO_LAUNCHED();
-    size_t tb = tmp.bytes;
-    TACO_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                                    vals.as<uint32_t>(), idx->ids.as<uint32_t>() + (size_t)j * n,
-                                                    (int64_t)n, 0, bits, st));
-    count_launch(bits <= 8 ? 2 : 1 + (bits + 7) / 8);
+    TACO_TRY(ls_pass(LsLabelKey{l2}, LsIota{}, LsIdOut{ids1.as<uint32_t>()}, n, kp, CRUN, idx->chunk,
+                     bh.as<uint32_t>(), nullptr, st));
+    TACO_TRY(ls_pass(LsIdKey{l1}, LsIds{ids1.as<uint32_t>()}, LsIdOut{idx->ids.as<uint32_t>() + (size_t)j * n}, n,
+                     kp, CRUN, idx->chunk, bh.as<uint32_t>(), nullptr, st));
   }
   cudaError_t e = cudaStreamSynchronize(st);
   chist.release();
-  keys.release(); keys2.release(); vals.release(); tmp.release();
+  ids1.release();
+  bh.release();
   if (e != cudaSuccess) TACO_FAIL(TACO_ERR_CUDA, "%s", cudaGetErrorString(e));
   idx->has_cells = true;
   if (idx->n_global == idx->n) idx->has_gsize = true;
@@ -2296,7 +2399,7 @@ int taco_kmeans(int device, const float* X_h, int64_t n, int32_t m, int32_t k, i
   X.release(); lab.release(); hist.release(); nit.release(); cent.release();
   DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64, &s.csq,
                   &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl, &s.hsum, &s.draws,
-                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs, &s.arena};
+                  &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.sorttmp, &s.xp, &s.xs, &s.arena};
   for (auto* b : sb) b->release();
   return rc;
 }

@@ -262,7 +262,7 @@ int taco_index_destroy(taco_index* idx) {
   for (auto& s : idx->bs) {
     DevBuf* sb[] = {&s.xsq, &s.best, &s.bsum, &s.picks, &s.uni, &s.forced, &s.status, &s.C64,
                     &s.csq, &s.newlab, &s.pd, &s.changed, &s.perm, &s.lhist, &s.loff, &s.ctl,
-                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.cubtmp, &s.xp, &s.xs, &s.arena};
+                    &s.hsum, &s.draws, &s.leaves, &s.pbuf, &s.cbuf, &s.iota, &s.keys2, &s.sorttmp, &s.xp, &s.xs, &s.arena};
     for (auto* b : sb) b->release();
   }
   for (auto st : idx->half_streams) cudaStreamDestroy(st);

@@ -56,7 +56,7 @@ struct QueryTile {
 
 struct BuildScratch {
   DevBuf xsq, best, bsum, picks, uni, forced, status, C64, csq, newlab, pd, changed, perm, lhist,
-      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, cubtmp, xp, xs, arena;
+      loff, ctl, hsum, draws, leaves, pbuf, cbuf, iota, keys2, sorttmp, xp, xs, arena;
   std::vector<char> leaf_blob;   // host copy of the pairwise leaves + combine tree (exact replay)
   int64_t nleaves = 0, leaves_n = -1;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // TACO_DEBUG_TIMING
