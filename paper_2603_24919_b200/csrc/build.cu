@@ -1563,7 +1563,7 @@ struct KMeansRun {
 //                 exclusive scan of each bucket's run counts -> item offsets
 //   k_ls_scatter  per-run cursors from bh, ranks by match_any, payload moves
 // With 2 N_s k-means halves in flight on their own streams, the narrow grids
-// (a warp per 4096 points) overlap across halves.
+// (a warp per 2048 points) overlap across halves.
 constexpr int LS_WARPS = 4;
 constexpr int LS_SCAN_THREADS = 1024;
 
@@ -1611,13 +1611,20 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_ls_hist(KeyF key, IdF idf, in
   for (int b = lane; b < B; b += 32) cnt[b] = 0;
   __syncwarp();
   const int64_t i0 = r * run, i1 = min(n, i0 + run);
-  for (int64_t base = i0; base < i1; base += 32) {
-    const int64_t i = base + lane;
-    const bool ok = i < i1;
-    const uint32_t k = ok ? key(i, idf(i)) : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    if (ok && lane == __ffs(peers) - 1) cnt[k] += __popc(peers);
-    __syncwarp();
+  constexpr int U = 8;   // rounds whose keys are loaded together
+  for (int64_t base = i0; base < i1; base += 32 * U) {
+    uint32_t k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      k[u] = i < i1 ? key(i, idf(i)) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned peers = __match_any_sync(0xffffffffu, k[u]);
+      if (k[u] != 0xFFFFFFFFu && lane == __ffs(peers) - 1) cnt[k[u]] += __popc(peers);
+      __syncwarp();
+    }
   }
   for (int b = lane; b < B; b += 32) bh[(size_t)b * nruns + r] = cnt[b];
 }
@@ -1673,17 +1680,25 @@ __global__ void __launch_bounds__(32 * LS_WARPS) k_ls_scatter(KeyF key, IdF idf,
   __syncwarp();
   const int64_t i0 = r * run, i1 = min(n, i0 + run);
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = i0; base < i1; base += 32) {
-    const int64_t i = base + lane;
-    const bool ok = i < i1;
-    const uint32_t id = ok ? idf(i) : 0u;
-    const uint32_t k = ok ? key(i, id) : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    const uint32_t pos = ok ? cur[k] + __popc(peers & lt) : 0u;
-    __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) cur[k] += __popc(peers);
-    __syncwarp();
-    if (ok) out((int64_t)pos, i, id);
+  constexpr int U = 4;   // rounds whose keys (and ids) are loaded together
+  for (int64_t base = i0; base < i1; base += 32 * U) {
+    uint32_t id[U], k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      id[u] = i < i1 ? idf(i) : 0u;
+      k[u] = i < i1 ? key(i, id[u]) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = k[u] != 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, k[u]);
+      const uint32_t pos = ok ? cur[k[u]] + __popc(peers & lt) : 0u;
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) cur[k[u]] += __popc(peers);
+      __syncwarp();
+      if (ok) out((int64_t)pos, base + u * 32 + lane, id[u]);
+    }
   }
 }
 
@@ -1703,7 +1718,7 @@ static int ls_pass(KeyF key, IdF idf, OutF out, int64_t n, int B, int run, int64
   return TACO_OK;
 }
 
-constexpr int LS_LRUN = 4096;   // points per warp in the Lloyd label sort
+constexpr int LS_LRUN = 2048;   // points per warp in the Lloyd label sort
 static size_t label_sort_bytes(int64_t n, int k) { return sizeof(uint32_t) * (size_t)k * ceil_div(n, LS_LRUN); }
 
 // Lloyd label sort: the point records (xp, index order) by new label into xs,

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 #include <condition_variable>
 #include <functional>
@@ -440,17 +441,25 @@ int upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st,
   const char* s = static_cast<const char*>(src);
   char* d = static_cast<char*>(dst);
   CopyPool& pool = CopyPool::get();
+  static const bool dbg = getenv("TACO_DEBUG_UPLOAD") != nullptr;
+  double t_wait = 0.0, t_copy = 0.0;
   for (size_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
     const int b = (int)(i % kStages);
     const size_t len = std::min(kStageBytes, bytes - off);
+    const auto ta = std::chrono::steady_clock::now();
     TACO_CHECK_CUDA(cudaEventSynchronize(g_stage_ev[b]));   // buffer b drained
+    const auto tb = std::chrono::steady_clock::now();
     char* stg = g_stage[b];
     pool.copy(stg, s + off, len);
+    const auto tc = std::chrono::steady_clock::now();
+    t_wait += std::chrono::duration<double, std::milli>(tb - ta).count();
+    t_copy += std::chrono::duration<double, std::milli>(tc - tb).count();
     TACO_CHECK_CUDA(cudaMemcpyAsync(d + off, stg, len, cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaEventRecord(g_stage_ev[b], st));
     if (on_chunk) TACO_TRY(on_chunk(off + len, g_stage_ev[b]));   // bytes [0, off + len) have landed once ev fires
   }
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (dbg) fprintf(stderr, "[taco] upload: host copies %.2f ms, waits for a drained buffer %.2f ms\n", t_copy, t_wait);
   return TACO_OK;
 }
 }  // namespace taco
@@ -477,10 +486,21 @@ int taco_index_set_data(taco_index* idx, const float* X_h) {
     rows_done = rows;
     return TACO_OK;
   };
+  static const bool dbg = getenv("TACO_DEBUG_UPLOAD") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   TACO_TRY(upload_h2d(idx->X.p, X_h, bytes, idx->stream, on_chunk));
+  const auto t1 = std::chrono::steady_clock::now();
   idx->mean_ready = rows_done == idx->n;
   idx->has_X = true;
-  return narrow_rows(idx);
+  const int rc = narrow_rows(idx);
+  if (dbg) {
+    cudaStreamSynchronize(idx->aux);
+    const auto t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[taco] set_data: upload %.2f ms, narrow rows %.2f ms (%zu MB)\n",
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(t2 - t1).count(), bytes >> 20);
+  }
+  return rc;
 }
 
 int32_t taco_index_row_format(const taco_index* idx) {
