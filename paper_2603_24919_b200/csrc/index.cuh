@@ -73,6 +73,7 @@ struct taco_index {
   taco::DevBuf X, mean, M, T, cb1, cb2, labels, hist, niter, ids, offs, gsize;
   taco::DevBuf cenc, coffs;   // encoded, group-padded CSR of the TMA count (build_count_csr)
   size_t cstride = 0;         // entries per subspace in cenc
+  int cunit = 8;              // entries per cenc unit (8 cluster mode, 4 global mode)
   bool has_ccsr = false;
   taco::DevBuf Xn;            // lossless narrow copy of X for the rerank (xfmt != TACO_ROWS_F32)
   taco::DevBuf Xsq;           // u8 rows: int32 sum of squares per row (integer rerank path)

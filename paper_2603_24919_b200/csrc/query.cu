@@ -824,7 +824,6 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 #define EC_RELAX 1   // relaxed cluster arrive after the histogram gather
 #endif
 constexpr uint32_t EC_SENT = 32u;
-constexpr int EC_U = 8;                  // entries per unit (32 bytes, one sector)
 constexpr uint32_t EC_GMASK = 0x1FFFFFFFu;   // unit offset bits of coffs (top 3 bits: padding count)
 
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t s) {
@@ -864,6 +863,9 @@ struct EncSmem {
   int lh[256];
 };
 
+template <int NT>
+__device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S);
+
 // tallies -> level histogram, cluster exchange, Alg. 5, compaction (the
 // k_count_cluster epilogue for NT threads).  Thread 0 reserves the CTA's
 // candidate segment with one global atomic; while it is in flight the CTA
@@ -875,39 +877,10 @@ __device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_su
                              uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
                              int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
                              int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int rank = (int)cluster.block_rank();
   const int csz = (int)cluster.num_blocks();
-  // #score >= l = #increments leaving l - 1.  When every lane's packed 16-bit
-  // tallies are < 8192 they are summed packed over 8-lane groups (no carry
-  // between fields) and lanes 0, 8, 16, 24 add their levels; otherwise per
-  // level over the whole warp
-  uint64_t a0 = T.a0, a1 = T.a1;
-  constexpr uint64_t HI3 = 0xE000E000E000E000ull;
-  if (!__any_sync(0xffffffffu, ((a0 | a1) & HI3) != 0)) {
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-    }
-    if ((lane & 7) == 0)
-      for (int l = 1; l <= n_sub; ++l) {
-        const uint64_t w = ((l - 1) & 1) ? a1 : a0;
-        const int x = (int)((w >> (16 * ((l - 1) >> 1))) & 0xFFFFull);
-        if (x) atomicAdd(&S.ge[l], x);
-      }
-  } else {
-    for (int l = 1; l <= n_sub; ++l) {
-      int x = T.level(l - 1, true);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0 && x) atomicAdd(&S.ge[l], x);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) S.ge[1] -= S.pads;   // padding entries counted as leaving level 0
-  __syncthreads();
-  chunk_levels(table, valid, n_sub, S);
+  enc_levels<NT>(T, table, valid, n_sub, S);
   cluster.sync();   // every CTA's level histogram is final
   for (int l = tid; l <= n_sub; l += NT) {
     int h = 0;
@@ -989,26 +962,20 @@ struct EcCfg {
   static constexpr int GC = 8 * NT;               // staged units per round: 8 per thread (8-bit tallies)
 };
 
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_count_enc(
-    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
-    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
-    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
-    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
-    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
-  constexpr int PER = EcCfg<NT>::PER, GC = EcCfg<NT>::GC;
-  extern __shared__ __align__(16) uint8_t table[];
-  __shared__ EncSmem<NT> S;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int64_t q = blockIdx.y;
-  const int64_t c = cluster.block_rank();
+// The counting phase of the encoded kernels for (query q, chunk c): table
+// zeroed and filled, tallies in T, padding entries counted in S.pads.  UW =
+// 16-byte words per unit (2: cluster mode's 8-entry units, 1: global mode's
+// 4-entry units).  Staging: gaddr[EcCfg<NT>::GC].
+template <int NT, int UW>
+__device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop,
+                                                int cap, const uint32_t* __restrict__ cenc, size_t cstride,
+                                                const uint32_t* __restrict__ coffs, int n_sub, int K2, int64_t nchunks,
+                                                int64_t q, int64_t c, int tbytes, uint8_t* table, uint32_t* gaddr,
+                                                EncSmem<NT>& S, Tally& T) {
+  constexpr int PER = EcCfg<NT>::PER, GC = EcCfg<NT>::GC, EU = 4 * UW;
   const int tid = threadIdx.x;
-  const int64_t base = c * chunk;
-  const int valid = (int)max((int64_t)0, min(chunk, n - base));
-  const int tbytes = (int)(chunk / 2);
-  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
   const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
-  const uint32_t jstride = (uint32_t)(cstride / EC_U);              // units per subspace
+  const uint32_t jstride = (uint32_t)(cstride / EU);                // units per subspace
   const size_t offs_len = (size_t)nchunks * K2 + 1;
   uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < tbytes / 16; i += NT) t4[i] = make_uint4(0, 0, 0, 0);
@@ -1031,7 +998,6 @@ __global__ void __launch_bounds__(NT, MINB) k_count_enc(
   for (int jj = 0; jj < 8; ++jj) jp[jj] = S.jpref[jj];
   const uint32_t tsg = smem_u32(table);
   uint32_t ev = 0, od = 0;
-  Tally T;
   int pads = 0;
   for (int b0 = 0; b0 < P_all; b0 += NT * PER) {
     uint32_t ga[PER], ng[PER];   // unit index of the slice start, unit count
@@ -1066,47 +1032,130 @@ __global__ void __launch_bounds__(NT, MINB) k_count_enc(
       }
       __syncthreads();
       const int nr = (int)(r1 - r0);
-      // one unit (2 x 16 B) of lookahead: unit k + NT loads while unit k is applied
+      // one unit of lookahead: unit k + NT loads while unit k is applied
       uint4 a0, a1, b0v, b1v;
       auto fetch = [&](int kk, uint4& x0, uint4& x1) {
         if (kk < nr) {
-          const uint4* src = E4 + 2 * (size_t)gaddr[kk];
+          const uint4* src = E4 + UW * (size_t)gaddr[kk];
           x0 = src[0];
-          x1 = src[1];
+          if (UW == 2) x1 = src[1];
         }
+      };
+      auto apply = [&](const uint4& x0, const uint4& x1) {
+        apply_group(x0, tsg, ev, od);
+        if (UW == 2) apply_group(x1, tsg, ev, od);
       };
       int k = tid;
       fetch(k, a0, a1);
       if (EC_PP) {   // ping-pong registers: no moves between units
         while (k < nr) {
           fetch(k + NT, b0v, b1v);
-          apply_group(a0, tsg, ev, od);
-          apply_group(a1, tsg, ev, od);
+          apply(a0, a1);
           k += NT;
           if (k >= nr) break;
           fetch(k + NT, a0, a1);
-          apply_group(b0v, tsg, ev, od);
-          apply_group(b1v, tsg, ev, od);
+          apply(b0v, b1v);
           k += NT;
         }
       } else {
         for (; k < nr; k += NT) {
           fetch(k + NT, b0v, b1v);
-          apply_group(a0, tsg, ev, od);
-          apply_group(a1, tsg, ev, od);
+          apply(a0, a1);
           a0 = b0v;
           a1 = b1v;
         }
       }
-      T.add_round(ev, od);   // <= 8 per unit, <= 8 units per thread per round: 8-bit fields
+      T.add_round(ev, od);   // <= 4 UW per unit, <= 8 units per thread per round: 8-bit fields
       ev = od = 0;
       __syncthreads();
     }
   }
   if (pads) atomicAdd(&S.pads, pads);
   __syncthreads();
+}
+
+// tallies -> the chunk's level histogram S.ge / S.lh (packed reduction as in
+// enc_epilogue; padding entries taken off level 0)
+template <int NT>
+__device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint64_t a0 = T.a0, a1 = T.a1;
+  constexpr uint64_t HI3 = 0xE000E000E000E000ull;
+  if (!__any_sync(0xffffffffu, ((a0 | a1) & HI3) != 0)) {
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if ((lane & 7) == 0)
+      for (int l = 1; l <= n_sub; ++l) {
+        const uint64_t w = ((l - 1) & 1) ? a1 : a0;
+        const int x = (int)((w >> (16 * ((l - 1) >> 1))) & 0xFFFFull);
+        if (x) atomicAdd(&S.ge[l], x);
+      }
+  } else {
+    for (int l = 1; l <= n_sub; ++l) {
+      int x = T.level(l - 1, true);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0 && x) atomicAdd(&S.ge[l], x);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) S.ge[1] -= S.pads;   // padding entries counted as leaving level 0
+  __syncthreads();
+  chunk_levels(table, valid, n_sub, S);
+}
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_count_enc(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
+    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<NT> S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t q = blockIdx.y;
+  const int64_t c = cluster.block_rank();
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  const int tbytes = (int)(chunk / 2);
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
+  Tally T;
+  enc_count_phase<NT, 2>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S,
+                         T);
   enc_epilogue<NT>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
-                   lvl, gaddr, GC);
+                   lvl, gaddr, EcCfg<NT>::GC);
+}
+
+// Global mode, sweep 1 on the encoded CSR (4-entry units): per (chunk,
+// query) CTA the chunk's level histogram -> part, and its score >= 2 ids as
+// packed records (k_count CNT_HIST's contract; the emit sweep and the
+// recount are unchanged).
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_count_genc(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, uint8_t* __restrict__ scores, int32_t* __restrict__ part) {
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<NT> S;
+  const int64_t c = blockIdx.x, q = blockIdx.y;
+  const int64_t base = c * chunk;
+  const int valid = (int)min(chunk, n - base);
+  const int tbytes = (int)(chunk / 2);
+  const int rec_cap = tbytes / 4;   // records per spilled (query, chunk) slot
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);
+  Tally T;
+  enc_count_phase<NT, 1>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S, T);
+  if (threadIdx.x == 0) S.fill = 0;
+  enc_levels<NT>(T, table, valid, n_sub, S);   // ends with a barrier
+  if (scores && n_sub >= 2 && valid - S.lh[0] - S.lh[1] <= rec_cap)
+    compact_records<NT, true>(table, valid, reinterpret_cast<uint32_t*>(scores + ((size_t)q * nchunks + c) * tbytes),
+                              &S.fill);
+  int32_t* pp = part + ((size_t)q * nchunks + c) * (n_sub + 1);
+  for (int l = threadIdx.x; l <= n_sub; l += NT) pp[l] = S.lh[l];
 }
 
 constexpr int TC_CW = 16;
@@ -1257,12 +1306,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
 // of those sums, then per-slice offsets + the encoded fill.
 constexpr int CC_NT = 1024;
 __global__ void __launch_bounds__(CC_NT) k_ccsr_sums(const uint32_t* __restrict__ offs, size_t offs_len,
-                                                    int64_t nsl, uint32_t* __restrict__ bsum) {
+                                                    int64_t nsl, uint32_t* __restrict__ bsum, int U) {
   __shared__ uint32_t wtot[CC_NT / 32];
   const int j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
   const uint32_t* O = offs + (size_t)j * offs_len;
-  const uint32_t g = i < nsl ? (O[i + 1] - O[i] + (EC_U - 1)) / EC_U : 0u;
+  const uint32_t g = i < nsl ? (O[i + 1] - O[i] + (U - 1)) / U : 0u;
   uint32_t tot;
   block_excl_scan<CC_NT>(g, wtot, tot);
   if (threadIdx.x == 0) bsum[(size_t)j * gridDim.x + blockIdx.x] = tot;
@@ -1284,7 +1333,7 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
                                                     const uint32_t* __restrict__ offs, size_t offs_len,
                                                     int64_t nsl, int K2, int64_t n, int64_t chunk,
                                                     const uint32_t* __restrict__ bsum, uint32_t* __restrict__ coffs,
-                                                    uint32_t* __restrict__ cenc, size_t cstride) {
+                                                    uint32_t* __restrict__ cenc, size_t cstride, int U) {
   __shared__ uint32_t wtot[CC_NT / 32];
   const int j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
@@ -1294,17 +1343,17 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
     s0 = O[i];
     len = O[i + 1] - s0;
   }
-  const uint32_t g = (len + (EC_U - 1)) / EC_U;
+  const uint32_t g = (len + (U - 1)) / U;
   uint32_t tot;
   const uint32_t g0 = bsum[(size_t)j * gridDim.x + blockIdx.x] + block_excl_scan<CC_NT>(g, wtot, tot);
   uint32_t* C = coffs + (size_t)j * offs_len;
   if (i < nsl) {   // coffs is zeroed first: the padding bits of slice i land in C[i + 1]
     atomicOr(&C[i], g0);
-    atomicOr(&C[i + 1], ((EC_U * g - len) << 29) | (i + 1 == nsl ? g0 + g : 0u));
+    atomicOr(&C[i + 1], ((U * g - len) << 29) | (i + 1 == nsl ? g0 + g : 0u));
     const int64_t cbase = (i / K2) * chunk;
     const uint32_t* I = ids + (size_t)j * n + s0;
-    uint32_t* E = cenc + (size_t)j * cstride + EC_U * (size_t)g0;
-    for (uint32_t e = 0; e < EC_U * g; ++e) {
+    uint32_t* E = cenc + (size_t)j * cstride + U * (size_t)g0;
+    for (uint32_t e = 0; e < U * g; ++e) {
       uint32_t v = EC_SENT;
       if (e < len) {
         const uint32_t p = (uint32_t)(I[e] - cbase);
@@ -2301,27 +2350,31 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
 }
 
 
-// The TMA count runs in cluster mode with 4-bit tables and N_s <= 8
-// (TACO_COUNT_TMA=0 keeps the unit-staged k_count_cluster).
-static bool tma_count_enabled(const taco_index* idx) {
+// Entries per unit of the encoded count CSR, 0 = none (TACO_COUNT_TMA=0, or
+// layouts it does not cover): cluster mode 8-entry units (k_count_enc /
+// k_count_tma), global mode 4-entry units (k_count_genc); 4-bit tables with
+// N_s <= 8, and padding to whole units below ~n entries per subspace (large
+// K' with short slices keeps the unit-staged kernels).
+static int enc_unit(const taco_index* idx) {
   const char* e = getenv("TACO_COUNT_TMA");   // read per index (tests pin both kernels)
-  // padding to whole units must stay below ~n entries per subspace (large K'
-  // with short slices keeps the unit-staged kernel)
+  if ((e && e[0] == '0') || idx->n_sub > 8 || idx->chunk > kClusterMaxChunk) return 0;
+  const int U = idx->cluster_mode ? 8 : 4;
   const int64_t nsl = idx->nchunks * (int64_t)idx->kp * idx->kp;
-  return !(e && e[0] == '0') && idx->cluster_mode && idx->n_sub <= 8 && idx->chunk <= kClusterMaxChunk &&
-         (EC_U - 1) * nsl <= idx->n;
+  return (U - 1) * nsl <= idx->n ? U : 0;
 }
 
 int build_count_csr(taco_index* idx) {
   idx->has_ccsr = false;
-  if (!tma_count_enabled(idx)) {
+  const int U = enc_unit(idx);
+  if (!U) {
     idx->cenc.release();
     idx->coffs.release();
     return TACO_OK;
   }
   const int64_t K2 = (int64_t)idx->kp * idx->kp, nsl = idx->nchunks * K2;
   const size_t offs_len = (size_t)nsl + 1;
-  idx->cstride = (size_t)ceil_div(idx->n + (EC_U - 1) * nsl, EC_U) * EC_U;
+  idx->cunit = U;
+  idx->cstride = (size_t)ceil_div(idx->n + (U - 1) * nsl, U) * U;
   TACO_TRY(idx->cenc.ensure(sizeof(uint32_t) * idx->cstride * idx->n_sub));
   TACO_TRY(idx->coffs.ensure(sizeof(uint32_t) * offs_len * idx->n_sub));
   const int nb = (int)ceil_div(nsl, CC_NT);
@@ -2330,13 +2383,13 @@ int build_count_csr(taco_index* idx) {
   cudaStream_t st = idx->stream;
   TACO_CHECK_CUDA(cudaMemsetAsync(idx->coffs.p, 0, sizeof(uint32_t) * offs_len * idx->n_sub, st));
   k_ccsr_sums<<<dim3((unsigned)nb, (unsigned)idx->n_sub), CC_NT, 0, st>>>(idx->offs.as<uint32_t>(), offs_len, nsl,
-                                                                       bsum.as<uint32_t>());
+                                                                       bsum.as<uint32_t>(), U);
   TACO_LAUNCHED();
   k_ccsr_scan<<<(unsigned)idx->n_sub, CC_NT, 0, st>>>(bsum.as<uint32_t>(), nb);
   TACO_LAUNCHED();
   k_ccsr_fill<<<dim3((unsigned)nb, (unsigned)idx->n_sub), CC_NT, 0, st>>>(
       idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(), offs_len, nsl, (int)K2, idx->n, idx->chunk,
-      bsum.as<uint32_t>(), idx->coffs.as<uint32_t>(), idx->cenc.as<uint32_t>(), idx->cstride);
+      bsum.as<uint32_t>(), idx->coffs.as<uint32_t>(), idx->cenc.as<uint32_t>(), idx->cstride, U);
   TACO_LAUNCHED();
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   bsum.release();
@@ -2361,6 +2414,8 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<512>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_genc<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     done = true;
@@ -2371,7 +2426,15 @@ static int set_count_attrs(taco_index*) {
 // global mode, sweep 1: level histograms of every (chunk, query) -> t.hist
 static int global_count(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
   TACO_TRY(set_count_attrs(idx));
-  {
+  if (idx->has_ccsr) {   // encoded CSR (4-entry units)
+    dim3 g((unsigned)idx->nchunks, (unsigned)QS);
+    ProfScope ps(K_COUNT, st);
+    k_count_genc<256, 3><<<g, 256, table_bytes(idx) + sizeof(uint32_t) * EcCfg<256>::GC, st>>>(
+        t.pops.as<uint16_t>(), t.npop.as<int32_t>(), t.pop_cap, idx->cenc.as<uint32_t>(), idx->cstride,
+        idx->coffs.as<uint32_t>(), idx->n_sub, idx->K, idx->n, idx->nchunks, idx->chunk, t.gtab.as<uint8_t>(),
+        t.part.as<int32_t>());
+    TACO_LAUNCHED();
+  } else {
     dim3 g((unsigned)idx->nchunks, (unsigned)QS);
     ProfScope ps(K_COUNT, st);
     auto kern = nib_tables(idx) ? k_count<true> : k_count<false>;

@@ -8,7 +8,9 @@ The batched count has three layouts:
     per-CTA candidate segments.  TACO_CLUSTER_IDS shrinks the chunk so a
     20,000-point rig runs it with 10 CTAs per query;
   * global mode (sharded / n > 1.5M, config 4): per-(query, chunk) CTAs,
-    spilled score >= 2 records, emit sweep, recount list.
+    spilled score >= 2 records, emit sweep, recount list -- on the encoded
+    CSR (4-entry units, k_count_genc) or, with TACO_COUNT_TMA=0, the
+    unit-staged k_count.
 and three table widths: 4-bit (N_s <= 15), 8-bit with wide tallies
 (N_s = 16, config 3) and 8-bit with a table-scan level histogram (N_s > 16).
 rig2 (N_s = 8), rig4 (N_s = 16) and rig5 (N_s = 20) cover the widths; the
@@ -34,6 +36,8 @@ MODES = {
     "cluster_odd": ({"TACO_CLUSTER_IDS": "7000"}, (True, 2)),
     "global": ({"TACO_GLOBAL_MODE": "1"}, (False, 1)),
     "global_small_chunk": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "2048"}, (False, 5)),
+    # global mode without the encoded CSR (the unit-staged k_count sweep)
+    "global_units": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "2048", "TACO_COUNT_TMA": "0"}, (False, 5)),
 }
 
 
