@@ -1995,6 +1995,128 @@ __global__ void __launch_bounds__(32 * RowFmt<T>::WARPS, RowFmt<T>::CTAS) k_rera
   cp_async_wait<0>();
 }
 
+// ------------------------------------- rerank: the integer fast path
+// k_rerank_async's contract for the case config 2 runs: u8 rows, d <= 128
+// (d % 16 == 0: one row segment per tile) and every query of the launch
+// u8-exact, so every candidate takes the exact DP4A path.  Without the
+// generic kernel's segment loop, fp64 path and per-unit bookkeeping a tile
+// is: 8 row-copy instructions (8 lanes x 16 B per row, 4 rows each), 4
+// DP4A per 16 bytes, the running bound and the partial top-k.  Tile state is
+// staged so no load waits on another: descriptors three tiles ahead,
+// candidate ids two ahead, row / query sums of squares one ahead.
+#ifndef RI_WARPS_DEF
+#define RI_WARPS_DEF 8
+#endif
+#ifndef RI_CTAS_DEF
+#define RI_CTAS_DEF 2
+#endif
+constexpr int RI_WARPS = RI_WARPS_DEF, RI_CTAS = RI_CTAS_DEF, RI_PITCH = 144;
+struct RiStage {
+  uint8_t rows[GR][RI_PITCH];   // pitch = 16 B mod 128: conflict-free 16-byte row reads
+  uint8_t q[128];
+};
+struct RiTile {
+  int64_t q = 0;
+  int m = 0, out = 0;
+  uint32_t cid = 0;   // this lane's candidate (lane < m)
+  int32_t xs = 0, qs = 0;
+};
+
+__global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
+    const uint8_t* __restrict__ Xb, int d, const uint8_t* __restrict__ Qb, const int32_t* __restrict__ qsq,
+    const int32_t* __restrict__ xsq, const int4* __restrict__ desc, const uint32_t* __restrict__ cand,
+    int64_t ntiles, int kk, unsigned long long* __restrict__ pkey, uint32_t* __restrict__ pid,
+    unsigned long long* __restrict__ qthr) {
+  extern __shared__ __align__(128) unsigned char ri_sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  RiStage* st = reinterpret_cast<RiStage*>(ri_sm) + 2 * wid;
+  const int64_t gw = (int64_t)wid * gridDim.x + blockIdx.x, nw = (int64_t)gridDim.x * RI_WARPS;
+  if (gw >= ntiles) return;
+  const int64_t nt = (ntiles - gw + nw - 1) / nw;   // my tiles: gw + i * nw
+  const int nc = d / 16;                             // 16-byte chunks per row
+  auto dsc = [&](int64_t i) { return i < nt ? __ldg(desc + gw + i * nw) : make_int4(0, 0, 0, 0); };
+  auto ids_of = [&](const int4 dd, RiTile& r) {   // tile fields + this lane's candidate id
+    r.m = dd.z & 63;
+    r.q = dd.z >> 6;
+    r.out = dd.w;
+    const int64_t cb = (int64_t)(((uint64_t)(uint32_t)dd.y << 32) | (uint32_t)dd.x);
+    r.cid = lane < r.m ? cand[cb + lane] : 0u;
+  };
+  auto sums_of = [&](RiTile& r) {
+    r.xs = lane < r.m ? __ldg(xsq + r.cid) : 0;
+    r.qs = r.m > 0 ? __ldg(qsq + r.q) : 0;
+  };
+  const int r0 = lane >> 3, cl = lane & 7;
+  auto issue = [&](const RiTile& r, RiStage& s) {
+#pragma unroll
+    for (int j = 0; j < GR / 4; ++j) {
+      const int rr = j * 4 + r0;
+      const uint32_t c = __shfl_sync(0xffffffffu, r.cid, rr);
+      if (cl < nc && rr < r.m) cp_async16(&s.rows[rr][cl * 16], Xb + (size_t)c * d + cl * 16);
+    }
+    if (lane < nc && r.m > 0) cp_async16(s.q + lane * 16, Qb + (size_t)r.q * d + lane * 16);
+    cp_async_commit();
+  };
+  RiTile ta, tb, tc;              // computing i, issued i + 1, ids of i + 2
+  ids_of(dsc(0), ta);
+  sums_of(ta);
+  ids_of(dsc(1), tb);
+  int4 dn = dsc(2);
+  issue(ta, st[0]);
+  for (int64_t i = 0; i < nt; ++i) {
+    ids_of(dn, tc);               // ids of tile i + 2
+    dn = dsc(i + 3);
+    sums_of(tb);                  // tile i + 1's ids arrived during tile i - 1
+    if (i + 1 < nt) issue(tb, st[(i + 1) & 1]);
+    else cp_async_commit();
+    cp_async_wait<1>();           // tile i's rows and query bytes have landed
+    __syncwarp();
+    const RiStage& s = st[i & 1];
+    uint32_t acc = 0;
+    for (int c = 0; c < nc; ++c) {
+      const uint4 xw = *reinterpret_cast<const uint4*>(&s.rows[lane][c * 16]);
+      const uint4 qw = *reinterpret_cast<const uint4*>(s.q + c * 16);
+      acc = __dp4a(xw.x, qw.x, acc);
+      acc = __dp4a(xw.y, qw.y, acc);
+      acc = __dp4a(xw.z, qw.z, acc);
+      acc = __dp4a(xw.w, qw.w, acc);
+    }
+    // every step of the reference's fp64 sum is exact on these integers
+    const double v = (double)((int64_t)ta.xs - 2 * (int64_t)acc + (int64_t)ta.qs);
+    unsigned long long key = lane < ta.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+    uint32_t id = ta.cid;
+    const unsigned long long thr = __ldcg(qthr + ta.q);
+    const bool keep = key != ~0ull && key <= thr;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    const int ns = __popc(bal);
+    unsigned long long* ok = pkey + (int64_t)ta.out * kk;
+    uint32_t* oi = pid + (int64_t)ta.out * kk;
+    if (ns <= kk) {
+      if (keep) {
+        const int slot = __popc(bal & ((1u << lane) - 1u));
+        ok[slot] = key;
+        oi[slot] = id;
+      }
+      if (lane >= ns && lane < kk) {
+        ok[lane] = ~0ull;
+        oi[lane] = 0xFFFFFFFFu;
+      }
+    } else {
+      warp_sort_pairs(key, id);
+      if (lane < kk) {
+        ok[lane] = key;
+        oi[lane] = id;
+      }
+      const unsigned long long kth = __shfl_sync(0xffffffffu, key, kk - 1);
+      if (lane == 0 && kth != ~0ull) atomicMin(qthr + ta.q, kth);
+    }
+    __syncwarp();                 // stage i & 1 is refilled by tile i + 2
+    ta = tb;
+    tb = tc;
+  }
+  cp_async_wait<0>();
+}
+
 // Generic rerank for d % 4 != 0: lane = row, direct loads.
 __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ X, int d,
                                                       const float* __restrict__ Qf,
@@ -2664,7 +2786,7 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
                        const int64_t* tstart,
                        const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
                        int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, DevBuf& qthrb, double* out_d2,
-                       int64_t* out_ids, cudaStream_t st, const IntRerank& ir = IntRerank()) {
+                       int64_t* out_ids, cudaStream_t st, const IntRerank& ir = IntRerank(), bool all_int = false) {
   const int kk = std::min(k, GR);
   TACO_TRY(qthrb.ensure(sizeof(unsigned long long) * (size_t)QS));
   TACO_CHECK_CUDA(cudaMemsetAsync(qthrb.p, 0xFF, sizeof(unsigned long long) * (size_t)QS, st));
@@ -2682,7 +2804,20 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
   if (ntiles > 0) {
     ProfScope ps(K_RERANK, st);
     unsigned long long* pk = pkey.as<unsigned long long>();
-    if (fmt == TACO_ROWS_U8) {
+    static const bool fast = !(getenv("TACO_RERANK_I8") && getenv("TACO_RERANK_I8")[0] == '0');
+    if (fmt == TACO_ROWS_U8 && all_int && ir.qok && fast && d <= 128 && d % 16 == 0) {
+      // every query u8-exact: the integer fast path
+      const size_t smem = sizeof(RiStage) * 2 * RI_WARPS;
+      static bool attr = false;
+      if (!attr) {
+        TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      const int64_t grid = std::min<int64_t>(ceil_div(ntiles, RI_WARPS), (int64_t)num_sms() * RI_CTAS);
+      k_rerank_i8<<<(unsigned)grid, 32 * RI_WARPS, smem, st>>>(static_cast<const uint8_t*>(Xn), d, ir.Qb, ir.qsq,
+                                                                ir.xsq, desc, cand, ntiles, kk, pk,
+                                                                pid.as<uint32_t>(), qthr);
+    } else if (fmt == TACO_ROWS_U8) {
       TACO_TRY(launch_rerank_async<uint8_t>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, ir, st));
     } else if (fmt == TACO_ROWS_F16) {
       TACO_TRY(launch_rerank_async<__half>(Xn, d, Qf, desc, cand, ntiles, kk, pk, pid.as<uint32_t>(), qthr, ir, st));
@@ -2732,7 +2867,8 @@ static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_
   return rerank_core(idx->X.as<float>(), idx->Xn.p, idx->xfmt, idx->d, t.Q.as<float>(), QS, S, t.bpref.as<int64_t>(),
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      seg_base(idx, t), seg_cnt(idx, t), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
-                     t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st, ir);
+                     t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st, ir,
+                     intp && prepped && t.flags_h[4] == 0);   // flags[4]: some query is not u8-exact
 }
 
 static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total) {
@@ -2825,11 +2961,16 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
   for (QueryTile* t : tiles)
     if (t->pop_cap == 0) t->pop_cap = std::min(idx->K, 1024);
   const int64_t QSmax = std::min<int64_t>(nq, super_tile(idx, idx->qt.pop_cap));
-  static int ptiles = -1;   // tiles a pipelined batch is cut into (TACO_PIPE_TILES, default 2; 1 = off)
-  if (ptiles < 0) {
+  // tiles a pipelined batch is cut into (TACO_PIPE_TILES; 1 = off).  Default:
+  // off for u8 rows with d <= 128 (the integer re-rank is short enough that
+  // overlapping it with the next tile's count no longer pays: config 2,
+  // 1 tile 1.099 M QPS vs 2 tiles 1.060 M), else 2.
+  static int ptiles_env = -2;
+  if (ptiles_env == -2) {
     const char* e = getenv("TACO_PIPE_TILES");
-    ptiles = e ? std::max(1, atoi(e)) : 2;
+    ptiles_env = e ? std::max(1, atoi(e)) : -1;
   }
+  const int ptiles = ptiles_env > 0 ? ptiles_env : (idx->xfmt == TACO_ROWS_U8 && idx->d <= 128 ? 1 : 2);
   // profiled passes run unpipelined so per-kernel event times do not overlap
   const bool pipe = ptiles > 1 && nq >= 2 * kPipeMin && !g_prof.on;
   int64_t QT = QSmax;
