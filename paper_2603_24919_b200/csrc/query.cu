@@ -171,9 +171,28 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
   int64_t got = 0;
   uint16_t* out = pops + t * cap;
   double* kout = keys_out ? keys_out + t * cap : nullptr;
-  while (hn > 0) {
+  // Software-pipelined: the top's successor distances and labels are loaded
+  // before the pop's sift-down (which hides their latency), and a popped
+  // cell's size is loaded when it is popped but added one pop later, so no
+  // pop waits on the size load.  The pop made after the target was reached
+  // is dropped (np does not count it): same pops, counts and sizes as the
+  // reference loop.
+  int64_t psz = 0;        // size of the last counted pop, not yet added
+  bool pend = false;
+  const double d20 = d2[0];
+  while (true) {
+    if (hn == 0) {
+      if (pend) got += psz;
+      break;
+    }
     const double key = hk[0];
     const uint32_t pc = hp[0];
+    const int r = (int)(pc >> 16), c = (int)(pc & 0xFFFF);
+    const bool nr = c == 0 && r + 1 < kp, nc = c + 1 < kp;
+    const double dr1 = nr ? d1[r + 1] : 0.0;
+    const double dr = d1[r];
+    const double dc1 = nc ? d2[c + 1] : 0.0;
+    const int cell = (int)l1[r] * kp + (int)l2[c];
     --hn;
     if (hn > 0) {
       const double lk = hk[hn];
@@ -192,21 +211,183 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
       hk[i] = lk;
       hp[i] = lp;
     }
-    const int r = (int)(pc >> 16), c = (int)(pc & 0xFFFF);
-    const int cell = (int)l1[r] * kp + (int)l2[c];
     if (np < cap) {
       out[np] = (uint16_t)cell;
       if (kout) kout[np] = key;
     }
+    if (pend) {
+      got += psz;
+      if (got >= target) break;   // the previous pop reached the target: this one is not counted
+    }
+    psz = gs[cell];
+    pend = true;
     ++np;
-    got += gs[cell];
-    if (got >= target) break;
-    if (c == 0 && r + 1 < kp) push(__dadd_rn(d1[r + 1], d2[0]), (uint32_t)(r + 1) << 16);
-    if (c + 1 < kp) push(__dadd_rn(d1[r], d2[c + 1]), ((uint32_t)r << 16) | (uint32_t)(c + 1));
+    if (nr) push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 16);
+    if (nc) push(__dadd_rn(dr, dc1), ((uint32_t)r << 16) | (uint32_t)(c + 1));
   }
   npop[t] = np;
   ret[t] = got;
   if (np > cap) atomicMax((unsigned long long*)&flags[0], (unsigned long long)np);
+}
+
+// Same walk with the heap in shared memory (TS_THREADS walks per CTA, the
+// heap of walk x interleaved across threads): the thread-local heaps of
+// k_traverse (768 B per walk at K' = 64, ~415 KB per SM) do not fit L1 and
+// every sift step went to L2.  The walks' sorted distances and labels are
+// read through L1.
+constexpr int TS_THREADS = 64;
+template <int KMAX>
+__global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __restrict__ sd,
+                                                  const uint16_t* __restrict__ sl,
+                                                  const int64_t* __restrict__ gsize, int64_t Q,
+                                                  int n_sub, int kp, int64_t target,
+                                                  uint16_t* __restrict__ pops, int cap,
+                                                  double* __restrict__ keys_out,
+                                                  int32_t* __restrict__ npop,
+                                                  int64_t* __restrict__ ret,
+                                                  int64_t* __restrict__ flags) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Q * n_sub) return;
+  const int j = (int)(t % n_sub);
+  const double* d1 = sd + t * 2 * kp;
+  const double* d2 = d1 + kp;
+  const uint16_t* l1 = sl + t * 2 * kp;
+  const uint16_t* l2 = l1 + kp;
+  const int64_t* gs = gsize + (size_t)j * kp * kp;
+  // the heap lives in shared memory, element i of thread x at [i * TS_THREADS + x]
+  extern __shared__ __align__(16) unsigned char tsh_sm[];
+  double* const hkb = reinterpret_cast<double*>(tsh_sm) + threadIdx.x;
+  uint32_t* const hpb = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tsh_sm) + KMAX * TS_THREADS) + threadIdx.x;
+  struct HeapRef {
+    double* k;
+    uint32_t* p;
+    __device__ double& key(int i) const { return k[i * TS_THREADS]; }
+    __device__ uint32_t& pc(int i) const { return p[i * TS_THREADS]; }
+  };
+  const HeapRef H{hkb, hpb};
+#define hk(i) H.key(i)
+#define hp(i) H.pc(i)
+  int hn = 0;
+  auto less = [&](double ka, uint32_t pa, double kb, uint32_t pb) {
+    return ka < kb || (ka == kb && pa < pb);
+  };
+  auto push = [&](double key, uint32_t pc) {
+    int i = hn++;
+    while (i > 0) {
+      int par = (i - 1) >> 1;
+      if (!less(key, pc, hk(par), hp(par))) break;
+      hk(i) = hk(par);
+      hp(i) = hp(par);
+      i = par;
+    }
+    hk(i) = key;
+    hp(i) = pc;
+  };
+  push(__dadd_rn(d1[0], d2[0]), 0u);
+  int np = 0;
+  int64_t got = 0;
+  uint16_t* out = pops + t * cap;
+  double* kout = keys_out ? keys_out + t * cap : nullptr;
+  // Software-pipelined: the top's successor distances and labels are loaded
+  // before the pop's sift-down (which hides their latency), and a popped
+  // cell's size is loaded when it is popped but added one pop later, so no
+  // pop waits on the size load.  The pop made after the target was reached
+  // is dropped (np does not count it): same pops, counts and sizes as the
+  // reference loop.
+  int64_t psz = 0;        // size of the last counted pop, not yet added
+  bool pend = false;
+  const double d20 = d2[0];
+  while (true) {
+    if (hn == 0) {
+      if (pend) got += psz;
+      break;
+    }
+    const double key = hk(0);
+    const uint32_t pc = hp(0);
+    const int r = (int)(pc >> 16), c = (int)(pc & 0xFFFF);
+    const bool nr = c == 0 && r + 1 < kp, nc = c + 1 < kp;
+    const double dr1 = nr ? d1[r + 1] : 0.0;
+    const double dr = d1[r];
+    const double dc1 = nc ? d2[c + 1] : 0.0;
+    const int cell = (int)l1[r] * kp + (int)l2[c];
+    --hn;
+    if (hn > 0) {
+      const double lk = hk(hn);
+      const uint32_t lp = hp(hn);
+      int i = 0;
+      while (true) {
+        int a = 2 * i + 1;
+        if (a >= hn) break;
+        int b = a + 1;
+        int m = (b < hn && less(hk(b), hp(b), hk(a), hp(a))) ? b : a;
+        if (!less(hk(m), hp(m), lk, lp)) break;
+        hk(i) = hk(m);
+        hp(i) = hp(m);
+        i = m;
+      }
+      hk(i) = lk;
+      hp(i) = lp;
+    }
+    if (np < cap) {
+      out[np] = (uint16_t)cell;
+      if (kout) kout[np] = key;
+    }
+    if (pend) {
+      got += psz;
+      if (got >= target) break;   // the previous pop reached the target: this one is not counted
+    }
+    psz = gs[cell];
+    pend = true;
+    ++np;
+    if (nr) push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 16);
+    if (nc) push(__dadd_rn(dr, dc1), ((uint32_t)r << 16) | (uint32_t)(c + 1));
+  }
+  npop[t] = np;
+  ret[t] = got;
+  if (np > cap) atomicMax((unsigned long long*)&flags[0], (unsigned long long)np);
+}
+#undef hk
+#undef hp
+
+static bool traverse_local() {   // TACO_TRAVERSE=heap: the thread-local-heap kernel
+  const char* e = getenv("TACO_TRAVERSE");
+  return e && !strcmp(e, "heap");
+}
+
+// launch the traversal of Q queries x n_sub subspaces
+static int launch_traverse(const double* sd, const uint16_t* sl, const int64_t* gsize, int64_t Q, int n_sub, int kp,
+                           int64_t target, uint16_t* pops, int cap, double* keys_out, int32_t* npop, int64_t* ret,
+                           int64_t* flags, cudaStream_t st) {
+  const int64_t th = Q * n_sub;
+  if (!traverse_local()) {
+#define TRAVS(KM)                                                                                          \
+  {                                                                                                        \
+    const size_t smem = (size_t)KM * TS_THREADS * 12;                                                      \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_traverse_sh<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)smem));                                                    \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    k_traverse_sh<KM><<<(unsigned)ceil_div(th, TS_THREADS), TS_THREADS, smem, st>>>(                        \
+        sd, sl, gsize, Q, n_sub, kp, target, pops, cap, keys_out, npop, ret, flags);                        \
+  }
+    if (kp <= 32) TRAVS(32)
+    else if (kp <= 64) TRAVS(64)
+    else if (kp <= 128) TRAVS(128)
+    else TRAVS(256)
+#undef TRAVS
+    return TACO_OK;
+  }
+  const unsigned g = (unsigned)ceil_div(th, 128);
+#define TRAV(KM) \
+  k_traverse<KM><<<g, 128, 0, st>>>(sd, sl, gsize, Q, n_sub, kp, target, pops, cap, keys_out, npop, ret, flags)
+  if (kp <= 32) TRAV(32);
+  else if (kp <= 64) TRAV(64);
+  else if (kp <= 128) TRAV(128);
+  else TRAV(256);
+#undef TRAV
+  return TACO_OK;
 }
 
 // ---------------------------------------------------------- block helpers
@@ -2454,18 +2635,11 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
   {
     const int64_t th = QS * idx->n_sub;
     const int64_t target = retrieval_target(alpha, idx->n_global);
-    const unsigned g = (unsigned)ceil_div(th, 128);
+    (void)th;
     ProfScope ps(K_TRAVERSE, st);
-#define TRAV(KM)                                                                                  \
-  k_traverse<KM><<<g, 128, 0, st>>>(sd, sl, idx->gsize.as<int64_t>(), QS, idx->n_sub, kp, target,    \
-                                    t.pops.as<uint16_t>() + qn0 * t.pop_cap, t.pop_cap, keys_out,     \
-                                    t.npop.as<int32_t>() + qn0, t.ret.as<int64_t>() + qn0,            \
-                                    t.flags.as<int64_t>())
-    if (kp <= 32) TRAV(32);
-    else if (kp <= 64) TRAV(64);
-    else if (kp <= 128) TRAV(128);
-    else TRAV(256);
-#undef TRAV
+    TACO_TRY(launch_traverse(sd, sl, idx->gsize.as<int64_t>(), QS, idx->n_sub, kp, target,
+                             t.pops.as<uint16_t>() + qn0 * t.pop_cap, t.pop_cap, keys_out, t.npop.as<int32_t>() + qn0,
+                             t.ret.as<int64_t>() + qn0, t.flags.as<int64_t>(), st));
     TACO_LAUNCHED();
   }
   return TACO_OK;
@@ -3507,14 +3681,10 @@ int taco_traverse(int device, int32_t kp, const double* d1s_h, const int32_t* l1
     cudaMemcpy(sd.as<double>() + kp, d2s_h, 8 * (size_t)kp, cudaMemcpyHostToDevice);
     cudaMemcpy(sl.p, l.data(), 4 * (size_t)kp, cudaMemcpyHostToDevice);
     cudaMemcpy(gs.p, sizes_h, 8 * (size_t)K2, cudaMemcpyHostToDevice);
-#define TRAV1(KM) k_traverse<KM><<<1, 128>>>(sd.as<double>(), sl.as<uint16_t>(), gs.as<int64_t>(), 1, 1, kp, \
-                                            target, pops.as<uint16_t>(), K2, keys.as<double>(),        \
-                                            np.as<int32_t>(), ret.as<int64_t>(), fl.as<int64_t>())
-    if (kp <= 32) TRAV1(32);
-    else if (kp <= 64) TRAV1(64);
-    else if (kp <= 128) TRAV1(128);
-    else TRAV1(256);
-#undef TRAV1
+    if ((rc = launch_traverse(sd.as<double>(), sl.as<uint16_t>(), gs.as<int64_t>(), 1, 1, kp, target,
+                              pops.as<uint16_t>(), K2, keys.as<double>(), np.as<int32_t>(), ret.as<int64_t>(),
+                              fl.as<int64_t>(), 0)))
+      break;
     count_launch();
     int32_t n = 0;
     cudaMemcpy(&n, np.p, 4, cudaMemcpyDeviceToHost);

@@ -135,7 +135,12 @@ def test_rerank_edge_cases():
     assert res.ids.size == 0 and res.ids.dtype == np.int32
 
 
-def test_traversal_units(golden):
+@pytest.mark.parametrize("walk", ["smem_heap", "local_heap"])
+def test_traversal_units(golden, walk, monkeypatch):
+    """60 traversal instances with integer ties (reference pop traces), through
+    the shared-memory-heap walk (default) and the thread-local heap."""
+    if walk == "local_heap":
+        monkeypatch.setenv("TACO_TRAVERSE", "heap")
     u = golden("units")
     for c in range(int(u["n_trav"][0])):
         d1, d2, sizes = u[f"tr{c}_d1"], u[f"tr{c}_d2"], u[f"tr{c}_sizes"]
