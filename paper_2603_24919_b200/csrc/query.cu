@@ -3390,7 +3390,10 @@ int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d
     int64_t zero = 0;
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 1, &zero, 8, cudaMemcpyHostToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 3, &zero, 8, cudaMemcpyHostToDevice, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags.as<int64_t>() + 4, &zero, 8, cudaMemcpyHostToDevice, st));
     TACO_TRY(global_select(idx, t, nq, ghist_d, beta, st));
+    const bool intp = idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled();
+    if (intp) TACO_TRY(q_u8_prep(idx, t, nq, st));   // flags[4] is read back with the plan
     int64_t fl[4];
     TACO_TRY(plan_and_read(idx, t, nq, st, fl));
     if (fl[1]) {
@@ -3398,7 +3401,7 @@ int taco_query_finish_device(taco_index* idx, int64_t nq, const int64_t* ghist_d
       continue;
     }
     prof_stats(idx, t, nq, fl[3]);
-    TACO_TRY(rerank_stage(idx, t, nq, k, fl[2], st));
+    TACO_TRY(rerank_stage(idx, t, nq, k, fl[2], st, intp));
     TACO_CHECK_CUDA(cudaMemcpyAsync(topk_d2_d, t.tk_d2.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(topk_ids_d, t.tk_ids.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToDevice, st));
     TACO_CHECK_CUDA(cudaMemcpyAsync(cand_num_d, t.cnum.p, sizeof(int64_t) * nq, cudaMemcpyDeviceToDevice, st));
