@@ -18,6 +18,7 @@
 #include <ctime>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 
@@ -1747,24 +1748,34 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
   const int64_t nba = ceil_div(n, (int64_t)AS_THREADS);
   const int mp = m <= 8 ? 8 : m <= 16 ? 16 : 32;   // point-major stride (k_pp_step<MP> buckets)
   const size_t sort_bytes = label_sort_bytes(n, k);
-  // host side of the exact replay: numpy's pairwise leaves and combine tree for n
-  std::vector<char> blob;
+  // host side of the exact replay: numpy's pairwise leaves and combine tree
+  // for n -- the same for every half, computed once per n for the process
+  // (it cost ~1 ms per half per build)
   if (s.leaves_n != n || s.leaf_blob.empty()) {
-    std::vector<int64_t> lv;
-    pairwise_leaves(0, n, lv);
-    s.nleaves = (int64_t)lv.size() / 2;
-    const PwTree tree = pairwise_tree(n);
-    // layout: (off, len) per leaf as int64, then left[ni], right[ni], level_start[] as int32
-    blob.resize(8 * lv.size() + 4 * (tree.left.size() + tree.right.size() + tree.level_start.size()));
-    char* bp = blob.data();
-    memcpy(bp, lv.data(), 8 * lv.size());
-    bp += 8 * lv.size();
-    memcpy(bp, tree.left.data(), 4 * tree.left.size());
-    bp += 4 * tree.left.size();
-    memcpy(bp, tree.right.data(), 4 * tree.right.size());
-    bp += 4 * tree.right.size();
-    memcpy(bp, tree.level_start.data(), 4 * tree.level_start.size());
-    s.leaf_blob.swap(blob);
+    static std::mutex blob_mu;
+    static int64_t blob_n = -1, blob_leaves = 0;
+    static std::vector<char> blob_cache;
+    std::lock_guard<std::mutex> lk(blob_mu);
+    if (blob_n != n) {
+      std::vector<int64_t> lv;
+      pairwise_leaves(0, n, lv);
+      const PwTree tree = pairwise_tree(n);
+      // layout: (off, len) per leaf as int64, then left[ni], right[ni], level_start[] as int32
+      std::vector<char> blob(8 * lv.size() + 4 * (tree.left.size() + tree.right.size() + tree.level_start.size()));
+      char* bp = blob.data();
+      memcpy(bp, lv.data(), 8 * lv.size());
+      bp += 8 * lv.size();
+      memcpy(bp, tree.left.data(), 4 * tree.left.size());
+      bp += 4 * tree.left.size();
+      memcpy(bp, tree.right.data(), 4 * tree.right.size());
+      bp += 4 * tree.right.size();
+      memcpy(bp, tree.level_start.data(), 4 * tree.level_start.size());
+      blob_cache.swap(blob);
+      blob_leaves = (int64_t)lv.size() / 2;
+      blob_n = n;
+    }
+    s.leaf_blob = blob_cache;
+    s.nleaves = blob_leaves;
     s.leaves_n = n;
   }
   // One arena per half (a single pool allocation: the ~20 scratch buffers
