@@ -271,19 +271,32 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
   auto less = [&](double ka, uint32_t pa, double kb, uint32_t pb) {
     return ka < kb || (ka == kb && pa < pb);
   };
-  auto push = [&](double key, uint32_t pc) {
-    int i = hn++;
-    while (i > 0) {
-      int par = (i - 1) >> 1;
-      if (!less(key, pc, hk(par), hp(par))) break;
-      hk(i) = hk(par);
-      hp(i) = hp(par);
-      i = par;
+  // Fixed-depth, predicated sift-up / sift-down (TS_BF): every lane runs
+  // the same log2(KMAX) steps, so the 32 walks of a warp never diverge.
+  constexpr int LOGK = KMAX <= 32 ? 5 : KMAX <= 64 ? 6 : KMAX <= 128 ? 7 : 8;
+  auto push = [&](double key, uint32_t pc, bool doit) {
+    int i = hn;
+    hn += doit ? 1 : 0;
+    bool done = !doit || i == 0;
+#pragma unroll
+    for (int lev = 0; lev < LOGK; ++lev) {
+      const int par = done ? 0 : (i - 1) >> 1;
+      const double kp_ = hk(par);
+      const uint32_t pp_ = hp(par);
+      const bool go = !done && less(key, pc, kp_, pp_);
+      if (go) {
+        hk(i) = kp_;
+        hp(i) = pp_;
+        i = par;
+      }
+      done = done || !go || i == 0;
     }
-    hk(i) = key;
-    hp(i) = pc;
+    if (doit) {
+      hk(i) = key;
+      hp(i) = pc;
+    }
   };
-  push(__dadd_rn(d1[0], d2[0]), 0u);
+  push(__dadd_rn(d1[0], d2[0]), 0u, true);
   int np = 0;
   int64_t got = 0;
   uint16_t* out = pops + t * cap;
@@ -311,22 +324,33 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     const double dc1 = nc ? d2[c + 1] : 0.0;
     const int cell = (int)l1[r] * kp + (int)l2[c];
     --hn;
-    if (hn > 0) {
+    {
       const double lk = hk(hn);
       const uint32_t lp = hp(hn);
       int i = 0;
-      while (true) {
-        int a = 2 * i + 1;
-        if (a >= hn) break;
-        int b = a + 1;
-        int m = (b < hn && less(hk(b), hp(b), hk(a), hp(a))) ? b : a;
-        if (!less(hk(m), hp(m), lk, lp)) break;
-        hk(i) = hk(m);
-        hp(i) = hp(m);
-        i = m;
+      bool done = hn == 0;
+#pragma unroll
+      for (int lev = 0; lev < LOGK; ++lev) {
+        const int a = 2 * i + 1, b = a + 1;
+        const bool va = !done && a < hn, vb = !done && b < hn;
+        const int ia = va ? a : 0, ib = vb ? b : 0;
+        const double ka = hk(ia), kb = hk(ib);
+        const uint32_t pa = hp(ia), pb = hp(ib);
+        const bool useb = vb && less(kb, pb, ka, pa);
+        const double km = useb ? kb : ka;
+        const uint32_t pm = useb ? pb : pa;
+        const bool go = va && less(km, pm, lk, lp);
+        if (go) {
+          hk(i) = km;
+          hp(i) = pm;
+          i = useb ? b : a;
+        }
+        done = done || !go;
       }
-      hk(i) = lk;
-      hp(i) = lp;
+      if (hn > 0) {
+        hk(i) = lk;
+        hp(i) = lp;
+      }
     }
     if (np < cap) {
       out[np] = (uint16_t)cell;
@@ -339,8 +363,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     psz = gs[cell];
     pend = true;
     ++np;
-    if (nr) push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 16);
-    if (nc) push(__dadd_rn(dr, dc1), ((uint32_t)r << 16) | (uint32_t)(c + 1));
+    push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 16, nr);
+    push(__dadd_rn(dr, dc1), ((uint32_t)r << 16) | (uint32_t)(c + 1), nc);
   }
   npop[t] = np;
   ret[t] = got;
