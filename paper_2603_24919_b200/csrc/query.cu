@@ -235,8 +235,7 @@ __global__ void __launch_bounds__(128) k_traverse(const double* __restrict__ sd,
 // k_traverse (768 B per walk at K' = 64, ~415 KB per SM) do not fit L1 and
 // every sift step went to L2.  The walks' sorted distances and labels are
 // read through L1.
-constexpr int TS_THREADS = 64;
-template <int KMAX>
+template <int KMAX, int TS_THREADS>
 __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __restrict__ sd,
                                                   const uint16_t* __restrict__ sl,
                                                   const int64_t* __restrict__ gsize, int64_t Q,
@@ -257,12 +256,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
   // the heap lives in shared memory, element i of thread x at [i * TS_THREADS + x]
   extern __shared__ __align__(16) unsigned char tsh_sm[];
   double* const hkb = reinterpret_cast<double*>(tsh_sm) + threadIdx.x;
-  uint32_t* const hpb = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tsh_sm) + KMAX * TS_THREADS) + threadIdx.x;
+  // (row, col) as r << 8 | c (K' <= 256): the same (r, c) order as the heap's pc
+  uint16_t* const hpb = reinterpret_cast<uint16_t*>(reinterpret_cast<double*>(tsh_sm) + KMAX * TS_THREADS) + threadIdx.x;
   struct HeapRef {
     double* k;
-    uint32_t* p;
+    uint16_t* p;
     __device__ double& key(int i) const { return k[i * TS_THREADS]; }
-    __device__ uint32_t& pc(int i) const { return p[i * TS_THREADS]; }
+    __device__ uint16_t& pc(int i) const { return p[i * TS_THREADS]; }
   };
   const HeapRef H{hkb, hpb};
 #define hk(i) H.key(i)
@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
   // Fixed-depth, predicated sift-up / sift-down (TS_BF): every lane runs
   // the same log2(KMAX) steps, so the 32 walks of a warp never diverge.
   constexpr int LOGK = KMAX <= 32 ? 5 : KMAX <= 64 ? 6 : KMAX <= 128 ? 7 : 8;
-  auto push = [&](double key, uint32_t pc, bool doit) {
+  auto push = [&](double key, uint32_t pc32, bool doit) {
+    const uint16_t pc = (uint16_t)pc32;
     int i = hn;
     hn += doit ? 1 : 0;
     bool done = !doit || i == 0;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     for (int lev = 0; lev < LOGK; ++lev) {
       const int par = done ? 0 : (i - 1) >> 1;
       const double kp_ = hk(par);
-      const uint32_t pp_ = hp(par);
+      const uint16_t pp_ = hp(par);
       const bool go = !done && less(key, pc, kp_, pp_);
       if (go) {
         hk(i) = kp_;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     }
     const double key = hk(0);
     const uint32_t pc = hp(0);
-    const int r = (int)(pc >> 16), c = (int)(pc & 0xFFFF);
+    const int r = (int)(pc >> 8), c = (int)(pc & 0xFF);
     const bool nr = c == 0 && r + 1 < kp, nc = c + 1 < kp;
     const double dr1 = nr ? d1[r + 1] : 0.0;
     const double dr = d1[r];
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     --hn;
     {
       const double lk = hk(hn);
-      const uint32_t lp = hp(hn);
+      const uint16_t lp = hp(hn);
       int i = 0;
       bool done = hn == 0;
 #pragma unroll
@@ -335,10 +336,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
         const bool va = !done && a < hn, vb = !done && b < hn;
         const int ia = va ? a : 0, ib = vb ? b : 0;
         const double ka = hk(ia), kb = hk(ib);
-        const uint32_t pa = hp(ia), pb = hp(ib);
+        const uint16_t pa = hp(ia), pb = hp(ib);
         const bool useb = vb && less(kb, pb, ka, pa);
         const double km = useb ? kb : ka;
-        const uint32_t pm = useb ? pb : pa;
+        const uint16_t pm = useb ? pb : pa;
         const bool go = va && less(km, pm, lk, lp);
         if (go) {
           hk(i) = km;
@@ -363,8 +364,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
     psz = gs[cell];
     pend = true;
     ++np;
-    push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 16, nr);
-    push(__dadd_rn(dr, dc1), ((uint32_t)r << 16) | (uint32_t)(c + 1), nc);
+    push(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 8, nr);
+    push(__dadd_rn(dr, dc1), ((uint32_t)r << 8) | (uint32_t)(c + 1), nc);
   }
   npop[t] = np;
   ret[t] = got;
@@ -373,9 +374,14 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
 #undef hk
 #undef hp
 
-static bool traverse_local() {   // TACO_TRAVERSE=heap: the thread-local-heap kernel
+static int num_sms();
+
+// TACO_TRAVERSE=heap / =smem force the thread-local-heap / shared-memory
+// kernel (tests pin both); default: by batch size (launch_traverse)
+static int traverse_force() {
   const char* e = getenv("TACO_TRAVERSE");
-  return e && !strcmp(e, "heap");
+  if (!e) return 0;
+  return !strcmp(e, "heap") ? 1 : !strcmp(e, "smem") ? 2 : 0;
 }
 
 // launch the traversal of Q queries x n_sub subspaces
@@ -383,24 +389,33 @@ static int launch_traverse(const double* sd, const uint16_t* sl, const int64_t* 
                            int64_t target, uint16_t* pops, int cap, double* keys_out, int32_t* npop, int64_t* ret,
                            int64_t* flags, cudaStream_t st) {
   const int64_t th = Q * n_sub;
-  if (!traverse_local()) {
-#define TRAVS(KM)                                                                                          \
-  {                                                                                                        \
-    const size_t smem = (size_t)KM * TS_THREADS * 12;                                                      \
-    static bool attr = false;                                                                              \
-    if (!attr) {                                                                                           \
-      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_traverse_sh<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           (int)smem));                                                    \
-      attr = true;                                                                                         \
-    }                                                                                                      \
-    k_traverse_sh<KM><<<(unsigned)ceil_div(th, TS_THREADS), TS_THREADS, smem, st>>>(                        \
-        sd, sl, gsize, Q, n_sub, kp, target, pops, cap, keys_out, npop, ret, flags);                        \
+  // small batches (fewer than ~128 walks per SM): the thread-local heaps fit
+  // L1 and the variable-depth sifts finish sooner (configs 1 / 3: 0.23 / 0.25
+  // ms vs 0.29 / 0.27); large batches: the shared-memory fixed-depth heap
+  const int force = traverse_force();
+  if (force == 2 || (force == 0 && th >= (int64_t)num_sms() * 128)) {
+  // 64 walks per CTA; 32 when that would leave SMs idle
+  const bool narrow = th < (int64_t)num_sms() * 64 * 4;
+#define TRAVS1(KM, TS)                                                                                      \
+  {                                                                                                         \
+    const size_t smem = (size_t)KM * TS * 10;                                                               \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_traverse_sh<KM, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)smem));                                                     \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    k_traverse_sh<KM, TS><<<(unsigned)ceil_div(th, TS), TS, smem, st>>>(sd, sl, gsize, Q, n_sub, kp, target, \
+                                                                      pops, cap, keys_out, npop, ret, flags);  \
   }
+#define TRAVS(KM) \
+  if (narrow) TRAVS1(KM, 32) else TRAVS1(KM, 64)
     if (kp <= 32) TRAVS(32)
     else if (kp <= 64) TRAVS(64)
     else if (kp <= 128) TRAVS(128)
     else TRAVS(256)
 #undef TRAVS
+#undef TRAVS1
     return TACO_OK;
   }
   const unsigned g = (unsigned)ceil_div(th, 128);

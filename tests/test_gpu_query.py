@@ -29,7 +29,10 @@ def rig(request, golden):
     return g, X, Q, idx
 
 
-def test_batch_matches_reference(rig):
+@pytest.mark.parametrize("walk", ["default", "smem", "heap"])
+def test_batch_matches_reference(rig, walk, monkeypatch):
+    if walk != "default":
+        monkeypatch.setenv("TACO_TRAVERSE", walk)
     g, X, Q, idx = rig
     for gi, (alpha, beta, k) in enumerate(g["grid"]):
         qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
@@ -135,12 +138,12 @@ def test_rerank_edge_cases():
     assert res.ids.size == 0 and res.ids.dtype == np.int32
 
 
-@pytest.mark.parametrize("walk", ["smem_heap", "local_heap"])
+@pytest.mark.parametrize("walk", ["smem", "heap"])
 def test_traversal_units(golden, walk, monkeypatch):
     """60 traversal instances with integer ties (reference pop traces), through
-    the shared-memory-heap walk (default) and the thread-local heap."""
-    if walk == "local_heap":
-        monkeypatch.setenv("TACO_TRAVERSE", "heap")
+    the shared-memory fixed-depth heap (large batches) and the thread-local
+    heap (small batches)."""
+    monkeypatch.setenv("TACO_TRAVERSE", walk)
     u = golden("units")
     for c in range(int(u["n_trav"][0])):
         d1, d2, sizes = u[f"tr{c}_d1"], u[f"tr{c}_d2"], u[f"tr{c}_sizes"]
