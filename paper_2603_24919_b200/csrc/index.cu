@@ -230,7 +230,10 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
     // ids per CTA: 4-bit tables (n_sub <= 15) 128K = 64 KiB, 8-bit tables 64K (TACO_CLUSTER_IDS overrides)
     int64_t target = n_subspaces <= 15 ? 131072 : 65536;
     if (const char* e = getenv("TACO_CLUSTER_IDS")) target = std::max<int64_t>(1024, atoll(e));
-    target = std::min(target, n_subspaces <= 15 ? kClusterMaxChunk : kClusterMaxChunk8);
+    // 4-bit tables up to 128K ids per CTA (256K for N_s <= 8 with TACO_COUNT_NT=1024: one 1024-thread CTA per SM)
+    const char* wnt = getenv("TACO_COUNT_NT");
+    const int64_t cap4 = (n_subspaces <= 8 && wnt && atoi(wnt) == 1024) ? kClusterWideChunk : kClusterMaxChunk;
+    target = std::min(target, n_subspaces <= 15 ? cap4 : kClusterMaxChunk8);
     const int ctas = (int)std::min<int64_t>(kClusterMaxCtas, std::max<int64_t>(1, ceil_div(n, target)));
     idx->chunk = ceil_div(ceil_div(n, ctas), 1024) * 1024;
     idx->cluster_mode = true;

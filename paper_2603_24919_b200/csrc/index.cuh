@@ -25,6 +25,7 @@ namespace taco {
 constexpr int64_t kGlobalChunk = 65536;
 constexpr int64_t kClusterMaxChunk = 131072;   // 4-bit tables: 64 KiB; 8-bit tables are capped at 98304
 constexpr int64_t kClusterMaxChunk8 = 98304;
+constexpr int64_t kClusterWideChunk = 262144;   // TACO_CLUSTER_IDS up to this with the 1024-thread encoded count
 constexpr int kClusterMaxCtas = 16;             // non-portable cluster size
 constexpr int64_t kClusterMaxN = kClusterMaxChunk8 * kClusterMaxCtas;
 

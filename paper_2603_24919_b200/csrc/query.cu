@@ -2692,7 +2692,7 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
 // K' with short slices keeps the unit-staged kernels).
 static int enc_unit(const taco_index* idx) {
   const char* e = getenv("TACO_COUNT_TMA");   // read per index (tests pin both kernels)
-  if ((e && e[0] == '0') || idx->n_sub > 8 || idx->chunk > kClusterMaxChunk) return 0;
+  if ((e && e[0] == '0') || idx->n_sub > 8 || idx->chunk > kClusterWideChunk) return 0;
   const int U = idx->cluster_mode ? 8 : 4;
   const int64_t nsl = idx->nchunks * (int64_t)idx->kp * idx->kp;
   return (U - 1) * nsl <= idx->n ? U : 0;
@@ -2749,6 +2749,9 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<512>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterWideChunk / 2 + sizeof(uint32_t) * EcCfg<1024>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<1024, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_genc<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -2851,12 +2854,16 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
   if (idx->has_ccsr) {
     const char* fe = getenv("TACO_COUNT_FEED");   // =tma: the cp.async.bulk ring feed
     const int feed = (fe && !strcmp(fe, "tma")) ? 1 : 0;
-    const char* ne = getenv("TACO_COUNT_NT");   // 256 (3 CTAs per SM, default) or 512 (2 per SM)
-    const bool wide = ne && atoi(ne) == 512;
-    cfg.blockDim = dim3(feed ? TC_THREADS : wide ? 512 : 256, 1, 1);
+    const char* ne = getenv("TACO_COUNT_NT");   // 256 (3 CTAs per SM, default), 512 (2 per SM) or 1024 (1 per SM)
+    const int nt = ne ? atoi(ne) : 256;
+    const bool wide = nt == 512, huge = nt == 1024 || idx->chunk > kClusterMaxChunk;
+    cfg.blockDim = dim3(feed ? TC_THREADS : huge ? 1024 : wide ? 512 : 256, 1, 1);
     cfg.dynamicSmemBytes = table_bytes(idx) + (feed ? sizeof(uint4) * TC_RS * TC_SG
-                                                    : sizeof(uint32_t) * (wide ? EcCfg<512>::GC : EcCfg<256>::GC));
-    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma : wide ? k_count_enc<512, 2> : k_count_enc<256, 3>,
+                                                    : sizeof(uint32_t) * (huge ? EcCfg<1024>::GC
+                                                                          : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
+    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma
+                                             : huge ? k_count_enc<1024, 1>
+                                                    : wide ? k_count_enc<512, 2> : k_count_enc<256, 3>,
                                        (const uint16_t*)t.pops.as<uint16_t>(),
                                        (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
                                        (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
