@@ -2289,6 +2289,9 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
     sums_of(tb);                  // tile i + 1's ids arrived during tile i - 1
     if (i + 1 < nt) issue(tb, st[(i + 1) & 1]);
     else cp_async_commit();
+    // the running bound, loaded before the dot products hide its latency (a
+    // bound read early is only looser: qthr only decreases)
+    const unsigned long long thr = __ldcg(qthr + ta.q);
     cp_async_wait<1>();           // tile i's rows and query bytes have landed
     __syncwarp();
     const RiStage& s = st[i & 1];
@@ -2305,7 +2308,6 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
     const double v = (double)((int64_t)ta.xs - 2 * (int64_t)acc + (int64_t)ta.qs);
     unsigned long long key = lane < ta.m ? (unsigned long long)__double_as_longlong(v) : ~0ull;
     uint32_t id = ta.cid;
-    const unsigned long long thr = __ldcg(qthr + ta.q);
     const bool keep = key != ~0ull && key <= thr;
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
     const int ns = __popc(bal);
