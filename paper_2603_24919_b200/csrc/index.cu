@@ -65,6 +65,8 @@ void QueryTile::release() {
   for (auto* b : all) b->release();
   if (flags_h) cudaFreeHost(flags_h);
   flags_h = nullptr;
+  if (qev) cudaEventDestroy(qev);
+  qev = nullptr;
   cand_cap = 0;
 }
 

@@ -51,6 +51,8 @@ struct QueryTile {
   int64_t cand_cap = 0;
   int pop_cap = 0;
   int64_t front_rows = 0;       // rows the split-traversal buffers were sized for
+  bool fused = false;           // the tile ran k_count_fused: its answers are already in out_ids / out_d
+  cudaEvent_t qev = nullptr;    // q_u8_prep done (the fused-count decision reads flags[4])
   int64_t* flags_h = nullptr;   // pinned copy of flags[0..3] (async read-back)
   void release();
 };

@@ -2339,6 +2339,193 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------- fused count + re-rank
+// Cluster mode, N_s <= 8, u8 rows with d <= 128, every query u8-exact, k <=
+// 32 (config 2): k_count_enc's counting and Alg. 5, then, in the same CTA,
+// the exact integer re-rank of the chunk's candidates and the top-k -- no
+// candidate buffer round trip, no tile plan, no separate re-rank / top-k /
+// finalize launches.  After the compaction the 64 KB score table is dead and
+// becomes the warps' row staging; each warp re-ranks tiles of 32 candidates
+// (one row per lane, DP4A) and keeps its best 32 (d2, id) sorted across its
+// lanes (a tile is sorted and bitonic-merged in only when it beats the
+// current k-th); the CTA merges its warps' lists, and rank 0 of the cluster
+// merges the CTAs' lists over DSMEM and writes the query's answer.  Ties in
+// d2 go to the lower id (engine.py:275).
+__device__ __forceinline__ bool pair_less(unsigned long long ka, uint32_t ia, unsigned long long kb, uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+// (key, id) ascending across the warp's lanes in A; B sorted ascending: A
+// becomes the 32 smallest of A u B, sorted (bitonic merge)
+__device__ __forceinline__ void warp_merge_sorted(unsigned long long& ak, uint32_t& ai, unsigned long long bk,
+                                                  uint32_t bi) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long rk = __shfl_sync(0xffffffffu, bk, 31 - lane);   // B reversed: A ++ B^R is bitonic
+  const uint32_t ri = __shfl_sync(0xffffffffu, bi, 31 - lane);
+  if (pair_less(rk, ri, ak, ai)) {
+    ak = rk;
+    ai = ri;
+  }
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {   // half-cleaners: the bitonic 32 lowest, sorted
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ak, stride);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, ai, stride);
+    const bool lower = (lane & stride) == 0;
+    const bool other_less = pair_less(ok, oi, ak, ai);
+    if (lower ? other_less : (!other_less && !(ok == ak && oi == ai))) {
+      ak = ok;
+      ai = oi;
+    }
+  }
+}
+
+constexpr int FU_NT = 256;
+constexpr int FU_PITCH = 144;   // row staging pitch: 16 B mod 128, conflict-free 16-byte row reads
+// row staging + query bytes + warp lists, carved from the (then dead) table region
+constexpr int FU_SCRATCH = ((FU_NT / 32) * 32 * FU_PITCH + 128 + 12 * FU_NT + 1023) / 1024 * 1024;
+
+__global__ void __launch_bounds__(FU_NT, 3) k_count_fused(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ cnum, int32_t* __restrict__ lvl,
+    const uint8_t* __restrict__ Xb, int d, const uint8_t* __restrict__ Qb, const int32_t* __restrict__ qsq,
+    const int32_t* __restrict__ xsq, int k, int32_t* __restrict__ out_ids, float* __restrict__ out_d) {
+  constexpr int NT = FU_NT, GC = EcCfg<NT>::GC;
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<NT> S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t q = blockIdx.y;
+  const int rank = (int)cluster.block_rank();
+  const int csz = (int)cluster.num_blocks();
+  const int64_t c = rank;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  const int tbytes = (int)(chunk / 2);
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + max(tbytes, FU_SCRATCH));   // [GC]: staging, then the candidates
+  // after the compaction the table region holds: the warps' row staging
+  // (8 x 32 rows x FU_PITCH), the query bytes, the warp / CTA top lists
+  uint8_t* s_q = table + (NT / 32) * 32 * FU_PITCH;
+  unsigned long long (*s_key)[32] = reinterpret_cast<unsigned long long (*)[32]>(s_q + 128);
+  uint32_t (*s_id)[32] = reinterpret_cast<uint32_t (*)[32]>(s_q + 128 + sizeof(unsigned long long) * NT);
+  Tally T;
+  enc_count_phase<NT, 2>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S,
+                         T);
+  enc_levels<NT>(T, table, valid, n_sub, S);
+  cluster.sync();   // every CTA's level histogram is final
+  for (int l = tid; l <= n_sub; l += NT) {
+    int h = 0;
+    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
+    S.ge[l] = h;
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // done reading remote histograms
+  __syncthreads();
+  int64_t b = 0;
+  if (tid == 0) {
+    int64_t cands = 0;
+    const int L = alg5([&](int l) { return (int64_t)S.ge[l]; }, n_sub, budget, cands);
+    int64_t mine = 0;
+    for (int l = L; l <= n_sub; ++l) mine += S.lh[l];
+    S.L = L;
+    S.scnt = mine;
+    S.fill = 0;
+    if (rank == 0) {
+      cnum[q] = cands;
+      lvl[q] = L;
+    }
+    if (mine > GC) {   // more candidates than the staging holds: a global segment
+      b = (int64_t)atomicAdd((unsigned long long*)&flags[3], (unsigned long long)mine);
+      if (b + mine > cand_cap) flags[1] = 1;
+      S.sbase = b;
+    }
+  }
+  __syncthreads();
+  const int64_t mine = S.scnt;
+  const uint32_t* list = gaddr;
+  if (mine <= GC) {
+    compact_unordered<NT, true, true>(table, valid, (uint32_t)S.L, base, gaddr, &S.fill);
+  } else if (S.sbase + mine <= cand_cap) {
+    compact_unordered<NT, true, true>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
+    list = cand + S.sbase;
+  }
+  __syncthreads();   // the table is dead: row staging from here on
+  if (tid < 32 && d >= 16 * (tid + 1))
+    reinterpret_cast<uint4*>(s_q)[tid] = reinterpret_cast<const uint4*>(Qb + (size_t)q * d)[tid];
+  __syncthreads();
+  const bool ok_list = mine <= GC || S.sbase + mine <= cand_cap;
+  // ---- re-rank: warp w takes tiles w, w + 8, ... of the chunk's candidates
+  uint8_t* rows = table + (size_t)wid * 32 * FU_PITCH;
+  const int nc = d / 16;
+  const int32_t qs = qsq[q];
+  unsigned long long bk = ~0ull;   // this warp's best 32, sorted across lanes
+  uint32_t bi = 0xFFFFFFFFu;
+  const int r0 = lane >> 3, cl = lane & 7;
+  const int64_t ntile = ok_list ? (mine + 31) / 32 : 0;
+  for (int64_t tt = wid; tt < ntile; tt += NT / 32) {
+    const int64_t e = tt * 32 + lane;
+    const bool have = e < mine;
+    const uint32_t id = have ? list[e] : 0u;
+#pragma unroll
+    for (int j = 0; j < GR / 4; ++j) {   // rows j * 4 + r0, 8 lanes x 16 B per row
+      const int rr = j * 4 + r0;
+      const uint32_t rid = __shfl_sync(0xffffffffu, id, rr);
+      if (cl < nc && tt * 32 + rr < mine) cp_async16(rows + rr * FU_PITCH + cl * 16, Xb + (size_t)rid * d + cl * 16);
+    }
+    cp_async_commit();
+    const int32_t xs = have ? __ldg(xsq + id) : 0;
+    cp_async_wait<0>();
+    __syncwarp();
+    uint32_t acc = 0;
+    for (int cc = 0; cc < nc; ++cc) {
+      const uint4 xw = *reinterpret_cast<const uint4*>(rows + lane * FU_PITCH + cc * 16);
+      const uint4 qw = *reinterpret_cast<const uint4*>(s_q + cc * 16);
+      acc = __dp4a(xw.x, qw.x, acc);
+      acc = __dp4a(xw.y, qw.y, acc);
+      acc = __dp4a(xw.z, qw.z, acc);
+      acc = __dp4a(xw.w, qw.w, acc);
+    }
+    __syncwarp();   // the staging is refilled by the next tile
+    // every step of the reference's fp64 sum is exact on these integers
+    const double v = (double)((int64_t)xs - 2 * (int64_t)acc + (int64_t)qs);
+    unsigned long long key = have ? (unsigned long long)__double_as_longlong(v) : ~0ull;
+    uint32_t kid = have ? id : 0xFFFFFFFFu;
+    const unsigned long long kth = __shfl_sync(0xffffffffu, bk, k - 1);
+    const uint32_t kthi = __shfl_sync(0xffffffffu, bi, k - 1);
+    if (__any_sync(0xffffffffu, pair_less(key, kid, kth, kthi))) {
+      warp_sort_pairs(key, kid);
+      warp_merge_sorted(bk, bi, key, kid);
+    }
+  }
+  s_key[wid][lane] = bk;
+  s_id[wid][lane] = bi;
+  __syncthreads();
+  if (wid == 0) {   // the CTA's best 32
+    unsigned long long ak = s_key[0][lane];
+    uint32_t ai = s_id[0][lane];
+    for (int w = 1; w < NT / 32; ++w) warp_merge_sorted(ak, ai, s_key[w][lane], s_id[w][lane]);
+    s_key[0][lane] = ak;
+    s_id[0][lane] = ai;
+  }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");     // (histogram phase)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");   // my list is written
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (rank == 0 && wid == 0) {
+    unsigned long long ak = s_key[0][lane];
+    uint32_t ai = s_id[0][lane];
+    for (int r = 1; r < csz; ++r)
+      warp_merge_sorted(ak, ai, cluster.map_shared_rank(&s_key[0][0], r)[lane],
+                        cluster.map_shared_rank(&s_id[0][0], r)[lane]);
+    if (lane < k) {
+      const bool real = ak != ~0ull;
+      out_ids[q * k + lane] = real ? (int32_t)ai : -1;
+      out_d[q * k + lane] = real ? __double2float_rn(__dsqrt_rn(__longlong_as_double((long long)ak)))
+                                 : __int_as_float(0x7f800000);
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");   // rank 0 is done reading
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Generic rerank for d % 4 != 0: lane = row, direct loads.
 __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ X, int d,
                                                       const float* __restrict__ Qf,
@@ -2888,6 +3075,57 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
   return TACO_OK;
 }
 
+// The fused count + re-rank (k_count_fused) applies to this tile?  Needs the
+// encoded CSR in cluster mode, u8 rows with d <= 128 (d % 16 == 0), k <= 32
+// and every query u8-exact (q_u8_prep's flags[4], read back by the caller).
+// Opt-in (TACO_FUSED=1): measured slower at config 2 (10.9 ms against 5.6 +
+// 1.75 + 0.38 for the separate kernels) -- re-ranking per query inside the
+// count CTA loses the chunk-major order's L2 reuse of the candidate rows
+// (each row serves ~100 queries of a batch), so the rows stream from HBM.
+static bool fused_eligible(const taco_index* idx, int k) {
+  const char* e = getenv("TACO_FUSED");
+  return (e && e[0] == '1') && idx->cluster_mode && idx->has_ccsr && idx->cunit == 8 &&
+         idx->xfmt == TACO_ROWS_U8 && idx->d <= 128 && idx->d % 16 == 0 && k <= 32 && idx->Xsq.p;
+}
+
+static int cluster_count_fused(taco_index* idx, QueryTile& t, int64_t QS, double beta, int k, cudaStream_t st) {
+  TACO_TRY(set_count_attrs(idx));
+  static bool attr = false;
+  const size_t smem = (size_t)std::max<int64_t>(table_bytes(idx), FU_SCRATCH) + sizeof(uint32_t) * EcCfg<FU_NT>::GC;
+  if (!attr) {
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<FU_NT>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  const double budget = beta * (double)idx->n_global;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)idx->nchunks, (unsigned)QS, 1);
+  cfg.blockDim = dim3(FU_NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_c[1];
+  attr_c[0].id = cudaLaunchAttributeClusterDimension;
+  attr_c[0].val.clusterDim.x = (unsigned)idx->nchunks;
+  attr_c[0].val.clusterDim.y = 1;
+  attr_c[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_c;
+  cfg.numAttrs = 1;
+  ProfScope ps(K_COUNT, st);
+  TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_count_fused, (const uint16_t*)t.pops.as<uint16_t>(),
+                                     (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
+                                     (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
+                                     (const uint32_t*)idx->coffs.as<uint32_t>(), idx->n_sub, idx->K, idx->n,
+                                     idx->nchunks, idx->chunk, budget, t.cand.as<uint32_t>(), t.cand_cap,
+                                     t.flags.as<int64_t>(), t.cnum.as<int64_t>(), t.lvl.as<int32_t>(),
+                                     (const uint8_t*)idx->Xn.as<uint8_t>(), idx->d,
+                                     (const uint8_t*)t.qb.as<uint8_t>(), (const int32_t*)t.qsq.as<int32_t>(),
+                                     (const int32_t*)idx->Xsq.as<int32_t>(), k, t.out_ids.as<int32_t>(),
+                                     t.out_d.as<float>()));
+  TACO_LAUNCHED();
+  return TACO_OK;
+}
+
 // Tile plans: query-major output positions (t.bpref, for the top-k) and, in
 // cluster mode, the chunk-major processing order (t.ppref): all queries'
 // candidates in one id chunk are re-ranked before the next chunk, so the
@@ -3104,6 +3342,12 @@ static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total)
     g_prof.sumPops += v;
     g_prof.maxPops = std::max<int64_t>(g_prof.maxPops, v);
   }
+  if (t.fused) {   // the fused kernel keeps no global candidate count: |C| = candidate_num
+    std::vector<int64_t> cn((size_t)QS);
+    cudaMemcpy(cn.data(), t.cnum.p, 8 * cn.size(), cudaMemcpyDeviceToHost);
+    total = 0;
+    for (auto v : cn) total += v;
+  }
   g_prof.sumC += total;
   g_prof.queries += QS;
   g_prof.tiles += 1;
@@ -3124,20 +3368,43 @@ static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total)
 
 // Front half of a tile (queries already in t.Q): transform, ranks, traversal,
 // counting, Alg. 5, plans; flags read back asynchronously.
-static int tile_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, double beta, cudaStream_t st) {
+static int tile_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, double beta, int k,
+                      cudaStream_t st) {
   if (t.cand_cap == 0) {
     const int64_t est = QS * std::max<int64_t>(1024, (int64_t)(4.0 * beta * (double)idx->n_global)) + (1 << 20);
     TACO_TRY(ensure_cand(t, std::min<int64_t>(est, (int64_t)1 << 31)));
   }
   TACO_CHECK_CUDA(cudaMemsetAsync(t.flags.p, 0, sizeof(int64_t) * 8, st));
-  TACO_TRY(stage_front(idx, t, QS, alpha, st, nullptr));
+  const bool intp = idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled();
+  bool fuse = false;
+  t.fused = false;
+  if (intp && fused_eligible(idx, k)) {
+    // u8-exactness first (flags[4]): it decides the count kernel; the host
+    // waits only for this small kernel while the front runs on
+    TACO_TRY(q_u8_prep(idx, t, QS, st));
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h + 4, t.flags.as<int64_t>() + 4, sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, st));
+    if (!t.qev) TACO_CHECK_CUDA(cudaEventCreateWithFlags(&t.qev, cudaEventDisableTiming));
+    TACO_CHECK_CUDA(cudaEventRecord(t.qev, st));
+    TACO_TRY(stage_front(idx, t, QS, alpha, st, nullptr));
+    TACO_CHECK_CUDA(cudaEventSynchronize(t.qev));
+    fuse = t.flags_h[4] == 0;
+  } else {
+    TACO_TRY(stage_front(idx, t, QS, alpha, st, nullptr));
+  }
   if (idx->cluster_mode) {
-    TACO_TRY(cluster_count(idx, t, QS, beta, st));
+    if (fuse) TACO_TRY(cluster_count_fused(idx, t, QS, beta, k, st));
+    else TACO_TRY(cluster_count(idx, t, QS, beta, st));
   } else {
     TACO_TRY(global_count(idx, t, QS, st));
     TACO_TRY(global_select(idx, t, QS, t.hist.as<int64_t>(), beta, st));
   }
-  if (idx->xfmt == TACO_ROWS_U8 && int_rerank_enabled())   // integer re-rank eligibility -> flags[4]
+  if (fuse) {   // answers written by the count kernel: only the flags come back
+    t.fused = true;
+    TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, st));
+    return TACO_OK;
+  }
+  if (intp && !fused_eligible(idx, k))   // integer re-rank eligibility -> flags[4]
     TACO_TRY(q_u8_prep(idx, t, QS, st));
   return plan_async(idx, t, QS, st);
 }
@@ -3151,15 +3418,16 @@ static int tile_back(taco_index* idx, QueryTile& t, int64_t QS, double alpha, do
     if (fl[0] > t.pop_cap) {           // a traversal popped more cells than stored
       t.pop_cap = idx->K;
       TACO_TRY(t.pops.ensure(sizeof(uint16_t) * (size_t)QS * idx->n_sub * t.pop_cap));
-      TACO_TRY(tile_front(idx, t, QS, alpha, beta, st));
+      TACO_TRY(tile_front(idx, t, QS, alpha, beta, k, st));
       continue;
     }
     if (fl[1]) {                       // candidate buffer too small: grow to what was asked
       TACO_TRY(ensure_cand(t, fl[3] + fl[3] / 4 + 1024));
-      TACO_TRY(tile_front(idx, t, QS, alpha, beta, st));
+      TACO_TRY(tile_front(idx, t, QS, alpha, beta, k, st));
       continue;
     }
     prof_stats(idx, t, QS, fl[3]);
+    if (t.fused) return TACO_OK;       // k_count_fused already wrote the answers
     return rerank_stage(idx, t, QS, k, fl[2], st, true);
   }
   TACO_FAIL(TACO_ERR_CUDA, "query scratch did not converge");
@@ -3241,7 +3509,7 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
     cudaStream_t s = sts[pipe ? i & 1 : 0];
     const int64_t q0 = i * QT, QS = std::min<int64_t>(QT, nq - q0);
     TACO_CHECK_CUDA(cudaMemcpyAsync(t.Q.p, Q_src + (size_t)q0 * idx->d, sizeof(float) * (size_t)QS * idx->d, kin, s));
-    return tile_front(idx, t, QS, alpha, beta, s);
+    return tile_front(idx, t, QS, alpha, beta, k, s);
   };
   TACO_TRY(front(0));
   for (int64_t i = 0; i < ntile; ++i) {
@@ -3251,7 +3519,7 @@ static int query_batch_impl(taco_index* idx, const float* Q_src, bool src_host, 
     const int64_t q0 = i * QT, QS = std::min<int64_t>(QT, nq - q0);
     TACO_TRY(tile_back(idx, t, QS, alpha, beta, k, s));
     const int64_t tot = QS * k;
-    {
+    if (!t.fused) {
       ProfScope ps(K_FINAL, s);
       k_finalize<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), tot,
                                                               t.out_ids.as<int32_t>(), t.out_d.as<float>());

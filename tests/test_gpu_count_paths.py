@@ -108,11 +108,12 @@ def test_scores_tap_wide_levels(rig):
             assert hashlib.blake2b(sc.tobytes(), digest_size=16).hexdigest() == g[f"scores_digest_{gi}"][qi]
 
 
-@pytest.mark.parametrize("kernel", ["enc", "tma", "units"])
+@pytest.mark.parametrize("kernel", ["fused", "enc", "tma", "units"])
 @pytest.mark.parametrize("layout", ["cluster_1cta", "cluster_multi"])
 def test_cluster_count_kernels_extreme_budgets(kernel, layout, golden):
-    """The cluster count kernels (the encoded, padded CSR with direct loads or
-    the cp.async.bulk ring, and the unit-staged one) at budgets whose Alg. 5
+    """The cluster count kernels (the encoded, padded CSR with direct loads --
+    alone or fused with the integer re-rank and top-k -- or the cp.async.bulk
+    ring, and the unit-staged one) at budgets whose Alg. 5
     walk reaches level 1 (beta -> 1 with a small alpha: the level-1 count
     depends on the padding correction of the level-0 tally) and with almost
     every cell retrieved (alpha -> 1: slices far larger than a ring stage)."""
@@ -122,7 +123,8 @@ def test_cluster_count_kernels_extreme_budgets(kernel, layout, golden):
     oidx = O.deserialize(g["blob"].tobytes())
     env = dict(MODES[layout][0], TACO_COUNT_TMA="0" if kernel == "units" else "1")
     idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
-    feed = {"TACO_COUNT_FEED": "tma" if kernel == "tma" else "enc"}
+    feed = {"TACO_COUNT_FEED": "tma" if kernel == "tma" else "enc",
+            "TACO_FUSED": "1" if kernel == "fused" else "0"}
     for alpha, beta, k in ((0.999, 0.999, 7), (0.5, 0.2, 10), (0.02, 0.999, 3), (0.999, 0.001, 5)):
         oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, beta, k, threads=8)
         ids, dists, num, lvl = _with_env(feed, lambda: T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k)))
