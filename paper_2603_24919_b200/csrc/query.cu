@@ -2242,6 +2242,7 @@ struct RiTile {
   int32_t xs = 0, qs = 0;
 };
 
+template <int NC>   // 16-byte chunks per row (d / 16); 0 = runtime d
 __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
     const uint8_t* __restrict__ Xb, int d, const uint8_t* __restrict__ Qb, const int32_t* __restrict__ qsq,
     const int32_t* __restrict__ xsq, const int4* __restrict__ desc, const uint32_t* __restrict__ cand,
@@ -2253,7 +2254,7 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
   const int64_t gw = (int64_t)wid * gridDim.x + blockIdx.x, nw = (int64_t)gridDim.x * RI_WARPS;
   if (gw >= ntiles) return;
   const int64_t nt = (ntiles - gw + nw - 1) / nw;   // my tiles: gw + i * nw
-  const int nc = d / 16;                             // 16-byte chunks per row
+  const int nc = NC ? NC : d / 16;                   // 16-byte chunks per row
   auto dsc = [&](int64_t i) { return i < nt ? __ldg(desc + gw + i * nw) : make_int4(0, 0, 0, 0); };
   auto ids_of = [&](const int4 dd, RiTile& r) {   // tile fields + this lane's candidate id
     r.m = dd.z & 63;
@@ -3270,11 +3271,12 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
       const size_t smem = sizeof(RiStage) * 2 * RI_WARPS;
       static bool attr = false;
       if (!attr) {
-        TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_i8<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TACO_CHECK_CUDA(cudaFuncSetAttribute(k_rerank_i8<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
       }
       const int64_t grid = std::min<int64_t>(ceil_div(ntiles, RI_WARPS), (int64_t)num_sms() * RI_CTAS);
-      k_rerank_i8<<<(unsigned)grid, 32 * RI_WARPS, smem, st>>>(static_cast<const uint8_t*>(Xn), d, ir.Qb, ir.qsq,
+      (d == 128 ? k_rerank_i8<8> : k_rerank_i8<0>)<<<(unsigned)grid, 32 * RI_WARPS, smem, st>>>(static_cast<const uint8_t*>(Xn), d, ir.Qb, ir.qsq,
                                                                 ir.xsq, desc, cand, ntiles, kk, pk,
                                                                 pid.as<uint32_t>(), qthr);
     } else if (fmt == TACO_ROWS_U8) {
