@@ -1092,7 +1092,7 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
 // compacts into `stage` (shared memory, scap ids) and copies the segment out
 // coalesced once the base is known (direct global writes when it is larger).
 template <int NT>
-__device__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
+__device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
                              cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
                              uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
                              int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
@@ -1327,13 +1327,14 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
   chunk_levels(table, valid, n_sub, S);
 }
 
-template <int NT, int MINB>
+template <int NT, int MINB, int NSC = 0>   // NSC: N_s at compile time (0 = runtime)
 __global__ void __launch_bounds__(NT, MINB) k_count_enc(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
-    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub, int K2,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub_rt, int K2,
     int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
     int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
     int64_t* __restrict__ cnum, int32_t* __restrict__ lvl) {
+  const int n_sub = NSC ? NSC : n_sub_rt;
   extern __shared__ __align__(16) uint8_t table[];
   __shared__ EncSmem<NT> S;
   cg::cluster_group cluster = cg::this_cluster();
@@ -2936,6 +2937,9 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<512>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -3053,7 +3057,8 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
                                                                           : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
     TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma
                                              : huge ? k_count_enc<1024, 1>
-                                                    : wide ? k_count_enc<512, 2> : k_count_enc<256, 3>,
+                                                    : wide ? k_count_enc<512, 2>
+                                                    : idx->n_sub == 8 ? k_count_enc<256, 3, 8> : k_count_enc<256, 3>,
                                        (const uint16_t*)t.pops.as<uint16_t>(),
                                        (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
                                        (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
