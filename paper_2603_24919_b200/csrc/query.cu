@@ -508,6 +508,16 @@ struct Tally {
     else if (old < 12) a2 += inc;
     else a3 += inc;
   }
+  // levels 8..15 of the encoded kernels' wide tallies (a0 / a1 hold 0..7 as in add_round)
+  __device__ __forceinline__ void add_round_hi(uint32_t ev, uint32_t od) {
+    a2 += ((uint64_t)__byte_perm(ev, 0, 0x4342) << 32) | __byte_perm(ev, 0, 0x4140);
+    a3 += ((uint64_t)__byte_perm(od, 0, 0x4342) << 32) | __byte_perm(od, 0, 0x4140);
+  }
+  __device__ __forceinline__ int level2(int l) const {   // add_round / add_round_hi layout, l <= 15
+    const int b = l & 7;
+    const uint64_t w = l < 8 ? ((b & 1) ? a1 : a0) : ((b & 1) ? a3 : a2);
+    return (int)((w >> (16 * (b >> 1))) & 0xFFFFull);
+  }
   __device__ __forceinline__ int level(int l, bool small) const {   // tally of level l
     if (small) {
       const uint64_t w = (l & 1) ? a1 : a0;
@@ -1071,6 +1081,27 @@ __device__ __forceinline__ void apply_group(const uint4 e, uint32_t tsg, uint32_
   od += (u4 >> 4) & 0x0F0F0F0Fu;
 }
 
+// N_s 9..16: old values up to 15 -> 16 tally levels, 4-bit fields in two
+// words (r < 8: lo, else hi; the clamped shifts drop the other word's share).
+// Works for nibble and byte lanes (the lane value is < 16 either way).
+__device__ __forceinline__ void apply_group_w(const uint4 e, uint32_t tsg, uint32_t& ev, uint32_t& od,
+                                              uint32_t& evh, uint32_t& odh) {
+  const uint32_t s0 = e.x & 63u, s1 = e.y & 63u, s2 = e.z & 63u, s3 = e.w & 63u;
+  const uint32_t o0 = smem_atomic_add(tsg + (e.x >> 6), shl_clamp(1u, s0));
+  const uint32_t o1 = smem_atomic_add(tsg + (e.y >> 6), shl_clamp(1u, s1));
+  const uint32_t o2 = smem_atomic_add(tsg + (e.z >> 6), shl_clamp(1u, s2));
+  const uint32_t o3 = smem_atomic_add(tsg + (e.w >> 6), shl_clamp(1u, s3));
+  const uint32_t t0 = (shr_clamp(o0, s0) & 15u) << 2, t1 = (shr_clamp(o1, s1) & 15u) << 2,
+                 t2 = (shr_clamp(o2, s2) & 15u) << 2, t3 = (shr_clamp(o3, s3) & 15u) << 2;
+  const uint32_t lo = shl_clamp(1u, t0) + shl_clamp(1u, t1) + shl_clamp(1u, t2) + shl_clamp(1u, t3);
+  const uint32_t hi = shl_clamp(1u, t0 - 32u) + shl_clamp(1u, t1 - 32u) + shl_clamp(1u, t2 - 32u) +
+                      shl_clamp(1u, t3 - 32u);
+  ev += lo & 0x0F0F0F0Fu;
+  od += (lo >> 4) & 0x0F0F0F0Fu;
+  evh += hi & 0x0F0F0F0Fu;
+  odh += (hi >> 4) & 0x0F0F0F0Fu;
+}
+
 template <int NT>
 struct EncSmem {
   uint64_t full[8], empty[8];   // k_count_tma ring
@@ -1083,7 +1114,7 @@ struct EncSmem {
   int lh[256];
 };
 
-template <int NT>
+template <int NT, bool WIDE>
 __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S);
 
 // tallies -> level histogram, cluster exchange, Alg. 5, compaction (the
@@ -1091,7 +1122,7 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
 // candidate segment with one global atomic; while it is in flight the CTA
 // compacts into `stage` (shared memory, scap ids) and copies the segment out
 // coalesced once the base is known (direct global writes when it is larger).
-template <int NT>
+template <int NT, bool NIB = true, bool WIDE = false>
 __device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
                              cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
                              uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
@@ -1100,7 +1131,7 @@ __device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int
   const int tid = threadIdx.x;
   const int rank = (int)cluster.block_rank();
   const int csz = (int)cluster.num_blocks();
-  enc_levels<NT>(T, table, valid, n_sub, S);
+  enc_levels<NT, WIDE>(T, table, valid, n_sub, S);
   cluster.sync();   // every CTA's level histogram is final
   for (int l = tid; l <= n_sub; l += NT) {
     int h = 0;
@@ -1131,14 +1162,15 @@ __device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int
   __syncthreads();
   const int64_t mine = S.scnt;
   if (mine <= scap) {
-    compact_unordered<NT, true, EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
+    compact_unordered<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
     if (tid == 0) S.sbase = b;
     __syncthreads();
     const int64_t sb = S.sbase;
     if (sb + mine <= cand_cap)
       for (int i = tid; i < (int)mine; i += NT) cand[sb + i] = stage[i];
   } else if (S.sbase + mine <= cand_cap) {
-    compact_unordered<NT, true, EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, cand + S.sbase, &S.fill);
+    compact_unordered<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, cand + S.sbase,
+                                                              &S.fill);
   }
   if (tid == 0) {
     if (S.sbase + mine > cand_cap) flags[1] = 1;
@@ -1151,13 +1183,14 @@ __device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int
 // pop g of query q (flattened over subspaces; jpref = the subspaces' pop
 // prefix, in registers): its slice's (first unit, unit count, padding) in
 // chunk c and its subspace js
+template <int JM>   // subspaces held in jpref (>= N_s)
 __device__ __forceinline__ void enc_slice(const uint16_t* __restrict__ pops, const uint32_t* __restrict__ coffs,
                                           size_t offs_len, int cap, int n_sub, int K2, int64_t q, int64_t c,
-                                          const int (&jpref)[8], int g, uint32_t& g0, uint32_t& ng, uint32_t& pad,
+                                          const int (&jpref)[JM], int g, uint32_t& g0, uint32_t& ng, uint32_t& pad,
                                           uint32_t& js) {
   int j = 0, jb = 0;
 #pragma unroll
-  for (int jj = 1; jj < 8; ++jj)
+  for (int jj = 1; jj < JM; ++jj)
     if (jj < n_sub && g >= jpref[jj]) {
       j = jj;
       jb = jpref[jj];
@@ -1186,7 +1219,7 @@ struct EcCfg {
 // zeroed and filled, tallies in T, padding entries counted in S.pads.  UW =
 // 16-byte words per unit (2: cluster mode's 8-entry units, 1: global mode's
 // 4-entry units).  Staging: gaddr[EcCfg<NT>::GC].
-template <int NT, int UW>
+template <int NT, int UW, bool WIDE = false>
 __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop,
                                                 int cap, const uint32_t* __restrict__ cenc, size_t cstride,
                                                 const uint32_t* __restrict__ coffs, int n_sub, int K2, int64_t nchunks,
@@ -1213,11 +1246,12 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
   }
   __syncthreads();
   const int P_all = S.jpref[n_sub];
-  int jp[8];
+  constexpr int JM = WIDE ? 16 : 8;
+  int jp[JM];
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) jp[jj] = S.jpref[jj];
+  for (int jj = 0; jj < JM; ++jj) jp[jj] = S.jpref[jj];
   const uint32_t tsg = smem_u32(table);
-  uint32_t ev = 0, od = 0;
+  uint32_t ev = 0, od = 0, evh = 0, odh = 0;
   int pads = 0;
   for (int b0 = 0; b0 < P_all; b0 += NT * PER) {
     uint32_t ga[PER], ng[PER];   // unit index of the slice start, unit count
@@ -1262,8 +1296,13 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
         }
       };
       auto apply = [&](const uint4& x0, const uint4& x1) {
-        apply_group(x0, tsg, ev, od);
-        if (UW == 2) apply_group(x1, tsg, ev, od);
+        if (WIDE) {
+          apply_group_w(x0, tsg, ev, od, evh, odh);
+          if (UW == 2) apply_group_w(x1, tsg, ev, od, evh, odh);
+        } else {
+          apply_group(x0, tsg, ev, od);
+          if (UW == 2) apply_group(x1, tsg, ev, od);
+        }
       };
       int k = tid;
       fetch(k, a0, a1);
@@ -1286,7 +1325,8 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
         }
       }
       T.add_round(ev, od);   // <= 4 UW per unit, <= 8 units per thread per round: 8-bit fields
-      ev = od = 0;
+      if (WIDE) T.add_round_hi(evh, odh);
+      ev = od = evh = odh = 0;
       __syncthreads();
     }
   }
@@ -1296,26 +1336,30 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
 
 // tallies -> the chunk's level histogram S.ge / S.lh (packed reduction as in
 // enc_epilogue; padding entries taken off level 0)
-template <int NT>
+template <int NT, bool WIDE>
 __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S) {
   const int tid = threadIdx.x, lane = tid & 31;
-  uint64_t a0 = T.a0, a1 = T.a1;
+  Tally P = T;
   constexpr uint64_t HI3 = 0xE000E000E000E000ull;
-  if (!__any_sync(0xffffffffu, ((a0 | a1) & HI3) != 0)) {
+  const uint64_t any = P.a0 | P.a1 | (WIDE ? P.a2 | P.a3 : 0ull);
+  if (!__any_sync(0xffffffffu, (any & HI3) != 0)) {
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      P.a0 += __shfl_xor_sync(0xffffffffu, P.a0, o);
+      P.a1 += __shfl_xor_sync(0xffffffffu, P.a1, o);
+      if (WIDE) {
+        P.a2 += __shfl_xor_sync(0xffffffffu, P.a2, o);
+        P.a3 += __shfl_xor_sync(0xffffffffu, P.a3, o);
+      }
     }
     if ((lane & 7) == 0)
       for (int l = 1; l <= n_sub; ++l) {
-        const uint64_t w = ((l - 1) & 1) ? a1 : a0;
-        const int x = (int)((w >> (16 * ((l - 1) >> 1))) & 0xFFFFull);
+        const int x = P.level2(l - 1);
         if (x) atomicAdd(&S.ge[l], x);
       }
   } else {
     for (int l = 1; l <= n_sub; ++l) {
-      int x = T.level(l - 1, true);
+      int x = T.level2(l - 1);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       if (lane == 0 && x) atomicAdd(&S.ge[l], x);
@@ -1327,7 +1371,9 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
   chunk_levels(table, valid, n_sub, S);
 }
 
-template <int NT, int MINB, int NSC = 0>   // NSC: N_s at compile time (0 = runtime)
+// NSC: N_s at compile time (0 = runtime); NIB: 4-bit lanes (else 8-bit, N_s = 16);
+// WIDE: N_s > 8 (16 tally levels)
+template <int NT, int MINB, int NSC = 0, bool NIB = true, bool WIDE = false>
 __global__ void __launch_bounds__(NT, MINB) k_count_enc(
     const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
     const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub_rt, int K2,
@@ -1342,12 +1388,12 @@ __global__ void __launch_bounds__(NT, MINB) k_count_enc(
   const int64_t c = cluster.block_rank();
   const int64_t base = c * chunk;
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
-  const int tbytes = (int)(chunk / 2);
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
   uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
   Tally T;
-  enc_count_phase<NT, 2>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S,
-                         T);
-  enc_epilogue<NT>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
+  enc_count_phase<NT, 2, WIDE>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table,
+                               gaddr, S, T);
+  enc_epilogue<NT, NIB, WIDE>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
                    lvl, gaddr, EcCfg<NT>::GC);
 }
 
@@ -1371,7 +1417,7 @@ __global__ void __launch_bounds__(NT, MINB) k_count_genc(
   Tally T;
   enc_count_phase<NT, 1>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S, T);
   if (threadIdx.x == 0) S.fill = 0;
-  enc_levels<NT>(T, table, valid, n_sub, S);   // ends with a barrier
+  enc_levels<NT, false>(T, table, valid, n_sub, S);   // ends with a barrier
   if (scores && n_sub >= 2 && valid - S.lh[0] - S.lh[1] <= rec_cap)
     compact_records<NT, true>(table, valid, reinterpret_cast<uint32_t*>(scores + ((size_t)q * nchunks + c) * tbytes),
                               &S.fill);
@@ -1554,7 +1600,7 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
                                                     const uint32_t* __restrict__ offs, size_t offs_len,
                                                     int64_t nsl, int K2, int64_t n, int64_t chunk,
                                                     const uint32_t* __restrict__ bsum, uint32_t* __restrict__ coffs,
-                                                    uint32_t* __restrict__ cenc, size_t cstride, int U) {
+                                                    uint32_t* __restrict__ cenc, size_t cstride, int U, int nib) {
   __shared__ uint32_t wtot[CC_NT / 32];
   const int j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * CC_NT + threadIdx.x;
@@ -1578,7 +1624,8 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
       uint32_t v = EC_SENT;
       if (e < len) {
         const uint32_t p = (uint32_t)(I[e] - cbase);
-        v = ((p >> 3) << 8) | ((p & 7u) << 2);
+        // table word byte offset << 6 | lane shift (4-bit or 8-bit lanes)
+        v = nib ? ((p >> 3) << 8) | ((p & 7u) << 2) : ((p >> 2) << 8) | ((p & 3u) << 3);
       }
       E[e] = v;
     }
@@ -2413,7 +2460,7 @@ __global__ void __launch_bounds__(FU_NT, 3) k_count_fused(
   Tally T;
   enc_count_phase<NT, 2>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table, gaddr, S,
                          T);
-  enc_levels<NT>(T, table, valid, n_sub, S);
+  enc_levels<NT, false>(T, table, valid, n_sub, S);
   cluster.sync();   // every CTA's level histogram is final
   for (int l = tid; l <= n_sub; l += NT) {
     int h = 0;
@@ -2883,7 +2930,8 @@ static int stage_front(taco_index* idx, QueryTile& t, int64_t QS, double alpha, 
 // K' with short slices keeps the unit-staged kernels).
 static int enc_unit(const taco_index* idx) {
   const char* e = getenv("TACO_COUNT_TMA");   // read per index (tests pin both kernels)
-  if ((e && e[0] == '0') || idx->n_sub > 8 || idx->chunk > kClusterWideChunk) return 0;
+  // cluster mode: N_s <= 16 (4-bit lanes to 15, 8-bit lanes at 16); global mode: N_s <= 8
+  if ((e && e[0] == '0') || idx->n_sub > (idx->cluster_mode ? 16 : 8) || idx->chunk > kClusterWideChunk) return 0;
   const int U = idx->cluster_mode ? 8 : 4;
   const int64_t nsl = idx->nchunks * (int64_t)idx->kp * idx->kp;
   return (U - 1) * nsl <= idx->n ? U : 0;
@@ -2915,7 +2963,8 @@ int build_count_csr(taco_index* idx) {
   TACO_LAUNCHED();
   k_ccsr_fill<<<dim3((unsigned)nb, (unsigned)idx->n_sub), CC_NT, 0, st>>>(
       idx->ids.as<uint32_t>(), idx->offs.as<uint32_t>(), offs_len, nsl, (int)K2, idx->n, idx->chunk,
-      bsum.as<uint32_t>(), idx->coffs.as<uint32_t>(), idx->cenc.as<uint32_t>(), idx->cstride, U);
+      bsum.as<uint32_t>(), idx->coffs.as<uint32_t>(), idx->cenc.as<uint32_t>(), idx->cstride, U,
+      nib_tables(idx) ? 1 : 0);
   TACO_LAUNCHED();
   TACO_CHECK_CUDA(cudaStreamSynchronize(st));
   bsum.release();
@@ -2940,6 +2989,16 @@ static int set_count_attrs(taco_index*) {
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 0, true, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<256>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 0, true, true>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 16, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kClusterMaxChunk8 + sizeof(uint32_t) * EcCfg<256>::GC)));
+    TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<256, 3, 16, false, true>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kClusterMaxChunk / 2 + sizeof(uint32_t) * EcCfg<512>::GC)));
     TACO_CHECK_CUDA(cudaFuncSetAttribute(k_count_enc<512, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -3050,15 +3109,19 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
     const int feed = (fe && !strcmp(fe, "tma")) ? 1 : 0;
     const char* ne = getenv("TACO_COUNT_NT");   // 256 (3 CTAs per SM, default), 512 (2 per SM) or 1024 (1 per SM)
     const int nt = ne ? atoi(ne) : 256;
-    const bool wide = nt == 512, huge = nt == 1024 || idx->chunk > kClusterMaxChunk;
-    cfg.blockDim = dim3(feed ? TC_THREADS : huge ? 1024 : wide ? 512 : 256, 1, 1);
-    cfg.dynamicSmemBytes = table_bytes(idx) + (feed ? sizeof(uint4) * TC_RS * TC_SG
-                                                    : sizeof(uint32_t) * (huge ? EcCfg<1024>::GC
-                                                                          : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
-    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, feed ? k_count_tma
-                                             : huge ? k_count_enc<1024, 1>
-                                                    : wide ? k_count_enc<512, 2>
-                                                    : idx->n_sub == 8 ? k_count_enc<256, 3, 8> : k_count_enc<256, 3>,
+    const bool big = idx->n_sub > 8;   // 16 tally levels (4-bit lanes to N_s = 15, 8-bit at 16)
+    const bool wide = !big && nt == 512, huge = !big && (nt == 1024 || idx->chunk > kClusterMaxChunk);
+    const bool tfeed = feed && !big;
+    cfg.blockDim = dim3(tfeed ? TC_THREADS : huge ? 1024 : wide ? 512 : 256, 1, 1);
+    cfg.dynamicSmemBytes = table_bytes(idx) + (tfeed ? sizeof(uint4) * TC_RS * TC_SG
+                                                     : sizeof(uint32_t) * (huge ? EcCfg<1024>::GC
+                                                                           : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
+    auto kern = tfeed ? k_count_tma
+                : big ? (nib_tables(idx) ? k_count_enc<256, 3, 0, true, true> : k_count_enc<256, 3, 16, false, true>)
+                : huge ? k_count_enc<1024, 1>
+                : wide ? k_count_enc<512, 2>
+                : idx->n_sub == 8 ? k_count_enc<256, 3, 8> : k_count_enc<256, 3>;
+    TACO_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern,
                                        (const uint16_t*)t.pops.as<uint16_t>(),
                                        (const int32_t*)t.npop.as<int32_t>(), t.pop_cap,
                                        (const uint32_t*)idx->cenc.as<uint32_t>(), idx->cstride,
@@ -3090,7 +3153,7 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
 // (each row serves ~100 queries of a batch), so the rows stream from HBM.
 static bool fused_eligible(const taco_index* idx, int k) {
   const char* e = getenv("TACO_FUSED");
-  return (e && e[0] == '1') && idx->cluster_mode && idx->has_ccsr && idx->cunit == 8 &&
+  return (e && e[0] == '1') && idx->cluster_mode && idx->n_sub <= 8 && idx->has_ccsr && idx->cunit == 8 &&
          idx->xfmt == TACO_ROWS_U8 && idx->d <= 128 && idx->d % 16 == 0 && k <= 32 && idx->Xsq.p;
 }
 

@@ -132,3 +132,24 @@ def test_cluster_count_kernels_extreme_budgets(kernel, layout, golden):
         np.testing.assert_array_equal(lvl, ol)
         np.testing.assert_array_equal(ids, oi)
         np.testing.assert_array_equal(dists, od)
+
+
+@pytest.mark.parametrize("n_sub", [12, 15])
+@pytest.mark.parametrize("layout", ["cluster_1cta", "cluster_multi"])
+def test_wide_tallies_nibble_tables(n_sub, layout):
+    """N_s 9..15: 4-bit tables with 16 tally levels (the encoded kernel's wide
+    path); a GPU-built index answered by the GPU and by the oracle on the same
+    v1 bytes (rigs 2/4/5 cover N_s = 8, 16 and 20)."""
+    X, Q, _ = make_config(2, n=12000, nq=40, d=4 * n_sub)
+    idx = _with_env(MODES[layout][0], lambda: T.build_index(
+        X, T.IndexParams(n_subspaces=n_sub, subspace_dim=4, clusters=64, kmeans_iters=5, seed=3)))
+    chunk, nch, cluster = nat.index_layout(_device_of(idx).h)
+    assert cluster and nch >= MODES[layout][1][1]
+    oidx = O.deserialize(T.serialize_index(idx))
+    for alpha, beta, k in ((0.05, 0.01, 10), (0.3, 0.05, 7)):
+        oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, beta, k, threads=8)
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k))
+        np.testing.assert_array_equal(num, on)
+        np.testing.assert_array_equal(lvl, ol)
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(dists, od)
