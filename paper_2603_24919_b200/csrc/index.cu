@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstring>
 #include <chrono>
+#include <emmintrin.h>
 #include <mutex>
 #include <condition_variable>
 #include <functional>
@@ -367,6 +368,32 @@ static std::mutex g_stage_mu;
 static char* g_stage[kStages] = {nullptr, nullptr, nullptr};
 static cudaEvent_t g_stage_ev[kStages] = {nullptr, nullptr, nullptr};
 
+// memcpy into the pinned staging with non-temporal 16-byte stores: the
+// destination lines are not read for ownership first (the staging is written
+// once and then read by the DMA engine), so the host memory traffic of the
+// copy drops from ~3x to 2x the bytes moved.
+static void stream_copy(char* dst, const char* src, size_t len) {
+  size_t i = 0;
+  const size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+  if (head) {
+    const size_t h = std::min(head, len);
+    memcpy(dst, src, h);
+    i = h;
+  }
+  for (; i + 64 <= len; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), e);
+  }
+  if (i < len) memcpy(dst + i, src + i, len - i);
+  _mm_sfence();
+}
+
 // Host copy workers for the staged upload: plain threads that BLOCK between
 // jobs (an OpenMP team would spin for ~100 ms after each region and starve
 // the launch thread of the build that follows).
@@ -411,7 +438,7 @@ class CopyPool {
         len = len_;
       }
       const size_t a0 = len * t / n, a1 = len * (t + 1) / n;
-      memcpy(d + a0, s + a0, a1 - a0);
+      stream_copy(d + a0, s + a0, a1 - a0);
       std::lock_guard<std::mutex> lk(mu_);
       if (--pending_ == 0) done_.notify_one();
     }

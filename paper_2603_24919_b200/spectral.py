@@ -147,7 +147,12 @@ def jacobi_eigh(matrix, tol_rel: float = JACOBI_TOL_REL, max_sweeps: int = JACOB
     A = np.ascontiguousarray((A + A.T) / 2.0)
     if d <= 1:
         return np.diag(A).copy(), np.eye(d)
-    tol = tol_rel * float(np.linalg.norm(A, "fro"))
+    # ||A||_F without BLAS: np.linalg.norm routes through a threaded OpenBLAS
+    # ddot (n > 10^4), whose worker threads then spin for ~0.1 s and starve
+    # the staged upload of the next build of host cores (30 ms instead of 9).
+    # The threshold differs from it at most in the last bits, as the threaded
+    # ddot's own value does between machines with different core counts.
+    tol = tol_rel * math.sqrt(float(np.sum(A * A)))
     V = np.empty((d, d))
     sweeps = np.zeros(1, np.int32)
     resid = np.zeros(1)
