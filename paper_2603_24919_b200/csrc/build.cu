@@ -436,21 +436,29 @@ __device__ double np_combine(const double* leaf, int64_t n) {
 // fp64 add and the scan resumes from it.  There are ~log2(S / c_0) binade
 // changes, so the work is one pass over p plus O(log n) short restarts.
 constexpr int CX_V = 16;   // elements per thread per chunk
-__device__ void cumsum_exact_block(const double* __restrict__ best, double total, int64_t n, double* __restrict__ cdf) {
+// The range form: c_k = fl(c_{k-1} + p_k) for k in [i0, i1), starting from
+// c_in (started = false: the range begins the cumsum, c_{i0} = p_{i0}).  Writes
+// cdf[k - i0] when cdf is non-null; returns the last value (every thread).
+__device__ double cumsum_exact_range(const double* __restrict__ best, double total, int64_t i0, int64_t i1,
+                                     double c_in, bool started, double* __restrict__ cdf) {
   // p_k = best_k / total (numpy's elementwise division), formed on the fly
   auto P = [&](int64_t k) { return __ddiv_rn(__ldcg(best + k), total); };
   __shared__ double s_crun;
-  __shared__ long long s_i, s_stop;
+  __shared__ long long s_i, s_stop, s_pq;
   __shared__ long long s_wq[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NT = blockDim.x, NW = NT >> 5;
   if (tid == 0) {
     // head: sequential until the running value is a normal double well above underflow
-    double c = P(0);
-    cdf[0] = c;
-    int64_t i = 1;
-    while (i < n && !(c >= 0x1p-900)) {
+    double c = c_in;
+    int64_t i = i0;
+    if (!started && i < i1) {
+      c = P(i);
+      if (cdf) cdf[0] = c;
+      ++i;
+    }
+    while (i < i1 && !(c >= 0x1p-900)) {
       c = __dadd_rn(c, P(i));
-      cdf[i] = c;
+      if (cdf) cdf[i - i0] = c;
       ++i;
     }
     s_crun = c;
@@ -459,15 +467,15 @@ __device__ void cumsum_exact_block(const double* __restrict__ best, double total
   }
   __syncthreads();
   while (true) {
-    const int64_t i0 = s_i;
-    if (i0 >= n) break;
+    const int64_t ib = s_i;
+    if (ib >= i1) break;
     const double crun = s_crun;
     const int e = ilogb(crun);
     const double g = scalbn(1.0, e - 52), inv = scalbn(1.0, 52 - e);
     const long long Qlim = (long long)__dmul_rn(__dsub_rn(scalbn(1.0, e + 1), crun), inv);   // exact
     long long Qbase = 0;
     long long stop = LLONG_MAX;
-    for (int64_t j0 = i0; j0 < n; j0 += (int64_t)NT * CX_V) {
+    for (int64_t j0 = ib; j0 < i1; j0 += (int64_t)NT * CX_V) {
       long long lp[CX_V];
       long long tsum = 0;
       int tie = CX_V;
@@ -475,13 +483,13 @@ __device__ void cumsum_exact_block(const double* __restrict__ best, double total
 #pragma unroll
       for (int v = 0; v < CX_V; ++v) {
         const int64_t k = j0 + (int64_t)tid * CX_V + v;
-        bv[v] = k < n ? __ldcg(best + k) : 0.0;
+        bv[v] = k < i1 ? __ldcg(best + k) : 0.0;
       }
 #pragma unroll
       for (int v = 0; v < CX_V; ++v) {
         const int64_t k = j0 + (int64_t)tid * CX_V + v;
         long long q = 0;
-        if (k < n) {
+        if (k < i1) {
           const double t = __dmul_rn(__ddiv_rn(bv[v], total), inv);   // p_k, then exact power-of-two scaling
           if (t >= 0x1p60) {
             q = 1LL << 60;                         // certainly leaves the binade
@@ -518,34 +526,58 @@ __device__ void cumsum_exact_block(const double* __restrict__ best, double total
 #pragma unroll
       for (int v = 0; v < CX_V; ++v) {
         const int64_t k = j0 + (int64_t)tid * CX_V + v;
-        if (k < n && (excl + lp[v] >= Qlim || v == tie)) {
+        if (k < i1 && (excl + lp[v] >= Qlim || v == tie)) {
           atomicMin(&s_stop, (long long)k);
           break;
         }
       }
       __syncthreads();
       stop = s_stop;
+      {
+        // the owner of the stop element records the quotient prefix before it
+        const int64_t rel = stop - j0 - (int64_t)tid * CX_V;
+        if (rel >= 0 && rel < CX_V) {
+          long long pq = excl;
 #pragma unroll
-      for (int v = 0; v < CX_V; ++v) {
-        const int64_t k = j0 + (int64_t)tid * CX_V + v;
-        if (k < n && k < stop) cdf[k] = __dadd_rn(crun, __dmul_rn((double)(excl + lp[v]), g));   // exact
+          for (int v = 0; v < CX_V; ++v)
+            if (v < rel) pq = excl + lp[v];
+          s_pq = pq;
+        }
       }
-      __syncthreads();   // s_wq / s_stop reuse, cdf visible
+      if (cdf) {
+#pragma unroll
+        for (int v = 0; v < CX_V; ++v) {
+          const int64_t k = j0 + (int64_t)tid * CX_V + v;
+          if (k < i1 && k < stop) cdf[k - i0] = __dadd_rn(crun, __dmul_rn((double)(excl + lp[v]), g));   // exact
+        }
+      }
+      __syncthreads();   // s_wq / s_stop / s_pq, cdf visible
       if (stop != LLONG_MAX) break;
       Qbase += chunk_tot;
     }
-    if (stop == LLONG_MAX) break;   // ran to the end inside this binade
     if (tid == 0) {
-      const double prev = stop == i0 ? crun : cdf[stop - 1];
-      const double c = __dadd_rn(prev, P(stop));   // the element that leaves the binade (or ties)
-      cdf[stop] = c;
-      s_crun = c;
-      s_i = stop + 1;
-      s_stop = LLONG_MAX;
+      if (stop == LLONG_MAX) {
+        // ran to the end inside this binade: c = crun + g * Q (exact)
+        s_crun = __dadd_rn(crun, __dmul_rn((double)Qbase, g));
+        s_i = i1;
+      } else {
+        const double prev = __dadd_rn(crun, __dmul_rn((double)s_pq, g));   // exact (s_pq < Qlim)
+        const double c = __dadd_rn(prev, P(stop));   // the element that leaves the binade (or ties)
+        if (cdf) cdf[stop - i0] = c;
+        s_crun = c;
+        s_i = stop + 1;
+        s_stop = LLONG_MAX;
+      }
     }
     __syncthreads();
   }
+  const double r = s_crun;
   __syncthreads();
+  return r;
+}
+
+__device__ void cumsum_exact_block(const double* __restrict__ best, double total, int64_t n, double* __restrict__ cdf) {
+  cumsum_exact_range(best, total, 0, n, 0.0, false, cdf);
 }
 
 // One CTA: chooses picks[ci+1] from best (after centroids 0..ci) and u.
@@ -715,6 +747,65 @@ __device__ __forceinline__ void pp_search_body(HalfView h, const double* __restr
   if (!s_ok && tid == 0) status[7] = draw;   // undecided: k_pp_replay (next launch) replays numpy exactly
 }
 
+// numpy's pairwise sum of best (the total of Generator.choice's p): the
+// leaves (<= 128 elements, 8 strided accumulators) summed by 8 lanes each (the
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree by xor shuffles, then the tail),
+// thread `gt` of `gn` (a multiple of 32) taking leaves gt/8, gt/8 + gn/8, ...
+__device__ void pw_leaf_sums(const double* __restrict__ best, const int64_t* __restrict__ leaves, int64_t nleaves,
+                             double* __restrict__ lsum, int64_t gt, int64_t gn) {
+  const int j = (int)(gt & 7);
+  for (int64_t l0 = gt >> 3; l0 - (gt >> 3) < nleaves; l0 += gn / 8) {   // warp-uniform trip count
+    const int64_t l = l0;
+    double r = 0.0;
+    int64_t off = 0, len = 0;
+    if (l < nleaves) {
+      off = leaves[2 * l];
+      len = leaves[2 * l + 1];
+      if (len >= 8) {
+        // this lane's strided accumulator: all (<= 16) loads in flight, then the adds
+        const double* a = best + off;
+        const int nb8 = (int)(len / 8);
+        double v[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v[t] = t < nb8 ? __ldcg(a + 8 * t + j) : 0.0;
+        r = v[0];
+#pragma unroll
+        for (int t = 1; t < 16; ++t)
+          if (t < nb8) r = __dadd_rn(r, v[t]);
+      }
+    }
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (l < nleaves && j == 0) {
+      if (len < 8) {
+        r = 0.0;
+        for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
+      } else {
+        for (int64_t i = len - (len % 8); i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
+      }
+      lsum[l] = r;
+    }
+  }
+}
+
+// the combine tree over the leaf sums, level by level (node lists from the
+// host); one CTA, the leaf sums already visible to it; returns the total
+__device__ double pw_combine(const int64_t* __restrict__ leaves, int64_t nleaves, double* __restrict__ lsum) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int32_t* tl = reinterpret_cast<const int32_t*>(leaves + 2 * nleaves);   // left[ni], right[ni], level_start[]
+  const int ni = (int)(nleaves - 1);
+  const int32_t* tr = tl + ni;
+  const int32_t* lvs = tr + ni;
+  for (int lv = 0; ni > 0; ++lv) {
+    const int b0 = lvs[lv], b1 = lvs[lv + 1];
+    for (int i = b0 + tid; i < b1; i += NT) lsum[nleaves + i] = __dadd_rn(__ldcg(lsum + tl[i]), __ldcg(lsum + tr[i]));
+    __syncthreads();
+    if (b1 == ni) break;
+  }
+  return ni > 0 ? __ldcg(lsum + nleaves + ni - 1) : __ldcg(lsum);
+}
+
 // The exact replay of Generator.choice(n, p=best/total) for draw ci + 1 when
 // the certified search could not decide (status[7] == draw): its own launch of
 // one 1024-thread CTA (4x the warps of a k_pp_step CTA to hide the latencies
@@ -739,53 +830,11 @@ __global__ void __launch_bounds__(RP_THREADS) k_pp_replay(HalfView h, const doub
   // numpy pairwise total: 8 lanes per leaf (one per strided accumulator, the
   // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree by xor shuffles, then the tail),
   // then the combine tree level by level (node lists from the host)
+  pw_leaf_sums(best, leaves, nleaves, lsum, tid, NT);
+  __syncthreads();
   {
-    const int j = tid & 7;
-    for (int64_t l0 = 0; l0 < nleaves; l0 += NT / 8) {
-      const int64_t l = l0 + (tid >> 3);
-      double r = 0.0;
-      int64_t off = 0, len = 0;
-      if (l < nleaves) {
-        off = leaves[2 * l];
-        len = leaves[2 * l + 1];
-        if (len >= 8) {
-          // this lane's strided accumulator: all (<= 16) loads in flight, then the adds
-          const double* a = best + off;
-          const int nb8 = (int)(len / 8);
-          double v[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) v[t] = t < nb8 ? __ldcg(a + 8 * t + j) : 0.0;
-          r = v[0];
-#pragma unroll
-          for (int t = 1; t < 16; ++t)
-            if (t < nb8) r = __dadd_rn(r, v[t]);
-        }
-      }
-      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
-      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
-      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
-      if (l < nleaves && j == 0) {
-        if (len < 8) {
-          r = 0.0;
-          for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
-        } else {
-          for (int64_t i = len - (len % 8); i < len; ++i) r = __dadd_rn(r, __ldcg(best + off + i));
-        }
-        lsum[l] = r;
-      }
-    }
-    __syncthreads();
-    const int32_t* tl = reinterpret_cast<const int32_t*>(leaves + 2 * nleaves);   // left[ni], right[ni], level_start[]
-    const int ni = (int)(nleaves - 1);
-    const int32_t* tr = tl + ni;
-    const int32_t* lvs = tr + ni;
-    for (int lv = 0; ni > 0; ++lv) {
-      const int b0 = lvs[lv], b1 = lvs[lv + 1];
-      for (int i = b0 + tid; i < b1; i += NT) lsum[nleaves + i] = __dadd_rn(lsum[tl[i]], lsum[tr[i]]);
-      __syncthreads();
-      if (b1 == ni) break;
-    }
-    if (tid == 0) s_total = ni > 0 ? lsum[nleaves + ni - 1] : lsum[0];
+    const double t = pw_combine(leaves, nleaves, lsum);
+    if (tid == 0) s_total = t;
     __syncthreads();
   }
   const double total = s_total;
@@ -862,6 +911,249 @@ __global__ void __launch_bounds__(RP_THREADS) k_pp_replay(HalfView h, const doub
       if (cbuf[mid] > c_thr) hi = mid; else lo = mid;
     }
     picks[draw] = hi;
+    status[1] += 1;
+    status[7] = 0;
+  }
+}
+
+// ---- the exact replay across the GPU (k_ppx_total, then k_ppx_quanta; both
+// no-ops unless status[7] == draw).  The cumsum is cut into the k_pp_step
+// tiles (PP_BLOCK points, their block sums in bsum).  k_ppx_total: the
+// pairwise leaves over the grid, then its last CTA combines them into the total
+// and predicts each tile's binade from an approximate prefix of the block sums
+// (a tile whose approximate cdf range touches a binade edge gets none).
+// k_ppx_quanta: the integer quotient sum Q_t = sum round(p_k / g_e) of every
+// predicted tile (-1 on a tie or a quotient >= 2^52), then its last CTA walks
+// the tiles in order with the exact running value c: a window of tiles whose
+// predicted binade is c's and whose quotient prefix stays below the binade's
+// end is one exact step c + g * Q (a block scan); any other tile runs through
+// cumsum_exact_range.  tend[t] = the exact cdf after tile t; the crossing tile
+// of u is then replayed element by element.  Same numbers as k_pp_replay.
+constexpr int PX_THREADS = 512;
+constexpr long long PX_NOBIN = LLONG_MIN;
+__global__ void __launch_bounds__(256) k_ppx_total(HalfView h, const double* __restrict__ best, int ci,
+                                                   int64_t* __restrict__ status, const int64_t* __restrict__ leaves,
+                                                   int64_t nleaves, double* __restrict__ lsum,
+                                                   const double* __restrict__ bsum, int64_t nb,
+                                                   long long* __restrict__ tbin) {
+  if (__ldcg(status + 7) != ci + 1) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+  pw_leaf_sums(best, leaves, nleaves, lsum, (int64_t)blockIdx.x * NT + tid, (int64_t)gridDim.x * NT);
+  __shared__ int s_last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 10), 1ull) == (unsigned long long)(gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double total = pw_combine(leaves, nleaves, lsum);
+  if (tid == 0) {
+    status[10] = 0;
+    status[12] = __double_as_longlong(total);
+  }
+  // approximate exclusive / inclusive prefix of the block sums, NT tiles at a time
+  __shared__ double s_w[32];
+  __shared__ double s_base;
+  if (tid == 0) s_base = 0.0;
+  __syncthreads();
+  // the reference's sequential cdf differs from the exact prefix by <= (n + 2) u
+  // relative; the fp64 block sums and this scan by far less
+  const double rel = 4.0 * ((double)h.n + 4096.0) * U0 + 1e-13;
+  for (int64_t t0 = 0; t0 < nb; t0 += NT) {
+    const int64_t t = t0 + tid;
+    const double v = t < nb ? __ldcg(bsum + t) : 0.0;
+    double incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      double w = lane < NW ? s_w[lane] : 0.0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_w[lane] = w;
+    }
+    __syncthreads();
+    const double base = s_base;
+    const double hi = base + (wid ? s_w[wid - 1] : 0.0) + incl;
+    const double lo = hi - v;
+    if (t < nb) {
+      const double a = lo / total * (1.0 - rel), b = hi / total * (1.0 + rel);
+      long long e = PX_NOBIN;
+      if (a >= 0x1p-900 && ilogb(a) == ilogb(b)) e = ilogb(a);
+      tbin[t] = e;
+    }
+    __syncthreads();
+    if (tid == NT - 1) s_base = hi;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PX_THREADS) k_ppx_quanta(HalfView h, const double* __restrict__ best,
+                                                           const double* __restrict__ uni, int ci,
+                                                           int64_t* __restrict__ picks, int64_t* __restrict__ status,
+                                                           int64_t nb, const long long* __restrict__ tbin,
+                                                           long long* __restrict__ tq, double* __restrict__ tend,
+                                                           double* __restrict__ cbuf) {
+  const int draw = ci + 1;
+  if (__ldcg(status + 7) != draw) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+  const int64_t n = h.n;
+  const double total = __longlong_as_double((long long)__ldcg(status + 12));
+  // ---- quotient sums, one warp per tile
+  for (int64_t t = (int64_t)blockIdx.x * NW + wid; t < nb; t += (int64_t)gridDim.x * NW) {
+    const long long e = __ldcg(tbin + t);
+    if (e == PX_NOBIN) {
+      if (lane == 0) tq[t] = -1;
+      continue;
+    }
+    const double inv = scalbn(1.0, 52 - (int)e);
+    const int64_t k0 = t * PP_BLOCK, k1 = min(n, k0 + PP_BLOCK);
+    long long q = 0;
+    bool bad = false;
+    for (int64_t k = k0 + lane; k < k1; k += 128) {
+      double bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bv[u] = k + 32 * u < k1 ? __ldcg(best + k + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double x = __dmul_rn(__ddiv_rn(bv[u], total), inv);
+        if (x >= 0x1p52) {
+          bad = true;
+        } else {
+          const double fl = floor(x), fr = __dsub_rn(x, fl);
+          q += (long long)fl + (fr > 0.5 ? 1 : 0);
+          bad |= fr == 0.5;
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) tq[t] = bad ? -1 : q;
+  }
+  __shared__ int s_last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(status + 11), 1ull) == (unsigned long long)(gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- the ordered walk
+  __shared__ double s_c;
+  __shared__ int s_started;
+  __shared__ long long s_t0;
+  __shared__ int s_f;
+  __shared__ long long s_w[32];
+  __shared__ double s_cnew;
+  if (tid == 0) {
+    status[11] = 0;
+    s_c = 0.0;
+    s_started = 0;
+    s_t0 = 0;
+  }
+  __syncthreads();
+  while (true) {
+    const int64_t t0 = s_t0;
+    if (t0 >= nb) break;
+    const double c = s_c;
+    int64_t tel = t0;   // tile to run element by element
+    if (s_started && c >= 0x1p-900) {
+      const int e = ilogb(c);
+      const double g = scalbn(1.0, e - 52);
+      const long long Qlim = (long long)__dmul_rn(__dsub_rn(scalbn(1.0, e + 1), c), scalbn(1.0, 52 - e));
+      const int64_t t = t0 + tid;
+      const long long Q = t < nb ? __ldcg(tq + t) : -1;
+      const bool ok = t < nb && Q >= 0 && __ldcg(tbin + t) == (long long)e;
+      const long long qv = ok ? Q : 0;
+      long long incl = qv;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_w[wid] = incl;
+      if (tid == 0) s_f = NT;
+      __syncthreads();
+      if (wid == 0) {
+        long long w = lane < NW ? s_w[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += y;
+        }
+        s_w[lane] = w;
+      }
+      __syncthreads();
+      const long long P = (wid ? s_w[wid - 1] : 0) + incl;   // quotient prefix through tile t
+      if (!(ok && P < Qlim)) atomicMin(&s_f, tid);
+      __syncthreads();
+      const int f = s_f;
+      if (tid < f) tend[t] = __dadd_rn(c, __dmul_rn((double)P, g));   // exact
+      if (f > 0 && tid == f - 1) s_cnew = __dadd_rn(c, __dmul_rn((double)P, g));
+      __syncthreads();
+      const double cn = f > 0 ? s_cnew : c;
+      __syncthreads();
+      if (f == NT || t0 + f >= nb) {
+        if (tid == 0) {
+          s_c = cn;
+          s_t0 = t0 + f;
+        }
+        __syncthreads();
+        continue;
+      }
+      tel = t0 + f;
+      if (tid == 0) s_c = cn;
+      __syncthreads();
+    }
+    const double cs = s_c;
+    const bool st = s_started;
+    const double ce = cumsum_exact_range(best, total, tel * PP_BLOCK, min(n, (tel + 1) * PP_BLOCK), cs, st, nullptr);
+    if (tid == 0) {
+      tend[tel] = ce;
+      s_c = ce;
+      s_started = 1;
+      s_t0 = tel + 1;
+    }
+    __syncthreads();
+  }
+  // ---- the draw: first k with fl(cdf_k / last) > u
+  __shared__ long long s_ts;
+  __shared__ double s_thr;
+  __shared__ int s_k;
+  if (tid == 0) {
+    const double u = uni[ci];
+    const double last = s_c;
+    double c_thr = __dmul_rn(u, last);
+    while (__ddiv_rn(c_thr, last) > u) c_thr = __longlong_as_double(__double_as_longlong(c_thr) - 1);
+    while (true) {
+      const double nx = __longlong_as_double(__double_as_longlong(c_thr) + 1);
+      if (__ddiv_rn(nx, last) > u) break;
+      c_thr = nx;
+    }
+    int64_t lo = -1, hi = nb - 1;   // tend[nb-1] = last > c_thr: first tile whose end exceeds c_thr
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldcg(tend + mid) > c_thr) hi = mid; else lo = mid;
+    }
+    s_ts = hi;
+    s_thr = c_thr;
+    s_k = PP_BLOCK;
+  }
+  __syncthreads();
+  const int64_t ts = s_ts;
+  const int64_t k0 = ts * PP_BLOCK, k1 = min(n, k0 + PP_BLOCK);
+  cumsum_exact_range(best, total, k0, k1, ts > 0 ? __ldcg(tend + ts - 1) : 0.0, ts > 0, cbuf);
+  for (int64_t k = tid; k < k1 - k0; k += NT)
+    if (__ldcg(cbuf + k) > s_thr) atomicMin(&s_k, (int)k);
+  __syncthreads();
+  if (tid == 0) {
+    picks[draw] = k0 + min(s_k, (int)(k1 - k0 - 1));
     status[1] += 1;
     status[7] = 0;
   }
@@ -1532,6 +1824,8 @@ __global__ void k_status_init(int64_t* status, int k) {
   status[7] = 0;
   status[8] = 0;   // sum xsq (double bits)
   status[9] = 0;   // max csq of the chosen centroids (double bits)
+  status[10] = 0;  // k_ppx_total ticket
+  status[11] = 0;  // k_ppx_quanta ticket
   status[0] = k;
   status[1] = 0;
   status[2] = 0;
@@ -1788,8 +2082,9 @@ static int kmeans_prepare(const KMeansRun& r, int64_t first, const double* uni_h
       {&s.status, 8 * 16}, {&s.C64, 8 * (size_t)k * m}, {&s.newlab, 4 * (size_t)n}, {&s.pd, 8 * (size_t)n},
       {&s.keys2, 4 * (size_t)n}, {&s.ctl, 8 * 2 * (size_t)k}, {&s.hsum, 8 * (size_t)std::max<int64_t>(nba, ceil_div(n, TC_THREADS))},   // fp64 or tensor-core assign partials
       {&s.xp, 4 * (size_t)n * mp}, {&s.xs, 4 * (size_t)n * mp}, {&s.sorttmp, std::max<size_t>(sort_bytes, 16)},
-      {&s.leaves, s.leaf_blob.size()}, {&s.pbuf, 8 * (size_t)std::max<int64_t>(n, s.nleaves)},
-      {&s.cbuf, 8 * (size_t)std::max<int64_t>(n, 2 * s.nleaves)}};
+      {&s.leaves, s.leaf_blob.size()},
+      {&s.pbuf, 8 * (size_t)std::max<int64_t>(std::max<int64_t>(n, s.nleaves), 3 * nbp)},
+      {&s.cbuf, 8 * (size_t)std::max<int64_t>(std::max<int64_t>(n, 2 * s.nleaves), PP_BLOCK)}};
   size_t total = 0;
   for (const Cut& c : cuts) total += (c.bytes + 255) & ~(size_t)255;
   TACO_TRY(s.arena.ensure(total));
@@ -1879,11 +2174,23 @@ static int kmeans_step(const KMeansRun& r, const int64_t* forced_h, cudaStream_t
                    s.picks.as<int64_t>(), s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
                    s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(), g_force_replay);
     TACO_LAUNCHED();
-    if (ci + 1 < k) {
+    if (ci + 1 < k && g_force_replay >= 2) {
+      // test hooks: the one-CTA replay (2: the sequential chain, 3: the binade scan)
       k_pp_replay<<<1, RP_THREADS, 0, st>>>(h, s.best.as<double>(), s.uni.as<double>(), ci, s.picks.as<int64_t>(),
                                             s.status.as<int64_t>(), s.leaves.as<int64_t>(), s.nleaves,
                                             s.cbuf.as<double>(), s.pbuf.as<double>(), s.cbuf.as<double>(),
-                                            g_force_replay);
+                                            g_force_replay == 2 ? 2 : 1);
+      TACO_LAUNCHED();
+    } else if (ci + 1 < k) {
+      long long* tbin = reinterpret_cast<long long*>(s.pbuf.as<double>());
+      const int g1 = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(s.nleaves * 8, 256)), 2 * g_num_sms());
+      k_ppx_total<<<g1, 256, 0, st>>>(h, s.best.as<double>(), ci, s.status.as<int64_t>(), s.leaves.as<int64_t>(),
+                                      s.nleaves, s.cbuf.as<double>(), s.bsum.as<double>(), nbp, tbin);
+      TACO_LAUNCHED();
+      const int g2 = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(nbp, PX_THREADS / 32)), 2 * g_num_sms());
+      k_ppx_quanta<<<g2, PX_THREADS, 0, st>>>(h, s.best.as<double>(), s.uni.as<double>(), ci, s.picks.as<int64_t>(),
+                                              s.status.as<int64_t>(), nbp, tbin, tbin + nbp,
+                                              s.pbuf.as<double>() + 2 * nbp, s.cbuf.as<double>());
       TACO_LAUNCHED();
     }
     if (ci == k - 1 && timing) cudaEventRecord(s.ev[1], st);
@@ -2376,7 +2683,7 @@ int taco_get_local_sizes(taco_index* idx, int64_t* sizes_h) {
 
 // Test hook: 1 = every k-means++ draw takes the exact numpy replay path.
 int taco_debug_force_replay(int on) {
-  g_force_replay = on;   // 1: every draw replays (parallel exact cumsum); 2: replays with the sequential chain
+  g_force_replay = on;   // 1: every draw replays (k_ppx_*); 2: the one-CTA sequential chain; 3: the one-CTA binade scan
   return TACO_OK;
 }
 

@@ -142,21 +142,25 @@ def test_kmeans_exact_replay_path():
     from paper_2603_24919_b200 import _native as nat
     nat.call("taco_debug_force_replay", 1)
     try:
-        for shape, k, seed in [((5000, 8), 64, 1), ((3001, 5), 17, 4), ((1000, 3), 40, 13),
-                               ((200_000, 6), 16, 7)]:
+        for shape, k, seed, iters in [((5000, 8), 64, 1, 10), ((3001, 5), 17, 4, 10), ((1000, 3), 40, 13, 10),
+                                      ((200_000, 6), 16, 7, 10), ((1_500_000, 4), 8, 5, 2)]:
             X = np.random.default_rng(seed).normal(size=shape).astype(np.float32)
             if shape[0] > 100_000:
                 X[::3] *= 1e-3   # wide value range: many binade changes inside the cumsum
-            r = T.kmeans(X, k, 10, seed)
-            o = O.kmeans(X, k, 10, seed)
+            if shape[0] > 1_000_000:
+                X[:40_000] *= 1e-6   # a long low head: the tile walk starts many binades down
+            r = T.kmeans(X, k, iters, seed)
+            o = O.kmeans(X, k, iters, seed)
             np.testing.assert_array_equal(r.assignments, o.labels)
             np.testing.assert_array_equal(r.centroids, o.centroids)
-            # the parallel exact cumsum (mode 1) == the sequential chain (mode 2)
-            nat.call("taco_debug_force_replay", 2)
-            r2 = T.kmeans(X, k, 10, seed)
-            nat.call("taco_debug_force_replay", 1)
-            np.testing.assert_array_equal(r.assignments, r2.assignments)
-            np.testing.assert_array_equal(r.centroids, r2.centroids)
+            # the multi-CTA tile walk (mode 1) == the one-CTA sequential chain
+            # (mode 2) == the one-CTA binade scan (mode 3)
+            for mode in (2, 3):
+                nat.call("taco_debug_force_replay", mode)
+                r2 = T.kmeans(X, k, iters, seed)
+                nat.call("taco_debug_force_replay", 1)
+                np.testing.assert_array_equal(r.assignments, r2.assignments)
+                np.testing.assert_array_equal(r.centroids, r2.centroids)
     finally:
         nat.call("taco_debug_force_replay", 0)
 
