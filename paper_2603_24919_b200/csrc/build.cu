@@ -2479,7 +2479,6 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
     return (int)std::max<size_t>(1, (size_t)(0.85 * (double)fr) / per_half);
   };
   int NS = std::min({H, 16, fit()});
-  if (const char* e = getenv("TACO_KM_HALVES")) NS = std::max(1, std::min(NS, atoi(e)));   // experiments
   if (NS < std::min(H, 16)) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) {
@@ -2488,6 +2487,7 @@ int taco_kmeans_all(taco_index* idx, const int64_t* first_h, const double* unifo
     }
     NS = std::min({H, 16, fit()});
   }
+  if (const char* e = getenv("TACO_KM_HALVES")) NS = std::max(1, std::min(NS, atoi(e)));   // experiments
   TACO_TRY(ensure_half_streams(idx, NS));
   if ((int)idx->bs.size() < NS) idx->bs.resize(NS);
   TACO_TRY(idx->labels.ensure(sizeof(int32_t) * (size_t)n * H));
