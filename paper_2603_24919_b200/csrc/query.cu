@@ -2622,9 +2622,10 @@ __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ 
 // One CTA per query over its tiles' partial lists: radix select of the k-th
 // smallest d2 bits, then of the id among exact d2 ties (lower id wins,
 // engine.py:275), bitonic sort of the kk survivors on (d2, id).
-constexpr int TK_THREADS = 256;
+constexpr int TK_THREADS = 256;   // 512 when a query has many partial entries
 constexpr int TK_MAX = 2048;
 
+template <int NT>
 __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids, int64_t m, int kk,
                              bool by_id, unsigned long long key_eq, unsigned long long& out, int& remain,
                              unsigned* hist, unsigned long long* s_pre, int* s_rem) {
@@ -2635,30 +2636,71 @@ __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids
   const int passes = by_id ? 4 : 8;
   for (int p = 0; p < passes; ++p) {
     const int shift = (passes - 1 - p) * 8;
-    for (int i = tid; i < 256; i += TK_THREADS) hist[i] = 0;
+    for (int i = tid; i < 256; i += NT) hist[i] = 0;
     __syncthreads();
     const unsigned long long pre = *s_pre;
-    for (int64_t i = tid; i < m; i += TK_THREADS) {
-      unsigned long long v;
-      if (by_id) {
-        if (keys[i] != key_eq) continue;
-        v = (unsigned long long)ids[i];
-      } else {
-        v = keys[i];
+    // 4 keys per lane in flight; the keys of one query share their leading
+    // digits, so a warp whose taken keys all fall in one bin adds once
+    const int lane = tid & 31;
+    for (int64_t b = tid - lane; b < m; b += 4 * NT) {
+      unsigned long long v[4];
+      bool in[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = b + lane + (int64_t)u * NT;
+        in[u] = i < m;
+        v[u] = 0ull;
+        if (in[u]) {
+          if (by_id) {
+            in[u] = keys[i] == key_eq;
+            v[u] = (unsigned long long)ids[i];
+          } else {
+            v[u] = keys[i];
+          }
+        }
       }
-      if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255ull], 1u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool take = in[u] && (v[u] & msk) == pre;
+        const unsigned dg = (unsigned)((v[u] >> shift) & 255ull);
+        const unsigned tm = __ballot_sync(0xffffffffu, take);
+        if (tm == 0u) continue;
+        const unsigned d0 = __shfl_sync(0xffffffffu, dg, __ffs(tm) - 1);
+        if (__all_sync(0xffffffffu, !take || dg == d0)) {
+          if (lane == 0) atomicAdd(&hist[d0], (unsigned)__popc(tm));
+        } else if (take) {
+          atomicAdd(&hist[dg], 1u);
+        }
+      }
     }
     __syncthreads();
-    if (tid == 0) {
-      const int rem = *s_rem;
-      unsigned acc = 0;
-      int dg = 0;
-      for (; dg < 255; ++dg) {
-        if (acc + hist[dg] >= (unsigned)rem) break;
-        acc += hist[dg];
+    if (tid < 32) {   // the digit whose cumulative count reaches rem: warp 0, 8 bins per lane
+      const unsigned rem = (unsigned)*s_rem;
+      unsigned h[8], own = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        h[u] = hist[tid * 8 + u];
+        own += h[u];
       }
-      *s_rem = rem - (int)acc;
-      *s_pre = pre | ((unsigned long long)dg << shift);
+      unsigned inc = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= o) inc += y;
+      }
+      // first lane whose inclusive count reaches rem (the last lane if none: digit 255)
+      const unsigned bal = __ballot_sync(0xffffffffu, inc >= rem);
+      const int ln = bal ? __ffs(bal) - 1 : 31;
+      if (tid == ln) {
+        unsigned acc = inc - own;
+        int dg = tid * 8;
+        for (int u = 0; u < 7; ++u, ++dg) {
+          if (acc + h[u] >= rem) break;
+          acc += h[u];
+        }
+        *s_rem = (int)(rem - acc);
+        *s_pre = pre | ((unsigned long long)dg << shift);
+      }
     }
     msk |= 255ull << shift;
     __syncthreads();
@@ -2689,7 +2731,8 @@ __device__ __forceinline__ void bitonic_pairs(unsigned long long* key, uint32_t*
   }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* __restrict__ pkey,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_topk(const unsigned long long* __restrict__ pkey,
                                                       const uint32_t* __restrict__ pid,
                                                       const int64_t* __restrict__ tstart, int S, int kk_part,
                                                       const int64_t* __restrict__ scnt, int k, int64_t id_base,
@@ -2724,18 +2767,18 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* _
   if (kk > 0) {
     unsigned long long tau;
     int take;
-    radix_select(keys, ids, m, kk, false, 0ull, tau, take, hist, &s_pre, &s_rem);
+    radix_select<NT>(keys, ids, m, kk, false, 0ull, tau, take, hist, &s_pre, &s_rem);
     int64_t nties = 0;
-    for (int64_t i = tid; i < m; i += TK_THREADS) nties += keys[i] == tau;
+    for (int64_t i = tid; i < m; i += NT) nties += keys[i] == tau;
     for (int o = 16; o > 0; o >>= 1) nties += __shfl_xor_sync(0xffffffffu, nties, o);
     if ((tid & 31) == 0 && nties) atomicAdd((unsigned long long*)&s_ties, (unsigned long long)nties);
     __syncthreads();
     unsigned long long pi = ~0ull;
     if (s_ties > take) {
       int dummy;
-      radix_select(keys, ids, m, take, true, tau, pi, dummy, hist, &s_pre, &s_rem);
+      radix_select<NT>(keys, ids, m, take, true, tau, pi, dummy, hist, &s_pre, &s_rem);
     }
-    for (int64_t i = tid; i < m; i += TK_THREADS) {
+    for (int64_t i = tid; i < m; i += NT) {
       const unsigned long long kv = keys[i];
       if (kv < tau || (kv == tau && (unsigned long long)ids[i] <= pi)) {
         const int slot = atomicAdd(&s_fill, 1);
@@ -2747,13 +2790,13 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const unsigned long long* _
   }
   int P = 1;
   while (P < kk) P <<= 1;
-  for (int i = kk + tid; i < P; i += TK_THREADS) {
+  for (int i = kk + tid; i < P; i += NT) {
     skey[i] = ~0ull;
     sid[i] = 0xFFFFFFFFu;
   }
   __syncthreads();
   bitonic_pairs(skey, sid, P);
-  for (int r = tid; r < k; r += TK_THREADS) {
+  for (int r = tid; r < k; r += NT) {
     if (r < kk) {
       out_d2[q * k + r] = __longlong_as_double((long long)skey[r]);
       out_ids[q * k + r] = (int64_t)sid[r] + id_base;
@@ -3362,7 +3405,9 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
   }
   {
     ProfScope ps(K_TOPK, st);
-    k_topk<<<(unsigned)QS, TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart, (int)S,
+    // partial entries per query: many (k > 32 keeps every row) -> 512 threads
+    const bool wide = ntiles * kk >= (int64_t)8192 * std::max<int64_t>(QS, 1);
+    (wide ? k_topk<2 * TK_THREADS> : k_topk<TK_THREADS>)<<<(unsigned)QS, wide ? 2 * TK_THREADS : TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart, (int)S,
                                                 kk, scnt, k, id_base, out_d2, out_ids);
     TACO_LAUNCHED();
   }

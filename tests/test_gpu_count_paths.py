@@ -36,6 +36,8 @@ MODES = {
     "cluster_odd": ({"TACO_CLUSTER_IDS": "7000"}, (True, 2)),
     "global": ({"TACO_GLOBAL_MODE": "1"}, (False, 1)),
     "global_small_chunk": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "2048"}, (False, 5)),
+    # the 128K-id chunks (64 KiB tables) global mode takes past 1024 chunks (n > 67M)
+    "global_wide_chunk": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "131072"}, (False, 1)),
     # global mode without the encoded CSR (the unit-staged k_count sweep)
     "global_units": ({"TACO_GLOBAL_MODE": "1", "TACO_GLOBAL_CHUNK": "2048", "TACO_COUNT_TMA": "0"}, (False, 5)),
 }
