@@ -1047,8 +1047,17 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 #ifndef EC_PP
 #define EC_PP 1      // ping-pong lookahead registers in the consume loop
 #endif
+#ifndef EC_SPREAD
+#define EC_SPREAD 1  // padding entries point at a word of their own slice (not all at word 0)
+#endif
+#ifndef EC_SKIPHALF
+#define EC_SKIPHALF 0   // (with EC_PAIR) a lane whose half unit is all padding applies nothing
+#endif
+#ifndef EC_PAIR
+#define EC_PAIR 1    // lane pairs split a 32-byte unit (16 sectors per warp load)
+#endif
 #ifndef EC_FASTGE
-#define EC_FASTGE 1  // scores <= 8: lanes >= L as (w + (8 - L) * 0x11111111) & 0x88888888
+#define EC_FASTGE 1 // scores <= 8: lanes >= L as (w + (8 - L) * 0x11111111) & 0x88888888
 #endif
 #ifndef EC_RELAX
 #define EC_RELAX 1   // relaxed cluster arrive after the histogram gather
@@ -1068,12 +1077,29 @@ __device__ __forceinline__ uint32_t shr_clamp(uint32_t v, uint32_t s) {
 }
 // one group of 4 encoded entries into the table at shared address tsg;
 // ev/od collect "left level r" in 8-bit fields (levels 0,2,4,6 / 1,3,5,7)
+#ifndef EC_PRED
+#define EC_PRED 0    // padding entries skip their atomic (predicated) instead of adding 0
+#endif
+__device__ __forceinline__ uint32_t smem_atomic_add_unless_pad(uint32_t addr, uint32_t v, uint32_t s) {
+  uint32_t old;
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %3, 32;\n mov.u32 %0, 0;\n @p atom.shared::cta.add.u32 %0, [%1], %2;\n}"
+      : "=r"(old) : "r"(addr), "r"(v), "r"(s) : "memory");
+  return old;
+}
 __device__ __forceinline__ void apply_group(const uint4 e, uint32_t tsg, uint32_t& ev, uint32_t& od) {
   const uint32_t s0 = e.x & 63u, s1 = e.y & 63u, s2 = e.z & 63u, s3 = e.w & 63u;
+#if EC_PRED
+  const uint32_t o0 = smem_atomic_add_unless_pad(tsg + (e.x >> 6), shl_clamp(1u, s0), s0);
+  const uint32_t o1 = smem_atomic_add_unless_pad(tsg + (e.y >> 6), shl_clamp(1u, s1), s1);
+  const uint32_t o2 = smem_atomic_add_unless_pad(tsg + (e.z >> 6), shl_clamp(1u, s2), s2);
+  const uint32_t o3 = smem_atomic_add_unless_pad(tsg + (e.w >> 6), shl_clamp(1u, s3), s3);
+#else
   const uint32_t o0 = smem_atomic_add(tsg + (e.x >> 6), shl_clamp(1u, s0));
   const uint32_t o1 = smem_atomic_add(tsg + (e.y >> 6), shl_clamp(1u, s1));
   const uint32_t o2 = smem_atomic_add(tsg + (e.z >> 6), shl_clamp(1u, s2));
   const uint32_t o3 = smem_atomic_add(tsg + (e.w >> 6), shl_clamp(1u, s3));
+#endif
   // 4-bit field r (r <= 7: the funnel shift wraps mod 32)
   const uint32_t u4 = __funnelshift_l(0u, 1u, shr_clamp(o0, s0) << 2) + __funnelshift_l(0u, 1u, shr_clamp(o1, s1) << 2) +
                       __funnelshift_l(0u, 1u, shr_clamp(o2, s2) << 2) + __funnelshift_l(0u, 1u, shr_clamp(o3, s3) << 2);
@@ -1265,7 +1291,7 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
         uint32_t u0, pad, j;
         enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, jp, g, u0, ng[u], pad, j);
         ga[u] = j * jstride + u0;
-        pads += (int)pad;
+        pads += (int)((EC_PAIR && EC_SKIPHALF && UW == 2) ? pad & 3u : pad);
       }
       my += ng[u];
     }
@@ -1305,8 +1331,34 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
         }
       };
       int k = tid;
-      fetch(k, a0, a1);
-      if (EC_PP) {   // ping-pong registers: no moves between units
+      if (EC_PAIR && UW == 2) {
+        // lane pairs share a 32-byte unit (one sector per pair: a warp load
+        // touches 16 sectors instead of 32 half sectors); a thread's two
+        // groups in flight are groups k and k + NT of the round
+        const int G = 2 * nr;
+        auto fetch2 = [&](int kk, uint4& x0, uint4& x1) {
+          if (kk < G) x0 = E4[2 * (size_t)gaddr[kk >> 1] + (kk & 1)];
+          if (kk + NT < G) x1 = E4[2 * (size_t)gaddr[(kk + NT) >> 1] + (kk & 1)];
+        };
+        auto apply1 = [&](const uint4& x) {
+          if (EC_SKIPHALF && (x.x & 63u) == EC_SENT) return;   // an all-padding second half
+          if (WIDE) apply_group_w(x, tsg, ev, od, evh, odh);
+          else apply_group(x, tsg, ev, od);
+        };
+        fetch2(k, a0, a1);
+        while (k < G) {
+          fetch2(k + 2 * NT, b0v, b1v);
+          apply1(a0);
+          if (k + NT < G) apply1(a1);
+          k += 2 * NT;
+          if (k >= G) break;
+          fetch2(k + 2 * NT, a0, a1);
+          apply1(b0v);
+          if (k + NT < G) apply1(b1v);
+          k += 2 * NT;
+        }
+      } else if (EC_PP) {   // ping-pong registers: no moves between units
+        fetch(k, a0, a1);
         while (k < nr) {
           fetch(k + NT, b0v, b1v);
           apply(a0, a1);
@@ -1317,6 +1369,7 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
           k += NT;
         }
       } else {
+        fetch(k, a0, a1);
         for (; k < nr; k += NT) {
           fetch(k + NT, b0v, b1v);
           apply(a0, a1);
@@ -1621,12 +1674,13 @@ __global__ void __launch_bounds__(CC_NT) k_ccsr_fill(const uint32_t* __restrict_
     const uint32_t* I = ids + (size_t)j * n + s0;
     uint32_t* E = cenc + (size_t)j * cstride + U * (size_t)g0;
     for (uint32_t e = 0; e < U * g; ++e) {
-      uint32_t v = EC_SENT;
-      if (e < len) {
-        const uint32_t p = (uint32_t)(I[e] - cbase);
-        // table word byte offset << 6 | lane shift (4-bit or 8-bit lanes)
-        v = nib ? ((p >> 3) << 8) | ((p & 7u) << 2) : ((p >> 2) << 8) | ((p & 3u) << 3);
-      }
+      // table word byte offset << 6 | lane shift (4-bit or 8-bit lanes); a
+      // padding entry adds 0 (shift 32) to the word of one of the slice's own
+      // ids: a warp's padding lanes then spread over the banks like real
+      // entries instead of all hitting word 0
+      const uint32_t p = (uint32_t)(I[e < len ? e : (EC_SPREAD ? e % len : 0u)] - cbase);
+      uint32_t v = nib ? ((p >> 3) << 8) | ((p & 7u) << 2) : ((p >> 2) << 8) | ((p & 3u) << 3);
+      if (e >= len) v = EC_SPREAD ? (v & ~63u) | EC_SENT : EC_SENT;
       E[e] = v;
     }
   }
