@@ -1148,27 +1148,19 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
 // candidate segment with one global atomic; while it is in flight the CTA
 // compacts into `stage` (shared memory, scap ids) and copies the segment out
 // coalesced once the base is known (direct global writes when it is larger).
-template <int NT, bool NIB = true, bool WIDE = false>
-__device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
-                             cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
-                             uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
-                             int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
-                             int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
+// Alg. 5 on the group's level histogram S.ge, the CTA's candidate segment
+// and its compaction (the common tail of the encoded kernels' epilogues).
+// Thread 0 reserves the segment with one global atomic; while it is in
+// flight the CTA compacts into `stage` (shared memory, scap ids) and copies
+// the segment out coalesced once the base is known (direct global writes
+// when it is larger).
+template <int NT, bool NIB, bool WIDE>
+__device__ __forceinline__ void enc_finish(const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S, int rank, int csz,
+                                           int64_t q, int64_t base, double budget, uint32_t* __restrict__ cand,
+                                           int64_t cand_cap, int64_t* __restrict__ flags, int64_t* __restrict__ sbase,
+                                           int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
+                                           int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
   const int tid = threadIdx.x;
-  const int rank = (int)cluster.block_rank();
-  const int csz = (int)cluster.num_blocks();
-  enc_levels<NT, WIDE>(T, table, valid, n_sub, S);
-  cluster.sync();   // every CTA's level histogram is final
-  for (int l = tid; l <= n_sub; l += NT) {
-    int h = 0;
-    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
-    S.ge[l] = h;
-  }
-  if (EC_RELAX)   // publishes nothing: only "done reading the remote histograms"
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  else
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  __syncthreads();
   int64_t b = 0;
   if (tid == 0) {
     int64_t cands = 0;
@@ -1203,7 +1195,78 @@ __device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int
     sbase[q * csz + rank] = S.sbase;
     scnt[q * csz + rank] = mine;
   }
+}
+
+// tallies -> level histogram, cluster exchange over DSMEM, then enc_finish
+// (the k_count_cluster epilogue for NT threads).
+template <int NT, bool NIB = true, bool WIDE = false>
+__device__ __forceinline__ void enc_epilogue(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
+                             cg::cluster_group& cluster, int64_t q, int64_t base, double budget,
+                             uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
+                             int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
+                             int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
+  const int tid = threadIdx.x;
+  const int rank = (int)cluster.block_rank();
+  const int csz = (int)cluster.num_blocks();
+  enc_levels<NT, WIDE>(T, table, valid, n_sub, S);
+  cluster.sync();   // every CTA's level histogram is final
+  for (int l = tid; l <= n_sub; l += NT) {
+    int h = 0;
+    for (int r = 0; r < csz; ++r) h += cluster.map_shared_rank(S.lh, r)[l];
+    S.ge[l] = h;
+  }
+  if (EC_RELAX)   // publishes nothing: only "done reading the remote histograms"
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  else
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
+  enc_finish<NT, NIB, WIDE>(table, valid, n_sub, S, rank, csz, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
+                            lvl, stage, scap);
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// The same epilogue for a software group of csz CTAs (k_count_pg): every CTA
+// publishes its level histogram as value + 1 in its own zero-initialised slots
+// of xch[q][rank][level] and polls the group's slots until they are nonzero
+// (each word validates itself: no fence, no counter, one store trip and one
+// load trip).
+__device__ __forceinline__ void st_relaxed_gpu(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_relaxed_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+template <int NT, bool NIB = true, bool WIDE = false>
+__device__ __forceinline__ void enc_epilogue_sw(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
+                             int rank, int csz, int64_t q, int64_t base, double budget, int32_t* __restrict__ xch,
+                             uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
+                             int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
+                             int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
+  const int tid = threadIdx.x;
+  const int LV = n_sub + 1;
+  enc_levels<NT, WIDE>(T, table, valid, n_sub, S);   // S.lh final (ends with a barrier)
+  if (csz > 1 && (g_count_dbg & 4)) {   // timing experiment: no exchange (wrong levels)
+    if (tid < LV) S.ge[tid] = S.lh[tid] * csz;
+  } else if (csz > 1) {
+    int32_t* X = xch + (size_t)q * csz * LV;
+    if (tid < LV) {
+      st_relaxed_gpu(&X[rank * LV + tid], S.lh[tid] + 1);
+      S.ge[tid] = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < csz * LV; i += NT) {
+      int32_t v;
+      while ((v = ld_relaxed_gpu(&X[i])) == 0) __nanosleep(20);
+      atomicAdd(&S.ge[i % LV], v - 1);
+    }
+  } else if (tid < LV) {
+    S.ge[tid] = S.lh[tid];
+  }
+  __syncthreads();
+  enc_finish<NT, NIB, WIDE>(table, valid, n_sub, S, rank, csz, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
+                            lvl, stage, scap);
 }
 
 // pop g of query q (flattened over subspaces; jpref = the subspaces' pop
@@ -1448,6 +1511,43 @@ __global__ void __launch_bounds__(NT, MINB) k_count_enc(
                                gaddr, S, T);
   enc_epilogue<NT, NIB, WIDE>(T, table, valid, n_sub, S, cluster, q, base, budget, cand, cand_cap, flags, sbase, scnt, cnum,
                    lvl, gaddr, EcCfg<NT>::GC);
+}
+
+// k_count_pg: k_count_enc as a persistent kernel over SOFTWARE groups of
+// nchunks CTAs (group = blockIdx.x / nchunks walks queries grp, grp + ngrp,
+// ...).  A hardware cluster cannot span GPCs, so clusters of 8 (16) reach
+// only 384 (336) of the 444 co-resident CTA slots of this kernel's shape
+// (tools/mb_clusters.cu); groups synchronise through global memory instead
+// (enc_epilogue_sw) and use every slot.  The grid never exceeds the
+// co-resident capacity (cooperative launch), so a polling CTA's siblings are
+// always running.
+template <int NT, int MINB, int NSC = 0, bool NIB = true, bool WIDE = false>
+__global__ void __launch_bounds__(NT, MINB) k_count_pg(
+    const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop, int cap,
+    const uint32_t* __restrict__ cenc, size_t cstride, const uint32_t* __restrict__ coffs, int n_sub_rt, int K2,
+    int64_t n, int64_t nchunks, int64_t chunk, double budget, uint32_t* __restrict__ cand, int64_t cand_cap,
+    int64_t* __restrict__ flags, int64_t* __restrict__ sbase, int64_t* __restrict__ scnt,
+    int64_t* __restrict__ cnum, int32_t* __restrict__ lvl, int64_t Q, int32_t* __restrict__ xch) {
+  const int n_sub = NSC ? NSC : n_sub_rt;
+  extern __shared__ __align__(16) uint8_t table[];
+  __shared__ EncSmem<NT> S;
+  const int csz = (int)nchunks;
+  const int grp = (int)(blockIdx.x / csz), ngrp = (int)(gridDim.x / csz);
+  const int rank = (int)(blockIdx.x % csz);
+  if (grp >= ngrp) return;
+  const int64_t c = rank;
+  const int64_t base = c * chunk;
+  const int valid = (int)max((int64_t)0, min(chunk, n - base));
+  const int tbytes = (int)(NIB ? chunk / 2 : chunk);
+  uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
+  for (int64_t q = grp; q < Q; q += ngrp) {
+    Tally T;
+    enc_count_phase<NT, 2, WIDE>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table,
+                                 gaddr, S, T);
+    enc_epilogue_sw<NT, NIB, WIDE>(T, table, valid, n_sub, S, rank, csz, q, base, budget, xch, cand, cand_cap, flags,
+                                   sbase, scnt, cnum, lvl, gaddr, EcCfg<NT>::GC);
+    __syncthreads();   // the table and the staging are free for the next query
+  }
 }
 
 // Global mode, sweep 1 on the encoded CSR (4-entry units): per (chunk,
@@ -3213,6 +3313,64 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
     cfg.dynamicSmemBytes = table_bytes(idx) + (tfeed ? sizeof(uint4) * TC_RS * TC_SG
                                                      : sizeof(uint32_t) * (huge ? EcCfg<1024>::GC
                                                                            : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
+    static int pg_on = -1;   // TACO_COUNT_PG=0: hardware clusters (k_count_enc) instead of persistent software groups
+    if (pg_on < 0) {
+      const char* pe = getenv("TACO_COUNT_PG");
+      pg_on = (pe && pe[0] == '0') ? 0 : 1;
+    }
+    if (pg_on && !tfeed && !wide && !huge) {
+      auto pk = big ? (nib_tables(idx) ? k_count_pg<256, 3, 0, true, true> : k_count_pg<256, 3, 16, false, true>)
+                : idx->n_sub == 8 ? k_count_pg<256, 3, 8> : k_count_pg<256, 3>;
+      static int slots[4] = {0, 0, 0, 0};   // co-resident CTAs of each instantiation ...
+      static size_t slots_smem[4] = {0, 0, 0, 0};   // ... at this launch's shared-memory size
+      static bool attr_set[4] = {false, false, false, false};
+      const int which = big ? (nib_tables(idx) ? 0 : 1) : idx->n_sub == 8 ? 2 : 3;
+      const size_t smem = table_bytes(idx) + sizeof(uint32_t) * EcCfg<256>::GC;
+      if (!attr_set[which]) {
+        const int smem_max =
+            (int)((which == 1 ? kClusterMaxChunk8 : kClusterMaxChunk / 2) + sizeof(uint32_t) * EcCfg<256>::GC);
+        TACO_CHECK_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        attr_set[which] = true;
+      }
+      if (slots_smem[which] != smem) {
+        int per_sm = 0;
+        TACO_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, 256, smem));
+        slots[which] = per_sm * num_sms();
+        slots_smem[which] = smem;
+        if (slots[which] <= 0) TACO_FAIL(TACO_ERR_CUDA, "k_count_pg does not fit an SM");
+      }
+      const int64_t csz = idx->nchunks;
+      const int64_t ngrp = std::min<int64_t>(QS, slots[which] / csz);
+      if (ngrp >= 1) {
+        const int LV = idx->n_sub + 1;
+        const size_t xb = sizeof(int32_t) * (size_t)QS * (size_t)csz * LV;
+        TACO_TRY(t.xch.ensure(xb));
+        if (csz > 1) TACO_CHECK_CUDA(cudaMemsetAsync(t.xch.p, 0, xb, st));
+        const uint16_t* a_pops = t.pops.as<uint16_t>();
+        const int32_t* a_npop = t.npop.as<int32_t>();
+        int a_cap = t.pop_cap;
+        const uint32_t* a_cenc = idx->cenc.as<uint32_t>();
+        size_t a_cstride = idx->cstride;
+        const uint32_t* a_coffs = idx->coffs.as<uint32_t>();
+        int a_nsub = idx->n_sub, a_K = idx->K;
+        int64_t a_n = idx->n, a_nch = idx->nchunks, a_chunk = idx->chunk;
+        double a_budget = budget;
+        uint32_t* a_cand = t.cand.as<uint32_t>();
+        int64_t a_ccap = t.cand_cap;
+        int64_t *a_flags = t.flags.as<int64_t>(), *a_sb = t.qbase.as<int64_t>(), *a_sc = t.clocal.as<int64_t>(),
+                *a_cnum = t.cnum.as<int64_t>();
+        int32_t* a_lvl = t.lvl.as<int32_t>();
+        int64_t a_Q = QS;
+        int32_t* a_xch = t.xch.as<int32_t>();
+        void* args[] = {&a_pops, &a_npop, &a_cap, &a_cenc, &a_cstride, &a_coffs, &a_nsub, &a_K, &a_n, &a_nch, &a_chunk,
+                        &a_budget, &a_cand, &a_ccap, &a_flags, &a_sb, &a_sc, &a_cnum, &a_lvl, &a_Q, &a_xch};
+        // cooperative: the whole grid is co-resident while it runs (the groups poll each other)
+        TACO_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)pk, dim3((unsigned)(ngrp * csz)), dim3(256), args,
+                                                    smem, st));
+        TACO_LAUNCHED();
+        return TACO_OK;
+      }
+    }
     auto kern = tfeed ? k_count_tma
                 : big ? (nib_tables(idx) ? k_count_enc<256, 3, 0, true, true> : k_count_enc<256, 3, 16, false, true>)
                 : huge ? k_count_enc<1024, 1>
