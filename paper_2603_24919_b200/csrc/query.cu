@@ -896,6 +896,79 @@ __device__ void compact_unordered(const uint8_t* tab, int valid, uint32_t L, int
   }
 }
 
+// Two-phase unordered compaction for sparse hits (a query's candidates are
+// ~0.3% of the ids).  Phase 1 only asks "does this 16-byte vector hold any
+// lane >= L" (a few instructions per vector) and records the vector indices
+// (ballot-ranked, one reservation per warp step) in `rec`; phase 2 gives
+// every record to one thread, which recomputes the lane mask and writes the
+// ids.  The single-pass scan spends most of its instructions on per-lane hit
+// loops that run with one or two lanes active.  L >= 1; lanes past `valid`
+// are zero, so they never hit.  Returns false (nothing written) when the
+// records would not fit rcap.
+#ifndef EC_TWOPHASE
+#define EC_TWOPHASE 1
+#endif
+template <int NT, bool NIB, bool SMALL>
+__device__ bool compact_two_phase(const uint8_t* tab, int valid, uint32_t L, int64_t id0, uint32_t* dst, int* fill,
+                                  uint16_t* rec, int rcap, int* rfill) {
+  constexpr int LW = NIB ? 4 : 8;
+  constexpr int LPW = 32 / LW;
+  constexpr int IDS = 4 * LPW;
+  constexpr uint32_t H = NIB ? 0x88888888u : 0x80808080u;
+  const uint32_t D = NIB ? (16u - L) * 0x11111111u : (256u - L) * 0x01010101u;
+  const uint32_t K = (8u - L) * 0x11111111u;
+  const uint4* t4 = reinterpret_cast<const uint4*>(tab);
+  const int nvec = (valid + IDS - 1) / IDS;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  auto any_hit = [&](const uint4 v) -> bool {
+    if (SMALL) return ((((v.x + K) | (v.y + K)) | ((v.z + K) | (v.w + K))) & H) != 0u;
+    return ((lanes_ge<NIB>(v.x, D) | lanes_ge<NIB>(v.y, D)) | (lanes_ge<NIB>(v.z, D) | lanes_ge<NIB>(v.w, D))) != 0u;
+  };
+  for (int v0 = (threadIdx.x - lane) * CP_VPL; v0 < nvec; v0 += NT * CP_VPL) {
+    bool h[CP_VPL];
+    uint32_t b[CP_VPL];
+    int tot = 0;
+#pragma unroll
+    for (int e = 0; e < CP_VPL; ++e) {
+      const int vi = v0 + e * 32 + lane;
+      h[e] = vi < nvec && any_hit(t4[vi]);
+    }
+#pragma unroll
+    for (int e = 0; e < CP_VPL; ++e) {
+      b[e] = __ballot_sync(0xffffffffu, h[e]);
+      tot += __popc(b[e]);
+    }
+    if (tot == 0) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(rfill, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int e = 0; e < CP_VPL; ++e) {
+      const int at = base + __popc(b[e] & lt);
+      if (h[e] && at < rcap) rec[at] = (uint16_t)(v0 + e * 32 + lane);
+      base += __popc(b[e]);
+    }
+  }
+  __syncthreads();
+  const int R = *rfill;
+  if (R > rcap) return false;
+  for (int r = threadIdx.x; r < R; r += NT) {
+    const int vi = rec[r];
+    const uint4 v = t4[vi];
+    uint32_t mm = SMALL ? vec_hits_small(v, K, IDS) : vec_hits<NIB>(v, D, IDS);
+    uint32_t pos = (uint32_t)atomicAdd(fill, (int)__popc(mm));
+    const uint32_t idb = (uint32_t)(id0 + (int64_t)vi * IDS);
+    while (mm) {
+      const int bb = 31 - __clz(mm);
+      mm ^= 1u << bb;
+      const int u = LW - 1 - (bb & (LW - 1));
+      dst[pos++] = idb + (uint32_t)(u * LPW + bb / LW);
+    }
+  }
+  return true;
+}
+
 // Global-mode spill: the ids of a chunk table with score >= 2 as packed
 // records (chunk position << 8 | score), unordered, CP_VPL vectors per lane
 // per warp step as above.  The emit sweep filters them at the query's level
@@ -1132,7 +1205,7 @@ template <int NT>
 struct EncSmem {
   uint64_t full[8], empty[8];   // k_count_tma ring
   int cnt[8];
-  int pads, fill, L, ptot;
+  int pads, fill, L, ptot, rfill;
   int64_t sbase, scnt;
   uint32_t wtot[NT / 32];
   int jpref[17];
@@ -1171,6 +1244,7 @@ __device__ __forceinline__ void enc_finish(const uint8_t* table, int valid, int 
     S.L = L;
     S.scnt = mine;
     S.fill = 0;
+    S.rfill = 0;
     if (rank == 0) {
       cnum[q] = cands;
       lvl[q] = L;
@@ -1179,7 +1253,18 @@ __device__ __forceinline__ void enc_finish(const uint8_t* table, int valid, int 
   }
   __syncthreads();
   const int64_t mine = S.scnt;
-  if (mine <= scap) {
+  if (EC_TWOPHASE && S.L >= 1 && mine <= scap / 2 && valid <= 65536 * 16) {
+    // candidates in stage[0, scap/2), vector records (u16) in the upper half; every record
+    // holds at least one candidate, so there are at most `mine` of them
+    compact_two_phase<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill,
+                                                              reinterpret_cast<uint16_t*>(stage + scap / 2), scap,
+                                                              &S.rfill);
+    if (tid == 0) S.sbase = b;
+    __syncthreads();
+    const int64_t sb = S.sbase;
+    if (sb + mine <= cand_cap)
+      for (int i = tid; i < (int)mine; i += NT) cand[sb + i] = stage[i];
+  } else if (mine <= scap) {
     compact_unordered<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
     if (tid == 0) S.sbase = b;
     __syncthreads();
