@@ -1253,7 +1253,8 @@ __device__ __forceinline__ void enc_finish(const uint8_t* table, int valid, int 
   }
   __syncthreads();
   const int64_t mine = S.scnt;
-  if (EC_TWOPHASE && S.L >= 1 && mine <= scap / 2 && valid <= 65536 * 16) {
+  constexpr int IDSV = NIB ? 32 : 16;   // ids per 16-byte table vector
+  if (EC_TWOPHASE && S.L >= 1 && mine <= scap / 2) {
     // candidates in stage[0, scap/2), vector records (u16) in the upper half; every record
     // holds at least one candidate, so there are at most `mine` of them
     compact_two_phase<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill,
@@ -1264,6 +1265,15 @@ __device__ __forceinline__ void enc_finish(const uint8_t* table, int valid, int 
     const int64_t sb = S.sbase;
     if (sb + mine <= cand_cap)
       for (int i = tid; i < (int)mine; i += NT) cand[sb + i] = stage[i];
+  } else if (EC_TWOPHASE && S.L >= 1 && (valid + IDSV - 1) / IDSV <= 2 * scap) {
+    // a large segment: the records take the whole staging area (one per table vector at most) and
+    // phase 2 writes the ids straight to the segment (its base is back long before phase 1 ends)
+    if (tid == 0) S.sbase = b;
+    __syncthreads();
+    if (S.sbase + mine <= cand_cap)
+      compact_two_phase<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, cand + S.sbase,
+                                                                &S.fill, reinterpret_cast<uint16_t*>(stage), 2 * scap,
+                                                                &S.rfill);
   } else if (mine <= scap) {
     compact_unordered<NT, NIB, NIB && !WIDE && EC_FASTGE != 0>(table, valid, (uint32_t)S.L, base, stage, &S.fill);
     if (tid == 0) S.sbase = b;
