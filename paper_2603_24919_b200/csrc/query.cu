@@ -1126,6 +1126,9 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 #ifndef EC_SKIPHALF
 #define EC_SKIPHALF 0   // (with EC_PAIR) a lane whose half unit is all padding applies nothing
 #endif
+#ifndef EC_PREFETCH
+#define EC_PREFETCH 0   // k_count_pg: the next query's slice lookups are issued under this query's epilogue
+#endif
 #ifndef EC_PAIR
 #define EC_PAIR 1    // lane pairs split a 32-byte unit (16 sectors per warp load)
 #endif
@@ -1334,14 +1337,13 @@ __device__ __forceinline__ int32_t ld_relaxed_gpu(const int32_t* p) {
   return v;
 }
 template <int NT, bool NIB = true, bool WIDE = false>
-__device__ __forceinline__ void enc_epilogue_sw(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
+__device__ __forceinline__ void enc_epilogue_sw(const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S,
                              int rank, int csz, int64_t q, int64_t base, double budget, int32_t* __restrict__ xch,
                              uint32_t* __restrict__ cand, int64_t cand_cap, int64_t* __restrict__ flags,
                              int64_t* __restrict__ sbase, int64_t* __restrict__ scnt, int64_t* __restrict__ cnum,
                              int32_t* __restrict__ lvl, uint32_t* stage, int scap) {
   const int tid = threadIdx.x;
-  const int LV = n_sub + 1;
-  enc_levels<NT, WIDE>(T, table, valid, n_sub, S);   // S.lh final (ends with a barrier)
+  const int LV = n_sub + 1;   // S.lh is final (enc_levels, run by the caller, ends with a barrier)
   if (csz > 1 && (g_count_dbg & 4)) {   // timing experiment: no exchange (wrong levels)
     if (tid < LV) S.ge[tid] = S.lh[tid] * csz;
   } else if (csz > 1) {
@@ -1399,16 +1401,68 @@ struct EcCfg {
   static constexpr int GC = 8 * NT;               // staged units per round: 8 per thread (8-bit tallies)
 };
 
+// k_count_pg looks the NEXT query's first batch of popped slices up while
+// the current query is in its epilogue (the pops -> coffs chain is two
+// dependent global loads): enc_pre_cells reads the pop prefix and the cells,
+// enc_pre_offs the cells' unit offsets; the count phase then starts from
+// registers.
+template <int PER>
+struct EncPre {
+  uint32_t jc[PER];        // subspace << 16 | cell (0xFFFFFFFF: no slice)
+  uint32_t a[PER], b[PER]; // coffs[cell], coffs[cell + 1]
+};
+template <int NT, bool WIDE>
+__device__ __forceinline__ void enc_pre_cells(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop,
+                                              int cap, int n_sub, int64_t q, EncPre<EcCfg<NT>::PER>& P) {
+  constexpr int JM = WIDE ? 16 : 8, PER = EcCfg<NT>::PER;
+  int jp[JM];
+  int acc = 0;
+#pragma unroll
+  for (int jj = 0; jj < JM; ++jj) {
+    jp[jj] = acc;
+    if (jj < n_sub) acc += min(__ldg(npop + q * n_sub + jj), cap);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int g = u * NT + (int)threadIdx.x;
+    P.jc[u] = 0xFFFFFFFFu;
+    if (g < acc) {
+      int j = 0, jb = 0;
+#pragma unroll
+      for (int jj = 1; jj < JM; ++jj)
+        if (jj < n_sub && g >= jp[jj]) {
+          j = jj;
+          jb = jp[jj];
+        }
+      P.jc[u] = ((uint32_t)j << 16) | pops[((size_t)q * n_sub + j) * cap + (g - jb)];
+    }
+  }
+}
+template <int NT>
+__device__ __forceinline__ void enc_pre_offs(const uint32_t* __restrict__ coffs, size_t offs_len, int K2, int64_t c,
+                                             EncPre<EcCfg<NT>::PER>& P) {
+#pragma unroll
+  for (int u = 0; u < EcCfg<NT>::PER; ++u) {
+    P.a[u] = P.b[u] = 0u;
+    if (P.jc[u] != 0xFFFFFFFFu) {
+      const uint32_t* O = coffs + (size_t)(P.jc[u] >> 16) * offs_len + (size_t)c * K2 + (P.jc[u] & 0xFFFFu);
+      P.a[u] = __ldg(O);
+      P.b[u] = __ldg(O + 1);
+    }
+  }
+}
+
 // The counting phase of the encoded kernels for (query q, chunk c): table
 // zeroed and filled, tallies in T, padding entries counted in S.pads.  UW =
 // 16-byte words per unit (2: cluster mode's 8-entry units, 1: global mode's
 // 4-entry units).  Staging: gaddr[EcCfg<NT>::GC].
-template <int NT, int UW, bool WIDE = false>
+template <int NT, int UW, bool WIDE = false, bool PRE = false>
 __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pops, const int32_t* __restrict__ npop,
                                                 int cap, const uint32_t* __restrict__ cenc, size_t cstride,
                                                 const uint32_t* __restrict__ coffs, int n_sub, int K2, int64_t nchunks,
                                                 int64_t q, int64_t c, int tbytes, uint8_t* table, uint32_t* gaddr,
-                                                EncSmem<NT>& S, Tally& T) {
+                                                EncSmem<NT>& S, Tally& T,
+                                                const EncPre<EcCfg<NT>::PER>* pre = nullptr) {
   constexpr int PER = EcCfg<NT>::PER, GC = EcCfg<NT>::GC, EU = 4 * UW;
   const int tid = threadIdx.x;
   const uint4* E4 = reinterpret_cast<const uint4*>(cenc);
@@ -1445,7 +1499,12 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
       const int g = b0 + u * NT + tid;
       ga[u] = 0;
       ng[u] = 0;
-      if (g < P_all) {
+      if (PRE && b0 == 0) {   // looked up during the previous query's epilogue
+        const uint32_t u0 = pre->a[u] & EC_GMASK;
+        ng[u] = (pre->b[u] & EC_GMASK) - u0;
+        ga[u] = (pre->jc[u] >> 16) * jstride + u0;   // no slice: a = b = 0, and ga is never used
+        pads += (int)(pre->b[u] >> 29);
+      } else if (g < P_all) {
         uint32_t u0, pad, j;
         enc_slice(pops, coffs, offs_len, cap, n_sub, K2, q, c, jp, g, u0, ng[u], pad, j);
         ga[u] = j * jstride + u0;
@@ -1635,11 +1694,21 @@ __global__ void __launch_bounds__(NT, MINB) k_count_pg(
   const int valid = (int)max((int64_t)0, min(chunk, n - base));
   const int tbytes = (int)(NIB ? chunk / 2 : chunk);
   uint32_t* gaddr = reinterpret_cast<uint32_t*>(table + tbytes);   // [GC] unit indices
+  const size_t offs_len = (size_t)nchunks * K2 + 1;
+  EncPre<EcCfg<NT>::PER> pre;
+  if (EC_PREFETCH && grp < Q) {
+    enc_pre_cells<NT, WIDE>(pops, npop, cap, n_sub, grp, pre);
+    enc_pre_offs<NT>(coffs, offs_len, K2, c, pre);
+  }
   for (int64_t q = grp; q < Q; q += ngrp) {
     Tally T;
-    enc_count_phase<NT, 2, WIDE>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c, tbytes, table,
-                                 gaddr, S, T);
-    enc_epilogue_sw<NT, NIB, WIDE>(T, table, valid, n_sub, S, rank, csz, q, base, budget, xch, cand, cand_cap, flags,
+    enc_count_phase<NT, 2, WIDE, EC_PREFETCH != 0>(pops, npop, cap, cenc, cstride, coffs, n_sub, K2, nchunks, q, c,
+                                                   tbytes, table, gaddr, S, T, &pre);
+    const int64_t qn = q + ngrp;
+    if (EC_PREFETCH && qn < Q) enc_pre_cells<NT, WIDE>(pops, npop, cap, n_sub, qn, pre);
+    enc_levels<NT, WIDE>(T, table, valid, n_sub, S);   // S.lh final (ends with a barrier)
+    if (EC_PREFETCH && qn < Q) enc_pre_offs<NT>(coffs, offs_len, K2, c, pre);
+    enc_epilogue_sw<NT, NIB, WIDE>(table, valid, n_sub, S, rank, csz, q, base, budget, xch, cand, cand_cap, flags,
                                    sbase, scnt, cnum, lvl, gaddr, EcCfg<NT>::GC);
     __syncthreads();   // the table and the staging are free for the next query
   }
