@@ -241,10 +241,12 @@ int taco_index_create(int device, int64_t n, int32_t d, int32_t n_subspaces, int
     idx->chunk = ceil_div(ceil_div(n, ctas), 1024) * 1024;
     idx->cluster_mode = true;
   } else {
-    // 4-bit tables: 64K-id chunks, 128K past 1024 of them (n = 1e8: every CTA looks up
-    // every popped cell, so the slice lookups grow with the chunk count; config 5
-    // k_count 152 -> 138 ms per 2,000 queries); TACO_GLOBAL_CHUNK overrides
-    idx->chunk = (n_subspaces <= 15 && n > 1024 * kGlobalChunk) ? kClusterMaxChunk : kGlobalChunk;
+    // 4-bit tables: 64K-id chunks, 128K past 64 of them (every CTA looks up every
+    // popped cell, so the slice lookups grow with the chunk count, and a cell's
+    // slice of a chunk shrinks to a few ids: config 4 k_count 45.0 -> 42.5 ms per
+    // 10,000 queries, config 5 152 -> 138 ms per 2,000; config 2 forced into
+    // global mode measures the same either way); TACO_GLOBAL_CHUNK overrides
+    idx->chunk = (n_subspaces <= 15 && n > 64 * kGlobalChunk) ? kClusterMaxChunk : kGlobalChunk;
     if (const char* e = getenv("TACO_GLOBAL_CHUNK"))
       idx->chunk = std::min<int64_t>(n_subspaces <= 15 ? kClusterMaxChunk : kClusterMaxChunk8,
                                      std::max<int64_t>(1024, atoll(e) / 1024 * 1024));

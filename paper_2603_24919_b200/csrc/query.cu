@@ -3477,11 +3477,9 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
     cfg.dynamicSmemBytes = table_bytes(idx) + (tfeed ? sizeof(uint4) * TC_RS * TC_SG
                                                      : sizeof(uint32_t) * (huge ? EcCfg<1024>::GC
                                                                            : wide ? EcCfg<512>::GC : EcCfg<256>::GC));
-    static int pg_on = -1;   // TACO_COUNT_PG=0: hardware clusters (k_count_enc) instead of persistent software groups
-    if (pg_on < 0) {
-      const char* pe = getenv("TACO_COUNT_PG");
-      pg_on = (pe && pe[0] == '0') ? 0 : 1;
-    }
+    // TACO_COUNT_PG=0 (read per batch): hardware clusters (k_count_enc) instead of persistent software groups
+    const char* pe = getenv("TACO_COUNT_PG");
+    const bool pg_on = !(pe && pe[0] == '0');
     if (pg_on && !tfeed && !wide && !huge) {
       auto pk = big ? (nib_tables(idx) ? k_count_pg<256, 3, 0, true, true> : k_count_pg<256, 3, 16, false, true>)
                 : idx->n_sub == 8 ? k_count_pg<256, 3, 8> : k_count_pg<256, 3>;

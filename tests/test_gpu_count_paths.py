@@ -4,9 +4,12 @@ answers (golden fixtures from tests/golden/make_golden.py) and the oracle.
 The batched count has three layouts:
   * cluster mode with ONE CTA per query (n small: all earlier rigs);
   * cluster mode with SEVERAL CTAs per query -- the config-2/3 path: per-CTA
-    id chunks, level histograms gathered over DSMEM, split cluster barrier,
-    per-CTA candidate segments.  TACO_CLUSTER_IDS shrinks the chunk so a
-    20,000-point rig runs it with 10 CTAs per query;
+    id chunks and candidate segments; the CTAs of a query are a software
+    group of the persistent k_count_pg (level histograms exchanged through
+    global slots; the default) or, with TACO_COUNT_PG=0, one hardware cluster
+    of k_count_enc (histograms gathered over DSMEM, split cluster barrier).
+    TACO_CLUSTER_IDS shrinks the chunk so a 20,000-point rig runs it with 10
+    CTAs per query;
   * global mode (sharded / n > 1.5M, config 4): per-(query, chunk) CTAs,
     spilled score >= 2 records, emit sweep, recount list -- on the encoded
     CSR (4-entry units, k_count_genc) or, with TACO_COUNT_TMA=0, the
@@ -71,13 +74,15 @@ def test_count_layout_matches_reference(rig, mode):
     idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
     chunk, nch, cluster = nat.index_layout(_device_of(idx).h)
     assert cluster == want_cluster and nch >= min_chunks, (chunk, nch, cluster)
-    for gi, (alpha, beta, k) in enumerate(g["grid"]):
-        qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
-        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
-        np.testing.assert_array_equal(num, g[f"num_{gi}"])
-        np.testing.assert_array_equal(lvl, g[f"lvl_{gi}"])
-        np.testing.assert_array_equal(ids, g[f"ids_{gi}"])
-        np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
+    # cluster mode: the persistent software groups (default) and the hardware clusters
+    for pg in (("1", "0") if want_cluster else ("1",)):
+        for gi, (alpha, beta, k) in enumerate(g["grid"]):
+            qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
+            ids, dists, num, lvl = _with_env({"TACO_COUNT_PG": pg}, lambda: T.knn_query_batch(idx, X, Q, qp))
+            np.testing.assert_array_equal(num, g[f"num_{gi}"])
+            np.testing.assert_array_equal(lvl, g[f"lvl_{gi}"])
+            np.testing.assert_array_equal(ids, g[f"ids_{gi}"])
+            np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
 
 
 def test_multi_cta_against_oracle_many_queries(rig):
@@ -89,9 +94,12 @@ def test_multi_cta_against_oracle_many_queries(rig):
     oidx = O.deserialize(g["blob"].tobytes())
     alpha, beta, k = (float(v) for v in g["grid"][-1])
     oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, beta, int(k), threads=8)
-    for env in (MODES["cluster_multi"][0], MODES["global_small_chunk"][0]):
+    # 96 queries over 44 groups of 10 CTAs: the persistent groups walk several queries each
+    for env, pg in ((MODES["cluster_multi"][0], "1"), (MODES["cluster_multi"][0], "0"),
+                    (MODES["global_small_chunk"][0], "1")):
         idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
-        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, int(k)))
+        ids, dists, num, lvl = _with_env(
+            {"TACO_COUNT_PG": pg}, lambda: T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, int(k))))
         np.testing.assert_array_equal(num, on)
         np.testing.assert_array_equal(lvl, ol)
         np.testing.assert_array_equal(ids, oi)
@@ -110,12 +118,13 @@ def test_scores_tap_wide_levels(rig):
             assert hashlib.blake2b(sc.tobytes(), digest_size=16).hexdigest() == g[f"scores_digest_{gi}"][qi]
 
 
-@pytest.mark.parametrize("kernel", ["fused", "enc", "tma", "units"])
+@pytest.mark.parametrize("kernel", ["fused", "pg", "enc", "tma", "units"])
 @pytest.mark.parametrize("layout", ["cluster_1cta", "cluster_multi"])
 def test_cluster_count_kernels_extreme_budgets(kernel, layout, golden):
     """The cluster count kernels (the encoded, padded CSR with direct loads --
-    alone or fused with the integer re-rank and top-k -- or the cp.async.bulk
-    ring, and the unit-staged one) at budgets whose Alg. 5
+    as persistent software groups, as hardware clusters, or fused with the
+    integer re-rank and top-k -- or the cp.async.bulk ring, and the
+    unit-staged one) at budgets whose Alg. 5
     walk reaches level 1 (beta -> 1 with a small alpha: the level-1 count
     depends on the padding correction of the level-0 tally) and with almost
     every cell retrieved (alpha -> 1: slices far larger than a ring stage)."""
@@ -126,7 +135,8 @@ def test_cluster_count_kernels_extreme_budgets(kernel, layout, golden):
     env = dict(MODES[layout][0], TACO_COUNT_TMA="0" if kernel == "units" else "1")
     idx = _with_env(env, lambda: T.deserialize_index(g["blob"].tobytes()))
     feed = {"TACO_COUNT_FEED": "tma" if kernel == "tma" else "enc",
-            "TACO_FUSED": "1" if kernel == "fused" else "0"}
+            "TACO_FUSED": "1" if kernel == "fused" else "0",
+            "TACO_COUNT_PG": "1" if kernel == "pg" else "0"}
     for alpha, beta, k in ((0.999, 0.999, 7), (0.5, 0.2, 10), (0.02, 0.999, 3), (0.999, 0.001, 5)):
         oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, beta, k, threads=8)
         ids, dists, num, lvl = _with_env(feed, lambda: T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, beta, k)))

@@ -27,6 +27,15 @@ METRICS = [
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__occupancy_limit_shared_mem", "occupancy limit (smem)"),
     ("launch__cluster_dim_x", "cluster size"),
+    ("launch__grid_size", "grid size"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data-pipe wavefronts % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "shared atomic wavefronts"),
+    ("smsp__inst_executed_op_shared_atom.sum", "shared atomic instructions"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall: barrier / issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall: short scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall: long scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall: wait / issue"),
 ]
 UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "Tbyte": 1e12}
 
@@ -60,7 +69,7 @@ def main():
         out.append(f"- dram bytes per query    {(rb + wb) / a.queries:.1f} B")
         out.append("")
         key = {"k_count_cluster": "k_count", "k_count_enc": "k_count", "k_count_tma": "k_count",
-               "k_rerank_async": "k_rerank"}.get(name, name)
+               "k_count_pg": "k_count", "k_rerank_async": "k_rerank", "k_rerank_i8": "k_rerank"}.get(name, name)
         if a.config is not None:
             traffic.setdefault(f"cfg{a.config}", {})[key] = {
                 "dram_bytes_per_query": (rb + wb) / a.queries, "source": os.path.basename(a.report), "tag": a.tag}
