@@ -458,6 +458,31 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot, 
   return excl;
 }
 
+// block_excl_scan with two barriers: every thread sums the warp totals below
+// its warp itself (NT / 32 broadcast loads) instead of waiting for warp 0's scan
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan2(uint32_t v, uint32_t* wtot, uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtot[wid] = x;
+  __syncthreads();
+  uint32_t below = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    const uint32_t t = wtot[w];
+    all += t;
+    if (w < wid) below += t;
+  }
+  total = all;
+  __syncthreads();   // wtot is free again
+  return below + x - v;
+}
+
 // ------------------------------------------------------------ chunk counting
 // Counts into `table` (ids [base, base+chunk)) every id of the cells popped for
 // query q in subspaces 0..n_sub-1.  Phase A stages the slices of all popped
@@ -1126,6 +1151,12 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
 #ifndef EC_SKIPHALF
 #define EC_SKIPHALF 0   // (with EC_PAIR) a lane whose half unit is all padding applies nothing
 #endif
+#ifndef EC_SCAN2
+#define EC_SCAN2 1      // the slice-unit scan with two barriers (block_excl_scan2)
+#endif
+#ifndef EC_STAGE_UNROLL
+#define EC_STAGE_UNROLL 0
+#endif
 #ifndef EC_PREFETCH
 #define EC_PREFETCH 0   // k_count_pg: the next query's slice lookups are issued under this query's epilogue
 #endif
@@ -1513,7 +1544,7 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
       my += ng[u];
     }
     uint32_t tot;
-    uint32_t run = block_excl_scan<NT>(my, S.wtot, tot);
+    uint32_t run = EC_SCAN2 ? block_excl_scan2<NT>(my, S.wtot, tot) : block_excl_scan<NT>(my, S.wtot, tot);
     uint32_t gb[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -1525,6 +1556,11 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const uint32_t k0 = max(gb[u], r0), k1 = min(gb[u] + ng[u], r1);
+#if EC_STAGE_UNROLL == 2
+#pragma unroll 2
+#elif EC_STAGE_UNROLL == 4
+#pragma unroll 4
+#endif
         for (uint32_t k = k0; k < k1; ++k) gaddr[k - r0] = ga[u] + (k - gb[u]);
       }
       __syncthreads();
@@ -2634,14 +2670,21 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
     r.qs = r.m > 0 ? __ldg(qsq + r.q) : 0;
   };
   const int r0 = lane >> 3, cl = lane & 7;
+  // per-lane constants of the row copies: source column, destination offset inside a stage,
+  // row pitch in bytes as an unsigned 32-bit factor (one IMAD.WIDE.U32 per address)
+  const uint8_t* xcol = Xb + cl * 16;
+  const uint32_t dst0 = (uint32_t)(r0 * RI_PITCH + cl * 16);
+  const uint32_t rowb = NC ? (uint32_t)(NC * 16) : (uint32_t)d;
+  const bool colok = NC == 8 ? true : cl < nc;
   auto issue = [&](const RiTile& r, RiStage& s) {
+    uint8_t* dst = &s.rows[0][0] + dst0;
 #pragma unroll
     for (int j = 0; j < GR / 4; ++j) {
       const int rr = j * 4 + r0;
       const uint32_t c = __shfl_sync(0xffffffffu, r.cid, rr);
-      if (cl < nc && rr < r.m) cp_async16(&s.rows[rr][cl * 16], Xb + (size_t)c * d + cl * 16);
+      if (colok && rr < r.m) cp_async16(dst + j * 4 * RI_PITCH, xcol + (uint64_t)c * rowb);
     }
-    if (lane < nc && r.m > 0) cp_async16(s.q + lane * 16, Qb + (size_t)r.q * d + lane * 16);
+    if (lane < nc && r.m > 0) cp_async16(s.q + lane * 16, Qb + (uint64_t)r.q * rowb + lane * 16);
     cp_async_commit();
   };
   RiTile ta, tb, tc;              // computing i, issued i + 1, ids of i + 2
