@@ -222,7 +222,8 @@ def ncu_traffic(name, nq, launches, cfg):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            ent = json.load(fh)[f"cfg{cfg}"][name]
+            per_cfg = json.load(fh)[f"cfg{cfg}"]
+        ent = per_cfg.get(name) or per_cfg[name + "_genc"]   # global mode counts with k_count_genc
         return ent["dram_bytes_per_query"] * nq / max(launches, 1)
     except Exception:
         return None
