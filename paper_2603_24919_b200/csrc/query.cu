@@ -3523,7 +3523,8 @@ static int cluster_count(taco_index* idx, QueryTile& t, int64_t QS, double beta,
     // TACO_COUNT_PG=0 (read per batch): hardware clusters (k_count_enc) instead of persistent software groups
     const char* pe = getenv("TACO_COUNT_PG");
     const bool pg_on = !(pe && pe[0] == '0');
-    if (pg_on && !tfeed && !wide && !huge) {
+    // (a one-CTA query has no cluster to outgrow: the per-query launch balances better there)
+    if (pg_on && idx->nchunks > 1 && !tfeed && !wide && !huge) {
       auto pk = big ? (nib_tables(idx) ? k_count_pg<256, 3, 0, true, true> : k_count_pg<256, 3, 16, false, true>)
                 : idx->n_sub == 8 ? k_count_pg<256, 3, 8> : k_count_pg<256, 3>;
       static int slots[4] = {0, 0, 0, 0};   // co-resident CTAs of each instantiation ...

@@ -231,10 +231,36 @@ def sc_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "sclinear.npz"), **out)
 
 
+# (n, d, nq, k, integer-valued) -- inputs are rng(n + d) draws as in tests/test_dataio.py
+GT_CASES = [(5000, 32, 40, 10, False), (3000, 128, 33, 100, True), (2000, 37, 20, 7, False),
+            (1500, 960, 5, 10, False)]
+
+
+def gt_inputs(n, d, nq, ints):
+    rng = np.random.default_rng(n + d)
+    if ints:   # integer data: many exact distance ties -> id order decides
+        return (rng.integers(0, 4, (n, d)).astype(np.float32), rng.integers(0, 4, (nq, d)).astype(np.float32))
+    return rng.standard_normal((n, d)).astype(np.float32), rng.standard_normal((nq, d)).astype(np.float32)
+
+
+def gt_fixture(ref):
+    """dataio.compute_ground_truth (dataio.py:142-172) on small seeded inputs."""
+    out = {"cases": np.array([[n, d, nq, k, int(i)] for n, d, nq, k, i in GT_CASES], np.int64)}
+    for ci, (n, d, nq, k, ints) in enumerate(GT_CASES):
+        X, Q = gt_inputs(n, d, nq, ints)
+        gt = ref.dataio.compute_ground_truth(X, Q, k)
+        out[f"ids_{ci}"] = gt.ids
+        out[f"dists_{ci}"] = gt.dists
+    np.savez_compressed(os.path.join(HERE, "groundtruth.npz"), **out)
+
+
 def main():
     ref = load_reference()
     if sys.argv[1:] == ["sclinear"]:
         sc_fixture(ref)
+        return
+    if sys.argv[1:] == ["groundtruth"]:
+        gt_fixture(ref)
         return
     if sys.argv[1:]:   # named rigs only, e.g. `make_golden.py rig4 rig5`
         for rig in RIGS:
@@ -245,6 +271,7 @@ def main():
     for rig in RIGS:
         rig_fixture(ref, *rig)
     sc_fixture(ref)
+    gt_fixture(ref)
 
 
 if __name__ == "__main__":

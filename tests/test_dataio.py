@@ -96,3 +96,21 @@ def test_gpu_ground_truth_resident_index():
     b = T.compute_ground_truth(X, Q, 10)
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dists, b.dists)
+
+
+@pytest.mark.gpu
+def test_gpu_ground_truth_matches_reference_golden(golden):
+    """The GPU exact k-NN against dataio.compute_ground_truth's own outputs
+    (tests/golden/groundtruth.npz, made by running the reference)."""
+    g = golden("groundtruth")
+    for ci, (n, d, nq, k, ints) in enumerate(g["cases"].tolist()):
+        rng = np.random.default_rng(n + d)
+        if ints:
+            X = rng.integers(0, 4, (n, d)).astype(np.float32)
+            Q = rng.integers(0, 4, (nq, d)).astype(np.float32)
+        else:
+            X = rng.standard_normal((n, d)).astype(np.float32)
+            Q = rng.standard_normal((nq, d)).astype(np.float32)
+        gt = T.compute_ground_truth(X, Q, k)
+        np.testing.assert_array_equal(gt.ids, g[f"ids_{ci}"])
+        np.testing.assert_array_equal(gt.dists, g[f"dists_{ci}"])

@@ -144,3 +144,22 @@ def test_sc_linear_scores_vs_reference():
         for qi in range(q.shape[0]):
             for ai, a in enumerate(SC_ALPHAS):
                 np.testing.assert_array_equal(O.sc_linear_scores(T, q[qi], n_sub, s, a), g[f"sc_{ci}_{qi}_{ai}"])
+
+
+def _gt_inputs(n, d, nq, ints):
+    """The inputs of tests/golden/make_golden.py gt_fixture (rng(n + d) draws)."""
+    rng = np.random.default_rng(n + d)
+    if ints:
+        return (rng.integers(0, 4, (n, d)).astype(np.float32), rng.integers(0, 4, (nq, d)).astype(np.float32))
+    return rng.standard_normal((n, d)).astype(np.float32), rng.standard_normal((nq, d)).astype(np.float32)
+
+
+def test_ground_truth_vs_reference(golden):
+    """O.ground_truth against dataio.compute_ground_truth's own outputs
+    (dataio.py:142-172; integer data with exact distance ties, d up to 960, k = 100)."""
+    g = golden("groundtruth")
+    for ci, (n, d, nq, k, ints) in enumerate(g["cases"].tolist()):
+        X, Q = _gt_inputs(n, d, nq, bool(ints))
+        oi, od = O.ground_truth(X, Q, k)
+        np.testing.assert_array_equal(oi, g[f"ids_{ci}"])
+        np.testing.assert_array_equal(od, g[f"dists_{ci}"])
