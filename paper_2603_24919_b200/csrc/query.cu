@@ -374,14 +374,189 @@ __global__ void __launch_bounds__(TS_THREADS) k_traverse_sh(const double* __rest
 #undef hk
 #undef hp
 
+// k_traverse_sh with PERSISTENT LANES: a lane that finishes its walk takes
+// the next one from a global counter instead of idling until the longest of
+// its warp's 32 walks ends (walk lengths at config 2: ~110 pops on average,
+// 237 the longest), and the grid is one resident wave, so there is no second,
+// partly filled wave either.  Same pops, counts and sizes.
+template <int KMAX, int TS_THREADS>
+__global__ void __launch_bounds__(TS_THREADS) k_traverse_pl(const double* __restrict__ sd,
+                                                  const uint16_t* __restrict__ sl,
+                                                  const int64_t* __restrict__ gsize, int64_t Q,
+                                                  int n_sub, int kp, int64_t target,
+                                                  uint16_t* __restrict__ pops, int cap,
+                                                  double* __restrict__ keys_out,
+                                                  int32_t* __restrict__ npop,
+                                                  int64_t* __restrict__ ret,
+                                                  int64_t* __restrict__ flags,
+                                                  unsigned long long* __restrict__ next_walk) {
+  const int64_t total = Q * n_sub;
+  extern __shared__ __align__(16) unsigned char tsh_sm[];
+  double* const hkb = reinterpret_cast<double*>(tsh_sm) + threadIdx.x;
+  uint16_t* const hpb = reinterpret_cast<uint16_t*>(reinterpret_cast<double*>(tsh_sm) + KMAX * TS_THREADS) + threadIdx.x;
+  struct HeapRef {
+    double* k;
+    uint16_t* p;
+    __device__ double& key(int i) const { return k[i * TS_THREADS]; }
+    __device__ uint16_t& pc(int i) const { return p[i * TS_THREADS]; }
+  };
+  const HeapRef H{hkb, hpb};
+#define hk(i) H.key(i)
+#define hp(i) H.pc(i)
+  int hn = 0;
+  auto less = [&](double ka, uint32_t pa, double kb, uint32_t pb) {
+    return ka < kb || (ka == kb && pa < pb);
+  };
+  // 4-ary heap (depth 3 for K' <= 64): a sift level loads its 4 children at
+  // once, so a pop's dependent chain is half a binary heap's; the pop and the
+  // push of (r, c + 1) are ONE replace-top sift-down.  (key, r << 8 | c) is a
+  // strict total order, so any correct priority queue pops the same sequence.
+  constexpr int LOG4 = KMAX <= 21 ? 2 : KMAX <= 85 ? 3 : 4;
+  auto sift_up = [&](double key, uint32_t pc32, bool doit) {   // insert at the end
+    const uint16_t pc = (uint16_t)pc32;
+    int i = hn;
+    hn += doit ? 1 : 0;
+    bool done = !doit || i == 0;
+#pragma unroll
+    for (int lev = 0; lev < LOG4; ++lev) {
+      const int par = done ? 0 : (i - 1) >> 2;
+      const double kp_ = hk(par);
+      const uint16_t pp_ = hp(par);
+      const bool go = !done && less(key, pc, kp_, pp_);
+      if (go) {
+        hk(i) = kp_;
+        hp(i) = pp_;
+        i = par;
+      }
+      done = done || !go || i == 0;
+    }
+    if (doit) {
+      hk(i) = key;
+      hp(i) = pc;
+    }
+  };
+  auto sift_down_root = [&](double lk, uint32_t lp32, bool doit) {   // place (lk, lp) starting at the root
+    const uint16_t lp = (uint16_t)lp32;
+    int i = 0;
+    bool done = !doit;
+#pragma unroll
+    for (int lev = 0; lev < LOG4; ++lev) {
+      const int a = 4 * i + 1;
+      const bool v0 = !done && a < hn, v1 = !done && a + 1 < hn, v2 = !done && a + 2 < hn, v3 = !done && a + 3 < hn;
+      const int i0 = v0 ? a : 0, i1 = v1 ? a + 1 : 0, i2 = v2 ? a + 2 : 0, i3 = v3 ? a + 3 : 0;
+      const double k0 = hk(i0), k1 = hk(i1), k2 = hk(i2), k3 = hk(i3);
+      const uint16_t p0 = hp(i0), p1 = hp(i1), p2 = hp(i2), p3 = hp(i3);
+      // tournament: (0 vs 1), (2 vs 3), then the winners; an invalid child never wins
+      const bool b1 = v1 && less(k1, p1, k0, p0);
+      const double ka = b1 ? k1 : k0;
+      const uint16_t pa = b1 ? p1 : p0;
+      const int ia = b1 ? a + 1 : a;
+      const bool b3 = v3 && less(k3, p3, k2, p2);
+      const double kb = b3 ? k3 : k2;
+      const uint16_t pb = b3 ? p3 : p2;
+      const int ib = b3 ? a + 3 : a + 2;
+      const bool bb = v2 && less(kb, pb, ka, pa);
+      const double km = bb ? kb : ka;
+      const uint16_t pm = bb ? pb : pa;
+      const int im = bb ? ib : ia;
+      const bool go = v0 && less(km, pm, lk, lp);
+      if (go) {
+        hk(i) = km;
+        hp(i) = pm;
+        i = im;
+      }
+      done = done || !go;
+    }
+    if (doit) {
+      hk(i) = lk;
+      hp(i) = lp;
+    }
+  };
+  // the walk in progress
+  int64_t t = 0, got = 0, psz = 0;
+  const double *d1 = nullptr, *d2 = nullptr;
+  const uint16_t *l1 = nullptr, *l2 = nullptr;
+  const int64_t* gs = nullptr;
+  uint16_t* out = nullptr;
+  double* kout = nullptr;
+  double d20 = 0.0;
+  int np = 0;
+  bool pend = false, active = false;
+  while (true) {
+    if (!active) {
+      t = (int64_t)atomicAdd(next_walk, 1ull);
+      if (t >= total) break;
+      const int j = (int)(t % n_sub);
+      d1 = sd + t * 2 * kp;
+      d2 = d1 + kp;
+      l1 = sl + t * 2 * kp;
+      l2 = l1 + kp;
+      gs = gsize + (size_t)j * kp * kp;
+      out = pops + t * cap;
+      kout = keys_out ? keys_out + t * cap : nullptr;
+      hn = 0;
+      np = 0;
+      got = 0;
+      psz = 0;
+      pend = false;
+      d20 = d2[0];
+      sift_up(__dadd_rn(d1[0], d20), 0u, true);
+      active = true;
+    }
+    bool fin = false;
+    if (hn == 0) {
+      if (pend) got += psz;
+      fin = true;
+    } else {
+      const double key = hk(0);
+      const uint32_t pc = hp(0);
+      const int r = (int)(pc >> 8), c = (int)(pc & 0xFF);
+      const bool nr = c == 0 && r + 1 < kp, nc = c + 1 < kp;
+      const double dr1 = nr ? d1[r + 1] : 0.0;
+      const double dr = d1[r];
+      const double dc1 = nc ? d2[c + 1] : 0.0;
+      const int cell = (int)l1[r] * kp + (int)l2[c];
+      if (np < cap) {
+        out[np] = (uint16_t)cell;
+        if (kout) kout[np] = key;
+      }
+      if (pend) {
+        got += psz;
+        fin = got >= target;   // the previous pop reached the target: this one is not counted
+      }
+      if (!fin) {
+        psz = gs[cell];
+        pend = true;
+        ++np;
+        // the top is replaced by its row successor (r, c + 1), or by the last entry when the row ends
+        hn -= nc ? 0 : 1;
+        const int li = nc ? 0 : hn;
+        const double lk = nc ? __dadd_rn(dr, dc1) : hk(li);
+        const uint32_t lp = nc ? (((uint32_t)r << 8) | (uint32_t)(c + 1)) : (uint32_t)hp(li);
+        sift_down_root(lk, lp, hn > 0);
+        sift_up(__dadd_rn(dr1, d20), (uint32_t)(r + 1) << 8, nr);
+      }
+    }
+    if (fin) {
+      npop[t] = np;
+      ret[t] = got;
+      if (np > cap) atomicMax((unsigned long long*)&flags[0], (unsigned long long)np);
+      active = false;
+    }
+  }
+}
+#undef hk
+#undef hp
+
 static int num_sms();
 
-// TACO_TRAVERSE=heap / =smem force the thread-local-heap / shared-memory
-// kernel (tests pin both); default: by batch size (launch_traverse)
+// TACO_TRAVERSE=heap / =smem / =pl force the thread-local-heap / shared-memory
+// / persistent-lane kernel (tests pin all three); default: by batch size
+// (launch_traverse)
 static int traverse_force() {
   const char* e = getenv("TACO_TRAVERSE");
   if (!e) return 0;
-  return !strcmp(e, "heap") ? 1 : !strcmp(e, "smem") ? 2 : 0;
+  return !strcmp(e, "heap") ? 1 : !strcmp(e, "smem") ? 2 : !strcmp(e, "pl") ? 3 : 0;
 }
 
 // launch the traversal of Q queries x n_sub subspaces
@@ -393,9 +568,45 @@ static int launch_traverse(const double* sd, const uint16_t* sl, const int64_t* 
   // L1 and the variable-depth sifts finish sooner (configs 1 / 3: 0.23 / 0.25
   // ms vs 0.29 / 0.27); large batches: the shared-memory fixed-depth heap
   const int force = traverse_force();
-  if (force == 2 || (force == 0 && th >= (int64_t)num_sms() * 128)) {
+  if (force >= 2 || (force == 0 && th >= (int64_t)num_sms() * 128)) {
   // 64 walks per CTA; 32 when that would leave SMs idle
-  const bool narrow = th < (int64_t)num_sms() * 64 * 4;
+  static int narrow_env = -1;   // TACO_TRAVERSE_NARROW=1 / =0: force 32- / 64-walk CTAs (experiments)
+  if (narrow_env < 0) {
+    const char* e = getenv("TACO_TRAVERSE_NARROW");
+    narrow_env = !e ? 2 : (e[0] == '1' ? 1 : 0);
+  }
+  const bool narrow = narrow_env == 2 ? th < (int64_t)num_sms() * 64 * 4 : narrow_env == 1;
+#define TRAVP(KM)                                                                                           \
+  {                                                                                                         \
+    constexpr int TS = 32;                                                                                  \
+    const size_t smem = (size_t)KM * TS * 10;                                                               \
+    static int per_sm = 0;                                                                                  \
+    if (!per_sm) {                                                                                          \
+      TACO_CHECK_CUDA(cudaFuncSetAttribute(k_traverse_pl<KM, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)smem));                                                     \
+      TACO_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse_pl<KM, TS>, TS, smem)); \
+      if (per_sm < 1) per_sm = 1;                                                                           \
+    }                                                                                                       \
+    TACO_CHECK_CUDA(cudaMemsetAsync(flags + 5, 0, sizeof(int64_t), st));                                    \
+    const int64_t ctas = std::min<int64_t>(ceil_div(th, TS), (int64_t)per_sm * num_sms());                  \
+    k_traverse_pl<KM, TS><<<(unsigned)ctas, TS, smem, st>>>(sd, sl, gsize, Q, n_sub, kp, target, pops, cap, \
+                                                            keys_out, npop, ret, flags,                    \
+                                                            reinterpret_cast<unsigned long long*>(flags + 5)); \
+  }
+    // persistent lanes (flags[5] = the walk counter) once the batch exceeds one resident wave
+    static int pl_env = -1;   // TACO_TRAVERSE_PL=0: one walk per thread (k_traverse_sh)
+    if (pl_env < 0) {
+      const char* e = getenv("TACO_TRAVERSE_PL");
+      pl_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (force == 3 || (pl_env && force == 0 && th >= (int64_t)num_sms() * 256)) {
+      if (kp <= 32) TRAVP(32)
+      else if (kp <= 64) TRAVP(64)
+      else if (kp <= 128) TRAVP(128)
+      else TRAVP(256)
+      return TACO_OK;
+    }
+#undef TRAVP
 #define TRAVS1(KM, TS)                                                                                      \
   {                                                                                                         \
     const size_t smem = (size_t)KM * TS * 10;                                                               \

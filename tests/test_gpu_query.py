@@ -29,7 +29,7 @@ def rig(request, golden):
     return g, X, Q, idx
 
 
-@pytest.mark.parametrize("walk", ["default", "smem", "heap"])
+@pytest.mark.parametrize("walk", ["default", "smem", "heap", "pl"])
 def test_batch_matches_reference(rig, walk, monkeypatch):
     if walk != "default":
         monkeypatch.setenv("TACO_TRAVERSE", walk)
@@ -138,7 +138,7 @@ def test_rerank_edge_cases():
     assert res.ids.size == 0 and res.ids.dtype == np.int32
 
 
-@pytest.mark.parametrize("walk", ["smem", "heap"])
+@pytest.mark.parametrize("walk", ["smem", "heap", "pl"])
 def test_traversal_units(golden, walk, monkeypatch):
     """60 traversal instances with integer ties (reference pop traces), through
     the shared-memory fixed-depth heap (large batches) and the thread-local
