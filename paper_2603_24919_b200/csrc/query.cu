@@ -2904,15 +2904,17 @@ __global__ void __launch_bounds__(32 * RI_WARPS, RI_CTAS) k_rerank_i8(
   ids_of(dsc(1), tb);
   int4 dn = dsc(2);
   issue(ta, st[0]);
+  // the running bound of a tile is read one tile ahead (a bound read early is
+  // only looser: qthr only decreases), so no compare waits on its L2 round trip
+  unsigned long long thr_nx = __ldcg(qthr + ta.q);
   for (int64_t i = 0; i < nt; ++i) {
     ids_of(dn, tc);               // ids of tile i + 2
     dn = dsc(i + 3);
     sums_of(tb);                  // tile i + 1's ids arrived during tile i - 1
     if (i + 1 < nt) issue(tb, st[(i + 1) & 1]);
     else cp_async_commit();
-    // the running bound, loaded before the dot products hide its latency (a
-    // bound read early is only looser: qthr only decreases)
-    const unsigned long long thr = __ldcg(qthr + ta.q);
+    const unsigned long long thr = thr_nx;
+    thr_nx = __ldcg(qthr + tb.q);   // tb.q = 0 past the last tile: a valid address
     cp_async_wait<1>();           // tile i's rows and query bytes have landed
     __syncwarp();
     const RiStage& s = st[i & 1];
