@@ -927,7 +927,8 @@ __device__ __forceinline__ void count_chunk(const uint16_t* __restrict__ pops, c
 template <typename SM>
 __device__ void chunk_levels(const uint8_t* table, int valid, int n_sub, SM& S) {
   const int tid = threadIdx.x;
-  if (n_sub <= 16) {
+  constexpr bool kScan = sizeof(S.lh) / sizeof(int) >= 256;   // EncSmem holds 17 levels only
+  if (n_sub <= 16 || !kScan) {
     for (int l = tid; l <= n_sub; l += blockDim.x) {
       const int gl = l == 0 ? valid : S.ge[l];
       const int gn = l == n_sub ? 0 : S.ge[l + 1];
@@ -1454,9 +1455,10 @@ struct EncSmem {
   int64_t sbase, scnt;
   uint32_t wtot[NT / 32];
   int jpref[17];
-  int ge[257];
-  int lh[256];
+  int ge[33];   // the encoded kernels count N_s <= 16: 17 levels (the spare bytes went into the staging, EcCfg::GC)
+  int lh[32];
 };
+constexpr int EC_LEVELS = 33;
 
 template <int NT, bool WIDE>
 __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int valid, int n_sub, EncSmem<NT>& S);
@@ -1640,7 +1642,9 @@ __device__ __forceinline__ void enc_slice(const uint16_t* __restrict__ pops, con
 template <int NT>
 struct EcCfg {
   static constexpr int PER = NT >= 512 ? 2 : 4;   // pops per thread per batch
-  static constexpr int GC = 8 * NT;               // staged units per round: 8 per thread (8-bit tallies)
+  // staged units per round: 10 per thread at 256 threads (10 KiB next to the 64 KiB table: three
+  // CTAs per SM; 80 entries per thread per round keep the tallies' 8-bit fields), else 8
+  static constexpr int GC = (NT == 256 ? 10 : 8) * NT;
 };
 
 // k_count_pg looks the NEXT query's first batch of popped slices up while
@@ -1712,7 +1716,7 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
   const size_t offs_len = (size_t)nchunks * K2 + 1;
   uint4* t4 = reinterpret_cast<uint4*>(table);
   for (int i = tid; i < tbytes / 16; i += NT) t4[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 257; i += NT) S.ge[i] = 0;
+  for (int i = tid; i < EC_LEVELS; i += NT) S.ge[i] = 0;
   if (tid < 32) {
     const int np = tid < n_sub ? min(npop[q * n_sub + tid], cap) : 0;
     int x = np;
@@ -2017,7 +2021,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_count_tma(
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int i = tid; i < 257; i += TC_THREADS) S.ge[i] = 0;
+  for (int i = tid; i < EC_LEVELS; i += TC_THREADS) S.ge[i] = 0;
   if (tid < 32) {
     const int np = tid < n_sub ? min(npop[q * n_sub + tid], cap) : 0;
     int x = np;
