@@ -20,6 +20,7 @@ digest) re-uploads it.
 
 from __future__ import annotations
 
+import functools
 import hashlib
 import math
 import struct
@@ -128,10 +129,13 @@ class SearchResult:
 
 
 # ------------------------------------------------------------------- helpers
+@functools.lru_cache(maxsize=16)
+def _sample_rows(n: int):
+    return np.unique(np.linspace(0, max(n - 1, 0), num=min(n, 64)).astype(np.int64)) if n else np.zeros(0, np.int64)
+
+
 def _data_key(X: np.ndarray):
-    n = X.shape[0]
-    rows = np.unique(np.linspace(0, max(n - 1, 0), num=min(n, 64)).astype(np.int64)) if n else []
-    dig = hashlib.blake2b(np.ascontiguousarray(X[rows]).tobytes(), digest_size=16).hexdigest()
+    dig = hashlib.blake2b(X[_sample_rows(X.shape[0])].tobytes(), digest_size=16).digest()
     return (X.ctypes.data, X.shape, X.strides, X.dtype.str, dig)
 
 
