@@ -3,21 +3,32 @@
 // Whole-batch stages (super-tiles of up to kSuperTile queries), one stream:
 //   k_transform       qt = f32((q - mu) @ M)                     spectral.py:301-316
 //   k_csort           fp64 centroid distances + stable rank       imi.py:88-106
-//   k_traverse        multi-sequence heap traversal, one thread per (query,
-//                     subspace)                                   imi.py:130-166
+//   k_traverse_pl     multi-sequence heap traversal, a thread per (query,
+//                     subspace) walk, persistent lanes on a 4-ary
+//                     shared-memory heap (k_traverse_sh / k_traverse for
+//                     smaller batches)                            imi.py:130-166
 //   cluster mode (single GPU, n <= 1.5M):
-//   k_count_cluster   one thread-block CLUSTER per query, each CTA counts one id
-//                     chunk in shared memory; level histograms are exchanged
-//                     through DSMEM, Alg. 5 runs in-cluster and every CTA
-//                     compacts its candidates straight from smem   engine.py:201-251
+//   k_count_pg        persistent SOFTWARE groups of nchunks CTAs walk the
+//                     queries; each CTA counts one id chunk into a 4-bit (8-bit
+//                     at N_s = 16) shared-memory table from the encoded,
+//                     unit-padded CSR, the group exchanges level histograms
+//                     through global slots, Alg. 5 runs in every CTA and each
+//                     compacts its candidates straight from shared memory
+//                     (k_count_enc: the same as one hardware cluster per query;
+//                     k_count_cluster: the round-1 kernel on the plain CSR,
+//                     N_s > 16)                                   engine.py:201-251
 //   global mode (large shards / multi-GPU, query tiles):
-//   k_count           per (query, 64 Ki chunk) smem counting -> per-chunk
-//                     histograms + spilled score >= 2 records;  k_hist_reduce -> (all-reduce across
-//                     ranks) -> k_select (Alg. 5) -> k_compact
-//   k_plan_*          32-candidate tiles per candidate segment (two orders)
-//   k_rerank_tma      persistent warp-specialised gather: cp.async.bulk (TMA
-//                     bulk copies) of candidate row segments into an mbarrier
-//                     ring, fp64 einsum-order distances, warp top-k  engine.py:272-275
+//   k_count_genc      per (query, id chunk) shared-memory counting -> per-chunk
+//                     histograms + spilled score >= 2 records (k_count: the
+//                     plain-CSR sweep);  k_hist_reduce -> (all-reduce across
+//                     ranks) -> k_select (Alg. 5) -> k_emit_rec / recount
+//   k_plan_*          32-candidate tiles per candidate segment (query-major
+//                     output slots, chunk-major processing order)
+//   k_rerank_i8       u8 rows + u8-exact queries: warp-private cp.async (LDGSTS)
+//                     row pipelines, exact DP4A integer distances, running
+//                     bound, per-tile partial top-k
+//   k_rerank_async    other rows / queries: the same pipeline with fp64
+//                     einsum-order distances                      engine.py:256-279
 //   k_topk            final per-query top-k over the tile partials (radix select
 //                     on d2 bits then id, bitonic sort on (d2, id))  engine.py:275-279
 //   k_finalize        ids int32 / dists f32(sqrt(d2))              engine.py:276-279
@@ -1338,19 +1349,20 @@ __global__ void __launch_bounds__(CT_THREADS, 3) k_count_cluster(
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // nobody reads my histogram any more
 }
 
-// ------------------------------------------- encoded-CSR cluster count (N_s <= 8)
-// Same contract as k_count_cluster (4-bit tables, one cluster of nchunks CTAs
-// per query), fed by the encoded CSR of build_count_csr: every (chunk, cell)
-// slice is a run of 16-byte groups of 4 entries, entry = table word byte
-// offset << 6 | nibble shift; padding entries (EC_SENT) have shift 32, so they
-// add 0 to word 0 and read level 0.  Per entry: and (shift), lea (address),
-// shl (increment), atom, shr (old nibble), shl + funnel shift (tally field),
-// add -- no predicates, no per-id address arithmetic.  Padding entries'
-// level-0 tallies are subtracted (their count rides in the top 2 bits of the
-// slice offsets).  Two feeds:
-//  - k_count_enc: all threads stage the popped slices' group addresses in
-//    shared memory (one store per 16-byte group), then consume them with
-//    direct 16-byte loads, two groups of lookahead per thread;
+// ------------------------------------------- encoded-CSR cluster count (N_s <= 16)
+// Same contract as k_count_cluster (nchunks CTAs per query, one id chunk
+// each), fed by the encoded CSR of build_count_csr: every (chunk, cell) slice
+// is a run of 32-byte units of 8 entries (16-byte units of 4 in global mode),
+// entry = table word byte offset << 6 | lane shift; padding entries have
+// shift 32, so they add 0 (to a word of their own slice: EC_SPREAD) and read
+// level 0.  Per entry: and (shift), lea (address), shl (increment), atom, shr
+// (old lane), shl + funnel shift (tally field), add -- no predicates, no
+// per-id address arithmetic.  Padding entries' level-0 tallies are subtracted
+// (their count rides in the top 3 bits of the slice offsets).  Feeds:
+//  - k_count_pg / k_count_enc: all threads stage the popped slices' unit
+//    indices in shared memory (one store per unit), then consume them with
+//    direct 16-byte loads -- lane pairs share a unit (EC_PAIR), a thread has
+//    two groups of 4 entries in flight;
 //  - k_count_tma: a producer warp streams each slice with one cp.async.bulk
 //    into an mbarrier ring (TACO_COUNT_FEED=tma; measured slower: thousands
 //    of 100-200 byte bulk copies per CTA).
