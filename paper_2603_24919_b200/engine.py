@@ -135,16 +135,25 @@ def _sample_rows(n: int):
 
 
 def _data_key(X: np.ndarray):
-    dig = hashlib.blake2b(X[_sample_rows(X.shape[0])].tobytes(), digest_size=16).digest()
-    return (X.ctypes.data, X.shape, X.strides, X.dtype.str, dig)
+    # 64 sampled rows; of a wide row only its first and last 64 columns (at d = 960 hashing whole
+    # rows cost 0.25 ms per call, 6 % of a config-3 batch)
+    S = X[_sample_rows(X.shape[0])]
+    h = hashlib.blake2b(digest_size=16)
+    if X.ndim == 2 and X.shape[1] > 128:
+        h.update(np.ascontiguousarray(S[:, :64]).tobytes())
+        h.update(np.ascontiguousarray(S[:, -64:]).tobytes())
+    else:
+        h.update(S.tobytes())
+    return (X.ctypes.data, X.shape, X.strides, X.dtype.str, h.digest())
 
 
 def refresh_data(index: TacoIndex, data) -> None:
     """Re-upload ``data`` as the index's resident base matrix unconditionally.
 
     The per-call identity check (``_data_key``: pointer, shape, strides,
-    dtype and a digest of 64 sampled rows) cannot see an in-place edit of
-    rows it does not sample; a caller that mutates ``data`` in place between
+    dtype and a digest of 64 sampled rows -- of rows wider than 128 columns
+    their first and last 64) cannot see an in-place edit of values it does
+    not sample; a caller that mutates ``data`` in place between
     queries calls this."""
     dev = _device_of(index)
     X = as_f32_exact(np.asarray(data), "data")
