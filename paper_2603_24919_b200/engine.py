@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import functools
 import hashlib
+import zlib
 import math
 import struct
 import time
@@ -137,14 +138,13 @@ def _sample_rows(n: int):
 def _data_key(X: np.ndarray):
     # 64 sampled rows; of a wide row only its first and last 64 columns (at d = 960 hashing whole
     # rows cost 0.25 ms per call, 6 % of a config-3 batch)
+    # crc32 + adler32 (64 bits, ~20 us for 32 KB; blake2b took 50 us of a 540 us config-1 batch)
     S = X[_sample_rows(X.shape[0])]
-    h = hashlib.blake2b(digest_size=16)
     if X.ndim == 2 and X.shape[1] > 128:
-        h.update(np.ascontiguousarray(S[:, :64]).tobytes())
-        h.update(np.ascontiguousarray(S[:, -64:]).tobytes())
+        b = np.ascontiguousarray(S[:, :64]).tobytes() + np.ascontiguousarray(S[:, -64:]).tobytes()
     else:
-        h.update(S.tobytes())
-    return (X.ctypes.data, X.shape, X.strides, X.dtype.str, h.digest())
+        b = S.tobytes()
+    return (X.ctypes.data, X.shape, X.strides, X.dtype.str, zlib.crc32(b), zlib.adler32(b))
 
 
 def refresh_data(index: TacoIndex, data) -> None:
