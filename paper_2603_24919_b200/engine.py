@@ -408,8 +408,12 @@ def knn_query_batch(index: TacoIndex, data, queries, qp: QueryParams):
     if kk > TOPK_MAX:
         raise ParameterError(f"result count {k} exceeds the B200 top-k limit {TOPK_MAX} "
                              f"(n = {index.n})")
-    ids = np.full((nq, k), -1, np.int32)
-    dists = np.full((nq, k), np.inf, np.float32)
+    if kk == k and nq:   # the library writes every slot, padding included
+        ids = np.empty((nq, k), np.int32)
+        dists = np.empty((nq, k), np.float32)
+    else:
+        ids = np.full((nq, k), -1, np.int32)
+        dists = np.full((nq, k), np.inf, np.float32)
     num = np.empty(nq, np.int64)
     lvl = np.empty(nq, np.int32)
     if nq:
