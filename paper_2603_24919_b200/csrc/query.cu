@@ -3224,6 +3224,12 @@ __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ 
 // engine.py:275), bitonic sort of the kk survivors on (d2, id).
 constexpr int TK_THREADS = 256;   // 512 when a query has many partial entries
 constexpr int TK_MAX = 2048;
+#ifndef TK_MATCH
+#define TK_MATCH 1   // radix-select histogram adds aggregated per distinct digit of the warp ...
+#endif
+#ifndef TK_MATCH_MIN
+#define TK_MATCH_MIN 8192   // ... for lists at least this long (config 2's 3,300-entry lists: 0.43 vs 0.40 ms)
+#endif
 
 template <int NT>
 __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids, int64_t m, int kk,
@@ -3269,7 +3275,15 @@ __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids
         if (__all_sync(0xffffffffu, !take || dg == d0)) {
           if (lane == 0) atomicAdd(&hist[d0], (unsigned)__popc(tm));
         } else if (take) {
-          atomicAdd(&hist[dg], 1u);
+          if (TK_MATCH && m >= TK_MATCH_MIN) {
+            // long lists (k > 32 keeps every candidate): one add per distinct digit of the
+            // warp -- the keys of a query crowd into a few bins at the digit where they part,
+            // and per-lane adds to one bin serialise
+            const unsigned peers = __match_any_sync(tm, dg);
+            if (lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
+          } else {
+            atomicAdd(&hist[dg], 1u);
+          }
         }
       }
     }
