@@ -3224,12 +3224,6 @@ __global__ void __launch_bounds__(128) k_rerank_plain(const float* __restrict__ 
 // engine.py:275), bitonic sort of the kk survivors on (d2, id).
 constexpr int TK_THREADS = 256;   // 512 when a query has many partial entries
 constexpr int TK_MAX = 2048;
-#ifndef TK_MATCH
-#define TK_MATCH 1   // radix-select histogram adds aggregated per distinct digit of the warp ...
-#endif
-#ifndef TK_MATCH_MIN
-#define TK_MATCH_MIN 8192   // ... for lists at least this long (config 2's 3,300-entry lists: 0.43 vs 0.40 ms)
-#endif
 
 template <int NT>
 __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids, int64_t m, int kk,
@@ -3275,15 +3269,7 @@ __device__ void radix_select(const unsigned long long* keys, const uint32_t* ids
         if (__all_sync(0xffffffffu, !take || dg == d0)) {
           if (lane == 0) atomicAdd(&hist[d0], (unsigned)__popc(tm));
         } else if (take) {
-          if (TK_MATCH && m >= TK_MATCH_MIN) {
-            // long lists (k > 32 keeps every candidate): one add per distinct digit of the
-            // warp -- the keys of a query crowd into a few bins at the digit where they part,
-            // and per-lane adds to one bin serialise
-            const unsigned peers = __match_any_sync(tm, dg);
-            if (lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
-          } else {
-            atomicAdd(&hist[dg], 1u);
-          }
+          atomicAdd(&hist[dg], 1u);   // (match.any aggregation per distinct digit measured slower: config 5 58 -> 78 ms)
         }
       }
     }
@@ -3361,15 +3347,27 @@ __global__ void __launch_bounds__(NT) k_topk(const unsigned long long* __restric
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    int64_t c = 0, nt = 0;
-    for (int r = 0; r < S; ++r) {
-      c += scnt[q * S + r];
-      nt += (scnt[q * S + r] + GR - 1) / GR;
-    }
-    s_m = c;
-    s_nt = nt;
+    s_m = 0;
+    s_nt = 0;
     s_fill = 0;
     s_ties = 0;
+  }
+  __syncthreads();
+  {   // candidates and tiles of the query's S segments (S = 763 at config 5: not one thread's loop)
+    int64_t c = 0, nt = 0;
+    for (int r = tid; r < S; r += NT) {
+      const int64_t v = scnt[q * S + r];
+      c += v;
+      nt += (v + GR - 1) / GR;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      nt += __shfl_xor_sync(0xffffffffu, nt, o);
+    }
+    if ((tid & 31) == 0 && nt) {
+      atomicAdd((unsigned long long*)&s_m, (unsigned long long)c);
+      atomicAdd((unsigned long long*)&s_nt, (unsigned long long)nt);
+    }
   }
   __syncthreads();
   // the query's tiles are consecutive in the plan's processing order
