@@ -62,7 +62,7 @@ int DevBuf::ensure(size_t want) {
 void QueryTile::release() {
   DevBuf* all[] = {&Q, &qt, &sd, &sl, &pops, &npop, &ret, &flags, &scores, &part, &hist, &lvl, &cnum, &clocal,
                   &coff, &qbase, &cursor, &cand, &bpref, &pd2, &ppos, &tseg, &qthr, &qb, &qsq, &qok, &gsb, &gsc, &gtab, &rlist, &ppref, &psum, &tk_d2, &tk_ids,
-                  &out_ids, &out_d, &xch};
+                  &out_ids, &out_d, &xch, &tkx};
   for (auto* b : all) b->release();
   if (flags_h) cudaFreeHost(flags_h);
   flags_h = nullptr;

@@ -49,6 +49,7 @@ struct QueryTile {
   DevBuf Q, qt, sd, sl, pops, npop, ret, flags, scores, part, hist, lvl, cnum, clocal, coff, qbase,
       cursor, cand, bpref, pd2, ppos, tseg, qthr, qb, qsq, qok, gsb, gsc, gtab, rlist, ppref, psum, tk_d2, tk_ids, out_ids, out_d;
   DevBuf xch;                   // k_count_pg: the groups' level-histogram exchange slots
+  DevBuf tkx;                   // k_topk: the parts' best-k lists of split (long) queries
   int64_t cand_cap = 0;
   int pop_cap = 0;
   int64_t front_rows = 0;       // rows the split-traversal buffers were sized for

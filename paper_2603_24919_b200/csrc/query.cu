@@ -3331,13 +3331,21 @@ __device__ __forceinline__ void bitonic_pairs(unsigned long long* key, uint32_t*
   }
 }
 
+// A query whose partial list is long (a level-1 query of config 5 re-ranks 4M
+// candidates: one CTA's ten passes over them took 9 ms and set the kernel's
+// time) is selected in two steps: the list is cut into `parts` ranges, CTA
+// (q, y) of the first launch keeps range y's k best in xk / xi[(q * parts + y)
+// * k ...], and a second launch (merge = 1) selects among those parts * k.
+// Shorter lists are finished by CTA (q, 0) of the first launch as before.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_topk(const unsigned long long* __restrict__ pkey,
                                                       const uint32_t* __restrict__ pid,
                                                       const int64_t* __restrict__ tstart, int S, int kk_part,
                                                       const int64_t* __restrict__ scnt, int k, int64_t id_base,
                                                       double* __restrict__ out_d2,
-                                                      int64_t* __restrict__ out_ids) {
+                                                      int64_t* __restrict__ out_ids, int parts, int64_t split_min,
+                                                      unsigned long long* __restrict__ xk,
+                                                      uint32_t* __restrict__ xi, int merge) {
   __shared__ unsigned hist[256];
   __shared__ unsigned long long s_pre;
   __shared__ int s_rem, s_fill;
@@ -3372,10 +3380,33 @@ __global__ void __launch_bounds__(NT) k_topk(const unsigned long long* __restric
   __syncthreads();
   // the query's tiles are consecutive in the plan's processing order
   const int64_t lo = tstart[q * S] * kk_part;
-  const int64_t m = s_nt * kk_part;
-  const int kk = (int)min((int64_t)k, s_m);
+  int64_t m = s_nt * kk_part;
+  const bool split = parts > 1 && m > split_min;
+  if (merge ? !split : (!split && blockIdx.y > 0)) return;   // (block-uniform)
+  int kk = (int)min((int64_t)k, s_m);
   const unsigned long long* keys = pkey + lo;
   const uint32_t* ids = pid + lo;
+  const bool part = split && !merge;
+  if (part) {   // range y of the list; its real entries (padding slots hold all-ones keys)
+    const int64_t per = (m + parts - 1) / parts;
+    const int64_t b0 = min(m, (int64_t)blockIdx.y * per), b1 = min(m, b0 + per);
+    keys += b0;
+    ids += b0;
+    m = b1 - b0;
+    int64_t real = 0;
+    for (int64_t i = tid; i < m; i += NT) real += keys[i] != ~0ull;
+    for (int o = 16; o > 0; o >>= 1) real += __shfl_xor_sync(0xffffffffu, real, o);
+    if ((tid & 31) == 0 && real) atomicAdd((unsigned long long*)&s_ties, (unsigned long long)real);
+    __syncthreads();
+    kk = (int)min((int64_t)k, s_ties);
+    __syncthreads();
+    if (tid == 0) s_ties = 0;
+    __syncthreads();
+  } else if (merge) {
+    keys = xk + (size_t)q * parts * k;
+    ids = xi + (size_t)q * parts * k;
+    m = (int64_t)parts * k;
+  }
   if (kk > 0) {
     unsigned long long tau;
     int take;
@@ -3399,6 +3430,15 @@ __global__ void __launch_bounds__(NT) k_topk(const unsigned long long* __restric
       }
     }
     __syncthreads();
+  }
+  if (part) {   // the range's best kk (unsorted), all-ones padding to k
+    unsigned long long* ok = xk + ((size_t)q * parts + blockIdx.y) * k;
+    uint32_t* oi = xi + ((size_t)q * parts + blockIdx.y) * k;
+    for (int r = tid; r < k; r += NT) {
+      ok[r] = r < kk ? skey[r] : ~0ull;
+      oi[r] = r < kk ? sid[r] : 0xFFFFFFFFu;
+    }
+    return;
   }
   int P = 1;
   while (P < kk) P <<= 1;
@@ -3923,6 +3963,13 @@ static inline const int64_t* seg_cnt(const taco_index* idx, const QueryTile& t) 
   return idx->cluster_mode ? t.clocal.as<int64_t>() : t.gsc.as<int64_t>();
 }
 
+// flags[6] = the largest per-query candidate count of the tile (the top-k splits long lists)
+__global__ void k_max_i64(const int64_t* __restrict__ v, int64_t n, int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  long long x = i < n ? (long long)v[i] : 0;
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  if ((threadIdx.x & 31) == 0 && x > 0) atomicMax((long long*)out, x);
+}
 static int plan_async(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st) {
   const int64_t S = seg_per_query(idx);
   {
@@ -3937,7 +3984,9 @@ static int plan_async(taco_index* idx, QueryTile& t, int64_t QS, cudaStream_t st
                                                   t.flags.as<int64_t>());
     TACO_LAUNCHED();
   }
-  TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, st));
+  k_max_i64<<<(unsigned)ceil_div(QS, 256), 256, 0, st>>>(t.cnum.as<int64_t>(), QS, t.flags.as<int64_t>() + 6);
+  TACO_LAUNCHED();
+  TACO_CHECK_CUDA(cudaMemcpyAsync(t.flags_h, t.flags.p, sizeof(int64_t) * 7, cudaMemcpyDeviceToHost, st));
   return TACO_OK;
 }
 
@@ -4027,7 +4076,8 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
                        const int64_t* tstart,
                        const int64_t* tproc, const int64_t* sbase, const int64_t* scnt, const uint32_t* cand, int64_t ntiles, int k,
                        int64_t id_base, DevBuf& pkey, DevBuf& pid, DevBuf& tsegb, DevBuf& qthrb, double* out_d2,
-                       int64_t* out_ids, cudaStream_t st, const IntRerank& ir = IntRerank(), bool all_int = false) {
+                       int64_t* out_ids, cudaStream_t st, const IntRerank& ir = IntRerank(), bool all_int = false,
+                       int64_t max_cand = 0, DevBuf* xbuf = nullptr) {
   const int kk = std::min(k, GR);
   TACO_TRY(qthrb.ensure(sizeof(unsigned long long) * (size_t)QS));
   TACO_CHECK_CUDA(cudaMemsetAsync(qthrb.p, 0xFF, sizeof(unsigned long long) * (size_t)QS, st));
@@ -4076,9 +4126,35 @@ static int rerank_core(const float* X, const void* Xn, int fmt, int d, const flo
     ProfScope ps(K_TOPK, st);
     // partial entries per query: many (k > 32 keeps every row) -> 512 threads
     const bool wide = ntiles * kk >= (int64_t)8192 * std::max<int64_t>(QS, 1);
-    (wide ? k_topk<2 * TK_THREADS> : k_topk<TK_THREADS>)<<<(unsigned)QS, wide ? 2 * TK_THREADS : TK_THREADS, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart, (int)S,
-                                                kk, scnt, k, id_base, out_d2, out_ids);
+    // long lists are cut into parts (k_topk): max_cand = the tile's largest candidate count when
+    // the caller knows it (0: no split); scratch = QS x parts x k (key, id) pairs, capped at 1 GiB
+    // TACO_TOPK_SPLIT=n (read per batch): lists above n entries are split (the tests force it)
+    const char* se = getenv("TACO_TOPK_SPLIT");
+    const int64_t split_min = se ? std::max<int64_t>(64, atoll(se)) : 65536;
+    int parts = 1;
+    if (max_cand > split_min && xbuf != nullptr) {
+      parts = (int)std::min<int64_t>(32, ceil_div(max_cand, split_min / 2));
+      while (parts > 1 && (size_t)QS * parts * k * 12 > ((size_t)1 << 30)) --parts;
+    }
+    unsigned long long* xk = nullptr;
+    uint32_t* xi = nullptr;
+    if (parts > 1) {
+      const size_t nx = (size_t)QS * parts * k;
+      TACO_TRY(xbuf->ensure(nx * 12));
+      xk = xbuf->as<unsigned long long>();
+      xi = reinterpret_cast<uint32_t*>(xk + nx);
+    }
+    const int nt = wide ? 2 * TK_THREADS : TK_THREADS;
+    auto kern = wide ? k_topk<2 * TK_THREADS> : k_topk<TK_THREADS>;
+    kern<<<dim3((unsigned)QS, (unsigned)parts), nt, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart,
+                                                             (int)S, kk, scnt, k, id_base, out_d2, out_ids, parts,
+                                                             split_min, xk, xi, 0);
     TACO_LAUNCHED();
+    if (parts > 1) {
+      kern<<<dim3((unsigned)QS, 1), nt, 0, st>>>(pkey.as<unsigned long long>(), pid.as<uint32_t>(), tstart, (int)S, kk,
+                                                 scnt, k, id_base, out_d2, out_ids, parts, split_min, xk, xi, 1);
+      TACO_LAUNCHED();
+    }
   }
   return TACO_OK;
 }
@@ -4112,7 +4188,8 @@ static int rerank_stage(taco_index* idx, QueryTile& t, int64_t QS, int k, int64_
                      S > 1 ? t.ppref.as<int64_t>() : t.bpref.as<int64_t>(),
                      seg_base(idx, t), seg_cnt(idx, t), t.cand.as<uint32_t>(), ntiles, k, idx->id_base,
                      t.pd2, t.ppos, t.tseg, t.qthr, t.tk_d2.as<double>(), t.tk_ids.as<int64_t>(), st, ir,
-                     intp && prepped && t.flags_h[4] == 0);   // flags[4]: some query is not u8-exact
+                     intp && prepped && t.flags_h[4] == 0,   // flags[4]: some query is not u8-exact
+                     t.flags_h ? t.flags_h[6] : 0, &t.tkx);   // flags[6]: the tile's largest candidate count
 }
 
 static void prof_stats(taco_index* idx, QueryTile& t, int64_t QS, int64_t total) {

@@ -43,6 +43,26 @@ def test_batch_matches_reference(rig, walk, monkeypatch):
         np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
 
 
+@pytest.mark.parametrize("split", ["64", "300"])
+def test_split_topk_matches_reference(rig, split, monkeypatch):
+    """The two-step top-k of long partial lists (k_topk: ranges' best-k, then a merge
+    launch), forced onto the rigs' short lists; large k keeps every candidate."""
+    monkeypatch.setenv("TACO_TOPK_SPLIT", split)
+    g, X, Q, idx = rig
+    for gi, (alpha, beta, k) in enumerate(g["grid"]):
+        qp = T.QueryParams(alpha=float(alpha), beta=float(beta), k=int(k))
+        ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, qp)
+        np.testing.assert_array_equal(ids, g[f"ids_{gi}"])
+        np.testing.assert_array_equal(dists, g[f"dists_{gi}"])
+    # k > 32: no per-tile filtering, every candidate reaches the top-k; against the oracle
+    oidx = O.deserialize(g["blob"].tobytes())
+    alpha, beta, _ = (float(v) for v in g["grid"][0])
+    oi, od, on, ol = O.knn_batch(oidx, X, Q, alpha, max(beta, 0.05), 50, threads=4)
+    ids, dists, num, lvl = T.knn_query_batch(idx, X, Q, T.QueryParams(alpha, max(beta, 0.05), 50))
+    np.testing.assert_array_equal(ids, oi)
+    np.testing.assert_array_equal(dists, od)
+
+
 def test_single_query_api(rig):
     g, X, Q, idx = rig
     alpha, beta, k = g["grid"][0]
