@@ -1906,9 +1906,15 @@ __device__ __forceinline__ void enc_levels(Tally& T, const uint8_t* table, int v
     }
   }
   __syncthreads();
-  if (tid == 0) S.ge[1] -= S.pads;   // padding entries counted as leaving level 0
+  // level histogram from the tallies: lh[l] = #(score >= l) - #(score >= l + 1); the padding
+  // entries were tallied as leaving level 0, so they come off #(score >= 1)
+  for (int l = tid; l <= n_sub; l += NT) {
+    const int g1 = S.ge[1] - S.pads;
+    const int gl = l == 0 ? valid : (l == 1 ? g1 : S.ge[l]);
+    const int gn = l == n_sub ? 0 : (l == 0 ? g1 : S.ge[l + 1]);
+    S.lh[l] = gl - gn;
+  }
   __syncthreads();
-  chunk_levels(table, valid, n_sub, S);
 }
 
 // NSC: N_s at compile time (0 = runtime); NIB: 4-bit lanes (else 8-bit, N_s = 16);
