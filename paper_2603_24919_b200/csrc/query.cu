@@ -1870,8 +1870,7 @@ __device__ __forceinline__ void enc_count_phase(const uint16_t* __restrict__ pop
       __syncthreads();
     }
   }
-  if (pads) atomicAdd(&S.pads, pads);
-  __syncthreads();
+  if (pads) atomicAdd(&S.pads, pads);   // read after enc_levels' first barrier (every caller runs it next)
 }
 
 // tallies -> the chunk's level histogram S.ge / S.lh (packed reduction as in
